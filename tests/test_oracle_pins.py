@@ -1,0 +1,307 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix
+(DESIGN.md "Oracle pins" P1-P14).  CPU only."""
+import os
+
+import numpy as np
+import pytest
+
+import h2gen
+import oracle
+from h2gen import cid
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _cases():
+    out = []
+    for sym in (True, False):
+        for seed in range(3):
+            out.append(("rand", sym, seed))
+    return out
+
+
+@pytest.fixture(scope="module", params=_cases(), ids=lambda c: f"{c[0]}-{'sym' if c[1] else 'gen'}-{c[2]}")
+def small(request):
+    kind, sym, seed = request.param
+    h = h2gen.random_h2(L=4, B=8, seed=seed, symmetric=sym, eta=[0.4, 0.7, 1.5][seed])
+    res = oracle.sparsify(h)
+    A = oracle.dense_A(h)
+    U = oracle.dense_U(res, "row")
+    V = oracle.dense_U(res, "col")
+    S = oracle.s_dense(res)
+    return h, res, A, U, V, S
+
+
+# --------------------------------------------------------------------- P4
+@pytest.mark.parametrize("n,k", [(32, 8), (64, 16), (48, 24), (128, 32), (64, 32), (16, 0), (16, 16), (7, 3), (1, 1)])
+def test_P4_qr_matches_lapack(n, k):
+    """Convention H == LAPACK dgeqrf + dorgqr (numpy.linalg.qr 'complete')."""
+    rng = np.random.default_rng(n * 100 + k)
+    X = rng.standard_normal((n, k))
+    Q, R = oracle.householder_complete(X)
+    if k == 0:
+        assert np.array_equal(Q, np.eye(n))
+        return
+    Ql, Rl = np.linalg.qr(X, mode="complete")
+    assert np.abs(Q - Ql).max() <= 1e-13
+    assert np.abs(R - Rl[:k, :k]).max() <= 1e-13 * max(1.0, np.abs(Rl).max())
+    assert np.abs(Q[:, :k] @ R - X).max() <= 1e-13 * np.abs(X).max()
+
+
+def test_P4_qr_tie_breaks():
+    """sigma == 0 exactly -> no reflection; sgn(+-0) = +1 (reading 2)."""
+    Q, R = oracle.householder_complete(np.array([[-2.0], [0.0], [0.0]]))
+    assert np.array_equal(Q, np.eye(3)) and R[0, 0] == -2.0
+    Q, R = oracle.householder_complete(np.array([[-0.0], [3.0], [4.0]]))
+    assert R[0, 0] == -5.0          # beta = -sgn(-0) * 5 = -5
+    Q, R = oracle.householder_complete(np.array([[0.0], [3.0], [4.0]]))
+    assert R[0, 0] == -5.0
+    Q, R = oracle.householder_complete(np.array([[-1.0], [0.0], [1.0]]))
+    assert R[0, 0] > 0              # alpha < 0 -> beta = +hypot
+    assert np.abs(Q.T @ Q - np.eye(3)).max() < 1e-15
+
+
+# --------------------------------------------------------------------- P1-P3, P14
+def test_P1_dense_reconstruction(small):
+    """U S V^T = A_H2 (P:477-484, P:716 'does not worsen the accuracy')."""
+    h, res, A, U, V, S = small
+    assert np.linalg.norm(U @ S @ V.T - A) / np.linalg.norm(A) <= 1e-12
+
+
+def test_P2_definition(small):
+    """S == U^T A_H2 V and U^T A_H2 V vanishes off the pattern (Eq. fin)."""
+    h, res, A, U, V, S = small
+    Sd = U.T @ A @ V
+    assert np.linalg.norm(S - Sd) / np.linalg.norm(A) <= 1e-13
+    mask = np.zeros(S.shape, dtype=bool)
+    for (i, t, j, s), blk in res.S.items():
+        r0, c0 = res.off_row[cid(h.L, i, t)], res.off_col[cid(h.L, j, s)]
+        mask[r0:r0 + blk.shape[0], c0:c0 + blk.shape[1]] = True
+    assert np.abs(Sd[~mask]).max() <= 1e-13 * np.abs(A).max()
+
+
+def test_P3_orthogonality(small):
+    """Every Q_t and the dense U, V are orthogonal."""
+    h, res, A, U, V, S = small
+    for Q in res.Q_row + res.Q_col:
+        n = Q.shape[0]
+        if n:
+            assert np.abs(Q.T @ Q - np.eye(n)).max() <= 1e-14 * max(n, 1)
+    N = U.shape[0]
+    assert np.abs(U.T @ U - np.eye(N)).max() <= 1e-13
+    assert np.abs(V.T @ V - np.eye(N)).max() <= 1e-13
+
+
+def test_P14_non_extensive(small):
+    """S is N x N: sum m^R = sum m^C = N (P:41-44 footnote)."""
+    h, res, A, U, V, S = small
+    assert res.m_row.sum() == h.N and res.m_col.sum() == h.N
+    assert S.shape == (h.N, h.N)
+    rowptr, col, val = oracle.s_csr(res)
+    assert len(rowptr) == h.N + 1 and rowptr[-1] == len(val) == len(col)
+    assert col.max() < h.N
+
+
+def test_symmetric_mode_bitwise(small):
+    """Proposition: A symmetric -> U == V and S symmetric (bitwise in
+    our canonical-pair convention)."""
+    h, res, A, U, V, S = small
+    if not h.symmetric:
+        pytest.skip("general mode")
+    assert np.array_equal(U, V)
+    assert np.array_equal(S, S.T)
+
+
+# --------------------------------------------------------------------- P5
+@pytest.mark.parametrize("which", ["cfg1", "cfg2-small", "rand-gen"])
+def test_P5_frobenius_invariance(which):
+    """||S||_F = ||A_H2||_F by orthogonality of U, V; the right side from the
+    H^2 parameters through Gram matrices, independent of the QR convention."""
+    if which == "cfg1":
+        h = h2gen.make_config(1)
+    elif which == "cfg2-small":
+        h = h2gen.make_config(2, N=8192)
+    else:
+        h = h2gen.random_h2(L=6, B=16, seed=5, symmetric=False)
+    res = oracle.sparsify(h)
+    _, _, val = oracle.s_csr(res)
+    f = oracle.frobenius_sq(h)
+    assert abs(float(np.dot(val, val)) - f) / f <= 1e-12
+
+
+# --------------------------------------------------------------------- P6
+def test_P6_spectra_spd():
+    """S = U^T A V: same eigenvalues (sym) and S SPD when A_H2 SPD."""
+    h = h2gen.random_h2(L=4, B=8, seed=11, symmetric=True)
+    A = oracle.dense_A(h)
+    lam = np.linalg.eigvalsh(A)
+    shift = max(0.0, -lam.min()) + 1.0
+    for i, (t, s) in enumerate(h.near):
+        if t == s:
+            h.close[i] = h.close[i] + shift * np.eye(h.B)
+    A = oracle.dense_A(h)
+    res = oracle.sparsify(h)
+    S = oracle.s_dense(res)
+    ls, la = np.linalg.eigvalsh(S), np.linalg.eigvalsh(A)
+    assert np.abs(ls - la).max() <= 1e-13 * np.abs(la).max()
+    np.linalg.cholesky(S)           # raises if not SPD
+
+
+def test_P6_singular_values_general():
+    h = h2gen.random_h2(L=4, B=8, seed=12, symmetric=False)
+    A = oracle.dense_A(h)
+    S = oracle.s_dense(oracle.sparsify(h))
+    sa, ss = np.linalg.svd(A, compute_uv=False), np.linalg.svd(S, compute_uv=False)
+    assert np.abs(sa - ss).max() <= 1e-13 * sa[0]
+
+
+def test_P6_config1_spd():
+    h = h2gen.make_config(1)
+    res = oracle.sparsify(h)
+    S = oracle.s_dense(res)
+    assert np.array_equal(S, S.T)
+    np.linalg.cholesky(S)
+    A = oracle.dense_A(h)
+    U = oracle.dense_U(res)
+    assert np.linalg.norm(U @ S @ U.T - A) / np.linalg.norm(A) <= 1e-12
+
+
+# --------------------------------------------------------------------- P7, P8
+@pytest.mark.parametrize("sym", [True, False])
+def test_P7_eta0_identity(sym):
+    """eta = 0: all ranks 0, U = V = I, S = C bitwise."""
+    h = h2gen.eta0_h2(L=3, B=4, seed=3, symmetric=sym)
+    res = oracle.sparsify(h)
+    assert np.array_equal(oracle.s_dense(res), oracle.dense_A(h))
+    assert np.array_equal(oracle.dense_U(res), np.eye(h.N))
+
+
+@pytest.mark.parametrize("sym,seed", [(True, 1), (False, 2), (True, 3)])
+def test_P8_axis_aligned_permutation(sym, seed):
+    """Axis-aligned bases: every Q = I, U and V are the permutations P_r, P_c
+     and S = P_r^T A_H2 P_c bitwise (no rounding anywhere)."""
+    h = h2gen.axis_aligned_h2(L=4, B=8, seed=seed, symmetric=sym)
+    res = oracle.sparsify(h)
+    for Q in res.Q_row + res.Q_col:
+        assert np.array_equal(Q, np.eye(Q.shape[0]))
+    A = oracle.dense_A(h)
+    pr = np.argmax(oracle.dense_U(res, "row"), axis=0)
+    pc = np.argmax(oracle.dense_U(res, "col"), axis=0)
+    assert sorted(pr) == list(range(h.N)) and sorted(pc) == list(range(h.N))
+    assert np.array_equal(oracle.s_dense(res), A[pr][:, pc])
+    # the permutation puts level-0 non-basis indices (rows k_t..B-1 of leaf t,
+    # the basis being the first k_t unit vectors) first, order preserved
+    L = h.L
+    k0 = [int(h.rank_row[cid(L, 0, i)]) for i in range(1 << L)]
+    want = [i * h.B + a for i in range(1 << L) for a in range(k0[i], h.B)]
+    assert list(pr[:len(want)]) == want
+
+
+# --------------------------------------------------------------------- P9
+def _golden_fig3():
+    c0, fml = set(), set()
+    with open(os.path.join(GOLDEN, "fig3_structure.txt")) as f:
+        for line in f:
+            if line.startswith("#") or not line.strip():
+                continue
+            tag, r, c = line.split()
+            (c0 if tag == "C0" else fml).add((int(r), int(c)))
+    return c0, fml
+
+
+def test_P9_fig3_structure():
+    """Fig. 1 C_0 and Fig. 3 F^_ml1 (14 green blocks) from the paper; the
+    grouping rule gives N_1 (6 pairs), N_2 (all 4 pairs), A_1 (10 pairs)."""
+    c0, fml = _golden_fig3()
+    L, near0, adm = h2gen.fig3_structure()
+    assert set(map(tuple, near0.tolist())) == c0
+    assert set(map(tuple, adm[0].tolist())) == fml and len(fml) == 14
+    h = h2gen.fig3_h2(B=4, seed=0, rank_mode="half")
+    res = oracle.sparsify(h)
+    assert res.near_levels[1] == [(0, 0), (1, 1), (1, 2), (2, 1), (2, 2), (3, 3)]
+    assert res.near_levels[2] == [(0, 0), (0, 1), (1, 0), (1, 1)]
+    assert len(adm[1]) == 10
+    # F^_ml1 = children of N_1 pairs that are far at level 0 (Eq. cl1)
+    kids = {(2 * p + a, 2 * q + b) for (p, q) in res.near_levels[1] for a in range(2) for b in range(2)}
+    assert kids - c0 == fml
+
+
+def test_P9_fig3_block_counts():
+    """With every non-root rank r = B/2 (§3 hypothesis): 101 blocks, per
+    (row level, col level) as in DESIGN.md; with active-only ranks: 72."""
+    from collections import Counter
+    h = h2gen.fig3_h2(B=4, seed=0, rank_mode="half")
+    res = oracle.sparsify(h)
+    cnt = Counter((i, j) for (i, t, j, s) in res.S)
+    want = {(0, 0): 10, (0, 1): 10, (0, 2): 10, (0, 3): 8, (1, 0): 10, (1, 1): 6, (1, 2): 6, (1, 3): 4,
+            (2, 0): 10, (2, 1): 6, (2, 2): 4, (2, 3): 2, (3, 0): 8, (3, 1): 4, (3, 2): 2, (3, 3): 1}
+    assert dict(cnt) == want and len(res.S) == 101
+    # P12 (informational): the corrected double sum 4L-2+3*2^-L bounds it; the printed form does not
+    L, nb = 3, 10
+    assert len(res.S) <= (4 * L - 2 + 3 * 2.0 ** -L) * nb
+    assert len(res.S) > (4 * L + 6 * (2.0 ** -L - 1)) * nb
+    h2 = h2gen.fig3_h2(B=4, seed=0, rank_mode="active")
+    assert len(oracle.sparsify(h2).S) == 72
+
+
+# --------------------------------------------------------------------- P10
+@pytest.mark.parametrize("sym,eta,seed", [(True, 0.4, 0), (True, 0.7, 1), (True, 1.5, 2), (False, 0.4, 3),
+                                          (False, 0.7, 4), (False, 1.5, 5)])
+def test_P10_pattern_rule(sym, eta, seed):
+    h = h2gen.random_h2(L=5, B=8, seed=seed, symmetric=sym, eta=eta)
+    res = oracle.sparsify(h)
+    assert oracle.pattern_rule(h) == set(res.S.keys())
+
+
+# --------------------------------------------------------------------- P11
+def test_P11_solve_equivalence():
+    """x = V S^-1 U^T b equals A_H2^-1 b (Eq. sp0)."""
+    h = h2gen.random_h2(L=4, B=8, seed=21, symmetric=False)
+    A = oracle.dense_A(h)
+    res = oracle.sparsify(h)
+    S = oracle.s_dense(res)
+    b = np.random.default_rng(0).standard_normal((h.N, 3))
+    y = np.linalg.solve(S, oracle.apply_Ut(res, b, "row"))
+    x = oracle.apply_V(res, y, "col")
+    xa = np.linalg.solve(A, b)
+    cond = np.linalg.cond(A)
+    assert np.linalg.norm(x - xa) / np.linalg.norm(xa) <= cond * 1e-14
+
+
+def test_apply_matches_dense(small):
+    h, res, A, U, V, S = small
+    b = np.random.default_rng(1).standard_normal((h.N, 2))
+    assert np.abs(oracle.apply_Ut(res, b, "row") - U.T @ b).max() <= 1e-13 * np.abs(b).max()
+    assert np.abs(oracle.apply_V(res, b, "col") - V @ b).max() <= 1e-13 * np.abs(b).max()
+
+
+# --------------------------------------------------------------------- P13
+def test_P13_matvec_at_scale():
+    """U (S (V^T x)) == A_H2 x by the standard H^2 matvec, N = 16384."""
+    import scipy.sparse as sp
+    h = h2gen.make_config(2, N=16384)
+    res = oracle.sparsify(h)
+    rowptr, col, val = oracle.s_csr(res)
+    Sm = sp.csr_matrix((val, col, rowptr), shape=(h.N, h.N))
+    x = np.random.default_rng(2).standard_normal((h.N, 2))
+    y = oracle.apply_V(res, Sm @ oracle.apply_Ut(res, x, "col"), "row")
+    ya = oracle.h2_matvec(h, x)
+    assert np.linalg.norm(y - ya) / np.linalg.norm(ya) <= 1e-12
+
+
+def test_h2_matvec_vs_dense():
+    h = h2gen.random_h2(L=4, B=8, seed=7, symmetric=False)
+    x = np.random.default_rng(3).standard_normal(h.N)
+    A = oracle.dense_A(h)
+    assert np.abs(oracle.h2_matvec(h, x) - A @ x).max() <= 1e-12 * np.abs(A @ x).max()
+
+
+def test_csr_roundtrip(small):
+    h, res, A, U, V, S = small
+    rowptr, col, val = oracle.s_csr(res)
+    D = np.zeros((h.N, h.N))
+    for r in range(h.N):
+        cols = col[rowptr[r]:rowptr[r + 1]]
+        assert np.all(np.diff(cols) > 0)
+        D[r, cols] = val[rowptr[r]:rowptr[r + 1]]
+    assert np.array_equal(D, S)
