@@ -531,7 +531,7 @@ def _svd_h2(x, L, B, r, near0, adm, kspec, sym) -> H2Input:
                    coupling=coupling, points=x)
 
 
-def _random_ranks(L, B, rng, lo_frac=0.0, hi_frac=1.0, zero_prob=0.15, full_prob=0.1):
+def _random_ranks(L, B, rng, lo_frac=0.0, hi_frac=1.0, zero_prob=0.15, full_prob=0.1, max_rank=None):
     ncl = n_clusters(L)
     rank = np.zeros(ncl, dtype=np.int32)
     nloc = np.zeros(ncl, dtype=np.int64)
@@ -552,12 +552,14 @@ def _random_ranks(L, B, rng, lo_frac=0.0, hi_frac=1.0, zero_prob=0.15, full_prob
                 kk = n
             else:
                 kk = int(rng.integers(int(lo_frac * n), int(hi_frac * n) + 1)) if n > 0 else 0
+            if max_rank is not None:
+                kk = min(kk, max_rank)
             rank[c] = kk
     return rank
 
 
 def random_h2(L: int, B: int, seed: int, symmetric: bool, eta: float = 0.7, d: int = 2, spd_shift: float = 0.0,
-              ragged: bool = True, r: int = None) -> H2Input:
+              ragged: bool = True, r: int = None, max_rank: int = None) -> H2Input:
     """Random H^2 matrix on a KD tree of random points: Gaussian bases,
     transfers, couplings and close blocks; ragged per-cluster ranks (including
     k=0, k=n and n=0 clusters) when ``ragged``.  ``spd_shift`` is added to the
@@ -569,8 +571,8 @@ def random_h2(L: int, B: int, seed: int, symmetric: bool, eta: float = 0.7, d: i
     near0, adm = block_tree(lo, hi, L, eta)
     ncl = n_clusters(L)
     if ragged:
-        rank_row = _random_ranks(L, B, rng)
-        rank_col = rank_row if symmetric else _random_ranks(L, B, rng)
+        rank_row = _random_ranks(L, B, rng, max_rank=max_rank)
+        rank_col = rank_row if symmetric else _random_ranks(L, B, rng, max_rank=max_rank)
     else:
         rr = r if r is not None else max(1, B // 4)
         rank_row = far_ranks(L, near0, adm, rr, rr, 0)

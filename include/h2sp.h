@@ -1,0 +1,202 @@
+/*
+ * h2sp.h -- C ABI of the B200-native non-extensive sparsification of an H^2
+ * matrix (arXiv 1705.04601, "PAPER.md" = P below).
+ *
+ * Given the parameters of an H^2 matrix (Def. "H^2 matrix":
+ * A = C + sum_{b=(t,s) admissible} R_t D_b E_s^T, with nested cluster bases
+ * R_p = diag(R_c1, R_c2) T_p), the library computes the exact
+ * factorisation A = U S V^T (Eq. main_fact):
+ *   - U, V orthogonal: products of level-wise block-diagonal factors whose
+ *     blocks are the completed square bases Q_t = [W_t, W_t^perp]
+ *      and of the basis/non-basis permutations P_rk, P_ck
+ *     (P:219-223).  They are returned as the batch of Q_t blocks plus the
+ *     S-order offsets (the permutation) of every cluster.
+ *   - S sparse N x N ("non-extensive"), returned as CSR.
+ * and applies y = U^T b, x = V y (Eq. sp0).
+ *
+ * Conventions shared by every entry point
+ *   - Balanced binary cluster tree, level 0 = 2^L leaves of B indices each,
+ *     level L = root.  Cluster (k, i) has the level-major id
+ *     cid = (2^(L+1) - 2^(L-k+1)) + i; its children are (k-1, 2i), (k-1, 2i+1).
+ *     Indices are in cluster-tree order: leaf i owns [iB, (i+1)B).
+ *   - All dense blocks are row-major FP64.
+ *   - Local size n_t = B (leaf) or k_c1 + k_c2 (internal); frozen count
+ *     m_t = n_t - k_t; 0 <= k_t <= n_t, k_root = 0 (readings 3-5).
+ *   - S order: off(k,t) = sum_{k'<k} sum_t' m_t' + sum_{t'<t at level k} m_t'
+ *     (non-basis before basis, order preserved).  Row side uses
+ *     m^R, column side m^C; sum m^R = sum m^C = N.
+ *   - Q_t columns [0, k_t) span the orthogonalised basis; column k_t + a is the
+ *     a-th non-basis direction, i.e. S index off(k,t) + a.  Householder
+ *     convention H of DESIGN.md (LAPACK dgeqrf/dorg2r semantics).
+ *   - Every call returns h2sp_status; nothing throws across the ABI; a
+ *     thread-local message is kept for h2sp_last_error().
+ *   - Device pointers are caller-owned (torch tensors in the Python binding).
+ *     The plan owns only host memory.  No CPU fallback: a missing device or a
+ *     CUDA error is reported as H2SP_ECUDA.
+ */
+#ifndef H2SP_H
+#define H2SP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  H2SP_OK = 0,
+  H2SP_EINVAL = 1,       /* bad argument (NULL pointer, size too small, ...)  */
+  H2SP_ETREE = 2,        /* block cluster tree is not a partition / unsorted   */
+  H2SP_ERANK = 3,        /* rank outside [0, n_t] or nonzero root rank          */
+  H2SP_ENOMEM = 4,       /* host allocation failed                              */
+  H2SP_ECUDA = 5,        /* CUDA launch / runtime error                         */
+  H2SP_ENCCL = 6,        /* reserved for the multi-GPU halo exchange            */
+  H2SP_EUNSUPPORTED = 7  /* shape outside what the kernels are built for        */
+} h2sp_status;
+
+const char *h2sp_status_str(h2sp_status s);
+/* Detail of the last error raised on this host thread ("" if none). */
+const char *h2sp_last_error(void);
+
+typedef struct h2sp_plan_s *h2sp_plan;
+
+/* Structure of the H^2 matrix (HOST pointers, read during plan_create only).
+ *   rank_row/rank_col: [2^(L+1)-1] ranks k_t by level-major id; rank_col may be
+ *     NULL iff symmetric (then the column side is the row side).
+ *   near_ptr[2^L + 1], near_col[nnz]: N_0 (inadmissible leaf pairs) as CSR over
+ *     leaves, columns strictly ascending within a row.
+ *   adm_ptr[k][2^(L-k) + 1], adm_col[k][...]: A_k (admissible pairs at level
+ *     k = 0..L-1) as CSR per level, columns strictly ascending.
+ * Symmetric mode (symmetric != 0) requires both lists to be symmetric; the
+ * numeric inputs must then satisfy C_st = C_ts^T and D_st = D_ts^T (only the
+ * t <= s blocks are read).  The plan checks that the block tree is a partition
+ * (P:613-649): every pair of N_k (k >= 1, N_k = parents of N_{k-1} u A_{k-1})
+ * has its 4 children in N_{k-1} u A_{k-1}, no pair is both near and far, and
+ * N_L = {(root, root)}. */
+typedef struct {
+  int32_t L;
+  int32_t leaf_size;
+  int32_t symmetric;
+  const int32_t *rank_row;
+  const int32_t *rank_col;
+  const int64_t *near_ptr;
+  const int32_t *near_col;
+  const int64_t *const *adm_ptr;
+  const int32_t *const *adm_col;
+} h2sp_structure;
+
+/* Sizes derived by the plan (all element counts are numbers of doubles unless
+ * stated otherwise). */
+typedef struct {
+  int64_t n;                   /* N = B * 2^L                                  */
+  int64_t n_clusters;          /* 2^(L+1) - 1                                  */
+  int64_t leaf_row, transfer_row, leaf_col, transfer_col; /* input lengths    */
+  int64_t close, coupling;     /* input lengths: n_near*B*B, sum k_t*k_s        */
+  int64_t q_row, q_col;        /* output lengths of the Q batches (sum n_t^2)  */
+  int64_t s_nnz;               /* nonzeros of S                                */
+  int64_t s_blocks;            /* blocks (t@i, s@j) of S                       */
+  int64_t workspace_bytes;     /* device workspace for h2sp_build (incl. meta) */
+  int64_t meta_bytes;          /* leading part of every workspace: work lists  */
+  int64_t levels_active;       /* levels with any nonzero local size           */
+  int64_t launches;            /* kernel launches issued by one h2sp_build     */
+  double flops;                /* algorithmic FP64 flops of one build          */
+  double bytes;                /* algorithmic HBM bytes of one build           */
+  double flops_congruence;     /* of which: congruence H = Q^T G Q             */
+  double flops_strips;         /* of which: strip rotations                    */
+} h2sp_sizes;
+
+/* Numeric inputs (DEVICE pointers, read-only, row-major FP64):
+ *   leaf_basis_row: R_t of every leaf, B x k_t each, concatenated by leaf.
+ *   transfer_row:   T_p of every internal cluster, (k_c1 + k_c2) x k_p each
+ *                   (child 1 rows first), concatenated by level-major id.
+ *   *_col: the column side (ignored, may be NULL, if symmetric).
+ *   close:    C_ts (B x B) per N_0 pair in near_ptr/near_col order.
+ *   coupling: D_b (k_t x k_s) per A_k pair, level-major, CSR order. */
+typedef struct {
+  const double *leaf_basis_row;
+  const double *transfer_row;
+  const double *leaf_basis_col;
+  const double *transfer_col;
+  const double *close;
+  const double *coupling;
+} h2sp_inputs;
+
+/* Outputs (DEVICE pointers, caller-allocated with the lengths of h2sp_sizes):
+ *   q_row[q_row], q_col[q_col]: Q_t (n_t x n_t, row-major) concatenated by
+ *     level-major id (offsets from h2sp_plan_offsets); q_col ignored if
+ *     symmetric (U == V, use q_row).
+ *   s_rowptr[N+1] (int64), s_col[s_nnz] (int32), s_val[s_nnz]: S in CSR, rows
+ *     and columns in S order, columns ascending.  s_col / s_rowptr may be NULL
+ *     to skip writing the (value-independent) index arrays. */
+typedef struct {
+  double *q_row;
+  double *q_col;
+  int64_t *s_rowptr;
+  int32_t *s_col;
+  double *s_val;
+} h2sp_outputs;
+
+/* Symbolic phase (host, O(#blocks)): validates the structure and derives all
+ * sizes, S offsets, the S block pattern, CSR row pointers and the per-level
+ * work lists.  flags: reserved, pass 0. */
+h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out);
+h2sp_status h2sp_plan_sizes(h2sp_plan plan, h2sp_sizes *out);
+/* Host copies of per-cluster data (each array has n_clusters entries; any
+ * pointer may be NULL): S-order offsets (row / column side), offsets of Q_t in
+ * q_row / q_col, local sizes n_t (row / column). */
+h2sp_status h2sp_plan_offsets(h2sp_plan plan, int64_t *s_off_row, int64_t *s_off_col, int64_t *q_off_row,
+                              int64_t *q_off_col, int64_t *n_row, int64_t *n_col);
+/* Host copy of the symbolic CSR pattern of S: rowptr[N+1] (int64) and, if
+ * col != NULL, col[s_nnz] (int32) -- identical to what h2sp_build writes into
+ * s_rowptr / s_col.  Host only (no device needed). */
+h2sp_status h2sp_plan_pattern(h2sp_plan plan, int64_t *rowptr, int32_t *col);
+void h2sp_plan_destroy(h2sp_plan plan);
+
+/* Copies the plan's device work lists (sizes.meta_bytes bytes) into the first
+ * part of a device workspace `ws` (256-byte aligned) on `stream`.  Must be
+ * called once for every workspace before it is passed to h2sp_build or
+ * h2sp_apply_*; the work lists stay valid as long as the caller does not
+ * overwrite that region.  A workspace uploaded for another plan is detected
+ * on the device (kernel trap -> H2SP_ECUDA at the next synchronisation). */
+h2sp_status h2sp_plan_upload(h2sp_plan plan, void *ws, size_t ws_bytes, void *stream);
+
+/* Numeric phase: computes Q (both sides) and S on `stream` (a cudaStream_t;
+ * NULL = legacy default stream).  Asynchronous; errors of the launches are
+ * returned, faults inside kernels surface at the next synchronising call.
+ * ws: device workspace of at least sizes.workspace_bytes bytes, 256-byte
+ * aligned, uploaded with h2sp_plan_upload. */
+h2sp_status h2sp_build(h2sp_plan plan, const h2sp_inputs *in, const h2sp_outputs *out, void *ws,
+                       size_t ws_bytes, void *stream);
+
+/* End-to-end variant with HOST buffers: copies the host inputs into the given
+ * device input buffers, builds, and copies every output back into the host
+ * output buffers (host pointers should be pinned for overlap).  All copies
+ * are cudaMemcpyAsync on `stream`; the call returns after enqueueing them. */
+h2sp_status h2sp_build_host(h2sp_plan plan, const h2sp_inputs *host_in, const h2sp_outputs *host_out,
+                            const h2sp_inputs *dev_in, const h2sp_outputs *dev_out, void *ws, size_t ws_bytes,
+                            void *stream);
+
+/* Workspace bytes for h2sp_apply_Ut / h2sp_apply_V with nrhs right-hand sides
+ * (meta region + basis-coefficient buffer).  The build workspace may be reused
+ * when it is at least this large (after the build has completed on the
+ * stream); it must have been uploaded with h2sp_plan_upload. */
+int64_t h2sp_apply_ws_bytes(h2sp_plan plan, int nrhs);
+
+/* y = U^T b: b is N x nrhs column-major in tree order (leading
+ * dimension ldb), y is N x nrhs column-major in S order (row side, ldy).
+ * q_row as produced by h2sp_build.  Leaves to root: z = Q_t^T x_t,
+ * z[k_t:] -> y, z[:k_t] -> parent's local vector. */
+h2sp_status h2sp_apply_Ut(h2sp_plan plan, const double *q_row, const double *b, int64_t ldb, double *y,
+                          int64_t ldy, int nrhs, void *ws, size_t ws_bytes, void *stream);
+/* x = V y: y in S order (column side), x in tree order.  Root to leaves:
+ * x_t = Q_t [z_basis; y_t].  q_col as produced by h2sp_build (q_row if
+ * symmetric). */
+h2sp_status h2sp_apply_V(h2sp_plan plan, const double *q_col, const double *y, int64_t ldy, double *x,
+                         int64_t ldx, int nrhs, void *ws, size_t ws_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* H2SP_H */

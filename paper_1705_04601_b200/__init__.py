@@ -1,0 +1,257 @@
+"""Python binding of ``libh2sp`` -- the B200-native non-extensive sparsification of
+an H^2 matrix (arXiv 1705.04601), ``A = U S V^T`` (PAPER.md Eq. main_fact,
+P:477-484).
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels
+behind the C ABI declared in ``include/h2sp.h``.  PyTorch provides device
+memory and streams.  There is no CPU fallback: importing this package raises
+if ``libh2sp.so`` has not been built (``python -c "import __graft_entry__ as g;
+g.build()"``), and every call that reaches the device raises if CUDA is
+unavailable.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Dict, Optional
+
+import numpy as np
+
+__all__ = ["LIB_PATH", "H2spError", "Plan", "Sparsifier", "lib", "declared_symbols"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libh2sp.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "h2sp.h")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build the CUDA library first (__graft_entry__.build())")
+lib = ctypes.CDLL(LIB_PATH)
+
+_i32, _i64, _f64, _vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
+_P_i32, _P_i64, _P_f64 = ctypes.POINTER(_i32), ctypes.POINTER(_i64), ctypes.POINTER(_f64)
+
+
+class _Structure(ctypes.Structure):
+    _fields_ = [("L", _i32), ("leaf_size", _i32), ("symmetric", _i32), ("rank_row", _P_i32), ("rank_col", _P_i32),
+                ("near_ptr", _P_i64), ("near_col", _P_i32), ("adm_ptr", ctypes.POINTER(_P_i64)),
+                ("adm_col", ctypes.POINTER(_P_i32))]
+
+
+class _Sizes(ctypes.Structure):
+    _fields_ = [(n, _i64) for n in ("n", "n_clusters", "leaf_row", "transfer_row", "leaf_col", "transfer_col", "close",
+                                    "coupling", "q_row", "q_col", "s_nnz", "s_blocks", "workspace_bytes", "meta_bytes",
+                                    "levels_active", "launches")] + \
+               [(n, _f64) for n in ("flops", "bytes", "flops_congruence", "flops_strips")]
+
+
+class _Inputs(ctypes.Structure):
+    _fields_ = [(n, _vp) for n in ("leaf_basis_row", "transfer_row", "leaf_basis_col", "transfer_col", "close",
+                                   "coupling")]
+
+
+class _Outputs(ctypes.Structure):
+    _fields_ = [(n, _vp) for n in ("q_row", "q_col", "s_rowptr", "s_col", "s_val")]
+
+
+_st = ctypes.c_int
+lib.h2sp_status_str.restype = ctypes.c_char_p
+lib.h2sp_status_str.argtypes = [_st]
+lib.h2sp_last_error.restype = ctypes.c_char_p
+lib.h2sp_plan_create.argtypes = [ctypes.POINTER(_Structure), ctypes.c_int, ctypes.POINTER(_vp)]
+lib.h2sp_plan_sizes.argtypes = [_vp, ctypes.POINTER(_Sizes)]
+lib.h2sp_plan_offsets.argtypes = [_vp] + [_P_i64] * 6
+lib.h2sp_plan_pattern.argtypes = [_vp, _P_i64, _P_i32]
+lib.h2sp_plan_destroy.argtypes = [_vp]
+lib.h2sp_plan_destroy.restype = None
+lib.h2sp_plan_upload.argtypes = [_vp, _vp, ctypes.c_size_t, _vp]
+lib.h2sp_build.argtypes = [_vp, ctypes.POINTER(_Inputs), ctypes.POINTER(_Outputs), _vp, ctypes.c_size_t, _vp]
+lib.h2sp_build_host.argtypes = [_vp, ctypes.POINTER(_Inputs), ctypes.POINTER(_Outputs), ctypes.POINTER(_Inputs),
+                                ctypes.POINTER(_Outputs), _vp, ctypes.c_size_t, _vp]
+lib.h2sp_apply_ws_bytes.argtypes = [_vp, ctypes.c_int]
+lib.h2sp_apply_ws_bytes.restype = _i64
+lib.h2sp_apply_Ut.argtypes = [_vp, _vp, _vp, _i64, _vp, _i64, ctypes.c_int, _vp, ctypes.c_size_t, _vp]
+lib.h2sp_apply_V.argtypes = [_vp, _vp, _vp, _i64, _vp, _i64, ctypes.c_int, _vp, ctypes.c_size_t, _vp]
+
+
+class H2spError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        msg = lib.h2sp_status_str(status).decode()
+        detail = lib.h2sp_last_error().decode()
+        super().__init__(f"{where}: {msg} ({detail})")
+
+
+def _check(status: int, where: str):
+    if status != 0:
+        raise H2spError(status, where)
+
+
+def declared_symbols():
+    """Function names declared in include/h2sp.h (for the ABI export test)."""
+    import re
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(h2sp_[a-zA-Z_]+)\s*\(", txt)))
+
+
+def _ptr(a: np.ndarray, ct):
+    return a.ctypes.data_as(ctypes.POINTER(ct))
+
+
+class Plan:
+    """Symbolic phase (host): ``h2sp_plan_create`` on the structure arrays of a
+    packed H^2 input (``h2gen.pack``-style dict: L, B, symmetric, rank_row,
+    rank_col, near_ptr, near_col, adm_ptr[k], adm_col[k])."""
+
+    def __init__(self, packed: dict):
+        self._keep = []
+        L = int(packed["L"])
+        rr = np.ascontiguousarray(packed["rank_row"], dtype=np.int32)
+        rc = np.ascontiguousarray(packed["rank_col"], dtype=np.int32) if packed.get("rank_col") is not None else None
+        npt = np.ascontiguousarray(packed["near_ptr"], dtype=np.int64)
+        ncl = np.ascontiguousarray(packed["near_col"], dtype=np.int32)
+        aps = [np.ascontiguousarray(a, dtype=np.int64) for a in packed["adm_ptr"]]
+        acs = [np.ascontiguousarray(a, dtype=np.int32) for a in packed["adm_col"]]
+        self._keep += [rr, rc, npt, ncl, aps, acs]
+        ap_arr = (_P_i64 * max(L, 1))(*[_ptr(a, _i64) for a in aps])
+        ac_arr = (_P_i32 * max(L, 1))(*[_ptr(a, _i32) for a in acs])
+        self._keep += [ap_arr, ac_arr]
+        st = _Structure(L=L, leaf_size=int(packed["B"]), symmetric=int(packed["symmetric"]),
+                        rank_row=_ptr(rr, _i32), rank_col=_ptr(rc, _i32) if rc is not None else None,
+                        near_ptr=_ptr(npt, _i64), near_col=_ptr(ncl, _i32), adm_ptr=ap_arr, adm_col=ac_arr)
+        h = _vp()
+        _check(lib.h2sp_plan_create(ctypes.byref(st), 0, ctypes.byref(h)), "h2sp_plan_create")
+        self.handle = h
+        self._keep = None
+        sz = _Sizes()
+        _check(lib.h2sp_plan_sizes(self.handle, ctypes.byref(sz)), "h2sp_plan_sizes")
+        self.sizes = {f: getattr(sz, f) for f, _ in _Sizes._fields_}
+        self.L = L
+        self.B = int(packed["B"])
+        self.symmetric = bool(packed["symmetric"])
+        self.N = self.sizes["n"]
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            lib.h2sp_plan_destroy(h)
+            self.handle = None
+
+    def offsets(self) -> Dict[str, np.ndarray]:
+        n = self.sizes["n_clusters"]
+        out = {k: np.zeros(n, dtype=np.int64) for k in ("s_off_row", "s_off_col", "q_off_row", "q_off_col",
+                                                         "n_row", "n_col")}
+        _check(lib.h2sp_plan_offsets(self.handle, *[_ptr(out[k], _i64) for k in ("s_off_row", "s_off_col",
+                                                                                   "q_off_row", "q_off_col",
+                                                                                   "n_row", "n_col")]),
+               "h2sp_plan_offsets")
+        return out
+
+    def pattern(self, with_cols: bool = True):
+        rowptr = np.zeros(self.N + 1, dtype=np.int64)
+        col = np.zeros(self.sizes["s_nnz"], dtype=np.int32) if with_cols else None
+        _check(lib.h2sp_plan_pattern(self.handle, _ptr(rowptr, _i64), _ptr(col, _i32) if with_cols else None),
+               "h2sp_plan_pattern")
+        return rowptr, col
+
+
+def _dptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _stream_handle(stream) -> Optional[int]:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+class Sparsifier:
+    """Device buffers for one plan: inputs (copied once from a packed dict),
+    outputs and the uploaded workspace; ``build()`` runs ``h2sp_build``."""
+
+    def __init__(self, plan: Plan, packed: Optional[dict] = None, device="cuda", alloc_inputs: bool = True):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1705_04601_b200 needs a CUDA device (no CPU fallback)")
+        self.plan = plan
+        self.device = torch.device(device)
+        sz = plan.sizes
+        f64 = dict(dtype=torch.float64, device=self.device)
+        self.inputs = {}
+        if alloc_inputs:
+            names = [("leaf_basis_row", "leaf_row", "leaf_row"), ("transfer_row", "transfer_row", "transfer_row"),
+                     ("close", "close", "close"), ("coupling", "coupling", "coupling")]
+            if not plan.symmetric:
+                names += [("leaf_basis_col", "leaf_col", "leaf_col"), ("transfer_col", "transfer_col", "transfer_col")]
+            for abi, key, szk in names:
+                n = int(sz[szk])
+                t = torch.empty(max(n, 1), **f64)
+                if packed is not None and n:
+                    src = np.ascontiguousarray(packed[key], dtype=np.float64).ravel()
+                    if src.size != n:
+                        raise ValueError(f"input {key}: {src.size} values, plan expects {n}")
+                    t[:n].copy_(torch.from_numpy(src))
+                self.inputs[abi] = t
+        self.outputs = {
+            "q_row": torch.empty(max(int(sz["q_row"]), 1), **f64),
+            "q_col": torch.empty(max(int(sz["q_col"]), 1), **f64) if not plan.symmetric else None,
+            "s_rowptr": torch.empty(plan.N + 1, dtype=torch.int64, device=self.device),
+            "s_col": torch.empty(max(int(sz["s_nnz"]), 1), dtype=torch.int32, device=self.device),
+            "s_val": torch.empty(max(int(sz["s_nnz"]), 1), **f64),
+        }
+        self.ws = torch.empty(int(sz["workspace_bytes"]) + 256, dtype=torch.uint8, device=self.device)
+        self.ws_ptr = (self.ws.data_ptr() + 255) // 256 * 256
+        self.ws_bytes = int(sz["workspace_bytes"])
+        _check(lib.h2sp_plan_upload(plan.handle, self.ws_ptr, self.ws_bytes, _stream_handle(None)), "h2sp_plan_upload")
+
+    def _abi_inputs(self, inputs=None):
+        src = inputs if inputs is not None else self.inputs
+        return _Inputs(**{k: _dptr(src.get(k)) for k, _ in _Inputs._fields_})
+
+    def _abi_outputs(self, outputs=None):
+        o = outputs if outputs is not None else self.outputs
+        return _Outputs(**{k: _dptr(o.get(k)) for k, _ in _Outputs._fields_})
+
+    def build(self, stream=None, write_index: bool = True):
+        out = self._abi_outputs()
+        if not write_index:
+            out.s_rowptr = None
+            out.s_col = None
+        _check(lib.h2sp_build(self.plan.handle, ctypes.byref(self._abi_inputs()), ctypes.byref(out), self.ws_ptr,
+                              self.ws_bytes, _stream_handle(stream)), "h2sp_build")
+        return self.outputs
+
+    def build_host(self, host_inputs: dict, host_outputs: dict, stream=None):
+        """End-to-end: H2D of host (pinned) inputs, build, D2H of all outputs."""
+        hi = _Inputs(**{k: _dptr(host_inputs.get(k)) for k, _ in _Inputs._fields_})
+        ho = _Outputs(**{k: _dptr(host_outputs.get(k)) for k, _ in _Outputs._fields_})
+        _check(lib.h2sp_build_host(self.plan.handle, ctypes.byref(hi), ctypes.byref(ho),
+                                   ctypes.byref(self._abi_inputs()), ctypes.byref(self._abi_outputs()), self.ws_ptr,
+                                   self.ws_bytes, _stream_handle(stream)), "h2sp_build_host")
+
+    def apply_ws(self, nrhs: int):
+        import torch
+        need = int(lib.h2sp_apply_ws_bytes(self.plan.handle, nrhs))
+        if need <= self.ws_bytes:
+            return self.ws_ptr, self.ws_bytes
+        ws = torch.empty(need + 256, dtype=torch.uint8, device=self.device)
+        ptr = (ws.data_ptr() + 255) // 256 * 256
+        _check(lib.h2sp_plan_upload(self.plan.handle, ptr, need, _stream_handle(None)), "h2sp_plan_upload")
+        self._apply_ws = ws
+        return ptr, need
+
+    def apply_Ut(self, b, y, stream=None, ws=None):
+        """y = U^T b; b, y: (nrhs, N) contiguous float64 CUDA tensors (= N x nrhs column-major)."""
+        nrhs = b.shape[0] if b.dim() == 2 else 1
+        ptr, nb = ws if ws is not None else self.apply_ws(nrhs)
+        _check(lib.h2sp_apply_Ut(self.plan.handle, self.outputs["q_row"].data_ptr(), b.data_ptr(), self.plan.N,
+                                 y.data_ptr(), self.plan.N, nrhs, ptr, nb, _stream_handle(stream)), "h2sp_apply_Ut")
+        return y
+
+    def apply_V(self, y, x, stream=None, ws=None):
+        """x = V y; y, x: (nrhs, N) contiguous float64 CUDA tensors."""
+        nrhs = y.shape[0] if y.dim() == 2 else 1
+        ptr, nb = ws if ws is not None else self.apply_ws(nrhs)
+        q = self.outputs["q_row"] if self.plan.symmetric else self.outputs["q_col"]
+        _check(lib.h2sp_apply_V(self.plan.handle, q.data_ptr(), y.data_ptr(), self.plan.N, x.data_ptr(), self.plan.N,
+                                nrhs, ptr, nb, _stream_handle(stream)), "h2sp_apply_V")
+        return x

@@ -1,0 +1,123 @@
+// C-ABI entry points of the numeric phase (include/h2sp.h).  Argument checks,
+// workspace carving and stream-ordered copies; all arithmetic is in kernels.cu.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <string>
+
+#include "h2sp_internal.h"
+
+using namespace h2sp;
+
+namespace {
+
+h2sp_status check_ws(const h2sp_plan_s *P, const void *ws, size_t ws_bytes, size_t need) {
+  if (!ws) return fail(H2SP_EINVAL, "workspace is NULL");
+  if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(H2SP_EINVAL, "workspace not 256-byte aligned");
+  if (ws_bytes < need)
+    return fail(H2SP_EINVAL, "workspace too small: " + std::to_string(ws_bytes) + " < " + std::to_string(need));
+  (void)P;
+  return H2SP_OK;
+}
+
+h2sp_status cuda_ok(cudaError_t e, const char *what) {
+  if (e != cudaSuccess) return fail(H2SP_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return H2SP_OK;
+}
+
+h2sp_status check_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) return fail(H2SP_ECUDA, "no CUDA device (the library has no CPU fallback)");
+  return H2SP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+h2sp_status h2sp_plan_upload(h2sp_plan P, void *ws, size_t ws_bytes, void *stream) {
+  if (!P) return fail(H2SP_EINVAL, "NULL plan");
+  if (h2sp_status s = check_device()) return s;
+  if (h2sp_status s = check_ws(P, ws, ws_bytes, P->meta_bytes)) return s;
+  return cuda_ok(cudaMemcpyAsync(ws, P->meta.data(), P->meta_bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream),
+                 "upload of plan work lists");
+}
+
+h2sp_status h2sp_build(h2sp_plan P, const h2sp_inputs *in, const h2sp_outputs *out, void *ws, size_t ws_bytes,
+                       void *stream) {
+  if (!P || !in || !out) return fail(H2SP_EINVAL, "NULL plan, inputs or outputs");
+  if (h2sp_status s = check_ws(P, ws, ws_bytes, P->ws_total)) return s;
+  if (!in->leaf_basis_row || (P->tr_row_len && !in->transfer_row) || (P->close_len && !in->close) ||
+      (P->coupling_len && !in->coupling))
+    return fail(H2SP_EINVAL, "NULL input array");
+  if (!P->sym && ((P->leaf_col_len && !in->leaf_basis_col) || (P->tr_col_len && !in->transfer_col)))
+    return fail(H2SP_EINVAL, "NULL column-side input array in general mode");
+  if (!out->q_row || !out->s_val || (!P->sym && !out->q_col)) return fail(H2SP_EINVAL, "NULL output array");
+  if (h2sp_status s = check_device()) return s;
+  int64_t nl = 0;
+  return launch_build(P, in, out, static_cast<unsigned char *>(ws), stream, &nl);
+}
+
+h2sp_status h2sp_build_host(h2sp_plan P, const h2sp_inputs *hi, const h2sp_outputs *ho, const h2sp_inputs *di,
+                            const h2sp_outputs *dout, void *ws, size_t ws_bytes, void *stream) {
+  if (!P || !hi || !ho || !di || !dout) return fail(H2SP_EINVAL, "NULL argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  auto h2d = [&](const double *d, const double *h, int64_t n) -> h2sp_status {
+    if (n == 0) return H2SP_OK;
+    if (!d || !h) return fail(H2SP_EINVAL, "NULL input buffer");
+    return cuda_ok(cudaMemcpyAsync(const_cast<double *>(d), h, size_t(n) * 8, cudaMemcpyHostToDevice, st), "H2D");
+  };
+  if (h2sp_status s = h2d(di->leaf_basis_row, hi->leaf_basis_row, P->leaf_row_len)) return s;
+  if (h2sp_status s = h2d(di->transfer_row, hi->transfer_row, P->tr_row_len)) return s;
+  if (!P->sym) {
+    if (h2sp_status s = h2d(di->leaf_basis_col, hi->leaf_basis_col, P->leaf_col_len)) return s;
+    if (h2sp_status s = h2d(di->transfer_col, hi->transfer_col, P->tr_col_len)) return s;
+  }
+  if (h2sp_status s = h2d(di->close, hi->close, P->close_len)) return s;
+  if (h2sp_status s = h2d(di->coupling, hi->coupling, P->coupling_len)) return s;
+  if (h2sp_status s = h2sp_build(P, di, dout, ws, ws_bytes, stream)) return s;
+  auto d2h = [&](void *h, const void *d, size_t bytes) -> h2sp_status {
+    if (bytes == 0 || !h) return H2SP_OK;
+    if (!d) return fail(H2SP_EINVAL, "NULL device output");
+    return cuda_ok(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, st), "D2H");
+  };
+  if (h2sp_status s = d2h(ho->q_row, dout->q_row, size_t(P->q_row_len) * 8)) return s;
+  if (!P->sym)
+    if (h2sp_status s = d2h(ho->q_col, dout->q_col, size_t(P->q_col_len) * 8)) return s;
+  if (h2sp_status s = d2h(ho->s_val, dout->s_val, size_t(P->s_nnz) * 8)) return s;
+  if (dout->s_col)
+    if (h2sp_status s = d2h(ho->s_col, dout->s_col, size_t(P->s_nnz) * 4)) return s;
+  if (dout->s_rowptr)
+    if (h2sp_status s = d2h(ho->s_rowptr, dout->s_rowptr, size_t(P->N + 1) * 8)) return s;
+  return H2SP_OK;
+}
+
+int64_t h2sp_apply_ws_bytes(h2sp_plan P, int nrhs) {
+  if (!P || nrhs < 0) return -1;
+  int64_t z = P->zb_row_len > P->zb_col_len ? P->zb_row_len : P->zb_col_len;
+  return int64_t(P->meta_bytes) + z * int64_t(nrhs) * 8;
+}
+
+static h2sp_status apply_common(h2sp_plan P, const double *q, const void *a, int64_t lda, void *b, int64_t ldb,
+                                int nrhs, void *ws, size_t ws_bytes) {
+  if (!P || !q || !a || !b) return fail(H2SP_EINVAL, "NULL argument");
+  if (nrhs < 1) return fail(H2SP_EINVAL, "nrhs < 1");
+  if (lda < P->N || ldb < P->N) return fail(H2SP_EINVAL, "leading dimension < N");
+  if (h2sp_status s = check_ws(P, ws, ws_bytes, size_t(h2sp_apply_ws_bytes(P, nrhs)))) return s;
+  return check_device();
+}
+
+h2sp_status h2sp_apply_Ut(h2sp_plan P, const double *q_row, const double *b, int64_t ldb, double *y, int64_t ldy,
+                          int nrhs, void *ws, size_t ws_bytes, void *stream) {
+  if (h2sp_status s = apply_common(P, q_row, b, ldb, y, ldy, nrhs, ws, ws_bytes)) return s;
+  return launch_apply_Ut(P, q_row, b, ldb, y, ldy, nrhs, static_cast<unsigned char *>(ws), stream, false);
+}
+
+h2sp_status h2sp_apply_V(h2sp_plan P, const double *q_col, const double *y, int64_t ldy, double *x, int64_t ldx,
+                         int nrhs, void *ws, size_t ws_bytes, void *stream) {
+  if (h2sp_status s = apply_common(P, q_col, y, ldy, x, ldx, nrhs, ws, ws_bytes)) return s;
+  return launch_apply_V(P, q_col, y, ldy, x, ldx, nrhs, static_cast<unsigned char *>(ws), stream, !P->sym);
+}
+
+}  // extern "C"

@@ -1,0 +1,138 @@
+// Internal plan / work-list layout shared by the host plan (plan.cpp) and the
+// sm_100a kernels (kernels.cu).  Every struct here is POD and lives verbatim in
+// the device "meta" region at the start of the build workspace.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/h2sp.h"
+
+namespace h2sp {
+
+// Source kinds of the four quadrants of a merged close block G_ts (step (iv),
+// P:238-250): children pair (t_a, s_b) is near -> its H basis x basis part;
+// admissible -> its orthogonalised coupling D~.  "_T" = read the canonical
+// (t <= s) block transposed (symmetric mode).
+enum GKind : int32_t { G_EMPTY = 0, G_BB = 1, G_BB_T = 2, G_DT = 3, G_DT_T = 4 };
+
+// One congruence H_ts = Q^R_t^T G_ts Q^C_s for (t, s) in N_k (canonical t <= s
+// when symmetric).  Offsets are element offsets (doubles) into the named
+// buffers; -1 = not produced.
+struct PairItem {
+  int32_t t, s;          // level-major cluster ids (row side t, column side s)
+  int32_t gkind;         // 4 x 4 bits (quadrant a*2+b at bits 4*(a*2+b)), level >= 1
+  int32_t s_ld;          // row length (elements) of S block row (t@k)
+  int32_t s_ld_m;        // row length of S block row (s@k) (mirror, symmetric)
+  int32_t pad_;
+  int64_t g_src[4];      // level 0: g_src[0] = offset of C_ts in `close`; else slot offsets
+  int64_t s_dst;         // S block (t@k, s@k): element (0,0) in s_val
+  int64_t s_dst_m;       // symmetric: S block (s@k, t@k) (transpose), t != s
+  int64_t bb_dst;        // H[:k_t, :k_s]      -> bb buffer (k_t x k_s)
+  int64_t yr_dst;        // H[:k_t, k_s:]      -> row strip (k_t x m_s)
+  int64_t yc_dst;        // H[k_t:, :k_s]^T    -> transposed column strip (k_s x m_t);
+                         //                      symmetric: row strip of (s, t)
+};
+
+// One strip rotation W = Q_q^T Z (Eq. u1v1): Z stacks the strips of
+// the two children of q (child 2 rows at offset k_c1), width m.  Frozen rows
+// [k_q, n_q) of W go to S (directly and/or transposed), basis rows continue.
+struct StripItem {
+  int32_t q;             // rotating cluster (level-major id)
+  int32_t m;             // strip width (frozen size of the fixed cluster)
+  int32_t s_ld;          // row length for the direct S block
+  int32_t s_ld_t;        // row length for the transposed S block
+  int64_t src[2];        // child strip slots (k_c x m), -1 if absent
+  int64_t s_dst;         // S[s_dst + a*s_ld + b]   = W[k_q + a][b]
+  int64_t s_dst_t;       // S[s_dst_t + b*s_ld_t + a] = W[k_q + a][b]
+  int64_t y_dst;         // W[:k_q] -> continuing strip slot (k_q x m)
+};
+
+// A run of items that share the rotating cluster (Q kept in shared memory).
+struct Chunk {
+  int32_t begin, end;
+};
+
+struct CouplingItem {    // D~ = R^R_t D R^C_s^T (reading 11)
+  int32_t t, s;          // level-major ids
+  int64_t d_src;         // offset of D_ts in `coupling`
+  int64_t dt_dst;        // slot offset in the dt buffer
+};
+
+struct CsrBlockRow {     // rows [row0, row0 + m_r) of S, all with the same column pattern
+  int64_t row0;
+  int64_t p_base;        // s_val offset of row row0
+  int32_t m_r;
+  int32_t rowlen;
+  int32_t blk_begin, nblk;
+};
+
+struct CsrBlock {        // columns [col0, col0 + m_c) at row positions [colpos, colpos + m_c)
+  int32_t col0, m_c, colpos, pad_;
+};
+
+struct LevelPlan {
+  int k;
+  int np_row, np_col;    // max n_t at this level (row / column side)
+  int mp;                // max strip width at this level
+  int64_t n_pairs, n_pair_chunks;
+  int64_t n_rstrips, n_rstrip_chunks;
+  int64_t n_cstrips, n_cstrip_chunks;
+  int64_t n_coup;
+  size_t pairs_off, pair_chunks_off;          // byte offsets in meta
+  size_t rstrips_off, rstrip_chunks_off;
+  size_t cstrips_off, cstrip_chunks_off;
+  size_t coup_off;
+  int np_pair;           // padded tile size for the congruence at this level
+  int np_rstrip, np_cstrip;
+};
+
+struct ClusterArrays {   // byte offsets in meta of per-cluster arrays
+  size_t n_row, k_row, n_col, k_col;       // int32 [ncl]
+  size_t q_off_row, q_off_col;             // int64 [ncl]
+  size_t rh_off_row, rh_off_col;           // int64 [ncl]
+  size_t leaf_off_row, leaf_off_col;       // int64 [n_leaves]
+  size_t tr_off_row, tr_off_col;           // int64 [ncl]
+  size_t s_off_row, s_off_col;             // int64 [ncl]
+  size_t zb_off_row, zb_off_col;           // int64 [ncl]: apply basis-coefficient slots (per rhs)
+};
+
+}  // namespace h2sp
+
+struct h2sp_plan_s {
+  int32_t L, B, sym;
+  int64_t N, ncl;
+  std::vector<int32_t> n_row, k_row, n_col, k_col;
+  std::vector<int64_t> q_off_row, q_off_col, s_off_row, s_off_col;
+  int64_t q_row_len, q_col_len;
+  int64_t leaf_row_len, leaf_col_len, tr_row_len, tr_col_len, close_len, coupling_len;
+  int64_t rh_row_len, rh_col_len, dt_len, bb_len, yr_len, yc_len;
+  int64_t zb_row_len, zb_col_len;          // per rhs
+  int64_t s_nnz, s_blocks;
+  int levels_active;
+  double flops, bytes, flops_cong, flops_strip;
+  std::vector<h2sp::LevelPlan> levels;
+  h2sp::ClusterArrays ca;
+  size_t csr_rows_off, csr_blocks_off, rowptr_off;
+  int64_t n_csr_rows, n_csr_blocks;
+  std::vector<unsigned char> meta;          // device image of all work lists
+  size_t meta_bytes;
+  // workspace layout after the meta region (byte offsets)
+  size_t ws_rh_row, ws_rh_col, ws_dt, ws_bb, ws_yr, ws_yc, ws_total;
+  int64_t launches;
+  uint64_t magic;                           // first 8 bytes of the meta image (checked on device)
+};
+
+namespace h2sp {
+void set_error(const std::string &msg);
+h2sp_status fail(h2sp_status s, const std::string &msg);
+
+// kernels.cu
+h2sp_status launch_build(const h2sp_plan_s *p, const h2sp_inputs *in, const h2sp_outputs *out, unsigned char *ws,
+                         void *stream, int64_t *launches);
+h2sp_status launch_apply_Ut(const h2sp_plan_s *p, const double *q, const double *b, int64_t ldb, double *y,
+                            int64_t ldy, int nrhs, unsigned char *ws, void *stream, bool col_side);
+h2sp_status launch_apply_V(const h2sp_plan_s *p, const double *q, const double *y, int64_t ldy, double *x,
+                           int64_t ldx, int nrhs, unsigned char *ws, void *stream, bool col_side);
+}  // namespace h2sp

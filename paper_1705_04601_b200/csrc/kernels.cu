@@ -1,0 +1,827 @@
+// sm_100a FP64 kernels of the H^2 sparsification hot path:
+//   qr_kernel        step (i)   QR completion Q_t = [W_t, W_t^perp], R^_t
+//   coupling_kernel             D~ = R^_t D R^_s^T
+//   pair_kernel      (iv)+(ii)+(iii)  merge G_ts, H = Q_t^T G Q_s, freeze
+//   strip_kernel     (ii)/(iii) strips W = Q_q^T Z, freeze                  (Eq. u1v1)
+//   csr_cols_kernel  (iii)      CSR column indices of S
+//   apply_*          U^T b, V y
+// Dense contractions use FP64 DMMA (mma.sync m8n8k4 .f64, the native FP64
+// tensor-core shape on sm_100a; tcgen05 has no f64 kind) with operands staged
+// in shared memory; Q_t of the rotating cluster stays resident in shared
+// memory across the run of items (a block row) of one CTA.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+
+#include "h2sp_internal.h"
+
+namespace h2sp {
+
+struct Clusters {  // device views of the per-cluster arrays in the meta region
+  const int32_t *n_row, *k_row, *n_col, *k_col;
+  const int64_t *q_off_row, *q_off_col, *rh_off_row, *rh_off_col;
+  const int64_t *leaf_off_row, *leaf_off_col, *tr_off_row, *tr_off_col;
+  const int64_t *s_off_row, *s_off_col, *zb_off_row, *zb_off_col;
+};
+
+static Clusters make_clusters(const h2sp_plan_s *p, const unsigned char *meta) {
+  Clusters c;
+  c.n_row = (const int32_t *)(meta + p->ca.n_row);
+  c.k_row = (const int32_t *)(meta + p->ca.k_row);
+  c.n_col = (const int32_t *)(meta + p->ca.n_col);
+  c.k_col = (const int32_t *)(meta + p->ca.k_col);
+  c.q_off_row = (const int64_t *)(meta + p->ca.q_off_row);
+  c.q_off_col = (const int64_t *)(meta + p->ca.q_off_col);
+  c.rh_off_row = (const int64_t *)(meta + p->ca.rh_off_row);
+  c.rh_off_col = (const int64_t *)(meta + p->ca.rh_off_col);
+  c.leaf_off_row = (const int64_t *)(meta + p->ca.leaf_off_row);
+  c.leaf_off_col = (const int64_t *)(meta + p->ca.leaf_off_col);
+  c.tr_off_row = (const int64_t *)(meta + p->ca.tr_off_row);
+  c.tr_off_col = (const int64_t *)(meta + p->ca.tr_off_col);
+  c.s_off_row = (const int64_t *)(meta + p->ca.s_off_row);
+  c.s_off_col = (const int64_t *)(meta + p->ca.s_off_col);
+  c.zb_off_row = (const int64_t *)(meta + p->ca.zb_off_row);
+  c.zb_off_col = (const int64_t *)(meta + p->ca.zb_off_col);
+  return c;
+}
+
+struct Side {  // one side (row or column) of the cluster arrays
+  const int32_t *n, *k;
+  const int64_t *q_off, *rh_off, *leaf_off, *tr_off, *s_off, *zb_off;
+};
+
+static Side side_of(const Clusters &c, bool col) {
+  Side s;
+  s.n = col ? c.n_col : c.n_row;
+  s.k = col ? c.k_col : c.k_row;
+  s.q_off = col ? c.q_off_col : c.q_off_row;
+  s.rh_off = col ? c.rh_off_col : c.rh_off_row;
+  s.leaf_off = col ? c.leaf_off_col : c.leaf_off_row;
+  s.tr_off = col ? c.tr_off_col : c.tr_off_row;
+  s.s_off = col ? c.s_off_col : c.s_off_row;
+  s.zb_off = col ? c.zb_off_col : c.zb_off_row;
+  return s;
+}
+
+__host__ __device__ inline int64_t lvl_off_d(int L, int k) {
+  return (int64_t(1) << (L + 1)) - (int64_t(1) << (L - k + 1));
+}
+
+// --------------------------------------------------------------------------
+// DMMA helper: D(8x8) += A(8x4, row) * B(4x8, col), FP64.
+// Fragments (PTX ISA, mma.m8n8k4 .f64): a = A[lane/4][lane%4],
+// b = B[lane%4][lane/4], d = D[lane/4][2*(lane%4) + {0,1}].
+// --------------------------------------------------------------------------
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// Warp GEMM on shared-memory tiles with leading dimension LD:
+//   acc[i][j] (8x8 tile at rows m0+8i, cols n0+8j) += sum_kk A(m, kk) B(kk, n)
+//   A(m, kk) = AT ? sA[kk*LD + m] : sA[m*LD + kk];  B(kk, n) = sB[kk*LD + n].
+template <int LD, int TM, int TN, bool AT>
+__device__ __forceinline__ void warp_gemm(const double *__restrict__ sA, const double *__restrict__ sB, int m0,
+                                          int n0, int kmax, double (&acc)[TM][TN][2]) {
+  const int lane = threadIdx.x & 31;
+  const int r = lane >> 2, q = lane & 3;
+#pragma unroll 4
+  for (int k0 = 0; k0 < kmax; k0 += 4) {
+    double a[TM], b[TN];
+#pragma unroll
+    for (int i = 0; i < TM; i++) a[i] = AT ? sA[(k0 + q) * LD + m0 + i * 8 + r] : sA[(m0 + i * 8 + r) * LD + k0 + q];
+#pragma unroll
+    for (int j = 0; j < TN; j++) b[j] = sB[(k0 + q) * LD + n0 + j * 8 + r];
+#pragma unroll
+    for (int i = 0; i < TM; i++)
+#pragma unroll
+      for (int j = 0; j < TN; j++) dmma(acc[i][j], a[i], b[j]);
+  }
+}
+
+template <int LD, int TM, int TN>
+__device__ __forceinline__ void warp_store(double *sC, int m0, int n0, const double (&acc)[TM][TN][2]) {
+  const int lane = threadIdx.x & 31;
+  const int r = lane >> 2, q = lane & 3;
+#pragma unroll
+  for (int i = 0; i < TM; i++)
+#pragma unroll
+    for (int j = 0; j < TN; j++) {
+      double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
+      *reinterpret_cast<double2 *>(&sC[(m0 + i * 8 + r) * LD + n0 + j * 8 + 2 * q]) = v;
+    }
+}
+
+template <int TM, int TN>
+__device__ __forceinline__ void zero_acc(double (&acc)[TM][TN][2]) {
+#pragma unroll
+  for (int i = 0; i < TM; i++)
+#pragma unroll
+    for (int j = 0; j < TN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+}
+
+// Load an n x m row-major global block into a padded NR x NC shared tile (LD), zero fill.
+template <int NR, int NC, int LD>
+__device__ __forceinline__ void load_tile(double *s, const double *__restrict__ g, int n, int m, int ldg) {
+  for (int idx = threadIdx.x; idx < NR * NC; idx += blockDim.x) {
+    int i = idx / NC, j = idx % NC;
+    s[i * LD + j] = (i < n && j < m) ? g[int64_t(i) * ldg + j] : 0.0;
+  }
+}
+
+// --------------------------------------------------------------------------
+// Step (i): QR completion (convention H, readings 1-2).
+// One CTA per cluster of the level; 128 threads.
+//   X = R_leaf (level 0) or [R^_c1 T[:k1]; R^_c2 T[k1:]] (internal)
+//   Householder on X (alpha = x_0, sigma = ||x_1:||; sigma == 0 -> tau = 0;
+//   beta = -sgn(alpha) hypot(alpha, sigma), sgn(+-0) = +1), R^ = triu(X[:k]),
+//   Q = H_0 ... H_{k-1} I_n.
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) qr_kernel(Side sd, int L, int level, const double *__restrict__ leaf,
+                                                 const double *__restrict__ transfer, double *__restrict__ rh,
+                                                 double *__restrict__ qout, const uint64_t *meta_magic,
+                                                 uint64_t magic) {
+  if (meta_magic && threadIdx.x == 0 && blockIdx.x == 0 && *meta_magic != magic) __trap();
+  const int64_t base = lvl_off_d(L, level);
+  const int64_t cl = base + blockIdx.x;
+  const int n = sd.n[cl], k = sd.k[cl];
+  if (n == 0) return;
+  extern __shared__ double sm[];
+  const int ldx = k + 1;           // X: n x k (ldx), reflectors stored below the diagonal
+  const int ldq = n + 1;           // Q: n x n
+  double *X = sm;
+  double *Q = X + n * ldx;
+  double *tau = Q + n * ldq;
+  __shared__ double s_scal[3];     // beta, tau, 1/(alpha - beta) unused; scale divisor
+  const int tid = threadIdx.x;
+  // ---- load X
+  if (level == 0) {
+    const double *R = leaf + sd.leaf_off[cl];
+    for (int idx = tid; idx < n * k; idx += blockDim.x) X[(idx / k) * ldx + idx % k] = R[idx];
+  } else {
+    const int64_t ci = cl - base;
+    const int64_t c1 = lvl_off_d(L, level - 1) + 2 * ci, c2 = c1 + 1;
+    const int k1 = sd.k[c1], k2 = sd.k[c2];
+    const double *T = transfer + sd.tr_off[cl];       // n x k
+    const double *R1 = rh + sd.rh_off[c1];            // k1 x k1 upper
+    const double *R2 = rh + sd.rh_off[c2];            // k2 x k2 upper
+    for (int idx = tid; idx < n * k; idx += blockDim.x) {
+      const int i = idx / k, j = idx % k;
+      double acc = 0.0;
+      if (i < k1) {
+        for (int l = i; l < k1; l++) acc = fma(R1[i * k1 + l], T[l * k + j], acc);
+      } else {
+        const int ii = i - k1;
+        for (int l = ii; l < k2; l++) acc = fma(R2[ii * k2 + l], T[(k1 + l) * k + j], acc);
+      }
+      X[i * ldx + j] = acc;
+    }
+  }
+  __syncthreads();
+  const int warp = tid >> 5, lane = tid & 31;
+  // ---- Householder factorisation
+  for (int j = 0; j < k; j++) {
+    if (warp == 0) {
+      double ss = 0.0;
+      for (int i = j + 1 + lane; i < n; i += 32) ss = fma(X[i * ldx + j], X[i * ldx + j], ss);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) {
+        const double alpha = X[j * ldx + j];
+        const double sigma = sqrt(ss);
+        double beta, t;
+        if (sigma == 0.0) {
+          t = 0.0;
+          beta = alpha;
+        } else {
+          const double sgn = alpha < 0.0 ? -1.0 : 1.0;
+          beta = -sgn * hypot(alpha, sigma);
+          t = (beta - alpha) / beta;
+        }
+        s_scal[0] = beta;
+        s_scal[1] = t;
+        s_scal[2] = alpha - beta;
+        tau[j] = t;
+      }
+    }
+    __syncthreads();
+    const double t = s_scal[1];
+    if (t != 0.0) {
+      const double div = s_scal[2];
+      for (int i = j + 1 + tid; i < n; i += blockDim.x) X[i * ldx + j] = X[i * ldx + j] / div;
+    }
+    __syncthreads();
+    if (t != 0.0) {
+      // trailing columns: w_c = X[j][c] + sum_{i>j} v_i X[i][c]; X[i][c] -= tau v_i w_c
+      for (int c = j + 1 + warp; c < k; c += blockDim.x / 32) {
+        double w = 0.0;
+        for (int i = j + 1 + lane; i < n; i += 32) w = fma(X[i * ldx + j], X[i * ldx + c], w);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+        w += X[j * ldx + c];
+        const double tw = t * w;
+        __syncwarp();
+        if (lane == 0) X[j * ldx + c] -= tw;
+        for (int i = j + 1 + lane; i < n; i += 32) X[i * ldx + c] = fma(-tw, X[i * ldx + j], X[i * ldx + c]);
+      }
+    }
+    if (tid == 0) X[j * ldx + j] = s_scal[0];
+    __syncthreads();
+  }
+  // ---- R^ (k x k upper triangular)
+  if (k > 0) {
+    double *R = rh + sd.rh_off[cl];
+    for (int idx = tid; idx < k * k; idx += blockDim.x) {
+      const int i = idx / k, j = idx % k;
+      R[idx] = j >= i ? X[i * ldx + j] : 0.0;
+    }
+  }
+  // ---- Q = H_0 ... H_{k-1} I: thread per column, reflectors in reverse order
+  for (int c = tid; c < n; c += blockDim.x) {
+    for (int i = 0; i < n; i++) Q[i * ldq + c] = (i == c) ? 1.0 : 0.0;
+    for (int j = k - 1; j >= 0; j--) {
+      const double t = tau[j];
+      if (t == 0.0) continue;
+      double w = Q[j * ldq + c];
+      for (int i = j + 1; i < n; i++) w = fma(X[i * ldx + j], Q[i * ldq + c], w);
+      const double tw = t * w;
+      Q[j * ldq + c] -= tw;
+      for (int i = j + 1; i < n; i++) Q[i * ldq + c] = fma(-tw, X[i * ldx + j], Q[i * ldq + c]);
+    }
+  }
+  __syncthreads();
+  double *Qg = qout + sd.q_off[cl];
+  for (int idx = tid; idx < n * n; idx += blockDim.x) Qg[idx] = Q[(idx / n) * ldq + idx % n];
+}
+
+// --------------------------------------------------------------------------
+// Couplings in orthogonalised coordinates: D~ = R^R_t D R^C_s^T.
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) coupling_kernel(const CouplingItem *__restrict__ items, Side rs, Side cs,
+                                                       const double *__restrict__ rh_row,
+                                                       const double *__restrict__ rh_col,
+                                                       const double *__restrict__ D, double *__restrict__ dt) {
+  const CouplingItem it = items[blockIdx.x];
+  const int kt = rs.k[it.t], ks = cs.k[it.s];
+  extern __shared__ double sm[];
+  double *sD = sm;               // kt x ks
+  double *sT = sm + kt * ks;     // kt x ks: D R^_s^T
+  const double *Rt = rh_row + rs.rh_off[it.t];
+  const double *Rs = rh_col + cs.rh_off[it.s];
+  for (int idx = threadIdx.x; idx < kt * ks; idx += blockDim.x) sD[idx] = D[it.d_src + idx];
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < kt * ks; idx += blockDim.x) {
+    const int i = idx / ks, j = idx % ks;
+    double acc = 0.0;
+    for (int l = j; l < ks; l++) acc = fma(sD[i * ks + l], Rs[j * ks + l], acc);
+    sT[idx] = acc;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < kt * ks; idx += blockDim.x) {
+    const int i = idx / ks, j = idx % ks;
+    double acc = 0.0;
+    for (int l = i; l < kt; l++) acc = fma(Rt[i * kt + l], sT[l * ks + j], acc);
+    dt[it.dt_dst + idx] = acc;
+  }
+}
+
+// --------------------------------------------------------------------------
+// Steps (iv)+(ii)+(iii): one CTA per chunk of pairs (t, s_1..s_c) of one block
+// row t.  Q_t resident in shared memory; per pair: gather G (level 0: C_ts;
+// else the 2x2 children arrangement of bb parts / D~), T = Q_t^T G, H = T Q_s,
+// then scatter H's four parts (nn -> S, bb -> next level, bn / nb -> strips).
+// --------------------------------------------------------------------------
+template <int NP>
+struct PairCfg {
+  static constexpr int LD = NP + 4;                 // conflict-free DMMA fragment loads
+  static constexpr int WN = (NP == 64) ? 32 : 16;   // warp tile 16 x WN
+  static constexpr int TM = 2, TN = WN / 8;
+  static constexpr int NWM = NP / 16, NWN = NP / WN;
+  static constexpr int WARPS = NWM * NWN;
+  static constexpr int THREADS = WARPS * 32;
+  static constexpr size_t SMEM = size_t(3) * NP * LD * sizeof(double);
+};
+
+struct PairArgs {
+  const PairItem *items;
+  const Chunk *chunks;
+  Side rs, cs;
+  int L, level, B;
+  int sym;
+  const double *close;
+  const double *bb_in, *dt_in;        // level k-1 results
+  const double *q_row, *q_col;
+  double *s_val, *bb_out, *yr, *yc;   // yc: transposed column strips (general) / yr (symmetric)
+};
+
+template <int NP>
+__global__ void __launch_bounds__(PairCfg<NP>::THREADS) pair_kernel(PairArgs A) {
+  using C = PairCfg<NP>;
+  constexpr int LD = C::LD;
+  extern __shared__ __align__(16) double sm[];
+  double *sQt = sm;
+  double *sG = sm + NP * LD;
+  double *sQs = sm + 2 * NP * LD;
+  const Chunk ch = A.chunks[blockIdx.x];
+  const int t = A.items[ch.begin].t;
+  const int nt = A.rs.n[t], ktt = A.rs.k[t];
+  const int warp = threadIdx.x >> 5;
+  const int m0 = (warp / C::NWN) * 16, n0 = (warp % C::NWN) * C::WN;
+  load_tile<NP, NP, LD>(sQt, A.q_row + A.rs.q_off[t], nt, nt, nt);
+  const int64_t lbase = lvl_off_d(A.L, A.level);
+  for (int p = ch.begin; p < ch.end; p++) {
+    const PairItem it = A.items[p];
+    const int s = it.s;
+    const int ns = A.cs.n[s], kss = A.cs.k[s];
+    __syncthreads();  // previous pair's epilogue done with sG / sQs
+    if (A.level == 0) {
+      load_tile<NP, NP, LD>(sG, A.close + it.g_src[0], nt, ns, A.B);
+    } else {
+      const int64_t tc1 = lvl_off_d(A.L, A.level - 1) + 2 * (t - lbase);
+      const int64_t sc1 = lvl_off_d(A.L, A.level - 1) + 2 * (s - lbase);
+      const int kr0 = A.rs.k[tc1], kr1 = A.rs.k[tc1 + 1];
+      const int kc0 = A.cs.k[sc1], kc1 = A.cs.k[sc1 + 1];
+      for (int idx = threadIdx.x; idx < NP * NP; idx += blockDim.x) {
+        const int i = idx / NP, j = idx % NP;
+        double v = 0.0;
+        if (i < nt && j < ns) {
+          const int a = i >= kr0, b = j >= kc0;
+          const int ii = a ? i - kr0 : i, jj = b ? j - kc0 : j;
+          const int ka = a ? kr1 : kr0, kb = b ? kc1 : kc0;
+          const int q = a * 2 + b;
+          const int kind = (it.gkind >> (4 * q)) & 15;
+          const int64_t src = it.g_src[q];
+          switch (kind) {
+            case G_BB: v = A.bb_in[src + ii * kb + jj]; break;
+            case G_BB_T: v = A.bb_in[src + jj * ka + ii]; break;
+            case G_DT: v = A.dt_in[src + ii * kb + jj]; break;
+            case G_DT_T: v = A.dt_in[src + jj * ka + ii]; break;
+            default: v = 0.0;
+          }
+        }
+        sG[i * LD + j] = v;
+      }
+    }
+    load_tile<NP, NP, LD>(sQs, A.q_col + A.cs.q_off[s], ns, ns, ns);
+    __syncthreads();
+    double acc[C::TM][C::TN][2];
+    // T = Q_t^T G
+    zero_acc(acc);
+    warp_gemm<LD, C::TM, C::TN, true>(sQt, sG, m0, n0, NP, acc);
+    __syncthreads();
+    warp_store<LD>(sG, m0, n0, acc);
+    __syncthreads();
+    // H = T Q_s
+    zero_acc(acc);
+    warp_gemm<LD, C::TM, C::TN, false>(sG, sQs, m0, n0, NP, acc);
+    __syncthreads();
+    warp_store<LD>(sG, m0, n0, acc);
+    __syncthreads();
+    if (A.sym && s == t) {  // H_tt made exactly symmetric (upper -> lower)
+      for (int idx = threadIdx.x; idx < nt * nt; idx += blockDim.x) {
+        const int i = idx / nt, j = idx % nt;
+        if (i > j) sG[i * LD + j] = sG[j * LD + i];
+      }
+      __syncthreads();
+    }
+    // ---- step (iii): scatter
+    const int mt = nt - ktt, ms = ns - kss;
+    if (it.s_dst >= 0) {
+      for (int idx = threadIdx.x; idx < mt * ms; idx += blockDim.x) {
+        const int a = idx / ms, b = idx % ms;
+        A.s_val[it.s_dst + int64_t(a) * it.s_ld + b] = sG[(ktt + a) * LD + kss + b];
+      }
+    }
+    if (it.s_dst_m >= 0) {
+      for (int idx = threadIdx.x; idx < mt * ms; idx += blockDim.x) {
+        const int b = idx / mt, a = idx % mt;
+        A.s_val[it.s_dst_m + int64_t(b) * it.s_ld_m + a] = sG[(ktt + a) * LD + kss + b];
+      }
+    }
+    if (it.bb_dst >= 0) {
+      for (int idx = threadIdx.x; idx < ktt * kss; idx += blockDim.x) {
+        const int i = idx / kss, j = idx % kss;
+        A.bb_out[it.bb_dst + idx] = sG[i * LD + j];
+      }
+    }
+    if (it.yr_dst >= 0) {
+      for (int idx = threadIdx.x; idx < ktt * ms; idx += blockDim.x) {
+        const int i = idx / ms, b = idx % ms;
+        A.yr[it.yr_dst + idx] = sG[i * LD + kss + b];
+      }
+    }
+    if (it.yc_dst >= 0) {
+      for (int idx = threadIdx.x; idx < kss * mt; idx += blockDim.x) {
+        const int j = idx / mt, a = idx % mt;
+        A.yc[it.yc_dst + idx] = sG[(ktt + a) * LD + j];
+      }
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// Strips (Eq. u1v1): W = Q_q^T Z, Z = [Y_c1; Y_c2] (n_q x m), Q_q resident.
+// --------------------------------------------------------------------------
+template <int NP, int MP>
+struct StripCfg {
+  static constexpr int LDQ = NP + 4;
+  static constexpr int LDZ = MP + 4;
+  static constexpr int NWM = NP / 16, NWN = MP / 16;
+  static constexpr int WARPS = NWM * NWN;
+  static constexpr int THREADS = WARPS * 32;
+  static constexpr size_t SMEM = (size_t(NP) * LDQ + size_t(NP) * LDZ) * sizeof(double);
+};
+
+struct StripArgs {
+  const StripItem *items;
+  const Chunk *chunks;
+  Side sd;
+  int L, level;
+  const double *q;
+  const double *y_in;
+  double *y_out;
+  double *s_val;
+};
+
+template <int NP, int MP>
+__global__ void __launch_bounds__(StripCfg<NP, MP>::THREADS) strip_kernel(StripArgs A) {
+  using C = StripCfg<NP, MP>;
+  extern __shared__ __align__(16) double sm[];
+  double *sQ = sm;                 // NP x LDQ
+  double *sZ = sm + NP * C::LDQ;   // NP x LDZ (Z, then W)
+  const Chunk ch = A.chunks[blockIdx.x];
+  const int q = A.items[ch.begin].q;
+  const int n = A.sd.n[q], kq = A.sd.k[q];
+  const int64_t c1 = lvl_off_d(A.L, A.level - 1) + 2 * (q - lvl_off_d(A.L, A.level));
+  const int k1 = A.sd.k[c1], k2 = A.sd.k[c1 + 1];
+  const int warp = threadIdx.x >> 5;
+  const int m0 = (warp / C::NWN) * 16, n0 = (warp % C::NWN) * 16;
+  load_tile<NP, NP, C::LDQ>(sQ, A.q + A.sd.q_off[q], n, n, n);
+  for (int p = ch.begin; p < ch.end; p++) {
+    const StripItem it = A.items[p];
+    const int m = it.m;
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < NP * MP; idx += blockDim.x) {
+      const int i = idx / MP, b = idx % MP;
+      double v = 0.0;
+      if (b < m) {
+        if (i < k1) {
+          if (it.src[0] >= 0) v = A.y_in[it.src[0] + int64_t(i) * m + b];
+        } else if (i < k1 + k2) {
+          if (it.src[1] >= 0) v = A.y_in[it.src[1] + int64_t(i - k1) * m + b];
+        }
+      }
+      sZ[i * C::LDZ + b] = v;
+    }
+    __syncthreads();
+    // each warp: one 16 x 16 tile of W = 2 x 2 DMMA tiles
+    double acc2[2][2][2];
+    zero_acc(acc2);
+    {
+      const int lane = threadIdx.x & 31;
+      const int r = lane >> 2, qq = lane & 3;
+      for (int k0 = 0; k0 < NP; k0 += 4) {
+        double a[2], bq[2];
+#pragma unroll
+        for (int i = 0; i < 2; i++) a[i] = sQ[(k0 + qq) * C::LDQ + m0 + i * 8 + r];
+#pragma unroll
+        for (int j = 0; j < 2; j++) bq[j] = sZ[(k0 + qq) * C::LDZ + n0 + j * 8 + r];
+#pragma unroll
+        for (int i = 0; i < 2; i++)
+#pragma unroll
+          for (int j = 0; j < 2; j++) dmma(acc2[i][j], a[i], bq[j]);
+      }
+    }
+    __syncthreads();
+    warp_store<C::LDZ>(sZ, m0, n0, acc2);
+    __syncthreads();
+    const int mq = n - kq;
+    if (it.s_dst >= 0) {
+      for (int idx = threadIdx.x; idx < mq * m; idx += blockDim.x) {
+        const int a = idx / m, b = idx % m;
+        A.s_val[it.s_dst + int64_t(a) * it.s_ld + b] = sZ[(kq + a) * C::LDZ + b];
+      }
+    }
+    if (it.s_dst_t >= 0) {
+      for (int idx = threadIdx.x; idx < mq * m; idx += blockDim.x) {
+        const int b = idx / mq, a = idx % mq;
+        A.s_val[it.s_dst_t + int64_t(b) * it.s_ld_t + a] = sZ[(kq + a) * C::LDZ + b];
+      }
+    }
+    if (it.y_dst >= 0) {
+      for (int idx = threadIdx.x; idx < kq * m; idx += blockDim.x) {
+        const int i = idx / m, b = idx % m;
+        A.y_out[it.y_dst + idx] = sZ[i * C::LDZ + b];
+      }
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// CSR column indices: block row br has m_r rows with identical column pattern.
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) csr_cols_kernel(const CsrBlockRow *__restrict__ rows,
+                                                       const CsrBlock *__restrict__ blks, int32_t *__restrict__ col) {
+  const CsrBlockRow br = rows[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int a = warp; a < br.m_r; a += nw) {
+    int32_t *dst = col + br.p_base + int64_t(a) * br.rowlen;
+    for (int j = 0; j < br.nblk; j++) {
+      const CsrBlock b = blks[br.blk_begin + j];
+      for (int e = lane; e < b.m_c; e += 32) dst[b.colpos + e] = b.col0 + e;
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// Apply: y = U^T b (leaves -> root), x = V y (root -> leaves).  One CTA per
+// cluster; vectors column-major (ld) with nrhs columns; zb = basis-coefficient
+// buffer (column-major, ld = zb_len).
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, int level, const double *__restrict__ q,
+                                                       const double *__restrict__ b, int64_t ldb, double *__restrict__ y,
+                                                       int64_t ldy, double *__restrict__ zb, int64_t zbl, int nrhs, int B) {
+  const int64_t base = lvl_off_d(L, level);
+  const int64_t cl = base + blockIdx.x;
+  const int n = sd.n[cl], k = sd.k[cl];
+  if (n == 0) return;
+  __shared__ double sx[64];
+  const double *Q = q + sd.q_off[cl];
+  int64_t c1 = 0;
+  int k1 = 0;
+  if (level > 0) {
+    c1 = lvl_off_d(L, level - 1) + 2 * (cl - base);
+    k1 = sd.k[c1];
+  }
+  for (int r = 0; r < nrhs; r++) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      double v;
+      if (level == 0) v = b[(int64_t(blockIdx.x) * B + i) + r * ldb];
+      else if (i < k1) v = zb[sd.zb_off[c1] + i + r * zbl];
+      else v = zb[sd.zb_off[c1 + 1] + (i - k1) + r * zbl];
+      sx[i] = v;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      double acc = 0.0;
+      for (int i = 0; i < n; i++) acc = fma(Q[i * n + j], sx[i], acc);
+      if (j < k) zb[sd.zb_off[cl] + j + r * zbl] = acc;
+      else y[sd.s_off[cl] + (j - k) + r * ldy] = acc;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, int level, const double *__restrict__ q,
+                                                      const double *__restrict__ y, int64_t ldy, double *__restrict__ x,
+                                                      int64_t ldx, double *__restrict__ zb, int64_t zbl, int nrhs, int B) {
+  const int64_t base = lvl_off_d(L, level);
+  const int64_t cl = base + blockIdx.x;
+  const int n = sd.n[cl], k = sd.k[cl];
+  if (n == 0) return;
+  __shared__ double sQ[64 * 65];
+  __shared__ double sv[64];
+  const double *Q = q + sd.q_off[cl];
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) sQ[(idx / n) * 65 + idx % n] = Q[idx];
+  int64_t c1 = 0;
+  int k1 = 0;
+  if (level > 0) {
+    c1 = lvl_off_d(L, level - 1) + 2 * (cl - base);
+    k1 = sd.k[c1];
+  }
+  for (int r = 0; r < nrhs; r++) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < n; j += blockDim.x)
+      sv[j] = j < k ? zb[sd.zb_off[cl] + j + r * zbl] : y[sd.s_off[cl] + (j - k) + r * ldy];
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      double acc = 0.0;
+      for (int j = 0; j < n; j++) acc = fma(sQ[i * 65 + j], sv[j], acc);
+      if (level == 0) x[(int64_t(blockIdx.x) * B + i) + r * ldx] = acc;
+      else if (i < k1) zb[sd.zb_off[c1] + i + r * zbl] = acc;
+      else zb[sd.zb_off[c1 + 1] + (i - k1) + r * zbl] = acc;
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// Host orchestration
+// --------------------------------------------------------------------------
+#define H2SP_CK(x)                                                                                       \
+  do {                                                                                                   \
+    cudaError_t e_ = (x);                                                                                \
+    if (e_ != cudaSuccess) return fail(H2SP_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <int NP>
+static h2sp_status launch_pairs(const PairArgs &a, int64_t nchunks, cudaStream_t st) {
+  using C = PairCfg<NP>;
+  static bool attr = false;
+  if (!attr) {
+    H2SP_CK(cudaFuncSetAttribute(pair_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
+    attr = true;
+  }
+  pair_kernel<NP><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a);
+  H2SP_CK(cudaGetLastError());
+  return H2SP_OK;
+}
+
+template <int NP, int MP>
+static h2sp_status launch_strips2(const StripArgs &a, int64_t nchunks, cudaStream_t st) {
+  using C = StripCfg<NP, MP>;
+  static bool attr = false;
+  if (!attr) {
+    H2SP_CK(cudaFuncSetAttribute(strip_kernel<NP, MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
+    attr = true;
+  }
+  strip_kernel<NP, MP><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a);
+  H2SP_CK(cudaGetLastError());
+  return H2SP_OK;
+}
+
+static int pad16(int x) { return x <= 16 ? 16 : x <= 32 ? 32 : x <= 48 ? 48 : 64; }
+
+template <int NP>
+static h2sp_status launch_strips1(const StripArgs &a, int mp, int64_t nchunks, cudaStream_t st) {
+  switch (pad16(mp)) {
+    case 16: return launch_strips2<NP, 16>(a, nchunks, st);
+    case 32: return launch_strips2<NP, 32>(a, nchunks, st);
+    case 48: return launch_strips2<NP, 48>(a, nchunks, st);
+    default: return launch_strips2<NP, 64>(a, nchunks, st);
+  }
+}
+
+static h2sp_status launch_strips(const StripArgs &a, int np, int mp, int64_t nchunks, cudaStream_t st) {
+  switch (pad16(np)) {
+    case 16: return launch_strips1<16>(a, mp, nchunks, st);
+    case 32: return launch_strips1<32>(a, mp, nchunks, st);
+    case 48: return launch_strips1<48>(a, mp, nchunks, st);
+    default: return launch_strips1<64>(a, mp, nchunks, st);
+  }
+}
+
+h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp_outputs *out, unsigned char *ws,
+                         void *stream, int64_t *launches) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned char *meta = ws;
+  const Clusters cl = make_clusters(P, meta);
+  const Side rs = side_of(cl, false), cs = side_of(cl, true);
+  const bool sym = P->sym != 0;
+  double *rh_row = (double *)(ws + P->ws_rh_row);
+  double *rh_col = sym ? rh_row : (double *)(ws + P->ws_rh_col);
+  double *dt = (double *)(ws + P->ws_dt);
+  double *bb = (double *)(ws + P->ws_bb);
+  double *yr = (double *)(ws + P->ws_yr);
+  double *yc = sym ? yr : (double *)(ws + P->ws_yc);
+  const double *leaf_col = sym ? in->leaf_basis_row : in->leaf_basis_col;
+  const double *tr_col = sym ? in->transfer_row : in->transfer_col;
+  double *q_col = sym ? out->q_row : out->q_col;
+  const int L = P->L;
+  int64_t nl = 0;
+  static bool qr_attr = false;
+  if (!qr_attr) {
+    H2SP_CK(cudaFuncSetAttribute(qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+    H2SP_CK(cudaFuncSetAttribute(coupling_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * 64 * 8));
+    qr_attr = true;
+  }
+  for (int k = 0; k <= L; k++) {
+    const LevelPlan &lp = P->levels[k];
+    const unsigned M = unsigned(int64_t(1) << (L - k));
+    // ---- step (i)
+    if (lp.np_row > 0) {
+      const int n = lp.np_row;
+      size_t smem = size_t(n) * (n + 1) * 8 * 2 + size_t(n) * 8 + 64;
+      qr_kernel<<<M, 128, smem, st>>>(rs, L, k, in->leaf_basis_row, in->transfer_row, rh_row, out->q_row,
+                                      k == 0 ? (const uint64_t *)meta : nullptr, P->magic);
+      H2SP_CK(cudaGetLastError());
+      nl++;
+    }
+    if (!sym && lp.np_col > 0) {
+      const int n = lp.np_col;
+      size_t smem = size_t(n) * (n + 1) * 8 * 2 + size_t(n) * 8 + 64;
+      qr_kernel<<<M, 128, smem, st>>>(cs, L, k, leaf_col, tr_col, rh_col, q_col, nullptr, P->magic);
+      H2SP_CK(cudaGetLastError());
+      nl++;
+    }
+    // ---- couplings of level k
+    if (lp.n_coup) {
+      int kmax = 64;
+      coupling_kernel<<<unsigned(lp.n_coup), 128, size_t(2) * kmax * kmax * 8, st>>>(
+          (const CouplingItem *)(meta + lp.coup_off), rs, cs, rh_row, rh_col, in->coupling, dt);
+      H2SP_CK(cudaGetLastError());
+      nl++;
+    }
+    // ---- merge + congruence + freeze
+    if (lp.n_pairs) {
+      PairArgs a;
+      a.items = (const PairItem *)(meta + lp.pairs_off);
+      a.chunks = (const Chunk *)(meta + lp.pair_chunks_off);
+      a.rs = rs;
+      a.cs = cs;
+      a.L = L;
+      a.level = k;
+      a.B = P->B;
+      a.sym = P->sym;
+      a.close = in->close;
+      a.bb_in = bb;
+      a.dt_in = dt;
+      a.q_row = out->q_row;
+      a.q_col = q_col;
+      a.s_val = out->s_val;
+      a.bb_out = bb;
+      a.yr = yr;
+      a.yc = yc;
+      h2sp_status s;
+      switch (pad16(lp.np_pair)) {
+        case 16: s = launch_pairs<16>(a, lp.n_pair_chunks, st); break;
+        case 32: s = launch_pairs<32>(a, lp.n_pair_chunks, st); break;
+        case 48: s = launch_pairs<48>(a, lp.n_pair_chunks, st); break;
+        default: s = launch_pairs<64>(a, lp.n_pair_chunks, st); break;
+      }
+      if (s != H2SP_OK) return s;
+      nl++;
+    }
+    // ---- strips arriving from level k-1
+    if (lp.n_rstrips) {
+      StripArgs a;
+      a.items = (const StripItem *)(meta + lp.rstrips_off);
+      a.chunks = (const Chunk *)(meta + lp.rstrip_chunks_off);
+      a.sd = rs;
+      a.L = L;
+      a.level = k;
+      a.q = out->q_row;
+      a.y_in = yr;
+      a.y_out = yr;
+      a.s_val = out->s_val;
+      h2sp_status s = launch_strips(a, lp.np_rstrip, lp.mp, lp.n_rstrip_chunks, st);
+      if (s != H2SP_OK) return s;
+      nl++;
+    }
+    if (lp.n_cstrips) {
+      StripArgs a;
+      a.items = (const StripItem *)(meta + lp.cstrips_off);
+      a.chunks = (const Chunk *)(meta + lp.cstrip_chunks_off);
+      a.sd = cs;
+      a.L = L;
+      a.level = k;
+      a.q = q_col;
+      a.y_in = yc;
+      a.y_out = yc;
+      a.s_val = out->s_val;
+      h2sp_status s = launch_strips(a, lp.np_cstrip, lp.mp, lp.n_cstrip_chunks, st);
+      if (s != H2SP_OK) return s;
+      nl++;
+    }
+  }
+  if (out->s_rowptr)
+    H2SP_CK(cudaMemcpyAsync(out->s_rowptr, meta + P->rowptr_off, size_t(P->N + 1) * sizeof(int64_t),
+                            cudaMemcpyDeviceToDevice, st));
+  if (P->n_csr_rows) {
+    if (out->s_col) {
+      csr_cols_kernel<<<unsigned(P->n_csr_rows), 256, 0, st>>>((const CsrBlockRow *)(meta + P->csr_rows_off),
+                                                             (const CsrBlock *)(meta + P->csr_blocks_off), out->s_col);
+      H2SP_CK(cudaGetLastError());
+    }
+    nl++;
+  }
+  if (launches) *launches = nl;
+  return H2SP_OK;
+}
+
+h2sp_status launch_apply_Ut(const h2sp_plan_s *P, const double *q, const double *b, int64_t ldb, double *y,
+                            int64_t ldy, int nrhs, unsigned char *ws, void *stream, bool col_side) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const Clusters cl = make_clusters(P, ws);
+  const Side sd = side_of(cl, col_side);
+  double *zb = (double *)(ws + P->meta_bytes);
+  const int64_t zbl = col_side ? P->zb_col_len : P->zb_row_len;
+  for (int k = 0; k <= P->L; k++) {
+    const LevelPlan &lp = P->levels[k];
+    if ((col_side ? lp.np_col : lp.np_row) == 0) continue;
+    apply_ut_kernel<<<unsigned(int64_t(1) << (P->L - k)), 128, 0, st>>>(sd, P->L, k, q, b, ldb, y, ldy, zb, zbl,
+                                                                         nrhs, P->B);
+    H2SP_CK(cudaGetLastError());
+  }
+  return H2SP_OK;
+}
+
+h2sp_status launch_apply_V(const h2sp_plan_s *P, const double *q, const double *y, int64_t ldy, double *x,
+                           int64_t ldx, int nrhs, unsigned char *ws, void *stream, bool col_side) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const Clusters cl = make_clusters(P, ws);
+  const Side sd = side_of(cl, col_side);
+  double *zb = (double *)(ws + P->meta_bytes);
+  const int64_t zbl = col_side ? P->zb_col_len : P->zb_row_len;
+  for (int k = P->L; k >= 0; k--) {
+    const LevelPlan &lp = P->levels[k];
+    if ((col_side ? lp.np_col : lp.np_row) == 0) continue;
+    apply_v_kernel<<<unsigned(int64_t(1) << (P->L - k)), 128, 0, st>>>(sd, P->L, k, q, y, ldy, x, ldx, zb, zbl,
+                                                                        nrhs, P->B);
+    H2SP_CK(cudaGetLastError());
+  }
+  return H2SP_OK;
+}
+
+}  // namespace h2sp

@@ -1,0 +1,689 @@
+// Host symbolic phase ("plan"): validates the block cluster
+// tree, derives local sizes, the S order (the permutations P_rk / P_ck,
+// P:219-223), the block pattern of S, CSR row pointers
+// and every per-level device work list.  Integer work only, O(#blocks log).
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "h2sp_internal.h"
+
+namespace h2sp {
+static thread_local std::string g_err;
+void set_error(const std::string &m) { g_err = m; }
+h2sp_status fail(h2sp_status s, const std::string &m) {
+  g_err = m;
+  return s;
+}
+}  // namespace h2sp
+
+using namespace h2sp;
+
+namespace {
+
+struct PlanError : std::runtime_error {
+  h2sp_status code;
+  PlanError(h2sp_status c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+inline int64_t lvl_off(int L, int k) { return (int64_t(1) << (L + 1)) - (int64_t(1) << (L - k + 1)); }
+inline uint64_t pkey(int64_t t, int64_t s) { return (uint64_t(uint32_t(t)) << 32) | uint64_t(uint32_t(s)); }
+inline int32_t kt(uint64_t k) { return int32_t(k >> 32); }
+inline int32_t ks(uint64_t k) { return int32_t(k & 0xffffffffu); }
+
+int64_t find(const std::vector<uint64_t> &v, uint64_t key) {
+  auto it = std::lower_bound(v.begin(), v.end(), key);
+  if (it == v.end() || *it != key) return -1;
+  return int64_t(it - v.begin());
+}
+
+std::vector<uint64_t> read_csr(const int64_t *ptr, const int32_t *col, int64_t M, const char *what) {
+  std::vector<uint64_t> out;
+  if (M == 0) return out;
+  if (!ptr) throw PlanError(H2SP_EINVAL, std::string(what) + ": NULL row pointer");
+  if (ptr[0] != 0) throw PlanError(H2SP_ETREE, std::string(what) + ": ptr[0] != 0");
+  for (int64_t t = 0; t < M; t++) {
+    if (ptr[t + 1] < ptr[t]) throw PlanError(H2SP_ETREE, std::string(what) + ": decreasing row pointer");
+    for (int64_t j = ptr[t]; j < ptr[t + 1]; j++) {
+      int32_t s = col[j];
+      if (s < 0 || s >= M) throw PlanError(H2SP_ETREE, std::string(what) + ": column out of range");
+      if (j > ptr[t] && col[j - 1] >= s) throw PlanError(H2SP_ETREE, std::string(what) + ": columns not strictly ascending");
+      out.push_back(pkey(t, s));
+    }
+  }
+  return out;
+}
+
+struct StripRec {  // a live strip at some level: rotating cluster c (in-level), fixed group (l, s)
+  int32_t c, l, s;
+  int64_t slot;
+};
+
+struct BlockRec {
+  int64_t roff, coff;
+  int32_t mr, mc;
+  int32_t kind;  // 0 pair direct, 1 pair mirror, 2 rstrip direct, 3 rstrip transposed, 4 cstrip transposed
+  int32_t level;
+  int64_t idx;   // item index within its level list
+};
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct MetaBuilder {
+  std::vector<unsigned char> buf;
+  template <class T>
+  size_t put(const std::vector<T> &v) {
+    size_t off = align_up(buf.size(), 256);
+    buf.resize(off + v.size() * sizeof(T));
+    if (!v.empty()) std::memcpy(buf.data() + off, v.data(), v.size() * sizeof(T));
+    return off;
+  }
+};
+
+int round8(int x) { return (x + 7) / 8 * 8; }
+
+}  // namespace
+
+extern "C" {
+
+const char *h2sp_status_str(h2sp_status s) {
+  switch (s) {
+    case H2SP_OK: return "ok";
+    case H2SP_EINVAL: return "invalid argument";
+    case H2SP_ETREE: return "invalid block cluster tree";
+    case H2SP_ERANK: return "invalid rank distribution";
+    case H2SP_ENOMEM: return "out of host memory";
+    case H2SP_ECUDA: return "CUDA error";
+    case H2SP_ENCCL: return "NCCL error";
+    case H2SP_EUNSUPPORTED: return "unsupported shape";
+  }
+  return "unknown status";
+}
+
+const char *h2sp_last_error(void) { return g_err.c_str(); }
+
+void h2sp_plan_destroy(h2sp_plan p) { delete p; }
+
+h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out) {
+  (void)flags;
+  if (!st || !out) return fail(H2SP_EINVAL, "NULL structure or output pointer");
+  *out = nullptr;
+  h2sp_plan_s *P = nullptr;
+  try {
+    const int L = st->L, B = st->leaf_size;
+    if (L < 0 || L > 24) throw PlanError(H2SP_EINVAL, "L out of range [0, 24]");
+    if (B < 1) throw PlanError(H2SP_EINVAL, "leaf_size < 1");
+    if (!st->rank_row) throw PlanError(H2SP_EINVAL, "rank_row is NULL");
+    if (!st->symmetric && !st->rank_col) throw PlanError(H2SP_EINVAL, "rank_col is NULL in general mode");
+    P = new h2sp_plan_s();
+    P->L = L;
+    P->B = B;
+    P->sym = st->symmetric ? 1 : 0;
+    P->N = int64_t(B) << L;
+    const int64_t ncl = (int64_t(1) << (L + 1)) - 1;
+    const int64_t nleaf = int64_t(1) << L;
+    P->ncl = ncl;
+    auto &nr = P->n_row, &kr = P->k_row, &nc = P->n_col, &kc = P->k_col;
+    kr.assign(st->rank_row, st->rank_row + ncl);
+    if (P->sym) {
+      if (st->rank_col)
+        for (int64_t c = 0; c < ncl; c++)
+          if (st->rank_col[c] != st->rank_row[c]) throw PlanError(H2SP_ERANK, "symmetric mode needs rank_col == rank_row");
+      kc = kr;
+    } else {
+      kc.assign(st->rank_col, st->rank_col + ncl);
+    }
+    auto local = [&](const std::vector<int32_t> &k, std::vector<int32_t> &n, const char *side) {
+      n.assign(ncl, 0);
+      for (int64_t i = 0; i < nleaf; i++) n[i] = B;
+      for (int k_ = 1; k_ <= L; k_++)
+        for (int64_t i = 0; i < (int64_t(1) << (L - k_)); i++)
+          n[lvl_off(L, k_) + i] = k[lvl_off(L, k_ - 1) + 2 * i] + k[lvl_off(L, k_ - 1) + 2 * i + 1];
+      for (int64_t c = 0; c < ncl; c++)
+        if (k[c] < 0 || k[c] > n[c])
+          throw PlanError(H2SP_ERANK, std::string(side) + " rank outside [0, n_t] at cluster " + std::to_string(c));
+      if (k[ncl - 1] != 0) throw PlanError(H2SP_ERANK, std::string(side) + " root rank must be 0");
+    };
+    local(kr, nr, "row");
+    local(kc, nc, "column");
+    for (int64_t c = 0; c < ncl; c++)
+      if (nr[c] > 64 || nc[c] > 64)
+        throw PlanError(H2SP_EUNSUPPORTED, "local size n_t > 64 (kernels are built for B, 2r <= 64)");
+
+    // ---------------------------------------------------------------- block tree
+    std::vector<std::vector<uint64_t>> near(L + 1), adm(L + 1);
+    if (!st->near_col && st->near_ptr && st->near_ptr[nleaf] > 0) throw PlanError(H2SP_EINVAL, "near_col is NULL");
+    near[0] = read_csr(st->near_ptr, st->near_col, nleaf, "near");
+    std::vector<int64_t> adm_in_off(L + 1, 0);  // CSR order index base per level (coupling offsets)
+    for (int k = 0; k < L; k++) {
+      if (!st->adm_ptr || !st->adm_col) throw PlanError(H2SP_EINVAL, "adm_ptr/adm_col is NULL");
+      adm[k] = read_csr(st->adm_ptr[k], st->adm_col[k], int64_t(1) << (L - k), "adm");
+    }
+    if (P->sym) {
+      auto check_sym = [&](const std::vector<uint64_t> &v, const char *w) {
+        for (uint64_t x : v)
+          if (find(v, pkey(ks(x), kt(x))) < 0) throw PlanError(H2SP_ETREE, std::string(w) + " list not symmetric");
+      };
+      check_sym(near[0], "near");
+      for (int k = 0; k < L; k++) check_sym(adm[k], "adm");
+    }
+    for (int k = 1; k <= L; k++) {
+      std::vector<uint64_t> par;
+      par.reserve(near[k - 1].size() / 2 + adm[k - 1].size() / 2 + 1);
+      for (uint64_t x : near[k - 1]) par.push_back(pkey(kt(x) / 2, ks(x) / 2));
+      for (uint64_t x : adm[k - 1]) par.push_back(pkey(kt(x) / 2, ks(x) / 2));
+      std::sort(par.begin(), par.end());
+      par.erase(std::unique(par.begin(), par.end()), par.end());
+      near[k] = std::move(par);
+      for (uint64_t x : near[k]) {
+        if (k < L && find(adm[k], x) >= 0) throw PlanError(H2SP_ETREE, "pair is both near and admissible");
+        for (int a = 0; a < 2; a++)
+          for (int b = 0; b < 2; b++) {
+            uint64_t ch = pkey(2 * kt(x) + a, 2 * ks(x) + b);
+            bool inn = find(near[k - 1], ch) >= 0, ina = find(adm[k - 1], ch) >= 0;
+            if (inn == ina) throw PlanError(H2SP_ETREE, "children of a close block are not partitioned by N u A at level " + std::to_string(k - 1));
+          }
+      }
+    }
+    if (L == 0) {
+      if (near[0].size() != 1) throw PlanError(H2SP_ETREE, "L = 0 needs the single near pair (0, 0)");
+    } else if (near[L].size() != 1 || near[L][0] != pkey(0, 0)) {
+      throw PlanError(H2SP_ETREE, "block tree does not cover the matrix (N_L != {(root, root)})");
+    }
+
+    // ---------------------------------------------------------------- offsets
+    auto mr = [&](int64_t c) { return nr[c] - kr[c]; };
+    auto mc = [&](int64_t c) { return nc[c] - kc[c]; };
+    P->s_off_row.assign(ncl, 0);
+    P->s_off_col.assign(ncl, 0);
+    {
+      int64_t a = 0, b = 0;
+      for (int64_t c = 0; c < ncl; c++) {  // level-major order == S order
+        P->s_off_row[c] = a;
+        a += mr(c);
+        P->s_off_col[c] = b;
+        b += mc(c);
+      }
+      if (a != P->N || b != P->N) throw PlanError(H2SP_ERANK, "sum of frozen sizes != N");
+    }
+    std::vector<int64_t> rh_off_row(ncl), rh_off_col(ncl), tr_off_row(ncl, 0), tr_off_col(ncl, 0), zb_row(ncl),
+        zb_col(ncl);
+    std::vector<int64_t> leaf_off_row(nleaf), leaf_off_col(nleaf);
+    P->q_off_row.assign(ncl, 0);
+    P->q_off_col.assign(ncl, 0);
+    {
+      int64_t q1 = 0, q2 = 0, r1 = 0, r2 = 0, t1 = 0, t2 = 0, z1 = 0, z2 = 0, l1 = 0, l2 = 0;
+      for (int64_t c = 0; c < ncl; c++) {
+        P->q_off_row[c] = q1;
+        q1 += int64_t(nr[c]) * nr[c];
+        P->q_off_col[c] = q2;
+        q2 += int64_t(nc[c]) * nc[c];
+        rh_off_row[c] = r1;
+        r1 += int64_t(kr[c]) * kr[c];
+        rh_off_col[c] = r2;
+        r2 += int64_t(kc[c]) * kc[c];
+        zb_row[c] = z1;
+        z1 += kr[c];
+        zb_col[c] = z2;
+        z2 += kc[c];
+        if (c >= nleaf) {
+          tr_off_row[c] = t1;
+          t1 += int64_t(nr[c]) * kr[c];
+          tr_off_col[c] = t2;
+          t2 += int64_t(nc[c]) * kc[c];
+        } else {
+          leaf_off_row[c] = l1;
+          l1 += int64_t(B) * kr[c];
+          leaf_off_col[c] = l2;
+          l2 += int64_t(B) * kc[c];
+        }
+      }
+      P->q_row_len = q1;
+      P->q_col_len = P->sym ? 0 : q2;
+      P->rh_row_len = r1;
+      P->rh_col_len = P->sym ? 0 : r2;
+      P->tr_row_len = t1;
+      P->tr_col_len = P->sym ? 0 : t2;
+      P->leaf_row_len = l1;
+      P->leaf_col_len = P->sym ? 0 : l2;
+      P->zb_row_len = z1;
+      P->zb_col_len = z2;
+    }
+    P->close_len = int64_t(near[0].size()) * B * B;
+    std::vector<std::vector<int64_t>> coup_in(L + 1);  // input offset of D per adm pair
+    {
+      int64_t o = 0;
+      for (int k = 0; k < L; k++) {
+        coup_in[k].resize(adm[k].size());
+        for (size_t j = 0; j < adm[k].size(); j++) {
+          coup_in[k][j] = o;
+          o += int64_t(kr[lvl_off(L, k) + kt(adm[k][j])]) * kc[lvl_off(L, k) + ks(adm[k][j])];
+        }
+      }
+      P->coupling_len = o;
+    }
+
+    // ---------------------------------------------------------------- work lists
+    const bool sym = P->sym;
+    double flops_qr = 0, flops_coup = 0, flops_cong = 0, flops_strip = 0;
+    int64_t dt_len = 0, bb_len = 0, yr_len = 0, yc_len = 0;
+    std::vector<std::vector<PairItem>> pairs(L + 1);
+    std::vector<std::vector<StripItem>> rstr(L + 1), cstr(L + 1);
+    std::vector<std::vector<CouplingItem>> coup(L + 1);
+    std::vector<std::vector<int64_t>> dt_slot(L + 1), bb_slot(L + 1);
+    std::vector<std::vector<int64_t>> pair_index(L + 1);   // near index -> item index (canonical) or -1
+    std::vector<BlockRec> blocks;
+    std::vector<StripRec> R_prev, C_prev;
+    for (int k = 0; k <= L; k++) {
+      const int64_t base = lvl_off(L, k);
+      const int64_t M = int64_t(1) << (L - k);
+      // QR flops (approximate Householder count)
+      for (int64_t i = 0; i < M; i++) {
+        double n = nr[base + i], kk = kr[base + i];
+        flops_qr += 2 * n * kk * kk + 4 * n * n * kk;
+        if (!sym) {
+          n = nc[base + i];
+          kk = kc[base + i];
+          flops_qr += 2 * n * kk * kk + 4 * n * n * kk;
+        }
+      }
+      // couplings
+      if (k < L) {
+        dt_slot[k].assign(adm[k].size(), -1);
+        for (size_t j = 0; j < adm[k].size(); j++) {
+          int32_t t = kt(adm[k][j]), s = ks(adm[k][j]);
+          if (sym && t > s) continue;
+          int64_t ct = base + t, cs = base + s;
+          int64_t sz = int64_t(kr[ct]) * kc[cs];
+          if (sz == 0) continue;
+          dt_slot[k][j] = dt_len;
+          coup[k].push_back(CouplingItem{int32_t(ct), int32_t(cs), coup_in[k][j], dt_len});
+          dt_len += sz;
+          flops_coup += 2.0 * kr[ct] * kc[cs] * (kr[ct] + kc[cs]);
+        }
+      }
+      // near pairs: items for canonical pairs
+      const auto &Nk = near[k];
+      pair_index[k].assign(Nk.size(), -1);
+      bb_slot[k].assign(Nk.size(), -1);
+      for (size_t j = 0; j < Nk.size(); j++) {
+        int32_t t = kt(Nk[j]), s = ks(Nk[j]);
+        if (sym && t > s) continue;
+        int64_t ct = base + t, cs = base + s;
+        if (nr[ct] == 0 || nc[cs] == 0) continue;  // empty block: nothing to compute
+        PairItem it{};
+        it.t = int32_t(ct);
+        it.s = int32_t(cs);
+        it.s_dst = it.s_dst_m = it.bb_dst = it.yr_dst = it.yc_dst = -1;
+        for (int q = 0; q < 4; q++) it.g_src[q] = -1;
+        if (k == 0) {
+          it.g_src[0] = int64_t(j) * B * B;
+        } else {
+          int32_t gk = 0;
+          for (int a = 0; a < 2; a++)
+            for (int b = 0; b < 2; b++) {
+              int32_t ca = 2 * t + a, db = 2 * s + b;
+              int64_t kca = kr[lvl_off(L, k - 1) + ca], kdb = kc[lvl_off(L, k - 1) + db];
+              int kind = G_EMPTY;
+              int64_t src = -1;
+              if (kca > 0 && kdb > 0) {
+                bool tr = sym && ca > db;
+                uint64_t key = tr ? pkey(db, ca) : pkey(ca, db);
+                int64_t jn = find(near[k - 1], key);
+                if (jn >= 0) {
+                  kind = tr ? G_BB_T : G_BB;
+                  src = bb_slot[k - 1][jn];
+                } else {
+                  int64_t ja = find(adm[k - 1], key);
+                  if (ja < 0) throw PlanError(H2SP_ETREE, "internal: child pair neither near nor admissible");
+                  kind = tr ? G_DT_T : G_DT;
+                  src = dt_slot[k - 1][ja];
+                }
+                if (src < 0) throw PlanError(H2SP_ETREE, "internal: missing child block slot");
+              }
+              gk |= kind << (4 * (a * 2 + b));
+              it.g_src[a * 2 + b] = src;
+            }
+          it.gkind = gk;
+        }
+        if (k < L && kr[ct] > 0 && kc[cs] > 0) {
+          bb_slot[k][j] = bb_len;
+          it.bb_dst = bb_len;
+          bb_len += int64_t(kr[ct]) * kc[cs];
+        }
+        pair_index[k][j] = int64_t(pairs[k].size());
+        pairs[k].push_back(it);
+        flops_cong += 2.0 * nr[ct] * nc[cs] * (nr[ct] + nc[cs]);
+      }
+      // strips started at this level (from every pair of N_k) and S blocks of pairs
+      std::vector<StripRec> R_cur, C_cur;
+      for (size_t j = 0; j < Nk.size(); j++) {
+        int32_t t = kt(Nk[j]), s = ks(Nk[j]);
+        int64_t ct = base + t, cs = base + s;
+        bool canon = !sym || t <= s;
+        int64_t item = canon ? pair_index[k][j] : pair_index[k][find(Nk, pkey(s, t))];
+        if (kr[ct] > 0 && mc(cs) > 0) {
+          int64_t slot = yr_len;
+          yr_len += int64_t(kr[ct]) * mc(cs);
+          R_cur.push_back(StripRec{t, k, s, slot});
+          if (canon) pairs[k][item].yr_dst = slot;
+          else pairs[k][item].yc_dst = slot;  // H_ts = H_st^T: row strip of (t,s) = (nb part of H_st)^T
+        }
+        if (!sym && mr(ct) > 0 && kc[cs] > 0) {
+          int64_t slot = yc_len;
+          yc_len += int64_t(kc[cs]) * mr(ct);
+          C_cur.push_back(StripRec{s, k, t, slot});  // transposed column strip: rotating cluster s
+          pairs[k][item].yc_dst = slot;
+        }
+        if (canon && mr(ct) > 0 && mc(cs) > 0) {
+          blocks.push_back(BlockRec{P->s_off_row[ct], P->s_off_col[cs], mr(ct), mc(cs), 0, k, item});
+          if (sym && t != s)
+            blocks.push_back(BlockRec{P->s_off_row[cs], P->s_off_col[ct], mc(cs), mr(ct), 1, k, item});
+        }
+      }
+      // strips arriving from level k-1 (Eq. u1v1)
+      auto merge = [&](std::vector<StripRec> &prev, bool row_side, std::vector<StripItem> &items,
+                       std::vector<StripRec> &cur, int64_t &ylen) {
+        std::sort(prev.begin(), prev.end(), [](const StripRec &a, const StripRec &b) {
+          if (a.c / 2 != b.c / 2) return a.c / 2 < b.c / 2;
+          if (a.l != b.l) return a.l < b.l;
+          if (a.s != b.s) return a.s < b.s;
+          return a.c < b.c;
+        });
+        const auto &kq = row_side ? kr : kc;
+        const auto &nq = row_side ? nr : nc;
+        for (size_t j = 0; j < prev.size();) {
+          size_t e = j + 1;
+          while (e < prev.size() && prev[e].c / 2 == prev[j].c / 2 && prev[e].l == prev[j].l && prev[e].s == prev[j].s)
+            e++;
+          int32_t p = prev[j].c / 2, l = prev[j].l, s = prev[j].s;
+          int64_t cq = base + p, cf = lvl_off(L, l) + s;  // rotating / fixed cluster
+          int32_t m = row_side ? mc(cf) : mr(cf);
+          StripItem it{};
+          it.q = int32_t(cq);
+          it.m = m;
+          it.src[0] = it.src[1] = -1;
+          it.s_dst = it.s_dst_t = it.y_dst = -1;
+          double rows_present = 0;
+          for (size_t x = j; x < e; x++) {
+            it.src[prev[x].c % 2] = prev[x].slot;
+            rows_present += kq[lvl_off(L, k - 1) + prev[x].c];
+          }
+          int64_t idx = int64_t(items.size());
+          int32_t mq = nq[cq] - kq[cq];
+          if (mq > 0) {
+            if (row_side) {
+              blocks.push_back(BlockRec{P->s_off_row[cq], P->s_off_col[cf], mq, m, 2, k, idx});
+              if (sym) blocks.push_back(BlockRec{P->s_off_row[cf], P->s_off_col[cq], m, mq, 3, k, idx});
+            } else {
+              blocks.push_back(BlockRec{P->s_off_row[cf], P->s_off_col[cq], m, mq, 4, k, idx});
+            }
+          }
+          if (kq[cq] > 0) {
+            it.y_dst = ylen;
+            cur.push_back(StripRec{p, l, s, ylen});
+            ylen += int64_t(kq[cq]) * m;
+          }
+          flops_strip += 2.0 * nq[cq] * rows_present * m;
+          items.push_back(it);
+          j = e;
+        }
+      };
+      if (k > 0) {
+        merge(R_prev, true, rstr[k], R_cur, yr_len);
+        if (!sym) merge(C_prev, false, cstr[k], C_cur, yc_len);
+      }
+      R_prev.swap(R_cur);
+      C_prev.swap(C_cur);
+    }
+
+    // ---------------------------------------------------------------- S pattern, CSR
+    std::sort(blocks.begin(), blocks.end(), [](const BlockRec &a, const BlockRec &b) {
+      return a.roff != b.roff ? a.roff < b.roff : a.coff < b.coff;
+    });
+    for (size_t j = 1; j < blocks.size(); j++)
+      if (blocks[j].roff == blocks[j - 1].roff && blocks[j].coff == blocks[j - 1].coff)
+        throw PlanError(H2SP_ETREE, "internal: S block produced twice");
+    std::vector<CsrBlockRow> csr_rows;
+    std::vector<CsrBlock> csr_blocks;
+    std::vector<int64_t> rowptr(P->N + 1, 0);
+    int64_t nnz = 0;
+    {
+      size_t j = 0;
+      int64_t row = 0;  // next S row without a pointer
+      while (j < blocks.size()) {
+        size_t e = j;
+        int64_t rowlen = 0;
+        while (e < blocks.size() && blocks[e].roff == blocks[j].roff) rowlen += blocks[e++].mc;
+        if (rowlen > INT32_MAX) throw PlanError(H2SP_EUNSUPPORTED, "S row longer than 2^31");
+        const int64_t r0 = blocks[j].roff, m_r = blocks[j].mr;
+        for (; row < r0; row++) rowptr[row] = nnz;  // empty rows
+        CsrBlockRow br{r0, nnz, int32_t(m_r), int32_t(rowlen), int32_t(csr_blocks.size()), int32_t(e - j)};
+        csr_rows.push_back(br);
+        int64_t colpos = 0;
+        for (size_t x = j; x < e; x++) {
+          const BlockRec &b = blocks[x];
+          if (b.mr != m_r) throw PlanError(H2SP_ETREE, "internal: inconsistent block row height");
+          csr_blocks.push_back(CsrBlock{int32_t(b.coff), b.mc, int32_t(colpos), 0});
+          int64_t dst = nnz + colpos;
+          switch (b.kind) {
+            case 0: pairs[b.level][b.idx].s_dst = dst; pairs[b.level][b.idx].s_ld = int32_t(rowlen); break;
+            case 1: pairs[b.level][b.idx].s_dst_m = dst; pairs[b.level][b.idx].s_ld_m = int32_t(rowlen); break;
+            case 2: rstr[b.level][b.idx].s_dst = dst; rstr[b.level][b.idx].s_ld = int32_t(rowlen); break;
+            case 3: rstr[b.level][b.idx].s_dst_t = dst; rstr[b.level][b.idx].s_ld_t = int32_t(rowlen); break;
+            case 4: cstr[b.level][b.idx].s_dst_t = dst; cstr[b.level][b.idx].s_ld_t = int32_t(rowlen); break;
+          }
+          colpos += b.mc;
+        }
+        for (int64_t a = 0; a < m_r; a++) rowptr[r0 + a] = nnz + a * rowlen;
+        row = r0 + m_r;
+        nnz += m_r * rowlen;
+        j = e;
+      }
+      for (; row <= P->N; row++) rowptr[row] = nnz;
+    }
+    P->s_nnz = nnz;
+    P->s_blocks = int64_t(blocks.size());
+
+    // ---------------------------------------------------------------- meta image
+    MetaBuilder mb;
+    mb.buf.resize(256, 0);
+    P->magic = 0x4832535050000000ull ^ (uint64_t(P->N) << 8) ^ uint64_t(nnz & 0xffffff) ^ (uint64_t(blocks.size()) << 40);
+    std::memcpy(mb.buf.data(), &P->magic, 8);
+    P->ca.n_row = mb.put(nr);
+    P->ca.k_row = mb.put(kr);
+    P->ca.n_col = mb.put(sym ? nr : nc);
+    P->ca.k_col = mb.put(sym ? kr : kc);
+    P->ca.q_off_row = mb.put(P->q_off_row);
+    P->ca.q_off_col = mb.put(sym ? P->q_off_row : P->q_off_col);
+    P->ca.rh_off_row = mb.put(rh_off_row);
+    P->ca.rh_off_col = mb.put(sym ? rh_off_row : rh_off_col);
+    P->ca.leaf_off_row = mb.put(leaf_off_row);
+    P->ca.leaf_off_col = mb.put(sym ? leaf_off_row : leaf_off_col);
+    P->ca.tr_off_row = mb.put(tr_off_row);
+    P->ca.tr_off_col = mb.put(sym ? tr_off_row : tr_off_col);
+    P->ca.s_off_row = mb.put(P->s_off_row);
+    P->ca.s_off_col = mb.put(P->s_off_col);
+    P->ca.zb_off_row = mb.put(zb_row);
+    P->ca.zb_off_col = mb.put(zb_col);
+    P->levels.resize(L + 1);
+    int levels_active = 0;
+    int64_t launches = 0;
+    const int CH = 8;  // items per CTA chunk sharing one rotating cluster
+    auto chunk = [&](const auto &items, auto qof) {
+      std::vector<Chunk> ch;
+      size_t j = 0;
+      while (j < items.size()) {
+        size_t e = j + 1;
+        while (e < items.size() && qof(items[e]) == qof(items[j]) && int(e - j) < CH) e++;
+        ch.push_back(Chunk{int32_t(j), int32_t(e)});
+        j = e;
+      }
+      return ch;
+    };
+    for (int k = 0; k <= L; k++) {
+      LevelPlan &lp = P->levels[k];
+      lp = LevelPlan{};
+      lp.k = k;
+      const int64_t base = lvl_off(L, k), M = int64_t(1) << (L - k);
+      int npr = 0, npc = 0;
+      for (int64_t i = 0; i < M; i++) {
+        npr = std::max(npr, int(nr[base + i]));
+        npc = std::max(npc, int(nc[base + i]));
+      }
+      lp.np_row = npr;
+      lp.np_col = npc;
+      if (npr > 0 || npc > 0) levels_active++;
+      int mp = 0;
+      for (auto &s : rstr[k]) mp = std::max(mp, int(s.m));
+      for (auto &s : cstr[k]) mp = std::max(mp, int(s.m));
+      lp.mp = mp;
+      lp.np_pair = round8(std::max(npr, npc));
+      lp.np_rstrip = round8(npr);
+      lp.np_cstrip = round8(npc);
+      lp.n_pairs = int64_t(pairs[k].size());
+      lp.pairs_off = mb.put(pairs[k]);
+      auto pc = chunk(pairs[k], [](const PairItem &x) { return x.t; });
+      lp.n_pair_chunks = int64_t(pc.size());
+      lp.pair_chunks_off = mb.put(pc);
+      lp.n_rstrips = int64_t(rstr[k].size());
+      lp.rstrips_off = mb.put(rstr[k]);
+      auto rc = chunk(rstr[k], [](const StripItem &x) { return x.q; });
+      lp.n_rstrip_chunks = int64_t(rc.size());
+      lp.rstrip_chunks_off = mb.put(rc);
+      lp.n_cstrips = int64_t(cstr[k].size());
+      lp.cstrips_off = mb.put(cstr[k]);
+      auto cc = chunk(cstr[k], [](const StripItem &x) { return x.q; });
+      lp.n_cstrip_chunks = int64_t(cc.size());
+      lp.cstrip_chunks_off = mb.put(cc);
+      lp.n_coup = int64_t(coup[k].size());
+      lp.coup_off = mb.put(coup[k]);
+      // launches issued by launch_build (kept in sync with kernels.cu)
+      if (npr > 0) launches++;
+      if (!sym && npc > 0) launches++;
+      if (lp.n_coup) launches++;
+      if (lp.n_pairs) launches++;
+      if (lp.n_rstrips) launches++;
+      if (lp.n_cstrips) launches++;
+    }
+    P->n_csr_rows = int64_t(csr_rows.size());
+    P->n_csr_blocks = int64_t(csr_blocks.size());
+    P->csr_rows_off = mb.put(csr_rows);
+    P->csr_blocks_off = mb.put(csr_blocks);
+    P->rowptr_off = mb.put(rowptr);
+    if (P->n_csr_rows) launches++;  // CSR column expansion (rowptr is a D2D copy)
+    P->launches = launches;
+    P->levels_active = levels_active;
+    P->meta_bytes = align_up(mb.buf.size(), 256);
+    mb.buf.resize(P->meta_bytes, 0);
+    P->meta.swap(mb.buf);
+    // workspace layout
+    size_t o = P->meta_bytes;
+    auto carve = [&](int64_t n_doubles) {
+      size_t r = o;
+      o = align_up(o + size_t(n_doubles) * 8, 256);
+      return r;
+    };
+    P->dt_len = dt_len;
+    P->bb_len = bb_len;
+    P->yr_len = yr_len;
+    P->yc_len = yc_len;
+    P->ws_rh_row = carve(P->rh_row_len);
+    P->ws_rh_col = carve(P->rh_col_len);
+    P->ws_dt = carve(dt_len);
+    P->ws_bb = carve(bb_len);
+    P->ws_yr = carve(yr_len);
+    P->ws_yc = carve(yc_len);
+    P->ws_total = o;
+    // algorithmic work
+    double close_read = 0;
+    for (uint64_t x : near[0])
+      if (!sym || kt(x) <= ks(x)) close_read += double(B) * B;
+    double coup_read = 0;
+    for (int k = 0; k < L; k++)
+      for (size_t j = 0; j < adm[k].size(); j++)
+        if (!sym || kt(adm[k][j]) <= ks(adm[k][j]))
+          coup_read += double(kr[lvl_off(L, k) + kt(adm[k][j])]) * kc[lvl_off(L, k) + ks(adm[k][j])];
+    double in_bytes = 8.0 * (close_read + coup_read + P->leaf_row_len + P->leaf_col_len + P->tr_row_len + P->tr_col_len);
+    double out_bytes = 8.0 * (P->q_row_len + P->q_col_len) + 12.0 * double(nnz) + 8.0 * double(P->N + 1);
+    double mid_bytes = 2.0 * 8.0 * double(P->rh_row_len + P->rh_col_len + dt_len + bb_len + yr_len + yc_len);
+    P->flops = flops_qr + flops_coup + flops_cong + flops_strip;
+    P->flops_cong = flops_cong;
+    P->flops_strip = flops_strip;
+    P->bytes = in_bytes + out_bytes + mid_bytes;
+    *out = P;
+    return H2SP_OK;
+  } catch (const PlanError &e) {
+    delete P;
+    return fail(e.code, e.what());
+  } catch (const std::bad_alloc &) {
+    delete P;
+    return fail(H2SP_ENOMEM, "host allocation failed in plan_create");
+  } catch (const std::exception &e) {
+    delete P;
+    return fail(H2SP_EINVAL, e.what());
+  }
+}
+
+h2sp_status h2sp_plan_sizes(h2sp_plan P, h2sp_sizes *o) {
+  if (!P || !o) return fail(H2SP_EINVAL, "NULL plan or output");
+  std::memset(o, 0, sizeof(*o));
+  o->n = P->N;
+  o->n_clusters = P->ncl;
+  o->leaf_row = P->leaf_row_len;
+  o->transfer_row = P->tr_row_len;
+  o->leaf_col = P->leaf_col_len;
+  o->transfer_col = P->tr_col_len;
+  o->close = P->close_len;
+  o->coupling = P->coupling_len;
+  o->q_row = P->q_row_len;
+  o->q_col = P->q_col_len;
+  o->s_nnz = P->s_nnz;
+  o->s_blocks = P->s_blocks;
+  o->workspace_bytes = int64_t(P->ws_total);
+  o->meta_bytes = int64_t(P->meta_bytes);
+  o->levels_active = P->levels_active;
+  o->launches = P->launches;
+  o->flops = P->flops;
+  o->bytes = P->bytes;
+  o->flops_congruence = P->flops_cong;
+  o->flops_strips = P->flops_strip;
+  return H2SP_OK;
+}
+
+h2sp_status h2sp_plan_offsets(h2sp_plan P, int64_t *s_off_row, int64_t *s_off_col, int64_t *q_off_row,
+                              int64_t *q_off_col, int64_t *n_row, int64_t *n_col) {
+  if (!P) return fail(H2SP_EINVAL, "NULL plan");
+  for (int64_t c = 0; c < P->ncl; c++) {
+    if (s_off_row) s_off_row[c] = P->s_off_row[c];
+    if (s_off_col) s_off_col[c] = P->s_off_col[c];
+    if (q_off_row) q_off_row[c] = P->q_off_row[c];
+    if (q_off_col) q_off_col[c] = P->sym ? P->q_off_row[c] : P->q_off_col[c];
+    if (n_row) n_row[c] = P->n_row[c];
+    if (n_col) n_col[c] = P->n_col[c];
+  }
+  return H2SP_OK;
+}
+
+h2sp_status h2sp_plan_pattern(h2sp_plan P, int64_t *rowptr, int32_t *col) {
+  if (!P || !rowptr) return fail(H2SP_EINVAL, "NULL plan or rowptr");
+  std::memcpy(rowptr, P->meta.data() + P->rowptr_off, size_t(P->N + 1) * sizeof(int64_t));
+  if (col) {
+    const CsrBlockRow *rows = reinterpret_cast<const CsrBlockRow *>(P->meta.data() + P->csr_rows_off);
+    const CsrBlock *blks = reinterpret_cast<const CsrBlock *>(P->meta.data() + P->csr_blocks_off);
+    for (int64_t r = 0; r < P->n_csr_rows; r++)
+      for (int32_t a = 0; a < rows[r].m_r; a++) {
+        int32_t *dst = col + rows[r].p_base + int64_t(a) * rows[r].rowlen;
+        for (int32_t j = 0; j < rows[r].nblk; j++) {
+          const CsrBlock &b = blks[rows[r].blk_begin + j];
+          for (int32_t e = 0; e < b.m_c; e++) dst[b.colpos + e] = b.col0 + e;
+        }
+      }
+  }
+  return H2SP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,225 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Structure (S order, CSR rowptr/col) bit-exact; S values
+within relative Frobenius error 1e-11 and Q blocks within 1e-12 (BASELINE.json
+north_star); apply U^T b / V y within 1e-12."""
+import numpy as np
+import pytest
+
+import h2gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _run(h):
+    import paper_1705_04601_b200 as h2sp
+    packed = h2gen.pack(h)
+    plan = h2sp.Plan(packed)
+    sp = h2sp.Sparsifier(plan, packed)
+    out = sp.build()
+    torch.cuda.synchronize()
+    return plan, sp, out
+
+
+def _compare(h, plan, out, res=None, tol=1e-11, qtol=1e-12):
+    res = res or oracle.sparsify(h)
+    rowptr, col, val = oracle.s_csr(res)
+    nnz = len(val)
+    assert plan.sizes["s_nnz"] == nnz
+    assert np.array_equal(out["s_rowptr"].cpu().numpy(), rowptr)
+    assert np.array_equal(out["s_col"][:nnz].cpu().numpy(), col)
+    v = out["s_val"][:nnz].cpu().numpy()
+    nv = np.linalg.norm(val)
+    err = np.linalg.norm(v - val) / nv if nv > 0 else np.linalg.norm(v)
+    assert err <= tol, err
+    off = plan.offsets()
+    qr = out["q_row"].cpu().numpy()
+    qc = qr if h.symmetric else out["q_col"].cpu().numpy()
+    for c in range(len(res.Q_row)):
+        n = int(res.n_row[c])
+        if n:
+            Q = qr[off["q_off_row"][c]:off["q_off_row"][c] + n * n].reshape(n, n)
+            assert np.abs(Q - res.Q_row[c]).max() <= qtol, c
+        n = int(res.n_col[c])
+        if n:
+            Q = qc[off["q_off_col"][c]:off["q_off_col"][c] + n * n].reshape(n, n)
+            assert np.abs(Q - res.Q_col[c]).max() <= qtol, c
+    return res, v, err
+
+
+CASES = []
+for _sym in (True, False):
+    for _seed, _eta in ((0, 0.4), (1, 0.7), (2, 1.5), (3, 0.7)):
+        CASES.append((f"rand-{'sym' if _sym else 'gen'}-{_seed}",
+                      (lambda sym=_sym, seed=_seed, eta=_eta: h2gen.random_h2(5, 16, seed, sym, eta=eta))))
+CASES += [
+    ("rand-B64-sym", lambda: h2gen.random_h2(4, 64, 7, True, eta=0.7, max_rank=32)),
+    ("rand-B64-gen", lambda: h2gen.random_h2(4, 64, 8, False, eta=0.7, max_rank=32)),
+    ("rand-B40-gen-ragged", lambda: h2gen.random_h2(5, 40, 9, False, eta=0.5, max_rank=32)),
+    ("rand-B24-sym-uniform", lambda: h2gen.random_h2(5, 24, 10, True, eta=0.7, ragged=False, r=12)),
+    ("fig3-half", lambda: h2gen.fig3_h2(8, 0, "half")),
+    ("fig3-active-gen", lambda: h2gen.fig3_h2(8, 1, "active", symmetric=False)),
+    ("cfg1", lambda: h2gen.make_config(1)),
+    ("cfg2-16384", lambda: h2gen.make_config(2, N=16384)),
+]
+
+
+@pytest.mark.parametrize("name,make", CASES, ids=[c[0] for c in CASES])
+def test_parity_small(name, make):
+    _need_gpu()
+    h = make()
+    plan, sp, out = _run(h)
+    res, v, err = _compare(h, plan, out)
+    if h.symmetric:
+        # Proposition: S bitwise symmetric in our convention
+        import scipy.sparse as sps
+        nnz = plan.sizes["s_nnz"]
+        S = sps.csr_matrix((v, out["s_col"][:nnz].cpu().numpy(), out["s_rowptr"].cpu().numpy()), shape=(h.N, h.N))
+        assert (S != S.T).nnz == 0
+
+
+@pytest.mark.parametrize("sym", [True, False])
+def test_eta0_bitwise(sym):
+    """eta = 0: S = C bitwise on the GPU path too."""
+    _need_gpu()
+    h = h2gen.eta0_h2(3, 16, 5, symmetric=sym)
+    plan, sp, out = _run(h)
+    A = oracle.dense_A(h)
+    rowptr = out["s_rowptr"].cpu().numpy()
+    col = out["s_col"].cpu().numpy()
+    val = out["s_val"].cpu().numpy()
+    D = np.zeros_like(A)
+    for r in range(h.N):
+        D[r, col[rowptr[r]:rowptr[r + 1]]] = val[rowptr[r]:rowptr[r + 1]]
+    assert np.array_equal(D, A)
+
+
+def test_single_leaf():
+    _need_gpu()
+    h = h2gen.eta0_h2(0, 32, 6, symmetric=False)
+    plan, sp, out = _run(h)
+    assert np.array_equal(out["s_val"].cpu().numpy(), h.close[0].ravel())
+
+
+@pytest.mark.parametrize("sym,seed", [(True, 1), (False, 2)])
+def test_axis_aligned_bitwise(sym, seed):
+    """Every Q = I exactly, so the GPU cascade is exact: S equals the oracle's
+    (= P_r^T A_H2 P_c) bit for bit -- pins all permutation / strip bookkeeping."""
+    _need_gpu()
+    h = h2gen.axis_aligned_h2(5, 16, seed, sym)
+    plan, sp, out = _run(h)
+    res = oracle.sparsify(h)
+    rowptr, col, val = oracle.s_csr(res)
+    assert np.array_equal(out["s_val"][:len(val)].cpu().numpy(), val)
+
+
+def test_dense_reconstruction_from_gpu_factors():
+    """U S V^T = A_H2 with U, V assembled from the GPU's Q blocks (P1 on the GPU path)."""
+    _need_gpu()
+    h = h2gen.random_h2(4, 16, 12, False, eta=0.7)
+    plan, sp, out = _run(h)
+    res = oracle.sparsify(h)
+    off = plan.offsets()
+    qr, qc = out["q_row"].cpu().numpy(), out["q_col"].cpu().numpy()
+    res.Q_row = [qr[off["q_off_row"][c]:off["q_off_row"][c] + int(n) ** 2].reshape(int(n), int(n))
+                 for c, n in enumerate(res.n_row)]
+    res.Q_col = [qc[off["q_off_col"][c]:off["q_off_col"][c] + int(n) ** 2].reshape(int(n), int(n))
+                 for c, n in enumerate(res.n_col)]
+    U, V = oracle.dense_U(res, "row"), oracle.dense_U(res, "col")
+    nnz = plan.sizes["s_nnz"]
+    rowptr, col = out["s_rowptr"].cpu().numpy(), out["s_col"].cpu().numpy()
+    val = out["s_val"][:nnz].cpu().numpy()
+    S = np.zeros((h.N, h.N))
+    for r in range(h.N):
+        S[r, col[rowptr[r]:rowptr[r + 1]]] = val[rowptr[r]:rowptr[r + 1]]
+    A = oracle.dense_A(h)
+    assert np.linalg.norm(U @ S @ V.T - A) / np.linalg.norm(A) <= 1e-12
+
+
+@pytest.mark.parametrize("sym", [True, False])
+def test_apply_parity(sym):
+    _need_gpu()
+    h = h2gen.random_h2(5, 16, 20 + sym, sym, eta=0.7)
+    plan, sp, out = _run(h)
+    res = oracle.sparsify(h)
+    rng = np.random.default_rng(3)
+    b = rng.standard_normal((3, h.N))
+    bt = torch.from_numpy(b).cuda()
+    y = torch.empty_like(bt)
+    sp.apply_Ut(bt, y)
+    x = torch.empty_like(bt)
+    sp.apply_V(y, x)
+    torch.cuda.synchronize()
+    yo = oracle.apply_Ut(res, b.T, "row").T
+    xo = oracle.apply_V(res, yo.T, "col").T
+    assert np.abs(y.cpu().numpy() - yo).max() <= 1e-12 * np.abs(b).max()
+    assert np.abs(x.cpu().numpy() - xo).max() <= 1e-12 * np.abs(b).max()
+
+
+def test_solve_through_gpu_factors():
+    """x = V S^-1 U^T b equals A_H2^-1 b (Eq. sp0) using GPU apply and GPU S."""
+    _need_gpu()
+    import scipy.sparse as sps
+    import scipy.sparse.linalg as spla
+    h = h2gen.random_h2(4, 16, 31, True, eta=0.7, spd_shift=60.0)
+    plan, sp, out = _run(h)
+    nnz = plan.sizes["s_nnz"]
+    S = sps.csr_matrix((out["s_val"][:nnz].cpu().numpy(), out["s_col"][:nnz].cpu().numpy(),
+                        out["s_rowptr"].cpu().numpy()), shape=(h.N, h.N))
+    b = np.random.default_rng(4).standard_normal((1, h.N))
+    bt = torch.from_numpy(b).cuda()
+    y = torch.empty_like(bt)
+    sp.apply_Ut(bt, y)
+    z = spla.spsolve(S.tocsc(), y.cpu().numpy()[0])
+    x = torch.empty_like(bt)
+    sp.apply_V(torch.from_numpy(z[None, :]).cuda(), x)
+    A = oracle.dense_A(h)
+    xa = np.linalg.solve(A, b[0])
+    assert np.linalg.norm(x.cpu().numpy()[0] - xa) / np.linalg.norm(xa) <= np.linalg.cond(A) * 1e-14
+
+
+def test_build_is_deterministic_and_repeatable():
+    _need_gpu()
+    h = h2gen.random_h2(5, 16, 40, False, eta=0.7)
+    plan, sp, out = _run(h)
+    v1 = out["s_val"].clone()
+    sp.build()
+    torch.cuda.synchronize()
+    assert torch.equal(v1, out["s_val"])
+
+
+def test_build_host_e2e():
+    """h2sp_build_host: host inputs -> device -> host outputs equals the device path."""
+    _need_gpu()
+    import paper_1705_04601_b200 as h2sp
+    h = h2gen.random_h2(5, 16, 41, False, eta=0.7)
+    packed = h2gen.pack(h)
+    plan = h2sp.Plan(packed)
+    sp = h2sp.Sparsifier(plan, packed)
+    ref = {k: (v.clone() if v is not None else None) for k, v in sp.build().items()}
+    host_in = {k: v.cpu().pin_memory() for k, v in sp.inputs.items()}
+    host_out = {k: (torch.empty_like(v, device="cpu").pin_memory() if v is not None else None)
+                for k, v in sp.outputs.items()}
+    sp.build_host(host_in, host_out)
+    torch.cuda.synchronize()
+    for k in ("s_val", "s_col", "s_rowptr", "q_row", "q_col"):
+        assert torch.equal(host_out[k], ref[k].cpu()), k
+
+
+def test_parity_config2_full():
+    """BASELINE configs[1] at full size (N = 65536), the bench workload: full S,
+    all Q blocks against the oracle."""
+    _need_gpu()
+    h = h2gen.make_config(2)
+    plan, sp, out = _run(h)
+    res, v, err = _compare(h, plan, out)
+    # Frobenius invariance (P5) of the GPU S
+    f = oracle.frobenius_sq(h)
+    assert abs(float(np.dot(v, v)) - f) / f <= 1e-12

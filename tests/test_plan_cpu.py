@@ -1,0 +1,116 @@
+"""Host-side checks of the C-ABI library (no GPU needed): exported symbols,
+and the symbolic plan (S order, S pattern, CSR) against the oracle bitwise."""
+import ctypes
+
+import numpy as np
+import pytest
+
+import h2gen
+import oracle
+import paper_1705_04601_b200 as h2sp
+
+
+def test_library_exports_every_declared_symbol():
+    names = h2sp.declared_symbols()
+    assert len(names) >= 12
+    for n in names:
+        assert hasattr(h2sp.lib, n), n
+        ctypes.cast(getattr(h2sp.lib, n), ctypes.c_void_p)
+
+
+def _cases():
+    yield "cfg1", lambda: h2gen.make_config(1)
+    yield "cfg2-4096", lambda: h2gen.make_config(2, N=4096)
+    for sym in (True, False):
+        for seed, eta in ((0, 0.4), (1, 0.7), (2, 1.5)):
+            yield f"rand-{'sym' if sym else 'gen'}-{seed}", (lambda sym=sym, seed=seed, eta=eta:
+                                                             h2gen.random_h2(5, 8, seed, sym, eta=eta))
+    yield "fig3-half", lambda: h2gen.fig3_h2(4, 0, "half")
+    yield "fig3-active", lambda: h2gen.fig3_h2(4, 0, "active")
+    yield "eta0", lambda: h2gen.eta0_h2(3, 4, 0)
+    yield "axis-gen", lambda: h2gen.axis_aligned_h2(4, 8, 2, False)
+    yield "L0", lambda: h2gen.eta0_h2(0, 16, 0)
+
+
+CASES = list(_cases())
+
+
+@pytest.mark.parametrize("name,make", CASES, ids=[c[0] for c in CASES])
+def test_plan_structure_matches_oracle(name, make):
+    h = make()
+    res = oracle.sparsify(h)
+    plan = h2sp.Plan(h2gen.pack(h))
+    off = plan.offsets()
+    assert np.array_equal(off["s_off_row"], res.off_row)
+    assert np.array_equal(off["s_off_col"], res.off_col)
+    assert np.array_equal(off["n_row"], res.n_row) and np.array_equal(off["n_col"], res.n_col)
+    rowptr, col, val = oracle.s_csr(res)
+    prow, pcol = plan.pattern()
+    assert np.array_equal(prow, rowptr)
+    assert np.array_equal(pcol, col)
+    assert plan.sizes["s_nnz"] == len(val)
+    assert plan.sizes["s_blocks"] == len(res.S)
+    assert plan.sizes["q_row"] == sum(int(n) ** 2 for n in res.n_row)
+
+
+def _struct_with(h, **kw):
+    p = h2gen.pack(h)
+    p.update(kw)
+    return p
+
+
+def test_plan_rejects_bad_structures():
+    h = h2gen.random_h2(4, 8, 3, True, eta=0.7)
+    p = h2gen.pack(h)
+    # drop one near pair -> block tree no longer a partition / not symmetric
+    npt, ncol = p["near_ptr"].copy(), p["near_col"].copy()
+    ncol2 = np.delete(ncol, 1)
+    npt2 = npt.copy()
+    npt2[1:] -= 1
+    npt2[0] = 0
+    npt2 = np.maximum(npt2, 0)
+    with pytest.raises(h2sp.H2spError) as e:
+        h2sp.Plan(_struct_with(h, near_ptr=npt2, near_col=ncol2))
+    assert e.value.status == 2
+    # rank above the local size
+    rr = p["rank_row"].copy()
+    rr[0] = h.B + 1
+    with pytest.raises(h2sp.H2spError) as e:
+        h2sp.Plan(_struct_with(h, rank_row=rr, rank_col=rr))
+    assert e.value.status == 3
+    # nonzero root rank
+    rr = p["rank_row"].copy()
+    rr[-1] = 1
+    with pytest.raises(h2sp.H2spError) as e:
+        h2sp.Plan(_struct_with(h, rank_row=rr, rank_col=rr))
+    assert e.value.status == 3
+    # unsorted columns
+    ncol3 = ncol.copy()
+    r0 = slice(npt[0], npt[1])
+    ncol3[r0] = ncol3[r0][::-1]
+    if npt[1] - npt[0] > 1:
+        with pytest.raises(h2sp.H2spError) as e:
+            h2sp.Plan(_struct_with(h, near_col=ncol3))
+        assert e.value.status == 2
+    # a pair both near and admissible at level 1
+    gen = h2gen.random_h2(4, 8, 4, False, eta=0.7)
+    pg = h2gen.pack(gen)
+    adm1 = set(map(tuple, gen.adm[1].tolist()))
+    near1 = sorted({(t // 2, s // 2) for (t, s) in gen.near.tolist()} | {(t // 2, s // 2) for (t, s) in gen.adm[0].tolist()})
+    extra = [x for x in near1 if x not in adm1][0]
+    newadm = np.array(sorted(adm1 | {extra}), dtype=np.int32)
+    M = 1 << (gen.L - 1)
+    ptr = np.zeros(M + 1, dtype=np.int64)
+    np.add.at(ptr, newadm[:, 0] + 1, 1)
+    pg["adm_ptr"][1] = np.cumsum(ptr)
+    pg["adm_col"][1] = newadm[:, 1].astype(np.int32)
+    with pytest.raises(h2sp.H2spError) as e:
+        h2sp.Plan(pg)
+    assert e.value.status == 2
+
+
+def test_plan_unsupported_leaf_size():
+    h = h2gen.eta0_h2(1, 128, 0)
+    with pytest.raises(h2sp.H2spError) as e:
+        h2sp.Plan(h2gen.pack(h))
+    assert e.value.status == 7
