@@ -1,0 +1,420 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native H^2 sparsification hot path (arXiv 1705.04601).
+
+One *step* = one pass of the whole hot path of SURVEY.md §8(a) over one
+synthetic H^2 matrix already resident in HBM: h2sp_build (QR completion,
+couplings, merge + congruence + freeze, strips, CSR) followed by
+y = U^T b and x = V y (h2sp_apply_Ut / h2sp_apply_V).  The symbolic plan
+(row a1, host, structure only) is created once per matrix and reported as
+``config.plan_ms``.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Default workload: BASELINE.json configs[1] (N = 65,536 points in the unit
+square, exp(-|x-y|/0.1) + 1e-2 I, B = 64, r = 16, eta = 0.7, SPD -> symmetric
+mode).  With N > 1 GPUs (torchrun, one rank per GPU) every rank sparsifies its
+own independent matrix of the same recipe (weak scaling, no data-path
+collective); time = max over ranks.
+
+``--impl reference`` times the CPU oracle (oracle/, numpy, 1 thread) on a
+bounded sample of the workload; only rank 0 works.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "H2 sparsification time & FP64 TFLOP/s (frac. of peak) at 1/2/4/8 B200 vs CPU oracle"
+UNIT = "TFLOP/s"
+# FP64 peaks measured on this pool's B200 (profiles/r01_fp64_peak.txt): DMMA m8n8k4
+# microbenchmark 37.0 TFLOP/s (the ceiling used as roofline peak), cuBLAS DGEMM 35.5.
+FP64_PEAK_TFLOPS = 37.0
+FP64_DGEMM_TFLOPS = 35.5
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "fallback": True}
+
+
+def workload_desc(cfg_idx: int, h) -> str:
+    import h2gen
+    c = h2gen.CONFIGS[cfg_idx]
+    k = c["kernel"]
+    kern = {"exp": f"exp(-r/{k.get('ell')})+{k.get('nugget')}*I", "invh": "1/(r+h)+1.0*I (h=N^-1/3)",
+            "laplace": "1/(4 pi r), diag 1/(4 pi h)"}[k["kind"]]
+    return (f"BASELINE configs[{cfg_idx - 1}]: N={h.N} {c['points']} points, {kern}, B={c['B']}, r={c['r']}, "
+            f"eta={c['eta']}, {'symmetric (SPD)' if c['symmetric'] else 'general'} mode, seed={h.meta.get('seed')}")
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    def __init__(self, dev_index: int, period_s: float = 0.001):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.period = period_s
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    _NAMES = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+              0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+              0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self._NAMES.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": getattr(self, "max_mhz", None), "reasons": [],
+                    "note": getattr(self, "err", "no samples")}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def oracle_baseline(h, flops: float, sample: str):
+    """The oracle as it stands, single thread, on host cores."""
+    import oracle
+    try:
+        from threadpoolctl import threadpool_limits
+        ctx = threadpool_limits(1)
+        cores = 1
+    except Exception:  # noqa: BLE001
+        import contextlib
+        ctx = contextlib.nullcontext()
+        cores = os.cpu_count()
+    with ctx:
+        t0 = time.perf_counter()
+        res = oracle.sparsify(h)
+        oracle.s_csr(res)
+        dt = time.perf_counter() - t0
+    return {"value": flops / dt / 1e12, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+            "seconds": dt, "host_cpus": os.cpu_count()}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle on a bounded sample of the workload."""
+    if rank != 0:
+        return
+    import h2gen
+    import oracle
+    n_sample = args.ref_n
+    h = h2gen.make_config(args.config, N=n_sample)
+    # algorithmic flops of the sample, counted from the oracle's own structure
+    res0 = oracle.sparsify(h)
+    flops = _oracle_flops(res0, h)
+    sample = (f"configs[{args.config - 1}] recipe at N={n_sample} (L={h.L}), one full oracle pass "
+              f"(sparsify + CSR assembly) per step")
+    try:
+        from threadpoolctl import threadpool_limits
+        lim = threadpool_limits(1)
+    except Exception:  # noqa: BLE001
+        lim = None
+    for _ in range(args.warmup):
+        oracle.s_csr(oracle.sparsify(h))
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.s_csr(oracle.sparsify(h))
+    dt = (time.perf_counter() - t0) / args.steps
+    del lim
+    val = flops / dt / 1e12
+    line = {"metric": METRIC, "value": val, "unit": UNIT, "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_desc(args.config, h2gen.make_config(args.config, N=n_sample)),
+                       "sample_N": n_sample, "flops_per_step": flops},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _oracle_flops(res, h):
+    """Algorithmic flops of one build, counted on the oracle's structure with the
+    plan's per-unit figures: QR 2nk^2 + 4n^2k, couplings
+    2 k_t k_s (k_t + k_s), congruence 2 n_t n_s (n_t + n_s), strip rotation
+    2 n_p (sum of present children ranks) m.  Independent of libh2sp."""
+    from h2gen import cid
+    L = h.L
+    f = 0.0
+    sides = [(res.n_row, res.k_row)] + ([] if h.symmetric else [(res.n_col, res.k_col)])
+    for n, k in sides:
+        f += float(sum(2.0 * n[c] * k[c] ** 2 + 4.0 * n[c] ** 2 * k[c] for c in range(len(n))))
+    for lvl in range(L):
+        for (t, s) in h.adm[lvl]:
+            if h.symmetric and t > s:
+                continue
+            a, b = float(res.k_row[cid(L, lvl, t)]), float(res.k_col[cid(L, lvl, s)])
+            f += 2.0 * a * b * (a + b)
+    for lvl, near in enumerate(res.near_levels):
+        for (t, s) in near:
+            if h.symmetric and t > s:
+                continue
+            a, b = float(res.n_row[cid(L, lvl, t)]), float(res.n_col[cid(L, lvl, s)])
+            f += 2.0 * a * b * (a + b)
+
+    def strips(n_rot, k_rot, m_fix, transpose):
+        groups = {}
+        for j, near in enumerate(res.near_levels):
+            for pair in near:
+                t0, s0 = (pair[1], pair[0]) if transpose else pair
+                if m_fix[cid(L, j, s0)] == 0:
+                    continue
+                t, lvl = t0, j
+                while lvl < L and k_rot[cid(L, lvl, t)] > 0:
+                    groups.setdefault((lvl + 1, t // 2, j, s0), set()).add(t % 2)
+                    t, lvl = t // 2, lvl + 1
+        tot = 0.0
+        for (lvl, p, j, s0), kids in groups.items():
+            rows = sum(float(k_rot[cid(L, lvl - 1, 2 * p + a)]) for a in kids)
+            tot += 2.0 * float(n_rot[cid(L, lvl, p)]) * rows * float(m_fix[cid(L, j, s0)])
+        return tot
+
+    f += strips(res.n_row, res.k_row, res.m_col, False)
+    if not h.symmetric:
+        f += strips(res.n_col, res.k_col, res.m_row, True)
+    return f
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--n", type=int, default=None, help="override N (smaller instance of the recipe)")
+    ap.add_argument("--nrhs", type=int, default=1)
+    ap.add_argument("--no-oracle", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ref-n", type=int, default=16384, help="--impl reference sample size")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import h2gen
+    import paper_1705_04601_b200 as h2sp
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    seed = args.config + 1000 * rank
+    h = h2gen.make_config(args.config, seed=seed, N=args.n)
+    packed = h2gen.pack(h)
+    t0 = time.perf_counter()
+    plan = h2sp.Plan(packed)
+    plan_ms = (time.perf_counter() - t0) * 1e3
+    sp = h2sp.Sparsifier(plan, packed, device=dev)
+    launches = plan.launches()
+    n_launch = len(launches)
+    assert n_launch == plan.sizes["launches"]
+    nrhs = args.nrhs
+    b = torch.randn(nrhs, plan.N, dtype=torch.float64, device=dev)
+    y = torch.empty_like(b)
+    x = torch.empty_like(b)
+    aws = sp.apply_ws(nrhs)
+    offs = plan.offsets()
+    n_apply_launch = 2 * sum(1 for k in range(plan.L + 1)
+                             if offs["n_row"][h2gen.lvl_off(plan.L, k):h2gen.lvl_off(plan.L, k) + (1 << (plan.L - k))].max() > 0)
+    apply_flops = 2 * 2.0 * nrhs * float(np.sum(offs["n_row"].astype(float) ** 2))
+    step_flops = plan.sizes["flops"] + apply_flops
+    stream = torch.cuda.current_stream()
+
+    def step(events=None):
+        if events is None:
+            sp.build()
+        else:
+            sp.build_profiled(events)
+        sp.apply_Ut(b, y, ws=aws)
+        sp.apply_V(y, x, ws=aws)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # per-launch events for the roofline of the dominant kernel (same stream)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * n_launch)] for _ in range(args.steps)]
+    for row in evs:            # torch creates the CUDA event lazily on first record
+        for e in row:
+            e.record(stream)
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        t_start.record(stream)
+        for i in range(args.steps):
+            step(evs[i])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t_start.elapsed_time(t_end) / args.steps
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    # per-launch durations averaged over the timed steps
+    per = np.zeros(n_launch)
+    for i in range(args.steps):
+        for j in range(n_launch):
+            per[j] += evs[i][2 * j].elapsed_time(evs[i][2 * j + 1])
+    per /= args.steps
+    kinds = {}
+    for j, li in enumerate(launches):
+        kinds[li["kind"]] = kinds.get(li["kind"], 0.0) + per[j]
+    top = int(np.argmax(per))
+    li = launches[top]
+    peaks = _peaks()
+    ai = li["flops"] / li["bytes"] if li["bytes"] else float("inf")
+    ridge = FP64_PEAK_TFLOPS * 1e12 / (peaks["hbm_gbs"] * 1e9)
+    if ai >= ridge:
+        roof = {"bound": "tensor", "achieved": li["flops"] / (per[top] * 1e-3) / 1e12, "peak": FP64_PEAK_TFLOPS,
+                "unit": "TFLOP/s"}
+    else:
+        roof = {"bound": "hbm", "achieved": li["bytes"] / (per[top] * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = _ncu_traffic(li)
+    roof.update({"kernel": f"{li['kind']}@level{li['level']}", "launch_ms": per[top],
+                 "share_of_step": per[top] / ms, "algorithmic_flops": li["flops"], "algorithmic_bytes": li["bytes"],
+                 "arithmetic_intensity": ai,
+                 "peak_source": "FP64 DMMA microbenchmark on this pool's B200 (profiles/r01_fp64_peak.txt); "
+                                f"cuBLAS DGEMM measured {FP64_DGEMM_TFLOPS}",
+                 "hbm_peak_gbs": peaks["hbm_gbs"]})
+    value = step_flops * world / (ms_max * 1e-3) / 1e12
+
+    # ---- e2e through the public API with HOST buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        host_in = {k: v.cpu().pin_memory() for k, v in sp.inputs.items()}
+        host_out = {k: (torch.empty(v.shape, dtype=v.dtype).pin_memory() if v is not None else None)
+                    for k, v in sp.outputs.items()}
+        hb = b.cpu().pin_memory()
+        hx = torch.empty(x.shape, dtype=x.dtype).pin_memory()
+
+        def step_e2e():
+            sp.build_host(host_in, host_out)
+            b.copy_(hb, non_blocking=True)
+            sp.apply_Ut(b, y, ws=aws)
+            sp.apply_V(y, x, ws=aws)
+            hx.copy_(x, non_blocking=True)
+
+        for _ in range(2):
+            step_e2e()
+        torch.cuda.synchronize()
+        k_e2e = max(3, min(args.steps, 10))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(k_e2e):
+            step_e2e()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = torch.tensor([e0.elapsed_time(e1) / k_e2e], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        h2d = sum(int(v.numel()) * v.element_size() for v in host_in.values()) + hb.numel() * 8
+        d2h = sum(int(v.numel()) * v.element_size() for v in host_out.values() if v is not None) + hx.numel() * 8
+        e2e = {"value": step_flops * world / (float(ems.item()) * 1e-3) / 1e12, "unit": UNIT,
+               "ms_per_step": float(ems.item()), "steps": k_e2e, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_oracle:
+        cpu = oracle_baseline(h, plan.sizes["flops"],
+                              f"one full oracle pass (sparsify + CSR assembly) of the same matrix "
+                              f"(N={plan.N}); build flops only")
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_desc(args.config, h), "N": plan.N, "B": plan.B, "L": plan.L,
+                       "nrhs": nrhs, "mode": "symmetric" if plan.symmetric else "general",
+                       "parallelism": f"replicas x{world} (independent matrices per rank, no collective)",
+                       "l2": "inputs (close blocks %.2f GB) and outputs (S %.2f GB) exceed the 126 MB L2; no flush"
+                             % (plan.sizes["close"] * 8e-9, plan.sizes["s_nnz"] * 12e-9),
+                       "plan_ms": plan_ms, "s_nnz": plan.sizes["s_nnz"], "s_blocks": plan.sizes["s_blocks"],
+                       "flops_per_step": step_flops, "bytes_per_step": plan.sizes["bytes"],
+                       "fp64_frac_of_peak_whole_step": value / world / FP64_PEAK_TFLOPS,
+                       "hbm_frac_whole_step": plan.sizes["bytes"] / (ms_max * 1e-3) / (peaks["hbm_gbs"] * 1e9),
+                       "breakdown_ms": {k: round(v, 4) for k, v in kinds.items()}},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps * (n_launch + n_apply_launch),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _ncu_traffic(li):
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    summary (profiles/*_ncu_top.json), if one exists for this kernel."""
+    import glob
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_top.json")), reverse=True):
+        try:
+            with open(p) as f:
+                d = json.load(f)
+            if d.get("kernel_kind") == li["kind"] and d.get("level") == li["level"]:
+                return d.get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            continue
+    return None
+
+
+if __name__ == "__main__":
+    main()

@@ -153,6 +153,21 @@ h2sp_status h2sp_plan_offsets(h2sp_plan plan, int64_t *s_off_row, int64_t *s_off
 h2sp_status h2sp_plan_pattern(h2sp_plan plan, int64_t *rowptr, int32_t *col);
 void h2sp_plan_destroy(h2sp_plan plan);
 
+/* Description of the kernel launches of one h2sp_build, in launch order
+ * (kind: 0 QR row side, 1 QR column side, 2 couplings, 3 merge+congruence+
+ * freeze, 4 row strips, 5 column strips, 6 CSR index expansion).  flops and
+ * bytes are the algorithmic FP64 flops and HBM bytes of that launch
+ * (SURVEY §8(d) per-unit figures x units in the launch); items = work units. */
+typedef struct {
+  int32_t kind;
+  int32_t level;
+  int64_t items;
+  double flops;
+  double bytes;
+} h2sp_launch_info;
+/* Writes min(max, count) records to out (may be NULL) and the count to *count. */
+h2sp_status h2sp_plan_launches(h2sp_plan plan, h2sp_launch_info *out, int64_t max, int64_t *count);
+
 /* Copies the plan's device work lists (sizes.meta_bytes bytes) into the first
  * part of a device workspace `ws` (256-byte aligned) on `stream`.  Must be
  * called once for every workspace before it is passed to h2sp_build or
@@ -168,6 +183,14 @@ h2sp_status h2sp_plan_upload(h2sp_plan plan, void *ws, size_t ws_bytes, void *st
  * aligned, uploaded with h2sp_plan_upload. */
 h2sp_status h2sp_build(h2sp_plan plan, const h2sp_inputs *in, const h2sp_outputs *out, void *ws,
                        size_t ws_bytes, void *stream);
+
+/* h2sp_build that also records CUDA events for profiling: events[2i] and
+ * events[2i+1] (cudaEvent_t) just before and just after launch i of
+ * h2sp_plan_launches, on the stream that launch runs on (the build forks
+ * independent chains -- QR/couplings of levels >= 1, CSR index expansion --
+ * onto internal side streams joined back into `stream`); n_events >= 2*count. */
+h2sp_status h2sp_build_ex(h2sp_plan plan, const h2sp_inputs *in, const h2sp_outputs *out, void *ws,
+                          size_t ws_bytes, void *stream, void *const *events, int64_t n_events);
 
 /* End-to-end variant with HOST buffers: copies the host inputs into the given
  * device input buffers, builds, and copies every output back into the host

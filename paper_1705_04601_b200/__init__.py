@@ -44,6 +44,13 @@ class _Sizes(ctypes.Structure):
                [(n, _f64) for n in ("flops", "bytes", "flops_congruence", "flops_strips")]
 
 
+class _LaunchInfo(ctypes.Structure):
+    _fields_ = [("kind", _i32), ("level", _i32), ("items", _i64), ("flops", _f64), ("bytes", _f64)]
+
+
+LAUNCH_KINDS = ("qr_row", "qr_col", "coupling", "congruence", "strips_row", "strips_col", "csr")
+
+
 class _Inputs(ctypes.Structure):
     _fields_ = [(n, _vp) for n in ("leaf_basis_row", "transfer_row", "leaf_basis_col", "transfer_col", "close",
                                    "coupling")]
@@ -65,6 +72,9 @@ lib.h2sp_plan_destroy.argtypes = [_vp]
 lib.h2sp_plan_destroy.restype = None
 lib.h2sp_plan_upload.argtypes = [_vp, _vp, ctypes.c_size_t, _vp]
 lib.h2sp_build.argtypes = [_vp, ctypes.POINTER(_Inputs), ctypes.POINTER(_Outputs), _vp, ctypes.c_size_t, _vp]
+lib.h2sp_build_ex.argtypes = [_vp, ctypes.POINTER(_Inputs), ctypes.POINTER(_Outputs), _vp, ctypes.c_size_t, _vp,
+                              ctypes.POINTER(_vp), _i64]
+lib.h2sp_plan_launches.argtypes = [_vp, ctypes.POINTER(_LaunchInfo), _i64, ctypes.POINTER(_i64)]
 lib.h2sp_build_host.argtypes = [_vp, ctypes.POINTER(_Inputs), ctypes.POINTER(_Outputs), ctypes.POINTER(_Inputs),
                                 ctypes.POINTER(_Outputs), _vp, ctypes.c_size_t, _vp]
 lib.h2sp_apply_ws_bytes.argtypes = [_vp, ctypes.c_int]
@@ -146,6 +156,15 @@ class Plan:
                "h2sp_plan_offsets")
         return out
 
+    def launches(self):
+        """Per-launch descriptors of one build (kind, level, items, flops, bytes)."""
+        n = _i64()
+        _check(lib.h2sp_plan_launches(self.handle, None, 0, ctypes.byref(n)), "h2sp_plan_launches")
+        arr = (_LaunchInfo * max(n.value, 1))()
+        _check(lib.h2sp_plan_launches(self.handle, arr, n.value, ctypes.byref(n)), "h2sp_plan_launches")
+        return [dict(kind=LAUNCH_KINDS[a.kind], level=a.level, items=a.items, flops=a.flops, bytes=a.bytes)
+                for a in arr[:n.value]]
+
     def pattern(self, with_cols: bool = True):
         rowptr = np.zeros(self.N + 1, dtype=np.int64)
         col = np.zeros(self.sizes["s_nnz"], dtype=np.int32) if with_cols else None
@@ -218,6 +237,15 @@ class Sparsifier:
             out.s_col = None
         _check(lib.h2sp_build(self.plan.handle, ctypes.byref(self._abi_inputs()), ctypes.byref(out), self.ws_ptr,
                               self.ws_bytes, _stream_handle(stream)), "h2sp_build")
+        return self.outputs
+
+    def build_profiled(self, events, stream=None):
+        """h2sp_build_ex: records events[i] (torch.cuda.Event) before launch i and
+        events[-1] after the last launch, on the launching stream."""
+        arr = (_vp * len(events))(*[e.cuda_event for e in events])
+        _check(lib.h2sp_build_ex(self.plan.handle, ctypes.byref(self._abi_inputs()),
+                                 ctypes.byref(self._abi_outputs()), self.ws_ptr, self.ws_bytes,
+                                 _stream_handle(stream), arr, len(events)), "h2sp_build_ex")
         return self.outputs
 
     def build_host(self, host_inputs: dict, host_outputs: dict, stream=None):

@@ -56,7 +56,20 @@ h2sp_status h2sp_build(h2sp_plan P, const h2sp_inputs *in, const h2sp_outputs *o
   if (!out->q_row || !out->s_val || (!P->sym && !out->q_col)) return fail(H2SP_EINVAL, "NULL output array");
   if (h2sp_status s = check_device()) return s;
   int64_t nl = 0;
-  return launch_build(P, in, out, static_cast<unsigned char *>(ws), stream, &nl);
+  return launch_build(P, in, out, static_cast<unsigned char *>(ws), stream, &nl, nullptr, 0);
+}
+
+h2sp_status h2sp_build_ex(h2sp_plan P, const h2sp_inputs *in, const h2sp_outputs *out, void *ws, size_t ws_bytes,
+                          void *stream, void *const *events, int64_t n_events) {
+  if (!P || !in || !out) return fail(H2SP_EINVAL, "NULL plan, inputs or outputs");
+  if (events && n_events < 2 * P->launches) return fail(H2SP_EINVAL, "need 2 * launches events");
+  if (h2sp_status s = check_ws(P, ws, ws_bytes, P->ws_total)) return s;
+  if (!out->q_row || !out->s_val || (!P->sym && !out->q_col)) return fail(H2SP_EINVAL, "NULL output array");
+  if (h2sp_status s = check_device()) return s;
+  int64_t nl = 0;
+  h2sp_status s = launch_build(P, in, out, static_cast<unsigned char *>(ws), stream, &nl, events, n_events);
+  if (s == H2SP_OK && nl != P->launches) return fail(H2SP_EINVAL, "internal: launch count mismatch");
+  return s;
 }
 
 h2sp_status h2sp_build_host(h2sp_plan P, const h2sp_inputs *hi, const h2sp_outputs *ho, const h2sp_inputs *di,

@@ -121,6 +121,7 @@ struct h2sp_plan_s {
   // workspace layout after the meta region (byte offsets)
   size_t ws_rh_row, ws_rh_col, ws_dt, ws_bb, ws_yr, ws_yc, ws_total;
   int64_t launches;
+  std::vector<h2sp_launch_info> launch_info;
   uint64_t magic;                           // first 8 bytes of the meta image (checked on device)
 };
 
@@ -130,7 +131,7 @@ h2sp_status fail(h2sp_status s, const std::string &msg);
 
 // kernels.cu
 h2sp_status launch_build(const h2sp_plan_s *p, const h2sp_inputs *in, const h2sp_outputs *out, unsigned char *ws,
-                         void *stream, int64_t *launches);
+                         void *stream, int64_t *launches, void *const *events, int64_t n_events);
 h2sp_status launch_apply_Ut(const h2sp_plan_s *p, const double *q, const double *b, int64_t ldb, double *y,
                             int64_t ldy, int nrhs, unsigned char *ws, void *stream, bool col_side);
 h2sp_status launch_apply_V(const h2sp_plan_s *p, const double *q, const double *y, int64_t ldy, double *x,

@@ -11,8 +11,10 @@
 // memory across the run of items (a block row) of one CTA.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <vector>
 
 #include "h2sp_internal.h"
 
@@ -122,12 +124,26 @@ __device__ __forceinline__ void zero_acc(double (&acc)[TM][TN][2]) {
     for (int j = 0; j < TN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
 }
 
-// Load an n x m row-major global block into a padded NR x NC shared tile (LD), zero fill.
+// cp.async (LDGSTS) helpers: every global->shared tile load is issued as a batch
+// of asynchronous 8-byte copies (zero-filled outside the valid region) and
+// waited for once, so the loads of a tile overlap instead of serialising.
+__device__ __forceinline__ void cp8(void *sdst, const void *gsrc, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gsrc), "r"(valid ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Asynchronously load an n x m row-major global block (leading dim ldg) into a
+// padded NR x NC shared tile with leading dimension LD, zero fill.  `any` is a
+// valid global address used for the zero-filled (not read) copies.
 template <int NR, int NC, int LD>
-__device__ __forceinline__ void load_tile(double *s, const double *__restrict__ g, int n, int m, int ldg) {
+__device__ __forceinline__ void async_tile(double *s, const double *__restrict__ g, int n, int m, int64_t ldg,
+                                           const void *any) {
   for (int idx = threadIdx.x; idx < NR * NC; idx += blockDim.x) {
-    int i = idx / NC, j = idx % NC;
-    s[i * LD + j] = (i < n && j < m) ? g[int64_t(i) * ldg + j] : 0.0;
+    const int i = idx / NC, j = idx % NC;
+    const bool v = i < n && j < m;
+    cp8(&s[i * LD + j], v ? (const void *)(g + int64_t(i) * ldg + j) : any, v);
   }
 }
 
@@ -137,8 +153,14 @@ __device__ __forceinline__ void load_tile(double *s, const double *__restrict__ 
 //   X = R_leaf (level 0) or [R^_c1 T[:k1]; R^_c2 T[k1:]] (internal)
 //   Householder on X (alpha = x_0, sigma = ||x_1:||; sigma == 0 -> tau = 0;
 //   beta = -sgn(alpha) hypot(alpha, sigma), sgn(+-0) = +1), R^ = triu(X[:k]),
-//   Q = H_0 ... H_{k-1} I_n.
+//   Q = H_0 ... H_{k-1} = I - V T V^T (compact WY form of the same product,
+//   T from the dlarft recurrence), written straight to global memory.
+// Shared memory: X/V (n x (k+1)) | stage T (n x k) | R^ children / M (n x n) | T (k x k) | Gv (k x k)
 // --------------------------------------------------------------------------
+__host__ __device__ inline size_t qr_smem_bytes(int n, int k) {
+  return sizeof(double) * (size_t(n) * (k + 1) + size_t(n) * k + size_t(n) * n + 2 * size_t(k) * k + 8);
+}
+
 __global__ void __launch_bounds__(128) qr_kernel(Side sd, int L, int level, const double *__restrict__ leaf,
                                                  const double *__restrict__ transfer, double *__restrict__ rh,
                                                  double *__restrict__ qout, const uint64_t *meta_magic,
@@ -148,40 +170,53 @@ __global__ void __launch_bounds__(128) qr_kernel(Side sd, int L, int level, cons
   const int64_t cl = base + blockIdx.x;
   const int n = sd.n[cl], k = sd.k[cl];
   if (n == 0) return;
-  extern __shared__ double sm[];
-  const int ldx = k + 1;           // X: n x k (ldx), reflectors stored below the diagonal
-  const int ldq = n + 1;           // Q: n x n
-  double *X = sm;
-  double *Q = X + n * ldx;
-  double *tau = Q + n * ldq;
-  __shared__ double s_scal[3];     // beta, tau, 1/(alpha - beta) unused; scale divisor
+  extern __shared__ __align__(16) double sm[];
+  const int ldx = k + 1;
+  double *X = sm;                    // n x ldx
+  double *stg = X + n * ldx;         // n x k: transfer T
+  double *sR = stg + n * k;          // n x n: R^_c1, R^_c2 staging; later M = T_wy V^T (k x n)
+  double *Tw = sR + n * n;           // k x k   (WY T factor)
+  double *Gv = Tw + k * k;           // k x k   (V^T V)
+  double *Mk = sR;
+  __shared__ double s_scal[3];
+  __shared__ double s_tau[64];
   const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
   // ---- load X
   if (level == 0) {
     const double *R = leaf + sd.leaf_off[cl];
-    for (int idx = tid; idx < n * k; idx += blockDim.x) X[(idx / k) * ldx + idx % k] = R[idx];
-  } else {
+    for (int idx = tid; idx < n * k; idx += blockDim.x) cp8(&X[(idx / k) * ldx + idx % k], R + idx, true);
+    cp_commit();
+    cp_wait_all();
+    __syncthreads();
+  } else if (k > 0) {
     const int64_t ci = cl - base;
     const int64_t c1 = lvl_off_d(L, level - 1) + 2 * ci, c2 = c1 + 1;
     const int k1 = sd.k[c1], k2 = sd.k[c2];
-    const double *T = transfer + sd.tr_off[cl];       // n x k
-    const double *R1 = rh + sd.rh_off[c1];            // k1 x k1 upper
-    const double *R2 = rh + sd.rh_off[c2];            // k2 x k2 upper
+    const double *T = transfer + sd.tr_off[cl];  // n x k
+    double *sR1 = sR, *sR2 = sR + k1 * k1;
+    const double *R1 = rh + sd.rh_off[c1];
+    const double *R2 = rh + sd.rh_off[c2];
+    for (int idx = tid; idx < n * k; idx += blockDim.x) cp8(&stg[idx], T + idx, true);
+    for (int idx = tid; idx < k1 * k1; idx += blockDim.x) cp8(&sR1[idx], R1 + idx, true);
+    for (int idx = tid; idx < k2 * k2; idx += blockDim.x) cp8(&sR2[idx], R2 + idx, true);
+    cp_commit();
+    cp_wait_all();
+    __syncthreads();
     for (int idx = tid; idx < n * k; idx += blockDim.x) {
       const int i = idx / k, j = idx % k;
       double acc = 0.0;
       if (i < k1) {
-        for (int l = i; l < k1; l++) acc = fma(R1[i * k1 + l], T[l * k + j], acc);
+        for (int l = i; l < k1; l++) acc = fma(sR1[i * k1 + l], stg[l * k + j], acc);
       } else {
         const int ii = i - k1;
-        for (int l = ii; l < k2; l++) acc = fma(R2[ii * k2 + l], T[(k1 + l) * k + j], acc);
+        for (int l = ii; l < k2; l++) acc = fma(sR2[ii * k2 + l], stg[(k1 + l) * k + j], acc);
       }
       X[i * ldx + j] = acc;
     }
+    __syncthreads();
   }
-  __syncthreads();
-  const int warp = tid >> 5, lane = tid & 31;
-  // ---- Householder factorisation
+  // ---- Householder factorisation (reflectors stored below the diagonal, v_j[0] = 1 implicit)
   for (int j = 0; j < k; j++) {
     if (warp == 0) {
       double ss = 0.0;
@@ -203,7 +238,7 @@ __global__ void __launch_bounds__(128) qr_kernel(Side sd, int L, int level, cons
         s_scal[0] = beta;
         s_scal[1] = t;
         s_scal[2] = alpha - beta;
-        tau[j] = t;
+        s_tau[j] = t;
       }
     }
     __syncthreads();
@@ -211,10 +246,7 @@ __global__ void __launch_bounds__(128) qr_kernel(Side sd, int L, int level, cons
     if (t != 0.0) {
       const double div = s_scal[2];
       for (int i = j + 1 + tid; i < n; i += blockDim.x) X[i * ldx + j] = X[i * ldx + j] / div;
-    }
-    __syncthreads();
-    if (t != 0.0) {
-      // trailing columns: w_c = X[j][c] + sum_{i>j} v_i X[i][c]; X[i][c] -= tau v_i w_c
+      __syncthreads();
       for (int c = j + 1 + warp; c < k; c += blockDim.x / 32) {
         double w = 0.0;
         for (int i = j + 1 + lane; i < n; i += 32) w = fma(X[i * ldx + j], X[i * ldx + c], w);
@@ -226,7 +258,10 @@ __global__ void __launch_bounds__(128) qr_kernel(Side sd, int L, int level, cons
         if (lane == 0) X[j * ldx + c] -= tw;
         for (int i = j + 1 + lane; i < n; i += 32) X[i * ldx + c] = fma(-tw, X[i * ldx + j], X[i * ldx + c]);
       }
+    } else {
+      for (int i = j + 1 + tid; i < n; i += blockDim.x) X[i * ldx + j] = 0.0;  // v_j = e_1
     }
+    __syncthreads();
     if (tid == 0) X[j * ldx + j] = s_scal[0];
     __syncthreads();
   }
@@ -238,51 +273,85 @@ __global__ void __launch_bounds__(128) qr_kernel(Side sd, int L, int level, cons
       R[idx] = j >= i ? X[i * ldx + j] : 0.0;
     }
   }
-  // ---- Q = H_0 ... H_{k-1} I: thread per column, reflectors in reverse order
-  for (int c = tid; c < n; c += blockDim.x) {
-    for (int i = 0; i < n; i++) Q[i * ldq + c] = (i == c) ? 1.0 : 0.0;
-    for (int j = k - 1; j >= 0; j--) {
-      const double t = tau[j];
-      if (t == 0.0) continue;
-      double w = Q[j * ldq + c];
-      for (int i = j + 1; i < n; i++) w = fma(X[i * ldx + j], Q[i * ldq + c], w);
-      const double tw = t * w;
-      Q[j * ldq + c] -= tw;
-      for (int i = j + 1; i < n; i++) Q[i * ldq + c] = fma(-tw, X[i * ldx + j], Q[i * ldq + c]);
+  // ---- compact WY: Gv = V^T V (V unit lower trapezoidal), T recurrence, M = T V^T
+  auto V = [&](int i, int j) -> double { return i < j ? 0.0 : (i == j ? 1.0 : X[i * ldx + j]); };
+  for (int idx = tid; idx < k * k; idx += blockDim.x) {
+    const int a = idx / k, b = idx % k;
+    double acc = 0.0;
+    if (a < b)
+      for (int i = b; i < n; i++) acc = fma(V(i, a), V(i, b), acc);
+    Gv[idx] = acc;
+  }
+  __syncthreads();
+  // T[j][j] = tau_j, T[0:j, j] = -tau_j T[0:j, 0:j] Gv[0:j, j]   (dlarft, forward, columnwise)
+  for (int j = 0; j < k; j++) {
+    const double tj = s_tau[j];
+    double v = 0.0;
+    if (tid < j) {
+      for (int l = tid; l < j; l++) v = fma(Tw[tid * k + l], Gv[l * k + j], v);
+      v = -tj * v;
     }
+    __syncthreads();
+    if (tid < j) Tw[tid * k + j] = v;
+    if (tid == j) Tw[j * k + j] = tj;
+    if (tid > j && tid < k) Tw[tid * k + j] = 0.0;
+    __syncthreads();
+  }
+  for (int idx = tid; idx < k * n; idx += blockDim.x) {
+    const int a = idx / n, c = idx % n;
+    double acc = 0.0;
+    for (int l = a; l < k; l++) acc = fma(Tw[a * k + l], V(c, l), acc);
+    Mk[a * n + c] = acc;
   }
   __syncthreads();
   double *Qg = qout + sd.q_off[cl];
-  for (int idx = tid; idx < n * n; idx += blockDim.x) Qg[idx] = Q[(idx / n) * ldq + idx % n];
+  for (int idx = tid; idx < n * n; idx += blockDim.x) {
+    const int i = idx / n, c = idx % n;
+    double acc = 0.0;
+    const int lmax = i + 1 < k ? i + 1 : k;   // V(i, l) = 0 for l > i
+    for (int l = 0; l < lmax; l++) acc = fma(V(i, l), Mk[l * n + c], acc);
+    Qg[idx] = (i == c ? 1.0 : 0.0) - acc;
+  }
 }
 
 // --------------------------------------------------------------------------
 // Couplings in orthogonalised coordinates: D~ = R^R_t D R^C_s^T.
+// One warp per admissible pair, `ipc` pairs per CTA; each warp stages its
+// operands (4 * kmax^2 doubles) in its own slice of shared memory.
 // --------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) coupling_kernel(const CouplingItem *__restrict__ items, Side rs, Side cs,
-                                                       const double *__restrict__ rh_row,
+__global__ void __launch_bounds__(128) coupling_kernel(const CouplingItem *__restrict__ items, int64_t n_items,
+                                                       int kmax, Side rs, Side cs, const double *__restrict__ rh_row,
                                                        const double *__restrict__ rh_col,
                                                        const double *__restrict__ D, double *__restrict__ dt) {
-  const CouplingItem it = items[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t item = int64_t(blockIdx.x) * (blockDim.x >> 5) + warp;
+  if (item >= n_items) return;
+  const CouplingItem it = items[item];
   const int kt = rs.k[it.t], ks = cs.k[it.s];
-  extern __shared__ double sm[];
-  double *sD = sm;               // kt x ks
-  double *sT = sm + kt * ks;     // kt x ks: D R^_s^T
+  extern __shared__ __align__(16) double sm[];
+  double *sD = sm + size_t(warp) * 4 * kmax * kmax;   // kt x ks
+  double *sT = sD + kt * ks;                            // kt x ks: D R^_s^T
+  double *sRt = sT + kt * ks;                           // kt x kt
+  double *sRs = sRt + kt * kt;                          // ks x ks
   const double *Rt = rh_row + rs.rh_off[it.t];
   const double *Rs = rh_col + cs.rh_off[it.s];
-  for (int idx = threadIdx.x; idx < kt * ks; idx += blockDim.x) sD[idx] = D[it.d_src + idx];
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < kt * ks; idx += blockDim.x) {
+  for (int idx = lane; idx < kt * ks; idx += 32) cp8(&sD[idx], D + it.d_src + idx, true);
+  for (int idx = lane; idx < kt * kt; idx += 32) cp8(&sRt[idx], Rt + idx, true);
+  for (int idx = lane; idx < ks * ks; idx += 32) cp8(&sRs[idx], Rs + idx, true);
+  cp_commit();
+  cp_wait_all();
+  __syncwarp();
+  for (int idx = lane; idx < kt * ks; idx += 32) {
     const int i = idx / ks, j = idx % ks;
     double acc = 0.0;
-    for (int l = j; l < ks; l++) acc = fma(sD[i * ks + l], Rs[j * ks + l], acc);
+    for (int l = j; l < ks; l++) acc = fma(sD[i * ks + l], sRs[j * ks + l], acc);
     sT[idx] = acc;
   }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < kt * ks; idx += blockDim.x) {
+  __syncwarp();
+  for (int idx = lane; idx < kt * ks; idx += 32) {
     const int i = idx / ks, j = idx % ks;
     double acc = 0.0;
-    for (int l = i; l < kt; l++) acc = fma(Rt[i * kt + l], sT[l * ks + j], acc);
+    for (int l = i; l < kt; l++) acc = fma(sRt[i * kt + l], sT[l * ks + j], acc);
     dt[it.dt_dst + idx] = acc;
   }
 }
@@ -290,8 +359,9 @@ __global__ void __launch_bounds__(128) coupling_kernel(const CouplingItem *__res
 // --------------------------------------------------------------------------
 // Steps (iv)+(ii)+(iii): one CTA per chunk of pairs (t, s_1..s_c) of one block
 // row t.  Q_t resident in shared memory; per pair: gather G (level 0: C_ts;
-// else the 2x2 children arrangement of bb parts / D~), T = Q_t^T G, H = T Q_s,
-// then scatter H's four parts (nn -> S, bb -> next level, bn / nb -> strips).
+// else the 2x2 children arrangement of bb parts / D~) and Q_s with cp.async,
+// T = Q_t^T G, H = T Q_s on the FP64 tensor pipe (DMMA), then scatter H's
+// four parts (nn -> S, bb -> next level, bn / nb -> strips).
 // --------------------------------------------------------------------------
 template <int NP>
 struct PairCfg {
@@ -317,6 +387,44 @@ struct PairArgs {
 };
 
 template <int NP>
+__device__ __forceinline__ void pair_load_operands(const PairArgs &A, const PairItem &it, int t, int nt, int64_t lbase,
+                                                   double *sG, double *sQs) {
+  constexpr int LD = PairCfg<NP>::LD;
+  const int s = it.s;
+  const int ns = A.cs.n[s];
+  const void *any = A.items;
+  if (A.level == 0) {
+    async_tile<NP, NP, LD>(sG, A.close + it.g_src[0], nt, ns, A.B, any);
+  } else {
+    const int64_t tc1 = lvl_off_d(A.L, A.level - 1) + 2 * (t - lbase);
+    const int64_t sc1 = lvl_off_d(A.L, A.level - 1) + 2 * (s - lbase);
+    const int kr0 = A.rs.k[tc1], kr1 = A.rs.k[tc1 + 1];
+    const int kc0 = A.cs.k[sc1], kc1 = A.cs.k[sc1 + 1];
+    for (int idx = threadIdx.x; idx < NP * NP; idx += blockDim.x) {
+      const int i = idx / NP, j = idx % NP;
+      const double *src = nullptr;
+      if (i < nt && j < ns) {
+        const int a = i >= kr0, b = j >= kc0;
+        const int ii = a ? i - kr0 : i, jj = b ? j - kc0 : j;
+        const int ka = a ? kr1 : kr0, kb = b ? kc1 : kc0;
+        const int q = a * 2 + b;
+        const int kind = (it.gkind >> (4 * q)) & 15;
+        const int64_t off = it.g_src[q];
+        switch (kind) {
+          case G_BB: src = A.bb_in + off + ii * kb + jj; break;
+          case G_BB_T: src = A.bb_in + off + jj * ka + ii; break;
+          case G_DT: src = A.dt_in + off + ii * kb + jj; break;
+          case G_DT_T: src = A.dt_in + off + jj * ka + ii; break;
+          default: break;
+        }
+      }
+      cp8(&sG[i * LD + j], src ? (const void *)src : any, src != nullptr);
+    }
+  }
+  async_tile<NP, NP, LD>(sQs, A.q_col + A.cs.q_off[s], ns, ns, ns, any);
+}
+
+template <int NP>
 __global__ void __launch_bounds__(PairCfg<NP>::THREADS) pair_kernel(PairArgs A) {
   using C = PairCfg<NP>;
   constexpr int LD = C::LD;
@@ -329,42 +437,16 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS) pair_kernel(PairArgs A) 
   const int nt = A.rs.n[t], ktt = A.rs.k[t];
   const int warp = threadIdx.x >> 5;
   const int m0 = (warp / C::NWN) * 16, n0 = (warp % C::NWN) * C::WN;
-  load_tile<NP, NP, LD>(sQt, A.q_row + A.rs.q_off[t], nt, nt, nt);
   const int64_t lbase = lvl_off_d(A.L, A.level);
+  async_tile<NP, NP, LD>(sQt, A.q_row + A.rs.q_off[t], nt, nt, nt, A.items);
   for (int p = ch.begin; p < ch.end; p++) {
     const PairItem it = A.items[p];
     const int s = it.s;
     const int ns = A.cs.n[s], kss = A.cs.k[s];
     __syncthreads();  // previous pair's epilogue done with sG / sQs
-    if (A.level == 0) {
-      load_tile<NP, NP, LD>(sG, A.close + it.g_src[0], nt, ns, A.B);
-    } else {
-      const int64_t tc1 = lvl_off_d(A.L, A.level - 1) + 2 * (t - lbase);
-      const int64_t sc1 = lvl_off_d(A.L, A.level - 1) + 2 * (s - lbase);
-      const int kr0 = A.rs.k[tc1], kr1 = A.rs.k[tc1 + 1];
-      const int kc0 = A.cs.k[sc1], kc1 = A.cs.k[sc1 + 1];
-      for (int idx = threadIdx.x; idx < NP * NP; idx += blockDim.x) {
-        const int i = idx / NP, j = idx % NP;
-        double v = 0.0;
-        if (i < nt && j < ns) {
-          const int a = i >= kr0, b = j >= kc0;
-          const int ii = a ? i - kr0 : i, jj = b ? j - kc0 : j;
-          const int ka = a ? kr1 : kr0, kb = b ? kc1 : kc0;
-          const int q = a * 2 + b;
-          const int kind = (it.gkind >> (4 * q)) & 15;
-          const int64_t src = it.g_src[q];
-          switch (kind) {
-            case G_BB: v = A.bb_in[src + ii * kb + jj]; break;
-            case G_BB_T: v = A.bb_in[src + jj * ka + ii]; break;
-            case G_DT: v = A.dt_in[src + ii * kb + jj]; break;
-            case G_DT_T: v = A.dt_in[src + jj * ka + ii]; break;
-            default: v = 0.0;
-          }
-        }
-        sG[i * LD + j] = v;
-      }
-    }
-    load_tile<NP, NP, LD>(sQs, A.q_col + A.cs.q_off[s], ns, ns, ns);
+    pair_load_operands<NP>(A, it, t, nt, lbase, sG, sQs);
+    cp_commit();
+    cp_wait_all();
     __syncthreads();
     double acc[C::TM][C::TN][2];
     // T = Q_t^T G
@@ -458,30 +540,32 @@ __global__ void __launch_bounds__(StripCfg<NP, MP>::THREADS) strip_kernel(StripA
   const int k1 = A.sd.k[c1], k2 = A.sd.k[c1 + 1];
   const int warp = threadIdx.x >> 5;
   const int m0 = (warp / C::NWN) * 16, n0 = (warp % C::NWN) * 16;
-  load_tile<NP, NP, C::LDQ>(sQ, A.q + A.sd.q_off[q], n, n, n);
+  async_tile<NP, NP, C::LDQ>(sQ, A.q + A.sd.q_off[q], n, n, n, A.items);
   for (int p = ch.begin; p < ch.end; p++) {
     const StripItem it = A.items[p];
     const int m = it.m;
     __syncthreads();
     for (int idx = threadIdx.x; idx < NP * MP; idx += blockDim.x) {
       const int i = idx / MP, b = idx % MP;
-      double v = 0.0;
+      const double *src = nullptr;
       if (b < m) {
         if (i < k1) {
-          if (it.src[0] >= 0) v = A.y_in[it.src[0] + int64_t(i) * m + b];
+          if (it.src[0] >= 0) src = A.y_in + it.src[0] + int64_t(i) * m + b;
         } else if (i < k1 + k2) {
-          if (it.src[1] >= 0) v = A.y_in[it.src[1] + int64_t(i - k1) * m + b];
+          if (it.src[1] >= 0) src = A.y_in + it.src[1] + int64_t(i - k1) * m + b;
         }
       }
-      sZ[i * C::LDZ + b] = v;
+      cp8(&sZ[i * C::LDZ + b], src ? (const void *)src : (const void *)A.items, src != nullptr);
     }
+    cp_commit();
+    cp_wait_all();
     __syncthreads();
-    // each warp: one 16 x 16 tile of W = 2 x 2 DMMA tiles
-    double acc2[2][2][2];
-    zero_acc(acc2);
+    double acc[2][2][2];
+    zero_acc(acc);
     {
       const int lane = threadIdx.x & 31;
       const int r = lane >> 2, qq = lane & 3;
+#pragma unroll 4
       for (int k0 = 0; k0 < NP; k0 += 4) {
         double a[2], bq[2];
 #pragma unroll
@@ -491,11 +575,11 @@ __global__ void __launch_bounds__(StripCfg<NP, MP>::THREADS) strip_kernel(StripA
 #pragma unroll
         for (int i = 0; i < 2; i++)
 #pragma unroll
-          for (int j = 0; j < 2; j++) dmma(acc2[i][j], a[i], bq[j]);
+          for (int j = 0; j < 2; j++) dmma(acc[i][j], a[i], bq[j]);
       }
     }
     __syncthreads();
-    warp_store<C::LDZ>(sZ, m0, n0, acc2);
+    warp_store<C::LDZ>(sZ, m0, n0, acc);
     __syncthreads();
     const int mq = n - kq;
     if (it.s_dst >= 0) {
@@ -520,17 +604,64 @@ __global__ void __launch_bounds__(StripCfg<NP, MP>::THREADS) strip_kernel(StripA
 }
 
 // --------------------------------------------------------------------------
-// CSR column indices: block row br has m_r rows with identical column pattern.
+// CSR column indices.  A block row (rows [row0, row0 + m_r)) is one contiguous
+// panel of m_r x rowlen entries in s_col, every row carrying the same column
+// pattern: expand the pattern once into shared memory, then stream the panel
+// out with coalesced stores.  Long panels are split over several CTAs.
 // --------------------------------------------------------------------------
+constexpr int CSR_PAT_MAX = 7680;      // pattern entries kept in shared memory (30 KB)
+constexpr int CSR_BLK_MAX = 1024;      // block descriptors staged in shared memory
+
+__device__ __forceinline__ int32_t csr_col_at(const CsrBlock *b, int nblk, int p) {
+  int lo = 0, hi = nblk - 1;  // last block with colpos <= p
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (b[mid].colpos <= p) lo = mid;
+    else hi = mid - 1;
+  }
+  return b[lo].col0 + (p - b[lo].colpos);
+}
+
 __global__ void __launch_bounds__(256) csr_cols_kernel(const CsrBlockRow *__restrict__ rows,
-                                                       const CsrBlock *__restrict__ blks, int32_t *__restrict__ col) {
-  const CsrBlockRow br = rows[blockIdx.x];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int a = warp; a < br.m_r; a += nw) {
-    int32_t *dst = col + br.p_base + int64_t(a) * br.rowlen;
-    for (int j = 0; j < br.nblk; j++) {
-      const CsrBlock b = blks[br.blk_begin + j];
-      for (int e = lane; e < b.m_c; e += 32) dst[b.colpos + e] = b.col0 + e;
+                                                       const CsrBlock *__restrict__ blks, int32_t *__restrict__ col,
+                                                       int splits) {
+  __shared__ int32_t pat[CSR_PAT_MAX];
+  __shared__ CsrBlock sb[CSR_BLK_MAX];
+  const CsrBlockRow br = rows[blockIdx.x / splits];
+  const int part = blockIdx.x % splits;
+  const int rowlen = br.rowlen;
+  const bool blk_smem = br.nblk <= CSR_BLK_MAX;
+  const bool pat_smem = blk_smem && rowlen <= CSR_PAT_MAX;
+  const CsrBlock *b = blks + br.blk_begin;
+  if (blk_smem) {
+    for (int j = threadIdx.x; j < br.nblk; j += blockDim.x) {
+      cp8(&sb[j], &b[j], true);
+      cp8(reinterpret_cast<char *>(&sb[j]) + 8, reinterpret_cast<const char *>(&b[j]) + 8, true);
+    }
+    cp_commit();
+    cp_wait_all();
+    __syncthreads();
+    b = sb;
+  }
+  if (pat_smem) {
+    for (int p = threadIdx.x; p < rowlen; p += blockDim.x) pat[p] = csr_col_at(b, br.nblk, p);
+    __syncthreads();
+  }
+  // this CTA writes whole rows [a0, a1) of the panel
+  const int a0 = int((int64_t(br.m_r) * part) / splits), a1 = int((int64_t(br.m_r) * (part + 1)) / splits);
+  int32_t *dst = col + br.p_base + int64_t(a0) * rowlen;
+  const int64_t total = int64_t(a1 - a0) * rowlen;
+  if (total <= 0) return;
+  if (rowlen >= 256) {
+    // thread t handles positions p = t, t+256, ... of every row (no division in the loop)
+    for (int a = 0; a < a1 - a0; a++) {
+      int32_t *d = dst + int64_t(a) * rowlen;
+      for (int p = threadIdx.x; p < rowlen; p += blockDim.x) d[p] = pat_smem ? pat[p] : csr_col_at(b, br.nblk, p);
+    }
+  } else {
+    for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
+      const int p = int(e % rowlen);
+      dst[e] = pat_smem ? pat[p] : csr_col_at(b, br.nblk, p);
     }
   }
 }
@@ -584,7 +715,9 @@ __global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, int level,
   __shared__ double sQ[64 * 65];
   __shared__ double sv[64];
   const double *Q = q + sd.q_off[cl];
-  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) sQ[(idx / n) * 65 + idx % n] = Q[idx];
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) cp8(&sQ[(idx / n) * 65 + idx % n], Q + idx, true);
+  cp_commit();
+  cp_wait_all();
   int64_t c1 = 0;
   int k1 = 0;
   if (level > 0) {
@@ -662,8 +795,42 @@ static h2sp_status launch_strips(const StripArgs &a, int np, int mp, int64_t nch
   }
 }
 
+// Side streams and events used to overlap the independent chains of one build
+// (QR + couplings of all levels, CSR index expansion) with the congruence
+// chain.  Created once per device; fork/join through events on the caller's
+// stream, so a build stays stream-ordered (and CUDA-graph capturable).
+struct DeviceAux {
+  bool init = false;
+  cudaStream_t side[2];
+  std::vector<cudaEvent_t> ev;
+};
+static DeviceAux g_aux[64];
+
+static h2sp_status get_aux(int L, DeviceAux **out) {
+  int dev = 0;
+  H2SP_CK(cudaGetDevice(&dev));
+  DeviceAux &a = g_aux[dev & 63];
+  if (!a.init) {
+    // s1 (QR / coupling chain, latency-bound, on the critical path of level 1)
+    // gets the highest priority so its CTAs take SM slots as soon as they free
+    // up; s2 (CSR index expansion, bandwidth filler) the lowest.
+    int lo = 0, hi = 0;
+    H2SP_CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    H2SP_CK(cudaStreamCreateWithPriority(&a.side[0], cudaStreamNonBlocking, hi));
+    H2SP_CK(cudaStreamCreateWithPriority(&a.side[1], cudaStreamNonBlocking, lo));
+    a.init = true;
+  }
+  while (int(a.ev.size()) < L + 8) {
+    cudaEvent_t e;
+    H2SP_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    a.ev.push_back(e);
+  }
+  *out = &a;
+  return H2SP_OK;
+}
+
 h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp_outputs *out, unsigned char *ws,
-                         void *stream, int64_t *launches) {
+                         void *stream, int64_t *launches, void *const *events, int64_t n_events) {
   cudaStream_t st = (cudaStream_t)stream;
   const unsigned char *meta = ws;
   const Clusters cl = make_clusters(P, meta);
@@ -679,40 +846,124 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   const double *tr_col = sym ? in->transfer_row : in->transfer_col;
   double *q_col = sym ? out->q_row : out->q_col;
   const int L = P->L;
+  DeviceAux *aux = nullptr;
+  if (h2sp_status e = get_aux(L, &aux)) return e;
+  cudaStream_t s1 = aux->side[0], s2 = aux->side[1];
+  cudaEvent_t ev_fork = aux->ev[0], ev_qr0 = aux->ev[1], ev_csr = aux->ev[2];
+  auto ev_ready = [&](int k) { return aux->ev[3 + k]; };   // QR_k and couplings_{k-1} done
+  // The launch order (and so the index of h2sp_plan_launches / profiling
+  // events) is: per level QR row, QR col, couplings, pairs, row strips,
+  // column strips; then the CSR expansion.  Events 2i / 2i+1 bracket launch i
+  // on the stream it runs on.
   int64_t nl = 0;
+  auto pre = [&](cudaStream_t s, int64_t i) -> h2sp_status {
+    if (events && 2 * i < n_events) H2SP_CK(cudaEventRecord((cudaEvent_t)events[2 * i], s));
+    return H2SP_OK;
+  };
+  auto post = [&](cudaStream_t s, int64_t i) -> h2sp_status {
+    if (events && 2 * i + 1 < n_events) H2SP_CK(cudaEventRecord((cudaEvent_t)events[2 * i + 1], s));
+    return H2SP_OK;
+  };
   static bool qr_attr = false;
   if (!qr_attr) {
-    H2SP_CK(cudaFuncSetAttribute(qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-    H2SP_CK(cudaFuncSetAttribute(coupling_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * 64 * 8));
+    H2SP_CK(cudaFuncSetAttribute(qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(qr_smem_bytes(64, 64))));
+    H2SP_CK(cudaFuncSetAttribute(coupling_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 64 * 64 * 8 + 1024));
     qr_attr = true;
+  }
+  // Launch indices are assigned in the plan's canonical order; precompute them.
+  struct LvlIdx { int64_t qr_row = -1, qr_col = -1, coup = -1, pairs = -1, rstr = -1, cstr = -1; };
+  std::vector<LvlIdx> li(L + 1);
+  int64_t csr_idx = -1;
+  {
+    int64_t c = 0;
+    for (int k = 0; k <= L; k++) {
+      const LevelPlan &lp = P->levels[k];
+      if (lp.np_row > 0) li[k].qr_row = c++;
+      if (!sym && lp.np_col > 0) li[k].qr_col = c++;
+      if (lp.n_coup) li[k].coup = c++;
+      if (lp.n_pairs) li[k].pairs = c++;
+      if (lp.n_rstrips) li[k].rstr = c++;
+      if (lp.n_cstrips) li[k].cstr = c++;
+    }
+    if (P->n_csr_rows) csr_idx = c++;
+    nl = c;
+  }
+  auto qr = [&](int k, cudaStream_t s) -> h2sp_status {
+    const LevelPlan &lp = P->levels[k];
+    const unsigned M = unsigned(int64_t(1) << (L - k));
+    int kmax_r = 0, kmax_c = 0;
+    for (unsigned i = 0; i < M; i++) {
+      kmax_r = std::max(kmax_r, P->k_row[lvl_off_d(L, k) + i]);
+      kmax_c = std::max(kmax_c, P->k_col[lvl_off_d(L, k) + i]);
+    }
+    if (lp.np_row > 0) {
+      if (h2sp_status e = pre(s, li[k].qr_row)) return e;
+      qr_kernel<<<M, 128, qr_smem_bytes(lp.np_row, kmax_r), s>>>(rs, L, k, in->leaf_basis_row, in->transfer_row,
+                                                                 rh_row, out->q_row,
+                                                                 k == 0 ? (const uint64_t *)meta : nullptr, P->magic);
+      H2SP_CK(cudaGetLastError());
+      if (h2sp_status e = post(s, li[k].qr_row)) return e;
+    }
+    if (!sym && lp.np_col > 0) {
+      if (h2sp_status e = pre(s, li[k].qr_col)) return e;
+      qr_kernel<<<M, 128, qr_smem_bytes(lp.np_col, kmax_c), s>>>(cs, L, k, leaf_col, tr_col, rh_col, q_col, nullptr,
+                                                                 P->magic);
+      H2SP_CK(cudaGetLastError());
+      if (h2sp_status e = post(s, li[k].qr_col)) return e;
+    }
+    return H2SP_OK;
+  };
+  auto coupling = [&](int k, cudaStream_t s) -> h2sp_status {
+    const LevelPlan &lp = P->levels[k];
+    if (!lp.n_coup) return H2SP_OK;
+    int kmax = 0;
+    for (int64_t i = 0; i < (int64_t(1) << (L - k)); i++)
+      kmax = std::max(kmax, std::max(P->k_row[lvl_off_d(L, k) + i], P->k_col[lvl_off_d(L, k) + i]));
+    if (h2sp_status e = pre(s, li[k].coup)) return e;
+    const size_t per_warp = size_t(4) * kmax * kmax * 8;
+    const int ipc = int(std::max<size_t>(1, std::min<size_t>(4, (96 * 1024) / std::max<size_t>(per_warp, 1))));
+    coupling_kernel<<<unsigned((lp.n_coup + ipc - 1) / ipc), 32 * ipc, per_warp * ipc, s>>>(
+        (const CouplingItem *)(meta + lp.coup_off), lp.n_coup, kmax, rs, cs, rh_row, rh_col, in->coupling, dt);
+    H2SP_CK(cudaGetLastError());
+    return post(s, li[k].coup);
+  };
+
+  // ---- fork: CSR index expansion on s2 (independent of all values)
+  H2SP_CK(cudaEventRecord(ev_fork, st));
+  H2SP_CK(cudaStreamWaitEvent(s2, ev_fork, 0));
+  if (csr_idx >= 0) {
+    if (h2sp_status e = pre(s2, csr_idx)) return e;
+    if (out->s_rowptr)
+      H2SP_CK(cudaMemcpyAsync(out->s_rowptr, meta + P->rowptr_off, size_t(P->N + 1) * sizeof(int64_t),
+                              cudaMemcpyDeviceToDevice, s2));
+    if (out->s_col) {
+      const int splits = 4;
+      csr_cols_kernel<<<unsigned(P->n_csr_rows * splits), 256, 0, s2>>>(
+          (const CsrBlockRow *)(meta + P->csr_rows_off), (const CsrBlock *)(meta + P->csr_blocks_off), out->s_col,
+          splits);
+      H2SP_CK(cudaGetLastError());
+    }
+    if (h2sp_status e = post(s2, csr_idx)) return e;
+  } else if (out->s_rowptr) {
+    H2SP_CK(cudaMemcpyAsync(out->s_rowptr, meta + P->rowptr_off, size_t(P->N + 1) * sizeof(int64_t),
+                            cudaMemcpyDeviceToDevice, s2));
+  }
+  H2SP_CK(cudaEventRecord(ev_csr, s2));
+  // ---- step (i) at level 0 on the main stream; the rest of the QR chain and
+  //      all couplings on s1, overlapping the level-0 congruence
+  if (h2sp_status e = qr(0, st)) return e;
+  H2SP_CK(cudaEventRecord(ev_qr0, st));
+  H2SP_CK(cudaStreamWaitEvent(s1, ev_qr0, 0));
+  for (int k = 0; k <= L; k++) {
+    if (k < L) {
+      if (h2sp_status e = coupling(k, s1)) return e;
+      if (h2sp_status e = qr(k + 1, s1)) return e;
+      H2SP_CK(cudaEventRecord(ev_ready(k + 1), s1));
+    }
   }
   for (int k = 0; k <= L; k++) {
     const LevelPlan &lp = P->levels[k];
-    const unsigned M = unsigned(int64_t(1) << (L - k));
-    // ---- step (i)
-    if (lp.np_row > 0) {
-      const int n = lp.np_row;
-      size_t smem = size_t(n) * (n + 1) * 8 * 2 + size_t(n) * 8 + 64;
-      qr_kernel<<<M, 128, smem, st>>>(rs, L, k, in->leaf_basis_row, in->transfer_row, rh_row, out->q_row,
-                                      k == 0 ? (const uint64_t *)meta : nullptr, P->magic);
-      H2SP_CK(cudaGetLastError());
-      nl++;
-    }
-    if (!sym && lp.np_col > 0) {
-      const int n = lp.np_col;
-      size_t smem = size_t(n) * (n + 1) * 8 * 2 + size_t(n) * 8 + 64;
-      qr_kernel<<<M, 128, smem, st>>>(cs, L, k, leaf_col, tr_col, rh_col, q_col, nullptr, P->magic);
-      H2SP_CK(cudaGetLastError());
-      nl++;
-    }
-    // ---- couplings of level k
-    if (lp.n_coup) {
-      int kmax = 64;
-      coupling_kernel<<<unsigned(lp.n_coup), 128, size_t(2) * kmax * kmax * 8, st>>>(
-          (const CouplingItem *)(meta + lp.coup_off), rs, cs, rh_row, rh_col, in->coupling, dt);
-      H2SP_CK(cudaGetLastError());
-      nl++;
-    }
+    if (k > 0) H2SP_CK(cudaStreamWaitEvent(st, ev_ready(k), 0));
     // ---- merge + congruence + freeze
     if (lp.n_pairs) {
       PairArgs a;
@@ -733,6 +984,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       a.bb_out = bb;
       a.yr = yr;
       a.yc = yc;
+      if (h2sp_status e = pre(st, li[k].pairs)) return e;
       h2sp_status s;
       switch (pad16(lp.np_pair)) {
         case 16: s = launch_pairs<16>(a, lp.n_pair_chunks, st); break;
@@ -741,7 +993,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
         default: s = launch_pairs<64>(a, lp.n_pair_chunks, st); break;
       }
       if (s != H2SP_OK) return s;
-      nl++;
+      if (h2sp_status e = post(st, li[k].pairs)) return e;
     }
     // ---- strips arriving from level k-1
     if (lp.n_rstrips) {
@@ -755,9 +1007,10 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       a.y_in = yr;
       a.y_out = yr;
       a.s_val = out->s_val;
+      if (h2sp_status e = pre(st, li[k].rstr)) return e;
       h2sp_status s = launch_strips(a, lp.np_rstrip, lp.mp, lp.n_rstrip_chunks, st);
       if (s != H2SP_OK) return s;
-      nl++;
+      if (h2sp_status e = post(st, li[k].rstr)) return e;
     }
     if (lp.n_cstrips) {
       StripArgs a;
@@ -770,22 +1023,15 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       a.y_in = yc;
       a.y_out = yc;
       a.s_val = out->s_val;
+      if (h2sp_status e = pre(st, li[k].cstr)) return e;
       h2sp_status s = launch_strips(a, lp.np_cstrip, lp.mp, lp.n_cstrip_chunks, st);
       if (s != H2SP_OK) return s;
-      nl++;
+      if (h2sp_status e = post(st, li[k].cstr)) return e;
     }
   }
-  if (out->s_rowptr)
-    H2SP_CK(cudaMemcpyAsync(out->s_rowptr, meta + P->rowptr_off, size_t(P->N + 1) * sizeof(int64_t),
-                            cudaMemcpyDeviceToDevice, st));
-  if (P->n_csr_rows) {
-    if (out->s_col) {
-      csr_cols_kernel<<<unsigned(P->n_csr_rows), 256, 0, st>>>((const CsrBlockRow *)(meta + P->csr_rows_off),
-                                                             (const CsrBlock *)(meta + P->csr_blocks_off), out->s_col);
-      H2SP_CK(cudaGetLastError());
-    }
-    nl++;
-  }
+  // ---- join
+  if (L > 0) H2SP_CK(cudaStreamWaitEvent(st, ev_ready(L), 0));
+  H2SP_CK(cudaStreamWaitEvent(st, ev_csr, 0));
   if (launches) *launches = nl;
   return H2SP_OK;
 }

@@ -512,8 +512,10 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
     P->levels.resize(L + 1);
     int levels_active = 0;
     int64_t launches = 0;
-    const int CH = 8;  // items per CTA chunk sharing one rotating cluster
+    // items per CTA chunk sharing one rotating cluster: up to 8 (reuse of the
+    // resident Q), fewer when a level has too few items to fill ~4 CTAs/SM
     auto chunk = [&](const auto &items, auto qof) {
+      const int CH = int(std::max<int64_t>(1, std::min<int64_t>(8, int64_t(items.size()) / (148 * 4))));
       std::vector<Chunk> ch;
       size_t j = 0;
       while (j < items.size()) {
@@ -561,20 +563,92 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
       lp.cstrip_chunks_off = mb.put(cc);
       lp.n_coup = int64_t(coup[k].size());
       lp.coup_off = mb.put(coup[k]);
-      // launches issued by launch_build (kept in sync with kernels.cu)
-      if (npr > 0) launches++;
-      if (!sym && npc > 0) launches++;
-      if (lp.n_coup) launches++;
-      if (lp.n_pairs) launches++;
-      if (lp.n_rstrips) launches++;
-      if (lp.n_cstrips) launches++;
+      // launches issued by launch_build (kept in sync with kernels.cu), with
+      // their algorithmic flops / HBM bytes
+      double qbytes_row = 0, qbytes_col = 0;
+      for (int64_t i = 0; i < M; i++) {
+        qbytes_row += 8.0 * nr[base + i] * nr[base + i];
+        qbytes_col += 8.0 * nc[base + i] * nc[base + i];
+      }
+      auto qr_info = [&](const std::vector<int32_t> &n, const std::vector<int32_t> &kk, int kind) {
+        h2sp_launch_info li{kind, k, 0, 0.0, 0.0};
+        for (int64_t i = 0; i < M; i++) {
+          const int64_t c = base + i;
+          const double nn = n[c], k_ = kk[c];
+          if (nn == 0) continue;
+          li.items++;
+          li.flops += 2 * nn * k_ * k_ + 4 * nn * nn * k_;
+          double in_ = (k == 0) ? double(B) * k_ : nn * k_;
+          if (k > 0) {
+            const int64_t c1 = lvl_off(L, k - 1) + 2 * i;
+            in_ += double(kk[c1]) * kk[c1] + double(kk[c1 + 1]) * kk[c1 + 1];
+          }
+          li.bytes += 8.0 * (in_ + nn * nn + k_ * k_);
+        }
+        return li;
+      };
+      if (npr > 0) {
+        launches++;
+        P->launch_info.push_back(qr_info(nr, kr, 0));
+      }
+      if (!sym && npc > 0) {
+        launches++;
+        P->launch_info.push_back(qr_info(nc, kc, 1));
+      }
+      if (lp.n_coup) {
+        launches++;
+        h2sp_launch_info li{2, k, lp.n_coup, 0.0, 0.0};
+        for (const auto &c : coup[k]) {
+          const double a = kr[c.t], b = kc[c.s];
+          li.flops += 2 * a * b * (a + b);
+          li.bytes += 8.0 * (2 * a * b + a * a + b * b);
+        }
+        P->launch_info.push_back(li);
+      }
+      if (lp.n_pairs) {
+        launches++;
+        h2sp_launch_info li{3, k, lp.n_pairs, 0.0, qbytes_row + (sym ? 0.0 : qbytes_col)};
+        for (const auto &it : pairs[k]) {
+          const double a = nr[it.t], b = nc[it.s];
+          li.flops += 2 * a * b * (a + b);
+          double outb = a * b;  // nn + bb + bn + nb
+          if (it.s_dst_m >= 0) outb += double(nr[it.t] - kr[it.t]) * (nc[it.s] - kc[it.s]);
+          li.bytes += 8.0 * (a * b + outb);
+        }
+        P->launch_info.push_back(li);
+      }
+      auto strip_info = [&](const std::vector<StripItem> &items, const std::vector<int32_t> &n,
+                            const std::vector<int32_t> &kk, int kind, double qb) {
+        h2sp_launch_info li{kind, k, int64_t(items.size()), 0.0, qb};
+        for (const auto &it : items) {
+          const int64_t c1 = lvl_off(L, k - 1) + 2 * (it.q - base);
+          double rows = (it.src[0] >= 0 ? kk[c1] : 0) + (it.src[1] >= 0 ? kk[c1 + 1] : 0);
+          const double nq = n[it.q], kq = kk[it.q], m = it.m;
+          li.flops += 2 * nq * rows * m;
+          double outb = (it.y_dst >= 0 ? kq * m : 0.0) + (it.s_dst >= 0 ? (nq - kq) * m : 0.0) +
+                        (it.s_dst_t >= 0 ? (nq - kq) * m : 0.0);
+          li.bytes += 8.0 * (rows * m + outb);
+        }
+        return li;
+      };
+      if (lp.n_rstrips) {
+        launches++;
+        P->launch_info.push_back(strip_info(rstr[k], nr, kr, 4, qbytes_row));
+      }
+      if (lp.n_cstrips) {
+        launches++;
+        P->launch_info.push_back(strip_info(cstr[k], nc, kc, 5, qbytes_col));
+      }
     }
     P->n_csr_rows = int64_t(csr_rows.size());
     P->n_csr_blocks = int64_t(csr_blocks.size());
     P->csr_rows_off = mb.put(csr_rows);
     P->csr_blocks_off = mb.put(csr_blocks);
     P->rowptr_off = mb.put(rowptr);
-    if (P->n_csr_rows) launches++;  // CSR column expansion (rowptr is a D2D copy)
+    if (P->n_csr_rows) {  // CSR column expansion (+ the rowptr D2D copy)
+      launches++;
+      P->launch_info.push_back(h2sp_launch_info{6, L, P->n_csr_rows, 0.0, 4.0 * double(nnz) + 16.0 * double(P->N + 1)});
+    }
     P->launches = launches;
     P->levels_active = levels_active;
     P->meta_bytes = align_up(mb.buf.size(), 256);
@@ -665,6 +739,14 @@ h2sp_status h2sp_plan_offsets(h2sp_plan P, int64_t *s_off_row, int64_t *s_off_co
     if (n_row) n_row[c] = P->n_row[c];
     if (n_col) n_col[c] = P->n_col[c];
   }
+  return H2SP_OK;
+}
+
+h2sp_status h2sp_plan_launches(h2sp_plan P, h2sp_launch_info *out, int64_t max, int64_t *count) {
+  if (!P || !count) return fail(H2SP_EINVAL, "NULL plan or count");
+  *count = int64_t(P->launch_info.size());
+  if (out)
+    for (int64_t i = 0; i < max && i < *count; i++) out[i] = P->launch_info[i];
   return H2SP_OK;
 }
 

@@ -114,3 +114,26 @@ def test_plan_unsupported_leaf_size():
     with pytest.raises(h2sp.H2spError) as e:
         h2sp.Plan(h2gen.pack(h))
     assert e.value.status == 7
+
+
+@pytest.mark.parametrize("name,make", [c for c in CASES if c[0] in ("cfg1", "rand-sym-1", "rand-gen-2", "fig3-half")],
+                         ids=lambda c: c if isinstance(c, str) else "")
+def test_plan_flops_match_structural_count(name, make):
+    """The plan's algorithmic flop count equals an independent count on the
+    oracle's structure (bench.py's reference arm uses the latter)."""
+    import bench
+    h = make()
+    res = oracle.sparsify(h)
+    plan = h2sp.Plan(h2gen.pack(h))
+    assert plan.sizes["flops"] == pytest.approx(bench._oracle_flops(res, h), rel=1e-12)
+    assert sum(l["flops"] for l in plan.launches()) == pytest.approx(plan.sizes["flops"], rel=1e-12)
+
+
+def test_sparsifier_refuses_without_cuda():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("CUDA present")
+    h = h2gen.random_h2(3, 8, 0, True)
+    plan = h2sp.Plan(h2gen.pack(h))
+    with pytest.raises(RuntimeError):
+        h2sp.Sparsifier(plan, h2gen.pack(h))
