@@ -25,28 +25,44 @@ struct PairItem {
   int32_t gkind;         // 4 x 4 bits (quadrant a*2+b at bits 4*(a*2+b)), level >= 1
   int32_t s_ld;          // row length (elements) of S block row (t@k)
   int32_t s_ld_m;        // row length of S block row (s@k) (mirror, symmetric)
+  int32_t yr_ld;         // leading dimension of the row-strip panel receiving bn
+  int32_t yc_ld;         // leading dimension of the panel receiving nb^T
   int32_t pad_;
   int64_t g_src[4];      // level 0: g_src[0] = offset of C_ts in `close`; else slot offsets
   int64_t s_dst;         // S block (t@k, s@k): element (0,0) in s_val
   int64_t s_dst_m;       // symmetric: S block (s@k, t@k) (transpose), t != s
   int64_t bb_dst;        // H[:k_t, :k_s]      -> bb buffer (k_t x k_s)
-  int64_t yr_dst;        // H[:k_t, k_s:]      -> row strip (k_t x m_s)
-  int64_t yc_dst;        // H[k_t:, :k_s]^T    -> transposed column strip (k_s x m_t);
-                         //                      symmetric: row strip of (s, t)
+  int64_t yr_dst;        // H[:k_t, k_s:]      -> row-strip panel of t (k_t rows, ld yr_ld)
+  int64_t yc_dst;        // H[k_t:, :k_s]^T    -> column-strip panel of s (general) /
+                         //                      row-strip panel of s (symmetric), ld yc_ld
 };
 
-// One strip rotation W = Q_q^T Z (Eq. u1v1): Z stacks the strips of
-// the two children of q (child 2 rows at offset k_c1), width m.  Frozen rows
-// [k_q, n_q) of W go to S (directly and/or transposed), basis rows continue.
-struct StripItem {
+// Strips (Eq. u1v1).  All strips rotated by cluster q at level k
+// are stored as one row-major panel (k_q rows; columns = the frozen groups
+// (l, s), in S column order).  At level k+1 the parent p stacks its children's
+// panels (union of their groups, child 2 rows at offset k_c1) into Z and
+// computes W = Q_p^T Z: rows [k_p, n_p) of W are S row block (p@k+1),
+// columns [0, width) -- contiguous in S --, rows [0, k_p) continue as p's panel.
+struct StripPanel {
   int32_t q;             // rotating cluster (level-major id)
-  int32_t m;             // strip width (frozen size of the fixed cluster)
-  int32_t s_ld;          // row length for the direct S block
-  int32_t s_ld_t;        // row length for the transposed S block
-  int64_t src[2];        // child strip slots (k_c x m), -1 if absent
-  int64_t s_dst;         // S[s_dst + a*s_ld + b]   = W[k_q + a][b]
-  int64_t s_dst_t;       // S[s_dst_t + b*s_ld_t + a] = W[k_q + a][b]
-  int64_t y_dst;         // W[:k_q] -> continuing strip slot (k_q x m)
+  int32_t width;         // columns of W (sum of the group widths)
+  int32_t ld_c1, ld_c2;  // leading dimensions of the children's panels
+  int64_t src_c1, src_c2;  // children's panels (k_c x ld_c), -1 if absent
+  int64_t y_dst;         // W[:k_q] -> y[y_dst + i*y_ld + c], -1 if k_q == 0
+  int64_t s_dst;         // W[k_q + a][c] -> S[s_dst + a*s_ld + c] (direct), -1 if none
+  int32_t y_ld, s_ld;
+  int32_t gbeg, gend;    // groups of this panel in the level's group array
+};
+
+struct StripGroup {      // one frozen group (l, s) of a panel
+  int32_t col0, m;       // columns [col0, col0 + m) of the panel
+  int32_t pos_c1, pos_c2;  // column of the group in the children's panels, -1 if absent
+  int64_t s_dst_t;       // W[k_q + a][col0 + b] -> S[s_dst_t + b*s_ld_t + a] (transposed), -1 if none
+  int32_t s_ld_t, pad_;
+};
+
+struct StripTile {       // columns [c0, c1) of one panel; g0 = first group overlapping c0
+  int32_t panel, c0, c1, g0;
 };
 
 // A run of items that share the rotating cluster (Q kept in shared memory).
@@ -77,12 +93,12 @@ struct LevelPlan {
   int np_row, np_col;    // max n_t at this level (row / column side)
   int mp;                // max strip width at this level
   int64_t n_pairs, n_pair_chunks;
-  int64_t n_rstrips, n_rstrip_chunks;
-  int64_t n_cstrips, n_cstrip_chunks;
+  int64_t n_rstrips, n_rpanels, n_rgroups;    // n_*strips = number of column tiles (launch size)
+  int64_t n_cstrips, n_cpanels, n_cgroups;
   int64_t n_coup;
   size_t pairs_off, pair_chunks_off;          // byte offsets in meta
-  size_t rstrips_off, rstrip_chunks_off;
-  size_t cstrips_off, cstrip_chunks_off;
+  size_t rtiles_off, rpanels_off, rgroups_off;
+  size_t ctiles_off, cpanels_off, cgroups_off;
   size_t coup_off;
   int np_pair;           // padded tile size for the congruence at this level
   int np_rstrip, np_cstrip;

@@ -81,10 +81,10 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-// Warp GEMM on shared-memory tiles with leading dimension LD:
+// Warp GEMM on shared-memory tiles with leading dimensions LDA / LDB:
 //   acc[i][j] (8x8 tile at rows m0+8i, cols n0+8j) += sum_kk A(m, kk) B(kk, n)
-//   A(m, kk) = AT ? sA[kk*LD + m] : sA[m*LD + kk];  B(kk, n) = sB[kk*LD + n].
-template <int LD, int TM, int TN, bool AT>
+//   A(m, kk) = AT ? sA[kk*LDA + m] : sA[m*LDA + kk];  B(kk, n) = sB[kk*LDB + n].
+template <int LDA, int LDB, int TM, int TN, bool AT>
 __device__ __forceinline__ void warp_gemm(const double *__restrict__ sA, const double *__restrict__ sB, int m0,
                                           int n0, int kmax, double (&acc)[TM][TN][2]) {
   const int lane = threadIdx.x & 31;
@@ -93,9 +93,9 @@ __device__ __forceinline__ void warp_gemm(const double *__restrict__ sA, const d
   for (int k0 = 0; k0 < kmax; k0 += 4) {
     double a[TM], b[TN];
 #pragma unroll
-    for (int i = 0; i < TM; i++) a[i] = AT ? sA[(k0 + q) * LD + m0 + i * 8 + r] : sA[(m0 + i * 8 + r) * LD + k0 + q];
+    for (int i = 0; i < TM; i++) a[i] = AT ? sA[(k0 + q) * LDA + m0 + i * 8 + r] : sA[(m0 + i * 8 + r) * LDA + k0 + q];
 #pragma unroll
-    for (int j = 0; j < TN; j++) b[j] = sB[(k0 + q) * LD + n0 + j * 8 + r];
+    for (int j = 0; j < TN; j++) b[j] = sB[(k0 + q) * LDB + n0 + j * 8 + r];
 #pragma unroll
     for (int i = 0; i < TM; i++)
 #pragma unroll
@@ -451,13 +451,13 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS) pair_kernel(PairArgs A) 
     double acc[C::TM][C::TN][2];
     // T = Q_t^T G
     zero_acc(acc);
-    warp_gemm<LD, C::TM, C::TN, true>(sQt, sG, m0, n0, NP, acc);
+    warp_gemm<LD, LD, C::TM, C::TN, true>(sQt, sG, m0, n0, NP, acc);
     __syncthreads();
     warp_store<LD>(sG, m0, n0, acc);
     __syncthreads();
     // H = T Q_s
     zero_acc(acc);
-    warp_gemm<LD, C::TM, C::TN, false>(sG, sQs, m0, n0, NP, acc);
+    warp_gemm<LD, LD, C::TM, C::TN, false>(sG, sQs, m0, n0, NP, acc);
     __syncthreads();
     warp_store<LD>(sG, m0, n0, acc);
     __syncthreads();
@@ -491,34 +491,39 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS) pair_kernel(PairArgs A) 
     if (it.yr_dst >= 0) {
       for (int idx = threadIdx.x; idx < ktt * ms; idx += blockDim.x) {
         const int i = idx / ms, b = idx % ms;
-        A.yr[it.yr_dst + idx] = sG[i * LD + kss + b];
+        A.yr[it.yr_dst + int64_t(i) * it.yr_ld + b] = sG[i * LD + kss + b];
       }
     }
     if (it.yc_dst >= 0) {
       for (int idx = threadIdx.x; idx < kss * mt; idx += blockDim.x) {
         const int j = idx / mt, a = idx % mt;
-        A.yc[it.yc_dst + idx] = sG[(ktt + a) * LD + j];
+        A.yc[it.yc_dst + int64_t(j) * it.yc_ld + a] = sG[(ktt + a) * LD + j];
       }
     }
   }
 }
 
 // --------------------------------------------------------------------------
-// Strips (Eq. u1v1): W = Q_q^T Z, Z = [Y_c1; Y_c2] (n_q x m), Q_q resident.
+// Strips (Eq. u1v1): one CTA per column tile (TN columns) of one
+// rotating cluster's panel.  Z = [Y_c1; Y_c2] is gathered from the children's
+// panels (union of their frozen groups), W = Q_q^T Z on the DMMA pipe, then
+// rows [k_q, n_q) -> S (contiguous row segments, and/or the transposed blocks),
+// rows [0, k_q) -> q's panel for the next level.
 // --------------------------------------------------------------------------
-template <int NP, int MP>
+template <int NP, int TN>
 struct StripCfg {
   static constexpr int LDQ = NP + 4;
-  static constexpr int LDZ = MP + 4;
-  static constexpr int NWM = NP / 16, NWN = MP / 16;
+  static constexpr int LDZ = TN + 4;
+  static constexpr int NWM = NP / 16, NWN = TN / 16;
   static constexpr int WARPS = NWM * NWN;
   static constexpr int THREADS = WARPS * 32;
-  static constexpr size_t SMEM = (size_t(NP) * LDQ + size_t(NP) * LDZ) * sizeof(double);
+  static constexpr size_t SMEM = (size_t(NP) * LDQ + size_t(NP) * LDZ) * sizeof(double) + TN * 16 + 64;
 };
 
 struct StripArgs {
-  const StripItem *items;
-  const Chunk *chunks;
+  const StripTile *tiles;
+  const StripPanel *panels;
+  const StripGroup *groups;
   Side sd;
   int L, level;
   const double *q;
@@ -527,78 +532,84 @@ struct StripArgs {
   double *s_val;
 };
 
-template <int NP, int MP>
-__global__ void __launch_bounds__(StripCfg<NP, MP>::THREADS) strip_kernel(StripArgs A) {
-  using C = StripCfg<NP, MP>;
+template <int NP, int TN>
+__global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS) strip_kernel(StripArgs A) {
+  using C = StripCfg<NP, TN>;
   extern __shared__ __align__(16) double sm[];
-  double *sQ = sm;                 // NP x LDQ
-  double *sZ = sm + NP * C::LDQ;   // NP x LDZ (Z, then W)
-  const Chunk ch = A.chunks[blockIdx.x];
-  const int q = A.items[ch.begin].q;
+  double *sQ = sm;                           // NP x LDQ
+  double *sZ = sm + NP * C::LDQ;             // NP x LDZ (Z, then W)
+  int64_t *tdst = reinterpret_cast<int64_t *>(sZ + NP * C::LDZ);  // per column: transposed S dst (b*ld folded in)
+  int32_t *src1 = reinterpret_cast<int32_t *>(tdst + TN);          // per column: column in child-1 panel or -1
+  int32_t *src2 = src1 + TN;
+  int32_t *tld = reinterpret_cast<int32_t *>(src2 + TN);           // unused padding slot
+  (void)tld;
+  const StripTile tile = A.tiles[blockIdx.x];
+  const StripPanel pn = A.panels[tile.panel];
+  const int q = pn.q;
   const int n = A.sd.n[q], kq = A.sd.k[q];
   const int64_t c1 = lvl_off_d(A.L, A.level - 1) + 2 * (q - lvl_off_d(A.L, A.level));
   const int k1 = A.sd.k[c1], k2 = A.sd.k[c1 + 1];
+  const int ncol = tile.c1 - tile.c0;
+  async_tile<NP, NP, C::LDQ>(sQ, A.q + A.sd.q_off[q], n, n, n, A.tiles);
+  cp_commit();
+  // per-column source / destination maps
+  for (int cc = threadIdx.x; cc < TN; cc += blockDim.x) {
+    int32_t a1 = -1, a2 = -1;
+    int64_t td = -1;
+    if (cc < ncol) {
+      const int c = tile.c0 + cc;
+      int g = tile.g0;
+      while (g + 1 < pn.gend && A.groups[g + 1].col0 <= c) g++;
+      const StripGroup sg = A.groups[g];
+      const int b = c - sg.col0;
+      if (sg.pos_c1 >= 0) a1 = sg.pos_c1 + b;
+      if (sg.pos_c2 >= 0) a2 = sg.pos_c2 + b;
+      if (sg.s_dst_t >= 0) td = sg.s_dst_t + int64_t(b) * sg.s_ld_t;
+    }
+    src1[cc] = a1;
+    src2[cc] = a2;
+    tdst[cc] = td;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < NP * TN; idx += blockDim.x) {
+    const int i = idx / TN, cc = idx % TN;
+    const double *src = nullptr;
+    if (i < k1) {
+      if (src1[cc] >= 0) src = A.y_in + pn.src_c1 + int64_t(i) * pn.ld_c1 + src1[cc];
+    } else if (i < k1 + k2) {
+      if (src2[cc] >= 0) src = A.y_in + pn.src_c2 + int64_t(i - k1) * pn.ld_c2 + src2[cc];
+    }
+    cp8(&sZ[i * C::LDZ + cc], src ? (const void *)src : (const void *)A.tiles, src != nullptr);
+  }
+  cp_commit();
+  cp_wait_all();
+  __syncthreads();
   const int warp = threadIdx.x >> 5;
   const int m0 = (warp / C::NWN) * 16, n0 = (warp % C::NWN) * 16;
-  async_tile<NP, NP, C::LDQ>(sQ, A.q + A.sd.q_off[q], n, n, n, A.items);
-  for (int p = ch.begin; p < ch.end; p++) {
-    const StripItem it = A.items[p];
-    const int m = it.m;
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < NP * MP; idx += blockDim.x) {
-      const int i = idx / MP, b = idx % MP;
-      const double *src = nullptr;
-      if (b < m) {
-        if (i < k1) {
-          if (it.src[0] >= 0) src = A.y_in + it.src[0] + int64_t(i) * m + b;
-        } else if (i < k1 + k2) {
-          if (it.src[1] >= 0) src = A.y_in + it.src[1] + int64_t(i - k1) * m + b;
-        }
-      }
-      cp8(&sZ[i * C::LDZ + b], src ? (const void *)src : (const void *)A.items, src != nullptr);
+  double acc[2][2][2];
+  zero_acc(acc);
+  warp_gemm<C::LDQ, C::LDZ, 2, 2, true>(sQ, sZ, m0, n0, NP, acc);
+  __syncthreads();
+  warp_store<C::LDZ>(sZ, m0, n0, acc);
+  __syncthreads();
+  const int mq = n - kq;
+  if (pn.s_dst >= 0) {
+    for (int idx = threadIdx.x; idx < mq * ncol; idx += blockDim.x) {
+      const int a = idx / ncol, cc = idx % ncol;
+      A.s_val[pn.s_dst + int64_t(a) * pn.s_ld + tile.c0 + cc] = sZ[(kq + a) * C::LDZ + cc];
     }
-    cp_commit();
-    cp_wait_all();
-    __syncthreads();
-    double acc[2][2][2];
-    zero_acc(acc);
-    {
-      const int lane = threadIdx.x & 31;
-      const int r = lane >> 2, qq = lane & 3;
-#pragma unroll 4
-      for (int k0 = 0; k0 < NP; k0 += 4) {
-        double a[2], bq[2];
-#pragma unroll
-        for (int i = 0; i < 2; i++) a[i] = sQ[(k0 + qq) * C::LDQ + m0 + i * 8 + r];
-#pragma unroll
-        for (int j = 0; j < 2; j++) bq[j] = sZ[(k0 + qq) * C::LDZ + n0 + j * 8 + r];
-#pragma unroll
-        for (int i = 0; i < 2; i++)
-#pragma unroll
-          for (int j = 0; j < 2; j++) dmma(acc[i][j], a[i], bq[j]);
-      }
+  }
+  if (pn.y_dst >= 0) {
+    for (int idx = threadIdx.x; idx < kq * ncol; idx += blockDim.x) {
+      const int i = idx / ncol, cc = idx % ncol;
+      A.y_out[pn.y_dst + int64_t(i) * pn.y_ld + tile.c0 + cc] = sZ[i * C::LDZ + cc];
     }
-    __syncthreads();
-    warp_store<C::LDZ>(sZ, m0, n0, acc);
-    __syncthreads();
-    const int mq = n - kq;
-    if (it.s_dst >= 0) {
-      for (int idx = threadIdx.x; idx < mq * m; idx += blockDim.x) {
-        const int a = idx / m, b = idx % m;
-        A.s_val[it.s_dst + int64_t(a) * it.s_ld + b] = sZ[(kq + a) * C::LDZ + b];
-      }
-    }
-    if (it.s_dst_t >= 0) {
-      for (int idx = threadIdx.x; idx < mq * m; idx += blockDim.x) {
-        const int b = idx / mq, a = idx % mq;
-        A.s_val[it.s_dst_t + int64_t(b) * it.s_ld_t + a] = sZ[(kq + a) * C::LDZ + b];
-      }
-    }
-    if (it.y_dst >= 0) {
-      for (int idx = threadIdx.x; idx < kq * m; idx += blockDim.x) {
-        const int i = idx / m, b = idx % m;
-        A.y_out[it.y_dst + idx] = sZ[i * C::LDZ + b];
-      }
+  }
+  if (mq > 0) {
+    for (int idx = threadIdx.x; idx < mq * ncol; idx += blockDim.x) {
+      const int cc = idx / mq, a = idx % mq;
+      const int64_t d = tdst[cc];
+      if (d >= 0) A.s_val[d + a] = sZ[(kq + a) * C::LDZ + cc];
     }
   }
 }
@@ -761,37 +772,29 @@ static h2sp_status launch_pairs(const PairArgs &a, int64_t nchunks, cudaStream_t
   return H2SP_OK;
 }
 
-template <int NP, int MP>
-static h2sp_status launch_strips2(const StripArgs &a, int64_t nchunks, cudaStream_t st) {
-  using C = StripCfg<NP, MP>;
+constexpr int STRIP_TN = 64;  // = plan.cpp STRIP_TN
+
+template <int NP>
+static h2sp_status launch_strips1(const StripArgs &a, int64_t ntiles, cudaStream_t st) {
+  using C = StripCfg<NP, STRIP_TN>;
   static bool attr = false;
   if (!attr) {
-    H2SP_CK(cudaFuncSetAttribute(strip_kernel<NP, MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
+    H2SP_CK(cudaFuncSetAttribute(strip_kernel<NP, STRIP_TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
     attr = true;
   }
-  strip_kernel<NP, MP><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a);
+  strip_kernel<NP, STRIP_TN><<<unsigned(ntiles), C::THREADS, C::SMEM, st>>>(a);
   H2SP_CK(cudaGetLastError());
   return H2SP_OK;
 }
 
 static int pad16(int x) { return x <= 16 ? 16 : x <= 32 ? 32 : x <= 48 ? 48 : 64; }
 
-template <int NP>
-static h2sp_status launch_strips1(const StripArgs &a, int mp, int64_t nchunks, cudaStream_t st) {
-  switch (pad16(mp)) {
-    case 16: return launch_strips2<NP, 16>(a, nchunks, st);
-    case 32: return launch_strips2<NP, 32>(a, nchunks, st);
-    case 48: return launch_strips2<NP, 48>(a, nchunks, st);
-    default: return launch_strips2<NP, 64>(a, nchunks, st);
-  }
-}
-
-static h2sp_status launch_strips(const StripArgs &a, int np, int mp, int64_t nchunks, cudaStream_t st) {
+static h2sp_status launch_strips(const StripArgs &a, int np, int64_t ntiles, cudaStream_t st) {
   switch (pad16(np)) {
-    case 16: return launch_strips1<16>(a, mp, nchunks, st);
-    case 32: return launch_strips1<32>(a, mp, nchunks, st);
-    case 48: return launch_strips1<48>(a, mp, nchunks, st);
-    default: return launch_strips1<64>(a, mp, nchunks, st);
+    case 16: return launch_strips1<16>(a, ntiles, st);
+    case 32: return launch_strips1<32>(a, ntiles, st);
+    case 48: return launch_strips1<48>(a, ntiles, st);
+    default: return launch_strips1<64>(a, ntiles, st);
   }
 }
 
@@ -998,8 +1001,9 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     // ---- strips arriving from level k-1
     if (lp.n_rstrips) {
       StripArgs a;
-      a.items = (const StripItem *)(meta + lp.rstrips_off);
-      a.chunks = (const Chunk *)(meta + lp.rstrip_chunks_off);
+      a.tiles = (const StripTile *)(meta + lp.rtiles_off);
+      a.panels = (const StripPanel *)(meta + lp.rpanels_off);
+      a.groups = (const StripGroup *)(meta + lp.rgroups_off);
       a.sd = rs;
       a.L = L;
       a.level = k;
@@ -1008,14 +1012,15 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       a.y_out = yr;
       a.s_val = out->s_val;
       if (h2sp_status e = pre(st, li[k].rstr)) return e;
-      h2sp_status s = launch_strips(a, lp.np_rstrip, lp.mp, lp.n_rstrip_chunks, st);
+      h2sp_status s = launch_strips(a, lp.np_rstrip, lp.n_rstrips, st);
       if (s != H2SP_OK) return s;
       if (h2sp_status e = post(st, li[k].rstr)) return e;
     }
     if (lp.n_cstrips) {
       StripArgs a;
-      a.items = (const StripItem *)(meta + lp.cstrips_off);
-      a.chunks = (const Chunk *)(meta + lp.cstrip_chunks_off);
+      a.tiles = (const StripTile *)(meta + lp.ctiles_off);
+      a.panels = (const StripPanel *)(meta + lp.cpanels_off);
+      a.groups = (const StripGroup *)(meta + lp.cgroups_off);
       a.sd = cs;
       a.L = L;
       a.level = k;
@@ -1024,7 +1029,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       a.y_out = yc;
       a.s_val = out->s_val;
       if (h2sp_status e = pre(st, li[k].cstr)) return e;
-      h2sp_status s = launch_strips(a, lp.np_cstrip, lp.mp, lp.n_cstrip_chunks, st);
+      h2sp_status s = launch_strips(a, lp.np_cstrip, lp.n_cstrips, st);
       if (s != H2SP_OK) return s;
       if (h2sp_status e = post(st, li[k].cstr)) return e;
     }

@@ -57,10 +57,11 @@ std::vector<uint64_t> read_csr(const int64_t *ptr, const int32_t *col, int64_t M
   return out;
 }
 
-struct StripRec {  // a live strip at some level: rotating cluster c (in-level), fixed group (l, s)
-  int32_t c, l, s;
-  int64_t slot;
+struct Grp {  // a frozen column group (l, s) of a strip panel, at columns [col0, col0 + m)
+  int32_t l, s, m, col0;
 };
+
+constexpr int STRIP_TN = 64;  // columns per strip tile (kernels.cu: strip_kernel TN)
 
 struct BlockRec {
   int64_t roff, coff;
@@ -271,12 +272,16 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
     double flops_qr = 0, flops_coup = 0, flops_cong = 0, flops_strip = 0;
     int64_t dt_len = 0, bb_len = 0, yr_len = 0, yc_len = 0;
     std::vector<std::vector<PairItem>> pairs(L + 1);
-    std::vector<std::vector<StripItem>> rstr(L + 1), cstr(L + 1);
+    std::vector<std::vector<StripPanel>> rpan(L + 1), cpan(L + 1);
+    std::vector<std::vector<StripGroup>> rgrp(L + 1), cgrp(L + 1);
+    std::vector<std::vector<StripTile>> rtil(L + 1), ctil(L + 1);
+    std::vector<std::vector<int64_t>> rgrp_direct(L + 1);   // direct S dst of each row group (checked below)
     std::vector<std::vector<CouplingItem>> coup(L + 1);
     std::vector<std::vector<int64_t>> dt_slot(L + 1), bb_slot(L + 1);
     std::vector<std::vector<int64_t>> pair_index(L + 1);   // near index -> item index (canonical) or -1
     std::vector<BlockRec> blocks;
-    std::vector<StripRec> R_prev, C_prev;
+    std::vector<std::vector<Grp>> R_prev, C_prev;     // groups of each panel at level k-1
+    std::vector<int64_t> Rb_prev, Cb_prev;            // panel bases at level k-1
     for (int k = 0; k <= L; k++) {
       const int64_t base = lvl_off(L, k);
       const int64_t M = int64_t(1) << (L - k);
@@ -358,25 +363,100 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
         pairs[k].push_back(it);
         flops_cong += 2.0 * nr[ct] * nc[cs] * (nr[ct] + nc[cs]);
       }
-      // strips started at this level (from every pair of N_k) and S blocks of pairs
-      std::vector<StripRec> R_cur, C_cur;
+      // ---- strips arriving from level k-1 (Eq. u1v1): one panel per rotating cluster
+      std::vector<std::vector<Grp>> R_cur(M), C_cur(M);
+      auto merge = [&](std::vector<std::vector<Grp>> &prev, std::vector<int64_t> &prev_base, bool row_side,
+                       std::vector<StripPanel> &pans, std::vector<StripGroup> &grps, std::vector<StripTile> &tils,
+                       std::vector<std::vector<Grp>> &cur) {
+        const auto &kq = row_side ? kr : kc;
+        const auto &nq = row_side ? nr : nc;
+        for (int64_t p = 0; p < M; p++) {
+          const auto &A = prev[2 * p], &Bv = prev[2 * p + 1];
+          if (A.empty() && Bv.empty()) continue;
+          const int64_t cq = base + p;
+          const int64_t c1 = lvl_off(L, k - 1) + 2 * p;
+          const int32_t mq = nq[cq] - kq[cq];
+          StripPanel pn{};
+          pn.q = int32_t(cq);
+          pn.ld_c1 = A.empty() ? 0 : A.back().col0 + A.back().m;
+          pn.ld_c2 = Bv.empty() ? 0 : Bv.back().col0 + Bv.back().m;
+          pn.src_c1 = A.empty() ? -1 : prev_base[2 * p];
+          pn.src_c2 = Bv.empty() ? -1 : prev_base[2 * p + 1];
+          pn.y_dst = pn.s_dst = -1;
+          pn.gbeg = int32_t(grps.size());
+          size_t i = 0, j = 0;
+          int32_t col = 0;
+          const int64_t pidx = int64_t(pans.size());
+          while (i < A.size() || j < Bv.size()) {
+            bool takeA, takeB;
+            if (i < A.size() && j < Bv.size()) {
+              const bool eq = A[i].l == Bv[j].l && A[i].s == Bv[j].s;
+              const bool lt = A[i].l < Bv[j].l || (A[i].l == Bv[j].l && A[i].s < Bv[j].s);
+              takeA = eq || lt;
+              takeB = eq || !lt;
+            } else {
+              takeA = i < A.size();
+              takeB = !takeA;
+            }
+            const Grp &g = takeA ? A[i] : Bv[j];
+            StripGroup sg{};
+            sg.col0 = col;
+            sg.m = g.m;
+            sg.pos_c1 = takeA ? A[i].col0 : -1;
+            sg.pos_c2 = takeB ? Bv[j].col0 : -1;
+            sg.s_dst_t = -1;
+            const int64_t gi = int64_t(grps.size());
+            const int64_t cf = lvl_off(L, g.l) + g.s;  // fixed cluster
+            if (mq > 0) {
+              if (row_side) {
+                blocks.push_back(BlockRec{P->s_off_row[cq], P->s_off_col[cf], mq, g.m, 2, k, gi});
+                if (sym) blocks.push_back(BlockRec{P->s_off_row[cf], P->s_off_col[cq], g.m, mq, 3, k, gi});
+              } else {
+                blocks.push_back(BlockRec{P->s_off_row[cf], P->s_off_col[cq], g.m, mq, 4, k, gi});
+              }
+            }
+            const double rows = (takeA ? kq[c1] : 0) + (takeB ? kq[c1 + 1] : 0);
+            flops_strip += 2.0 * nq[cq] * rows * g.m;
+            grps.push_back(sg);
+            if (kq[cq] > 0) cur[p].push_back(Grp{g.l, g.s, g.m, col});
+            col += g.m;
+            if (takeA) i++;
+            if (takeB) j++;
+          }
+          pn.width = col;
+          pn.gend = int32_t(grps.size());
+          for (int32_t c0 = 0; c0 < col; c0 += STRIP_TN) {
+            int32_t g0 = pn.gbeg;
+            while (g0 + 1 < pn.gend && grps[g0 + 1].col0 <= c0) g0++;
+            tils.push_back(StripTile{int32_t(pidx), c0, std::min(col, c0 + STRIP_TN), g0});
+          }
+          pans.push_back(pn);
+        }
+      };
+      if (k > 0) {
+        merge(R_prev, Rb_prev, true, rpan[k], rgrp[k], rtil[k], R_cur);
+        if (!sym) merge(C_prev, Cb_prev, false, cpan[k], cgrp[k], ctil[k], C_cur);
+      }
+      // ---- strips started at this level (from every pair of N_k) and S blocks of pairs
+      struct NewStrip { int64_t item; int which; int64_t c; int32_t col0; };  // which: 0 yr, 1 yc
+      std::vector<NewStrip> newr, newc;
       for (size_t j = 0; j < Nk.size(); j++) {
         int32_t t = kt(Nk[j]), s = ks(Nk[j]);
         int64_t ct = base + t, cs = base + s;
         bool canon = !sym || t <= s;
         int64_t item = canon ? pair_index[k][j] : pair_index[k][find(Nk, pkey(s, t))];
         if (kr[ct] > 0 && mc(cs) > 0) {
-          int64_t slot = yr_len;
-          yr_len += int64_t(kr[ct]) * mc(cs);
-          R_cur.push_back(StripRec{t, k, s, slot});
-          if (canon) pairs[k][item].yr_dst = slot;
-          else pairs[k][item].yc_dst = slot;  // H_ts = H_st^T: row strip of (t,s) = (nb part of H_st)^T
+          auto &lst = R_cur[t];
+          const int32_t col0 = lst.empty() ? 0 : lst.back().col0 + lst.back().m;
+          lst.push_back(Grp{k, s, mc(cs), col0});
+          // H_ts = H_st^T when t > s (symmetric): row strip of (t,s) = (nb part of H_st)^T
+          newr.push_back(NewStrip{item, canon ? 0 : 1, t, col0});
         }
         if (!sym && mr(ct) > 0 && kc[cs] > 0) {
-          int64_t slot = yc_len;
-          yc_len += int64_t(kc[cs]) * mr(ct);
-          C_cur.push_back(StripRec{s, k, t, slot});  // transposed column strip: rotating cluster s
-          pairs[k][item].yc_dst = slot;
+          auto &lst = C_cur[s];
+          const int32_t col0 = lst.empty() ? 0 : lst.back().col0 + lst.back().m;
+          lst.push_back(Grp{k, t, mr(ct), col0});
+          newc.push_back(NewStrip{item, 1, s, col0});
         }
         if (canon && mr(ct) > 0 && mc(cs) > 0) {
           blocks.push_back(BlockRec{P->s_off_row[ct], P->s_off_col[cs], mr(ct), mc(cs), 0, k, item});
@@ -384,60 +464,48 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
             blocks.push_back(BlockRec{P->s_off_row[cs], P->s_off_col[ct], mc(cs), mr(ct), 1, k, item});
         }
       }
-      // strips arriving from level k-1 (Eq. u1v1)
-      auto merge = [&](std::vector<StripRec> &prev, bool row_side, std::vector<StripItem> &items,
-                       std::vector<StripRec> &cur, int64_t &ylen) {
-        std::sort(prev.begin(), prev.end(), [](const StripRec &a, const StripRec &b) {
-          if (a.c / 2 != b.c / 2) return a.c / 2 < b.c / 2;
-          if (a.l != b.l) return a.l < b.l;
-          if (a.s != b.s) return a.s < b.s;
-          return a.c < b.c;
-        });
-        const auto &kq = row_side ? kr : kc;
-        const auto &nq = row_side ? nr : nc;
-        for (size_t j = 0; j < prev.size();) {
-          size_t e = j + 1;
-          while (e < prev.size() && prev[e].c / 2 == prev[j].c / 2 && prev[e].l == prev[j].l && prev[e].s == prev[j].s)
-            e++;
-          int32_t p = prev[j].c / 2, l = prev[j].l, s = prev[j].s;
-          int64_t cq = base + p, cf = lvl_off(L, l) + s;  // rotating / fixed cluster
-          int32_t m = row_side ? mc(cf) : mr(cf);
-          StripItem it{};
-          it.q = int32_t(cq);
-          it.m = m;
-          it.src[0] = it.src[1] = -1;
-          it.s_dst = it.s_dst_t = it.y_dst = -1;
-          double rows_present = 0;
-          for (size_t x = j; x < e; x++) {
-            it.src[prev[x].c % 2] = prev[x].slot;
-            rows_present += kq[lvl_off(L, k - 1) + prev[x].c];
-          }
-          int64_t idx = int64_t(items.size());
-          int32_t mq = nq[cq] - kq[cq];
-          if (mq > 0) {
-            if (row_side) {
-              blocks.push_back(BlockRec{P->s_off_row[cq], P->s_off_col[cf], mq, m, 2, k, idx});
-              if (sym) blocks.push_back(BlockRec{P->s_off_row[cf], P->s_off_col[cq], m, mq, 3, k, idx});
-            } else {
-              blocks.push_back(BlockRec{P->s_off_row[cf], P->s_off_col[cq], m, mq, 4, k, idx});
-            }
-          }
-          if (kq[cq] > 0) {
-            it.y_dst = ylen;
-            cur.push_back(StripRec{p, l, s, ylen});
-            ylen += int64_t(kq[cq]) * m;
-          }
-          flops_strip += 2.0 * nq[cq] * rows_present * m;
-          items.push_back(it);
-          j = e;
+      // ---- panel bases of level k, and the destinations that point into them
+      auto bases = [&](std::vector<std::vector<Grp>> &cur, const std::vector<int32_t> &kq, int64_t &ylen) {
+        std::vector<int64_t> b(M, -1);
+        for (int64_t c = 0; c < M; c++) {
+          if (cur[c].empty()) continue;
+          b[c] = ylen;
+          ylen += int64_t(kq[base + c]) * (cur[c].back().col0 + cur[c].back().m);
         }
+        return b;
       };
-      if (k > 0) {
-        merge(R_prev, true, rstr[k], R_cur, yr_len);
-        if (!sym) merge(C_prev, false, cstr[k], C_cur, yc_len);
+      std::vector<int64_t> Rb = bases(R_cur, kr, yr_len);
+      std::vector<int64_t> Cb = sym ? std::vector<int64_t>(M, -1) : bases(C_cur, kc, yc_len);
+      auto width = [](const std::vector<Grp> &g) { return g.empty() ? 0 : g.back().col0 + g.back().m; };
+      for (const NewStrip &ns : newr) {
+        PairItem &it = pairs[k][ns.item];
+        if (ns.which == 0) {
+          it.yr_dst = Rb[ns.c] + ns.col0;
+          it.yr_ld = width(R_cur[ns.c]);
+        } else {
+          it.yc_dst = Rb[ns.c] + ns.col0;
+          it.yc_ld = width(R_cur[ns.c]);
+        }
       }
+      for (const NewStrip &ns : newc) {
+        PairItem &it = pairs[k][ns.item];
+        it.yc_dst = Cb[ns.c] + ns.col0;
+        it.yc_ld = width(C_cur[ns.c]);
+      }
+      for (auto &pn : rpan[k])
+        if (kr[pn.q] > 0) {
+          pn.y_dst = Rb[pn.q - base];
+          pn.y_ld = width(R_cur[pn.q - base]);
+        }
+      for (auto &pn : cpan[k])
+        if (kc[pn.q] > 0) {
+          pn.y_dst = Cb[pn.q - base];
+          pn.y_ld = width(C_cur[pn.q - base]);
+        }
       R_prev.swap(R_cur);
       C_prev.swap(C_cur);
+      Rb_prev.swap(Rb);
+      Cb_prev.swap(Cb);
     }
 
     // ---------------------------------------------------------------- S pattern, CSR
@@ -472,9 +540,12 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
           switch (b.kind) {
             case 0: pairs[b.level][b.idx].s_dst = dst; pairs[b.level][b.idx].s_ld = int32_t(rowlen); break;
             case 1: pairs[b.level][b.idx].s_dst_m = dst; pairs[b.level][b.idx].s_ld_m = int32_t(rowlen); break;
-            case 2: rstr[b.level][b.idx].s_dst = dst; rstr[b.level][b.idx].s_ld = int32_t(rowlen); break;
-            case 3: rstr[b.level][b.idx].s_dst_t = dst; rstr[b.level][b.idx].s_ld_t = int32_t(rowlen); break;
-            case 4: cstr[b.level][b.idx].s_dst_t = dst; cstr[b.level][b.idx].s_ld_t = int32_t(rowlen); break;
+            case 2:
+              if (rgrp_direct[b.level].empty()) rgrp_direct[b.level].assign(rgrp[b.level].size(), -1);
+              rgrp_direct[b.level][b.idx] = dst;
+              break;
+            case 3: rgrp[b.level][b.idx].s_dst_t = dst; rgrp[b.level][b.idx].s_ld_t = int32_t(rowlen); break;
+            case 4: cgrp[b.level][b.idx].s_dst_t = dst; cgrp[b.level][b.idx].s_ld_t = int32_t(rowlen); break;
           }
           colpos += b.mc;
         }
@@ -487,6 +558,21 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
     }
     P->s_nnz = nnz;
     P->s_blocks = int64_t(blocks.size());
+    // direct strip output of a panel: its groups are the first blocks of S row
+    // block (q@k), so they must be contiguous from the row start
+    for (int k = 1; k <= L; k++)
+      for (auto &pn : rpan[k]) {
+        const int32_t mq = nr[pn.q] - kr[pn.q];
+        if (mq == 0 || pn.gend == pn.gbeg) continue;
+        const int64_t d0 = rgrp_direct[k][pn.gbeg];
+        const int64_t r0 = P->s_off_row[pn.q];
+        if (d0 != rowptr[r0]) throw PlanError(H2SP_ETREE, "internal: strip panel not at the start of its S row");
+        for (int32_t g = pn.gbeg; g < pn.gend; g++)
+          if (rgrp_direct[k][g] != d0 + rgrp[k][g].col0)
+            throw PlanError(H2SP_ETREE, "internal: strip panel not contiguous in S");
+        pn.s_dst = d0;
+        pn.s_ld = int32_t(rowptr[r0 + 1] - rowptr[r0]);
+      }
 
     // ---------------------------------------------------------------- meta image
     MetaBuilder mb;
@@ -539,10 +625,7 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
       lp.np_row = npr;
       lp.np_col = npc;
       if (npr > 0 || npc > 0) levels_active++;
-      int mp = 0;
-      for (auto &s : rstr[k]) mp = std::max(mp, int(s.m));
-      for (auto &s : cstr[k]) mp = std::max(mp, int(s.m));
-      lp.mp = mp;
+      lp.mp = STRIP_TN;
       lp.np_pair = round8(std::max(npr, npc));
       lp.np_rstrip = round8(npr);
       lp.np_cstrip = round8(npc);
@@ -551,16 +634,18 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
       auto pc = chunk(pairs[k], [](const PairItem &x) { return x.t; });
       lp.n_pair_chunks = int64_t(pc.size());
       lp.pair_chunks_off = mb.put(pc);
-      lp.n_rstrips = int64_t(rstr[k].size());
-      lp.rstrips_off = mb.put(rstr[k]);
-      auto rc = chunk(rstr[k], [](const StripItem &x) { return x.q; });
-      lp.n_rstrip_chunks = int64_t(rc.size());
-      lp.rstrip_chunks_off = mb.put(rc);
-      lp.n_cstrips = int64_t(cstr[k].size());
-      lp.cstrips_off = mb.put(cstr[k]);
-      auto cc = chunk(cstr[k], [](const StripItem &x) { return x.q; });
-      lp.n_cstrip_chunks = int64_t(cc.size());
-      lp.cstrip_chunks_off = mb.put(cc);
+      lp.n_rstrips = int64_t(rtil[k].size());
+      lp.n_rpanels = int64_t(rpan[k].size());
+      lp.n_rgroups = int64_t(rgrp[k].size());
+      lp.rtiles_off = mb.put(rtil[k]);
+      lp.rpanels_off = mb.put(rpan[k]);
+      lp.rgroups_off = mb.put(rgrp[k]);
+      lp.n_cstrips = int64_t(ctil[k].size());
+      lp.n_cpanels = int64_t(cpan[k].size());
+      lp.n_cgroups = int64_t(cgrp[k].size());
+      lp.ctiles_off = mb.put(ctil[k]);
+      lp.cpanels_off = mb.put(cpan[k]);
+      lp.cgroups_off = mb.put(cgrp[k]);
       lp.n_coup = int64_t(coup[k].size());
       lp.coup_off = mb.put(coup[k]);
       // launches issued by launch_build (kept in sync with kernels.cu), with
@@ -617,27 +702,32 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
         }
         P->launch_info.push_back(li);
       }
-      auto strip_info = [&](const std::vector<StripItem> &items, const std::vector<int32_t> &n,
+      auto strip_info = [&](const std::vector<StripPanel> &pans, const std::vector<StripGroup> &grps,
+                            const std::vector<StripTile> &tils, const std::vector<int32_t> &n,
                             const std::vector<int32_t> &kk, int kind, double qb) {
-        h2sp_launch_info li{kind, k, int64_t(items.size()), 0.0, qb};
-        for (const auto &it : items) {
-          const int64_t c1 = lvl_off(L, k - 1) + 2 * (it.q - base);
-          double rows = (it.src[0] >= 0 ? kk[c1] : 0) + (it.src[1] >= 0 ? kk[c1 + 1] : 0);
-          const double nq = n[it.q], kq = kk[it.q], m = it.m;
-          li.flops += 2 * nq * rows * m;
-          double outb = (it.y_dst >= 0 ? kq * m : 0.0) + (it.s_dst >= 0 ? (nq - kq) * m : 0.0) +
-                        (it.s_dst_t >= 0 ? (nq - kq) * m : 0.0);
-          li.bytes += 8.0 * (rows * m + outb);
+        h2sp_launch_info li{kind, k, int64_t(tils.size()), 0.0, qb};
+        for (const auto &pn : pans) {
+          const int64_t c1 = lvl_off(L, k - 1) + 2 * (pn.q - base);
+          const double nq = n[pn.q], kq = kk[pn.q];
+          for (int32_t g = pn.gbeg; g < pn.gend; g++) {
+            const StripGroup &sg = grps[g];
+            const double rows = (sg.pos_c1 >= 0 ? kk[c1] : 0) + (sg.pos_c2 >= 0 ? kk[c1 + 1] : 0);
+            const double m = sg.m;
+            li.flops += 2 * nq * rows * m;
+            const double outb = (pn.y_dst >= 0 ? kq * m : 0.0) + (pn.s_dst >= 0 ? (nq - kq) * m : 0.0) +
+                                (sg.s_dst_t >= 0 ? (nq - kq) * m : 0.0);
+            li.bytes += 8.0 * (rows * m + outb);
+          }
         }
         return li;
       };
       if (lp.n_rstrips) {
         launches++;
-        P->launch_info.push_back(strip_info(rstr[k], nr, kr, 4, qbytes_row));
+        P->launch_info.push_back(strip_info(rpan[k], rgrp[k], rtil[k], nr, kr, 4, qbytes_row));
       }
       if (lp.n_cstrips) {
         launches++;
-        P->launch_info.push_back(strip_info(cstr[k], nc, kc, 5, qbytes_col));
+        P->launch_info.push_back(strip_info(cpan[k], cgrp[k], ctil[k], nc, kc, 5, qbytes_col));
       }
     }
     P->n_csr_rows = int64_t(csr_rows.size());
