@@ -262,8 +262,7 @@ def main():
     x = torch.empty_like(b)
     aws = sp.apply_ws(nrhs)
     offs = plan.offsets()
-    n_apply_launch = 2 * sum(1 for k in range(plan.L + 1)
-                             if offs["n_row"][h2gen.lvl_off(plan.L, k):h2gen.lvl_off(plan.L, k) + (1 << (plan.L - k))].max() > 0)
+    n_apply_launch = 2   # one fused kernel per direction (apply_ut_kernel, apply_v_kernel)
     apply_flops = 2 * 2.0 * nrhs * float(np.sum(offs["n_row"].astype(float) ** 2))
     step_flops = plan.sizes["flops"] + apply_flops
     stream = torch.cuda.current_stream()

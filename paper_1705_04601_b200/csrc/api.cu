@@ -109,7 +109,8 @@ h2sp_status h2sp_build_host(h2sp_plan P, const h2sp_inputs *hi, const h2sp_outpu
 int64_t h2sp_apply_ws_bytes(h2sp_plan P, int nrhs) {
   if (!P || nrhs < 0) return -1;
   int64_t z = P->zb_row_len > P->zb_col_len ? P->zb_row_len : P->zb_col_len;
-  return int64_t(P->meta_bytes) + z * int64_t(nrhs) * 8;
+  // meta | basis coefficients (256-aligned) | arrival counters of the upward pass
+  return int64_t(P->meta_bytes) + (z * int64_t(nrhs) * 8 + 255) / 256 * 256 + P->ncl * 4;
 }
 
 static h2sp_status apply_common(h2sp_plan P, const double *q, const void *a, int64_t lda, void *b, int64_t ldb,

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "h2sp_internal.h"
@@ -134,184 +135,437 @@ __device__ __forceinline__ void cp8(void *sdst, const void *gsrc, bool valid) {
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+__device__ __forceinline__ void cp16(void *sdst, const void *gsrc) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+
 // Asynchronously load an n x m row-major global block (leading dim ldg) into a
-// padded NR x NC shared tile with leading dimension LD, zero fill.  `any` is a
-// valid global address used for the zero-filled (not read) copies.
+// padded NR x NC shared tile with leading dimension LD, zero fill.  Pairs of
+// columns move as one 16-byte copy when the global block is 16-byte aligned.
+// `any` is a valid global address used for the zero-filled (not read) copies.
 template <int NR, int NC, int LD>
 __device__ __forceinline__ void async_tile(double *s, const double *__restrict__ g, int n, int m, int64_t ldg,
                                            const void *any) {
-  for (int idx = threadIdx.x; idx < NR * NC; idx += blockDim.x) {
-    const int i = idx / NC, j = idx % NC;
-    const bool v = i < n && j < m;
-    cp8(&s[i * LD + j], v ? (const void *)(g + int64_t(i) * ldg + j) : any, v);
+  static_assert(NC % 2 == 0 && LD % 2 == 0, "paired columns");
+  const bool al = ((reinterpret_cast<uintptr_t>(g) | uintptr_t(ldg * 8)) & 15) == 0;
+  for (int idx = threadIdx.x; idx < NR * NC / 2; idx += blockDim.x) {
+    const int i = idx / (NC / 2), j = 2 * (idx % (NC / 2));
+    const bool v0 = i < n && j < m, v1 = i < n && j + 1 < m;
+    const double *src = g + int64_t(i) * ldg + j;
+    if (al && v0 && v1) {
+      cp16(&s[i * LD + j], src);
+    } else {
+      cp8(&s[i * LD + j], v0 ? (const void *)src : any, v0);
+      cp8(&s[i * LD + j + 1], v1 ? (const void *)(src + 1) : any, v1);
+    }
   }
 }
 
 // --------------------------------------------------------------------------
-// Step (i): QR completion (convention H, readings 1-2).
-// One CTA per cluster of the level; 128 threads.
+// Step (i): QR completion (convention H, readings 1-2), one WARP per
+// cluster (no block-level synchronisation):
 //   X = R_leaf (level 0) or [R^_c1 T[:k1]; R^_c2 T[k1:]] (internal)
 //   Householder on X (alpha = x_0, sigma = ||x_1:||; sigma == 0 -> tau = 0;
 //   beta = -sgn(alpha) hypot(alpha, sigma), sgn(+-0) = +1), R^ = triu(X[:k]),
-//   Q = H_0 ... H_{k-1} = I - V T V^T (compact WY form of the same product,
-//   T from the dlarft recurrence), written straight to global memory.
-// Shared memory: X/V (n x (k+1)) | stage T (n x k) | R^ children / M (n x n) | T (k x k) | Gv (k x k)
+//   Q = H_0 ... H_{k-1} = I - V T V^T: the compact WY form of the same product
+//   (T from the dlarft recurrence over V^T V), the three products V^T V, T V^T
+//   and V (T V^T) on the DMMA pipe, Q written from the accumulators.
+// Per-warp shared memory (doubles): X n x (k+1) | T K8 x LDT | G/M K4 x LDM | R^ staging
 // --------------------------------------------------------------------------
-__host__ __device__ inline size_t qr_smem_bytes(int n, int k) {
-  return sizeof(double) * (size_t(n) * (k + 1) + size_t(n) * k + size_t(n) * n + 2 * size_t(k) * k + 8);
+__host__ __device__ inline int rup(int x, int m) { return (x + m - 1) / m * m; }
+__host__ __device__ inline int qr_ldt(int k) { return rup(rup(k, 4), 16) + 4; }
+__host__ __device__ inline int qr_ldm(int n) { return rup(rup(n, 8), 16) + 4; }
+__host__ __device__ inline int qr_warp_doubles(int n, int k, int rstage) {
+  const int K4 = rup(k, 4), K8 = rup(k, 8);
+  const int mm = K4 * qr_ldm(n) > K8 * K8 ? K4 * qr_ldm(n) : K8 * K8;
+  const int stg = n * k > mm ? n * k : mm;   // transfer staging aliases G/M
+  return n * (k + 1) + K8 * qr_ldt(k) + stg + rstage + 2;
 }
 
-__global__ void __launch_bounds__(128) qr_kernel(Side sd, int L, int level, const double *__restrict__ leaf,
-                                                 const double *__restrict__ transfer, double *__restrict__ rh,
-                                                 double *__restrict__ qout, const uint64_t *meta_magic,
-                                                 uint64_t magic) {
+__global__ void __launch_bounds__(128) qr_kernel(Side sd, int L, int level, int nclust, int per_warp,
+                                                 const double *__restrict__ leaf, const double *__restrict__ transfer,
+                                                 double *__restrict__ rh, double *__restrict__ qout,
+                                                 const uint64_t *meta_magic, uint64_t magic) {
   if (meta_magic && threadIdx.x == 0 && blockIdx.x == 0 && *meta_magic != magic) __trap();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ci = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (ci >= nclust) return;
   const int64_t base = lvl_off_d(L, level);
-  const int64_t cl = base + blockIdx.x;
+  const int64_t cl = base + ci;
   const int n = sd.n[cl], k = sd.k[cl];
   if (n == 0) return;
+  double *Qg = qout + sd.q_off[cl];
+  if (k == 0) {
+    for (int idx = lane; idx < n * n; idx += 32) Qg[idx] = (idx / n == idx % n) ? 1.0 : 0.0;
+    return;
+  }
   extern __shared__ __align__(16) double sm[];
-  const int ldx = k + 1;
-  double *X = sm;                    // n x ldx
-  double *stg = X + n * ldx;         // n x k: transfer T
-  double *sR = stg + n * k;          // n x n: R^_c1, R^_c2 staging; later M = T_wy V^T (k x n)
-  double *Tw = sR + n * n;           // k x k   (WY T factor)
-  double *Gv = Tw + k * k;           // k x k   (V^T V)
-  double *Mk = sR;
-  __shared__ double s_scal[3];
-  __shared__ double s_tau[64];
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
+  const int K4 = rup(k, 4), K8 = rup(k, 8), N4 = rup(n, 4), N8 = rup(n, 8);
+  const int LDX = k + 1, LDT = qr_ldt(k), LDM = qr_ldm(n);
+  double *X = sm + size_t(warp) * per_warp;
+  double *Tw = X + n * LDX;                  // K8 x LDT
+  double *Mm = Tw + K8 * LDT;                // G = V^T V (K8 x K8), then M = T V^T (K4 x LDM); T staging
+  const int mm = K4 * LDM > K8 * K8 ? K4 * LDM : K8 * K8;
+  double *RS = Mm + (n * k > mm ? n * k : mm);   // children R^ staging (level >= 1)
+  for (int idx = lane; idx < K8 * LDT; idx += 32) Tw[idx] = 0.0;
   // ---- load X
   if (level == 0) {
     const double *R = leaf + sd.leaf_off[cl];
-    for (int idx = tid; idx < n * k; idx += blockDim.x) cp8(&X[(idx / k) * ldx + idx % k], R + idx, true);
+    for (int idx = lane; idx < n * k; idx += 32) cp8(&X[(idx / k) * LDX + idx % k], R + idx, true);
     cp_commit();
     cp_wait_all();
-    __syncthreads();
-  } else if (k > 0) {
-    const int64_t ci = cl - base;
+    __syncwarp();
+  } else {
     const int64_t c1 = lvl_off_d(L, level - 1) + 2 * ci, c2 = c1 + 1;
     const int k1 = sd.k[c1], k2 = sd.k[c2];
     const double *T = transfer + sd.tr_off[cl];  // n x k
-    double *sR1 = sR, *sR2 = sR + k1 * k1;
+    double *sT = Mm, *sR1 = RS, *sR2 = RS + k1 * k1;
     const double *R1 = rh + sd.rh_off[c1];
     const double *R2 = rh + sd.rh_off[c2];
-    for (int idx = tid; idx < n * k; idx += blockDim.x) cp8(&stg[idx], T + idx, true);
-    for (int idx = tid; idx < k1 * k1; idx += blockDim.x) cp8(&sR1[idx], R1 + idx, true);
-    for (int idx = tid; idx < k2 * k2; idx += blockDim.x) cp8(&sR2[idx], R2 + idx, true);
+    for (int idx = lane; idx < n * k; idx += 32) cp8(&sT[idx], T + idx, true);
+    for (int idx = lane; idx < k1 * k1; idx += 32) cp8(&sR1[idx], R1 + idx, true);
+    for (int idx = lane; idx < k2 * k2; idx += 32) cp8(&sR2[idx], R2 + idx, true);
     cp_commit();
     cp_wait_all();
-    __syncthreads();
-    for (int idx = tid; idx < n * k; idx += blockDim.x) {
+    __syncwarp();
+    for (int idx = lane; idx < n * k; idx += 32) {
       const int i = idx / k, j = idx % k;
       double acc = 0.0;
       if (i < k1) {
-        for (int l = i; l < k1; l++) acc = fma(sR1[i * k1 + l], stg[l * k + j], acc);
+        for (int l = i; l < k1; l++) acc = fma(sR1[i * k1 + l], sT[l * k + j], acc);
       } else {
         const int ii = i - k1;
-        for (int l = ii; l < k2; l++) acc = fma(sR2[ii * k2 + l], stg[(k1 + l) * k + j], acc);
+        for (int l = ii; l < k2; l++) acc = fma(sR2[ii * k2 + l], sT[(k1 + l) * k + j], acc);
       }
-      X[i * ldx + j] = acc;
+      X[i * LDX + j] = acc;
     }
-    __syncthreads();
+    __syncwarp();
   }
-  // ---- Householder factorisation (reflectors stored below the diagonal, v_j[0] = 1 implicit)
+  // ---- Householder factorisation; tau_j kept on the diagonal of T
   for (int j = 0; j < k; j++) {
-    if (warp == 0) {
-      double ss = 0.0;
-      for (int i = j + 1 + lane; i < n; i += 32) ss = fma(X[i * ldx + j], X[i * ldx + j], ss);
+    double ss = 0.0;
+    for (int i = j + 1 + lane; i < n; i += 32) ss = fma(X[i * LDX + j], X[i * LDX + j], ss);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-      if (lane == 0) {
-        const double alpha = X[j * ldx + j];
-        const double sigma = sqrt(ss);
-        double beta, t;
-        if (sigma == 0.0) {
-          t = 0.0;
-          beta = alpha;
-        } else {
-          const double sgn = alpha < 0.0 ? -1.0 : 1.0;
-          beta = -sgn * hypot(alpha, sigma);
-          t = (beta - alpha) / beta;
-        }
-        s_scal[0] = beta;
-        s_scal[1] = t;
-        s_scal[2] = alpha - beta;
-        s_tau[j] = t;
-      }
-    }
-    __syncthreads();
-    const double t = s_scal[1];
-    if (t != 0.0) {
-      const double div = s_scal[2];
-      for (int i = j + 1 + tid; i < n; i += blockDim.x) X[i * ldx + j] = X[i * ldx + j] / div;
-      __syncthreads();
-      for (int c = j + 1 + warp; c < k; c += blockDim.x / 32) {
-        double w = 0.0;
-        for (int i = j + 1 + lane; i < n; i += 32) w = fma(X[i * ldx + j], X[i * ldx + c], w);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-        w += X[j * ldx + c];
-        const double tw = t * w;
-        __syncwarp();
-        if (lane == 0) X[j * ldx + c] -= tw;
-        for (int i = j + 1 + lane; i < n; i += 32) X[i * ldx + c] = fma(-tw, X[i * ldx + j], X[i * ldx + c]);
-      }
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const double alpha = X[j * LDX + j];
+    const double sigma = sqrt(ss);
+    double beta, tau;
+    if (sigma == 0.0) {
+      tau = 0.0;
+      beta = alpha;
     } else {
-      for (int i = j + 1 + tid; i < n; i += blockDim.x) X[i * ldx + j] = 0.0;  // v_j = e_1
+      const double sgn = alpha < 0.0 ? -1.0 : 1.0;
+      beta = -sgn * hypot(alpha, sigma);
+      tau = (beta - alpha) / beta;
     }
-    __syncthreads();
-    if (tid == 0) X[j * ldx + j] = s_scal[0];
-    __syncthreads();
+    __syncwarp();
+    if (tau != 0.0) {
+      const double div = alpha - beta;
+      for (int i = j + 1 + lane; i < n; i += 32) X[i * LDX + j] = X[i * LDX + j] / div;
+      __syncwarp();
+      for (int c0 = j + 1; c0 < k; c0 += 4) {
+        double w[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          w[u] = 0.0;
+          if (c0 + u < k)
+            for (int i = j + 1 + lane; i < n; i += 32) w[u] = fma(X[i * LDX + j], X[i * LDX + c0 + u], w[u]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int u = 0; u < 4; u++) w[u] += __shfl_xor_sync(0xffffffffu, w[u], o);
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          if (c0 + u >= k) continue;
+          const double tw = tau * (w[u] + X[j * LDX + c0 + u]);
+          for (int i = j + 1 + lane; i < n; i += 32) X[i * LDX + c0 + u] = fma(-tw, X[i * LDX + j], X[i * LDX + c0 + u]);
+          __syncwarp();
+          if (lane == 0) X[j * LDX + c0 + u] -= tw;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      X[j * LDX + j] = beta;
+      Tw[j * LDT + j] = tau;
+    }
+    __syncwarp();
   }
   // ---- R^ (k x k upper triangular)
-  if (k > 0) {
+  {
     double *R = rh + sd.rh_off[cl];
-    for (int idx = tid; idx < k * k; idx += blockDim.x) {
+    for (int idx = lane; idx < k * k; idx += 32) {
       const int i = idx / k, j = idx % k;
-      R[idx] = j >= i ? X[i * ldx + j] : 0.0;
+      R[idx] = j >= i ? X[i * LDX + j] : 0.0;
     }
   }
-  // ---- compact WY: Gv = V^T V (V unit lower trapezoidal), T recurrence, M = T V^T
-  auto V = [&](int i, int j) -> double { return i < j ? 0.0 : (i == j ? 1.0 : X[i * ldx + j]); };
-  for (int idx = tid; idx < k * k; idx += blockDim.x) {
-    const int a = idx / k, b = idx % k;
-    double acc = 0.0;
-    if (a < b)
-      for (int i = b; i < n; i++) acc = fma(V(i, a), V(i, b), acc);
-    Gv[idx] = acc;
-  }
-  __syncthreads();
-  // T[j][j] = tau_j, T[0:j, j] = -tau_j T[0:j, 0:j] Gv[0:j, j]   (dlarft, forward, columnwise)
-  for (int j = 0; j < k; j++) {
-    const double tj = s_tau[j];
-    double v = 0.0;
-    if (tid < j) {
-      for (int l = tid; l < j; l++) v = fma(Tw[tid * k + l], Gv[l * k + j], v);
-      v = -tj * v;
+  // V(i, l): unit lower trapezoidal reflector matrix (zero padding outside n x k)
+  auto V = [&](int i, int l) -> double {
+    if (i >= n || l >= k || i < l) return 0.0;
+    return i == l ? 1.0 : X[i * LDX + l];
+  };
+  const int r = lane >> 2, q = lane & 3;
+  // ---- G = V^T V (upper tiles) -> Mm (K8 x K8)
+  for (int ta = 0; ta < K8 / 8; ta++)
+    for (int tb = ta; tb < K8 / 8; tb++) {
+      double acc[2] = {0.0, 0.0};
+      for (int k0 = 0; k0 < N4; k0 += 4) dmma(acc, V(k0 + q, ta * 8 + r), V(k0 + q, tb * 8 + r));
+      Mm[(ta * 8 + r) * K8 + tb * 8 + 2 * q] = acc[0];
+      Mm[(ta * 8 + r) * K8 + tb * 8 + 2 * q + 1] = acc[1];
     }
-    __syncthreads();
-    if (tid < j) Tw[tid * k + j] = v;
-    if (tid == j) Tw[j * k + j] = tj;
-    if (tid > j && tid < k) Tw[tid * k + j] = 0.0;
-    __syncthreads();
+  __syncwarp();
+  // ---- T recurrence (dlarft, forward, columnwise): T[0:j, j] = -tau_j T[0:j, 0:j] G[0:j, j]
+  for (int j = 1; j < k; j++) {
+    const double tj = Tw[j * LDT + j];
+    double v[2] = {0.0, 0.0};
+#pragma unroll
+    for (int u = 0; u < 2; u++) {
+      const int i = lane + 32 * u;
+      if (i < j)
+        for (int l = i; l < j; l++) v[u] = fma(Tw[i * LDT + l], Mm[l * K8 + j], v[u]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 2; u++) {
+      const int i = lane + 32 * u;
+      if (i < j) Tw[i * LDT + j] = -tj * v[u];
+    }
+    __syncwarp();
   }
-  for (int idx = tid; idx < k * n; idx += blockDim.x) {
-    const int a = idx / n, c = idx % n;
-    double acc = 0.0;
-    for (int l = a; l < k; l++) acc = fma(Tw[a * k + l], V(c, l), acc);
-    Mk[a * n + c] = acc;
-  }
-  __syncthreads();
+  // ---- M = T V^T (K4 x N8) -> Mm (ld LDM); G is dead now
+  for (int ta = 0; ta < K8 / 8; ta++)
+    for (int tc = 0; tc < N8 / 8; tc++) {
+      double acc[2] = {0.0, 0.0};
+      for (int k0 = 0; k0 < K4; k0 += 4) {
+        const int a = ta * 8 + r;
+        dmma(acc, Tw[a * LDT + k0 + q], V(tc * 8 + r, k0 + q));
+      }
+      __syncwarp();
+      const int a = ta * 8 + r;
+      if (a < K4) {
+        Mm[a * LDM + tc * 8 + 2 * q] = acc[0];
+        Mm[a * LDM + tc * 8 + 2 * q + 1] = acc[1];
+      }
+    }
+  __syncwarp();
+  // ---- Q = I - V M, straight to global
+  for (int ti = 0; ti < N8 / 8; ti++)
+    for (int tc = 0; tc < N8 / 8; tc++) {
+      double acc[2] = {0.0, 0.0};
+      for (int k0 = 0; k0 < K4; k0 += 4) dmma(acc, V(ti * 8 + r, k0 + q), Mm[(k0 + q) * LDM + tc * 8 + r]);
+      const int i = ti * 8 + r;
+#pragma unroll
+      for (int e = 0; e < 2; e++) {
+        const int c = tc * 8 + 2 * q + e;
+        if (i < n && c < n) Qg[i * n + c] = (i == c ? 1.0 : 0.0) - acc[e];
+      }
+    }
+}
+
+// --------------------------------------------------------------------------
+// Register-resident variant of the same QR completion for k <= KP <= 32 and
+// n <= 32 * NR: lane l holds rows l, l+32 of X; the Householder loop is fully
+// unrolled over the KP columns; every trailing-column dot product of one step
+// is reduced in the same butterfly.  Same convention H, same compact-WY
+// formation of Q (V staged once in shared memory with explicit unit diagonal).
+// Per-warp shared memory (doubles): V N8 x LDV | T K8 x LDT | G/M max(K8*K8, K4*LDM)
+// --------------------------------------------------------------------------
+__host__ __device__ inline int qr_ldv(int k) { return rup(rup(k, 4), 16) + 4; }
+__host__ __device__ inline int qr_reg_warp_doubles(int n, int k) {
+  const int K4 = rup(k, 4), K8 = rup(k, 8), N8 = rup(n, 8);
+  const int mm = K4 * qr_ldm(n) > K8 * K8 ? K4 * qr_ldm(n) : K8 * K8;
+  return N8 * qr_ldv(k) + K8 * qr_ldt(k) + mm + 2;
+}
+
+template <int NR, int KP>
+__global__ void __launch_bounds__(128) qr_reg_kernel(Side sd, int L, int level, int nclust, int per_warp,
+                                                     const double *__restrict__ leaf,
+                                                     const double *__restrict__ transfer, double *__restrict__ rh,
+                                                     double *__restrict__ qout, const uint64_t *meta_magic,
+                                                     uint64_t magic) {
+  if (meta_magic && threadIdx.x == 0 && blockIdx.x == 0 && *meta_magic != magic) __trap();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ci = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (ci >= nclust) return;
+  const int64_t base = lvl_off_d(L, level);
+  const int64_t cl = base + ci;
+  const int n = sd.n[cl], k = sd.k[cl];
+  if (n == 0) return;
   double *Qg = qout + sd.q_off[cl];
-  for (int idx = tid; idx < n * n; idx += blockDim.x) {
-    const int i = idx / n, c = idx % n;
-    double acc = 0.0;
-    const int lmax = i + 1 < k ? i + 1 : k;   // V(i, l) = 0 for l > i
-    for (int l = 0; l < lmax; l++) acc = fma(V(i, l), Mk[l * n + c], acc);
-    Qg[idx] = (i == c ? 1.0 : 0.0) - acc;
+  if (k == 0) {
+    for (int idx = lane; idx < n * n; idx += 32) Qg[idx] = (idx / n == idx % n) ? 1.0 : 0.0;
+    return;
   }
+  double x[NR][KP];
+  // ---- load X (rows lane + 32u)
+  if (level == 0) {
+    const double *R = leaf + sd.leaf_off[cl];
+#pragma unroll
+    for (int u = 0; u < NR; u++) {
+      const int i = lane + 32 * u;
+#pragma unroll
+      for (int c = 0; c < KP; c++) x[u][c] = (i < n && c < k) ? __ldg(R + i * k + c) : 0.0;
+    }
+  } else {
+    const int64_t c1 = lvl_off_d(L, level - 1) + 2 * ci, c2 = c1 + 1;
+    const int k1 = sd.k[c1], k2 = sd.k[c2];
+    const double *T = transfer + sd.tr_off[cl];  // n x k
+    const double *R1 = rh + sd.rh_off[c1];
+    const double *R2 = rh + sd.rh_off[c2];
+#pragma unroll
+    for (int u = 0; u < NR; u++) {
+      const int i = lane + 32 * u;
+#pragma unroll
+      for (int c = 0; c < KP; c++) x[u][c] = 0.0;
+      if (i < n) {
+        const bool first = i < k1;
+        const int ii = first ? i : i - k1, kk = first ? k1 : k2, roff = first ? 0 : k1;
+        const double *Rr = first ? R1 : R2;
+        for (int l = ii; l < kk; l++) {
+          const double rv = Rr[ii * kk + l];
+          const double *Trow = T + (roff + l) * k;
+#pragma unroll
+          for (int c = 0; c < KP; c++)
+            if (c < k) x[u][c] = fma(rv, __ldg(Trow + c), x[u][c]);
+        }
+      }
+    }
+  }
+  // shared memory: V (unit lower trapezoidal, zero padded), T (tau on the diagonal), G/M
+  extern __shared__ __align__(16) double sm[];
+  const int K4 = rup(k, 4), K8 = rup(k, 8), N4 = rup(n, 4), N8 = rup(n, 8);
+  const int LDV = qr_ldv(k), LDT = qr_ldt(k), LDM = qr_ldm(n);
+  double *Vs = sm + size_t(warp) * per_warp;   // N8 x LDV
+  double *Tw = Vs + N8 * LDV;                  // K8 x LDT
+  double *Mm = Tw + K8 * LDT;                  // G (K8 x K8), then M (K4 x LDM)
+  for (int idx = lane; idx < N8 * LDV; idx += 32) Vs[idx] = 0.0;
+  for (int idx = lane; idx < K8 * LDT; idx += 32) Tw[idx] = 0.0;
+  __syncwarp();
+  double *Rg = rh + sd.rh_off[cl];
+  // ---- Householder factorisation.  Runtime loop over j with a shifting register
+  //      window: x[u][0] is always the current column j, x[u][c] column j + c.
+  for (int j = 0; j < k; j++) {
+    const int w_left = k - j;   // columns j .. k-1 still in the window
+    double ss = 0.0;
+#pragma unroll
+    for (int u = 0; u < NR; u++)
+      if (lane + 32 * u > j && lane + 32 * u < n) ss = fma(x[u][0], x[u][0], ss);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const double own0 = (NR == 1 || j < 32) ? x[0][0] : x[NR - 1][0];
+    const double alpha = __shfl_sync(0xffffffffu, own0, j & 31);
+    const double sigma = sqrt(ss);
+    double beta, t;
+    if (sigma == 0.0) {
+      t = 0.0;
+      beta = alpha;
+    } else {
+      const double sgn = alpha < 0.0 ? -1.0 : 1.0;
+      beta = -sgn * hypot(alpha, sigma);
+      t = (beta - alpha) / beta;
+    }
+    double v[NR];
+    const double div = alpha - beta;
+#pragma unroll
+    for (int u = 0; u < NR; u++) {
+      const int i = lane + 32 * u;
+      v[u] = (i == j) ? 1.0 : ((t != 0.0 && i > j && i < n) ? x[u][0] / div : 0.0);
+    }
+    if (t != 0.0) {
+      double w[KP];
+#pragma unroll
+      for (int c = 1; c < KP; c++) {
+        w[c] = 0.0;
+        if (c < w_left)
+#pragma unroll
+          for (int u = 0; u < NR; u++) w[c] = fma(v[u], x[u][c], w[c]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int c = 1; c < KP; c++)
+          if (c < w_left) w[c] += __shfl_xor_sync(0xffffffffu, w[c], o);
+#pragma unroll
+      for (int c = 1; c < KP; c++)
+        if (c < w_left) {
+          const double tw = t * w[c];
+#pragma unroll
+          for (int u = 0; u < NR; u++) x[u][c] = fma(-tw, v[u], x[u][c]);
+        }
+    }
+    // reflector j -> V (rows > j; unit diagonal), tau_j -> T diagonal, row j of R^
+#pragma unroll
+    for (int u = 0; u < NR; u++) {
+      const int i = lane + 32 * u;
+      if (i >= j && i < n) Vs[i * LDV + j] = v[u];
+      if (i == j) {
+        for (int c = 0; c < j; c++) Rg[j * k + c] = 0.0;
+        Rg[j * k + j] = beta;
+#pragma unroll
+        for (int c = 1; c < KP; c++)
+          if (c < w_left) Rg[j * k + j + c] = x[u][c];
+      }
+    }
+    if (lane == 0) Tw[j * LDT + j] = t;
+    // shift the window
+#pragma unroll
+    for (int u = 0; u < NR; u++) {
+#pragma unroll
+      for (int c = 0; c < KP - 1; c++) x[u][c] = x[u][c + 1];
+      x[u][KP - 1] = 0.0;
+    }
+  }
+  __syncwarp();
+  const int r = lane >> 2, q = lane & 3;
+  // ---- G = V^T V (upper tiles)
+  for (int ta = 0; ta < K8 / 8; ta++)
+    for (int tb = ta; tb < K8 / 8; tb++) {
+      double acc[2] = {0.0, 0.0};
+      for (int k0 = 0; k0 < N4; k0 += 4)
+        dmma(acc, Vs[(k0 + q) * LDV + ta * 8 + r], Vs[(k0 + q) * LDV + tb * 8 + r]);
+      Mm[(ta * 8 + r) * K8 + tb * 8 + 2 * q] = acc[0];
+      Mm[(ta * 8 + r) * K8 + tb * 8 + 2 * q + 1] = acc[1];
+    }
+  __syncwarp();
+  // ---- T recurrence (dlarft, forward, columnwise): T[0:j, j] = -tau_j T[0:j, 0:j] G[0:j, j]
+  for (int j = 1; j < k; j++) {
+    const double tj = Tw[j * LDT + j];
+    double v = 0.0;
+    if (lane < j)
+      for (int l = lane; l < j; l++) v = fma(Tw[lane * LDT + l], Mm[l * K8 + j], v);
+    __syncwarp();
+    if (lane < j) Tw[lane * LDT + j] = -tj * v;
+    __syncwarp();
+  }
+  // ---- M = T V^T
+  for (int ta = 0; ta < K8 / 8; ta++)
+    for (int tc = 0; tc < N8 / 8; tc++) {
+      double acc[2] = {0.0, 0.0};
+      for (int k0 = 0; k0 < K4; k0 += 4)
+        dmma(acc, Tw[(ta * 8 + r) * LDT + k0 + q], Vs[(tc * 8 + r) * LDV + k0 + q]);
+      __syncwarp();
+      const int a = ta * 8 + r;
+      if (a < K4) {
+        Mm[a * LDM + tc * 8 + 2 * q] = acc[0];
+        Mm[a * LDM + tc * 8 + 2 * q + 1] = acc[1];
+      }
+    }
+  __syncwarp();
+  // ---- Q = I - V M, straight to global
+  for (int ti = 0; ti < N8 / 8; ti++)
+    for (int tc = 0; tc < N8 / 8; tc++) {
+      double acc[2] = {0.0, 0.0};
+      for (int k0 = 0; k0 < K4; k0 += 4)
+        dmma(acc, Vs[(ti * 8 + r) * LDV + k0 + q], Mm[(k0 + q) * LDM + tc * 8 + r]);
+      const int i = ti * 8 + r;
+#pragma unroll
+      for (int e = 0; e < 2; e++) {
+        const int c = tc * 8 + 2 * q + e;
+        if (i < n && c < n) Qg[i * n + c] = (i == c ? 1.0 : 0.0) - acc[e];
+      }
+    }
 }
 
 // --------------------------------------------------------------------------
@@ -365,13 +619,12 @@ __global__ void __launch_bounds__(128) coupling_kernel(const CouplingItem *__res
 // --------------------------------------------------------------------------
 template <int NP>
 struct PairCfg {
-  static constexpr int LD = NP + 4;                 // conflict-free DMMA fragment loads
-  static constexpr int WN = (NP == 64) ? 32 : 16;   // warp tile 16 x WN
-  static constexpr int TM = 2, TN = WN / 8;
-  static constexpr int NWM = NP / 16, NWN = NP / WN;
-  static constexpr int WARPS = NWM * NWN;
+  static constexpr int LD = NP + 4;       // conflict-free DMMA fragment loads
+  static constexpr int WARPS = NP / 16;   // warp w owns rows [16w, 16w + 16) of T and H
   static constexpr int THREADS = WARPS * 32;
+  static constexpr int TM = 2, TN = NP / 8;
   static constexpr size_t SMEM = size_t(3) * NP * LD * sizeof(double);
+  static constexpr int MIN_BLOCKS = (NP == 64) ? 2 : 4;
 };
 
 struct PairArgs {
@@ -386,9 +639,11 @@ struct PairArgs {
   double *s_val, *bb_out, *yr, *yc;   // yc: transposed column strips (general) / yr (symmetric)
 };
 
+// Issue the cp.async copies of G_ts (level 0: C_ts; else the 2x2 arrangement of
+// the children's bb parts / D~) into sG.
 template <int NP>
-__device__ __forceinline__ void pair_load_operands(const PairArgs &A, const PairItem &it, int t, int nt, int64_t lbase,
-                                                   double *sG, double *sQs) {
+__device__ __forceinline__ void pair_load_G(const PairArgs &A, const PairItem &it, int t, int nt, int64_t lbase,
+                                            double *sG) {
   constexpr int LD = PairCfg<NP>::LD;
   const int s = it.s;
   const int ns = A.cs.n[s];
@@ -421,13 +676,22 @@ __device__ __forceinline__ void pair_load_operands(const PairArgs &A, const Pair
       cp8(&sG[i * LD + j], src ? (const void *)src : any, src != nullptr);
     }
   }
-  async_tile<NP, NP, LD>(sQs, A.q_col + A.cs.q_off[s], ns, ns, ns, any);
 }
 
+// Steps (iv)+(ii)+(iii) for one chunk of pairs (t, s_1..s_c) of block row t.
+// Shared memory: Q_t (resident), G, Q_s; G and Q_s of pair p+1 are fetched
+// (cp.async) while pair p computes.  Warp w computes rows [16w, 16w+16) of
+// T = Q_t^T G and keeps them in registers; H = T Q_s takes its A fragments
+// from T by quad shuffles, and H is scattered straight from the accumulators:
+//   nn -> S (t@k, s@k) [+ mirror], bb -> next level, bn -> row strip panel,
+//   nb^T -> column strip panel (general) / row strip panel of s (symmetric).
+// Diagonal blocks in symmetric mode use H_sym[i][j] = H[min(i,j)][max(i,j)]
+// (each upper element written to both places) -- the oracle's convention.
 template <int NP>
-__global__ void __launch_bounds__(PairCfg<NP>::THREADS) pair_kernel(PairArgs A) {
+__global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS) pair_kernel(PairArgs A) {
   using C = PairCfg<NP>;
   constexpr int LD = C::LD;
+  constexpr int TN = C::TN;
   extern __shared__ __align__(16) double sm[];
   double *sQt = sm;
   double *sG = sm + NP * LD;
@@ -435,69 +699,123 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS) pair_kernel(PairArgs A) 
   const Chunk ch = A.chunks[blockIdx.x];
   const int t = A.items[ch.begin].t;
   const int nt = A.rs.n[t], ktt = A.rs.k[t];
-  const int warp = threadIdx.x >> 5;
-  const int m0 = (warp / C::NWN) * 16, n0 = (warp % C::NWN) * C::WN;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = lane >> 2, q = lane & 3;
+  const int m0 = warp * 16;
   const int64_t lbase = lvl_off_d(A.L, A.level);
+  const bool diag_sym = false;
+  (void)diag_sym;
+  // prologue: Q_t, G_0, Q_s0
   async_tile<NP, NP, LD>(sQt, A.q_row + A.rs.q_off[t], nt, nt, nt, A.items);
+  {
+    const PairItem it0 = A.items[ch.begin];
+    pair_load_G<NP>(A, it0, t, nt, lbase, sG);
+    const int ns0 = A.cs.n[it0.s];
+    async_tile<NP, NP, LD>(sQs, A.q_col + A.cs.q_off[it0.s], ns0, ns0, ns0, A.items);
+  }
+  cp_commit();
   for (int p = ch.begin; p < ch.end; p++) {
     const PairItem it = A.items[p];
     const int s = it.s;
     const int ns = A.cs.n[s], kss = A.cs.k[s];
-    __syncthreads();  // previous pair's epilogue done with sG / sQs
-    pair_load_operands<NP>(A, it, t, nt, lbase, sG, sQs);
-    cp_commit();
     cp_wait_all();
     __syncthreads();
-    double acc[C::TM][C::TN][2];
-    // T = Q_t^T G
-    zero_acc(acc);
-    warp_gemm<LD, LD, C::TM, C::TN, true>(sQt, sG, m0, n0, NP, acc);
-    __syncthreads();
-    warp_store<LD>(sG, m0, n0, acc);
-    __syncthreads();
-    // H = T Q_s
-    zero_acc(acc);
-    warp_gemm<LD, LD, C::TM, C::TN, false>(sG, sQs, m0, n0, NP, acc);
-    __syncthreads();
-    warp_store<LD>(sG, m0, n0, acc);
-    __syncthreads();
-    if (A.sym && s == t) {  // H_tt made exactly symmetric (upper -> lower)
-      for (int idx = threadIdx.x; idx < nt * nt; idx += blockDim.x) {
-        const int i = idx / nt, j = idx % nt;
-        if (i > j) sG[i * LD + j] = sG[j * LD + i];
-      }
-      __syncthreads();
+    // ---- T = Q_t^T G  (rows m0..m0+15, all NP columns)
+    double T[2][TN][2];
+    zero_acc(T);
+#pragma unroll 2
+    for (int k0 = 0; k0 < NP; k0 += 4) {
+      double a[2], b[TN];
+#pragma unroll
+      for (int i = 0; i < 2; i++) a[i] = sQt[(k0 + q) * LD + m0 + i * 8 + r];
+#pragma unroll
+      for (int j = 0; j < TN; j++) b[j] = sG[(k0 + q) * LD + j * 8 + r];
+#pragma unroll
+      for (int i = 0; i < 2; i++)
+#pragma unroll
+        for (int j = 0; j < TN; j++) dmma(T[i][j], a[i], b[j]);
     }
-    // ---- step (iii): scatter
-    const int mt = nt - ktt, ms = ns - kss;
-    if (it.s_dst >= 0) {
-      for (int idx = threadIdx.x; idx < mt * ms; idx += blockDim.x) {
-        const int a = idx / ms, b = idx % ms;
-        A.s_val[it.s_dst + int64_t(a) * it.s_ld + b] = sG[(ktt + a) * LD + kss + b];
-      }
+    __syncthreads();  // every warp is done with G
+    const bool more = p + 1 < ch.end;
+    if (more) {
+      pair_load_G<NP>(A, A.items[p + 1], t, nt, lbase, sG);
+      cp_commit();
     }
-    if (it.s_dst_m >= 0) {
-      for (int idx = threadIdx.x; idx < mt * ms; idx += blockDim.x) {
-        const int b = idx / mt, a = idx % mt;
-        A.s_val[it.s_dst_m + int64_t(b) * it.s_ld_m + a] = sG[(ktt + a) * LD + kss + b];
+    // ---- H = T Q_s; A fragment (row m0+8i+r, col k0+q) lives in lane (r, (k0%8+q)/2), element q%2
+    double H[2][TN][2];
+    zero_acc(H);
+    const int src_lo = r * 4 + (q >> 1), src_hi = src_lo + 2;
+#pragma unroll
+    for (int k0 = 0; k0 < NP; k0 += 4) {
+      const int jt = k0 >> 3;               // T tile column holding k0..k0+3
+      const int srcl = (k0 & 4) ? src_hi : src_lo;
+      double a[2], b[TN];
+#pragma unroll
+      for (int i = 0; i < 2; i++) {
+        const double e0 = __shfl_sync(0xffffffffu, T[i][jt][0], srcl);
+        const double e1 = __shfl_sync(0xffffffffu, T[i][jt][1], srcl);
+        a[i] = (q & 1) ? e1 : e0;
       }
+#pragma unroll
+      for (int j = 0; j < TN; j++) b[j] = sQs[(k0 + q) * LD + j * 8 + r];
+#pragma unroll
+      for (int i = 0; i < 2; i++)
+#pragma unroll
+        for (int j = 0; j < TN; j++) dmma(H[i][j], a[i], b[j]);
     }
-    if (it.bb_dst >= 0) {
-      for (int idx = threadIdx.x; idx < ktt * kss; idx += blockDim.x) {
-        const int i = idx / kss, j = idx % kss;
-        A.bb_out[it.bb_dst + idx] = sG[i * LD + j];
-      }
+    __syncthreads();  // every warp is done with Q_s
+    if (more) {
+      const PairItem nx = A.items[p + 1];
+      const int nsx = A.cs.n[nx.s];
+      async_tile<NP, NP, LD>(sQs, A.q_col + A.cs.q_off[nx.s], nsx, nsx, nsx, A.items);
+      cp_commit();
     }
-    if (it.yr_dst >= 0) {
-      for (int idx = threadIdx.x; idx < ktt * ms; idx += blockDim.x) {
-        const int i = idx / ms, b = idx % ms;
-        A.yr[it.yr_dst + int64_t(i) * it.yr_ld + b] = sG[i * LD + kss + b];
-      }
-    }
-    if (it.yc_dst >= 0) {
-      for (int idx = threadIdx.x; idx < kss * mt; idx += blockDim.x) {
-        const int j = idx / mt, a = idx % mt;
-        A.yc[it.yc_dst + int64_t(j) * it.yc_ld + a] = sG[(ktt + a) * LD + j];
+    // ---- step (iii): scatter from the accumulators
+    const bool dsym = A.sym && s == t;
+#pragma unroll
+    for (int i = 0; i < 2; i++) {
+      const int row = m0 + i * 8 + r;
+      if (row >= nt) continue;
+#pragma unroll
+      for (int j = 0; j < TN; j++) {
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          const int col = j * 8 + 2 * q + e;
+          if (col >= ns) continue;
+          const double v = H[i][j][e];
+          if (row >= ktt) {
+            const int a = row - ktt;
+            if (col >= kss) {  // nn -> S
+              const int b = col - kss;
+              if (dsym) {
+                if (a <= b) {
+                  A.s_val[it.s_dst + int64_t(a) * it.s_ld + b] = v;
+                  A.s_val[it.s_dst + int64_t(b) * it.s_ld + a] = v;
+                }
+              } else {
+                if (it.s_dst >= 0) A.s_val[it.s_dst + int64_t(a) * it.s_ld + b] = v;
+                if (it.s_dst_m >= 0) A.s_val[it.s_dst_m + int64_t(b) * it.s_ld_m + a] = v;
+              }
+            } else if (it.yc_dst >= 0) {  // nb^T
+              A.yc[it.yc_dst + int64_t(col) * it.yc_ld + a] = v;
+            }
+          } else {
+            if (col < kss) {  // bb
+              if (it.bb_dst >= 0) {
+                if (dsym) {
+                  if (row <= col) {
+                    A.bb_out[it.bb_dst + row * kss + col] = v;
+                    A.bb_out[it.bb_dst + col * kss + row] = v;
+                  }
+                } else {
+                  A.bb_out[it.bb_dst + row * kss + col] = v;
+                }
+              }
+            } else if (it.yr_dst >= 0) {  // bn
+              A.yr[it.yr_dst + int64_t(row) * it.yr_ld + (col - kss)] = v;
+            }
+          }
+        }
       }
     }
   }
@@ -593,23 +911,24 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS) strip_kernel(StripA
   warp_store<C::LDZ>(sZ, m0, n0, acc);
   __syncthreads();
   const int mq = n - kq;
+  const int lane = threadIdx.x & 31;
   if (pn.s_dst >= 0) {
-    for (int idx = threadIdx.x; idx < mq * ncol; idx += blockDim.x) {
-      const int a = idx / ncol, cc = idx % ncol;
-      A.s_val[pn.s_dst + int64_t(a) * pn.s_ld + tile.c0 + cc] = sZ[(kq + a) * C::LDZ + cc];
+    for (int a = warp; a < mq; a += C::WARPS) {
+      double *d = A.s_val + pn.s_dst + int64_t(a) * pn.s_ld + tile.c0;
+      for (int cc = lane; cc < ncol; cc += 32) d[cc] = sZ[(kq + a) * C::LDZ + cc];
     }
   }
   if (pn.y_dst >= 0) {
-    for (int idx = threadIdx.x; idx < kq * ncol; idx += blockDim.x) {
-      const int i = idx / ncol, cc = idx % ncol;
-      A.y_out[pn.y_dst + int64_t(i) * pn.y_ld + tile.c0 + cc] = sZ[i * C::LDZ + cc];
+    for (int i = warp; i < kq; i += C::WARPS) {
+      double *d = A.y_out + pn.y_dst + int64_t(i) * pn.y_ld + tile.c0;
+      for (int cc = lane; cc < ncol; cc += 32) d[cc] = sZ[i * C::LDZ + cc];
     }
   }
   if (mq > 0) {
-    for (int idx = threadIdx.x; idx < mq * ncol; idx += blockDim.x) {
-      const int cc = idx / mq, a = idx % mq;
+    for (int cc = warp; cc < ncol; cc += C::WARPS) {
       const int64_t d = tdst[cc];
-      if (d >= 0) A.s_val[d + a] = sZ[(kq + a) * C::LDZ + cc];
+      if (d < 0) continue;
+      for (int a = lane; a < mq; a += 32) A.s_val[d + a] = sZ[(kq + a) * C::LDZ + cc];
     }
   }
 }
@@ -642,7 +961,6 @@ __global__ void __launch_bounds__(256) csr_cols_kernel(const CsrBlockRow *__rest
   const int part = blockIdx.x % splits;
   const int rowlen = br.rowlen;
   const bool blk_smem = br.nblk <= CSR_BLK_MAX;
-  const bool pat_smem = blk_smem && rowlen <= CSR_PAT_MAX;
   const CsrBlock *b = blks + br.blk_begin;
   if (blk_smem) {
     for (int j = threadIdx.x; j < br.nblk; j += blockDim.x) {
@@ -654,98 +972,141 @@ __global__ void __launch_bounds__(256) csr_cols_kernel(const CsrBlockRow *__rest
     __syncthreads();
     b = sb;
   }
-  if (pat_smem) {
-    for (int p = threadIdx.x; p < rowlen; p += blockDim.x) pat[p] = csr_col_at(b, br.nblk, p);
-    __syncthreads();
-  }
-  // this CTA writes whole rows [a0, a1) of the panel
+  // this CTA writes whole rows [a0, a1) of the panel, column tile by column tile
   const int a0 = int((int64_t(br.m_r) * part) / splits), a1 = int((int64_t(br.m_r) * (part + 1)) / splits);
+  if (a1 <= a0) return;
   int32_t *dst = col + br.p_base + int64_t(a0) * rowlen;
-  const int64_t total = int64_t(a1 - a0) * rowlen;
-  if (total <= 0) return;
-  if (rowlen >= 256) {
-    // thread t handles positions p = t, t+256, ... of every row (no division in the loop)
+  for (int t0 = 0; t0 < rowlen; t0 += CSR_PAT_MAX) {
+    const int tl = rowlen - t0 < CSR_PAT_MAX ? rowlen - t0 : CSR_PAT_MAX;
+    for (int p = threadIdx.x; p < tl; p += blockDim.x) pat[p] = csr_col_at(b, br.nblk, t0 + p);
+    __syncthreads();
     for (int a = 0; a < a1 - a0; a++) {
-      int32_t *d = dst + int64_t(a) * rowlen;
-      for (int p = threadIdx.x; p < rowlen; p += blockDim.x) d[p] = pat_smem ? pat[p] : csr_col_at(b, br.nblk, p);
+      int32_t *d = dst + int64_t(a) * rowlen + t0;
+      // scalar head up to 16-byte alignment, int4 body, scalar tail
+      const int head = int(((16 - (reinterpret_cast<uintptr_t>(d) & 15)) & 15) >> 2) < tl
+                           ? int(((16 - (reinterpret_cast<uintptr_t>(d) & 15)) & 15) >> 2)
+                           : tl;
+      if (threadIdx.x < head) d[threadIdx.x] = pat[threadIdx.x];
+      const int nv = (tl - head) >> 2;
+      int4 *dv = reinterpret_cast<int4 *>(d + head);
+      for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+        const int p = head + 4 * v;
+        dv[v] = make_int4(pat[p], pat[p + 1], pat[p + 2], pat[p + 3]);
+      }
+      for (int p = head + 4 * nv + threadIdx.x; p < tl; p += blockDim.x) d[p] = pat[p];
     }
-  } else {
-    for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
-      const int p = int(e % rowlen);
-      dst[e] = pat_smem ? pat[p] : csr_col_at(b, br.nblk, p);
-    }
+    __syncthreads();
   }
 }
 
 // --------------------------------------------------------------------------
-// Apply: y = U^T b (leaves -> root), x = V y (root -> leaves).  One CTA per
-// cluster; vectors column-major (ld) with nrhs columns; zb = basis-coefficient
-// buffer (column-major, ld = zb_len).
+// Apply, one launch per direction.
+// y = U^T b, leaves -> root: one CTA per leaf; after a cluster is done, the
+// CTA that completes the second child of a parent (atomic arrival counter)
+// continues with the parent, so the whole upward pass is one kernel.
+// x = V y, root -> leaves: one CTA per leaf walks its root-to-leaf path,
+// recomputing the (few, small) ancestor products it needs.
+// Vectors column-major (ld) with nrhs columns; zb = basis coefficients.
 // --------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, int level, const double *__restrict__ q,
+__global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const double *__restrict__ q,
                                                        const double *__restrict__ b, int64_t ldb, double *__restrict__ y,
-                                                       int64_t ldy, double *__restrict__ zb, int64_t zbl, int nrhs, int B) {
-  const int64_t base = lvl_off_d(L, level);
-  const int64_t cl = base + blockIdx.x;
-  const int n = sd.n[cl], k = sd.k[cl];
-  if (n == 0) return;
+                                                       int64_t ldy, double *__restrict__ zb, int64_t zbl, int nrhs, int B,
+                                                       int *__restrict__ arrive) {
+  __shared__ __align__(16) double sQ[64 * 65];
   __shared__ double sx[64];
-  const double *Q = q + sd.q_off[cl];
-  int64_t c1 = 0;
-  int k1 = 0;
-  if (level > 0) {
-    c1 = lvl_off_d(L, level - 1) + 2 * (cl - base);
-    k1 = sd.k[c1];
-  }
-  for (int r = 0; r < nrhs; r++) {
+  __shared__ int s_go;
+  int level = 0;
+  int64_t idx = blockIdx.x;  // in-level index
+  while (true) {
+    const int64_t cl = lvl_off_d(L, level) + idx;
+    const int n = sd.n[cl], k = sd.k[cl];
+    if (n > 0) {
+      const double *Q = q + sd.q_off[cl];
+      for (int e = threadIdx.x; e < n * n; e += blockDim.x) cp8(&sQ[(e / n) * 65 + e % n], Q + e, true);
+      cp_commit();
+      int64_t c1 = 0;
+      int k1 = 0;
+      if (level > 0) {
+        c1 = lvl_off_d(L, level - 1) + 2 * idx;
+        k1 = sd.k[c1];
+      }
+      for (int r = 0; r < nrhs; r++) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+          double v;
+          if (level == 0) v = b[(idx * B + i) + r * ldb];
+          else if (i < k1) v = __ldcg(zb + sd.zb_off[c1] + i + r * zbl);
+          else v = __ldcg(zb + sd.zb_off[c1 + 1] + (i - k1) + r * zbl);
+          sx[i] = v;
+        }
+        cp_wait_all();
+        __syncthreads();
+        for (int j = threadIdx.x; j < n; j += blockDim.x) {
+          double acc = 0.0;
+          for (int i = 0; i < n; i++) acc = fma(sQ[i * 65 + j], sx[i], acc);
+          if (j < k) zb[sd.zb_off[cl] + j + r * zbl] = acc;
+          else y[sd.s_off[cl] + (j - k) + r * ldy] = acc;
+        }
+      }
+    }
+    if (level == L) break;
+    // arrival at the parent: the second child's CTA continues upward
+    __threadfence();
     __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      double v;
-      if (level == 0) v = b[(int64_t(blockIdx.x) * B + i) + r * ldb];
-      else if (i < k1) v = zb[sd.zb_off[c1] + i + r * zbl];
-      else v = zb[sd.zb_off[c1 + 1] + (i - k1) + r * zbl];
-      sx[i] = v;
+    if (threadIdx.x == 0) {
+      const int64_t parent = lvl_off_d(L, level + 1) + idx / 2;
+      s_go = atomicAdd(&arrive[parent], 1) == 1;
     }
     __syncthreads();
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
-      double acc = 0.0;
-      for (int i = 0; i < n; i++) acc = fma(Q[i * n + j], sx[i], acc);
-      if (j < k) zb[sd.zb_off[cl] + j + r * zbl] = acc;
-      else y[sd.s_off[cl] + (j - k) + r * ldy] = acc;
-    }
+    if (!s_go) break;
+    __threadfence();
+    level++;
+    idx >>= 1;
   }
 }
 
-__global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, int level, const double *__restrict__ q,
+__global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, const double *__restrict__ q,
                                                       const double *__restrict__ y, int64_t ldy, double *__restrict__ x,
-                                                      int64_t ldx, double *__restrict__ zb, int64_t zbl, int nrhs, int B) {
-  const int64_t base = lvl_off_d(L, level);
-  const int64_t cl = base + blockIdx.x;
-  const int n = sd.n[cl], k = sd.k[cl];
-  if (n == 0) return;
-  __shared__ double sQ[64 * 65];
+                                                      int64_t ldx, int nrhs, int B) {
+  __shared__ __align__(16) double sQ[64 * 65];
   __shared__ double sv[64];
-  const double *Q = q + sd.q_off[cl];
-  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) cp8(&sQ[(idx / n) * 65 + idx % n], Q + idx, true);
-  cp_commit();
-  cp_wait_all();
-  int64_t c1 = 0;
-  int k1 = 0;
-  if (level > 0) {
-    c1 = lvl_off_d(L, level - 1) + 2 * (cl - base);
-    k1 = sd.k[c1];
-  }
+  __shared__ double sw[64];
+  const int64_t leaf = blockIdx.x;
   for (int r = 0; r < nrhs; r++) {
-    __syncthreads();
-    for (int j = threadIdx.x; j < n; j += blockDim.x)
-      sv[j] = j < k ? zb[sd.zb_off[cl] + j + r * zbl] : y[sd.s_off[cl] + (j - k) + r * ldy];
-    __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      double acc = 0.0;
-      for (int j = 0; j < n; j++) acc = fma(sQ[i * 65 + j], sv[j], acc);
-      if (level == 0) x[(int64_t(blockIdx.x) * B + i) + r * ldx] = acc;
-      else if (i < k1) zb[sd.zb_off[c1] + i + r * zbl] = acc;
-      else zb[sd.zb_off[c1 + 1] + (i - k1) + r * zbl] = acc;
+    // walk the path root -> leaf; sv[0:k] holds the basis coefficients from the parent
+    for (int level = L; level >= 0; level--) {
+      const int64_t idx = leaf >> level;
+      const int64_t cl = lvl_off_d(L, level) + idx;
+      const int n = sd.n[cl], k = sd.k[cl];
+      __syncthreads();
+      if (n == 0) continue;
+      const double *Q = q + sd.q_off[cl];
+      for (int e = threadIdx.x; e < n * n; e += blockDim.x) cp8(&sQ[(e / n) * 65 + e % n], Q + e, true);
+      cp_commit();
+      for (int j = threadIdx.x; j < n; j += blockDim.x)
+        if (j >= k) sv[j] = y[sd.s_off[cl] + (j - k) + r * ldy];
+      cp_wait_all();
+      __syncthreads();
+      if (level == 0) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+          double acc = 0.0;
+          for (int j = 0; j < n; j++) acc = fma(sQ[i * 65 + j], sv[j], acc);
+          x[(leaf * B + i) + r * ldx] = acc;
+        }
+      } else {
+        // only the rows of the child on the path are needed
+        const int64_t c1 = lvl_off_d(L, level - 1) + 2 * idx;
+        const int k1 = sd.k[c1];
+        const bool second = (leaf >> (level - 1)) & 1;
+        const int rlo = second ? k1 : 0, rhi = second ? n : k1;
+        for (int i = rlo + threadIdx.x; i < rhi; i += blockDim.x) {
+          double acc = 0.0;
+          for (int j = 0; j < n; j++) acc = fma(sQ[i * 65 + j], sv[j], acc);
+          sw[i - rlo] = acc;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < rhi - rlo; i += blockDim.x) sv[i] = sw[i];
+      }
     }
   }
 }
@@ -761,6 +1122,7 @@ __global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, int level,
 
 template <int NP>
 static h2sp_status launch_pairs(const PairArgs &a, int64_t nchunks, cudaStream_t st) {
+  static_assert(PairCfg<NP>::WARPS >= 1, "");
   using C = PairCfg<NP>;
   static bool attr = false;
   if (!attr) {
@@ -852,6 +1214,11 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   DeviceAux *aux = nullptr;
   if (h2sp_status e = get_aux(L, &aux)) return e;
   cudaStream_t s1 = aux->side[0], s2 = aux->side[1];
+  static const bool serial = [] {
+    const char *e = getenv("H2SP_SERIAL");  // debugging / attribution: run every launch on `stream`
+    return e && e[0] == '1';
+  }();
+  if (serial) s1 = s2 = st;
   cudaEvent_t ev_fork = aux->ev[0], ev_qr0 = aux->ev[1], ev_csr = aux->ev[2];
   auto ev_ready = [&](int k) { return aux->ev[3 + k]; };   // QR_k and couplings_{k-1} done
   // The launch order (and so the index of h2sp_plan_launches / profiling
@@ -869,7 +1236,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   };
   static bool qr_attr = false;
   if (!qr_attr) {
-    H2SP_CK(cudaFuncSetAttribute(qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(qr_smem_bytes(64, 64))));
+    H2SP_CK(cudaFuncSetAttribute(qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     H2SP_CK(cudaFuncSetAttribute(coupling_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 64 * 64 * 8 + 1024));
     qr_attr = true;
   }
@@ -893,25 +1260,74 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   }
   auto qr = [&](int k, cudaStream_t s) -> h2sp_status {
     const LevelPlan &lp = P->levels[k];
-    const unsigned M = unsigned(int64_t(1) << (L - k));
-    int kmax_r = 0, kmax_c = 0;
-    for (unsigned i = 0; i < M; i++) {
-      kmax_r = std::max(kmax_r, P->k_row[lvl_off_d(L, k) + i]);
-      kmax_c = std::max(kmax_c, P->k_col[lvl_off_d(L, k) + i]);
-    }
+    const int M = int(int64_t(1) << (L - k));
+    auto launch = [&](const Side &sd, const std::vector<int32_t> &nn, const std::vector<int32_t> &kk, const double *leaf,
+                      const double *tr, double *rh, double *qo, const uint64_t *magic_ptr) -> h2sp_status {
+      int per_warp = 2, nmax = 0, kmax = 0, per_warp_reg = 2;
+      for (int i = 0; i < M; i++) {
+        const int64_t c = lvl_off_d(L, k) + i;
+        int rs_ = 0;
+        if (k > 0) {
+          const int64_t c1 = lvl_off_d(L, k - 1) + 2 * i;
+          rs_ = kk[c1] * kk[c1] + kk[c1 + 1] * kk[c1 + 1];
+        }
+        per_warp = std::max(per_warp, qr_warp_doubles(nn[c], kk[c], rs_));
+        per_warp_reg = std::max(per_warp_reg, qr_reg_warp_doubles(nn[c], kk[c]));
+        nmax = std::max(nmax, int(nn[c]));
+        kmax = std::max(kmax, int(kk[c]));
+      }
+      if (kmax <= 32) {
+        // spread small levels over many SMs (1 warp per CTA) to keep the latency chain short
+        const int wpb = std::max(1, std::min({4, int((96 * 1024) / (size_t(per_warp_reg) * 8)), M / 148}));
+        const unsigned grid = unsigned((M + wpb - 1) / wpb);
+        const size_t smem = size_t(per_warp_reg) * 8 * wpb;
+        const int kp = kmax <= 8 ? 8 : kmax <= 16 ? 16 : kmax <= 24 ? 24 : 32;
+#define H2SP_QR_REG(NR_, KP_)                                                                              \
+  do {                                                                                                     \
+    static bool attr_ = false;                                                                             \
+    if (!attr_) {                                                                                          \
+      H2SP_CK(cudaFuncSetAttribute(qr_reg_kernel<NR_, KP_>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                   100 * 1024));                                                           \
+      attr_ = true;                                                                                        \
+    }                                                                                                      \
+    qr_reg_kernel<NR_, KP_><<<grid, 32 * wpb, smem, s>>>(sd, L, k, M, per_warp_reg, leaf, tr, rh, qo,        \
+                                                        magic_ptr, P->magic);                              \
+  } while (0)
+        if (nmax <= 32) {
+          switch (kp) {
+            case 8: H2SP_QR_REG(1, 8); break;
+            case 16: H2SP_QR_REG(1, 16); break;
+            case 24: H2SP_QR_REG(1, 24); break;
+            default: H2SP_QR_REG(1, 32); break;
+          }
+        } else {
+          switch (kp) {
+            case 8: H2SP_QR_REG(2, 8); break;
+            case 16: H2SP_QR_REG(2, 16); break;
+            case 24: H2SP_QR_REG(2, 24); break;
+            default: H2SP_QR_REG(2, 32); break;
+          }
+        }
+#undef H2SP_QR_REG
+        H2SP_CK(cudaGetLastError());
+        return H2SP_OK;
+      }
+      const int wpb = std::max(1, std::min(4, int((96 * 1024) / (size_t(per_warp) * 8))));
+      qr_kernel<<<unsigned((M + wpb - 1) / wpb), 32 * wpb, size_t(per_warp) * 8 * wpb, s>>>(
+          sd, L, k, M, per_warp, leaf, tr, rh, qo, magic_ptr, P->magic);
+      H2SP_CK(cudaGetLastError());
+      return H2SP_OK;
+    };
     if (lp.np_row > 0) {
       if (h2sp_status e = pre(s, li[k].qr_row)) return e;
-      qr_kernel<<<M, 128, qr_smem_bytes(lp.np_row, kmax_r), s>>>(rs, L, k, in->leaf_basis_row, in->transfer_row,
-                                                                 rh_row, out->q_row,
-                                                                 k == 0 ? (const uint64_t *)meta : nullptr, P->magic);
-      H2SP_CK(cudaGetLastError());
+      if (h2sp_status e = launch(rs, P->n_row, P->k_row, in->leaf_basis_row, in->transfer_row, rh_row, out->q_row,
+                                 k == 0 ? (const uint64_t *)meta : nullptr))
+        return e;
       if (h2sp_status e = post(s, li[k].qr_row)) return e;
     }
     if (!sym && lp.np_col > 0) {
       if (h2sp_status e = pre(s, li[k].qr_col)) return e;
-      qr_kernel<<<M, 128, qr_smem_bytes(lp.np_col, kmax_c), s>>>(cs, L, k, leaf_col, tr_col, rh_col, q_col, nullptr,
-                                                                 P->magic);
-      H2SP_CK(cudaGetLastError());
+      if (h2sp_status e = launch(cs, P->n_col, P->k_col, leaf_col, tr_col, rh_col, q_col, nullptr)) return e;
       if (h2sp_status e = post(s, li[k].qr_col)) return e;
     }
     return H2SP_OK;
@@ -1048,13 +1464,11 @@ h2sp_status launch_apply_Ut(const h2sp_plan_s *P, const double *q, const double 
   const Side sd = side_of(cl, col_side);
   double *zb = (double *)(ws + P->meta_bytes);
   const int64_t zbl = col_side ? P->zb_col_len : P->zb_row_len;
-  for (int k = 0; k <= P->L; k++) {
-    const LevelPlan &lp = P->levels[k];
-    if ((col_side ? lp.np_col : lp.np_row) == 0) continue;
-    apply_ut_kernel<<<unsigned(int64_t(1) << (P->L - k)), 128, 0, st>>>(sd, P->L, k, q, b, ldb, y, ldy, zb, zbl,
-                                                                         nrhs, P->B);
-    H2SP_CK(cudaGetLastError());
-  }
+  int *arrive = (int *)(ws + P->meta_bytes + ((size_t(std::max(P->zb_row_len, P->zb_col_len)) * nrhs * 8 + 255) / 256) * 256);
+  H2SP_CK(cudaMemsetAsync(arrive, 0, size_t(P->ncl) * sizeof(int), st));
+  apply_ut_kernel<<<unsigned(int64_t(1) << P->L), 128, 0, st>>>(sd, P->L, q, b, ldb, y, ldy, zb, zbl, nrhs, P->B,
+                                                                 arrive);
+  H2SP_CK(cudaGetLastError());
   return H2SP_OK;
 }
 
@@ -1063,15 +1477,8 @@ h2sp_status launch_apply_V(const h2sp_plan_s *P, const double *q, const double *
   cudaStream_t st = (cudaStream_t)stream;
   const Clusters cl = make_clusters(P, ws);
   const Side sd = side_of(cl, col_side);
-  double *zb = (double *)(ws + P->meta_bytes);
-  const int64_t zbl = col_side ? P->zb_col_len : P->zb_row_len;
-  for (int k = P->L; k >= 0; k--) {
-    const LevelPlan &lp = P->levels[k];
-    if ((col_side ? lp.np_col : lp.np_row) == 0) continue;
-    apply_v_kernel<<<unsigned(int64_t(1) << (P->L - k)), 128, 0, st>>>(sd, P->L, k, q, y, ldy, x, ldx, zb, zbl,
-                                                                        nrhs, P->B);
-    H2SP_CK(cudaGetLastError());
-  }
+  apply_v_kernel<<<unsigned(int64_t(1) << P->L), 128, 0, st>>>(sd, P->L, q, y, ldy, x, ldx, nrhs, P->B);
+  H2SP_CK(cudaGetLastError());
   return H2SP_OK;
 }
 
