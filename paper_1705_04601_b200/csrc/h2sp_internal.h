@@ -79,6 +79,7 @@ struct CouplingItem {    // D~ = R^R_t D R^C_s^T (reading 11)
 struct CsrBlockRow {     // rows [row0, row0 + m_r) of S, all with the same column pattern
   int64_t row0;
   int64_t p_base;        // s_val offset of row row0
+  int64_t pat_off;       // the block row's column pattern (rowlen int32) in the pattern array
   int32_t m_r;
   int32_t rowlen;
   int32_t blk_begin, nblk;
@@ -130,7 +131,7 @@ struct h2sp_plan_s {
   double flops, bytes, flops_cong, flops_strip;
   std::vector<h2sp::LevelPlan> levels;
   h2sp::ClusterArrays ca;
-  size_t csr_rows_off, csr_blocks_off, rowptr_off;
+  size_t csr_rows_off, csr_blocks_off, rowptr_off, csr_pat_off;
   int64_t n_csr_rows, n_csr_blocks;
   std::vector<unsigned char> meta;          // device image of all work lists
   size_t meta_bytes;

@@ -570,11 +570,20 @@ __global__ void __launch_bounds__(128) qr_reg_kernel(Side sd, int L, int level, 
 
 // --------------------------------------------------------------------------
 // Couplings in orthogonalised coordinates: D~ = R^R_t D R^C_s^T.
-// One warp per admissible pair, `ipc` pairs per CTA; each warp stages its
-// operands (4 * kmax^2 doubles) in its own slice of shared memory.
+// One warp per admissible pair, `ipc` pairs per CTA.  Operands staged with
+// cp.async into the warp's slice of shared memory (zero padded), then the two
+// small products on the DMMA pipe: W = D R^_s^T, D~ = R^_t W.
+// Per-warp shared memory (doubles): D A8 x LDB | Rs B8 x LDB | Rt A8 x LDA | W A8 x LDB
 // --------------------------------------------------------------------------
+__host__ __device__ inline int coup_ld(int k) { return rup(rup(k, 8), 16) + 4; }
+__host__ __device__ inline int coup_warp_doubles(int kt, int ks) {
+  const int A8 = rup(kt, 8), B8 = rup(ks, 8);
+  return A8 * coup_ld(ks) * 2 + B8 * coup_ld(ks) + A8 * coup_ld(kt) + 2;
+}
+
 __global__ void __launch_bounds__(128) coupling_kernel(const CouplingItem *__restrict__ items, int64_t n_items,
-                                                       int kmax, Side rs, Side cs, const double *__restrict__ rh_row,
+                                                       int per_warp, Side rs, Side cs,
+                                                       const double *__restrict__ rh_row,
                                                        const double *__restrict__ rh_col,
                                                        const double *__restrict__ D, double *__restrict__ dt) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -582,32 +591,59 @@ __global__ void __launch_bounds__(128) coupling_kernel(const CouplingItem *__res
   if (item >= n_items) return;
   const CouplingItem it = items[item];
   const int kt = rs.k[it.t], ks = cs.k[it.s];
+  const int A8 = rup(kt, 8), B8 = rup(ks, 8), A4 = rup(kt, 4), B4 = rup(ks, 4);
+  const int LDA = coup_ld(kt), LDB = coup_ld(ks);
   extern __shared__ __align__(16) double sm[];
-  double *sD = sm + size_t(warp) * 4 * kmax * kmax;   // kt x ks
-  double *sT = sD + kt * ks;                            // kt x ks: D R^_s^T
-  double *sRt = sT + kt * ks;                           // kt x kt
-  double *sRs = sRt + kt * kt;                          // ks x ks
+  double *sD = sm + size_t(warp) * per_warp;   // A8 x LDB
+  double *sRs = sD + A8 * LDB;                 // B8 x LDB
+  double *sRt = sRs + B8 * LDB;                // A8 x LDA
+  double *sW = sRt + A8 * LDA;                 // A8 x LDB
   const double *Rt = rh_row + rs.rh_off[it.t];
   const double *Rs = rh_col + cs.rh_off[it.s];
-  for (int idx = lane; idx < kt * ks; idx += 32) cp8(&sD[idx], D + it.d_src + idx, true);
-  for (int idx = lane; idx < kt * kt; idx += 32) cp8(&sRt[idx], Rt + idx, true);
-  for (int idx = lane; idx < ks * ks; idx += 32) cp8(&sRs[idx], Rs + idx, true);
+  const double *Dg = D + it.d_src;
+  for (int idx = lane; idx < A8 * B8; idx += 32) {
+    const int i = idx / B8, j = idx % B8;
+    const bool v = i < kt && j < ks;
+    cp8(&sD[i * LDB + j], v ? (const void *)(Dg + i * ks + j) : (const void *)Dg, v);
+  }
+  for (int idx = lane; idx < B8 * B8; idx += 32) {
+    const int i = idx / B8, j = idx % B8;
+    const bool v = i < ks && j < ks;
+    cp8(&sRs[i * LDB + j], v ? (const void *)(Rs + i * ks + j) : (const void *)Rs, v);
+  }
+  for (int idx = lane; idx < A8 * A8; idx += 32) {
+    const int i = idx / A8, j = idx % A8;
+    const bool v = i < kt && j < kt;
+    cp8(&sRt[i * LDA + j], v ? (const void *)(Rt + i * kt + j) : (const void *)Rt, v);
+  }
   cp_commit();
   cp_wait_all();
   __syncwarp();
-  for (int idx = lane; idx < kt * ks; idx += 32) {
-    const int i = idx / ks, j = idx % ks;
-    double acc = 0.0;
-    for (int l = j; l < ks; l++) acc = fma(sD[i * ks + l], sRs[j * ks + l], acc);
-    sT[idx] = acc;
-  }
+  const int r = lane >> 2, q = lane & 3;
+  // W = D R^_s^T : A(m, kk) = D[m][kk], B(kk, n) = R^_s[n][kk]
+  for (int ti = 0; ti < A8 / 8; ti++)
+    for (int tj = 0; tj < B8 / 8; tj++) {
+      double acc[2] = {0.0, 0.0};
+      for (int k0 = 0; k0 < B4; k0 += 4)
+        dmma(acc, sD[(ti * 8 + r) * LDB + k0 + q], sRs[(tj * 8 + r) * LDB + k0 + q]);
+      sW[(ti * 8 + r) * LDB + tj * 8 + 2 * q] = acc[0];
+      sW[(ti * 8 + r) * LDB + tj * 8 + 2 * q + 1] = acc[1];
+    }
   __syncwarp();
-  for (int idx = lane; idx < kt * ks; idx += 32) {
-    const int i = idx / ks, j = idx % ks;
-    double acc = 0.0;
-    for (int l = i; l < kt; l++) acc = fma(sRt[i * kt + l], sT[l * ks + j], acc);
-    dt[it.dt_dst + idx] = acc;
-  }
+  // D~ = R^_t W : A(m, kk) = R^_t[m][kk], B(kk, n) = W[kk][n]
+  double *out = dt + it.dt_dst;
+  for (int ti = 0; ti < A8 / 8; ti++)
+    for (int tj = 0; tj < B8 / 8; tj++) {
+      double acc[2] = {0.0, 0.0};
+      for (int k0 = 0; k0 < A4; k0 += 4)
+        dmma(acc, sRt[(ti * 8 + r) * LDA + k0 + q], sW[(k0 + q) * LDB + tj * 8 + r]);
+      const int i = ti * 8 + r;
+#pragma unroll
+      for (int e = 0; e < 2; e++) {
+        const int j = tj * 8 + 2 * q + e;
+        if (i < kt && j < ks) out[i * ks + j] = acc[e];
+      }
+    }
 }
 
 // --------------------------------------------------------------------------
@@ -620,9 +656,10 @@ __global__ void __launch_bounds__(128) coupling_kernel(const CouplingItem *__res
 template <int NP>
 struct PairCfg {
   static constexpr int LD = NP + 4;       // conflict-free DMMA fragment loads
-  static constexpr int WARPS = NP / 16;   // warp w owns rows [16w, 16w + 16) of T and H
+  static constexpr int TM = (NP == 64) ? 1 : 2;   // 8-row tiles per warp
+  static constexpr int WARPS = NP / (8 * TM);     // warp w owns rows [8*TM*w, 8*TM*(w+1)) of T and H
   static constexpr int THREADS = WARPS * 32;
-  static constexpr int TM = 2, TN = NP / 8;
+  static constexpr int TN = NP / 8;
   static constexpr size_t SMEM = size_t(3) * NP * LD * sizeof(double);
   static constexpr int MIN_BLOCKS = (NP == 64) ? 2 : 4;
 };
@@ -637,6 +674,7 @@ struct PairArgs {
   const double *bb_in, *dt_in;        // level k-1 results
   const double *q_row, *q_col;
   double *s_val, *bb_out, *yr, *yc;   // yc: transposed column strips (general) / yr (symmetric)
+  int debug;                          // H2SP_PAIR_DEBUG (timing attribution only): 1 = skip scatter, 2 = skip loads
 };
 
 // Issue the cp.async copies of G_ts (level 0: C_ts; else the 2x2 arrangement of
@@ -678,20 +716,107 @@ __device__ __forceinline__ void pair_load_G(const PairArgs &A, const PairItem &i
   }
 }
 
+// Scatter of one lane's two horizontally adjacent H entries (row, col), (row, col+1)
+// of an 8x8 tile to the four parts of step (iii): nn -> S (+ mirror), bb -> next
+// level, bn -> row-strip panel, nb^T -> column-strip panel.  Whole tiles inside
+// one region (the common case) take the short branch; tiles that straddle
+// k_t / k_s or the matrix edge, and diagonal blocks in symmetric mode
+// (H_sym[i][j] = H[min][max], each upper entry written twice) go per element.
+struct PairDst {          // the destinations of one pair, kept in registers
+  int64_t s_dst, s_dst_m, bb_dst, yr_dst, yc_dst;
+  int32_t s_ld, s_ld_m, yr_ld, yc_ld;
+  int32_t nt, ns, kt, ks;
+  bool dsym;
+};
+
+__device__ __forceinline__ void scatter_pair2(const PairArgs &A, const PairDst &D, int row0, int col0, int row,
+                                              int col, double v0, double v1) {
+  const bool r_nn = row0 >= D.kt, r_bb = row0 + 8 <= D.kt;
+  const bool c_nn = col0 >= D.ks, c_bb = col0 + 8 <= D.ks;
+  if (row0 + 8 <= D.nt && col0 + 8 <= D.ns && !D.dsym && (r_nn || r_bb) && (c_nn || c_bb)) {
+    if (r_nn && c_nn) {
+      const int a = row - D.kt, b = col - D.ks;
+      if (D.s_dst >= 0) {
+        double *d = A.s_val + D.s_dst + int64_t(a) * D.s_ld + b;
+        d[0] = v0;
+        d[1] = v1;
+      }
+      if (D.s_dst_m >= 0) {
+        double *d = A.s_val + D.s_dst_m + int64_t(b) * D.s_ld_m + a;
+        d[0] = v0;
+        d[D.s_ld_m] = v1;
+      }
+    } else if (r_nn) {
+      if (D.yc_dst >= 0) {
+        double *d = A.yc + D.yc_dst + int64_t(col) * D.yc_ld + (row - D.kt);
+        d[0] = v0;
+        d[D.yc_ld] = v1;
+      }
+    } else if (c_bb) {
+      if (D.bb_dst >= 0) {
+        double *d = A.bb_out + D.bb_dst + row * D.ks + col;
+        d[0] = v0;
+        d[1] = v1;
+      }
+    } else if (D.yr_dst >= 0) {
+      double *d = A.yr + D.yr_dst + int64_t(row) * D.yr_ld + (col - D.ks);
+      d[0] = v0;
+      d[1] = v1;
+    }
+    return;
+  }
+  if (row >= D.nt) return;
+#pragma unroll 1
+  for (int e = 0; e < 2; e++) {
+    const int c = col + e;
+    if (c >= D.ns) continue;
+    const double v = e ? v1 : v0;
+    if (row >= D.kt) {
+      const int a = row - D.kt;
+      if (c >= D.ks) {
+        const int b = c - D.ks;
+        if (D.dsym) {
+          if (a <= b) {
+            A.s_val[D.s_dst + int64_t(a) * D.s_ld + b] = v;
+            A.s_val[D.s_dst + int64_t(b) * D.s_ld + a] = v;
+          }
+        } else {
+          if (D.s_dst >= 0) A.s_val[D.s_dst + int64_t(a) * D.s_ld + b] = v;
+          if (D.s_dst_m >= 0) A.s_val[D.s_dst_m + int64_t(b) * D.s_ld_m + a] = v;
+        }
+      } else if (D.yc_dst >= 0) {
+        A.yc[D.yc_dst + int64_t(c) * D.yc_ld + a] = v;
+      }
+    } else if (c < D.ks) {
+      if (D.bb_dst >= 0) {
+        if (D.dsym) {
+          if (row <= c) {
+            A.bb_out[D.bb_dst + row * D.ks + c] = v;
+            A.bb_out[D.bb_dst + c * D.ks + row] = v;
+          }
+        } else {
+          A.bb_out[D.bb_dst + row * D.ks + c] = v;
+        }
+      }
+    } else if (D.yr_dst >= 0) {
+      A.yr[D.yr_dst + int64_t(row) * D.yr_ld + (c - D.ks)] = v;
+    }
+  }
+}
+
 // Steps (iv)+(ii)+(iii) for one chunk of pairs (t, s_1..s_c) of block row t.
 // Shared memory: Q_t (resident), G, Q_s; G and Q_s of pair p+1 are fetched
 // (cp.async) while pair p computes.  Warp w computes rows [16w, 16w+16) of
 // T = Q_t^T G and keeps them in registers; H = T Q_s takes its A fragments
-// from T by quad shuffles, and H is scattered straight from the accumulators:
-//   nn -> S (t@k, s@k) [+ mirror], bb -> next level, bn -> row strip panel,
-//   nb^T -> column strip panel (general) / row strip panel of s (symmetric).
-// Diagonal blocks in symmetric mode use H_sym[i][j] = H[min(i,j)][max(i,j)]
-// (each upper element written to both places) -- the oracle's convention.
+// from T by quad shuffles.  The scatter of pair p's H is software-pipelined
+// into the T-GEMM of pair p+1 (one 8x8 tile per k-step), so the stores fill
+// issue slots between DMMAs instead of forming an idle phase.
 template <int NP>
 __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS) pair_kernel(PairArgs A) {
   using C = PairCfg<NP>;
   constexpr int LD = C::LD;
   constexpr int TN = C::TN;
+  constexpr int TM = C::TM;
   extern __shared__ __align__(16) double sm[];
   double *sQt = sm;
   double *sG = sm + NP * LD;
@@ -701,10 +826,8 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS)
   const int nt = A.rs.n[t], ktt = A.rs.k[t];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = lane >> 2, q = lane & 3;
-  const int m0 = warp * 16;
+  const int m0 = warp * 8 * TM;
   const int64_t lbase = lvl_off_d(A.L, A.level);
-  const bool diag_sym = false;
-  (void)diag_sym;
   // prologue: Q_t, G_0, Q_s0
   async_tile<NP, NP, LD>(sQt, A.q_row + A.rs.q_off[t], nt, nt, nt, A.items);
   {
@@ -714,44 +837,66 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS)
     async_tile<NP, NP, LD>(sQs, A.q_col + A.cs.q_off[it0.s], ns0, ns0, ns0, A.items);
   }
   cp_commit();
-  for (int p = ch.begin; p < ch.end; p++) {
+  double H[TM][TN][2];  // result of the previous pair, scattered during the next T-GEMM
+  PairDst prev;
+  bool have_prev = false;
+  for (int p = ch.begin; p <= ch.end; p++) {
+    if (p == ch.end) {  // drain: scatter the last pair
+      if (have_prev && !(A.debug & 1)) {
+#pragma unroll
+        for (int i = 0; i < TM; i++)
+#pragma unroll
+          for (int j = 0; j < TN; j++)
+            scatter_pair2(A, prev, m0 + i * 8, j * 8, m0 + i * 8 + r, j * 8 + 2 * q, H[i][j][0], H[i][j][1]);
+      }
+      break;
+    }
     const PairItem it = A.items[p];
     const int s = it.s;
-    const int ns = A.cs.n[s], kss = A.cs.k[s];
     cp_wait_all();
     __syncthreads();
-    // ---- T = Q_t^T G  (rows m0..m0+15, all NP columns)
-    double T[2][TN][2];
+    // ---- T = Q_t^T G (rows m0..m0+15), interleaved with the scatter of the previous H
+    double T[TM][TN][2];
     zero_acc(T);
-#pragma unroll 2
-    for (int k0 = 0; k0 < NP; k0 += 4) {
-      double a[2], b[TN];
+    const bool scat = have_prev && !(A.debug & 1);
 #pragma unroll
-      for (int i = 0; i < 2; i++) a[i] = sQt[(k0 + q) * LD + m0 + i * 8 + r];
+    for (int k0 = 0; k0 < NP; k0 += 4) {
+      double a[TM], b[TN];
+#pragma unroll
+      for (int i = 0; i < TM; i++) a[i] = sQt[(k0 + q) * LD + m0 + i * 8 + r];
 #pragma unroll
       for (int j = 0; j < TN; j++) b[j] = sG[(k0 + q) * LD + j * 8 + r];
 #pragma unroll
-      for (int i = 0; i < 2; i++)
+      for (int i = 0; i < TM; i++)
 #pragma unroll
         for (int j = 0; j < TN; j++) dmma(T[i][j], a[i], b[j]);
+      // tiles of the previous H spread over the NP/4 k-steps
+      constexpr int TPK = (TM * TN + NP / 4 - 1) / (NP / 4);
+#pragma unroll
+      for (int u = 0; u < TPK; u++) {
+        const int tile = (k0 / 4) * TPK + u;
+        if (tile < TM * TN && scat) {
+          const int i = tile / TN, j = tile % TN;
+          scatter_pair2(A, prev, m0 + i * 8, j * 8, m0 + i * 8 + r, j * 8 + 2 * q, H[i][j][0], H[i][j][1]);
+        }
+      }
     }
     __syncthreads();  // every warp is done with G
-    const bool more = p + 1 < ch.end;
+    const bool more = p + 1 < ch.end && !(A.debug & 2);
     if (more) {
       pair_load_G<NP>(A, A.items[p + 1], t, nt, lbase, sG);
       cp_commit();
     }
     // ---- H = T Q_s; A fragment (row m0+8i+r, col k0+q) lives in lane (r, (k0%8+q)/2), element q%2
-    double H[2][TN][2];
     zero_acc(H);
     const int src_lo = r * 4 + (q >> 1), src_hi = src_lo + 2;
 #pragma unroll
     for (int k0 = 0; k0 < NP; k0 += 4) {
-      const int jt = k0 >> 3;               // T tile column holding k0..k0+3
+      const int jt = k0 >> 3;
       const int srcl = (k0 & 4) ? src_hi : src_lo;
-      double a[2], b[TN];
+      double a[TM], b[TN];
 #pragma unroll
-      for (int i = 0; i < 2; i++) {
+      for (int i = 0; i < TM; i++) {
         const double e0 = __shfl_sync(0xffffffffu, T[i][jt][0], srcl);
         const double e1 = __shfl_sync(0xffffffffu, T[i][jt][1], srcl);
         a[i] = (q & 1) ? e1 : e0;
@@ -759,7 +904,7 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS)
 #pragma unroll
       for (int j = 0; j < TN; j++) b[j] = sQs[(k0 + q) * LD + j * 8 + r];
 #pragma unroll
-      for (int i = 0; i < 2; i++)
+      for (int i = 0; i < TM; i++)
 #pragma unroll
         for (int j = 0; j < TN; j++) dmma(H[i][j], a[i], b[j]);
     }
@@ -770,54 +915,21 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS)
       async_tile<NP, NP, LD>(sQs, A.q_col + A.cs.q_off[nx.s], nsx, nsx, nsx, A.items);
       cp_commit();
     }
-    // ---- step (iii): scatter from the accumulators
-    const bool dsym = A.sym && s == t;
-#pragma unroll
-    for (int i = 0; i < 2; i++) {
-      const int row = m0 + i * 8 + r;
-      if (row >= nt) continue;
-#pragma unroll
-      for (int j = 0; j < TN; j++) {
-#pragma unroll
-        for (int e = 0; e < 2; e++) {
-          const int col = j * 8 + 2 * q + e;
-          if (col >= ns) continue;
-          const double v = H[i][j][e];
-          if (row >= ktt) {
-            const int a = row - ktt;
-            if (col >= kss) {  // nn -> S
-              const int b = col - kss;
-              if (dsym) {
-                if (a <= b) {
-                  A.s_val[it.s_dst + int64_t(a) * it.s_ld + b] = v;
-                  A.s_val[it.s_dst + int64_t(b) * it.s_ld + a] = v;
-                }
-              } else {
-                if (it.s_dst >= 0) A.s_val[it.s_dst + int64_t(a) * it.s_ld + b] = v;
-                if (it.s_dst_m >= 0) A.s_val[it.s_dst_m + int64_t(b) * it.s_ld_m + a] = v;
-              }
-            } else if (it.yc_dst >= 0) {  // nb^T
-              A.yc[it.yc_dst + int64_t(col) * it.yc_ld + a] = v;
-            }
-          } else {
-            if (col < kss) {  // bb
-              if (it.bb_dst >= 0) {
-                if (dsym) {
-                  if (row <= col) {
-                    A.bb_out[it.bb_dst + row * kss + col] = v;
-                    A.bb_out[it.bb_dst + col * kss + row] = v;
-                  }
-                } else {
-                  A.bb_out[it.bb_dst + row * kss + col] = v;
-                }
-              }
-            } else if (it.yr_dst >= 0) {  // bn
-              A.yr[it.yr_dst + int64_t(row) * it.yr_ld + (col - kss)] = v;
-            }
-          }
-        }
-      }
-    }
+    prev.s_dst = it.s_dst;
+    prev.s_dst_m = it.s_dst_m;
+    prev.bb_dst = it.bb_dst;
+    prev.yr_dst = it.yr_dst;
+    prev.yc_dst = it.yc_dst;
+    prev.s_ld = it.s_ld;
+    prev.s_ld_m = it.s_ld_m;
+    prev.yr_ld = it.yr_ld;
+    prev.yc_ld = it.yc_ld;
+    prev.nt = nt;
+    prev.ns = A.cs.n[s];
+    prev.kt = ktt;
+    prev.ks = A.cs.k[s];
+    prev.dsym = A.sym && s == t;
+    have_prev = true;
   }
 }
 
@@ -939,63 +1051,33 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS) strip_kernel(StripA
 // pattern: expand the pattern once into shared memory, then stream the panel
 // out with coalesced stores.  Long panels are split over several CTAs.
 // --------------------------------------------------------------------------
-constexpr int CSR_PAT_MAX = 7680;      // pattern entries kept in shared memory (30 KB)
-constexpr int CSR_BLK_MAX = 1024;      // block descriptors staged in shared memory
-
-__device__ __forceinline__ int32_t csr_col_at(const CsrBlock *b, int nblk, int p) {
-  int lo = 0, hi = nblk - 1;  // last block with colpos <= p
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (b[mid].colpos <= p) lo = mid;
-    else hi = mid - 1;
-  }
-  return b[lo].col0 + (p - b[lo].colpos);
-}
-
 __global__ void __launch_bounds__(256) csr_cols_kernel(const CsrBlockRow *__restrict__ rows,
-                                                       const CsrBlock *__restrict__ blks, int32_t *__restrict__ col,
+                                                       const int32_t *__restrict__ pat, int32_t *__restrict__ col,
                                                        int splits) {
-  __shared__ int32_t pat[CSR_PAT_MAX];
-  __shared__ CsrBlock sb[CSR_BLK_MAX];
   const CsrBlockRow br = rows[blockIdx.x / splits];
   const int part = blockIdx.x % splits;
   const int rowlen = br.rowlen;
-  const bool blk_smem = br.nblk <= CSR_BLK_MAX;
-  const CsrBlock *b = blks + br.blk_begin;
-  if (blk_smem) {
-    for (int j = threadIdx.x; j < br.nblk; j += blockDim.x) {
-      cp8(&sb[j], &b[j], true);
-      cp8(reinterpret_cast<char *>(&sb[j]) + 8, reinterpret_cast<const char *>(&b[j]) + 8, true);
-    }
-    cp_commit();
-    cp_wait_all();
-    __syncthreads();
-    b = sb;
-  }
-  // this CTA writes whole rows [a0, a1) of the panel, column tile by column tile
+  // this CTA writes whole rows [a0, a1) of the panel: a broadcast copy of the
+  // block row's precomputed column pattern
   const int a0 = int((int64_t(br.m_r) * part) / splits), a1 = int((int64_t(br.m_r) * (part + 1)) / splits);
-  if (a1 <= a0) return;
+  const int32_t *src = pat + br.pat_off;
   int32_t *dst = col + br.p_base + int64_t(a0) * rowlen;
-  for (int t0 = 0; t0 < rowlen; t0 += CSR_PAT_MAX) {
-    const int tl = rowlen - t0 < CSR_PAT_MAX ? rowlen - t0 : CSR_PAT_MAX;
-    for (int p = threadIdx.x; p < tl; p += blockDim.x) pat[p] = csr_col_at(b, br.nblk, t0 + p);
-    __syncthreads();
-    for (int a = 0; a < a1 - a0; a++) {
-      int32_t *d = dst + int64_t(a) * rowlen + t0;
-      // scalar head up to 16-byte alignment, int4 body, scalar tail
-      const int head = int(((16 - (reinterpret_cast<uintptr_t>(d) & 15)) & 15) >> 2) < tl
-                           ? int(((16 - (reinterpret_cast<uintptr_t>(d) & 15)) & 15) >> 2)
-                           : tl;
-      if (threadIdx.x < head) d[threadIdx.x] = pat[threadIdx.x];
-      const int nv = (tl - head) >> 2;
-      int4 *dv = reinterpret_cast<int4 *>(d + head);
-      for (int v = threadIdx.x; v < nv; v += blockDim.x) {
-        const int p = head + 4 * v;
-        dv[v] = make_int4(pat[p], pat[p + 1], pat[p + 2], pat[p + 3]);
-      }
-      for (int p = head + 4 * nv + threadIdx.x; p < tl; p += blockDim.x) d[p] = pat[p];
+  constexpr int PER = 12;  // pattern entries held in registers per thread (chunk of 256 * PER columns)
+  for (int c0 = 0; c0 < rowlen; c0 += 256 * PER) {
+    int32_t v[PER];
+#pragma unroll
+    for (int i = 0; i < PER; i++) {
+      const int p = c0 + threadIdx.x + 256 * i;
+      v[i] = p < rowlen ? __ldg(src + p) : 0;
     }
-    __syncthreads();
+    for (int a = 0; a < a1 - a0; a++) {
+      int32_t *d = dst + int64_t(a) * rowlen + c0;
+#pragma unroll
+      for (int i = 0; i < PER; i++) {
+        const int p = threadIdx.x + 256 * i;
+        if (c0 + p < rowlen) d[p] = v[i];
+      }
+    }
   }
 }
 
@@ -1166,7 +1248,7 @@ static h2sp_status launch_strips(const StripArgs &a, int np, int64_t ntiles, cud
 // stream, so a build stays stream-ordered (and CUDA-graph capturable).
 struct DeviceAux {
   bool init = false;
-  cudaStream_t side[2];
+  cudaStream_t side[3];
   std::vector<cudaEvent_t> ev;
 };
 static DeviceAux g_aux[64];
@@ -1183,9 +1265,10 @@ static h2sp_status get_aux(int L, DeviceAux **out) {
     H2SP_CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     H2SP_CK(cudaStreamCreateWithPriority(&a.side[0], cudaStreamNonBlocking, hi));
     H2SP_CK(cudaStreamCreateWithPriority(&a.side[1], cudaStreamNonBlocking, lo));
+    H2SP_CK(cudaStreamCreateWithPriority(&a.side[2], cudaStreamNonBlocking, lo));  // strips
     a.init = true;
   }
-  while (int(a.ev.size()) < L + 8) {
+  while (int(a.ev.size()) < 3 * L + 12) {
     cudaEvent_t e;
     H2SP_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     a.ev.push_back(e);
@@ -1213,14 +1296,16 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   const int L = P->L;
   DeviceAux *aux = nullptr;
   if (h2sp_status e = get_aux(L, &aux)) return e;
-  cudaStream_t s1 = aux->side[0], s2 = aux->side[1];
+  cudaStream_t s1 = aux->side[0], s2 = aux->side[1], s3 = aux->side[2];
   static const bool serial = [] {
     const char *e = getenv("H2SP_SERIAL");  // debugging / attribution: run every launch on `stream`
     return e && e[0] == '1';
   }();
-  if (serial) s1 = s2 = st;
+  if (serial) s1 = s2 = s3 = st;
   cudaEvent_t ev_fork = aux->ev[0], ev_qr0 = aux->ev[1], ev_csr = aux->ev[2];
   auto ev_ready = [&](int k) { return aux->ev[3 + k]; };   // QR_k and couplings_{k-1} done
+  auto ev_pairs = [&](int k) { return aux->ev[4 + L + k]; };  // congruence of level k done (main stream)
+  cudaEvent_t ev_strips_done = aux->ev[5 + 2 * L];
   // The launch order (and so the index of h2sp_plan_launches / profiling
   // events) is: per level QR row, QR col, couplings, pairs, row strips,
   // column strips; then the CSR expansion.  Events 2i / 2i+1 bracket launch i
@@ -1237,7 +1322,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   static bool qr_attr = false;
   if (!qr_attr) {
     H2SP_CK(cudaFuncSetAttribute(qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    H2SP_CK(cudaFuncSetAttribute(coupling_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 64 * 64 * 8 + 1024));
+    H2SP_CK(cudaFuncSetAttribute(coupling_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     qr_attr = true;
   }
   // Launch indices are assigned in the plan's canonical order; precompute them.
@@ -1339,35 +1424,41 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     for (int64_t i = 0; i < (int64_t(1) << (L - k)); i++)
       kmax = std::max(kmax, std::max(P->k_row[lvl_off_d(L, k) + i], P->k_col[lvl_off_d(L, k) + i]));
     if (h2sp_status e = pre(s, li[k].coup)) return e;
-    const size_t per_warp = size_t(4) * kmax * kmax * 8;
-    const int ipc = int(std::max<size_t>(1, std::min<size_t>(4, (96 * 1024) / std::max<size_t>(per_warp, 1))));
-    coupling_kernel<<<unsigned((lp.n_coup + ipc - 1) / ipc), 32 * ipc, per_warp * ipc, s>>>(
-        (const CouplingItem *)(meta + lp.coup_off), lp.n_coup, kmax, rs, cs, rh_row, rh_col, in->coupling, dt);
+    const int per_warp = coup_warp_doubles(kmax, kmax);
+    const int ipc = std::max(1, std::min(4, int((96 * 1024) / (size_t(per_warp) * 8))));
+    coupling_kernel<<<unsigned((lp.n_coup + ipc - 1) / ipc), 32 * ipc, size_t(per_warp) * 8 * ipc, s>>>(
+        (const CouplingItem *)(meta + lp.coup_off), lp.n_coup, per_warp, rs, cs, rh_row, rh_col, in->coupling, dt);
     H2SP_CK(cudaGetLastError());
     return post(s, li[k].coup);
   };
 
-  // ---- fork: CSR index expansion on s2 (independent of all values)
-  H2SP_CK(cudaEventRecord(ev_fork, st));
-  H2SP_CK(cudaStreamWaitEvent(s2, ev_fork, 0));
-  if (csr_idx >= 0) {
-    if (h2sp_status e = pre(s2, csr_idx)) return e;
-    if (out->s_rowptr)
+  // ---- CSR index expansion on s2 (independent of all values).  It is a pure
+  //      HBM write stream, so it is started after the level-0 congruence (which
+  //      needs every SM slot) and overlaps the latency-bound upper levels.
+  auto csr = [&]() -> h2sp_status {
+    if (csr_idx >= 0) {
+      if (h2sp_status e = pre(s2, csr_idx)) return e;
+      if (out->s_rowptr)
+        H2SP_CK(cudaMemcpyAsync(out->s_rowptr, meta + P->rowptr_off, size_t(P->N + 1) * sizeof(int64_t),
+                                cudaMemcpyDeviceToDevice, s2));
+      if (out->s_col) {
+        const int splits = 4;
+        csr_cols_kernel<<<unsigned(P->n_csr_rows * splits), 256, 0, s2>>>(
+            (const CsrBlockRow *)(meta + P->csr_rows_off), (const int32_t *)(meta + P->csr_pat_off), out->s_col,
+            splits);
+        H2SP_CK(cudaGetLastError());
+      }
+      if (h2sp_status e = post(s2, csr_idx)) return e;
+    } else if (out->s_rowptr) {
       H2SP_CK(cudaMemcpyAsync(out->s_rowptr, meta + P->rowptr_off, size_t(P->N + 1) * sizeof(int64_t),
                               cudaMemcpyDeviceToDevice, s2));
-    if (out->s_col) {
-      const int splits = 4;
-      csr_cols_kernel<<<unsigned(P->n_csr_rows * splits), 256, 0, s2>>>(
-          (const CsrBlockRow *)(meta + P->csr_rows_off), (const CsrBlock *)(meta + P->csr_blocks_off), out->s_col,
-          splits);
-      H2SP_CK(cudaGetLastError());
     }
-    if (h2sp_status e = post(s2, csr_idx)) return e;
-  } else if (out->s_rowptr) {
-    H2SP_CK(cudaMemcpyAsync(out->s_rowptr, meta + P->rowptr_off, size_t(P->N + 1) * sizeof(int64_t),
-                            cudaMemcpyDeviceToDevice, s2));
-  }
-  H2SP_CK(cudaEventRecord(ev_csr, s2));
+    H2SP_CK(cudaEventRecord(ev_csr, s2));
+    return H2SP_OK;
+  };
+  H2SP_CK(cudaEventRecord(ev_fork, st));
+  H2SP_CK(cudaStreamWaitEvent(s2, ev_fork, 0));
+  if (h2sp_status e = csr()) return e;
   // ---- step (i) at level 0 on the main stream; the rest of the QR chain and
   //      all couplings on s1, overlapping the level-0 congruence
   if (h2sp_status e = qr(0, st)) return e;
@@ -1403,6 +1494,11 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       a.bb_out = bb;
       a.yr = yr;
       a.yc = yc;
+      static const int pair_debug = [] {
+        const char *e = getenv("H2SP_PAIR_DEBUG");
+        return e ? atoi(e) : 0;
+      }();
+      a.debug = pair_debug;
       if (h2sp_status e = pre(st, li[k].pairs)) return e;
       h2sp_status s;
       switch (pad16(lp.np_pair)) {
@@ -1414,7 +1510,13 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       if (s != H2SP_OK) return s;
       if (h2sp_status e = post(st, li[k].pairs)) return e;
     }
-    // ---- strips arriving from level k-1
+    // ---- strips arriving from level k-1, on s3 concurrently with the next
+    //      congruence: they need the level-(k-1) congruence (new strips) and Q_k
+    H2SP_CK(cudaEventRecord(ev_pairs(k), st));
+    if (lp.n_rstrips || lp.n_cstrips) {
+      H2SP_CK(cudaStreamWaitEvent(s3, ev_pairs(k - 1), 0));
+      H2SP_CK(cudaStreamWaitEvent(s3, ev_ready(k), 0));
+    }
     if (lp.n_rstrips) {
       StripArgs a;
       a.tiles = (const StripTile *)(meta + lp.rtiles_off);
@@ -1427,10 +1529,10 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       a.y_in = yr;
       a.y_out = yr;
       a.s_val = out->s_val;
-      if (h2sp_status e = pre(st, li[k].rstr)) return e;
-      h2sp_status s = launch_strips(a, lp.np_rstrip, lp.n_rstrips, st);
+      if (h2sp_status e = pre(s3, li[k].rstr)) return e;
+      h2sp_status s = launch_strips(a, lp.np_rstrip, lp.n_rstrips, s3);
       if (s != H2SP_OK) return s;
-      if (h2sp_status e = post(st, li[k].rstr)) return e;
+      if (h2sp_status e = post(s3, li[k].rstr)) return e;
     }
     if (lp.n_cstrips) {
       StripArgs a;
@@ -1444,15 +1546,17 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       a.y_in = yc;
       a.y_out = yc;
       a.s_val = out->s_val;
-      if (h2sp_status e = pre(st, li[k].cstr)) return e;
-      h2sp_status s = launch_strips(a, lp.np_cstrip, lp.n_cstrips, st);
+      if (h2sp_status e = pre(s3, li[k].cstr)) return e;
+      h2sp_status s = launch_strips(a, lp.np_cstrip, lp.n_cstrips, s3);
       if (s != H2SP_OK) return s;
-      if (h2sp_status e = post(st, li[k].cstr)) return e;
+      if (h2sp_status e = post(s3, li[k].cstr)) return e;
     }
   }
+  H2SP_CK(cudaEventRecord(ev_strips_done, s3));
   // ---- join
   if (L > 0) H2SP_CK(cudaStreamWaitEvent(st, ev_ready(L), 0));
   H2SP_CK(cudaStreamWaitEvent(st, ev_csr, 0));
+  H2SP_CK(cudaStreamWaitEvent(st, ev_strips_done, 0));
   if (launches) *launches = nl;
   return H2SP_OK;
 }

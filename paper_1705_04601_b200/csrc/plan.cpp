@@ -3,6 +3,7 @@
 // P:219-223), the block pattern of S, CSR row pointers
 // and every per-level device work list.  Integer work only, O(#blocks log).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <stdexcept>
@@ -529,7 +530,7 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
         if (rowlen > INT32_MAX) throw PlanError(H2SP_EUNSUPPORTED, "S row longer than 2^31");
         const int64_t r0 = blocks[j].roff, m_r = blocks[j].mr;
         for (; row < r0; row++) rowptr[row] = nnz;  // empty rows
-        CsrBlockRow br{r0, nnz, int32_t(m_r), int32_t(rowlen), int32_t(csr_blocks.size()), int32_t(e - j)};
+        CsrBlockRow br{r0, nnz, 0, int32_t(m_r), int32_t(rowlen), int32_t(csr_blocks.size()), int32_t(e - j)};
         csr_rows.push_back(br);
         int64_t colpos = 0;
         for (size_t x = j; x < e; x++) {
@@ -601,7 +602,8 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
     // items per CTA chunk sharing one rotating cluster: up to 8 (reuse of the
     // resident Q), fewer when a level has too few items to fill ~4 CTAs/SM
     auto chunk = [&](const auto &items, auto qof) {
-      const int CH = int(std::max<int64_t>(1, std::min<int64_t>(8, int64_t(items.size()) / (148 * 4))));
+      static const int CHMAX = getenv("H2SP_CHUNK") ? atoi(getenv("H2SP_CHUNK")) : 6;
+      const int CH = int(std::max<int64_t>(1, std::min<int64_t>(CHMAX, int64_t(items.size()) / (148 * 4))));
       std::vector<Chunk> ch;
       size_t j = 0;
       while (j < items.size()) {
@@ -732,6 +734,17 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
     }
     P->n_csr_rows = int64_t(csr_rows.size());
     P->n_csr_blocks = int64_t(csr_blocks.size());
+    // per block row column pattern (value-independent), 16-byte aligned rows
+    std::vector<int32_t> csr_pat;
+    for (auto &br : csr_rows) {
+      br.pat_off = int64_t(csr_pat.size());
+      for (int32_t j = 0; j < br.nblk; j++) {
+        const CsrBlock &b = csr_blocks[br.blk_begin + j];
+        for (int32_t e = 0; e < b.m_c; e++) csr_pat.push_back(b.col0 + e);
+      }
+      while (csr_pat.size() % 4) csr_pat.push_back(0);
+    }
+    P->csr_pat_off = mb.put(csr_pat);
     P->csr_rows_off = mb.put(csr_rows);
     P->csr_blocks_off = mb.put(csr_blocks);
     P->rowptr_off = mb.put(rowptr);
