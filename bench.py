@@ -225,6 +225,7 @@ def main():
     ap.add_argument("--no-oracle", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-n", type=int, default=16384, help="--impl reference sample size")
+    ap.add_argument("--timeline", action="store_true", help="print per-launch start/end of the last step (stderr)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -306,6 +307,14 @@ def main():
         for j in range(n_launch):
             per[j] += evs[i][2 * j].elapsed_time(evs[i][2 * j + 1])
     per /= args.steps
+    if args.timeline:
+        ev = evs[-1]
+        base_ev = ev[0]
+        for j, li in enumerate(launches):
+            st_ms = base_ev.elapsed_time(ev[2 * j])
+            en_ms = base_ev.elapsed_time(ev[2 * j + 1])
+            print(f"timeline {li['kind']:>11s} L{li['level']:<2d} start {st_ms * 1e3:8.1f} us  end {en_ms * 1e3:8.1f} us "
+                  f"dur {(en_ms - st_ms) * 1e3:7.1f} us", file=sys.stderr)
     kinds = {}
     for j, li in enumerate(launches):
         kinds[li["kind"]] = kinds.get(li["kind"], 0.0) + per[j]

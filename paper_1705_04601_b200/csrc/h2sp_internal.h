@@ -61,6 +61,8 @@ struct StripGroup {      // one frozen group (l, s) of a panel
   int32_t s_ld_t, pad_;
 };
 
+static_assert(sizeof(StripGroup) == 32, "staged as 4 x 8 bytes");
+
 struct StripTile {       // columns [c0, c1) of one panel; g0 = first group overlapping c0
   int32_t panel, c0, c1, g0;
 };

@@ -656,12 +656,12 @@ __global__ void __launch_bounds__(128) coupling_kernel(const CouplingItem *__res
 template <int NP>
 struct PairCfg {
   static constexpr int LD = NP + 4;       // conflict-free DMMA fragment loads
-  static constexpr int TM = (NP == 64) ? 1 : 2;   // 8-row tiles per warp
+  static constexpr int TM = 1;                    // 8-row tiles per warp
   static constexpr int WARPS = NP / (8 * TM);     // warp w owns rows [8*TM*w, 8*TM*(w+1)) of T and H
   static constexpr int THREADS = WARPS * 32;
   static constexpr int TN = NP / 8;
   static constexpr size_t SMEM = size_t(3) * NP * LD * sizeof(double);
-  static constexpr int MIN_BLOCKS = (NP == 64) ? 2 : 4;
+  static constexpr int MIN_BLOCKS = (NP == 64) ? 2 : 6;
 };
 
 struct PairArgs {
@@ -944,7 +944,8 @@ template <int NP, int TN>
 struct StripCfg {
   static constexpr int LDQ = NP + 4;
   static constexpr int LDZ = TN + 4;
-  static constexpr int NWM = NP / 16, NWN = TN / 16;
+  static constexpr int WN = 32;                    // warp tile 16 x 32
+  static constexpr int NWM = NP / 16, NWN = TN / WN;
   static constexpr int WARPS = NWM * NWN;
   static constexpr int THREADS = WARPS * 32;
   static constexpr size_t SMEM = (size_t(NP) * LDQ + size_t(NP) * LDZ) * sizeof(double) + TN * 16 + 64;
@@ -973,6 +974,8 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS) strip_kernel(StripA
   int32_t *src2 = src1 + TN;
   int32_t *tld = reinterpret_cast<int32_t *>(src2 + TN);           // unused padding slot
   (void)tld;
+  __shared__ StripGroup sg[TN + 1];            // groups overlapping this tile (<= TN of them)
+  __shared__ int s_ng;
   const StripTile tile = A.tiles[blockIdx.x];
   const StripPanel pn = A.panels[tile.panel];
   const int q = pn.q;
@@ -981,20 +984,30 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS) strip_kernel(StripA
   const int k1 = A.sd.k[c1], k2 = A.sd.k[c1 + 1];
   const int ncol = tile.c1 - tile.c0;
   async_tile<NP, NP, C::LDQ>(sQ, A.q + A.sd.q_off[q], n, n, n, A.tiles);
+  // stage the (at most TN) groups overlapping [c0, c1) in one batch
+  {
+    const int gmax = min(pn.gend - tile.g0, TN + 1);
+    if (threadIdx.x == 0) s_ng = gmax;
+    for (int g = threadIdx.x; g < gmax * 4; g += blockDim.x)
+      cp8(reinterpret_cast<char *>(&sg[g >> 2]) + 8 * (g & 3),
+          reinterpret_cast<const char *>(&A.groups[tile.g0 + (g >> 2)]) + 8 * (g & 3), true);
+  }
   cp_commit();
+  cp_wait_all();
+  __syncthreads();
   // per-column source / destination maps
   for (int cc = threadIdx.x; cc < TN; cc += blockDim.x) {
     int32_t a1 = -1, a2 = -1;
     int64_t td = -1;
     if (cc < ncol) {
       const int c = tile.c0 + cc;
-      int g = tile.g0;
-      while (g + 1 < pn.gend && A.groups[g + 1].col0 <= c) g++;
-      const StripGroup sg = A.groups[g];
-      const int b = c - sg.col0;
-      if (sg.pos_c1 >= 0) a1 = sg.pos_c1 + b;
-      if (sg.pos_c2 >= 0) a2 = sg.pos_c2 + b;
-      if (sg.s_dst_t >= 0) td = sg.s_dst_t + int64_t(b) * sg.s_ld_t;
+      int g = 0;
+      while (g + 1 < s_ng && sg[g + 1].col0 <= c) g++;
+      const StripGroup gr = sg[g];
+      const int b = c - gr.col0;
+      if (gr.pos_c1 >= 0) a1 = gr.pos_c1 + b;
+      if (gr.pos_c2 >= 0) a2 = gr.pos_c2 + b;
+      if (gr.s_dst_t >= 0) td = gr.s_dst_t + int64_t(b) * gr.s_ld_t;
     }
     src1[cc] = a1;
     src2[cc] = a2;
@@ -1015,10 +1028,10 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS) strip_kernel(StripA
   cp_wait_all();
   __syncthreads();
   const int warp = threadIdx.x >> 5;
-  const int m0 = (warp / C::NWN) * 16, n0 = (warp % C::NWN) * 16;
-  double acc[2][2][2];
+  const int m0 = (warp / C::NWN) * 16, n0 = (warp % C::NWN) * C::WN;
+  double acc[2][C::WN / 8][2];
   zero_acc(acc);
-  warp_gemm<C::LDQ, C::LDZ, 2, 2, true>(sQ, sZ, m0, n0, NP, acc);
+  warp_gemm<C::LDQ, C::LDZ, 2, C::WN / 8, true>(sQ, sZ, m0, n0, NP, acc);
   __syncthreads();
   warp_store<C::LDZ>(sZ, m0, n0, acc);
   __syncthreads();
@@ -1037,10 +1050,12 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS) strip_kernel(StripA
     }
   }
   if (mq > 0) {
-    for (int cc = warp; cc < ncol; cc += C::WARPS) {
+    // transposed blocks: element (column cc, frozen row a) -> S[tdst[cc] + a]; consecutive
+    // threads take consecutive a (coalesced runs of m_q), then the next column
+    for (int idx = threadIdx.x; idx < mq * ncol; idx += blockDim.x) {
+      const int cc = idx / mq, a = idx - cc * mq;
       const int64_t d = tdst[cc];
-      if (d < 0) continue;
-      for (int a = lane; a < mq; a += 32) A.s_val[d + a] = sZ[(kq + a) * C::LDZ + cc];
+      if (d >= 0) A.s_val[d + a] = sZ[(kq + a) * C::LDZ + cc];
     }
   }
 }
@@ -1216,7 +1231,7 @@ static h2sp_status launch_pairs(const PairArgs &a, int64_t nchunks, cudaStream_t
   return H2SP_OK;
 }
 
-constexpr int STRIP_TN = 64;  // = plan.cpp STRIP_TN
+constexpr int STRIP_TN = 128;  // = plan.cpp STRIP_TN
 
 template <int NP>
 static h2sp_status launch_strips1(const StripArgs &a, int64_t ntiles, cudaStream_t st) {
@@ -1362,8 +1377,9 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
         kmax = std::max(kmax, int(kk[c]));
       }
       if (kmax <= 32) {
-        // spread small levels over many SMs (1 warp per CTA) to keep the latency chain short
-        const int wpb = std::max(1, std::min({4, int((96 * 1024) / (size_t(per_warp_reg) * 8)), M / 148}));
+        // 4 independent warps (clusters) per CTA: same per-cluster latency, a quarter of
+        // the SM slots taken from the concurrent congruence
+        const int wpb = std::max(1, std::min(4, int((96 * 1024) / (size_t(per_warp_reg) * 8))));
         const unsigned grid = unsigned((M + wpb - 1) / wpb);
         const size_t smem = size_t(per_warp_reg) * 8 * wpb;
         const int kp = kmax <= 8 ? 8 : kmax <= 16 ? 16 : kmax <= 24 ? 24 : 32;
@@ -1456,13 +1472,15 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     H2SP_CK(cudaEventRecord(ev_csr, s2));
     return H2SP_OK;
   };
-  H2SP_CK(cudaEventRecord(ev_fork, st));
-  H2SP_CK(cudaStreamWaitEvent(s2, ev_fork, 0));
-  if (h2sp_status e = csr()) return e;
   // ---- step (i) at level 0 on the main stream; the rest of the QR chain and
   //      all couplings on s1, overlapping the level-0 congruence
   if (h2sp_status e = qr(0, st)) return e;
   H2SP_CK(cudaEventRecord(ev_qr0, st));
+  // CSR expansion after QR0 (which is on the critical path): overlaps the
+  // compute-bound level-0 congruence
+  H2SP_CK(cudaStreamWaitEvent(s2, ev_qr0, 0));
+  if (h2sp_status e = csr()) return e;
+  (void)ev_fork;
   H2SP_CK(cudaStreamWaitEvent(s1, ev_qr0, 0));
   for (int k = 0; k <= L; k++) {
     if (k < L) {
