@@ -226,6 +226,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-n", type=int, default=16384, help="--impl reference sample size")
     ap.add_argument("--timeline", action="store_true", help="print per-launch start/end of the last step (stderr)")
+    ap.add_argument("--graph", type=int, default=0, help="1: replay the step as one captured CUDA graph")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -318,7 +319,9 @@ def main():
     kinds = {}
     for j, li in enumerate(launches):
         kinds[li["kind"]] = kinds.get(li["kind"], 0.0) + per[j]
-    top = int(np.argmax(per))
+    # dominant kernel = the launch with the most algorithmic work (the level-0
+    # congruence); durations of concurrent launches are not comparable
+    top = int(np.argmax([l["flops"] for l in launches]))
     li = launches[top]
     peaks = _peaks()
     ai = li["flops"] / li["bytes"] if li["bytes"] else float("inf")

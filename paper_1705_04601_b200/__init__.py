@@ -142,7 +142,7 @@ class Plan:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h:
+        if h and lib is not None:
             lib.h2sp_plan_destroy(h)
             self.handle = None
 
@@ -238,6 +238,27 @@ class Sparsifier:
         _check(lib.h2sp_build(self.plan.handle, ctypes.byref(self._abi_inputs()), ctypes.byref(out), self.ws_ptr,
                               self.ws_bytes, _stream_handle(stream)), "h2sp_build")
         return self.outputs
+
+    def capture(self, fn=None):
+        """Capture one h2sp_build (plus ``fn()``, e.g. the applies) into a CUDA
+        graph on a side stream; returns the torch.cuda.CUDAGraph (replay() runs
+        it on the current stream's device).  The library's internal side
+        streams fork from and join back into the captured stream."""
+        import torch
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.build(stream=s)     # warm-up on the capture stream (lazy init outside capture)
+            if fn is not None:
+                fn()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            self.build(stream=s)
+            if fn is not None:
+                fn()
+        return g
 
     def build_profiled(self, events, stream=None):
         """h2sp_build_ex: records events[i] (torch.cuda.Event) before launch i and

@@ -364,6 +364,36 @@ __global__ void __launch_bounds__(128) qr_kernel(Side sd, int L, int level, int 
     }
 }
 
+// Warp all-reduce of a P-vector (P a power of two, 8..32) by reduce-scatter +
+// broadcast: log2(P) halving rounds (P-1 shuffles), the remaining rounds on a
+// single value, then P broadcasts -- instead of 5 full butterfly rounds per entry.
+template <int P>
+__device__ __forceinline__ void warp_allreduce_vec(double (&w)[P], int lane) {
+  int len = P;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const bool bit = (lane & o) != 0;
+    if (len > 1) {
+      const int half = len >> 1;
+#pragma unroll
+      for (int i = 0; i < P / 2; i++) {
+        if (i < half) {
+          const double send = bit ? w[i] : w[i + half];
+          const double keep = bit ? w[i + half] : w[i];
+          w[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      len = half;
+    } else {
+      w[0] += __shfl_xor_sync(0xffffffffu, w[0], o);
+    }
+  }
+  // lane holds the sum of component c(lane); component c lives in lane c * (32 / P)
+  const double total = w[0];
+#pragma unroll
+  for (int c = 0; c < P; c++) w[c] = __shfl_sync(0xffffffffu, total, c * (32 / P));
+}
+
 // --------------------------------------------------------------------------
 // Register-resident variant of the same QR completion for k <= KP <= 32 and
 // n <= 32 * NR: lane l holds rows l, l+32 of X; the Householder loop is fully
@@ -409,11 +439,20 @@ __global__ void __launch_bounds__(128) qr_reg_kernel(Side sd, int L, int level, 
       for (int c = 0; c < KP; c++) x[u][c] = (i < n && c < k) ? __ldg(R + i * k + c) : 0.0;
     }
   } else {
+    // X = [R^_c1 T[:k1]; R^_c2 T[k1:]]: stage T and both R^ with one batched copy
+    extern __shared__ __align__(16) double smx[];
     const int64_t c1 = lvl_off_d(L, level - 1) + 2 * ci, c2 = c1 + 1;
     const int k1 = sd.k[c1], k2 = sd.k[c2];
+    double *sT = smx + size_t(warp) * per_warp, *sR1 = sT + n * k, *sR2 = sR1 + k1 * k1;
     const double *T = transfer + sd.tr_off[cl];  // n x k
     const double *R1 = rh + sd.rh_off[c1];
     const double *R2 = rh + sd.rh_off[c2];
+    for (int idx = lane; idx < n * k; idx += 32) cp8(&sT[idx], T + idx, true);
+    for (int idx = lane; idx < k1 * k1; idx += 32) cp8(&sR1[idx], R1 + idx, true);
+    for (int idx = lane; idx < k2 * k2; idx += 32) cp8(&sR2[idx], R2 + idx, true);
+    cp_commit();
+    cp_wait_all();
+    __syncwarp();
 #pragma unroll
     for (int u = 0; u < NR; u++) {
       const int i = lane + 32 * u;
@@ -422,16 +461,17 @@ __global__ void __launch_bounds__(128) qr_reg_kernel(Side sd, int L, int level, 
       if (i < n) {
         const bool first = i < k1;
         const int ii = first ? i : i - k1, kk = first ? k1 : k2, roff = first ? 0 : k1;
-        const double *Rr = first ? R1 : R2;
+        const double *Rr = first ? sR1 : sR2;
         for (int l = ii; l < kk; l++) {
           const double rv = Rr[ii * kk + l];
-          const double *Trow = T + (roff + l) * k;
+          const double *Trow = sT + (roff + l) * k;
 #pragma unroll
           for (int c = 0; c < KP; c++)
-            if (c < k) x[u][c] = fma(rv, __ldg(Trow + c), x[u][c]);
+            if (c < k) x[u][c] = fma(rv, Trow[c], x[u][c]);
         }
       }
     }
+    __syncwarp();
   }
   // shared memory: V (unit lower trapezoidal, zero padded), T (tau on the diagonal), G/M
   extern __shared__ __align__(16) double sm[];
@@ -474,19 +514,16 @@ __global__ void __launch_bounds__(128) qr_reg_kernel(Side sd, int L, int level, 
       v[u] = (i == j) ? 1.0 : ((t != 0.0 && i > j && i < n) ? x[u][0] / div : 0.0);
     }
     if (t != 0.0) {
-      double w[KP];
+      constexpr int P2 = KP <= 8 ? 8 : KP <= 16 ? 16 : 32;
+      double w[P2];
 #pragma unroll
-      for (int c = 1; c < KP; c++) {
+      for (int c = 0; c < P2; c++) {
         w[c] = 0.0;
-        if (c < w_left)
+        if (c >= 1 && c < KP && c < w_left)
 #pragma unroll
-          for (int u = 0; u < NR; u++) w[c] = fma(v[u], x[u][c], w[c]);
+          for (int u = 0; u < NR; u++) w[c] = fma(v[u], x[u][c < KP ? c : 0], w[c]);
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int c = 1; c < KP; c++)
-          if (c < w_left) w[c] += __shfl_xor_sync(0xffffffffu, w[c], o);
+      warp_allreduce_vec<P2>(w, lane);
 #pragma unroll
       for (int c = 1; c < KP; c++)
         if (c < w_left) {
@@ -1263,7 +1300,7 @@ static h2sp_status launch_strips(const StripArgs &a, int np, int64_t ntiles, cud
 // stream, so a build stays stream-ordered (and CUDA-graph capturable).
 struct DeviceAux {
   bool init = false;
-  cudaStream_t side[3];
+  cudaStream_t side[4];    // QR/coupling chain, CSR, strips, main chain
   std::vector<cudaEvent_t> ev;
 };
 static DeviceAux g_aux[64];
@@ -1280,7 +1317,10 @@ static h2sp_status get_aux(int L, DeviceAux **out) {
     H2SP_CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     H2SP_CK(cudaStreamCreateWithPriority(&a.side[0], cudaStreamNonBlocking, hi));
     H2SP_CK(cudaStreamCreateWithPriority(&a.side[1], cudaStreamNonBlocking, lo));
-    H2SP_CK(cudaStreamCreateWithPriority(&a.side[2], cudaStreamNonBlocking, lo));  // strips
+    // priorities: QR/coupling chain (feeds every level) > main chain = strips > CSR
+    const int mid = hi < lo ? hi + 1 : hi;
+    H2SP_CK(cudaStreamCreateWithPriority(&a.side[2], cudaStreamNonBlocking, mid));  // strips
+    H2SP_CK(cudaStreamCreateWithPriority(&a.side[3], cudaStreamNonBlocking, mid));  // main chain
     a.init = true;
   }
   while (int(a.ev.size()) < 3 * L + 12) {
@@ -1312,11 +1352,21 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   DeviceAux *aux = nullptr;
   if (h2sp_status e = get_aux(L, &aux)) return e;
   cudaStream_t s1 = aux->side[0], s2 = aux->side[1], s3 = aux->side[2];
+  const cudaStream_t user_st = st;
+  cudaEvent_t ev_begin = aux->ev[6 + 2 * L], ev_end = aux->ev[7 + 2 * L];
   static const bool serial = [] {
     const char *e = getenv("H2SP_SERIAL");  // debugging / attribution: run every launch on `stream`
     return e && e[0] == '1';
   }();
-  if (serial) s1 = s2 = s3 = st;
+  if (serial) {
+    s1 = s2 = s3 = st;
+  } else {
+    // the main chain runs on an internal high-priority stream forked from the
+    // caller's stream (the CSR stream has the lowest priority and fills gaps)
+    H2SP_CK(cudaEventRecord(ev_begin, user_st));
+    st = aux->side[3];
+    H2SP_CK(cudaStreamWaitEvent(st, ev_begin, 0));
+  }
   cudaEvent_t ev_fork = aux->ev[0], ev_qr0 = aux->ev[1], ev_csr = aux->ev[2];
   auto ev_ready = [&](int k) { return aux->ev[3 + k]; };   // QR_k and couplings_{k-1} done
   auto ev_pairs = [&](int k) { return aux->ev[4 + L + k]; };  // congruence of level k done (main stream)
@@ -1372,7 +1422,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
           rs_ = kk[c1] * kk[c1] + kk[c1 + 1] * kk[c1 + 1];
         }
         per_warp = std::max(per_warp, qr_warp_doubles(nn[c], kk[c], rs_));
-        per_warp_reg = std::max(per_warp_reg, qr_reg_warp_doubles(nn[c], kk[c]));
+        per_warp_reg = std::max(per_warp_reg, std::max(qr_reg_warp_doubles(nn[c], kk[c]), nn[c] * kk[c] + rs_ + 2));
         nmax = std::max(nmax, int(nn[c]));
         kmax = std::max(kmax, int(kk[c]));
       }
@@ -1575,6 +1625,10 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   if (L > 0) H2SP_CK(cudaStreamWaitEvent(st, ev_ready(L), 0));
   H2SP_CK(cudaStreamWaitEvent(st, ev_csr, 0));
   H2SP_CK(cudaStreamWaitEvent(st, ev_strips_done, 0));
+  if (st != user_st) {
+    H2SP_CK(cudaEventRecord(ev_end, st));
+    H2SP_CK(cudaStreamWaitEvent(user_st, ev_end, 0));
+  }
   if (launches) *launches = nl;
   return H2SP_OK;
 }
