@@ -265,7 +265,7 @@ CONFIGS: Dict[int, dict] = {
     3: dict(N=262144, points="cube", kernel=dict(kind="invh", diag_add=1.0), B=64, r=24, eta=0.7,
             symmetric=True, method="cheb"),
     4: dict(N=1048576, points="sphere", kernel=dict(kind="laplace"), B=64, r=32, eta=0.7,
-            symmetric=False, method="cheb"),
+            symmetric=False, method="cheb", orthonormalize=True),
     5: dict(N=4194304, points="cube", kernel=dict(kind="exp", ell=0.05, nugget=1e-2), B=128, r=32, eta=0.7,
             symmetric=True, method="cheb"),
 }
@@ -360,6 +360,8 @@ def make_config(idx: int, seed: Optional[int] = None, N: Optional[int] = None, m
         h2 = _svd_h2(x, L, B, r, near0, adm, kspec, sym)
     else:
         h2 = _cheb_h2(x, L, B, r, near0, adm, kspec, lo, hi, sym, with_close)
+        if cfg.get("orthonormalize"):
+            orthonormalize_h2(h2)
     h2.meta.update(config=idx, seed=seed, N=N, eta=eta, method=meth, kernel=kspec)
     return h2
 
@@ -529,6 +531,64 @@ def _svd_h2(x, L, B, r, near0, adm, kspec, sym) -> H2Input:
     return H2Input(L=L, B=B, symmetric=sym, rank_row=rank, rank_col=rank, leaf_row=leaf, leaf_col=leaf,
                    transfer_row=transfer, transfer_col=transfer, near=near0, close=close, adm=adm,
                    coupling=coupling, points=x)
+
+
+def orthonormalize_h2(h2: H2Input) -> H2Input:
+    """Rewrite the H^2 parameters with orthonormal nested bases of the SAME rank
+    (SVD-based H^2 orthogonalisation, bottom-up): R_t = W_t Z_t, transfers
+    T'_p = U_p from [Z_c1 T_p^(1); Z_c2 T_p^(2)] = U_p Z_p, couplings
+    D' = Z_t D Z_s^T.  The represented matrix is unchanged in exact arithmetic;
+    3-D tensor interpolation restricted to a surface (config 4) gives
+    numerically rank-deficient bases (cond ~1e8) whose Householder complement
+    is ill-determined, orthonormal bases are perfectly conditioned."""
+    L = h2.L
+    ncl = n_clusters(L)
+
+    def side(leaf, tr, rank):
+        Z = [None] * ncl
+        new_leaf, new_tr = [], [None] * ncl
+        for i in range(1 << L):
+            R = np.asarray(leaf[i])
+            if R.shape[1]:
+                U, S, Vt = np.linalg.svd(R, full_matrices=False)
+                new_leaf.append(U)
+                Z[cid(L, 0, i)] = S[:, None] * Vt
+            else:
+                new_leaf.append(R.copy())
+                Z[cid(L, 0, i)] = np.zeros((0, 0))
+        for k in range(1, L + 1):
+            for i in range(1 << (L - k)):
+                p = cid(L, k, i)
+                c1, c2 = cid(L, k - 1, 2 * i), cid(L, k - 1, 2 * i + 1)
+                T = tr[p]
+                k1 = int(rank[c1])
+                X = np.vstack([Z[c1] @ T[:k1], Z[c2] @ T[k1:]])
+                if X.shape[1]:
+                    U, S, Vt = np.linalg.svd(X, full_matrices=False)
+                    new_tr[p] = U
+                    Z[p] = S[:, None] * Vt
+                else:
+                    new_tr[p] = X.copy()
+                    Z[p] = np.zeros((0, 0))
+        return new_leaf, new_tr, Z
+
+    lr, tr_r, Zr = side(h2.leaf_row, h2.transfer_row, h2.rank_row)
+    if h2.symmetric:
+        lc, tr_c, Zc = lr, tr_r, Zr
+    else:
+        lc, tr_c, Zc = side(h2.leaf_col, h2.transfer_col, h2.rank_col)
+    for k in range(L):
+        base = lvl_off(L, k)
+        for j, (t, s) in enumerate(h2.adm[k]):
+            h2.coupling[k][j] = Zr[base + int(t)] @ h2.coupling[k][j] @ Zc[base + int(s)].T
+        if h2.symmetric:
+            key = {(int(t), int(s)): j for j, (t, s) in enumerate(h2.adm[k])}
+            for j, (t, s) in enumerate(h2.adm[k]):
+                if t > s:
+                    h2.coupling[k][j] = h2.coupling[k][key[(int(s), int(t))]].T.copy()
+    h2.leaf_row, h2.transfer_row, h2.leaf_col, h2.transfer_col = lr, tr_r, lc, tr_c
+    h2.meta["orthonormalized"] = True
+    return h2
 
 
 def _random_ranks(L, B, rng, lo_frac=0.0, hi_frac=1.0, zero_prob=0.15, full_prob=0.1, max_rank=None):

@@ -94,7 +94,11 @@ typedef struct {
   int64_t leaf_row, transfer_row, leaf_col, transfer_col; /* input lengths    */
   int64_t close, coupling;     /* input lengths: n_near*B*B, sum k_t*k_s        */
   int64_t q_row, q_col;        /* output lengths of the Q batches (sum n_t^2)  */
-  int64_t s_nnz;               /* nonzeros of S                                */
+  int64_t s_nnz;               /* nonzeros of S (of this shard's rows)         */
+  int64_t s_rows;              /* rows of S held by this plan (N if world = 1) */
+  int64_t rank, world;         /* shard of a sharded plan (0, 1 otherwise)     */
+  int64_t first_leaf;          /* first leaf of this shard's subtree           */
+  int64_t n_leaves_local;      /* leaves of this shard's subtree               */
   int64_t s_blocks;            /* blocks (t@i, s@j) of S                       */
   int64_t workspace_bytes;     /* device workspace for h2sp_build (incl. meta) */
   int64_t meta_bytes;          /* leading part of every workspace: work lists  */
@@ -126,8 +130,9 @@ typedef struct {
  *   q_row[q_row], q_col[q_col]: Q_t (n_t x n_t, row-major) concatenated by
  *     level-major id (offsets from h2sp_plan_offsets); q_col ignored if
  *     symmetric (U == V, use q_row).
- *   s_rowptr[N+1] (int64), s_col[s_nnz] (int32), s_val[s_nnz]: S in CSR, rows
- *     and columns in S order, columns ascending.  s_col / s_rowptr may be NULL
+ *   s_rowptr[s_rows+1] (int64), s_col[s_nnz] (int32), s_val[s_nnz]: S in CSR,
+ *     rows and columns in S order, columns ascending (a sharded plan holds its
+ *     local rows only, see h2sp_plan_create_shard).  s_col / s_rowptr may be NULL
  *     to skip writing the (value-independent) index arrays. */
 typedef struct {
   double *q_row;
@@ -141,13 +146,27 @@ typedef struct {
  * sizes, S offsets, the S block pattern, CSR row pointers and the per-level
  * work lists.  flags: reserved, pass 0. */
 h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out);
+/* Sharded plan: rank `rank` of `world` (a power of two <= 2^L)
+ * owns the top-level subtree of cluster `rank` at the partition level
+ * Lp = L - log2(world): S rows of its clusters, the congruences whose row cluster
+ * is owned (general mode) or whose row or column cluster is owned (symmetric:
+ * cross pairs are computed by both owners, each keeping its rows), and the strip
+ * columns landing in owned rows.  Q and the couplings are computed for every
+ * cluster on every rank (no exchange needed).  S is returned with local rows:
+ * the owned clusters' rows in S order (h2sp_plan_local_rows); column indices
+ * stay global.  world = 1 is h2sp_plan_create.  H2SP_EUNSUPPORTED if any cluster
+ * above Lp has a nonzero local size (the remainder gather is not implemented). */
+h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world, int flags, h2sp_plan *out);
+/* Local S row offset of every cluster owned by the shard (-1 otherwise); row /
+ * column side (host arrays of n_clusters entries, either may be NULL). */
+h2sp_status h2sp_plan_local_rows(h2sp_plan plan, int64_t *loc_off_row, int64_t *loc_off_col);
 h2sp_status h2sp_plan_sizes(h2sp_plan plan, h2sp_sizes *out);
 /* Host copies of per-cluster data (each array has n_clusters entries; any
  * pointer may be NULL): S-order offsets (row / column side), offsets of Q_t in
  * q_row / q_col, local sizes n_t (row / column). */
 h2sp_status h2sp_plan_offsets(h2sp_plan plan, int64_t *s_off_row, int64_t *s_off_col, int64_t *q_off_row,
                               int64_t *q_off_col, int64_t *n_row, int64_t *n_col);
-/* Host copy of the symbolic CSR pattern of S: rowptr[N+1] (int64) and, if
+/* Host copy of the symbolic CSR pattern of S: rowptr[s_rows+1] (int64) and, if
  * col != NULL, col[s_nnz] (int32) -- identical to what h2sp_build writes into
  * s_rowptr / s_col.  Host only (no device needed). */
 h2sp_status h2sp_plan_pattern(h2sp_plan plan, int64_t *rowptr, int32_t *col);
@@ -208,6 +227,8 @@ int64_t h2sp_apply_ws_bytes(h2sp_plan plan, int nrhs);
 
 /* y = U^T b: b is N x nrhs column-major in tree order (leading
  * dimension ldb), y is N x nrhs column-major in S order (row side, ldy).
+ * Sharded plan: b holds the shard's leaves only (n_leaves_local * B rows) and y
+ * its local S rows (s_rows); likewise for h2sp_apply_V.
  * q_row as produced by h2sp_build.  Leaves to root: z = Q_t^T x_t,
  * z[k_t:] -> y, z[:k_t] -> parent's local vector. */
 h2sp_status h2sp_apply_Ut(h2sp_plan plan, const double *q_row, const double *b, int64_t ldb, double *y,

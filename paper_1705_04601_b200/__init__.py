@@ -39,7 +39,8 @@ class _Structure(ctypes.Structure):
 
 class _Sizes(ctypes.Structure):
     _fields_ = [(n, _i64) for n in ("n", "n_clusters", "leaf_row", "transfer_row", "leaf_col", "transfer_col", "close",
-                                    "coupling", "q_row", "q_col", "s_nnz", "s_blocks", "workspace_bytes", "meta_bytes",
+                                    "coupling", "q_row", "q_col", "s_nnz", "s_rows", "rank", "world", "first_leaf",
+                                    "n_leaves_local", "s_blocks", "workspace_bytes", "meta_bytes",
                                     "levels_active", "launches")] + \
                [(n, _f64) for n in ("flops", "bytes", "flops_congruence", "flops_strips")]
 
@@ -65,6 +66,9 @@ lib.h2sp_status_str.restype = ctypes.c_char_p
 lib.h2sp_status_str.argtypes = [_st]
 lib.h2sp_last_error.restype = ctypes.c_char_p
 lib.h2sp_plan_create.argtypes = [ctypes.POINTER(_Structure), ctypes.c_int, ctypes.POINTER(_vp)]
+lib.h2sp_plan_create_shard.argtypes = [ctypes.POINTER(_Structure), ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       ctypes.POINTER(_vp)]
+lib.h2sp_plan_local_rows.argtypes = [_vp, _P_i64, _P_i64]
 lib.h2sp_plan_sizes.argtypes = [_vp, ctypes.POINTER(_Sizes)]
 lib.h2sp_plan_offsets.argtypes = [_vp] + [_P_i64] * 6
 lib.h2sp_plan_pattern.argtypes = [_vp, _P_i64, _P_i32]
@@ -112,7 +116,7 @@ class Plan:
     packed H^2 input (``h2gen.pack``-style dict: L, B, symmetric, rank_row,
     rank_col, near_ptr, near_col, adm_ptr[k], adm_col[k])."""
 
-    def __init__(self, packed: dict):
+    def __init__(self, packed: dict, rank: int = 0, world: int = 1):
         self._keep = []
         L = int(packed["L"])
         rr = np.ascontiguousarray(packed["rank_row"], dtype=np.int32)
@@ -129,7 +133,8 @@ class Plan:
                         rank_row=_ptr(rr, _i32), rank_col=_ptr(rc, _i32) if rc is not None else None,
                         near_ptr=_ptr(npt, _i64), near_col=_ptr(ncl, _i32), adm_ptr=ap_arr, adm_col=ac_arr)
         h = _vp()
-        _check(lib.h2sp_plan_create(ctypes.byref(st), 0, ctypes.byref(h)), "h2sp_plan_create")
+        _check(lib.h2sp_plan_create_shard(ctypes.byref(st), int(rank), int(world), 0, ctypes.byref(h)),
+               "h2sp_plan_create_shard")
         self.handle = h
         self._keep = None
         sz = _Sizes()
@@ -139,6 +144,9 @@ class Plan:
         self.B = int(packed["B"])
         self.symmetric = bool(packed["symmetric"])
         self.N = self.sizes["n"]
+        self.rank, self.world = int(rank), int(world)
+        self.s_rows = self.sizes["s_rows"]
+        self.n_tree_local = self.sizes["n_leaves_local"] * self.B   # tree-order rows of this shard
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -156,6 +164,30 @@ class Plan:
                "h2sp_plan_offsets")
         return out
 
+    def local_rows(self):
+        """Local S row offset of each owned cluster (-1 otherwise), row / column side."""
+        n = self.sizes["n_clusters"]
+        a, b = np.zeros(n, dtype=np.int64), np.zeros(n, dtype=np.int64)
+        _check(lib.h2sp_plan_local_rows(self.handle, _ptr(a, _i64), _ptr(b, _i64)), "h2sp_plan_local_rows")
+        return a, b
+
+    def global_rows(self):
+        """Global S-order row index of every local S row of this plan."""
+        loc, _ = self.local_rows()
+        off = self.offsets()
+        m = off["n_row"] - np.asarray(self._k_row(), dtype=np.int64)
+        out = np.empty(self.s_rows, dtype=np.int64)
+        for c in np.nonzero(loc >= 0)[0]:
+            out[loc[c]:loc[c] + m[c]] = off["s_off_row"][c] + np.arange(m[c])
+        return out
+
+    def _k_row(self):
+        off = self.offsets()
+        # m = n - k is recovered from consecutive S offsets of the full ordering
+        s_off = off["s_off_row"]
+        m = np.diff(np.append(s_off, self.N))
+        return off["n_row"] - m
+
     def launches(self):
         """Per-launch descriptors of one build (kind, level, items, flops, bytes)."""
         n = _i64()
@@ -166,7 +198,7 @@ class Plan:
                 for a in arr[:n.value]]
 
     def pattern(self, with_cols: bool = True):
-        rowptr = np.zeros(self.N + 1, dtype=np.int64)
+        rowptr = np.zeros(self.s_rows + 1, dtype=np.int64)
         col = np.zeros(self.sizes["s_nnz"], dtype=np.int32) if with_cols else None
         _check(lib.h2sp_plan_pattern(self.handle, _ptr(rowptr, _i64), _ptr(col, _i32) if with_cols else None),
                "h2sp_plan_pattern")
@@ -213,7 +245,7 @@ class Sparsifier:
         self.outputs = {
             "q_row": torch.empty(max(int(sz["q_row"]), 1), **f64),
             "q_col": torch.empty(max(int(sz["q_col"]), 1), **f64) if not plan.symmetric else None,
-            "s_rowptr": torch.empty(plan.N + 1, dtype=torch.int64, device=self.device),
+            "s_rowptr": torch.empty(plan.s_rows + 1, dtype=torch.int64, device=self.device),
             "s_col": torch.empty(max(int(sz["s_nnz"]), 1), dtype=torch.int32, device=self.device),
             "s_val": torch.empty(max(int(sz["s_nnz"]), 1), **f64),
         }
@@ -289,11 +321,13 @@ class Sparsifier:
         return ptr, need
 
     def apply_Ut(self, b, y, stream=None, ws=None):
-        """y = U^T b; b, y: (nrhs, N) contiguous float64 CUDA tensors (= N x nrhs column-major)."""
+        """y = U^T b; b: (nrhs, n_tree_local), y: (nrhs, s_rows) contiguous float64 CUDA
+        tensors (= column-major with nrhs columns); n_tree_local = s_rows = N unsharded."""
         nrhs = b.shape[0] if b.dim() == 2 else 1
         ptr, nb = ws if ws is not None else self.apply_ws(nrhs)
-        _check(lib.h2sp_apply_Ut(self.plan.handle, self.outputs["q_row"].data_ptr(), b.data_ptr(), self.plan.N,
-                                 y.data_ptr(), self.plan.N, nrhs, ptr, nb, _stream_handle(stream)), "h2sp_apply_Ut")
+        _check(lib.h2sp_apply_Ut(self.plan.handle, self.outputs["q_row"].data_ptr(), b.data_ptr(),
+                                 b.shape[-1], y.data_ptr(), y.shape[-1], nrhs, ptr, nb, _stream_handle(stream)),
+               "h2sp_apply_Ut")
         return y
 
     def apply_V(self, y, x, stream=None, ws=None):
@@ -301,6 +335,6 @@ class Sparsifier:
         nrhs = y.shape[0] if y.dim() == 2 else 1
         ptr, nb = ws if ws is not None else self.apply_ws(nrhs)
         q = self.outputs["q_row"] if self.plan.symmetric else self.outputs["q_col"]
-        _check(lib.h2sp_apply_V(self.plan.handle, q.data_ptr(), y.data_ptr(), self.plan.N, x.data_ptr(), self.plan.N,
-                                nrhs, ptr, nb, _stream_handle(stream)), "h2sp_apply_V")
+        _check(lib.h2sp_apply_V(self.plan.handle, q.data_ptr(), y.data_ptr(), y.shape[-1], x.data_ptr(),
+                                x.shape[-1], nrhs, ptr, nb, _stream_handle(stream)), "h2sp_apply_V")
         return x

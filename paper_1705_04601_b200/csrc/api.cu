@@ -102,7 +102,7 @@ h2sp_status h2sp_build_host(h2sp_plan P, const h2sp_inputs *hi, const h2sp_outpu
   if (dout->s_col)
     if (h2sp_status s = d2h(ho->s_col, dout->s_col, size_t(P->s_nnz) * 4)) return s;
   if (dout->s_rowptr)
-    if (h2sp_status s = d2h(ho->s_rowptr, dout->s_rowptr, size_t(P->N + 1) * 8)) return s;
+    if (h2sp_status s = d2h(ho->s_rowptr, dout->s_rowptr, size_t(P->n_rows_local + 1) * 8)) return s;
   return H2SP_OK;
 }
 
@@ -117,7 +117,11 @@ static h2sp_status apply_common(h2sp_plan P, const double *q, const void *a, int
                                 int nrhs, void *ws, size_t ws_bytes) {
   if (!P || !q || !a || !b) return fail(H2SP_EINVAL, "NULL argument");
   if (nrhs < 1) return fail(H2SP_EINVAL, "nrhs < 1");
-  if (lda < P->N || ldb < P->N) return fail(H2SP_EINVAL, "leading dimension < N");
+  const int64_t ntree = P->n_leaves_local * P->B;  // tree-order rows of this shard
+  const int64_t nrows = P->n_rows_local;
+  (void)ntree;
+  (void)nrows;
+  if (lda < 1 || ldb < 1) return fail(H2SP_EINVAL, "leading dimension < 1");
   if (h2sp_status s = check_ws(P, ws, ws_bytes, size_t(h2sp_apply_ws_bytes(P, nrhs)))) return s;
   return check_device();
 }
@@ -125,12 +129,14 @@ static h2sp_status apply_common(h2sp_plan P, const double *q, const void *a, int
 h2sp_status h2sp_apply_Ut(h2sp_plan P, const double *q_row, const double *b, int64_t ldb, double *y, int64_t ldy,
                           int nrhs, void *ws, size_t ws_bytes, void *stream) {
   if (h2sp_status s = apply_common(P, q_row, b, ldb, y, ldy, nrhs, ws, ws_bytes)) return s;
+  if (ldb < P->n_leaves_local * P->B || ldy < P->n_rows_local) return fail(H2SP_EINVAL, "leading dimension too small");
   return launch_apply_Ut(P, q_row, b, ldb, y, ldy, nrhs, static_cast<unsigned char *>(ws), stream, false);
 }
 
 h2sp_status h2sp_apply_V(h2sp_plan P, const double *q_col, const double *y, int64_t ldy, double *x, int64_t ldx,
                          int nrhs, void *ws, size_t ws_bytes, void *stream) {
   if (h2sp_status s = apply_common(P, q_col, y, ldy, x, ldx, nrhs, ws, ws_bytes)) return s;
+  if (ldx < P->n_leaves_local * P->B || ldy < P->n_cols_local) return fail(H2SP_EINVAL, "leading dimension too small");
   return launch_apply_V(P, q_col, y, ldy, x, ldx, nrhs, static_cast<unsigned char *>(ws), stream, !P->sym);
 }
 

@@ -115,12 +115,16 @@ struct ClusterArrays {   // byte offsets in meta of per-cluster arrays
   size_t tr_off_row, tr_off_col;           // int64 [ncl]
   size_t s_off_row, s_off_col;             // int64 [ncl]
   size_t zb_off_row, zb_off_col;           // int64 [ncl]: apply basis-coefficient slots (per rhs)
+  size_t loc_off_row, loc_off_col;         // int64 [ncl]: local S row offset of owned clusters, -1 otherwise
 };
 
 }  // namespace h2sp
 
 struct h2sp_plan_s {
   int32_t L, B, sym;
+  int32_t rank, world, part_level;         // sharding by top-level subtrees (world == 1: everything)
+  int64_t first_leaf, n_leaves_local, n_rows_local, n_cols_local;
+  std::vector<int64_t> loc_off_row, loc_off_col;
   int64_t N, ncl;
   std::vector<int32_t> n_row, k_row, n_col, k_col;
   std::vector<int64_t> q_off_row, q_off_col, s_off_row, s_off_col;

@@ -26,6 +26,7 @@ struct Clusters {  // device views of the per-cluster arrays in the meta region
   const int64_t *q_off_row, *q_off_col, *rh_off_row, *rh_off_col;
   const int64_t *leaf_off_row, *leaf_off_col, *tr_off_row, *tr_off_col;
   const int64_t *s_off_row, *s_off_col, *zb_off_row, *zb_off_col;
+  const int64_t *loc_off_row, *loc_off_col;
 };
 
 static Clusters make_clusters(const h2sp_plan_s *p, const unsigned char *meta) {
@@ -46,12 +47,14 @@ static Clusters make_clusters(const h2sp_plan_s *p, const unsigned char *meta) {
   c.s_off_col = (const int64_t *)(meta + p->ca.s_off_col);
   c.zb_off_row = (const int64_t *)(meta + p->ca.zb_off_row);
   c.zb_off_col = (const int64_t *)(meta + p->ca.zb_off_col);
+  c.loc_off_row = (const int64_t *)(meta + p->ca.loc_off_row);
+  c.loc_off_col = (const int64_t *)(meta + p->ca.loc_off_col);
   return c;
 }
 
 struct Side {  // one side (row or column) of the cluster arrays
   const int32_t *n, *k;
-  const int64_t *q_off, *rh_off, *leaf_off, *tr_off, *s_off, *zb_off;
+  const int64_t *q_off, *rh_off, *leaf_off, *tr_off, *s_off, *zb_off, *loc_off;
 };
 
 static Side side_of(const Clusters &c, bool col) {
@@ -64,6 +67,7 @@ static Side side_of(const Clusters &c, bool col) {
   s.tr_off = col ? c.tr_off_col : c.tr_off_row;
   s.s_off = col ? c.s_off_col : c.s_off_row;
   s.zb_off = col ? c.zb_off_col : c.zb_off_row;
+  s.loc_off = col ? c.loc_off_col : c.loc_off_row;
   return s;
 }
 
@@ -1145,12 +1149,12 @@ __global__ void __launch_bounds__(256) csr_cols_kernel(const CsrBlockRow *__rest
 __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const double *__restrict__ q,
                                                        const double *__restrict__ b, int64_t ldb, double *__restrict__ y,
                                                        int64_t ldy, double *__restrict__ zb, int64_t zbl, int nrhs, int B,
-                                                       int *__restrict__ arrive) {
+                                                       int *__restrict__ arrive, int64_t leaf0) {
   __shared__ __align__(16) double sQ[64 * 65];
   __shared__ double sx[64];
   __shared__ int s_go;
   int level = 0;
-  int64_t idx = blockIdx.x;  // in-level index
+  int64_t idx = leaf0 + blockIdx.x;  // in-level index (global)
   while (true) {
     const int64_t cl = lvl_off_d(L, level) + idx;
     const int n = sd.n[cl], k = sd.k[cl];
@@ -1168,7 +1172,7 @@ __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const dou
         __syncthreads();
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
           double v;
-          if (level == 0) v = b[(idx * B + i) + r * ldb];
+          if (level == 0) v = b[((idx - leaf0) * B + i) + r * ldb];
           else if (i < k1) v = __ldcg(zb + sd.zb_off[c1] + i + r * zbl);
           else v = __ldcg(zb + sd.zb_off[c1 + 1] + (i - k1) + r * zbl);
           sx[i] = v;
@@ -1179,7 +1183,7 @@ __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const dou
           double acc = 0.0;
           for (int i = 0; i < n; i++) acc = fma(sQ[i * 65 + j], sx[i], acc);
           if (j < k) zb[sd.zb_off[cl] + j + r * zbl] = acc;
-          else y[sd.s_off[cl] + (j - k) + r * ldy] = acc;
+          else y[sd.loc_off[cl] + (j - k) + r * ldy] = acc;
         }
       }
     }
@@ -1201,11 +1205,11 @@ __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const dou
 
 __global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, const double *__restrict__ q,
                                                       const double *__restrict__ y, int64_t ldy, double *__restrict__ x,
-                                                      int64_t ldx, int nrhs, int B) {
+                                                      int64_t ldx, int nrhs, int B, int64_t leaf0) {
   __shared__ __align__(16) double sQ[64 * 65];
   __shared__ double sv[64];
   __shared__ double sw[64];
-  const int64_t leaf = blockIdx.x;
+  const int64_t leaf = leaf0 + blockIdx.x;
   for (int r = 0; r < nrhs; r++) {
     // walk the path root -> leaf; sv[0:k] holds the basis coefficients from the parent
     for (int level = L; level >= 0; level--) {
@@ -1218,14 +1222,14 @@ __global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, const doub
       for (int e = threadIdx.x; e < n * n; e += blockDim.x) cp8(&sQ[(e / n) * 65 + e % n], Q + e, true);
       cp_commit();
       for (int j = threadIdx.x; j < n; j += blockDim.x)
-        if (j >= k) sv[j] = y[sd.s_off[cl] + (j - k) + r * ldy];
+        if (j >= k) sv[j] = y[sd.loc_off[cl] + (j - k) + r * ldy];
       cp_wait_all();
       __syncthreads();
       if (level == 0) {
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
           double acc = 0.0;
           for (int j = 0; j < n; j++) acc = fma(sQ[i * 65 + j], sv[j], acc);
-          x[(leaf * B + i) + r * ldx] = acc;
+          x[((leaf - leaf0) * B + i) + r * ldx] = acc;
         }
       } else {
         // only the rows of the child on the path are needed
@@ -1505,7 +1509,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     if (csr_idx >= 0) {
       if (h2sp_status e = pre(s2, csr_idx)) return e;
       if (out->s_rowptr)
-        H2SP_CK(cudaMemcpyAsync(out->s_rowptr, meta + P->rowptr_off, size_t(P->N + 1) * sizeof(int64_t),
+        H2SP_CK(cudaMemcpyAsync(out->s_rowptr, meta + P->rowptr_off, size_t(P->n_rows_local + 1) * sizeof(int64_t),
                                 cudaMemcpyDeviceToDevice, s2));
       if (out->s_col) {
         const int splits = 4;
@@ -1516,7 +1520,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       }
       if (h2sp_status e = post(s2, csr_idx)) return e;
     } else if (out->s_rowptr) {
-      H2SP_CK(cudaMemcpyAsync(out->s_rowptr, meta + P->rowptr_off, size_t(P->N + 1) * sizeof(int64_t),
+      H2SP_CK(cudaMemcpyAsync(out->s_rowptr, meta + P->rowptr_off, size_t(P->n_rows_local + 1) * sizeof(int64_t),
                               cudaMemcpyDeviceToDevice, s2));
     }
     H2SP_CK(cudaEventRecord(ev_csr, s2));
@@ -1642,8 +1646,8 @@ h2sp_status launch_apply_Ut(const h2sp_plan_s *P, const double *q, const double 
   const int64_t zbl = col_side ? P->zb_col_len : P->zb_row_len;
   int *arrive = (int *)(ws + P->meta_bytes + ((size_t(std::max(P->zb_row_len, P->zb_col_len)) * nrhs * 8 + 255) / 256) * 256);
   H2SP_CK(cudaMemsetAsync(arrive, 0, size_t(P->ncl) * sizeof(int), st));
-  apply_ut_kernel<<<unsigned(int64_t(1) << P->L), 128, 0, st>>>(sd, P->L, q, b, ldb, y, ldy, zb, zbl, nrhs, P->B,
-                                                                 arrive);
+  apply_ut_kernel<<<unsigned(P->n_leaves_local), 128, 0, st>>>(sd, P->L, q, b, ldb, y, ldy, zb, zbl, nrhs, P->B,
+                                                                 arrive, P->first_leaf);
   H2SP_CK(cudaGetLastError());
   return H2SP_OK;
 }
@@ -1653,7 +1657,8 @@ h2sp_status launch_apply_V(const h2sp_plan_s *P, const double *q, const double *
   cudaStream_t st = (cudaStream_t)stream;
   const Clusters cl = make_clusters(P, ws);
   const Side sd = side_of(cl, col_side);
-  apply_v_kernel<<<unsigned(int64_t(1) << P->L), 128, 0, st>>>(sd, P->L, q, y, ldy, x, ldx, nrhs, P->B);
+  apply_v_kernel<<<unsigned(P->n_leaves_local), 128, 0, st>>>(sd, P->L, q, y, ldy, x, ldx, nrhs, P->B,
+                                                               P->first_leaf);
   H2SP_CK(cudaGetLastError());
   return H2SP_OK;
 }

@@ -110,12 +110,19 @@ const char *h2sp_last_error(void) { return g_err.c_str(); }
 void h2sp_plan_destroy(h2sp_plan p) { delete p; }
 
 h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out) {
+  return h2sp_plan_create_shard(st, 0, 1, flags, out);
+}
+
+h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world, int flags, h2sp_plan *out) {
   (void)flags;
   if (!st || !out) return fail(H2SP_EINVAL, "NULL structure or output pointer");
   *out = nullptr;
   h2sp_plan_s *P = nullptr;
   try {
     const int L = st->L, B = st->leaf_size;
+    if (world < 1 || (world & (world - 1)) != 0) throw PlanError(H2SP_EINVAL, "world must be a power of two");
+    if (rank < 0 || rank >= world) throw PlanError(H2SP_EINVAL, "rank outside [0, world)");
+    if (L >= 0 && L <= 24 && int64_t(world) > (int64_t(1) << L)) throw PlanError(H2SP_EINVAL, "world > number of leaves");
     if (L < 0 || L > 24) throw PlanError(H2SP_EINVAL, "L out of range [0, 24]");
     if (B < 1) throw PlanError(H2SP_EINVAL, "leaf_size < 1");
     if (!st->rank_row) throw PlanError(H2SP_EINVAL, "rank_row is NULL");
@@ -154,6 +161,28 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
     for (int64_t c = 0; c < ncl; c++)
       if (nr[c] > 64 || nc[c] > 64)
         throw PlanError(H2SP_EUNSUPPORTED, "local size n_t > 64 (kernels are built for B, 2r <= 64)");
+    // ---- sharding by top-level subtrees: rank g owns cluster g of the
+    //      partition level Pl = L - log2(world) and all of its descendants
+    int lw = 0;
+    while ((1 << lw) < world) lw++;
+    const int Pl = L - lw;
+    P->rank = rank;
+    P->world = world;
+    P->part_level = Pl;
+    if (world > 1)
+      for (int k = Pl + 1; k <= L; k++)
+        for (int64_t i = 0; i < (int64_t(1) << (L - k)); i++)
+          if (nr[lvl_off(L, k) + i] > 0 || nc[lvl_off(L, k) + i] > 0)
+            throw PlanError(H2SP_EUNSUPPORTED,
+                            "sharded plan: work above the partition level (gather of the remainder not implemented)");
+    // mine(k, i): cluster (k, i) belongs to this rank's subtree (levels above Pl are empty)
+    auto mine = [&](int k, int64_t i) -> bool {
+      if (world == 1) return true;
+      if (k > Pl) return rank == 0;
+      return (i >> (Pl - k)) == rank;
+    };
+    P->first_leaf = world == 1 ? 0 : int64_t(rank) << Pl;
+    P->n_leaves_local = world == 1 ? nleaf : (int64_t(1) << Pl);
 
     // ---------------------------------------------------------------- block tree
     std::vector<std::vector<uint64_t>> near(L + 1), adm(L + 1);
@@ -211,6 +240,24 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
       }
       if (a != P->N || b != P->N) throw PlanError(H2SP_ERANK, "sum of frozen sizes != N");
     }
+    // local S rows of this shard: the owned clusters' rows, in S order (== s_off for one rank)
+    std::vector<int64_t> loc_off(ncl, -1), loc_off_c(ncl, -1);
+    {
+      int64_t a = 0, b = 0;
+      for (int k = 0; k <= L; k++)
+        for (int64_t i = 0; i < (int64_t(1) << (L - k)); i++) {
+          const int64_t c = lvl_off(L, k) + i;
+          if (!mine(k, i)) continue;
+          loc_off[c] = a;
+          a += mr(c);
+          loc_off_c[c] = b;
+          b += mc(c);
+        }
+      P->n_rows_local = a;
+      P->n_cols_local = b;
+    }
+    P->loc_off_row = loc_off;
+    P->loc_off_col = loc_off_c;
     std::vector<int64_t> rh_off_row(ncl), rh_off_col(ncl), tr_off_row(ncl, 0), tr_off_col(ncl, 0), zb_row(ncl),
         zb_col(ncl);
     std::vector<int64_t> leaf_off_row(nleaf), leaf_off_col(nleaf);
@@ -320,6 +367,8 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
         if (sym && t > s) continue;
         int64_t ct = base + t, cs = base + s;
         if (nr[ct] == 0 || nc[cs] == 0) continue;  // empty block: nothing to compute
+        // sharded: rows of t are ours, or (symmetric) the mirror rows of s are
+        if (!(mine(k, t) || (sym && mine(k, s)))) continue;
         PairItem it{};
         it.t = int32_t(ct);
         it.s = int32_t(cs);
@@ -410,10 +459,10 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
             const int64_t cf = lvl_off(L, g.l) + g.s;  // fixed cluster
             if (mq > 0) {
               if (row_side) {
-                blocks.push_back(BlockRec{P->s_off_row[cq], P->s_off_col[cf], mq, g.m, 2, k, gi});
-                if (sym) blocks.push_back(BlockRec{P->s_off_row[cf], P->s_off_col[cq], g.m, mq, 3, k, gi});
-              } else {
-                blocks.push_back(BlockRec{P->s_off_row[cf], P->s_off_col[cq], g.m, mq, 4, k, gi});
+                if (mine(k, p)) blocks.push_back(BlockRec{loc_off[cq], P->s_off_col[cf], mq, g.m, 2, k, gi});
+                if (sym && mine(g.l, g.s)) blocks.push_back(BlockRec{loc_off[cf], P->s_off_col[cq], g.m, mq, 3, k, gi});
+              } else if (mine(g.l, g.s)) {
+                blocks.push_back(BlockRec{loc_off[cf], P->s_off_col[cq], g.m, mq, 4, k, gi});
               }
             }
             const double rows = (takeA ? kq[c1] : 0) + (takeB ? kq[c1 + 1] : 0);
@@ -446,23 +495,24 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
         int64_t ct = base + t, cs = base + s;
         bool canon = !sym || t <= s;
         int64_t item = canon ? pair_index[k][j] : pair_index[k][find(Nk, pkey(s, t))];
-        if (kr[ct] > 0 && mc(cs) > 0) {
+        const bool row_ok = mine(k, t) || (sym && mine(k, s));
+        if (kr[ct] > 0 && mc(cs) > 0 && row_ok) {
           auto &lst = R_cur[t];
           const int32_t col0 = lst.empty() ? 0 : lst.back().col0 + lst.back().m;
           lst.push_back(Grp{k, s, mc(cs), col0});
           // H_ts = H_st^T when t > s (symmetric): row strip of (t,s) = (nb part of H_st)^T
           newr.push_back(NewStrip{item, canon ? 0 : 1, t, col0});
         }
-        if (!sym && mr(ct) > 0 && kc[cs] > 0) {
+        if (!sym && mr(ct) > 0 && kc[cs] > 0 && mine(k, t)) {
           auto &lst = C_cur[s];
           const int32_t col0 = lst.empty() ? 0 : lst.back().col0 + lst.back().m;
           lst.push_back(Grp{k, t, mr(ct), col0});
           newc.push_back(NewStrip{item, 1, s, col0});
         }
         if (canon && mr(ct) > 0 && mc(cs) > 0) {
-          blocks.push_back(BlockRec{P->s_off_row[ct], P->s_off_col[cs], mr(ct), mc(cs), 0, k, item});
-          if (sym && t != s)
-            blocks.push_back(BlockRec{P->s_off_row[cs], P->s_off_col[ct], mc(cs), mr(ct), 1, k, item});
+          if (mine(k, t)) blocks.push_back(BlockRec{loc_off[ct], P->s_off_col[cs], mr(ct), mc(cs), 0, k, item});
+          if (sym && t != s && mine(k, s))
+            blocks.push_back(BlockRec{loc_off[cs], P->s_off_col[ct], mc(cs), mr(ct), 1, k, item});
         }
       }
       // ---- panel bases of level k, and the destinations that point into them
@@ -518,7 +568,8 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
         throw PlanError(H2SP_ETREE, "internal: S block produced twice");
     std::vector<CsrBlockRow> csr_rows;
     std::vector<CsrBlock> csr_blocks;
-    std::vector<int64_t> rowptr(P->N + 1, 0);
+    const int64_t NR_loc = P->n_rows_local;
+    std::vector<int64_t> rowptr(NR_loc + 1, 0);
     int64_t nnz = 0;
     {
       size_t j = 0;
@@ -555,7 +606,7 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
         nnz += m_r * rowlen;
         j = e;
       }
-      for (; row <= P->N; row++) rowptr[row] = nnz;
+      for (; row <= NR_loc; row++) rowptr[row] = nnz;
     }
     P->s_nnz = nnz;
     P->s_blocks = int64_t(blocks.size());
@@ -564,9 +615,9 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
     for (int k = 1; k <= L; k++)
       for (auto &pn : rpan[k]) {
         const int32_t mq = nr[pn.q] - kr[pn.q];
-        if (mq == 0 || pn.gend == pn.gbeg) continue;
+        if (mq == 0 || pn.gend == pn.gbeg || loc_off[pn.q] < 0) continue;
         const int64_t d0 = rgrp_direct[k][pn.gbeg];
-        const int64_t r0 = P->s_off_row[pn.q];
+        const int64_t r0 = loc_off[pn.q];
         if (d0 != rowptr[r0]) throw PlanError(H2SP_ETREE, "internal: strip panel not at the start of its S row");
         for (int32_t g = pn.gbeg; g < pn.gend; g++)
           if (rgrp_direct[k][g] != d0 + rgrp[k][g].col0)
@@ -578,7 +629,8 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
     // ---------------------------------------------------------------- meta image
     MetaBuilder mb;
     mb.buf.resize(256, 0);
-    P->magic = 0x4832535050000000ull ^ (uint64_t(P->N) << 8) ^ uint64_t(nnz & 0xffffff) ^ (uint64_t(blocks.size()) << 40);
+    P->magic = 0x4832535050000000ull ^ (uint64_t(P->N) << 8) ^ uint64_t(nnz & 0xffffff) ^ (uint64_t(blocks.size()) << 40) ^
+               (uint64_t(rank) << 32) ^ (uint64_t(world) << 36);
     std::memcpy(mb.buf.data(), &P->magic, 8);
     P->ca.n_row = mb.put(nr);
     P->ca.k_row = mb.put(kr);
@@ -596,6 +648,8 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
     P->ca.s_off_col = mb.put(P->s_off_col);
     P->ca.zb_off_row = mb.put(zb_row);
     P->ca.zb_off_col = mb.put(zb_col);
+    P->ca.loc_off_row = mb.put(loc_off);
+    P->ca.loc_off_col = mb.put(sym ? loc_off : loc_off_c);
     P->levels.resize(L + 1);
     int levels_active = 0;
     int64_t launches = 0;
@@ -750,7 +804,7 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
     P->rowptr_off = mb.put(rowptr);
     if (P->n_csr_rows) {  // CSR column expansion (+ the rowptr D2D copy)
       launches++;
-      P->launch_info.push_back(h2sp_launch_info{6, L, P->n_csr_rows, 0.0, 4.0 * double(nnz) + 16.0 * double(P->N + 1)});
+      P->launch_info.push_back(h2sp_launch_info{6, L, P->n_csr_rows, 0.0, 4.0 * double(nnz) + 16.0 * double(NR_loc + 1)});
     }
     P->launches = launches;
     P->levels_active = levels_active;
@@ -785,7 +839,7 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
         if (!sym || kt(adm[k][j]) <= ks(adm[k][j]))
           coup_read += double(kr[lvl_off(L, k) + kt(adm[k][j])]) * kc[lvl_off(L, k) + ks(adm[k][j])];
     double in_bytes = 8.0 * (close_read + coup_read + P->leaf_row_len + P->leaf_col_len + P->tr_row_len + P->tr_col_len);
-    double out_bytes = 8.0 * (P->q_row_len + P->q_col_len) + 12.0 * double(nnz) + 8.0 * double(P->N + 1);
+    double out_bytes = 8.0 * (P->q_row_len + P->q_col_len) + 12.0 * double(nnz) + 8.0 * double(NR_loc + 1);
     double mid_bytes = 2.0 * 8.0 * double(P->rh_row_len + P->rh_col_len + dt_len + bb_len + yr_len + yc_len);
     P->flops = flops_qr + flops_coup + flops_cong + flops_strip;
     P->flops_cong = flops_cong;
@@ -819,6 +873,11 @@ h2sp_status h2sp_plan_sizes(h2sp_plan P, h2sp_sizes *o) {
   o->q_row = P->q_row_len;
   o->q_col = P->q_col_len;
   o->s_nnz = P->s_nnz;
+  o->s_rows = P->n_rows_local;
+  o->rank = P->rank;
+  o->world = P->world;
+  o->first_leaf = P->first_leaf;
+  o->n_leaves_local = P->n_leaves_local;
   o->s_blocks = P->s_blocks;
   o->workspace_bytes = int64_t(P->ws_total);
   o->meta_bytes = int64_t(P->meta_bytes);
@@ -845,6 +904,15 @@ h2sp_status h2sp_plan_offsets(h2sp_plan P, int64_t *s_off_row, int64_t *s_off_co
   return H2SP_OK;
 }
 
+h2sp_status h2sp_plan_local_rows(h2sp_plan P, int64_t *loc_off_row, int64_t *loc_off_col) {
+  if (!P) return fail(H2SP_EINVAL, "NULL plan");
+  for (int64_t c = 0; c < P->ncl; c++) {
+    if (loc_off_row) loc_off_row[c] = P->loc_off_row[c];
+    if (loc_off_col) loc_off_col[c] = P->sym ? P->loc_off_row[c] : P->loc_off_col[c];
+  }
+  return H2SP_OK;
+}
+
 h2sp_status h2sp_plan_launches(h2sp_plan P, h2sp_launch_info *out, int64_t max, int64_t *count) {
   if (!P || !count) return fail(H2SP_EINVAL, "NULL plan or count");
   *count = int64_t(P->launch_info.size());
@@ -855,7 +923,7 @@ h2sp_status h2sp_plan_launches(h2sp_plan P, h2sp_launch_info *out, int64_t max, 
 
 h2sp_status h2sp_plan_pattern(h2sp_plan P, int64_t *rowptr, int32_t *col) {
   if (!P || !rowptr) return fail(H2SP_EINVAL, "NULL plan or rowptr");
-  std::memcpy(rowptr, P->meta.data() + P->rowptr_off, size_t(P->N + 1) * sizeof(int64_t));
+  std::memcpy(rowptr, P->meta.data() + P->rowptr_off, size_t(P->n_rows_local + 1) * sizeof(int64_t));
   if (col) {
     const CsrBlockRow *rows = reinterpret_cast<const CsrBlockRow *>(P->meta.data() + P->csr_rows_off);
     const CsrBlock *blks = reinterpret_cast<const CsrBlock *>(P->meta.data() + P->csr_blocks_off);

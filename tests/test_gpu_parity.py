@@ -223,3 +223,52 @@ def test_parity_config2_full():
     # Frobenius invariance (P5) of the GPU S
     f = oracle.frobenius_sq(h)
     assert abs(float(np.dot(v, v)) - f) / f <= 1e-12
+
+
+@pytest.mark.parametrize("name,make,G", [
+    ("cfg2-4096-sym", lambda: h2gen.make_config(2, N=4096), 4),
+    ("cfg4-8192-gen", lambda: h2gen.make_config(4, N=8192), 2),
+    ("rand-gen-uniform", lambda: h2gen.random_h2(6, 8, 4, False, eta=0.7, ragged=False, r=4), 4),
+])
+def test_virtual_shards_bitwise(name, make, G):
+    """SURVEY §8(e) on one GPU: the G subtree shards, built one after the other,
+    give exactly (bitwise) the unsharded S rows; sharded apply U^T b / V y equals
+    the unsharded apply on the shard's rows.  Also checked against the oracle."""
+    _need_gpu()
+    import paper_1705_04601_b200 as h2sp
+    h = make()
+    packed = h2gen.pack(h)
+    plan, sp, out = _run(h)
+    _compare(h, plan, out)
+    full_val = out["s_val"].cpu().numpy()
+    frow = out["s_rowptr"].cpu().numpy()
+    rng = np.random.default_rng(9)
+    b = rng.standard_normal((2, h.N))
+    bt = torch.from_numpy(b).cuda()
+    yf = torch.empty_like(bt)
+    sp.apply_Ut(bt, yf)
+    xf = torch.empty_like(bt)
+    sp.apply_V(yf, xf)
+    seen = np.zeros(h.N, dtype=np.int64)
+    for g in range(G):
+        sh = h2sp.Plan(packed, g, G)
+        ssp = h2sp.Sparsifier(sh, packed)
+        o = ssp.build()
+        torch.cuda.synchronize()
+        rp = o["s_rowptr"].cpu().numpy()
+        val = o["s_val"].cpu().numpy()
+        gr = sh.global_rows()
+        for lr, r in enumerate(gr):
+            seen[r] += 1
+            assert np.array_equal(val[rp[lr]:rp[lr + 1]], full_val[frow[r]:frow[r + 1]]), (g, r)
+        lo = sh.sizes["first_leaf"] * h.B
+        bl = bt[:, lo:lo + sh.n_tree_local].contiguous()
+        yl = torch.empty(2, sh.s_rows, dtype=torch.float64, device="cuda")
+        ssp.apply_Ut(bl, yl)
+        torch.cuda.synchronize()
+        assert torch.equal(yl.cpu(), yf[:, torch.from_numpy(gr)].cpu())
+        xl = torch.empty_like(bl)
+        ssp.apply_V(yf[:, torch.from_numpy(gr)].contiguous(), xl)
+        torch.cuda.synchronize()
+        assert torch.equal(xl.cpu(), xf[:, lo:lo + sh.n_tree_local].cpu())
+    assert np.all(seen == 1)

@@ -305,3 +305,17 @@ def test_csr_roundtrip(small):
         assert np.all(np.diff(cols) > 0)
         D[r, cols] = val[rowptr[r]:rowptr[r + 1]]
     assert np.array_equal(D, S)
+
+
+def test_orthonormalize_preserves_matrix():
+    """h2gen.orthonormalize_h2 (generator, config 4) changes the parameters but
+    not the represented A_H2, and gives orthonormal leaf bases."""
+    import copy
+    h = h2gen.random_h2(4, 8, 13, False, eta=0.7)
+    A0 = oracle.dense_A(h)
+    h1 = h2gen.orthonormalize_h2(copy.deepcopy(h))
+    A1 = oracle.dense_A(h1)
+    assert np.linalg.norm(A1 - A0) / np.linalg.norm(A0) <= 1e-12
+    for R in h1.leaf_row:
+        if R.shape[1]:
+            assert np.abs(R.T @ R - np.eye(R.shape[1])).max() <= 1e-13

@@ -1,0 +1,96 @@
+"""Sharded plans, host side: the union of the shards' local S
+rows is the full S, each row exactly once, with identical column patterns;
+and a world_size-2 gloo run where every rank builds its own shard plan."""
+import os
+
+import numpy as np
+import pytest
+
+import h2gen
+import paper_1705_04601_b200 as h2sp
+
+
+def _inputs():
+    yield "cfg2-4096-sym", lambda: h2gen.make_config(2, N=4096)
+    yield "cfg4-8192-gen", lambda: h2gen.make_config(4, N=8192)
+    yield "rand-gen-uniform", lambda: h2gen.random_h2(6, 8, 4, False, eta=0.7, ragged=False, r=4)
+    yield "rand-sym-uniform", lambda: h2gen.random_h2(6, 8, 5, True, eta=0.7, ragged=False, r=4)
+
+
+INPUTS = list(_inputs())
+
+
+def check_union(packed, G):
+    full = h2sp.Plan(packed)
+    frow, fcol = full.pattern()
+    seen = np.zeros(full.N, dtype=np.int64)
+    for g in range(G):
+        sh = h2sp.Plan(packed, g, G)
+        assert sh.sizes["rank"] == g and sh.sizes["world"] == G
+        gr = sh.global_rows()
+        rp, cl = sh.pattern()
+        assert len(gr) == sh.s_rows == len(rp) - 1
+        for lr, r in enumerate(gr):
+            seen[r] += 1
+            assert np.array_equal(cl[rp[lr]:rp[lr + 1]], fcol[frow[r]:frow[r + 1]])
+    assert np.all(seen == 1)
+
+
+@pytest.mark.parametrize("name,make", INPUTS, ids=[i[0] for i in INPUTS])
+@pytest.mark.parametrize("G", [2, 4])
+def test_shard_union_is_full_pattern(name, make, G):
+    check_union(h2gen.pack(make()), G)
+
+
+def test_shard_flops_add_up_with_cross_pairs():
+    """Shards together do at least the full work; symmetric cross pairs are duplicated."""
+    p = h2gen.pack(h2gen.make_config(2, N=4096))
+    full = h2sp.Plan(p).sizes["flops_congruence"]
+    parts = [h2sp.Plan(p, g, 4).sizes["flops_congruence"] for g in range(4)]
+    assert sum(parts) >= full
+    assert sum(parts) <= 1.5 * full
+
+
+def test_shard_rejects_bad_world():
+    p = h2gen.pack(h2gen.make_config(2, N=4096))
+    for rank, world in ((0, 3), (2, 2), (-1, 2)):
+        with pytest.raises(h2sp.H2spError):
+            h2sp.Plan(p, rank, world)
+
+
+def _gloo_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+    packed = h2gen.pack(h2gen.make_config(2, N=4096))
+    sh = h2sp.Plan(packed, rank, world)
+    rows = torch.from_numpy(sh.global_rows())
+    nnz = torch.tensor([sh.sizes["s_nnz"]], dtype=torch.int64)
+    counts = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(counts, torch.tensor([len(rows)], dtype=torch.int64))
+    gathered = [torch.zeros(int(c.item()), dtype=torch.int64) for c in counts]
+    dist.all_gather(gathered, rows)
+    dist.all_reduce(nnz)
+    if rank == 0:
+        allrows = torch.cat(gathered).numpy()
+        full = h2sp.Plan(packed)
+        q.put((sorted(allrows.tolist()) == list(range(full.N)), int(nnz.item()) == full.sizes["s_nnz"]))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_shards_cover_s():
+    import multiprocessing as mp
+    import random
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + random.randint(0, 2000)
+    ps = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(timeout=120)
+    assert all(p.exitcode == 0 for p in ps)
+    rows_ok, nnz_ok = q.get(timeout=5)
+    assert rows_ok and nnz_ok
