@@ -48,14 +48,14 @@ def _peaks():
         return {"hbm_gbs": 6650.0, "fallback": True}
 
 
-def workload_desc(cfg_idx: int, h) -> str:
+def workload_desc(cfg_idx: int, N: int, seed) -> str:
     import h2gen
     c = h2gen.CONFIGS[cfg_idx]
     k = c["kernel"]
     kern = {"exp": f"exp(-r/{k.get('ell')})+{k.get('nugget')}*I", "invh": "1/(r+h)+1.0*I (h=N^-1/3)",
             "laplace": "1/(4 pi r), diag 1/(4 pi h)"}[k["kind"]]
-    return (f"BASELINE configs[{cfg_idx - 1}]: N={h.N} {c['points']} points, {kern}, B={c['B']}, r={c['r']}, "
-            f"eta={c['eta']}, {'symmetric (SPD)' if c['symmetric'] else 'general'} mode, seed={h.meta.get('seed')}")
+    return (f"BASELINE configs[{cfg_idx - 1}]: N={N} {c['points']} points, {kern}, B={c['B']}, r={c['r']}, "
+            f"eta={c['eta']}, {'symmetric (SPD)' if c['symmetric'] else 'general'} mode, seed={seed}")
 
 
 class ClockSampler:
@@ -159,8 +159,8 @@ def run_reference(args, rank, world):
     line = {"metric": METRIC, "value": val, "unit": UNIT, "impl": "reference", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_desc(args.config, h2gen.make_config(args.config, N=n_sample)),
-                       "sample_N": n_sample, "flops_per_step": flops},
+            "config": {"workload": workload_desc(args.config, args.n or h2gen.CONFIGS[args.config]["N"], args.config),
+                       "sample": sample, "sample_N": n_sample, "flops_per_step": flops},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -226,7 +226,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-n", type=int, default=16384, help="--impl reference sample size")
     ap.add_argument("--timeline", action="store_true", help="print per-launch start/end of the last step (stderr)")
-    ap.add_argument("--graph", type=int, default=0, help="1: replay the step as one captured CUDA graph")
+    ap.add_argument("--shard", action="store_true",
+                    help="N>1: split ONE matrix into N top-level subtree shards (strong scaling) "
+                         "instead of N independent matrices (weak scaling, default)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -248,24 +250,26 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    seed = args.config + 1000 * rank
+    shard = args.shard and world > 1
+    seed = args.config + (0 if shard else 1000 * rank)
     h = h2gen.make_config(args.config, seed=seed, N=args.n)
     packed = h2gen.pack(h)
     t0 = time.perf_counter()
-    plan = h2sp.Plan(packed)
+    plan = h2sp.Plan(packed, rank, world) if shard else h2sp.Plan(packed)
     plan_ms = (time.perf_counter() - t0) * 1e3
     sp = h2sp.Sparsifier(plan, packed, device=dev)
     launches = plan.launches()
     n_launch = len(launches)
     assert n_launch == plan.sizes["launches"]
     nrhs = args.nrhs
-    b = torch.randn(nrhs, plan.N, dtype=torch.float64, device=dev)
-    y = torch.empty_like(b)
+    b = torch.randn(nrhs, plan.n_tree_local, dtype=torch.float64, device=dev)
+    y = torch.empty(nrhs, plan.s_rows, dtype=torch.float64, device=dev)
     x = torch.empty_like(b)
     aws = sp.apply_ws(nrhs)
     offs = plan.offsets()
     n_apply_launch = 2   # one fused kernel per direction (apply_ut_kernel, apply_v_kernel)
-    apply_flops = 2 * 2.0 * nrhs * float(np.sum(offs["n_row"].astype(float) ** 2))
+    loc_r, _ = plan.local_rows()
+    apply_flops = 2 * 2.0 * nrhs * float(np.sum(offs["n_row"][loc_r >= 0].astype(float) ** 2))
     step_flops = plan.sizes["flops"] + apply_flops
     stream = torch.cuda.current_stream()
 
@@ -340,7 +344,12 @@ def main():
                  "peak_source": "FP64 DMMA microbenchmark on this pool's B200 (profiles/r01_fp64_peak.txt); "
                                 f"cuBLAS DGEMM measured {FP64_DGEMM_TFLOPS}",
                  "hbm_peak_gbs": peaks["hbm_gbs"]})
-    value = step_flops * world / (ms_max * 1e-3) / 1e12
+    # whole-job throughput: the work of every rank (shards: their own flops) / max time
+    fl_t = torch.tensor([step_flops], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(fl_t)
+    job_flops = float(fl_t.item())
+    value = job_flops / (ms_max * 1e-3) / 1e12
 
     # ---- e2e through the public API with HOST buffers (pinned), copies inside the timed region
     e2e = None
@@ -376,7 +385,7 @@ def main():
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         h2d = sum(int(v.numel()) * v.element_size() for v in host_in.values()) + hb.numel() * 8
         d2h = sum(int(v.numel()) * v.element_size() for v in host_out.values() if v is not None) + hx.numel() * 8
-        e2e = {"value": step_flops * world / (float(ems.item()) * 1e-3) / 1e12, "unit": UNIT,
+        e2e = {"value": job_flops / (float(ems.item()) * 1e-3) / 1e12, "unit": UNIT,
                "ms_per_step": float(ems.item()), "steps": k_e2e, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h}
 
@@ -389,16 +398,20 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": "strong" if shard else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_desc(args.config, h), "N": plan.N, "B": plan.B, "L": plan.L,
+            "config": {"workload": workload_desc(args.config, plan.N, h.meta.get("seed")), "N": plan.N, "B": plan.B, "L": plan.L,
                        "nrhs": nrhs, "mode": "symmetric" if plan.symmetric else "general",
-                       "parallelism": f"replicas x{world} (independent matrices per rank, no collective)",
+                       "parallelism": (f"subtree shards x{world} of one matrix (no data-path collective; "
+                                       f"Q of halo clusters recomputed per shard)") if shard else
+                                      f"replicas x{world} (independent matrices per rank, no collective)",
                        "l2": "inputs (close blocks %.2f GB) and outputs (S %.2f GB) exceed the 126 MB L2; no flush"
                              % (plan.sizes["close"] * 8e-9, plan.sizes["s_nnz"] * 12e-9),
                        "plan_ms": plan_ms, "s_nnz": plan.sizes["s_nnz"], "s_blocks": plan.sizes["s_blocks"],
                        "flops_per_step": step_flops, "bytes_per_step": plan.sizes["bytes"],
                        "fp64_frac_of_peak_whole_step": value / world / FP64_PEAK_TFLOPS,
+                       "job_flops_per_step": job_flops,
                        "hbm_frac_whole_step": plan.sizes["bytes"] / (ms_max * 1e-3) / (peaks["hbm_gbs"] * 1e9),
                        "breakdown_ms": {k: round(v, 4) for k, v in kinds.items()}},
             "roofline": roof,

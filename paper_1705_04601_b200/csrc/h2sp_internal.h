@@ -116,6 +116,7 @@ struct ClusterArrays {   // byte offsets in meta of per-cluster arrays
   size_t s_off_row, s_off_col;             // int64 [ncl]
   size_t zb_off_row, zb_off_col;           // int64 [ncl]: apply basis-coefficient slots (per rhs)
   size_t loc_off_row, loc_off_col;         // int64 [ncl]: local S row offset of owned clusters, -1 otherwise
+  size_t need_row, need_col;               // int8 [ncl]: Q needed by this shard
 };
 
 }  // namespace h2sp
@@ -125,6 +126,7 @@ struct h2sp_plan_s {
   int32_t rank, world, part_level;         // sharding by top-level subtrees (world == 1: everything)
   int64_t first_leaf, n_leaves_local, n_rows_local, n_cols_local;
   std::vector<int64_t> loc_off_row, loc_off_col;
+  std::vector<int8_t> need_r, need_c;
   int64_t N, ncl;
   std::vector<int32_t> n_row, k_row, n_col, k_col;
   std::vector<int64_t> q_off_row, q_off_col, s_off_row, s_off_col;

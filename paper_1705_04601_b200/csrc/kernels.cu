@@ -27,6 +27,7 @@ struct Clusters {  // device views of the per-cluster arrays in the meta region
   const int64_t *leaf_off_row, *leaf_off_col, *tr_off_row, *tr_off_col;
   const int64_t *s_off_row, *s_off_col, *zb_off_row, *zb_off_col;
   const int64_t *loc_off_row, *loc_off_col;
+  const int8_t *need_row, *need_col;
 };
 
 static Clusters make_clusters(const h2sp_plan_s *p, const unsigned char *meta) {
@@ -49,12 +50,15 @@ static Clusters make_clusters(const h2sp_plan_s *p, const unsigned char *meta) {
   c.zb_off_col = (const int64_t *)(meta + p->ca.zb_off_col);
   c.loc_off_row = (const int64_t *)(meta + p->ca.loc_off_row);
   c.loc_off_col = (const int64_t *)(meta + p->ca.loc_off_col);
+  c.need_row = (const int8_t *)(meta + p->ca.need_row);
+  c.need_col = (const int8_t *)(meta + p->ca.need_col);
   return c;
 }
 
 struct Side {  // one side (row or column) of the cluster arrays
   const int32_t *n, *k;
   const int64_t *q_off, *rh_off, *leaf_off, *tr_off, *s_off, *zb_off, *loc_off;
+  const int8_t *need;
 };
 
 static Side side_of(const Clusters &c, bool col) {
@@ -68,6 +72,7 @@ static Side side_of(const Clusters &c, bool col) {
   s.s_off = col ? c.s_off_col : c.s_off_row;
   s.zb_off = col ? c.zb_off_col : c.zb_off_row;
   s.loc_off = col ? c.loc_off_col : c.loc_off_row;
+  s.need = col ? c.need_col : c.need_row;
   return s;
 }
 
@@ -198,7 +203,7 @@ __global__ void __launch_bounds__(128) qr_kernel(Side sd, int L, int level, int 
   const int64_t base = lvl_off_d(L, level);
   const int64_t cl = base + ci;
   const int n = sd.n[cl], k = sd.k[cl];
-  if (n == 0) return;
+  if (n == 0 || !sd.need[cl]) return;
   double *Qg = qout + sd.q_off[cl];
   if (k == 0) {
     for (int idx = lane; idx < n * n; idx += 32) Qg[idx] = (idx / n == idx % n) ? 1.0 : 0.0;
@@ -426,7 +431,7 @@ __global__ void __launch_bounds__(128) qr_reg_kernel(Side sd, int L, int level, 
   const int64_t base = lvl_off_d(L, level);
   const int64_t cl = base + ci;
   const int n = sd.n[cl], k = sd.k[cl];
-  if (n == 0) return;
+  if (n == 0 || !sd.need[cl]) return;
   double *Qg = qout + sd.q_off[cl];
   if (k == 0) {
     for (int idx = lane; idx < n * n; idx += 32) Qg[idx] = (idx / n == idx % n) ? 1.0 : 0.0;

@@ -352,6 +352,8 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
           int64_t ct = base + t, cs = base + s;
           int64_t sz = int64_t(kr[ct]) * kc[cs];
           if (sz == 0) continue;
+          // sharded: only the couplings feeding a congruence of this shard at level k+1
+          if (!(mine(k + 1, t / 2) || (sym && mine(k + 1, s / 2)))) continue;
           dt_slot[k][j] = dt_len;
           coup[k].push_back(CouplingItem{int32_t(ct), int32_t(cs), coup_in[k][j], dt_len});
           dt_len += sz;
@@ -559,6 +561,43 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
       Cb_prev.swap(Cb);
     }
 
+    // ---------------------------------------------------------------- Q needed by this shard
+    // Q_t (and the R^ chain below it) is needed for every cluster a kept item
+    // rotates with, and for the owned clusters (apply); closure over descendants.
+    std::vector<int8_t> need_r(ncl, world == 1 ? 1 : 0), need_c(ncl, world == 1 ? 1 : 0);
+    if (world > 1) {
+      for (int k = 0; k <= L; k++) {
+        for (const auto &it : pairs[k]) {
+          need_r[it.t] = 1;
+          need_c[it.s] = 1;
+        }
+        for (const auto &pn : rpan[k]) need_r[pn.q] = 1;
+        for (const auto &pn : cpan[k]) need_c[pn.q] = 1;
+        for (const auto &ci : coup[k]) {
+          need_r[ci.t] = 1;
+          need_c[ci.s] = 1;
+        }
+        for (int64_t i = 0; i < (int64_t(1) << (L - k)); i++)
+          if (mine(k, i)) need_r[lvl_off(L, k) + i] = need_c[lvl_off(L, k) + i] = 1;
+      }
+      for (int k = L; k >= 1; k--)
+        for (int64_t i = 0; i < (int64_t(1) << (L - k)); i++) {
+          const int64_t c = lvl_off(L, k) + i, c1 = lvl_off(L, k - 1) + 2 * i;
+          if (need_r[c]) need_r[c1] = need_r[c1 + 1] = 1;
+          if (need_c[c]) need_c[c1] = need_c[c1 + 1] = 1;
+        }
+      if (sym)
+        for (int64_t c = 0; c < ncl; c++) need_r[c] = need_c[c] = (need_r[c] | need_c[c]);
+      // QR flops of this shard
+      flops_qr = 0;
+      for (int64_t c = 0; c < ncl; c++) {
+        if (need_r[c]) flops_qr += 2.0 * nr[c] * kr[c] * kr[c] + 4.0 * nr[c] * nr[c] * kr[c];
+        if (!sym && need_c[c]) flops_qr += 2.0 * nc[c] * kc[c] * kc[c] + 4.0 * nc[c] * nc[c] * kc[c];
+      }
+    }
+    P->need_r = need_r;
+    P->need_c = need_c;
+
     // ---------------------------------------------------------------- S pattern, CSR
     std::sort(blocks.begin(), blocks.end(), [](const BlockRec &a, const BlockRec &b) {
       return a.roff != b.roff ? a.roff < b.roff : a.coff < b.coff;
@@ -650,6 +689,8 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
     P->ca.zb_off_col = mb.put(zb_col);
     P->ca.loc_off_row = mb.put(loc_off);
     P->ca.loc_off_col = mb.put(sym ? loc_off : loc_off_c);
+    P->ca.need_row = mb.put(need_r);
+    P->ca.need_col = mb.put(sym ? need_r : need_c);
     P->levels.resize(L + 1);
     int levels_active = 0;
     int64_t launches = 0;
@@ -713,10 +754,11 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
       }
       auto qr_info = [&](const std::vector<int32_t> &n, const std::vector<int32_t> &kk, int kind) {
         h2sp_launch_info li{kind, k, 0, 0.0, 0.0};
+        const auto &need = (kind == 0) ? need_r : need_c;
         for (int64_t i = 0; i < M; i++) {
           const int64_t c = base + i;
           const double nn = n[c], k_ = kk[c];
-          if (nn == 0) continue;
+          if (nn == 0 || !need[c]) continue;
           li.items++;
           li.flops += 2 * nn * k_ * k_ + 4 * nn * nn * k_;
           double in_ = (k == 0) ? double(B) * k_ : nn * k_;
