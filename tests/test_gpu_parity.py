@@ -68,6 +68,8 @@ CASES += [
     ("fig3-active-gen", lambda: h2gen.fig3_h2(8, 1, "active", symmetric=False)),
     ("cfg1", lambda: h2gen.make_config(1)),
     ("cfg2-16384", lambda: h2gen.make_config(2, N=16384)),
+    ("cfg3-16384", lambda: h2gen.make_config(3, N=16384)),      # 3-D, r = 24: 48-wide internal tiles
+    ("cfg4-16384", lambda: h2gen.make_config(4, N=16384)),      # sphere, general mode, r = 32
 ]
 
 
@@ -272,3 +274,24 @@ def test_virtual_shards_bitwise(name, make, G):
         torch.cuda.synchronize()
         assert torch.equal(xl.cpu(), xf[:, lo:lo + sh.n_tree_local].cpu())
     assert np.all(seen == 1)
+
+
+def test_graph_capture_replay_equals_direct():
+    """The whole build (fork/join over the library's side streams) captured in a
+    CUDA graph and replayed gives the direct build's S and Q bitwise."""
+    _need_gpu()
+    import paper_1705_04601_b200 as h2sp
+    h = h2gen.random_h2(5, 16, 50, True, eta=0.7)
+    packed = h2gen.pack(h)
+    plan = h2sp.Plan(packed)
+    sp = h2sp.Sparsifier(plan, packed)
+    ref = {k: v.clone() for k, v in sp.build().items() if v is not None}
+    torch.cuda.synchronize()
+    for v in sp.outputs.values():
+        if v is not None:
+            v.zero_()
+    g = sp.capture()
+    g.replay()
+    torch.cuda.synchronize()
+    for k, v in ref.items():
+        assert torch.equal(v, sp.outputs[k]), k
