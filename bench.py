@@ -266,6 +266,7 @@ def main():
     y = torch.empty(nrhs, plan.s_rows, dtype=torch.float64, device=dev)
     x = torch.empty_like(b)
     aws = sp.apply_ws(nrhs)
+    apply_ws_sep = sp.apply_workspace(nrhs)   # h2sp_build_apply runs the applies concurrently with the build
     offs = plan.offsets()
     n_apply_launch = 2   # one fused kernel per direction (apply_ut_kernel, apply_v_kernel)
     loc_r, _ = plan.local_rows()
@@ -274,12 +275,8 @@ def main():
     stream = torch.cuda.current_stream()
 
     def step(events=None):
-        if events is None:
-            sp.build()
-        else:
-            sp.build_profiled(events)
-        sp.apply_Ut(b, y, ws=aws)
-        sp.apply_V(y, x, ws=aws)
+        # one pass of the hot path: build + y = U^T b + x = V y (h2sp_build_apply)
+        sp.build_apply(b, y, y, x, apply_ws_sep, events=events)
 
     for _ in range(args.warmup):
         step()

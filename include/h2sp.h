@@ -211,6 +211,31 @@ h2sp_status h2sp_build(h2sp_plan plan, const h2sp_inputs *in, const h2sp_outputs
 h2sp_status h2sp_build_ex(h2sp_plan plan, const h2sp_inputs *in, const h2sp_outputs *out, void *ws,
                           size_t ws_bytes, void *stream, void *const *events, int64_t n_events);
 
+/* One pass of the whole hot path (BASELINE.json north_star: "the same pass also
+ * applies U^T b and V y"): h2sp_build plus y = U^T b and x = V w.  The applies
+ * depend only on Q, so they run on the build's QR side stream right after the
+ * QR chain, overlapping the congruence and strips.  Either apply is skipped if
+ * its input pointer is NULL; w may be y (then x = V U^T b).  `ws` of the apply
+ * must be a DIFFERENT uploaded workspace (>= h2sp_apply_ws_bytes(nrhs)) than
+ * the build's.  Layouts as in h2sp_apply_Ut / h2sp_apply_V.  `events` as in
+ * h2sp_build_ex (may be NULL). */
+typedef struct {
+  const double *b;
+  int64_t ldb;
+  double *y;
+  int64_t ldy;
+  const double *w;
+  int64_t ldw;
+  double *x;
+  int64_t ldx;
+  int nrhs;
+  void *ws;
+  size_t ws_bytes;
+} h2sp_apply_args;
+h2sp_status h2sp_build_apply(h2sp_plan plan, const h2sp_inputs *in, const h2sp_outputs *out, void *ws,
+                             size_t ws_bytes, const h2sp_apply_args *ap, void *stream, void *const *events,
+                             int64_t n_events);
+
 /* End-to-end variant with HOST buffers: copies the host inputs into the given
  * device input buffers, builds, and copies every output back into the host
  * output buffers (host pointers should be pinned for overlap).  All copies

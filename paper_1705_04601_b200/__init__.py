@@ -52,6 +52,11 @@ class _LaunchInfo(ctypes.Structure):
 LAUNCH_KINDS = ("qr_row", "qr_col", "coupling", "congruence", "strips_row", "strips_col", "csr")
 
 
+class _ApplyArgs(ctypes.Structure):
+    _fields_ = [("b", _vp), ("ldb", _i64), ("y", _vp), ("ldy", _i64), ("w", _vp), ("ldw", _i64), ("x", _vp),
+                ("ldx", _i64), ("nrhs", ctypes.c_int), ("ws", _vp), ("ws_bytes", ctypes.c_size_t)]
+
+
 class _Inputs(ctypes.Structure):
     _fields_ = [(n, _vp) for n in ("leaf_basis_row", "transfer_row", "leaf_basis_col", "transfer_col", "close",
                                    "coupling")]
@@ -79,6 +84,8 @@ lib.h2sp_build.argtypes = [_vp, ctypes.POINTER(_Inputs), ctypes.POINTER(_Outputs
 lib.h2sp_build_ex.argtypes = [_vp, ctypes.POINTER(_Inputs), ctypes.POINTER(_Outputs), _vp, ctypes.c_size_t, _vp,
                               ctypes.POINTER(_vp), _i64]
 lib.h2sp_plan_launches.argtypes = [_vp, ctypes.POINTER(_LaunchInfo), _i64, ctypes.POINTER(_i64)]
+lib.h2sp_build_apply.argtypes = [_vp, ctypes.POINTER(_Inputs), ctypes.POINTER(_Outputs), _vp, ctypes.c_size_t,
+                                 ctypes.POINTER(_ApplyArgs), _vp, ctypes.POINTER(_vp), _i64]
 lib.h2sp_build_host.argtypes = [_vp, ctypes.POINTER(_Inputs), ctypes.POINTER(_Outputs), ctypes.POINTER(_Inputs),
                                 ctypes.POINTER(_Outputs), _vp, ctypes.c_size_t, _vp]
 lib.h2sp_apply_ws_bytes.argtypes = [_vp, ctypes.c_int]
@@ -299,6 +306,30 @@ class Sparsifier:
         _check(lib.h2sp_build_ex(self.plan.handle, ctypes.byref(self._abi_inputs()),
                                  ctypes.byref(self._abi_outputs()), self.ws_ptr, self.ws_bytes,
                                  _stream_handle(stream), arr, len(events)), "h2sp_build_ex")
+        return self.outputs
+
+    def apply_workspace(self, nrhs: int):
+        """A separate uploaded workspace for the applies of h2sp_build_apply."""
+        import torch
+        need = int(lib.h2sp_apply_ws_bytes(self.plan.handle, nrhs))
+        ws = torch.empty(need + 256, dtype=torch.uint8, device=self.device)
+        ptr = (ws.data_ptr() + 255) // 256 * 256
+        _check(lib.h2sp_plan_upload(self.plan.handle, ptr, need, _stream_handle(None)), "h2sp_plan_upload")
+        return ws, ptr, need
+
+    def build_apply(self, b, y, w, x, apply_ws, events=None, stream=None):
+        """One pass: build + y = U^T b + x = V w (w may be y), the applies
+        overlapping the congruence (h2sp_build_apply).  b, x: (nrhs, n_tree_local);
+        y, w: (nrhs, s_rows); apply_ws from apply_workspace()."""
+        nrhs = b.shape[0] if b is not None else w.shape[0]
+        _, ptr, need = apply_ws
+        a = _ApplyArgs(b=_dptr(b), ldb=b.shape[-1] if b is not None else 0, y=_dptr(y),
+                       ldy=y.shape[-1] if y is not None else 0, w=_dptr(w), ldw=w.shape[-1] if w is not None else 0,
+                       x=_dptr(x), ldx=x.shape[-1] if x is not None else 0, nrhs=nrhs, ws=ptr, ws_bytes=need)
+        arr = (_vp * len(events))(*[e.cuda_event for e in events]) if events else None
+        _check(lib.h2sp_build_apply(self.plan.handle, ctypes.byref(self._abi_inputs()),
+                                    ctypes.byref(self._abi_outputs()), self.ws_ptr, self.ws_bytes, ctypes.byref(a),
+                                    _stream_handle(stream), arr, len(events) if events else 0), "h2sp_build_apply")
         return self.outputs
 
     def build_host(self, host_inputs: dict, host_outputs: dict, stream=None):

@@ -72,6 +72,26 @@ h2sp_status h2sp_build_ex(h2sp_plan P, const h2sp_inputs *in, const h2sp_outputs
   return s;
 }
 
+h2sp_status h2sp_build_apply(h2sp_plan P, const h2sp_inputs *in, const h2sp_outputs *out, void *ws, size_t ws_bytes,
+                             const h2sp_apply_args *ap, void *stream, void *const *events, int64_t n_events) {
+  if (!P || !in || !out || !ap) return fail(H2SP_EINVAL, "NULL plan, inputs, outputs or apply arguments");
+  if (events && n_events < 2 * P->launches) return fail(H2SP_EINVAL, "need 2 * launches events");
+  if (h2sp_status s = check_ws(P, ws, ws_bytes, P->ws_total)) return s;
+  if (!out->q_row || !out->s_val || (!P->sym && !out->q_col)) return fail(H2SP_EINVAL, "NULL output array");
+  if (ap->ws == ws) return fail(H2SP_EINVAL, "the apply workspace must differ from the build workspace");
+  if (ap->nrhs < 1) return fail(H2SP_EINVAL, "nrhs < 1");
+  if (h2sp_status s = check_ws(P, ap->ws, ap->ws_bytes, size_t(h2sp_apply_ws_bytes(P, ap->nrhs)))) return s;
+  if (ap->b && (!ap->y || ap->ldb < P->n_leaves_local * P->B || ap->ldy < P->n_rows_local))
+    return fail(H2SP_EINVAL, "bad U^T b arguments");
+  if (ap->w && (!ap->x || ap->ldx < P->n_leaves_local * P->B || ap->ldw < P->n_cols_local))
+    return fail(H2SP_EINVAL, "bad V w arguments");
+  if (h2sp_status s = check_device()) return s;
+  int64_t nl = 0;
+  h2sp_status s = launch_build(P, in, out, static_cast<unsigned char *>(ws), stream, &nl, events, n_events, ap);
+  if (s == H2SP_OK && nl != P->launches) return fail(H2SP_EINVAL, "internal: launch count mismatch");
+  return s;
+}
+
 h2sp_status h2sp_build_host(h2sp_plan P, const h2sp_inputs *hi, const h2sp_outputs *ho, const h2sp_inputs *di,
                             const h2sp_outputs *dout, void *ws, size_t ws_bytes, void *stream) {
   if (!P || !hi || !ho || !di || !dout) return fail(H2SP_EINVAL, "NULL argument");

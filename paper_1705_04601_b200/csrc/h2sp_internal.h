@@ -156,7 +156,8 @@ h2sp_status fail(h2sp_status s, const std::string &msg);
 
 // kernels.cu
 h2sp_status launch_build(const h2sp_plan_s *p, const h2sp_inputs *in, const h2sp_outputs *out, unsigned char *ws,
-                         void *stream, int64_t *launches, void *const *events, int64_t n_events);
+                         void *stream, int64_t *launches, void *const *events, int64_t n_events,
+                         const h2sp_apply_args *ap = nullptr);
 h2sp_status launch_apply_Ut(const h2sp_plan_s *p, const double *q, const double *b, int64_t ldb, double *y,
                             int64_t ldy, int nrhs, unsigned char *ws, void *stream, bool col_side);
 h2sp_status launch_apply_V(const h2sp_plan_s *p, const double *q, const double *y, int64_t ldy, double *x,

@@ -1342,7 +1342,8 @@ static h2sp_status get_aux(int L, DeviceAux **out) {
 }
 
 h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp_outputs *out, unsigned char *ws,
-                         void *stream, int64_t *launches, void *const *events, int64_t n_events) {
+                         void *stream, int64_t *launches, void *const *events, int64_t n_events,
+                         const h2sp_apply_args *ap) {
   cudaStream_t st = (cudaStream_t)stream;
   const unsigned char *meta = ws;
   const Clusters cl = make_clusters(P, meta);
@@ -1548,6 +1549,21 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       H2SP_CK(cudaEventRecord(ev_ready(k + 1), s1));
     }
   }
+  // ---- the applies of the same pass (need Q only): on s1 after the QR chain
+  cudaEvent_t ev_apply = aux->ev[8 + 2 * L];
+  if (ap) {
+    unsigned char *aws = static_cast<unsigned char *>(ap->ws);
+    if (ap->b) {
+      if (h2sp_status e = launch_apply_Ut(P, out->q_row, ap->b, ap->ldb, ap->y, ap->ldy, ap->nrhs, aws, s1, false))
+        return e;
+    }
+    if (ap->w) {
+      if (h2sp_status e = launch_apply_V(P, sym ? out->q_row : q_col, ap->w, ap->ldw, ap->x, ap->ldx, ap->nrhs, aws,
+                                         s1, !sym))
+        return e;
+    }
+    H2SP_CK(cudaEventRecord(ev_apply, s1));
+  }
   for (int k = 0; k <= L; k++) {
     const LevelPlan &lp = P->levels[k];
     if (k > 0) H2SP_CK(cudaStreamWaitEvent(st, ev_ready(k), 0));
@@ -1632,6 +1648,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   H2SP_CK(cudaEventRecord(ev_strips_done, s3));
   // ---- join
   if (L > 0) H2SP_CK(cudaStreamWaitEvent(st, ev_ready(L), 0));
+  if (ap) H2SP_CK(cudaStreamWaitEvent(st, ev_apply, 0));
   H2SP_CK(cudaStreamWaitEvent(st, ev_csr, 0));
   H2SP_CK(cudaStreamWaitEvent(st, ev_strips_done, 0));
   if (st != user_st) {

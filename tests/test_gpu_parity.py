@@ -295,3 +295,28 @@ def test_graph_capture_replay_equals_direct():
     torch.cuda.synchronize()
     for k, v in ref.items():
         assert torch.equal(v, sp.outputs[k]), k
+
+
+@pytest.mark.parametrize("sym", [True, False])
+def test_build_apply_matches_separate_calls(sym):
+    """h2sp_build_apply (applies on the QR side stream, overlapping the build)
+    equals h2sp_build followed by h2sp_apply_Ut / h2sp_apply_V, bitwise."""
+    _need_gpu()
+    import paper_1705_04601_b200 as h2sp
+    h = h2gen.random_h2(5, 16, 60 + sym, sym, eta=0.7)
+    packed = h2gen.pack(h)
+    plan = h2sp.Plan(packed)
+    sp = h2sp.Sparsifier(plan, packed)
+    b = torch.from_numpy(np.random.default_rng(5).standard_normal((2, h.N))).cuda()
+    y1, x1 = torch.empty_like(b), torch.empty_like(b)
+    sp.build()
+    sp.apply_Ut(b, y1)
+    sp.apply_V(y1, x1)
+    torch.cuda.synchronize()
+    s1 = sp.outputs["s_val"].clone()
+    y2, x2 = torch.zeros_like(b), torch.zeros_like(b)
+    aws = sp.apply_workspace(2)
+    sp.build_apply(b, y2, y2, x2, aws)
+    torch.cuda.synchronize()
+    assert torch.equal(s1, sp.outputs["s_val"])
+    assert torch.equal(y1, y2) and torch.equal(x1, x2)
