@@ -96,13 +96,14 @@ struct LevelPlan {
   int np_row, np_col;    // max n_t at this level (row / column side)
   int mp;                // max strip width at this level
   int64_t n_pairs, n_pair_chunks;
-  int64_t n_rstrips, n_rpanels, n_rgroups;    // n_*strips = number of column tiles (launch size)
-  int64_t n_cstrips, n_cpanels, n_cgroups;
   int64_t n_coup;
   size_t pairs_off, pair_chunks_off;          // byte offsets in meta
-  size_t rtiles_off, rpanels_off, rgroups_off;
-  size_t ctiles_off, cpanels_off, cgroups_off;
   size_t coup_off;
+  struct StripSet {                           // strip panels of one set at this level (tiles = launch size)
+    int64_t n_rtiles, n_ctiles;
+    size_t rtiles_off, rpanels_off, rgroups_off;
+    size_t ctiles_off, cpanels_off, cgroups_off;
+  } sp[2];                                    // [0]: groups born at level 0, [1]: born at a level >= 1
   int np_pair;           // padded tile size for the congruence at this level
   int np_rstrip, np_cstrip;
 };

@@ -868,8 +868,8 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS)
   double *sG = sm + NP * LD;
   double *sQs = sm + 2 * NP * LD;
   const Chunk ch = A.chunks[blockIdx.x];
-  const int t = A.items[ch.begin].t;
-  const int nt = A.rs.n[t], ktt = A.rs.k[t];
+  int t = A.items[ch.begin].t;   // current block row (the chunk may cross rows)
+  int nt = A.rs.n[t], ktt = A.rs.k[t];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = lane >> 2, q = lane & 3;
   const int m0 = warp * 8 * TM;
@@ -901,6 +901,15 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS)
     const int s = it.s;
     cp_wait_all();
     __syncthreads();
+    if (it.t != t) {  // new block row: reload the resident Q_t (G and Q_s of this pair are in flight/landed)
+      t = it.t;
+      nt = A.rs.n[t];
+      ktt = A.rs.k[t];
+      async_tile<NP, NP, LD>(sQt, A.q_row + A.rs.q_off[t], nt, nt, nt, A.items);
+      cp_commit();
+      cp_wait_all();
+      __syncthreads();
+    }
     // ---- T = Q_t^T G (rows m0..m0+15), interleaved with the scatter of the previous H
     double T[TM][TN][2];
     zero_acc(T);
@@ -930,7 +939,8 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS)
     __syncthreads();  // every warp is done with G
     const bool more = p + 1 < ch.end && !(A.debug & 2);
     if (more) {
-      pair_load_G<NP>(A, A.items[p + 1], t, nt, lbase, sG);
+      const PairItem nx = A.items[p + 1];
+      pair_load_G<NP>(A, nx, nx.t, A.rs.n[nx.t], lbase, sG);
       cp_commit();
     }
     // ---- H = T Q_s; A fragment (row m0+8i+r, col k0+q) lives in lane (r, (k0%8+q)/2), element q%2
@@ -1309,7 +1319,7 @@ static h2sp_status launch_strips(const StripArgs &a, int np, int64_t ntiles, cud
 // stream, so a build stays stream-ordered (and CUDA-graph capturable).
 struct DeviceAux {
   bool init = false;
-  cudaStream_t side[4];    // QR/coupling chain, CSR, strips, main chain
+  cudaStream_t side[5];    // QR/coupling chain, CSR, strips (set 0), main chain, strips (set 1)
   std::vector<cudaEvent_t> ev;
 };
 static DeviceAux g_aux[64];
@@ -1330,6 +1340,7 @@ static h2sp_status get_aux(int L, DeviceAux **out) {
     const int mid = hi < lo ? hi + 1 : hi;
     H2SP_CK(cudaStreamCreateWithPriority(&a.side[2], cudaStreamNonBlocking, mid));  // strips
     H2SP_CK(cudaStreamCreateWithPriority(&a.side[3], cudaStreamNonBlocking, mid));  // main chain
+    H2SP_CK(cudaStreamCreateWithPriority(&a.side[4], cudaStreamNonBlocking, mid));  // strips, set 1
     a.init = true;
   }
   while (int(a.ev.size()) < 3 * L + 12) {
@@ -1361,7 +1372,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   const int L = P->L;
   DeviceAux *aux = nullptr;
   if (h2sp_status e = get_aux(L, &aux)) return e;
-  cudaStream_t s1 = aux->side[0], s2 = aux->side[1], s3 = aux->side[2];
+  cudaStream_t s1 = aux->side[0], s2 = aux->side[1], s3 = aux->side[2], s4 = aux->side[4];
   const cudaStream_t user_st = st;
   cudaEvent_t ev_begin = aux->ev[6 + 2 * L], ev_end = aux->ev[7 + 2 * L];
   static const bool serial = [] {
@@ -1369,7 +1380,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     return e && e[0] == '1';
   }();
   if (serial) {
-    s1 = s2 = s3 = st;
+    s1 = s2 = s3 = s4 = st;
   } else {
     // the main chain runs on an internal high-priority stream forked from the
     // caller's stream (the CSR stream has the lowest priority and fills gaps)
@@ -1401,7 +1412,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     qr_attr = true;
   }
   // Launch indices are assigned in the plan's canonical order; precompute them.
-  struct LvlIdx { int64_t qr_row = -1, qr_col = -1, coup = -1, pairs = -1, rstr = -1, cstr = -1; };
+  struct LvlIdx { int64_t qr_row = -1, qr_col = -1, coup = -1, pairs = -1, rstr[2] = {-1, -1}, cstr[2] = {-1, -1}; };
   std::vector<LvlIdx> li(L + 1);
   int64_t csr_idx = -1;
   {
@@ -1412,8 +1423,10 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       if (!sym && lp.np_col > 0) li[k].qr_col = c++;
       if (lp.n_coup) li[k].coup = c++;
       if (lp.n_pairs) li[k].pairs = c++;
-      if (lp.n_rstrips) li[k].rstr = c++;
-      if (lp.n_cstrips) li[k].cstr = c++;
+      for (int set = 0; set < 2; set++) {
+        if (lp.sp[set].n_rtiles) li[k].rstr[set] = c++;
+        if (lp.sp[set].n_ctiles) li[k].cstr[set] = c++;
+      }
     }
     if (P->n_csr_rows) csr_idx = c++;
     nl = c;
@@ -1603,54 +1616,63 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       if (s != H2SP_OK) return s;
       if (h2sp_status e = post(st, li[k].pairs)) return e;
     }
-    // ---- strips arriving from level k-1, on s3 concurrently with the next
-    //      congruence: they need the level-(k-1) congruence (new strips) and Q_k
+    // ---- strips arriving from level k-1.  Set 0 (groups born at level 0) on s3:
+    //      it needs only the level-0 congruence and Q_k, so it runs concurrently
+    //      with the whole upper-level congruence chain.  Set 1 (born at a level
+    //      >= 1) on s4: it needs the level-(k-1) congruence (its new strips).
     H2SP_CK(cudaEventRecord(ev_pairs(k), st));
-    if (lp.n_rstrips || lp.n_cstrips) {
-      H2SP_CK(cudaStreamWaitEvent(s3, ev_pairs(k - 1), 0));
-      H2SP_CK(cudaStreamWaitEvent(s3, ev_ready(k), 0));
-    }
-    if (lp.n_rstrips) {
-      StripArgs a;
-      a.tiles = (const StripTile *)(meta + lp.rtiles_off);
-      a.panels = (const StripPanel *)(meta + lp.rpanels_off);
-      a.groups = (const StripGroup *)(meta + lp.rgroups_off);
-      a.sd = rs;
-      a.L = L;
-      a.level = k;
-      a.q = out->q_row;
-      a.y_in = yr;
-      a.y_out = yr;
-      a.s_val = out->s_val;
-      if (h2sp_status e = pre(s3, li[k].rstr)) return e;
-      h2sp_status s = launch_strips(a, lp.np_rstrip, lp.n_rstrips, s3);
-      if (s != H2SP_OK) return s;
-      if (h2sp_status e = post(s3, li[k].rstr)) return e;
-    }
-    if (lp.n_cstrips) {
-      StripArgs a;
-      a.tiles = (const StripTile *)(meta + lp.ctiles_off);
-      a.panels = (const StripPanel *)(meta + lp.cpanels_off);
-      a.groups = (const StripGroup *)(meta + lp.cgroups_off);
-      a.sd = cs;
-      a.L = L;
-      a.level = k;
-      a.q = q_col;
-      a.y_in = yc;
-      a.y_out = yc;
-      a.s_val = out->s_val;
-      if (h2sp_status e = pre(s3, li[k].cstr)) return e;
-      h2sp_status s = launch_strips(a, lp.np_cstrip, lp.n_cstrips, s3);
-      if (s != H2SP_OK) return s;
-      if (h2sp_status e = post(s3, li[k].cstr)) return e;
+    for (int set = 0; set < 2; set++) {
+      const LevelPlan::StripSet &sp = lp.sp[set];
+      cudaStream_t ss = set == 0 ? s3 : s4;
+      if (sp.n_rtiles || sp.n_ctiles) {
+        H2SP_CK(cudaStreamWaitEvent(ss, ev_pairs(set == 0 ? 0 : k - 1), 0));
+        H2SP_CK(cudaStreamWaitEvent(ss, ev_ready(k), 0));
+      }
+      if (sp.n_rtiles) {
+        StripArgs a;
+        a.tiles = (const StripTile *)(meta + sp.rtiles_off);
+        a.panels = (const StripPanel *)(meta + sp.rpanels_off);
+        a.groups = (const StripGroup *)(meta + sp.rgroups_off);
+        a.sd = rs;
+        a.L = L;
+        a.level = k;
+        a.q = out->q_row;
+        a.y_in = yr;
+        a.y_out = yr;
+        a.s_val = out->s_val;
+        if (h2sp_status e = pre(ss, li[k].rstr[set])) return e;
+        h2sp_status s = launch_strips(a, lp.np_rstrip, sp.n_rtiles, ss);
+        if (s != H2SP_OK) return s;
+        if (h2sp_status e = post(ss, li[k].rstr[set])) return e;
+      }
+      if (sp.n_ctiles) {
+        StripArgs a;
+        a.tiles = (const StripTile *)(meta + sp.ctiles_off);
+        a.panels = (const StripPanel *)(meta + sp.cpanels_off);
+        a.groups = (const StripGroup *)(meta + sp.cgroups_off);
+        a.sd = cs;
+        a.L = L;
+        a.level = k;
+        a.q = q_col;
+        a.y_in = yc;
+        a.y_out = yc;
+        a.s_val = out->s_val;
+        if (h2sp_status e = pre(ss, li[k].cstr[set])) return e;
+        h2sp_status s = launch_strips(a, lp.np_cstrip, sp.n_ctiles, ss);
+        if (s != H2SP_OK) return s;
+        if (h2sp_status e = post(ss, li[k].cstr[set])) return e;
+      }
     }
   }
   H2SP_CK(cudaEventRecord(ev_strips_done, s3));
+  cudaEvent_t ev_strips1_done = aux->ev[9 + 2 * L];
+  H2SP_CK(cudaEventRecord(ev_strips1_done, s4));
   // ---- join
   if (L > 0) H2SP_CK(cudaStreamWaitEvent(st, ev_ready(L), 0));
   if (ap) H2SP_CK(cudaStreamWaitEvent(st, ev_apply, 0));
   H2SP_CK(cudaStreamWaitEvent(st, ev_csr, 0));
   H2SP_CK(cudaStreamWaitEvent(st, ev_strips_done, 0));
+  H2SP_CK(cudaStreamWaitEvent(st, ev_strips1_done, 0));
   if (st != user_st) {
     H2SP_CK(cudaEventRecord(ev_end, st));
     H2SP_CK(cudaStreamWaitEvent(user_st, ev_end, 0));

@@ -320,16 +320,17 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
     double flops_qr = 0, flops_coup = 0, flops_cong = 0, flops_strip = 0;
     int64_t dt_len = 0, bb_len = 0, yr_len = 0, yc_len = 0;
     std::vector<std::vector<PairItem>> pairs(L + 1);
-    std::vector<std::vector<StripPanel>> rpan(L + 1), cpan(L + 1);
-    std::vector<std::vector<StripGroup>> rgrp(L + 1), cgrp(L + 1);
-    std::vector<std::vector<StripTile>> rtil(L + 1), ctil(L + 1);
-    std::vector<std::vector<int64_t>> rgrp_direct(L + 1);   // direct S dst of each row group (checked below)
+    // strip panels, index set * (L+1) + level (set 0: groups born at level 0, set 1: later)
+    std::vector<std::vector<StripPanel>> rpan(2 * (L + 1)), cpan(2 * (L + 1));
+    std::vector<std::vector<StripGroup>> rgrp(2 * (L + 1)), cgrp(2 * (L + 1));
+    std::vector<std::vector<StripTile>> rtil(2 * (L + 1)), ctil(2 * (L + 1));
+    std::vector<std::vector<int64_t>> rgrp_direct(2 * (L + 1));   // direct S dst of each row group (checked below)
     std::vector<std::vector<CouplingItem>> coup(L + 1);
     std::vector<std::vector<int64_t>> dt_slot(L + 1), bb_slot(L + 1);
     std::vector<std::vector<int64_t>> pair_index(L + 1);   // near index -> item index (canonical) or -1
     std::vector<BlockRec> blocks;
-    std::vector<std::vector<Grp>> R_prev, C_prev;     // groups of each panel at level k-1
-    std::vector<int64_t> Rb_prev, Cb_prev;            // panel bases at level k-1
+    std::vector<std::vector<Grp>> R_prev[2], C_prev[2];   // groups of each panel at level k-1, per set
+    std::vector<int64_t> Rb_prev[2], Cb_prev[2];          // panel bases at level k-1, per set
     for (int k = 0; k <= L; k++) {
       const int64_t base = lvl_off(L, k);
       const int64_t M = int64_t(1) << (L - k);
@@ -416,10 +417,14 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
         flops_cong += 2.0 * nr[ct] * nc[cs] * (nr[ct] + nc[cs]);
       }
       // ---- strips arriving from level k-1 (Eq. u1v1): one panel per rotating cluster
-      std::vector<std::vector<Grp>> R_cur(M), C_cur(M);
+      //      and per panel set: set 0 = groups born at level 0 (they depend on the
+      //      level-0 congruence only and run concurrently with the upper levels),
+      //      set 1 = groups born at a level >= 1.  Index of (set, level): set*(L+1)+k.
+      std::vector<std::vector<Grp>> R_cur[2] = {std::vector<std::vector<Grp>>(M), std::vector<std::vector<Grp>>(M)};
+      std::vector<std::vector<Grp>> C_cur[2] = {std::vector<std::vector<Grp>>(M), std::vector<std::vector<Grp>>(M)};
       auto merge = [&](std::vector<std::vector<Grp>> &prev, std::vector<int64_t> &prev_base, bool row_side,
-                       std::vector<StripPanel> &pans, std::vector<StripGroup> &grps, std::vector<StripTile> &tils,
-                       std::vector<std::vector<Grp>> &cur) {
+                       int sidx, std::vector<StripPanel> &pans, std::vector<StripGroup> &grps,
+                       std::vector<StripTile> &tils, std::vector<std::vector<Grp>> &cur) {
         const auto &kq = row_side ? kr : kc;
         const auto &nq = row_side ? nr : nc;
         for (int64_t p = 0; p < M; p++) {
@@ -461,10 +466,11 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
             const int64_t cf = lvl_off(L, g.l) + g.s;  // fixed cluster
             if (mq > 0) {
               if (row_side) {
-                if (mine(k, p)) blocks.push_back(BlockRec{loc_off[cq], P->s_off_col[cf], mq, g.m, 2, k, gi});
-                if (sym && mine(g.l, g.s)) blocks.push_back(BlockRec{loc_off[cf], P->s_off_col[cq], g.m, mq, 3, k, gi});
+                if (mine(k, p)) blocks.push_back(BlockRec{loc_off[cq], P->s_off_col[cf], mq, g.m, 2, sidx, gi});
+                if (sym && mine(g.l, g.s))
+                  blocks.push_back(BlockRec{loc_off[cf], P->s_off_col[cq], g.m, mq, 3, sidx, gi});
               } else if (mine(g.l, g.s)) {
-                blocks.push_back(BlockRec{loc_off[cf], P->s_off_col[cq], g.m, mq, 4, k, gi});
+                blocks.push_back(BlockRec{loc_off[cf], P->s_off_col[cq], g.m, mq, 4, sidx, gi});
               }
             }
             const double rows = (takeA ? kq[c1] : 0) + (takeB ? kq[c1 + 1] : 0);
@@ -485,11 +491,14 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
           pans.push_back(pn);
         }
       };
-      if (k > 0) {
-        merge(R_prev, Rb_prev, true, rpan[k], rgrp[k], rtil[k], R_cur);
-        if (!sym) merge(C_prev, Cb_prev, false, cpan[k], cgrp[k], ctil[k], C_cur);
-      }
+      if (k > 0)
+        for (int set = 0; set < 2; set++) {
+          const int sidx = set * (L + 1) + k;
+          merge(R_prev[set], Rb_prev[set], true, sidx, rpan[sidx], rgrp[sidx], rtil[sidx], R_cur[set]);
+          if (!sym) merge(C_prev[set], Cb_prev[set], false, sidx, cpan[sidx], cgrp[sidx], ctil[sidx], C_cur[set]);
+        }
       // ---- strips started at this level (from every pair of N_k) and S blocks of pairs
+      const int nset = k == 0 ? 0 : 1;  // the panel set new strips of this level belong to
       struct NewStrip { int64_t item; int which; int64_t c; int32_t col0; };  // which: 0 yr, 1 yc
       std::vector<NewStrip> newr, newc;
       for (size_t j = 0; j < Nk.size(); j++) {
@@ -499,14 +508,14 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
         int64_t item = canon ? pair_index[k][j] : pair_index[k][find(Nk, pkey(s, t))];
         const bool row_ok = mine(k, t) || (sym && mine(k, s));
         if (kr[ct] > 0 && mc(cs) > 0 && row_ok) {
-          auto &lst = R_cur[t];
+          auto &lst = R_cur[nset][t];
           const int32_t col0 = lst.empty() ? 0 : lst.back().col0 + lst.back().m;
           lst.push_back(Grp{k, s, mc(cs), col0});
           // H_ts = H_st^T when t > s (symmetric): row strip of (t,s) = (nb part of H_st)^T
           newr.push_back(NewStrip{item, canon ? 0 : 1, t, col0});
         }
         if (!sym && mr(ct) > 0 && kc[cs] > 0 && mine(k, t)) {
-          auto &lst = C_cur[s];
+          auto &lst = C_cur[nset][s];
           const int32_t col0 = lst.empty() ? 0 : lst.back().col0 + lst.back().m;
           lst.push_back(Grp{k, t, mr(ct), col0});
           newc.push_back(NewStrip{item, 1, s, col0});
@@ -527,38 +536,44 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
         }
         return b;
       };
-      std::vector<int64_t> Rb = bases(R_cur, kr, yr_len);
-      std::vector<int64_t> Cb = sym ? std::vector<int64_t>(M, -1) : bases(C_cur, kc, yc_len);
+      std::vector<int64_t> Rb[2], Cb[2];
+      for (int set = 0; set < 2; set++) {
+        Rb[set] = bases(R_cur[set], kr, yr_len);
+        Cb[set] = sym ? std::vector<int64_t>(M, -1) : bases(C_cur[set], kc, yc_len);
+      }
       auto width = [](const std::vector<Grp> &g) { return g.empty() ? 0 : g.back().col0 + g.back().m; };
       for (const NewStrip &ns : newr) {
         PairItem &it = pairs[k][ns.item];
         if (ns.which == 0) {
-          it.yr_dst = Rb[ns.c] + ns.col0;
-          it.yr_ld = width(R_cur[ns.c]);
+          it.yr_dst = Rb[nset][ns.c] + ns.col0;
+          it.yr_ld = width(R_cur[nset][ns.c]);
         } else {
-          it.yc_dst = Rb[ns.c] + ns.col0;
-          it.yc_ld = width(R_cur[ns.c]);
+          it.yc_dst = Rb[nset][ns.c] + ns.col0;
+          it.yc_ld = width(R_cur[nset][ns.c]);
         }
       }
       for (const NewStrip &ns : newc) {
         PairItem &it = pairs[k][ns.item];
-        it.yc_dst = Cb[ns.c] + ns.col0;
-        it.yc_ld = width(C_cur[ns.c]);
+        it.yc_dst = Cb[nset][ns.c] + ns.col0;
+        it.yc_ld = width(C_cur[nset][ns.c]);
       }
-      for (auto &pn : rpan[k])
-        if (kr[pn.q] > 0) {
-          pn.y_dst = Rb[pn.q - base];
-          pn.y_ld = width(R_cur[pn.q - base]);
-        }
-      for (auto &pn : cpan[k])
-        if (kc[pn.q] > 0) {
-          pn.y_dst = Cb[pn.q - base];
-          pn.y_ld = width(C_cur[pn.q - base]);
-        }
-      R_prev.swap(R_cur);
-      C_prev.swap(C_cur);
-      Rb_prev.swap(Rb);
-      Cb_prev.swap(Cb);
+      for (int set = 0; set < 2; set++) {
+        const int sidx = set * (L + 1) + k;
+        for (auto &pn : rpan[sidx])
+          if (kr[pn.q] > 0) {
+            pn.y_dst = Rb[set][pn.q - base];
+            pn.y_ld = width(R_cur[set][pn.q - base]);
+          }
+        for (auto &pn : cpan[sidx])
+          if (kc[pn.q] > 0) {
+            pn.y_dst = Cb[set][pn.q - base];
+            pn.y_ld = width(C_cur[set][pn.q - base]);
+          }
+        R_prev[set].swap(R_cur[set]);
+        C_prev[set].swap(C_cur[set]);
+        Rb_prev[set].swap(Rb[set]);
+        Cb_prev[set].swap(Cb[set]);
+      }
     }
 
     // ---------------------------------------------------------------- Q needed by this shard
@@ -571,8 +586,10 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
           need_r[it.t] = 1;
           need_c[it.s] = 1;
         }
-        for (const auto &pn : rpan[k]) need_r[pn.q] = 1;
-        for (const auto &pn : cpan[k]) need_c[pn.q] = 1;
+        for (int set = 0; set < 2; set++) {
+          for (const auto &pn : rpan[set * (L + 1) + k]) need_r[pn.q] = 1;
+          for (const auto &pn : cpan[set * (L + 1) + k]) need_c[pn.q] = 1;
+        }
         for (const auto &ci : coup[k]) {
           need_r[ci.t] = 1;
           need_c[ci.s] = 1;
@@ -649,17 +666,17 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
     }
     P->s_nnz = nnz;
     P->s_blocks = int64_t(blocks.size());
-    // direct strip output of a panel: its groups are the first blocks of S row
-    // block (q@k), so they must be contiguous from the row start
-    for (int k = 1; k <= L; k++)
-      for (auto &pn : rpan[k]) {
+    // direct strip output of a panel: its groups are consecutive blocks of S row
+    // block (q@k) (set 0 at the row start, set 1 right after), so contiguous in S
+    for (int sidx = 0; sidx < 2 * (L + 1); sidx++)
+      for (auto &pn : rpan[sidx]) {
         const int32_t mq = nr[pn.q] - kr[pn.q];
         if (mq == 0 || pn.gend == pn.gbeg || loc_off[pn.q] < 0) continue;
-        const int64_t d0 = rgrp_direct[k][pn.gbeg];
+        const int64_t d0 = rgrp_direct[sidx][pn.gbeg];
         const int64_t r0 = loc_off[pn.q];
-        if (d0 != rowptr[r0]) throw PlanError(H2SP_ETREE, "internal: strip panel not at the start of its S row");
+        if (sidx <= L && d0 != rowptr[r0]) throw PlanError(H2SP_ETREE, "internal: strip panel not at the start of its S row");
         for (int32_t g = pn.gbeg; g < pn.gend; g++)
-          if (rgrp_direct[k][g] != d0 + rgrp[k][g].col0)
+          if (rgrp_direct[sidx][g] != d0 + rgrp[sidx][g].col0)
             throw PlanError(H2SP_ETREE, "internal: strip panel not contiguous in S");
         pn.s_dst = d0;
         pn.s_ld = int32_t(rowptr[r0 + 1] - rowptr[r0]);
@@ -731,18 +748,17 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
       auto pc = chunk(pairs[k], [](const PairItem &x) { return x.t; });
       lp.n_pair_chunks = int64_t(pc.size());
       lp.pair_chunks_off = mb.put(pc);
-      lp.n_rstrips = int64_t(rtil[k].size());
-      lp.n_rpanels = int64_t(rpan[k].size());
-      lp.n_rgroups = int64_t(rgrp[k].size());
-      lp.rtiles_off = mb.put(rtil[k]);
-      lp.rpanels_off = mb.put(rpan[k]);
-      lp.rgroups_off = mb.put(rgrp[k]);
-      lp.n_cstrips = int64_t(ctil[k].size());
-      lp.n_cpanels = int64_t(cpan[k].size());
-      lp.n_cgroups = int64_t(cgrp[k].size());
-      lp.ctiles_off = mb.put(ctil[k]);
-      lp.cpanels_off = mb.put(cpan[k]);
-      lp.cgroups_off = mb.put(cgrp[k]);
+      for (int set = 0; set < 2; set++) {
+        const int sidx = set * (L + 1) + k;
+        lp.sp[set].n_rtiles = int64_t(rtil[sidx].size());
+        lp.sp[set].rtiles_off = mb.put(rtil[sidx]);
+        lp.sp[set].rpanels_off = mb.put(rpan[sidx]);
+        lp.sp[set].rgroups_off = mb.put(rgrp[sidx]);
+        lp.sp[set].n_ctiles = int64_t(ctil[sidx].size());
+        lp.sp[set].ctiles_off = mb.put(ctil[sidx]);
+        lp.sp[set].cpanels_off = mb.put(cpan[sidx]);
+        lp.sp[set].cgroups_off = mb.put(cgrp[sidx]);
+      }
       lp.n_coup = int64_t(coup[k].size());
       lp.coup_off = mb.put(coup[k]);
       // launches issued by launch_build (kept in sync with kernels.cu), with
@@ -819,13 +835,16 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
         }
         return li;
       };
-      if (lp.n_rstrips) {
-        launches++;
-        P->launch_info.push_back(strip_info(rpan[k], rgrp[k], rtil[k], nr, kr, 4, qbytes_row));
-      }
-      if (lp.n_cstrips) {
-        launches++;
-        P->launch_info.push_back(strip_info(cpan[k], cgrp[k], ctil[k], nc, kc, 5, qbytes_col));
+      for (int set = 0; set < 2; set++) {
+        const int sidx = set * (L + 1) + k;
+        if (lp.sp[set].n_rtiles) {
+          launches++;
+          P->launch_info.push_back(strip_info(rpan[sidx], rgrp[sidx], rtil[sidx], nr, kr, 4, qbytes_row));
+        }
+        if (lp.sp[set].n_ctiles) {
+          launches++;
+          P->launch_info.push_back(strip_info(cpan[sidx], cgrp[sidx], ctil[sidx], nc, kc, 5, qbytes_col));
+        }
       }
     }
     P->n_csr_rows = int64_t(csr_rows.size());
