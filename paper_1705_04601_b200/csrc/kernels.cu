@@ -1524,8 +1524,12 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   // ---- CSR index expansion on s2 (independent of all values).  It is a pure
   //      HBM write stream, so it is started after the level-0 congruence (which
   //      needs every SM slot) and overlaps the latency-bound upper levels.
+  static const bool no_csr = [] {   // debugging / attribution only: skip the index expansion
+    const char *e = getenv("H2SP_NO_CSR");
+    return e && e[0] == '1';
+  }();
   auto csr = [&]() -> h2sp_status {
-    if (csr_idx >= 0) {
+    if (csr_idx >= 0 && !no_csr) {
       if (h2sp_status e = pre(s2, csr_idx)) return e;
       if (out->s_rowptr)
         H2SP_CK(cudaMemcpyAsync(out->s_rowptr, meta + P->rowptr_off, size_t(P->n_rows_local + 1) * sizeof(int64_t),
