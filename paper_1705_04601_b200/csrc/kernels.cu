@@ -775,6 +775,15 @@ struct PairDst {          // the destinations of one pair, kept in registers
   bool dsym;
 };
 
+__device__ __forceinline__ void store2(double *d, double v0, double v1) {
+  if ((reinterpret_cast<uintptr_t>(d) & 15) == 0) {
+    *reinterpret_cast<double2 *>(d) = make_double2(v0, v1);
+  } else {
+    d[0] = v0;
+    d[1] = v1;
+  }
+}
+
 __device__ __forceinline__ void scatter_pair2(const PairArgs &A, const PairDst &D, int row0, int col0, int row,
                                               int col, double v0, double v1) {
   const bool r_nn = row0 >= D.kt, r_bb = row0 + 8 <= D.kt;
@@ -782,12 +791,8 @@ __device__ __forceinline__ void scatter_pair2(const PairArgs &A, const PairDst &
   if (row0 + 8 <= D.nt && col0 + 8 <= D.ns && !D.dsym && (r_nn || r_bb) && (c_nn || c_bb)) {
     if (r_nn && c_nn) {
       const int a = row - D.kt, b = col - D.ks;
-      if (D.s_dst >= 0) {
-        double *d = A.s_val + D.s_dst + int64_t(a) * D.s_ld + b;
-        d[0] = v0;
-        d[1] = v1;
-      }
-      if (D.s_dst_m >= 0) {
+      if (D.s_dst >= 0) store2(A.s_val + D.s_dst + int64_t(a) * D.s_ld + b, v0, v1);
+      if (D.s_dst_m >= 0 && !(A.debug & 4)) {
         double *d = A.s_val + D.s_dst_m + int64_t(b) * D.s_ld_m + a;
         d[0] = v0;
         d[D.s_ld_m] = v1;
@@ -799,15 +804,9 @@ __device__ __forceinline__ void scatter_pair2(const PairArgs &A, const PairDst &
         d[D.yc_ld] = v1;
       }
     } else if (c_bb) {
-      if (D.bb_dst >= 0) {
-        double *d = A.bb_out + D.bb_dst + row * D.ks + col;
-        d[0] = v0;
-        d[1] = v1;
-      }
+      if (D.bb_dst >= 0) store2(A.bb_out + D.bb_dst + row * D.ks + col, v0, v1);
     } else if (D.yr_dst >= 0) {
-      double *d = A.yr + D.yr_dst + int64_t(row) * D.yr_ld + (col - D.ks);
-      d[0] = v0;
-      d[1] = v1;
+      store2(A.yr + D.yr_dst + int64_t(row) * D.yr_ld + (col - D.ks), v0, v1);
     }
     return;
   }
@@ -1553,10 +1552,17 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   //      all couplings on s1, overlapping the level-0 congruence
   if (h2sp_status e = qr(0, st)) return e;
   H2SP_CK(cudaEventRecord(ev_qr0, st));
-  // CSR expansion after QR0 (which is on the critical path): overlaps the
-  // compute-bound level-0 congruence
-  H2SP_CK(cudaStreamWaitEvent(s2, ev_qr0, 0));
-  if (h2sp_status e = csr()) return e;
+  // CSR expansion: H2SP_CSR_AFTER=1 starts it after the level-0 congruence
+  // (fills gaps of the upper levels), default right after QR0 (overlaps the
+  // compute-bound level-0 congruence)
+  static const bool csr_after = [] {
+    const char *e = getenv("H2SP_CSR_AFTER");
+    return e && e[0] == '1';
+  }();
+  if (!csr_after) {
+    H2SP_CK(cudaStreamWaitEvent(s2, ev_qr0, 0));
+    if (h2sp_status e = csr()) return e;
+  }
   (void)ev_fork;
   H2SP_CK(cudaStreamWaitEvent(s1, ev_qr0, 0));
   for (int k = 0; k <= L; k++) {
@@ -1625,6 +1631,10 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     //      with the whole upper-level congruence chain.  Set 1 (born at a level
     //      >= 1) on s4: it needs the level-(k-1) congruence (its new strips).
     H2SP_CK(cudaEventRecord(ev_pairs(k), st));
+    if (k == 0 && csr_after) {
+      H2SP_CK(cudaStreamWaitEvent(s2, ev_pairs(0), 0));
+      if (h2sp_status e = csr()) return e;
+    }
     for (int set = 0; set < 2; set++) {
       const LevelPlan::StripSet &sp = lp.sp[set];
       cudaStream_t ss = set == 0 ? s3 : s4;
