@@ -410,7 +410,14 @@ def main():
                        "fp64_frac_of_peak_whole_step": value / world / FP64_PEAK_TFLOPS,
                        "job_flops_per_step": job_flops,
                        "hbm_frac_whole_step": plan.sizes["bytes"] / (ms_max * 1e-3) / (peaks["hbm_gbs"] * 1e9),
-                       "breakdown_ms": {k: round(v, 4) for k, v in kinds.items()}},
+                       "breakdown_ms": {k: round(v, 4) for k, v in kinds.items()},
+                       # the paper's sparsity figures (Fig. 1 nnz/row; §3 Proposition, reading 12:
+                       # informational, the printed bound is garbled)
+                       "sparsity": {"nnz_per_row": plan.sizes["s_nnz"] / plan.s_rows,
+                                    "s_blocks": plan.sizes["s_blocks"], "close_blocks": int(len(h.near)),
+                                    "s_blocks_per_close_block": plan.sizes["s_blocks"] / max(1, len(h.near)),
+                                    "bound_printed": 4 * plan.L + 6 * (2.0 ** -plan.L - 1),
+                                    "bound_corrected": 4 * plan.L - 2 + 3 * 2.0 ** -plan.L}},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -137,3 +137,16 @@ def test_sparsifier_refuses_without_cuda():
     plan = h2sp.Plan(h2gen.pack(h))
     with pytest.raises(RuntimeError):
         h2sp.Sparsifier(plan, h2gen.pack(h))
+
+
+def test_binding_fails_loudly_without_library(tmp_path):
+    """No CPU fallback: the package refuses to import without libh2sp.so."""
+    import shutil
+    import subprocess
+    import sys
+    pkg = tmp_path / "paper_1705_04601_b200"
+    shutil.copytree(h2sp.__path__[0], pkg, ignore=shutil.ignore_patterns("*.so", "csrc", "__pycache__"))
+    (tmp_path / "include").mkdir()
+    r = subprocess.run([sys.executable, "-c", "import paper_1705_04601_b200"], cwd=tmp_path, capture_output=True,
+                       text=True)
+    assert r.returncode != 0 and "libh2sp.so" in r.stderr
