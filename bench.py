@@ -338,6 +338,10 @@ def main():
     roof.update({"kernel": f"{li['kind']}@level{li['level']}", "launch_ms": per[top],
                  "share_of_step": per[top] / ms, "algorithmic_flops": li["flops"], "algorithmic_bytes": li["bytes"],
                  "arithmetic_intensity": ai,
+                 # what the kernel actually issues (compact-WY level-0 congruence:
+                 # 4 n_t n_s (k_t + k_s) per pair instead of 2 n_t n_s (n_t + n_s))
+                 "executed_flops": li["flops_exec"],
+                 "executed_frac": li["flops_exec"] / (per[top] * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
                  "peak_source": "FP64 DMMA microbenchmark on this pool's B200 (profiles/r01_fp64_peak.txt); "
                                 f"cuBLAS DGEMM measured {FP64_DGEMM_TFLOPS}",
                  "hbm_peak_gbs": peaks["hbm_gbs"]})
@@ -407,6 +411,9 @@ def main():
                              % (plan.sizes["close"] * 8e-9, plan.sizes["s_nnz"] * 12e-9),
                        "plan_ms": plan_ms, "s_nnz": plan.sizes["s_nnz"], "s_blocks": plan.sizes["s_blocks"],
                        "flops_per_step": step_flops, "bytes_per_step": plan.sizes["bytes"],
+                       "flops_convention": "algorithmic (SURVEY 8(d): explicit-Q congruence 2 n_t n_s (n_t + n_s)); "
+                                           "executed_flops_per_step counts what the kernels issue",
+                       "executed_flops_per_step": plan.sizes["flops_executed"] + apply_flops,
                        "fp64_frac_of_peak_whole_step": value / world / FP64_PEAK_TFLOPS,
                        "job_flops_per_step": job_flops,
                        "hbm_frac_whole_step": plan.sizes["bytes"] / (ms_max * 1e-3) / (peaks["hbm_gbs"] * 1e9),
@@ -431,13 +438,16 @@ def main():
 
 def _ncu_traffic(li):
     """dram bytes per launch of the dominant kernel from the committed ncu
-    summary (profiles/*_ncu_top.json), if one exists for this kernel."""
+    summary (profiles/*_ncu_top.json), if one exists for this kernel on this
+    workload (matched on its algorithmic flop count)."""
     import glob
     for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_top.json")), reverse=True):
         try:
             with open(p) as f:
                 d = json.load(f)
-            if d.get("kernel_kind") == li["kind"] and d.get("level") == li["level"]:
+            if (d.get("kernel_kind") == li["kind"] and d.get("level") == li["level"]
+                    and d.get("algorithmic_flops") == li["flops"]
+                    and d.get("executed_flops", li["flops"]) == li["flops_exec"]):
                 return d.get("dram_bytes_per_launch")
         except (OSError, ValueError):
             continue

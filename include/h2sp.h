@@ -108,6 +108,7 @@ typedef struct {
   double bytes;                /* algorithmic HBM bytes of one build           */
   double flops_congruence;     /* of which: congruence H = Q^T G Q             */
   double flops_strips;         /* of which: strip rotations                    */
+  double flops_executed;       /* FP64 flops actually issued (<= flops)        */
 } h2sp_sizes;
 
 /* Numeric inputs (DEVICE pointers, read-only, row-major FP64):
@@ -144,8 +145,16 @@ typedef struct {
 
 /* Symbolic phase (host, O(#blocks)): validates the structure and derives all
  * sizes, S offsets, the S block pattern, CSR row pointers and the per-level
- * work lists.  flags: reserved, pass 0. */
+ * work lists.  flags: 0 or H2SP_PLAN_EXPLICIT_Q. */
 h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out);
+
+/* Plan flags.  By default the level-0 congruence H = Q_t^T G Q_s (n_t = B <= 64,
+ * k <= 24) applies each Q in its compact-WY form Q = I - V M, M = T V^T (the
+ * Householder vectors of step (i)), costing 4 n_t n_s (k_t + k_s)
+ * flops instead of 2 n_t n_s (n_t + n_s); equal to the explicit product up to
+ * rounding (and exactly equal when every Q is a permutation).
+ * H2SP_PLAN_EXPLICIT_Q forces the explicit-Q product at every level. */
+#define H2SP_PLAN_EXPLICIT_Q 1
 /* Sharded plan: rank `rank` of `world` (a power of two <= 2^L)
  * owns the top-level subtree of cluster `rank` at the partition level
  * Lp = L - log2(world): S rows of its clusters, the congruences whose row cluster
@@ -176,13 +185,16 @@ void h2sp_plan_destroy(h2sp_plan plan);
  * (kind: 0 QR row side, 1 QR column side, 2 couplings, 3 merge+congruence+
  * freeze, 4 row strips, 5 column strips, 6 CSR index expansion).  flops and
  * bytes are the algorithmic FP64 flops and HBM bytes of that launch
- * (SURVEY §8(d) per-unit figures x units in the launch); items = work units. */
+ * (SURVEY §8(d) per-unit figures x units in the launch); items = work units;
+ * flops_exec = the FP64 flops the kernel actually issues (differs from flops
+ * only for the compact-WY level-0 congruence, see H2SP_PLAN_EXPLICIT_Q). */
 typedef struct {
   int32_t kind;
   int32_t level;
   int64_t items;
   double flops;
   double bytes;
+  double flops_exec;
 } h2sp_launch_info;
 /* Writes min(max, count) records to out (may be NULL) and the count to *count. */
 h2sp_status h2sp_plan_launches(h2sp_plan plan, h2sp_launch_info *out, int64_t max, int64_t *count);

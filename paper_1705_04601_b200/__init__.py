@@ -42,13 +42,14 @@ class _Sizes(ctypes.Structure):
                                     "coupling", "q_row", "q_col", "s_nnz", "s_rows", "rank", "world", "first_leaf",
                                     "n_leaves_local", "s_blocks", "workspace_bytes", "meta_bytes",
                                     "levels_active", "launches")] + \
-               [(n, _f64) for n in ("flops", "bytes", "flops_congruence", "flops_strips")]
+               [(n, _f64) for n in ("flops", "bytes", "flops_congruence", "flops_strips", "flops_executed")]
 
 
 class _LaunchInfo(ctypes.Structure):
-    _fields_ = [("kind", _i32), ("level", _i32), ("items", _i64), ("flops", _f64), ("bytes", _f64)]
+    _fields_ = [("kind", _i32), ("level", _i32), ("items", _i64), ("flops", _f64), ("bytes", _f64), ("flops_exec", _f64)]
 
 
+PLAN_EXPLICIT_Q = 1   # include/h2sp.h H2SP_PLAN_EXPLICIT_Q
 LAUNCH_KINDS = ("qr_row", "qr_col", "coupling", "congruence", "strips_row", "strips_col", "csr")
 
 
@@ -121,9 +122,10 @@ def _ptr(a: np.ndarray, ct):
 class Plan:
     """Symbolic phase (host): ``h2sp_plan_create`` on the structure arrays of a
     packed H^2 input (``h2gen.pack``-style dict: L, B, symmetric, rank_row,
-    rank_col, near_ptr, near_col, adm_ptr[k], adm_col[k])."""
+    rank_col, near_ptr, near_col, adm_ptr[k], adm_col[k]).  ``explicit_q``
+    sets H2SP_PLAN_EXPLICIT_Q (no compact-WY level-0 congruence)."""
 
-    def __init__(self, packed: dict, rank: int = 0, world: int = 1):
+    def __init__(self, packed: dict, rank: int = 0, world: int = 1, explicit_q: bool = False):
         self._keep = []
         L = int(packed["L"])
         rr = np.ascontiguousarray(packed["rank_row"], dtype=np.int32)
@@ -140,7 +142,8 @@ class Plan:
                         rank_row=_ptr(rr, _i32), rank_col=_ptr(rc, _i32) if rc is not None else None,
                         near_ptr=_ptr(npt, _i64), near_col=_ptr(ncl, _i32), adm_ptr=ap_arr, adm_col=ac_arr)
         h = _vp()
-        _check(lib.h2sp_plan_create_shard(ctypes.byref(st), int(rank), int(world), 0, ctypes.byref(h)),
+        _check(lib.h2sp_plan_create_shard(ctypes.byref(st), int(rank), int(world), PLAN_EXPLICIT_Q if explicit_q else 0,
+                                          ctypes.byref(h)),
                "h2sp_plan_create_shard")
         self.handle = h
         self._keep = None
@@ -196,12 +199,13 @@ class Plan:
         return off["n_row"] - m
 
     def launches(self):
-        """Per-launch descriptors of one build (kind, level, items, flops, bytes)."""
+        """Per-launch descriptors of one build (kind, level, items, flops, bytes, flops_exec)."""
         n = _i64()
         _check(lib.h2sp_plan_launches(self.handle, None, 0, ctypes.byref(n)), "h2sp_plan_launches")
         arr = (_LaunchInfo * max(n.value, 1))()
         _check(lib.h2sp_plan_launches(self.handle, arr, n.value, ctypes.byref(n)), "h2sp_plan_launches")
-        return [dict(kind=LAUNCH_KINDS[a.kind], level=a.level, items=a.items, flops=a.flops, bytes=a.bytes)
+        return [dict(kind=LAUNCH_KINDS[a.kind], level=a.level, items=a.items, flops=a.flops, bytes=a.bytes,
+                     flops_exec=a.flops_exec)
                 for a in arr[:n.value]]
 
     def pattern(self, with_cols: bool = True):

@@ -137,7 +137,7 @@ struct h2sp_plan_s {
   int64_t zb_row_len, zb_col_len;          // per rhs
   int64_t s_nnz, s_blocks;
   int levels_active;
-  double flops, bytes, flops_cong, flops_strip;
+  double flops, bytes, flops_cong, flops_strip, flops_exec;
   std::vector<h2sp::LevelPlan> levels;
   h2sp::ClusterArrays ca;
   size_t csr_rows_off, csr_blocks_off, rowptr_off, csr_pat_off;
@@ -146,6 +146,10 @@ struct h2sp_plan_s {
   size_t meta_bytes;
   // workspace layout after the meta region (byte offsets)
   size_t ws_rh_row, ws_rh_col, ws_dt, ws_bb, ws_yr, ws_yc, ws_total;
+  // compact-WY form of the level-0 Q (0 = explicit Q everywhere): per leaf,
+  // V (64 x wy_kp, row-major) then M = T V^T (wy_kp x 64), zero padded
+  int32_t wy_kp;
+  size_t ws_wy_row, ws_wy_col;
   int64_t launches;
   std::vector<h2sp_launch_info> launch_info;
   uint64_t magic;                           // first 8 bytes of the meta image (checked on device)

@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(128) qr_reg_kernel(Side sd, int L, int level, 
                                                      const double *__restrict__ leaf,
                                                      const double *__restrict__ transfer, double *__restrict__ rh,
                                                      double *__restrict__ qout, const uint64_t *meta_magic,
-                                                     uint64_t magic) {
+                                                     uint64_t magic, double *__restrict__ wy, int wy_kp) {
   if (meta_magic && threadIdx.x == 0 && blockIdx.x == 0 && *meta_magic != magic) __trap();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ci = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -433,8 +433,12 @@ __global__ void __launch_bounds__(128) qr_reg_kernel(Side sd, int L, int level, 
   const int n = sd.n[cl], k = sd.k[cl];
   if (n == 0 || !sd.need[cl]) return;
   double *Qg = qout + sd.q_off[cl];
+  // compact-WY copy (level 0 only): V (64 x wy_kp) then M = T V^T (wy_kp x 64), zero padded
+  double *Wg = wy ? wy + int64_t(ci) * 128 * wy_kp : nullptr;
   if (k == 0) {
     for (int idx = lane; idx < n * n; idx += 32) Qg[idx] = (idx / n == idx % n) ? 1.0 : 0.0;
+    if (Wg)
+      for (int idx = lane; idx < 128 * wy_kp; idx += 32) Wg[idx] = 0.0;
     return;
   }
   double x[NR][KP];
@@ -599,6 +603,26 @@ __global__ void __launch_bounds__(128) qr_reg_kernel(Side sd, int L, int level, 
       }
     }
   __syncwarp();
+  if (Wg) {
+    for (int idx = lane; idx < 64 * wy_kp; idx += 32) {
+      const int i = idx / wy_kp, c = idx - i * wy_kp;
+      Wg[idx] = (i < n && c < k) ? Vs[i * LDV + c] : 0.0;
+    }
+    for (int idx = lane; idx < 64 * wy_kp; idx += 32) {
+      const int a = idx >> 6, c = idx & 63;
+      Wg[64 * wy_kp + idx] = (a < k && c < n) ? Mm[a * LDM + c] : 0.0;
+    }
+  }
+  if (Wg) {
+    for (int idx = lane; idx < 64 * wy_kp; idx += 32) {
+      const int i = idx / wy_kp, c = idx - i * wy_kp;
+      Wg[idx] = (i < n && c < k) ? Vs[i * LDV + c] : 0.0;
+    }
+    for (int idx = lane; idx < 64 * wy_kp; idx += 32) {
+      const int a = idx >> 6, c = idx & 63;
+      Wg[64 * wy_kp + idx] = (a < k && c < n) ? Mm[a * LDM + c] : 0.0;
+    }
+  }
   // ---- Q = I - V M, straight to global
   for (int ti = 0; ti < N8 / 8; ti++)
     for (int tc = 0; tc < N8 / 8; tc++) {
@@ -739,25 +763,39 @@ __device__ __forceinline__ void pair_load_G(const PairArgs &A, const PairItem &i
     const int64_t sc1 = lvl_off_d(A.L, A.level - 1) + 2 * (s - lbase);
     const int kr0 = A.rs.k[tc1], kr1 = A.rs.k[tc1 + 1];
     const int kc0 = A.cs.k[sc1], kc1 = A.cs.k[sc1 + 1];
-    for (int idx = threadIdx.x; idx < NP * NP; idx += blockDim.x) {
-      const int i = idx / NP, j = idx % NP;
-      const double *src = nullptr;
-      if (i < nt && j < ns) {
-        const int a = i >= kr0, b = j >= kc0;
-        const int ii = a ? i - kr0 : i, jj = b ? j - kc0 : j;
-        const int ka = a ? kr1 : kr0, kb = b ? kc1 : kc0;
-        const int q = a * 2 + b;
-        const int kind = (it.gkind >> (4 * q)) & 15;
-        const int64_t off = it.g_src[q];
-        switch (kind) {
-          case G_BB: src = A.bb_in + off + ii * kb + jj; break;
-          case G_BB_T: src = A.bb_in + off + jj * ka + ii; break;
-          case G_DT: src = A.dt_in + off + ii * kb + jj; break;
-          case G_DT_T: src = A.dt_in + off + jj * ka + ii; break;
-          default: break;
-        }
+    // blockDim.x is a multiple of NP: each thread keeps one column j and walks
+    // rows i = tid/NP, +R, ...; the two quadrant sources of that column (a = 0, 1)
+    // are resolved once into a base pointer and a row stride.
+    const int j = threadIdx.x % NP;
+    const int R = blockDim.x / NP;
+    const int b = j >= kc0;
+    const int jj = b ? j - kc0 : j, kb = b ? kc1 : kc0;
+    const bool jok = j < ns;
+    const double *base[2];
+    int64_t st[2];
+#pragma unroll
+    for (int a = 0; a < 2; a++) {
+      const int ka = a ? kr1 : kr0;
+      const int q = a * 2 + b;
+      const int kind = (it.gkind >> (4 * q)) & 15;
+      const int64_t off = it.g_src[q];
+      base[a] = nullptr;
+      st[a] = 0;
+      switch (kind) {
+        case G_BB: base[a] = A.bb_in + off + jj; st[a] = kb; break;
+        case G_BB_T: base[a] = A.bb_in + off + int64_t(jj) * ka; st[a] = 1; break;
+        case G_DT: base[a] = A.dt_in + off + jj; st[a] = kb; break;
+        case G_DT_T: base[a] = A.dt_in + off + int64_t(jj) * ka; st[a] = 1; break;
+        default: break;
       }
-      cp8(&sG[i * LD + j], src ? (const void *)src : any, src != nullptr);
+    }
+    for (int i = threadIdx.x / NP; i < NP; i += R) {
+      const int a = i >= kr0;
+      const int ii = a ? i - kr0 : i;
+      const double *bp = a ? base[1] : base[0];
+      const bool ok = jok && i < nt && bp != nullptr;
+      const double *src = ok ? bp + ii * (a ? st[1] : st[0]) : reinterpret_cast<const double *>(any);
+      cp8(&sG[i * LD + j], src, ok);
     }
   }
 }
@@ -968,6 +1006,175 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS)
       const PairItem nx = A.items[p + 1];
       const int nsx = A.cs.n[nx.s];
       async_tile<NP, NP, LD>(sQs, A.q_col + A.cs.q_off[nx.s], nsx, nsx, nsx, A.items);
+      cp_commit();
+    }
+    prev.s_dst = it.s_dst;
+    prev.s_dst_m = it.s_dst_m;
+    prev.bb_dst = it.bb_dst;
+    prev.yr_dst = it.yr_dst;
+    prev.yc_dst = it.yc_dst;
+    prev.s_ld = it.s_ld;
+    prev.s_ld_m = it.s_ld_m;
+    prev.yr_ld = it.yr_ld;
+    prev.yc_ld = it.yc_ld;
+    prev.nt = nt;
+    prev.ns = A.cs.n[s];
+    prev.kt = ktt;
+    prev.ks = A.cs.k[s];
+    prev.dsym = A.sym && s == t;
+    have_prev = true;
+  }
+}
+
+// --------------------------------------------------------------------------
+// Level-0 congruence with Q in compact-WY form (H2SP_PLAN_EXPLICIT_Q unset):
+// Q = I - V M, M = T V^T (V: the n x k Householder vectors of step (i)), so
+//   H = Q_t^T G Q_s = T1 - (T1 V_s) M_s,   T1 = G - M_t^T (V_t^T G),
+// four skinny products costing 4 n_t n_s (k_t + k_s) flops instead of the
+// 2 n_t n_s (n_t + n_s) of the explicit product (1.78x fewer at n = 64, k = 16).
+// Same result up to rounding; when every reflector has tau = 0 (M = 0) it is
+// G itself, bit for bit.  Block layout as pair_kernel<64>: 8 warps, warp w owns
+// rows 8w..8w+7 of T1 and H (registers), V_t / M_t resident per block row,
+// G and V_s / M_s reloaded per pair, the previous H scattered during step 1.
+// --------------------------------------------------------------------------
+template <int KP>
+struct PairWyCfg {
+  static constexpr int NP = 64;
+  static constexpr int LD = NP + 4;       // G, P, M (rows of 64)
+  static constexpr int LDV = KP + 4;      // V (rows of KP): LDV = 4 (mod 8) -> conflict-free fragments
+  static constexpr int WARPS = 8;
+  static constexpr int THREADS = WARPS * 32;
+  static constexpr int V_D = NP * LDV, M_D = KP * LD, G_D = NP * LD, P_D = KP * LD;
+  static constexpr size_t SMEM = size_t(2 * V_D + 2 * M_D + G_D + P_D) * sizeof(double);
+};
+
+template <int KP>
+__device__ __forceinline__ void wy_load(double *sV, double *sM, const double *wy, int64_t c) {
+  using C = PairWyCfg<KP>;
+  const double *g = wy + c * (2 * 64 * KP);
+  async_tile<64, KP, C::LDV>(sV, g, 64, KP, KP, g);
+  async_tile<KP, 64, C::LD>(sM, g + 64 * KP, KP, 64, 64, g);
+}
+
+template <int KP>
+__global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(PairArgs A, const double *wy_row,
+                                                                              const double *wy_col) {
+  using C = PairWyCfg<KP>;
+  constexpr int LD = C::LD, LDV = C::LDV, TN = 8;
+  extern __shared__ __align__(16) double sm[];
+  double *sVt = sm, *sVs = sVt + C::V_D;
+  double *sMt = sVs + C::V_D, *sMs = sMt + C::M_D;
+  double *sG = sMs + C::M_D, *sP = sG + C::G_D;
+  const Chunk ch = A.chunks[blockIdx.x];
+  int t = A.items[ch.begin].t;
+  int nt = A.rs.n[t], ktt = A.rs.k[t];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = lane >> 2, q = lane & 3;
+  const int m0 = warp * 8;
+  wy_load<KP>(sVt, sMt, wy_row, t);
+  {
+    const PairItem it0 = A.items[ch.begin];
+    async_tile<64, 64, LD>(sG, A.close + it0.g_src[0], nt, A.cs.n[it0.s], A.B, A.items);
+    wy_load<KP>(sVs, sMs, wy_col, it0.s);
+  }
+  cp_commit();
+  double H[TN][2];
+  PairDst prev;
+  bool have_prev = false;
+  const int src_lo = r * 4 + (q >> 1), src_hi = src_lo + 2;
+  for (int p = ch.begin;; p++) {
+    if (p == ch.end) {
+      if (have_prev && !(A.debug & 1)) {
+#pragma unroll
+        for (int j = 0; j < TN; j++) scatter_pair2(A, prev, m0, j * 8, m0 + r, j * 8 + 2 * q, H[j][0], H[j][1]);
+      }
+      break;
+    }
+    const PairItem it = A.items[p];
+    const int s = it.s;
+    cp_wait_all();
+    __syncthreads();
+    if (it.t != t) {
+      t = it.t;
+      nt = A.rs.n[t];
+      ktt = A.rs.k[t];
+      wy_load<KP>(sVt, sMt, wy_row, t);
+      cp_commit();
+      cp_wait_all();
+      __syncthreads();
+    }
+    const bool scat = have_prev && !(A.debug & 1);
+    // ---- step 1: P = V_t^T G (KP x 64); warp w computes columns 8w..8w+7,
+    //      interleaved with the scatter of the previous H (one tile per k-step)
+    {
+      double pacc[KP / 8][2];
+#pragma unroll
+      for (int i = 0; i < KP / 8; i++) pacc[i][0] = pacc[i][1] = 0.0;
+#pragma unroll
+      for (int k0 = 0; k0 < 64; k0 += 4) {
+        const double b = sG[(k0 + q) * LD + m0 + r];
+#pragma unroll
+        for (int i = 0; i < KP / 8; i++) dmma(pacc[i], sVt[(k0 + q) * LDV + i * 8 + r], b);
+        if (k0 / 4 < TN && scat) {
+          const int j = k0 / 4;
+          scatter_pair2(A, prev, m0, j * 8, m0 + r, j * 8 + 2 * q, H[j][0], H[j][1]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < KP / 8; i++) {
+        sP[(i * 8 + r) * LD + m0 + 2 * q] = pacc[i][0];
+        sP[(i * 8 + r) * LD + m0 + 2 * q + 1] = pacc[i][1];
+      }
+    }
+    __syncthreads();
+    // ---- step 2: T1 = G - M_t^T P (rows m0..m0+7 of T1 in H's registers)
+#pragma unroll
+    for (int j = 0; j < TN; j++) {
+      H[j][0] = sG[(m0 + r) * LD + j * 8 + 2 * q];
+      H[j][1] = sG[(m0 + r) * LD + j * 8 + 2 * q + 1];
+    }
+#pragma unroll
+    for (int k0 = 0; k0 < KP; k0 += 4) {
+      const double a = -sMt[(k0 + q) * LD + m0 + r];
+#pragma unroll
+      for (int j = 0; j < TN; j++) dmma(H[j], a, sP[(k0 + q) * LD + j * 8 + r]);
+    }
+    __syncthreads();  // every warp is done with G and P
+    const bool more = p + 1 < ch.end && !(A.debug & 2);
+    if (more) {
+      const PairItem nx = A.items[p + 1];
+      async_tile<64, 64, LD>(sG, A.close + nx.g_src[0], A.rs.n[nx.t], A.cs.n[nx.s], A.B, A.items);
+      cp_commit();
+    }
+    // ---- step 3: R = T1 V_s (8 x KP per warp), A fragments from the T1 accumulators
+    double R[KP / 8][2];
+#pragma unroll
+    for (int i = 0; i < KP / 8; i++) R[i][0] = R[i][1] = 0.0;
+#pragma unroll
+    for (int k0 = 0; k0 < 64; k0 += 4) {
+      const int jt = k0 >> 3;
+      const int srcl = (k0 & 4) ? src_hi : src_lo;
+      const double e0 = __shfl_sync(0xffffffffu, H[jt][0], srcl);
+      const double e1 = __shfl_sync(0xffffffffu, H[jt][1], srcl);
+      const double a = (q & 1) ? e1 : e0;
+#pragma unroll
+      for (int i = 0; i < KP / 8; i++) dmma(R[i], a, sVs[(k0 + q) * LDV + i * 8 + r]);
+    }
+    // ---- step 4: H = T1 - R M_s
+#pragma unroll
+    for (int k0 = 0; k0 < KP; k0 += 4) {
+      const int jt = k0 >> 3;
+      const int srcl = (k0 & 4) ? src_hi : src_lo;
+      const double e0 = __shfl_sync(0xffffffffu, R[jt][0], srcl);
+      const double e1 = __shfl_sync(0xffffffffu, R[jt][1], srcl);
+      const double a = -((q & 1) ? e1 : e0);
+#pragma unroll
+      for (int j = 0; j < TN; j++) dmma(H[j], a, sMs[(k0 + q) * LD + j * 8 + r]);
+    }
+    __syncthreads();  // every warp is done with V_s / M_s
+    if (more) {
+      const PairItem nx = A.items[p + 1];
+      wy_load<KP>(sVs, sMs, wy_col, nx.s);
       cp_commit();
     }
     prev.s_dst = it.s_dst;
@@ -1286,6 +1493,20 @@ static h2sp_status launch_pairs(const PairArgs &a, int64_t nchunks, cudaStream_t
   return H2SP_OK;
 }
 
+template <int KP>
+static h2sp_status launch_pairs_wy(const PairArgs &a, const double *wy_row, const double *wy_col, int64_t nchunks,
+                                   cudaStream_t st) {
+  using C = PairWyCfg<KP>;
+  static bool attr = false;
+  if (!attr) {
+    H2SP_CK(cudaFuncSetAttribute(pair_wy_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
+    attr = true;
+  }
+  pair_wy_kernel<KP><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a, wy_row, wy_col);
+  H2SP_CK(cudaGetLastError());
+  return H2SP_OK;
+}
+
 constexpr int STRIP_TN = 128;  // = plan.cpp STRIP_TN
 
 template <int NP>
@@ -1368,6 +1589,8 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   const double *leaf_col = sym ? in->leaf_basis_row : in->leaf_basis_col;
   const double *tr_col = sym ? in->transfer_row : in->transfer_col;
   double *q_col = sym ? out->q_row : out->q_col;
+  double *wy_row = P->wy_kp ? (double *)(ws + P->ws_wy_row) : nullptr;
+  double *wy_col = P->wy_kp ? (double *)(ws + P->ws_wy_col) : nullptr;
   const int L = P->L;
   DeviceAux *aux = nullptr;
   if (h2sp_status e = get_aux(L, &aux)) return e;
@@ -1434,7 +1657,8 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     const LevelPlan &lp = P->levels[k];
     const int M = int(int64_t(1) << (L - k));
     auto launch = [&](const Side &sd, const std::vector<int32_t> &nn, const std::vector<int32_t> &kk, const double *leaf,
-                      const double *tr, double *rh, double *qo, const uint64_t *magic_ptr) -> h2sp_status {
+                      const double *tr, double *rh, double *qo, const uint64_t *magic_ptr,
+                      double *wyo) -> h2sp_status {
       int per_warp = 2, nmax = 0, kmax = 0, per_warp_reg = 2;
       for (int i = 0; i < M; i++) {
         const int64_t c = lvl_off_d(L, k) + i;
@@ -1464,7 +1688,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       attr_ = true;                                                                                        \
     }                                                                                                      \
     qr_reg_kernel<NR_, KP_><<<grid, 32 * wpb, smem, s>>>(sd, L, k, M, per_warp_reg, leaf, tr, rh, qo,        \
-                                                        magic_ptr, P->magic);                              \
+                                                        magic_ptr, P->magic, wyo, P->wy_kp);               \
   } while (0)
         if (nmax <= 32) {
           switch (kp) {
@@ -1494,13 +1718,15 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     if (lp.np_row > 0) {
       if (h2sp_status e = pre(s, li[k].qr_row)) return e;
       if (h2sp_status e = launch(rs, P->n_row, P->k_row, in->leaf_basis_row, in->transfer_row, rh_row, out->q_row,
-                                 k == 0 ? (const uint64_t *)meta : nullptr))
+                                 k == 0 ? (const uint64_t *)meta : nullptr, k == 0 ? wy_row : nullptr))
         return e;
       if (h2sp_status e = post(s, li[k].qr_row)) return e;
     }
     if (!sym && lp.np_col > 0) {
       if (h2sp_status e = pre(s, li[k].qr_col)) return e;
-      if (h2sp_status e = launch(cs, P->n_col, P->k_col, leaf_col, tr_col, rh_col, q_col, nullptr)) return e;
+      if (h2sp_status e = launch(cs, P->n_col, P->k_col, leaf_col, tr_col, rh_col, q_col, nullptr,
+                                 k == 0 ? wy_col : nullptr))
+        return e;
       if (h2sp_status e = post(s, li[k].qr_col)) return e;
     }
     return H2SP_OK;
@@ -1617,7 +1843,10 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       a.debug = pair_debug;
       if (h2sp_status e = pre(st, li[k].pairs)) return e;
       h2sp_status s;
-      switch (pad16(lp.np_pair)) {
+      if (k == 0 && P->wy_kp) {
+        s = P->wy_kp == 16 ? launch_pairs_wy<16>(a, wy_row, wy_col, lp.n_pair_chunks, st)
+                           : launch_pairs_wy<24>(a, wy_row, wy_col, lp.n_pair_chunks, st);
+      } else switch (pad16(lp.np_pair)) {
         case 16: s = launch_pairs<16>(a, lp.n_pair_chunks, st); break;
         case 32: s = launch_pairs<32>(a, lp.n_pair_chunks, st); break;
         case 48: s = launch_pairs<48>(a, lp.n_pair_chunks, st); break;

@@ -114,7 +114,7 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
 }
 
 h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world, int flags, h2sp_plan *out) {
-  (void)flags;
+  if (flags & ~H2SP_PLAN_EXPLICIT_Q) return fail(H2SP_EINVAL, "unknown plan flags");
   if (!st || !out) return fail(H2SP_EINVAL, "NULL structure or output pointer");
   *out = nullptr;
   h2sp_plan_s *P = nullptr;
@@ -741,6 +741,15 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
       if (npr > 0 || npc > 0) levels_active++;
       lp.mp = STRIP_TN;
       lp.np_pair = round8(std::max(npr, npc));
+      if (k == 0) {
+        // compact-WY congruence at level 0 (kernels.cu pair_wy_kernel): n <= 64
+        // tiles padded to 64, every k <= 24; pays off for k <= n / 2
+        int kmx = 0;
+        for (int64_t i = 0; i < M; i++) kmx = std::max(kmx, int(std::max(kr[base + i], kc[base + i])));
+        P->wy_kp = 0;
+        if (!(flags & H2SP_PLAN_EXPLICIT_Q) && lp.np_pair > 48 && lp.np_pair <= 64 && kmx >= 1 && kmx <= 24)
+          P->wy_kp = kmx <= 16 ? 16 : 24;
+      }
       lp.np_rstrip = round8(npr);
       lp.np_cstrip = round8(npc);
       lp.n_pairs = int64_t(pairs[k].size());
@@ -810,6 +819,7 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
         for (const auto &it : pairs[k]) {
           const double a = nr[it.t], b = nc[it.s];
           li.flops += 2 * a * b * (a + b);
+          li.flops_exec += (k == 0 && P->wy_kp) ? 4 * a * b * (kr[it.t] + kc[it.s]) : 2 * a * b * (a + b);
           double outb = a * b;  // nn + bb + bn + nb
           if (it.s_dst_m >= 0) outb += double(nr[it.t] - kr[it.t]) * (nc[it.s] - kc[it.s]);
           li.bytes += 8.0 * (a * b + outb);
@@ -869,6 +879,11 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
     }
     P->launches = launches;
     P->levels_active = levels_active;
+    P->flops_exec = 0;
+    for (auto &x : P->launch_info) {
+      if (x.kind != 3) x.flops_exec = x.flops;
+      P->flops_exec += x.flops_exec;
+    }
     P->meta_bytes = align_up(mb.buf.size(), 256);
     mb.buf.resize(P->meta_bytes, 0);
     P->meta.swap(mb.buf);
@@ -889,6 +904,12 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
     P->ws_bb = carve(bb_len);
     P->ws_yr = carve(yr_len);
     P->ws_yc = carve(yc_len);
+    P->ws_wy_row = P->ws_wy_col = 0;
+    if (P->wy_kp) {
+      const int64_t per = int64_t(2) * 64 * P->wy_kp;
+      P->ws_wy_row = carve(per * nleaf);
+      P->ws_wy_col = sym ? P->ws_wy_row : carve(per * nleaf);
+    }
     P->ws_total = o;
     // algorithmic work
     double close_read = 0;
@@ -948,6 +969,7 @@ h2sp_status h2sp_plan_sizes(h2sp_plan P, h2sp_sizes *o) {
   o->bytes = P->bytes;
   o->flops_congruence = P->flops_cong;
   o->flops_strips = P->flops_strip;
+  o->flops_executed = P->flops_exec;
   return H2SP_OK;
 }
 

@@ -18,10 +18,10 @@ def _need_gpu():
         pytest.skip("no CUDA device")
 
 
-def _run(h):
+def _run(h, explicit_q=False):
     import paper_1705_04601_b200 as h2sp
     packed = h2gen.pack(h)
-    plan = h2sp.Plan(packed)
+    plan = h2sp.Plan(packed, explicit_q=explicit_q)
     sp = h2sp.Sparsifier(plan, packed)
     out = sp.build()
     torch.cuda.synchronize()
@@ -320,3 +320,27 @@ def test_build_apply_matches_separate_calls(sym):
     torch.cuda.synchronize()
     assert torch.equal(s1, sp.outputs["s_val"])
     assert torch.equal(y1, y2) and torch.equal(x1, x2)
+
+
+@pytest.mark.parametrize("name", ["cfg2-16384", "cfg3-16384", "rand-gen-B64"])
+def test_explicit_q_and_wy_agree(name):
+    """Both level-0 congruence variants (compact-WY, default; explicit Q with
+    H2SP_PLAN_EXPLICIT_Q) match the oracle, and each other to rounding."""
+    _need_gpu()
+    if name == "cfg2-16384":
+        h = h2gen.make_config(2, N=16384)
+    elif name == "cfg3-16384":
+        h = h2gen.make_config(3, N=16384)
+    else:
+        h = h2gen.random_h2(4, 64, 31, False, eta=0.7, max_rank=16)
+    res = oracle.sparsify(h)
+    outs = []
+    for ex in (False, True):
+        plan, sp, out = _run(h, explicit_q=ex)
+        lv0 = [l for l in plan.launches() if l["kind"] == "congruence" and l["level"] == 0][0]
+        if ex:
+            assert lv0["flops_exec"] == lv0["flops"]
+        _compare(h, plan, out, res)
+        outs.append(out["s_val"].cpu().numpy())
+    a, b = outs
+    assert np.linalg.norm(a - b) <= 1e-13 * np.linalg.norm(b)

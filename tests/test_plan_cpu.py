@@ -150,3 +150,20 @@ def test_binding_fails_loudly_without_library(tmp_path):
     r = subprocess.run([sys.executable, "-c", "import paper_1705_04601_b200"], cwd=tmp_path, capture_output=True,
                        text=True)
     assert r.returncode != 0 and "libh2sp.so" in r.stderr
+
+
+def test_wy_congruence_flops():
+    """Compact-WY level-0 congruence: executed flops 4 n_t n_s (k_t + k_s) per
+    pair; the algorithmic count is unchanged; explicit_q disables it."""
+    import paper_1705_04601_b200 as h2sp
+    h = h2gen.make_config(2, N=4096, with_close=False)
+    packed = h2gen.pack(h)
+    for ex in (False, True):
+        plan = h2sp.Plan(packed, explicit_q=ex)
+        li = [l for l in plan.launches() if l["kind"] == "congruence" and l["level"] == 0][0]
+        n, k = 64.0, 16.0
+        assert li["flops"] == li["items"] * 2 * n * n * (2 * n)
+        want = li["items"] * 4 * n * n * (2 * k) if not ex else li["flops"]
+        assert li["flops_exec"] == want
+        assert plan.sizes["flops_executed"] == pytest.approx(sum(l["flops_exec"] for l in plan.launches()))
+        assert plan.sizes["flops"] == pytest.approx(sum(l["flops"] for l in plan.launches()))
