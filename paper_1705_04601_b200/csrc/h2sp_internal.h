@@ -15,6 +15,8 @@ namespace h2sp {
 // P:238-250): children pair (t_a, s_b) is near -> its H basis x basis part;
 // admissible -> its orthogonalised coupling D~.  "_T" = read the canonical
 // (t <= s) block transposed (symmetric mode).
+constexpr int STRIP_TN = 128;  // columns per strip tile (plan.cpp tiles, kernels.cu strip_kernel TN)
+
 enum GKind : int32_t { G_EMPTY = 0, G_BB = 1, G_BB_T = 2, G_DT = 3, G_DT_T = 4 };
 
 // One congruence H_ts = Q^R_t^T G_ts Q^C_s for (t, s) in N_k (canonical t <= s

@@ -1107,14 +1107,16 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
     // ---- step 1: P = V_t^T G (KP x 64); warp w computes columns 8w..8w+7,
     //      interleaved with the scatter of the previous H (one tile per k-step)
     {
-      double pacc[KP / 8][2];
+      // two partial sums per tile (even / odd k-steps): twice the independent
+      // DMMA chains of this skinny product
+      double pacc[2][KP / 8][2];
 #pragma unroll
-      for (int i = 0; i < KP / 8; i++) pacc[i][0] = pacc[i][1] = 0.0;
+      for (int i = 0; i < KP / 8; i++) pacc[0][i][0] = pacc[0][i][1] = pacc[1][i][0] = pacc[1][i][1] = 0.0;
 #pragma unroll
       for (int k0 = 0; k0 < 64; k0 += 4) {
         const double b = sG[(k0 + q) * LD + m0 + r];
 #pragma unroll
-        for (int i = 0; i < KP / 8; i++) dmma(pacc[i], sVt[(k0 + q) * LDV + i * 8 + r], b);
+        for (int i = 0; i < KP / 8; i++) dmma(pacc[(k0 >> 2) & 1][i], sVt[(k0 + q) * LDV + i * 8 + r], b);
         if (k0 / 4 < TN && scat) {
           const int j = k0 / 4;
           scatter_pair2(A, prev, m0, j * 8, m0 + r, j * 8 + 2 * q, H[j][0], H[j][1]);
@@ -1122,8 +1124,8 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
       }
 #pragma unroll
       for (int i = 0; i < KP / 8; i++) {
-        sP[(i * 8 + r) * LD + m0 + 2 * q] = pacc[i][0];
-        sP[(i * 8 + r) * LD + m0 + 2 * q + 1] = pacc[i][1];
+        sP[(i * 8 + r) * LD + m0 + 2 * q] = pacc[0][i][0] + pacc[1][i][0];
+        sP[(i * 8 + r) * LD + m0 + 2 * q + 1] = pacc[0][i][1] + pacc[1][i][1];
       }
     }
     __syncthreads();
@@ -1147,9 +1149,9 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
       cp_commit();
     }
     // ---- step 3: R = T1 V_s (8 x KP per warp), A fragments from the T1 accumulators
-    double R[KP / 8][2];
+    double R[KP / 8][2], R2[KP / 8][2];
 #pragma unroll
-    for (int i = 0; i < KP / 8; i++) R[i][0] = R[i][1] = 0.0;
+    for (int i = 0; i < KP / 8; i++) R[i][0] = R[i][1] = R2[i][0] = R2[i][1] = 0.0;
 #pragma unroll
     for (int k0 = 0; k0 < 64; k0 += 4) {
       const int jt = k0 >> 3;
@@ -1158,7 +1160,12 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
       const double e1 = __shfl_sync(0xffffffffu, H[jt][1], srcl);
       const double a = (q & 1) ? e1 : e0;
 #pragma unroll
-      for (int i = 0; i < KP / 8; i++) dmma(R[i], a, sVs[(k0 + q) * LDV + i * 8 + r]);
+      for (int i = 0; i < KP / 8; i++) dmma((k0 & 4) ? R2[i] : R[i], a, sVs[(k0 + q) * LDV + i * 8 + r]);
+    }
+#pragma unroll
+    for (int i = 0; i < KP / 8; i++) {
+      R[i][0] += R2[i][0];
+      R[i][1] += R2[i][1];
     }
     // ---- step 4: H = T1 - R M_s
 #pragma unroll
@@ -1276,48 +1283,63 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS) strip_kernel(StripA
     tdst[cc] = td;
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < NP * TN; idx += blockDim.x) {
-    const int i = idx / TN, cc = idx % TN;
-    const double *src = nullptr;
-    if (i < k1) {
-      if (src1[cc] >= 0) src = A.y_in + pn.src_c1 + int64_t(i) * pn.ld_c1 + src1[cc];
-    } else if (i < k1 + k2) {
-      if (src2[cc] >= 0) src = A.y_in + pn.src_c2 + int64_t(i - k1) * pn.ld_c2 + src2[cc];
+  // gather Z: each thread keeps one column cc (blockDim.x is a multiple of TN)
+  // and walks its rows; rows of an absent child and rows [n, n4) are zero-filled
+  const int n4 = rup(n, 4);
+  {
+    const int cc = threadIdx.x % TN, R = blockDim.x / TN;
+    const double *b1 = src1[cc] >= 0 ? A.y_in + pn.src_c1 + src1[cc] : nullptr;
+    const double *b2 = src2[cc] >= 0 ? A.y_in + pn.src_c2 + src2[cc] : nullptr;
+    for (int i = threadIdx.x / TN; i < n4; i += R) {
+      const bool first = i < k1;
+      const double *bp = first ? b1 : (i < k1 + k2 ? b2 : nullptr);
+      const double *src = bp ? bp + int64_t(first ? i : i - k1) * (first ? pn.ld_c1 : pn.ld_c2)
+                             : reinterpret_cast<const double *>(A.tiles);
+      cp8(&sZ[i * C::LDZ + cc], src, bp != nullptr);
     }
-    cp8(&sZ[i * C::LDZ + cc], src ? (const void *)src : (const void *)A.tiles, src != nullptr);
   }
   cp_commit();
   cp_wait_all();
   __syncthreads();
   const int warp = threadIdx.x >> 5;
   const int m0 = (warp / C::NWN) * 16, n0 = (warp % C::NWN) * C::WN;
+  if (m0 >= n) return;  // no rows of W for this warp (nothing after this needs the CTA barrier)
   double acc[2][C::WN / 8][2];
   zero_acc(acc);
-  warp_gemm<C::LDQ, C::LDZ, 2, C::WN / 8, true>(sQ, sZ, m0, n0, NP, acc);
-  __syncthreads();
-  warp_store<C::LDZ>(sZ, m0, n0, acc);
-  __syncthreads();
-  const int mq = n - kq;
+  warp_gemm<C::LDQ, C::LDZ, 2, C::WN / 8, true>(sQ, sZ, m0, n0, n4, acc);
+  // epilogue straight from the accumulators: lane (r, q) holds W[row][col], W[row][col + 1]
+  // rows [0, k_q) -> q's panel; rows [k_q, n_q) -> S row segment and the transposed block
   const int lane = threadIdx.x & 31;
-  if (pn.s_dst >= 0) {
-    for (int a = warp; a < mq; a += C::WARPS) {
-      double *d = A.s_val + pn.s_dst + int64_t(a) * pn.s_ld + tile.c0;
-      for (int cc = lane; cc < ncol; cc += 32) d[cc] = sZ[(kq + a) * C::LDZ + cc];
-    }
-  }
-  if (pn.y_dst >= 0) {
-    for (int i = warp; i < kq; i += C::WARPS) {
-      double *d = A.y_out + pn.y_dst + int64_t(i) * pn.y_ld + tile.c0;
-      for (int cc = lane; cc < ncol; cc += 32) d[cc] = sZ[i * C::LDZ + cc];
-    }
-  }
-  if (mq > 0) {
-    // transposed blocks: element (column cc, frozen row a) -> S[tdst[cc] + a]; consecutive
-    // threads take consecutive a (coalesced runs of m_q), then the next column
-    for (int idx = threadIdx.x; idx < mq * ncol; idx += blockDim.x) {
-      const int cc = idx / mq, a = idx - cc * mq;
-      const int64_t d = tdst[cc];
-      if (d >= 0) A.s_val[d + a] = sZ[(kq + a) * C::LDZ + cc];
+  const int r = lane >> 2, q4 = lane & 3;
+#pragma unroll
+  for (int i = 0; i < 2; i++) {
+    const int row = m0 + i * 8 + r;
+    if (row >= n) continue;
+#pragma unroll
+    for (int j = 0; j < C::WN / 8; j++) {
+      const int col = n0 + j * 8 + 2 * q4;
+      if (col >= ncol) continue;
+      const bool two = col + 1 < ncol;
+      const double v0 = acc[i][j][0], v1 = acc[i][j][1];
+      double *d = nullptr;
+      if (row < kq) {
+        if (pn.y_dst >= 0) d = A.y_out + pn.y_dst + int64_t(row) * pn.y_ld + tile.c0 + col;
+      } else {
+        const int a = row - kq;
+        if (pn.s_dst >= 0) d = A.s_val + pn.s_dst + int64_t(a) * pn.s_ld + tile.c0 + col;
+        const int64_t t0 = tdst[col];
+        if (t0 >= 0) A.s_val[t0 + a] = v0;
+        if (two) {
+          const int64_t t1 = tdst[col + 1];
+          if (t1 >= 0) A.s_val[t1 + a] = v1;
+        }
+      }
+      if (d) {
+        if (two)
+          store2(d, v0, v1);
+        else
+          d[0] = v0;
+      }
     }
   }
 }
@@ -1507,7 +1529,6 @@ static h2sp_status launch_pairs_wy(const PairArgs &a, const double *wy_row, cons
   return H2SP_OK;
 }
 
-constexpr int STRIP_TN = 128;  // = plan.cpp STRIP_TN
 
 template <int NP>
 static h2sp_status launch_strips1(const StripArgs &a, int64_t ntiles, cudaStream_t st) {

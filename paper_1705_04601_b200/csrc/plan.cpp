@@ -62,7 +62,6 @@ struct Grp {  // a frozen column group (l, s) of a strip panel, at columns [col0
   int32_t l, s, m, col0;
 };
 
-constexpr int STRIP_TN = 128;  // columns per strip tile (kernels.cu: strip_kernel TN)
 
 struct BlockRec {
   int64_t roff, coff;
