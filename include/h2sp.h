@@ -183,7 +183,8 @@ void h2sp_plan_destroy(h2sp_plan plan);
 
 /* Description of the kernel launches of one h2sp_build, in launch order
  * (kind: 0 QR row side, 1 QR column side, 2 couplings, 3 merge+congruence+
- * freeze, 4 row strips, 5 column strips, 6 CSR index expansion).  flops and
+ * freeze, 4 row strips, 5 column strips, 6 CSR index expansion, 7 level-0 Q
+ * formed from its compact-WY factors, both sides).  flops and
  * bytes are the algorithmic FP64 flops and HBM bytes of that launch
  * (SURVEY §8(d) per-unit figures x units in the launch); items = work units;
  * flops_exec = the FP64 flops the kernel actually issues (differs from flops

@@ -50,7 +50,7 @@ class _LaunchInfo(ctypes.Structure):
 
 
 PLAN_EXPLICIT_Q = 1   # include/h2sp.h H2SP_PLAN_EXPLICIT_Q
-LAUNCH_KINDS = ("qr_row", "qr_col", "coupling", "congruence", "strips_row", "strips_col", "csr")
+LAUNCH_KINDS = ("qr_row", "qr_col", "coupling", "congruence", "strips_row", "strips_col", "csr", "q_form")
 
 
 class _ApplyArgs(ctypes.Structure):

@@ -30,6 +30,9 @@ struct PairItem {
   int32_t yr_ld;         // leading dimension of the row-strip panel receiving bn
   int32_t yc_ld;         // leading dimension of the panel receiving nb^T
   int32_t pad_;
+  int16_t nt, ns, kt, ks;      // local sizes / ranks of t (row side) and s (column side)
+  int16_t kr0, kr1, kc0, kc1;  // ranks of the children of t and of s (level >= 1)
+  int64_t q_off_t, q_off_s;    // Q_t in q_row, Q_s in q_col
   int64_t g_src[4];      // level 0: g_src[0] = offset of C_ts in `close`; else slot offsets
   int64_t s_dst;         // S block (t@k, s@k): element (0,0) in s_val
   int64_t s_dst_m;       // symmetric: S block (s@k, t@k) (transpose), t != s
@@ -37,7 +40,10 @@ struct PairItem {
   int64_t yr_dst;        // H[:k_t, k_s:]      -> row-strip panel of t (k_t rows, ld yr_ld)
   int64_t yc_dst;        // H[k_t:, :k_s]^T    -> column-strip panel of s (general) /
                          //                      row-strip panel of s (symmetric), ld yc_ld
+  int64_t pad2_;
 };
+static_assert(sizeof(PairItem) == 144, "PairItem is staged into shared memory in 16-byte pieces");
+constexpr int PAIR_CHUNK_MAX = 8;  // items per congruence CTA (staged in shared memory)
 
 // Strips (Eq. u1v1).  All strips rotated by cluster q at level k
 // are stored as one row-major panel (k_q rows; columns = the frozen groups

@@ -141,6 +141,14 @@ __device__ __forceinline__ void cp8(void *sdst, const void *gsrc, bool valid) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gsrc), "r"(valid ? 8 : 0) : "memory");
 }
+__device__ __forceinline__ void store2(double *d, double v0, double v1) {
+  if ((reinterpret_cast<uintptr_t>(d) & 15) == 0) {
+    *reinterpret_cast<double2 *>(d) = make_double2(v0, v1);
+  } else {
+    d[0] = v0;
+    d[1] = v1;
+  }
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
@@ -436,9 +444,11 @@ __global__ void __launch_bounds__(128) qr_reg_kernel(Side sd, int L, int level, 
   // compact-WY copy (level 0 only): V (64 x wy_kp) then M = T V^T (wy_kp x 64), zero padded
   double *Wg = wy ? wy + int64_t(ci) * 128 * wy_kp : nullptr;
   if (k == 0) {
-    for (int idx = lane; idx < n * n; idx += 32) Qg[idx] = (idx / n == idx % n) ? 1.0 : 0.0;
-    if (Wg)
+    if (Wg) {  // V = M = 0: wy_form_q_kernel writes Q = I
       for (int idx = lane; idx < 128 * wy_kp; idx += 32) Wg[idx] = 0.0;
+      return;
+    }
+    for (int idx = lane; idx < n * n; idx += 32) Qg[idx] = (idx / n == idx % n) ? 1.0 : 0.0;
     return;
   }
   double x[NR][KP];
@@ -520,11 +530,11 @@ __global__ void __launch_bounds__(128) qr_reg_kernel(Side sd, int L, int level, 
       t = (beta - alpha) / beta;
     }
     double v[NR];
-    const double div = alpha - beta;
+    const double rdiv = 1.0 / (alpha - beta);
 #pragma unroll
     for (int u = 0; u < NR; u++) {
       const int i = lane + 32 * u;
-      v[u] = (i == j) ? 1.0 : ((t != 0.0 && i > j && i < n) ? x[u][0] / div : 0.0);
+      v[u] = (i == j) ? 1.0 : ((t != 0.0 && i > j && i < n) ? x[u][0] * rdiv : 0.0);
     }
     if (t != 0.0) {
       constexpr int P2 = KP <= 8 ? 8 : KP <= 16 ? 16 : 32;
@@ -604,6 +614,8 @@ __global__ void __launch_bounds__(128) qr_reg_kernel(Side sd, int L, int level, 
     }
   __syncwarp();
   if (Wg) {
+    // V and M for the compact-WY congruence; Q itself is formed later off the
+    // critical path (wy_form_q_kernel)
     for (int idx = lane; idx < 64 * wy_kp; idx += 32) {
       const int i = idx / wy_kp, c = idx - i * wy_kp;
       Wg[idx] = (i < n && c < k) ? Vs[i * LDV + c] : 0.0;
@@ -612,16 +624,7 @@ __global__ void __launch_bounds__(128) qr_reg_kernel(Side sd, int L, int level, 
       const int a = idx >> 6, c = idx & 63;
       Wg[64 * wy_kp + idx] = (a < k && c < n) ? Mm[a * LDM + c] : 0.0;
     }
-  }
-  if (Wg) {
-    for (int idx = lane; idx < 64 * wy_kp; idx += 32) {
-      const int i = idx / wy_kp, c = idx - i * wy_kp;
-      Wg[idx] = (i < n && c < k) ? Vs[i * LDV + c] : 0.0;
-    }
-    for (int idx = lane; idx < 64 * wy_kp; idx += 32) {
-      const int a = idx >> 6, c = idx & 63;
-      Wg[64 * wy_kp + idx] = (a < k && c < n) ? Mm[a * LDM + c] : 0.0;
-    }
+    return;
   }
   // ---- Q = I - V M, straight to global
   for (int ti = 0; ti < N8 / 8; ti++)
@@ -636,6 +639,56 @@ __global__ void __launch_bounds__(128) qr_reg_kernel(Side sd, int L, int level, 
         if (i < n && c < n) Qg[i * n + c] = (i == c ? 1.0 : 0.0) - acc[e];
       }
     }
+}
+
+// --------------------------------------------------------------------------
+// Level-0 Q from its compact-WY form, Q = I - V M (the same product qr_reg_kernel
+// forms at the other levels), when the level-0 congruence runs on V / M: it is
+// only an output (and input of the applies), so it is formed off the critical
+// path.  One CTA (4 warps) per leaf; warp w computes rows 16w..16w+15.
+// --------------------------------------------------------------------------
+template <int KP>
+__global__ void __launch_bounds__(128) wy_form_q_kernel(Side sr, Side sc, const double *__restrict__ wy_r,
+                                                        const double *__restrict__ wy_c, double *__restrict__ q_r,
+                                                        double *__restrict__ q_c, int64_t nclust) {
+  constexpr int LDV = KP + 4, LDM = 64 + 4;
+  __shared__ __align__(16) double sV[64 * LDV];
+  __shared__ __align__(16) double sM[KP * LDM];
+  const bool col = blockIdx.x >= nclust;  // second half of the grid: column side (general mode)
+  const int64_t cl = col ? blockIdx.x - nclust : blockIdx.x;
+  const Side &sd = col ? sc : sr;
+  const double *wy = col ? wy_c : wy_r;
+  double *qout = col ? q_c : q_r;
+  const int n = sd.n[cl];
+  if (n == 0 || !sd.need[cl]) return;
+  const double *g = wy + cl * (2 * 64 * KP);
+  async_tile<64, KP, LDV>(sV, g, 64, KP, KP, g);
+  async_tile<KP, 64, LDM>(sM, g + 64 * KP, KP, 64, 64, g);
+  cp_commit();
+  cp_wait_all();
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = lane >> 2, q = lane & 3;
+  const int m0 = warp * 16;
+  double acc[2][8][2];
+  zero_acc(acc);
+  warp_gemm<LDV, LDM, 2, 8, false>(sV, sM, m0, 0, KP, acc);
+  double *Q = qout + sd.q_off[cl];
+#pragma unroll
+  for (int i = 0; i < 2; i++) {
+    const int row = m0 + i * 8 + r;
+    if (row >= n) continue;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const int col = j * 8 + 2 * q;
+      const double v0 = (row == col ? 1.0 : 0.0) - acc[i][j][0];
+      const double v1 = (row == col + 1 ? 1.0 : 0.0) - acc[i][j][1];
+      if (col + 1 < n)
+        store2(Q + int64_t(row) * n + col, v0, v1);
+      else if (col < n)
+        Q[int64_t(row) * n + col] = v0;
+    }
+  }
 }
 
 // --------------------------------------------------------------------------
@@ -731,7 +784,7 @@ struct PairCfg {
   static constexpr int THREADS = WARPS * 32;
   static constexpr int TN = NP / 8;
   static constexpr size_t SMEM = size_t(3) * NP * LD * sizeof(double);
-  static constexpr int MIN_BLOCKS = (NP == 64) ? 2 : 6;
+  static constexpr int MIN_BLOCKS = (NP == 64) ? 2 : (NP == 48) ? 3 : 6;  // smem-bound anyway at 48, 64
 };
 
 struct PairArgs {
@@ -750,19 +803,15 @@ struct PairArgs {
 // Issue the cp.async copies of G_ts (level 0: C_ts; else the 2x2 arrangement of
 // the children's bb parts / D~) into sG.
 template <int NP>
-__device__ __forceinline__ void pair_load_G(const PairArgs &A, const PairItem &it, int t, int nt, int64_t lbase,
-                                            double *sG) {
+__device__ __forceinline__ void pair_load_G(const PairArgs &A, const PairItem &it, double *sG) {
   constexpr int LD = PairCfg<NP>::LD;
-  const int s = it.s;
-  const int ns = A.cs.n[s];
-  const void *any = A.items;
+  const int nt = it.nt, ns = it.ns;
+  const void *any = A.chunks;
   if (A.level == 0) {
     async_tile<NP, NP, LD>(sG, A.close + it.g_src[0], nt, ns, A.B, any);
   } else {
-    const int64_t tc1 = lvl_off_d(A.L, A.level - 1) + 2 * (t - lbase);
-    const int64_t sc1 = lvl_off_d(A.L, A.level - 1) + 2 * (s - lbase);
-    const int kr0 = A.rs.k[tc1], kr1 = A.rs.k[tc1 + 1];
-    const int kc0 = A.cs.k[sc1], kc1 = A.cs.k[sc1 + 1];
+    const int kr0 = it.kr0, kr1 = it.kr1;
+    const int kc0 = it.kc0, kc1 = it.kc1;
     // blockDim.x is a multiple of NP: each thread keeps one column j and walks
     // rows i = tid/NP, +R, ...; the two quadrant sources of that column (a = 0, 1)
     // are resolved once into a base pointer and a row stride.
@@ -812,15 +861,6 @@ struct PairDst {          // the destinations of one pair, kept in registers
   int32_t nt, ns, kt, ks;
   bool dsym;
 };
-
-__device__ __forceinline__ void store2(double *d, double v0, double v1) {
-  if ((reinterpret_cast<uintptr_t>(d) & 15) == 0) {
-    *reinterpret_cast<double2 *>(d) = make_double2(v0, v1);
-  } else {
-    d[0] = v0;
-    d[1] = v1;
-  }
-}
 
 __device__ __forceinline__ void scatter_pair2(const PairArgs &A, const PairDst &D, int row0, int col0, int row,
                                               int col, double v0, double v1) {
@@ -894,6 +934,21 @@ __device__ __forceinline__ void scatter_pair2(const PairArgs &A, const PairDst &
 // from T by quad shuffles.  The scatter of pair p's H is software-pipelined
 // into the T-GEMM of pair p+1 (one 8x8 tile per k-step), so the stores fill
 // issue slots between DMMAs instead of forming an idle phase.
+// Stage the chunk's work items (<= PAIR_CHUNK_MAX, 144 B each, everything a
+// pair needs precomputed by the plan) into shared memory with one batch of
+// 16-byte async copies: one global round trip per CTA instead of a chain of
+// dependent descriptor loads per pair.
+__device__ __forceinline__ int stage_items(const PairItem *items, const Chunk &ch, PairItem *s_it) {
+  const int nit = ch.end - ch.begin;
+  const char *src = reinterpret_cast<const char *>(items + ch.begin);
+  for (int c = threadIdx.x; c < nit * int(sizeof(PairItem) / 16); c += blockDim.x)
+    cp16(reinterpret_cast<char *>(s_it) + 16 * c, src + 16 * c);
+  cp_commit();
+  cp_wait_all();
+  __syncthreads();
+  return nit;
+}
+
 template <int NP>
 __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS) pair_kernel(PairArgs A) {
   using C = PairCfg<NP>;
@@ -904,21 +959,18 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS)
   double *sQt = sm;
   double *sG = sm + NP * LD;
   double *sQs = sm + 2 * NP * LD;
+  __shared__ __align__(16) PairItem s_it[PAIR_CHUNK_MAX];
   const Chunk ch = A.chunks[blockIdx.x];
-  int t = A.items[ch.begin].t;   // current block row (the chunk may cross rows)
-  int nt = A.rs.n[t], ktt = A.rs.k[t];
+  stage_items(A.items, ch, s_it);
+  int t = s_it[0].t;   // current block row (the chunk may cross rows)
+  int nt = s_it[0].nt, ktt = s_it[0].kt;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = lane >> 2, q = lane & 3;
   const int m0 = warp * 8 * TM;
-  const int64_t lbase = lvl_off_d(A.L, A.level);
   // prologue: Q_t, G_0, Q_s0
-  async_tile<NP, NP, LD>(sQt, A.q_row + A.rs.q_off[t], nt, nt, nt, A.items);
-  {
-    const PairItem it0 = A.items[ch.begin];
-    pair_load_G<NP>(A, it0, t, nt, lbase, sG);
-    const int ns0 = A.cs.n[it0.s];
-    async_tile<NP, NP, LD>(sQs, A.q_col + A.cs.q_off[it0.s], ns0, ns0, ns0, A.items);
-  }
+  async_tile<NP, NP, LD>(sQt, A.q_row + s_it[0].q_off_t, nt, nt, nt, A.chunks);
+  pair_load_G<NP>(A, s_it[0], sG);
+  async_tile<NP, NP, LD>(sQs, A.q_col + s_it[0].q_off_s, s_it[0].ns, s_it[0].ns, s_it[0].ns, A.chunks);
   cp_commit();
   double H[TM][TN][2];  // result of the previous pair, scattered during the next T-GEMM
   PairDst prev;
@@ -934,15 +986,15 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS)
       }
       break;
     }
-    const PairItem it = A.items[p];
+    const PairItem &it = s_it[p - ch.begin];
     const int s = it.s;
     cp_wait_all();
     __syncthreads();
     if (it.t != t) {  // new block row: reload the resident Q_t (G and Q_s of this pair are in flight/landed)
       t = it.t;
-      nt = A.rs.n[t];
-      ktt = A.rs.k[t];
-      async_tile<NP, NP, LD>(sQt, A.q_row + A.rs.q_off[t], nt, nt, nt, A.items);
+      nt = it.nt;
+      ktt = it.kt;
+      async_tile<NP, NP, LD>(sQt, A.q_row + it.q_off_t, nt, nt, nt, A.chunks);
       cp_commit();
       cp_wait_all();
       __syncthreads();
@@ -976,8 +1028,7 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS)
     __syncthreads();  // every warp is done with G
     const bool more = p + 1 < ch.end && !(A.debug & 2);
     if (more) {
-      const PairItem nx = A.items[p + 1];
-      pair_load_G<NP>(A, nx, nx.t, A.rs.n[nx.t], lbase, sG);
+      pair_load_G<NP>(A, s_it[p + 1 - ch.begin], sG);
       cp_commit();
     }
     // ---- H = T Q_s; A fragment (row m0+8i+r, col k0+q) lives in lane (r, (k0%8+q)/2), element q%2
@@ -1003,9 +1054,8 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS)
     }
     __syncthreads();  // every warp is done with Q_s
     if (more) {
-      const PairItem nx = A.items[p + 1];
-      const int nsx = A.cs.n[nx.s];
-      async_tile<NP, NP, LD>(sQs, A.q_col + A.cs.q_off[nx.s], nsx, nsx, nsx, A.items);
+      const PairItem &nx = s_it[p + 1 - ch.begin];
+      async_tile<NP, NP, LD>(sQs, A.q_col + nx.q_off_s, nx.ns, nx.ns, nx.ns, A.chunks);
       cp_commit();
     }
     prev.s_dst = it.s_dst;
@@ -1018,9 +1068,9 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS)
     prev.yr_ld = it.yr_ld;
     prev.yc_ld = it.yc_ld;
     prev.nt = nt;
-    prev.ns = A.cs.n[s];
+    prev.ns = it.ns;
     prev.kt = ktt;
-    prev.ks = A.cs.k[s];
+    prev.ks = it.ks;
     prev.dsym = A.sym && s == t;
     have_prev = true;
   }
@@ -1065,18 +1115,17 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
   double *sVt = sm, *sVs = sVt + C::V_D;
   double *sMt = sVs + C::V_D, *sMs = sMt + C::M_D;
   double *sG = sMs + C::M_D, *sP = sG + C::G_D;
+  __shared__ __align__(16) PairItem s_it[PAIR_CHUNK_MAX];
   const Chunk ch = A.chunks[blockIdx.x];
-  int t = A.items[ch.begin].t;
-  int nt = A.rs.n[t], ktt = A.rs.k[t];
+  stage_items(A.items, ch, s_it);
+  int t = s_it[0].t;
+  int nt = s_it[0].nt, ktt = s_it[0].kt;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = lane >> 2, q = lane & 3;
   const int m0 = warp * 8;
   wy_load<KP>(sVt, sMt, wy_row, t);
-  {
-    const PairItem it0 = A.items[ch.begin];
-    async_tile<64, 64, LD>(sG, A.close + it0.g_src[0], nt, A.cs.n[it0.s], A.B, A.items);
-    wy_load<KP>(sVs, sMs, wy_col, it0.s);
-  }
+  async_tile<64, 64, LD>(sG, A.close + s_it[0].g_src[0], nt, s_it[0].ns, A.B, A.chunks);
+  wy_load<KP>(sVs, sMs, wy_col, s_it[0].s);
   cp_commit();
   double H[TN][2];
   PairDst prev;
@@ -1090,14 +1139,14 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
       }
       break;
     }
-    const PairItem it = A.items[p];
+    const PairItem &it = s_it[p - ch.begin];
     const int s = it.s;
     cp_wait_all();
     __syncthreads();
     if (it.t != t) {
       t = it.t;
-      nt = A.rs.n[t];
-      ktt = A.rs.k[t];
+      nt = it.nt;
+      ktt = it.kt;
       wy_load<KP>(sVt, sMt, wy_row, t);
       cp_commit();
       cp_wait_all();
@@ -1144,8 +1193,8 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
     __syncthreads();  // every warp is done with G and P
     const bool more = p + 1 < ch.end && !(A.debug & 2);
     if (more) {
-      const PairItem nx = A.items[p + 1];
-      async_tile<64, 64, LD>(sG, A.close + nx.g_src[0], A.rs.n[nx.t], A.cs.n[nx.s], A.B, A.items);
+      const PairItem &nx = s_it[p + 1 - ch.begin];
+      async_tile<64, 64, LD>(sG, A.close + nx.g_src[0], nx.nt, nx.ns, A.B, A.chunks);
       cp_commit();
     }
     // ---- step 3: R = T1 V_s (8 x KP per warp), A fragments from the T1 accumulators
@@ -1180,8 +1229,7 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
     }
     __syncthreads();  // every warp is done with V_s / M_s
     if (more) {
-      const PairItem nx = A.items[p + 1];
-      wy_load<KP>(sVs, sMs, wy_col, nx.s);
+      wy_load<KP>(sVs, sMs, wy_col, s_it[p + 1 - ch.begin].s);
       cp_commit();
     }
     prev.s_dst = it.s_dst;
@@ -1194,9 +1242,9 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
     prev.yr_ld = it.yr_ld;
     prev.yc_ld = it.yc_ld;
     prev.nt = nt;
-    prev.ns = A.cs.n[s];
+    prev.ns = it.ns;
     prev.kt = ktt;
-    prev.ks = A.cs.k[s];
+    prev.ks = it.ks;
     prev.dsym = A.sym && s == t;
     have_prev = true;
   }
@@ -1657,7 +1705,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   // Launch indices are assigned in the plan's canonical order; precompute them.
   struct LvlIdx { int64_t qr_row = -1, qr_col = -1, coup = -1, pairs = -1, rstr[2] = {-1, -1}, cstr[2] = {-1, -1}; };
   std::vector<LvlIdx> li(L + 1);
-  int64_t csr_idx = -1;
+  int64_t csr_idx = -1, qform_idx = -1;
   {
     int64_t c = 0;
     for (int k = 0; k <= L; k++) {
@@ -1672,6 +1720,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       }
     }
     if (P->n_csr_rows) csr_idx = c++;
+    if (P->wy_kp) qform_idx = c++;
     nl = c;
   }
   auto qr = [&](int k, cudaStream_t s) -> h2sp_status {
@@ -1795,18 +1844,22 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     H2SP_CK(cudaEventRecord(ev_csr, s2));
     return H2SP_OK;
   };
+  // CSR expansion start (H2SP_CSR_AT, scheduling experiments): 0 (default) at the
+  // start of the build, overlapping the latency-bound QR0 and the level-0
+  // congruence; 1 after QR0; 2 after the level-0 congruence (upper-level gaps)
+  static const int csr_at = [] {
+    const char *e = getenv("H2SP_CSR_AT");
+    return e ? atoi(e) : 0;
+  }();
+  if (csr_at == 0) {
+    if (!serial) H2SP_CK(cudaStreamWaitEvent(s2, ev_begin, 0));
+    if (h2sp_status e = csr()) return e;
+  }
   // ---- step (i) at level 0 on the main stream; the rest of the QR chain and
   //      all couplings on s1, overlapping the level-0 congruence
   if (h2sp_status e = qr(0, st)) return e;
   H2SP_CK(cudaEventRecord(ev_qr0, st));
-  // CSR expansion: H2SP_CSR_AFTER=1 starts it after the level-0 congruence
-  // (fills gaps of the upper levels), default right after QR0 (overlaps the
-  // compute-bound level-0 congruence)
-  static const bool csr_after = [] {
-    const char *e = getenv("H2SP_CSR_AFTER");
-    return e && e[0] == '1';
-  }();
-  if (!csr_after) {
+  if (csr_at == 1) {
     H2SP_CK(cudaStreamWaitEvent(s2, ev_qr0, 0));
     if (h2sp_status e = csr()) return e;
   }
@@ -1818,6 +1871,19 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       if (h2sp_status e = qr(k + 1, s1)) return e;
       H2SP_CK(cudaEventRecord(ev_ready(k + 1), s1));
     }
+  }
+  // ---- level-0 Q from V / M (compact-WY path): only an output and an input of
+  //      the applies, so it trails the QR / coupling chain on s1
+  if (P->wy_kp) {
+    if (h2sp_status e = pre(s1, qform_idx)) return e;
+    const int64_t nleaf = int64_t(1) << L;
+    const unsigned grid = unsigned(nleaf * (sym ? 1 : 2));
+    if (P->wy_kp == 16)
+      wy_form_q_kernel<16><<<grid, 128, 0, s1>>>(rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf);
+    else
+      wy_form_q_kernel<24><<<grid, 128, 0, s1>>>(rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf);
+    H2SP_CK(cudaGetLastError());
+    if (h2sp_status e = post(s1, qform_idx)) return e;
   }
   // ---- the applies of the same pass (need Q only): on s1 after the QR chain
   cudaEvent_t ev_apply = aux->ev[8 + 2 * L];
@@ -1881,7 +1947,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     //      with the whole upper-level congruence chain.  Set 1 (born at a level
     //      >= 1) on s4: it needs the level-(k-1) congruence (its new strips).
     H2SP_CK(cudaEventRecord(ev_pairs(k), st));
-    if (k == 0 && csr_after) {
+    if (k == 0 && csr_at == 2) {
       H2SP_CK(cudaStreamWaitEvent(s2, ev_pairs(0), 0));
       if (h2sp_status e = csr()) return e;
     }

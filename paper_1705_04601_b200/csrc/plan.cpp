@@ -374,6 +374,19 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
         PairItem it{};
         it.t = int32_t(ct);
         it.s = int32_t(cs);
+        it.nt = int16_t(nr[ct]);
+        it.ns = int16_t(nc[cs]);
+        it.kt = int16_t(kr[ct]);
+        it.ks = int16_t(kc[cs]);
+        if (k > 0) {
+          const int64_t t1 = lvl_off(L, k - 1) + 2 * int64_t(t), s1 = lvl_off(L, k - 1) + 2 * int64_t(s);
+          it.kr0 = int16_t(kr[t1]);
+          it.kr1 = int16_t(kr[t1 + 1]);
+          it.kc0 = int16_t(kc[s1]);
+          it.kc1 = int16_t(kc[s1 + 1]);
+        }
+        it.q_off_t = P->q_off_row[ct];
+        it.q_off_s = sym ? P->q_off_row[cs] : P->q_off_col[cs];
         it.s_dst = it.s_dst_m = it.bb_dst = it.yr_dst = it.yc_dst = -1;
         for (int q = 0; q < 4; q++) it.g_src[q] = -1;
         if (k == 0) {
@@ -713,7 +726,8 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
     // items per CTA chunk sharing one rotating cluster: up to 8 (reuse of the
     // resident Q), fewer when a level has too few items to fill ~4 CTAs/SM
     auto chunk = [&](const auto &items, auto qof) {
-      static const int CHMAX = getenv("H2SP_CHUNK") ? atoi(getenv("H2SP_CHUNK")) : 6;
+      static const int CHMAX =
+          std::max(1, std::min(PAIR_CHUNK_MAX, getenv("H2SP_CHUNK") ? atoi(getenv("H2SP_CHUNK")) : 6));
       const int CH = int(std::max<int64_t>(1, std::min<int64_t>(CHMAX, int64_t(items.size()) / (148 * 4))));
       std::vector<Chunk> ch;
       size_t j = 0;
@@ -875,6 +889,31 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
     if (P->n_csr_rows) {  // CSR column expansion (+ the rowptr D2D copy)
       launches++;
       P->launch_info.push_back(h2sp_launch_info{6, L, P->n_csr_rows, 0.0, 4.0 * double(nnz) + 16.0 * double(NR_loc + 1)});
+    }
+    if (P->wy_kp) {  // level-0 Q formed from V / M (kernels.cu wy_form_q_kernel), after the CSR entry
+      launches++;
+      h2sp_launch_info li{7, 0, 0, 0.0, 0.0};
+      for (int side = 0; side < (sym ? 1 : 2); side++) {
+        const auto &n = side ? nc : nr;
+        const auto &kk = side ? kc : kr;
+        const auto &need = side ? need_c : need_r;
+        for (int64_t c = 0; c < nleaf; c++) {
+          if (n[c] == 0 || !need[c]) continue;
+          li.items++;
+          li.flops += 2.0 * n[c] * n[c] * kk[c];
+          li.bytes += 8.0 * (n[c] * n[c] + 2.0 * 64 * P->wy_kp);
+        }
+      }
+      P->launch_info.push_back(li);
+      // the QR launches of level 0 no longer form Q: move those flops (keeps the total)
+      for (auto &x : P->launch_info)
+        if (x.level == 0 && (x.kind == 0 || x.kind == 1)) {
+          const auto &n = x.kind ? nc : nr;
+          const auto &kk = x.kind ? kc : kr;
+          const auto &need = x.kind ? need_c : need_r;
+          for (int64_t c = 0; c < nleaf; c++)
+            if (n[c] && need[c]) x.flops -= 2.0 * n[c] * n[c] * kk[c];
+        }
     }
     P->launches = launches;
     P->levels_active = levels_active;
