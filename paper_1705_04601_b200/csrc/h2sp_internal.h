@@ -75,6 +75,20 @@ struct StripTile {       // columns [c0, c1) of one panel; g0 = first group over
   int32_t panel, c0, c1, g0;
 };
 
+// Kernel-side strip tile: the tile, its panel and the cluster sizes folded into
+// one 96-byte record (staged with 16-byte async copies: one round trip).
+struct StripTileX {
+  int32_t q, c0, ncol, g0;     // rotating cluster, panel columns [c0, c0 + ncol), first group
+  int32_t gend;                // end of the panel's groups
+  int16_t n, kq, k1, k2;       // n_q, k_q, k_c1, k_c2
+  int32_t ld_c1, ld_c2, y_ld, s_ld;
+  int32_t pad_;
+  int64_t q_off;               // Q_q in the side's Q array
+  int64_t src_c1, src_c2, y_dst, s_dst;  // as StripPanel
+  int64_t pad2_;
+};
+static_assert(sizeof(StripTileX) == 96, "staged as 6 x 16 bytes");
+
 // A run of items that share the rotating cluster (Q kept in shared memory).
 struct Chunk {
   int32_t begin, end;

@@ -1269,10 +1269,8 @@ struct StripCfg {
 };
 
 struct StripArgs {
-  const StripTile *tiles;
-  const StripPanel *panels;
+  const StripTileX *tiles;
   const StripGroup *groups;
-  Side sd;
   int L, level;
   const double *q;
   const double *y_in;
@@ -1285,30 +1283,28 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS) strip_kernel(StripA
   using C = StripCfg<NP, TN>;
   extern __shared__ __align__(16) double sm[];
   double *sQ = sm;                           // NP x LDQ
-  double *sZ = sm + NP * C::LDQ;             // NP x LDZ (Z, then W)
+  double *sZ = sm + NP * C::LDQ;             // NP x LDZ
   int64_t *tdst = reinterpret_cast<int64_t *>(sZ + NP * C::LDZ);  // per column: transposed S dst (b*ld folded in)
   int32_t *src1 = reinterpret_cast<int32_t *>(tdst + TN);          // per column: column in child-1 panel or -1
   int32_t *src2 = src1 + TN;
-  int32_t *tld = reinterpret_cast<int32_t *>(src2 + TN);           // unused padding slot
-  (void)tld;
   __shared__ StripGroup sg[TN + 1];            // groups overlapping this tile (<= TN of them)
-  __shared__ int s_ng;
-  const StripTile tile = A.tiles[blockIdx.x];
-  const StripPanel pn = A.panels[tile.panel];
-  const int q = pn.q;
-  const int n = A.sd.n[q], kq = A.sd.k[q];
-  const int64_t c1 = lvl_off_d(A.L, A.level - 1) + 2 * (q - lvl_off_d(A.L, A.level));
-  const int k1 = A.sd.k[c1], k2 = A.sd.k[c1 + 1];
-  const int ncol = tile.c1 - tile.c0;
-  async_tile<NP, NP, C::LDQ>(sQ, A.q + A.sd.q_off[q], n, n, n, A.tiles);
-  // stage the (at most TN) groups overlapping [c0, c1) in one batch
-  {
-    const int gmax = min(pn.gend - tile.g0, TN + 1);
-    if (threadIdx.x == 0) s_ng = gmax;
-    for (int g = threadIdx.x; g < gmax * 4; g += blockDim.x)
-      cp8(reinterpret_cast<char *>(&sg[g >> 2]) + 8 * (g & 3),
-          reinterpret_cast<const char *>(&A.groups[tile.g0 + (g >> 2)]) + 8 * (g & 3), true);
-  }
+  __shared__ __align__(16) StripTileX s_tile;
+  // round trip 1: the self-contained tile descriptor
+  if (threadIdx.x < sizeof(StripTileX) / 16)
+    cp16(reinterpret_cast<char *>(&s_tile) + 16 * threadIdx.x,
+         reinterpret_cast<const char *>(A.tiles + blockIdx.x) + 16 * threadIdx.x);
+  cp_commit();
+  cp_wait_all();
+  __syncthreads();
+  const StripTileX &T = s_tile;
+  const int n = T.n, kq = T.kq, k1 = T.k1, k2 = T.k2;
+  const int ncol = T.ncol;
+  // round trip 2: Q_q and the (at most TN + 1) groups overlapping the tile
+  async_tile<NP, NP, C::LDQ>(sQ, A.q + T.q_off, n, n, n, A.tiles);
+  const int ng = min(T.gend - T.g0, TN + 1);
+  for (int g = threadIdx.x; g < ng * 2; g += blockDim.x)
+    cp16(reinterpret_cast<char *>(&sg[g >> 1]) + 16 * (g & 1),
+         reinterpret_cast<const char *>(&A.groups[T.g0 + (g >> 1)]) + 16 * (g & 1));
   cp_commit();
   cp_wait_all();
   __syncthreads();
@@ -1317,9 +1313,9 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS) strip_kernel(StripA
     int32_t a1 = -1, a2 = -1;
     int64_t td = -1;
     if (cc < ncol) {
-      const int c = tile.c0 + cc;
+      const int c = T.c0 + cc;
       int g = 0;
-      while (g + 1 < s_ng && sg[g + 1].col0 <= c) g++;
+      while (g + 1 < ng && sg[g + 1].col0 <= c) g++;
       const StripGroup gr = sg[g];
       const int b = c - gr.col0;
       if (gr.pos_c1 >= 0) a1 = gr.pos_c1 + b;
@@ -1336,12 +1332,12 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS) strip_kernel(StripA
   const int n4 = rup(n, 4);
   {
     const int cc = threadIdx.x % TN, R = blockDim.x / TN;
-    const double *b1 = src1[cc] >= 0 ? A.y_in + pn.src_c1 + src1[cc] : nullptr;
-    const double *b2 = src2[cc] >= 0 ? A.y_in + pn.src_c2 + src2[cc] : nullptr;
+    const double *b1 = src1[cc] >= 0 ? A.y_in + T.src_c1 + src1[cc] : nullptr;
+    const double *b2 = src2[cc] >= 0 ? A.y_in + T.src_c2 + src2[cc] : nullptr;
     for (int i = threadIdx.x / TN; i < n4; i += R) {
       const bool first = i < k1;
       const double *bp = first ? b1 : (i < k1 + k2 ? b2 : nullptr);
-      const double *src = bp ? bp + int64_t(first ? i : i - k1) * (first ? pn.ld_c1 : pn.ld_c2)
+      const double *src = bp ? bp + int64_t(first ? i : i - k1) * (first ? T.ld_c1 : T.ld_c2)
                              : reinterpret_cast<const double *>(A.tiles);
       cp8(&sZ[i * C::LDZ + cc], src, bp != nullptr);
     }
@@ -1371,10 +1367,10 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS) strip_kernel(StripA
       const double v0 = acc[i][j][0], v1 = acc[i][j][1];
       double *d = nullptr;
       if (row < kq) {
-        if (pn.y_dst >= 0) d = A.y_out + pn.y_dst + int64_t(row) * pn.y_ld + tile.c0 + col;
+        if (T.y_dst >= 0) d = A.y_out + T.y_dst + int64_t(row) * T.y_ld + T.c0 + col;
       } else {
         const int a = row - kq;
-        if (pn.s_dst >= 0) d = A.s_val + pn.s_dst + int64_t(a) * pn.s_ld + tile.c0 + col;
+        if (T.s_dst >= 0) d = A.s_val + T.s_dst + int64_t(a) * T.s_ld + T.c0 + col;
         const int64_t t0 = tdst[col];
         if (t0 >= 0) A.s_val[t0 + a] = v0;
         if (two) {
@@ -1960,10 +1956,8 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       }
       if (sp.n_rtiles) {
         StripArgs a;
-        a.tiles = (const StripTile *)(meta + sp.rtiles_off);
-        a.panels = (const StripPanel *)(meta + sp.rpanels_off);
+        a.tiles = (const StripTileX *)(meta + sp.rtiles_off);
         a.groups = (const StripGroup *)(meta + sp.rgroups_off);
-        a.sd = rs;
         a.L = L;
         a.level = k;
         a.q = out->q_row;
@@ -1977,10 +1971,8 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       }
       if (sp.n_ctiles) {
         StripArgs a;
-        a.tiles = (const StripTile *)(meta + sp.ctiles_off);
-        a.panels = (const StripPanel *)(meta + sp.cpanels_off);
+        a.tiles = (const StripTileX *)(meta + sp.ctiles_off);
         a.groups = (const StripGroup *)(meta + sp.cgroups_off);
-        a.sd = cs;
         a.L = L;
         a.level = k;
         a.q = q_col;

@@ -31,6 +31,11 @@ struct PlanError : std::runtime_error {
 };
 
 inline int64_t lvl_off(int L, int k) { return (int64_t(1) << (L + 1)) - (int64_t(1) << (L - k + 1)); }
+inline int level_of(int L, int64_t c) {  // level of level-major cluster id c
+  int k = 0;
+  while (k < L && c >= lvl_off(L, k + 1)) k++;
+  return k;
+}
 inline uint64_t pkey(int64_t t, int64_t s) { return (uint64_t(uint32_t(t)) << 32) | uint64_t(uint32_t(s)); }
 inline int32_t kt(uint64_t k) { return int32_t(k >> 32); }
 inline int32_t ks(uint64_t k) { return int32_t(k & 0xffffffffu); }
@@ -739,6 +744,40 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
       }
       return ch;
     };
+    auto flat_tiles = [&](const std::vector<StripTile> &tils, const std::vector<StripPanel> &pans, bool row_side) {
+      const auto &n = row_side ? nr : nc;
+      const auto &kk = row_side ? kr : kc;
+      const auto &qoff = (row_side || sym) ? P->q_off_row : P->q_off_col;
+      std::vector<StripTileX> out(tils.size());
+      for (size_t i = 0; i < tils.size(); i++) {
+        const StripTile &t = tils[i];
+        const StripPanel &pn = pans[t.panel];
+        const int64_t q = pn.q;
+        const int k = level_of(L, q);
+        const int64_t c1 = lvl_off(L, k - 1) + 2 * (q - lvl_off(L, k));
+        StripTileX &x = out[i];
+        x = StripTileX{};
+        x.q = pn.q;
+        x.c0 = t.c0;
+        x.ncol = t.c1 - t.c0;
+        x.g0 = t.g0;
+        x.gend = pn.gend;
+        x.n = int16_t(n[q]);
+        x.kq = int16_t(kk[q]);
+        x.k1 = int16_t(kk[c1]);
+        x.k2 = int16_t(kk[c1 + 1]);
+        x.ld_c1 = pn.ld_c1;
+        x.ld_c2 = pn.ld_c2;
+        x.y_ld = pn.y_ld;
+        x.s_ld = pn.s_ld;
+        x.q_off = qoff[q];
+        x.src_c1 = pn.src_c1;
+        x.src_c2 = pn.src_c2;
+        x.y_dst = pn.y_dst;
+        x.s_dst = pn.s_dst;
+      }
+      return out;
+    };
     for (int k = 0; k <= L; k++) {
       LevelPlan &lp = P->levels[k];
       lp = LevelPlan{};
@@ -773,11 +812,11 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
       for (int set = 0; set < 2; set++) {
         const int sidx = set * (L + 1) + k;
         lp.sp[set].n_rtiles = int64_t(rtil[sidx].size());
-        lp.sp[set].rtiles_off = mb.put(rtil[sidx]);
+        lp.sp[set].rtiles_off = mb.put(flat_tiles(rtil[sidx], rpan[sidx], true));
         lp.sp[set].rpanels_off = mb.put(rpan[sidx]);
         lp.sp[set].rgroups_off = mb.put(rgrp[sidx]);
         lp.sp[set].n_ctiles = int64_t(ctil[sidx].size());
-        lp.sp[set].ctiles_off = mb.put(ctil[sidx]);
+        lp.sp[set].ctiles_off = mb.put(flat_tiles(ctil[sidx], cpan[sidx], false));
         lp.sp[set].cpanels_off = mb.put(cpan[sidx]);
         lp.sp[set].cgroups_off = mb.put(cgrp[sidx]);
       }
