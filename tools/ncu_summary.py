@@ -13,7 +13,7 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct"]
 
 
-def main(rep, out_json, kind, level, note):
+def main(rep, out_json, kind, level, note, workload="", alg_flops=None, exec_flops=None):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(io.StringIO(raw)))
     h, u, v = r[0], r[1], r[2]
@@ -29,7 +29,8 @@ def main(rep, out_json, kind, level, note):
         return f * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}.get(unit, 1.0)
 
     traffic = mb(m["dram__bytes_read.sum"]) + mb(m["dram__bytes_write.sum"])
-    out = {"kernel_kind": kind, "level": level, "kernel": d.get("Kernel Name", ("", ""))[0],
+    out = {"kernel_kind": kind, "level": level, "workload": workload, "algorithmic_flops": alg_flops,
+           "executed_flops": exec_flops, "kernel": d.get("Kernel Name", ("", ""))[0],
            "dram_bytes_per_launch": traffic, "metrics": {k: f"{a} {b}" for k, (a, b) in m.items()},
            "stalls_per_issue": stalls, "note": note}
     json.dump(out, open(out_json, "w"), indent=1)
@@ -37,4 +38,6 @@ def main(rep, out_json, kind, level, note):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4]), sys.argv[5] if len(sys.argv) > 5 else "")
+    a = sys.argv
+    main(a[1], a[2], a[3], int(a[4]), a[5] if len(a) > 5 else "", a[6] if len(a) > 6 else "",
+         float(a[7]) if len(a) > 7 else None, float(a[8]) if len(a) > 8 else None)
