@@ -169,9 +169,10 @@ struct h2sp_plan_s {
   // workspace layout after the meta region (byte offsets)
   size_t ws_rh_row, ws_rh_col, ws_dt, ws_bb, ws_yr, ws_yc, ws_total;
   // compact-WY form of the level-0 Q (0 = explicit Q everywhere): per leaf,
-  // V (64 x wy_kp, row-major) then M = T V^T (wy_kp x 64), zero padded
-  int32_t wy_kp;
+  // V (wy_n x wy_kp, row-major) then M = T V^T (wy_kp x wy_n), zero padded
+  int32_t wy_kp, wy_n;                      // wy_n: padded leaf size of V / M (64 or 128)
   size_t ws_wy_row, ws_wy_col;
+  int32_t nmax;                             // largest local size n_t
   int64_t launches;
   std::vector<h2sp_launch_info> launch_info;
   uint64_t magic;                           // first 8 bytes of the meta image (checked on device)

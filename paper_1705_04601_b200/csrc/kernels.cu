@@ -203,7 +203,8 @@ __host__ __device__ inline int qr_warp_doubles(int n, int k, int rstage) {
 __global__ void __launch_bounds__(128) qr_kernel(Side sd, int L, int level, int nclust, int per_warp,
                                                  const double *__restrict__ leaf, const double *__restrict__ transfer,
                                                  double *__restrict__ rh, double *__restrict__ qout,
-                                                 const uint64_t *meta_magic, uint64_t magic) {
+                                                 const uint64_t *meta_magic, uint64_t magic, double *__restrict__ wy,
+                                                 int wy_kp, int wy_n) {
   if (meta_magic && threadIdx.x == 0 && blockIdx.x == 0 && *meta_magic != magic) __trap();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ci = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -213,7 +214,13 @@ __global__ void __launch_bounds__(128) qr_kernel(Side sd, int L, int level, int 
   const int n = sd.n[cl], k = sd.k[cl];
   if (n == 0 || !sd.need[cl]) return;
   double *Qg = qout + sd.q_off[cl];
+  // compact-WY copy (level 0 only), as qr_reg_kernel
+  double *Wg = wy ? wy + int64_t(ci) * 2 * wy_n * wy_kp : nullptr;
   if (k == 0) {
+    if (Wg) {
+      for (int idx = lane; idx < 2 * wy_n * wy_kp; idx += 32) Wg[idx] = 0.0;
+      return;
+    }
     for (int idx = lane; idx < n * n; idx += 32) Qg[idx] = (idx / n == idx % n) ? 1.0 : 0.0;
     return;
   }
@@ -367,6 +374,17 @@ __global__ void __launch_bounds__(128) qr_kernel(Side sd, int L, int level, int 
       }
     }
   __syncwarp();
+  if (Wg) {
+    for (int idx = lane; idx < wy_n * wy_kp; idx += 32) {
+      const int i = idx / wy_kp, c = idx - i * wy_kp;
+      Wg[idx] = V(i, c);
+    }
+    for (int idx = lane; idx < wy_n * wy_kp; idx += 32) {
+      const int a = idx / wy_n, c = idx - a * wy_n;
+      Wg[wy_n * wy_kp + idx] = (a < k && c < n) ? Mm[a * LDM + c] : 0.0;
+    }
+    return;
+  }
   // ---- Q = I - V M, straight to global
   for (int ti = 0; ti < N8 / 8; ti++)
     for (int tc = 0; tc < N8 / 8; tc++) {
@@ -431,7 +449,7 @@ __global__ void __launch_bounds__(128) qr_reg_kernel(Side sd, int L, int level, 
                                                      const double *__restrict__ leaf,
                                                      const double *__restrict__ transfer, double *__restrict__ rh,
                                                      double *__restrict__ qout, const uint64_t *meta_magic,
-                                                     uint64_t magic, double *__restrict__ wy, int wy_kp) {
+                                                     uint64_t magic, double *__restrict__ wy, int wy_kp, int wy_n) {
   if (meta_magic && threadIdx.x == 0 && blockIdx.x == 0 && *meta_magic != magic) __trap();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ci = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -441,11 +459,11 @@ __global__ void __launch_bounds__(128) qr_reg_kernel(Side sd, int L, int level, 
   const int n = sd.n[cl], k = sd.k[cl];
   if (n == 0 || !sd.need[cl]) return;
   double *Qg = qout + sd.q_off[cl];
-  // compact-WY copy (level 0 only): V (64 x wy_kp) then M = T V^T (wy_kp x 64), zero padded
-  double *Wg = wy ? wy + int64_t(ci) * 128 * wy_kp : nullptr;
+  // compact-WY copy (level 0 only): V (wy_n x wy_kp) then M = T V^T (wy_kp x wy_n), zero padded
+  double *Wg = wy ? wy + int64_t(ci) * 2 * wy_n * wy_kp : nullptr;
   if (k == 0) {
     if (Wg) {  // V = M = 0: wy_form_q_kernel writes Q = I
-      for (int idx = lane; idx < 128 * wy_kp; idx += 32) Wg[idx] = 0.0;
+      for (int idx = lane; idx < 2 * wy_n * wy_kp; idx += 32) Wg[idx] = 0.0;
       return;
     }
     for (int idx = lane; idx < n * n; idx += 32) Qg[idx] = (idx / n == idx % n) ? 1.0 : 0.0;
@@ -616,13 +634,13 @@ __global__ void __launch_bounds__(128) qr_reg_kernel(Side sd, int L, int level, 
   if (Wg) {
     // V and M for the compact-WY congruence; Q itself is formed later off the
     // critical path (wy_form_q_kernel)
-    for (int idx = lane; idx < 64 * wy_kp; idx += 32) {
+    for (int idx = lane; idx < wy_n * wy_kp; idx += 32) {
       const int i = idx / wy_kp, c = idx - i * wy_kp;
       Wg[idx] = (i < n && c < k) ? Vs[i * LDV + c] : 0.0;
     }
-    for (int idx = lane; idx < 64 * wy_kp; idx += 32) {
-      const int a = idx >> 6, c = idx & 63;
-      Wg[64 * wy_kp + idx] = (a < k && c < n) ? Mm[a * LDM + c] : 0.0;
+    for (int idx = lane; idx < wy_n * wy_kp; idx += 32) {
+      const int a = idx / wy_n, c = idx - a * wy_n;
+      Wg[wy_n * wy_kp + idx] = (a < k && c < n) ? Mm[a * LDM + c] : 0.0;
     }
     return;
   }
@@ -642,18 +660,158 @@ __global__ void __launch_bounds__(128) qr_reg_kernel(Side sd, int L, int level, 
 }
 
 // --------------------------------------------------------------------------
+// Level-0 QR completion for leaves with 64 < n <= 128 (config 5: B = 128, k <= 32):
+// one CTA of 128 threads per leaf, thread i owns row i of X in registers
+// (shifting column window as qr_reg_kernel); the per-column reductions are a
+// warp butterfly plus a 4-way cross-warp sum through shared memory.  Same
+// convention H; emits R^ and the compact-WY factors V, M = T V^T only (leaves
+// this large always take the compact-WY congruence; wy_form_q_kernel forms Q).
+// --------------------------------------------------------------------------
+template <int KP>
+__global__ void __launch_bounds__(128) qr_cta_kernel(Side sd, int nclust, const double *__restrict__ leaf,
+                                                     double *__restrict__ rh, double *__restrict__ wy, int wy_kp,
+                                                     int wy_n, const uint64_t *meta_magic, uint64_t magic) {
+  if (meta_magic && threadIdx.x == 0 && blockIdx.x == 0 && *meta_magic != magic) __trap();
+  constexpr int LDV = KP + 4, LDT = KP + 4, LDM = 128 + 4;
+  extern __shared__ __align__(16) double smc[];
+  double *Vs = smc;              // 128 x LDV (unit lower trapezoidal, zero padded)
+  double *Tw = Vs + 128 * LDV;   // KP x LDT
+  double *Mm = Tw + KP * LDT;    // G = V^T V (KP x KP, ld LDT), then M = T V^T (KP x LDM)
+  __shared__ double red_ss[2][4], red_w[2][4][KP], wsum[KP];
+  __shared__ double s_alpha[2];
+  const int ci = blockIdx.x;
+  if (ci >= nclust) return;
+  const int64_t cl = ci;  // level 0
+  const int n = sd.n[cl], k = sd.k[cl];
+  if (n == 0 || !sd.need[cl]) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double *Wg = wy + int64_t(ci) * 2 * wy_n * wy_kp;
+  if (k == 0) {
+    for (int idx = tid; idx < 2 * wy_n * wy_kp; idx += blockDim.x) Wg[idx] = 0.0;
+    return;
+  }
+  double x[KP];
+  {
+    const double *R = leaf + sd.leaf_off[cl];
+#pragma unroll
+    for (int c = 0; c < KP; c++) x[c] = (tid < n && c < k) ? __ldg(R + int64_t(tid) * k + c) : 0.0;
+  }
+  for (int idx = tid; idx < 128 * LDV; idx += blockDim.x) Vs[idx] = 0.0;
+  for (int idx = tid; idx < KP * LDT; idx += blockDim.x) Tw[idx] = 0.0;
+  double *Rg = rh + sd.rh_off[cl];
+  for (int j = 0; j < k; j++) {
+    const int b = j & 1, w_left = k - j;
+    double ss = (tid > j && tid < n) ? x[0] * x[0] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) red_ss[b][warp] = ss;
+    if (tid == j) s_alpha[b] = x[0];
+    __syncthreads();
+    ss = (red_ss[b][0] + red_ss[b][1]) + (red_ss[b][2] + red_ss[b][3]);
+    const double alpha = s_alpha[b];
+    const double sigma = sqrt(ss);
+    double beta, t;
+    if (sigma == 0.0) {
+      t = 0.0;
+      beta = alpha;
+    } else {
+      const double sgn = alpha < 0.0 ? -1.0 : 1.0;
+      beta = -sgn * hypot(alpha, sigma);
+      t = (beta - alpha) / beta;
+    }
+    const double rdiv = 1.0 / (alpha - beta);
+    const double v = (tid == j) ? 1.0 : ((t != 0.0 && tid > j && tid < n) ? x[0] * rdiv : 0.0);
+    if (t != 0.0) {  // uniform over the CTA
+      double w[KP];
+#pragma unroll
+      for (int c = 0; c < KP; c++) w[c] = (c >= 1 && c < w_left) ? v * x[c] : 0.0;
+      warp_allreduce_vec<KP>(w, lane);
+      if (lane < KP) {
+        double mine = w[0];
+#pragma unroll
+        for (int c = 1; c < KP; c++)
+          if (lane == c) mine = w[c];
+        red_w[b][warp][lane] = mine;
+      }
+      __syncthreads();
+      if (tid < KP) wsum[tid] = (red_w[b][0][tid] + red_w[b][1][tid]) + (red_w[b][2][tid] + red_w[b][3][tid]);
+      __syncthreads();
+#pragma unroll
+      for (int c = 1; c < KP; c++)
+        if (c < w_left) x[c] = fma(-(t * wsum[c]), v, x[c]);
+    }
+    if (tid >= j && tid < n) Vs[tid * LDV + j] = v;
+    if (tid == j) {
+      for (int c = 0; c < j; c++) Rg[j * k + c] = 0.0;
+      Rg[j * k + j] = beta;
+#pragma unroll
+      for (int c = 1; c < KP; c++)
+        if (c < w_left) Rg[j * k + j + c] = x[c];
+    }
+    if (tid == 0) Tw[j * LDT + j] = t;
+#pragma unroll
+    for (int c = 0; c < KP - 1; c++) x[c] = x[c + 1];
+    x[KP - 1] = 0.0;
+  }
+  __syncthreads();
+  const int r = lane >> 2, q = lane & 3;
+  constexpr int KT = KP / 8;
+  // ---- G = V^T V (KP x KP, all tiles; warps take tiles round robin)
+  for (int tile = warp; tile < KT * KT; tile += 4) {
+    const int ta = tile / KT, tb = tile % KT;
+    double acc[2] = {0.0, 0.0};
+    for (int k0 = 0; k0 < 128; k0 += 4) dmma(acc, Vs[(k0 + q) * LDV + ta * 8 + r], Vs[(k0 + q) * LDV + tb * 8 + r]);
+    Mm[(ta * 8 + r) * LDT + tb * 8 + 2 * q] = acc[0];
+    Mm[(ta * 8 + r) * LDT + tb * 8 + 2 * q + 1] = acc[1];
+  }
+  __syncthreads();
+  // ---- T recurrence (dlarft, forward, columnwise), warp 0
+  if (warp == 0) {
+    for (int j = 1; j < k; j++) {
+      const double tj = Tw[j * LDT + j];
+      double vv = 0.0;
+      if (lane < j)
+        for (int l = lane; l < j; l++) vv = fma(Tw[lane * LDT + l], Mm[l * LDT + j], vv);
+      __syncwarp();
+      if (lane < j) Tw[lane * LDT + j] = -tj * vv;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // ---- M = T V^T (KP x 128) -> Mm (ld LDM); G is dead
+  for (int tile = warp; tile < KT * 16; tile += 4) {
+    const int ta = tile / 16, tc = tile % 16;
+    double acc[2] = {0.0, 0.0};
+#pragma unroll
+    for (int k0 = 0; k0 < KP; k0 += 4) dmma(acc, Tw[(ta * 8 + r) * LDT + k0 + q], Vs[(tc * 8 + r) * LDV + k0 + q]);
+    __syncwarp();
+    Mm[(ta * 8 + r) * LDM + tc * 8 + 2 * q] = acc[0];
+    Mm[(ta * 8 + r) * LDM + tc * 8 + 2 * q + 1] = acc[1];
+  }
+  __syncthreads();
+  for (int idx = tid; idx < wy_n * wy_kp; idx += blockDim.x) {
+    const int i = idx / wy_kp, c = idx - i * wy_kp;
+    Wg[idx] = (i < n && c < k) ? Vs[i * LDV + c] : 0.0;
+  }
+  for (int idx = tid; idx < wy_n * wy_kp; idx += blockDim.x) {
+    const int a = idx / wy_n, c = idx - a * wy_n;
+    Wg[wy_n * wy_kp + idx] = (a < k && c < n) ? Mm[a * LDM + c] : 0.0;
+  }
+}
+
+// --------------------------------------------------------------------------
 // Level-0 Q from its compact-WY form, Q = I - V M (the same product qr_reg_kernel
 // forms at the other levels), when the level-0 congruence runs on V / M: it is
 // only an output (and input of the applies), so it is formed off the critical
 // path.  One CTA (4 warps) per leaf; warp w computes rows 16w..16w+15.
 // --------------------------------------------------------------------------
-template <int KP>
-__global__ void __launch_bounds__(128) wy_form_q_kernel(Side sr, Side sc, const double *__restrict__ wy_r,
-                                                        const double *__restrict__ wy_c, double *__restrict__ q_r,
-                                                        double *__restrict__ q_c, int64_t nclust) {
-  constexpr int LDV = KP + 4, LDM = 64 + 4;
-  __shared__ __align__(16) double sV[64 * LDV];
-  __shared__ __align__(16) double sM[KP * LDM];
+template <int KP, int NW>
+__global__ void __launch_bounds__(NW * 2) wy_form_q_kernel(Side sr, Side sc, const double *__restrict__ wy_r,
+                                                           const double *__restrict__ wy_c, double *__restrict__ q_r,
+                                                           double *__restrict__ q_c, int64_t nclust) {
+  constexpr int LDV = KP + 4, LDM = NW + 4;
+  extern __shared__ __align__(16) double smw[];
+  double *sV = smw, *sM = smw + NW * LDV;
   const bool col = blockIdx.x >= nclust;  // second half of the grid: column side (general mode)
   const int64_t cl = col ? blockIdx.x - nclust : blockIdx.x;
   const Side &sd = col ? sc : sr;
@@ -661,34 +819,48 @@ __global__ void __launch_bounds__(128) wy_form_q_kernel(Side sr, Side sc, const 
   double *qout = col ? q_c : q_r;
   const int n = sd.n[cl];
   if (n == 0 || !sd.need[cl]) return;
-  const double *g = wy + cl * (2 * 64 * KP);
-  async_tile<64, KP, LDV>(sV, g, 64, KP, KP, g);
-  async_tile<KP, 64, LDM>(sM, g + 64 * KP, KP, 64, 64, g);
+  const double *g = wy + cl * (2 * NW * KP);
+  async_tile<NW, KP, LDV>(sV, g, NW, KP, KP, g);
+  async_tile<KP, NW, LDM>(sM, g + NW * KP, KP, NW, NW, g);
   cp_commit();
   cp_wait_all();
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = lane >> 2, q = lane & 3;
   const int m0 = warp * 16;
-  double acc[2][8][2];
-  zero_acc(acc);
-  warp_gemm<LDV, LDM, 2, 8, false>(sV, sM, m0, 0, KP, acc);
   double *Q = qout + sd.q_off[cl];
+  for (int n0 = 0; n0 < NW; n0 += 64) {  // 16 x 64 output tiles per warp
+    double acc[2][8][2];
+    zero_acc(acc);
+    warp_gemm<LDV, LDM, 2, 8, false>(sV, sM, m0, n0, KP, acc);
 #pragma unroll
-  for (int i = 0; i < 2; i++) {
-    const int row = m0 + i * 8 + r;
-    if (row >= n) continue;
+    for (int i = 0; i < 2; i++) {
+      const int row = m0 + i * 8 + r;
+      if (row >= n) continue;
 #pragma unroll
-    for (int j = 0; j < 8; j++) {
-      const int col = j * 8 + 2 * q;
-      const double v0 = (row == col ? 1.0 : 0.0) - acc[i][j][0];
-      const double v1 = (row == col + 1 ? 1.0 : 0.0) - acc[i][j][1];
-      if (col + 1 < n)
-        store2(Q + int64_t(row) * n + col, v0, v1);
-      else if (col < n)
-        Q[int64_t(row) * n + col] = v0;
+      for (int j = 0; j < 8; j++) {
+        const int c = n0 + j * 8 + 2 * q;
+        const double v0 = (row == c ? 1.0 : 0.0) - acc[i][j][0];
+        const double v1 = (row == c + 1 ? 1.0 : 0.0) - acc[i][j][1];
+        if (c + 1 < n)
+          store2(Q + int64_t(row) * n + c, v0, v1);
+        else if (c < n)
+          Q[int64_t(row) * n + c] = v0;
+      }
     }
   }
+}
+
+template <int KP, int NW>
+static void launch_wy_form_q(unsigned grid, cudaStream_t st, const Side &rs, const Side &cs, const double *wr,
+                             const double *wc, double *qr, double *qc, int64_t nleaf) {
+  constexpr size_t smem = size_t(NW * (KP + 4) + KP * (NW + 4)) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(wy_form_q_kernel<KP, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = true;
+  }
+  wy_form_q_kernel<KP, NW><<<grid, NW * 2, smem, st>>>(rs, cs, wr, wc, qr, qc, nleaf);
 }
 
 // --------------------------------------------------------------------------
@@ -1251,6 +1423,158 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
 }
 
 // --------------------------------------------------------------------------
+// Level-0 compact-WY congruence for 128-point leaves (config 5: B = 128, r = 32).
+// Same four products as pair_wy_kernel; a 128 x 128 G plus one V / M pair fill
+// 206 KB of shared memory, so one CTA (16 warps) per SM and the two sides' V / M
+// share one buffer: V_t, M_t for steps 1-2 (P = V_t^T G lands in the V buffer),
+// then V_s, M_s for steps 3-4 (their load is the one exposed latency per pair;
+// the next G streams in behind steps 3-4).  Warp w owns rows 8w..8w+7.
+// --------------------------------------------------------------------------
+template <int KP>
+struct PairWy128Cfg {
+  static constexpr int NP = 128;
+  static constexpr int LD = NP + 4;    // G, M, P rows
+  static constexpr int LDV = KP + 4;   // V rows
+  static constexpr int WARPS = 16;
+  static constexpr int THREADS = WARPS * 32;
+  static constexpr int G_D = NP * LD, V_D = NP * LDV, M_D = KP * LD;
+  static_assert(KP * LD <= NP * LDV, "P aliases the V buffer");
+  static constexpr size_t SMEM = size_t(G_D + V_D + M_D) * sizeof(double);
+};
+
+template <int KP>
+__device__ __forceinline__ void wy128_load(double *sV, double *sM, const double *wy, int64_t c) {
+  using C = PairWy128Cfg<KP>;
+  const double *g = wy + c * (2 * 128 * KP);
+  async_tile<128, KP, C::LDV>(sV, g, 128, KP, KP, g);
+  async_tile<KP, 128, C::LD>(sM, g + 128 * KP, KP, 128, 128, g);
+}
+
+template <int KP>
+__global__ void __launch_bounds__(PairWy128Cfg<KP>::THREADS, 1) pair_wy128_kernel(PairArgs A, const double *wy_row,
+                                                                                   const double *wy_col) {
+  using C = PairWy128Cfg<KP>;
+  constexpr int LD = C::LD, LDV = C::LDV, TN = 16;
+  extern __shared__ __align__(16) double sm[];
+  double *sG = sm, *sV = sG + C::G_D, *sM = sV + C::V_D;
+  double *sP = sV;  // KP x LD, after step 1
+  __shared__ __align__(16) PairItem s_it[PAIR_CHUNK_MAX];
+  const Chunk ch = A.chunks[blockIdx.x];
+  stage_items(A.items, ch, s_it);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = lane >> 2, q = lane & 3;
+  const int m0 = warp * 8;
+  const int src_lo = r * 4 + (q >> 1), src_hi = src_lo + 2;
+  async_tile<128, 128, LD>(sG, A.close + s_it[0].g_src[0], s_it[0].nt, s_it[0].ns, A.B, A.chunks);
+  wy128_load<KP>(sV, sM, wy_row, s_it[0].t);
+  cp_commit();
+  for (int p = ch.begin; p < ch.end; p++) {
+    const PairItem &it = s_it[p - ch.begin];
+    cp_wait_all();
+    __syncthreads();
+    // ---- step 1: P = V_t^T G (KP x 128); warp w: columns 8w..8w+7
+    {
+      double pacc[2][KP / 8][2];
+#pragma unroll
+      for (int i = 0; i < KP / 8; i++) pacc[0][i][0] = pacc[0][i][1] = pacc[1][i][0] = pacc[1][i][1] = 0.0;
+#pragma unroll 8
+      for (int k0 = 0; k0 < 128; k0 += 4) {
+        const double b = sG[(k0 + q) * LD + m0 + r];
+#pragma unroll
+        for (int i = 0; i < KP / 8; i++) dmma(pacc[(k0 >> 2) & 1][i], sV[(k0 + q) * LDV + i * 8 + r], b);
+      }
+      __syncthreads();  // every warp is done with V_t: P overwrites it
+#pragma unroll
+      for (int i = 0; i < KP / 8; i++) {
+        sP[(i * 8 + r) * LD + m0 + 2 * q] = pacc[0][i][0] + pacc[1][i][0];
+        sP[(i * 8 + r) * LD + m0 + 2 * q + 1] = pacc[0][i][1] + pacc[1][i][1];
+      }
+    }
+    __syncthreads();
+    // ---- step 2: T1 = G - M_t^T P (rows m0..m0+7 in registers)
+    double H[TN][2];
+#pragma unroll
+    for (int j = 0; j < TN; j++) {
+      H[j][0] = sG[(m0 + r) * LD + j * 8 + 2 * q];
+      H[j][1] = sG[(m0 + r) * LD + j * 8 + 2 * q + 1];
+    }
+#pragma unroll 2
+    for (int k0 = 0; k0 < KP; k0 += 4) {
+      const double a = -sM[(k0 + q) * LD + m0 + r];
+#pragma unroll
+      for (int j = 0; j < TN; j++) dmma(H[j], a, sP[(k0 + q) * LD + j * 8 + r]);
+    }
+    __syncthreads();  // G, P, M_t are dead
+    const bool more = p + 1 < ch.end && !(A.debug & 2);
+    wy128_load<KP>(sV, sM, wy_col, it.s);
+    cp_commit();
+    if (more) {  // G of pair p+1 streams in behind steps 3-4
+      const PairItem &nx = s_it[p + 1 - ch.begin];
+      async_tile<128, 128, LD>(sG, A.close + nx.g_src[0], nx.nt, nx.ns, A.B, A.chunks);
+      cp_commit();
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // V_s / M_s landed
+    } else {
+      cp_wait_all();
+    }
+    __syncthreads();
+    // ---- step 3: R = T1 V_s (8 x KP per warp)
+    double R[2][KP / 8][2];
+#pragma unroll
+    for (int i = 0; i < KP / 8; i++) R[0][i][0] = R[0][i][1] = R[1][i][0] = R[1][i][1] = 0.0;
+#pragma unroll
+    for (int k0 = 0; k0 < 128; k0 += 4) {
+      const int jt = k0 >> 3;
+      const int srcl = (k0 & 4) ? src_hi : src_lo;
+      const double e0 = __shfl_sync(0xffffffffu, H[jt][0], srcl);
+      const double e1 = __shfl_sync(0xffffffffu, H[jt][1], srcl);
+      const double a = (q & 1) ? e1 : e0;
+#pragma unroll
+      for (int i = 0; i < KP / 8; i++) dmma(R[(k0 >> 2) & 1][i], a, sV[(k0 + q) * LDV + i * 8 + r]);
+    }
+#pragma unroll
+    for (int i = 0; i < KP / 8; i++) {
+      R[0][i][0] += R[1][i][0];
+      R[0][i][1] += R[1][i][1];
+    }
+    // ---- step 4: H = T1 - R M_s
+#pragma unroll
+    for (int k0 = 0; k0 < KP; k0 += 4) {
+      const int jt = k0 >> 3;
+      const int srcl = (k0 & 4) ? src_hi : src_lo;
+      const double e0 = __shfl_sync(0xffffffffu, R[0][jt][0], srcl);
+      const double e1 = __shfl_sync(0xffffffffu, R[0][jt][1], srcl);
+      const double a = -((q & 1) ? e1 : e0);
+#pragma unroll
+      for (int j = 0; j < TN; j++) dmma(H[j], a, sM[(k0 + q) * LD + j * 8 + r]);
+    }
+    __syncthreads();  // every warp is done with V_s / M_s
+    if (more) {  // V_t / M_t of the next pair, in flight during the scatter
+      wy128_load<KP>(sV, sM, wy_row, s_it[p + 1 - ch.begin].t);
+      cp_commit();
+    }
+    if (!(A.debug & 1)) {
+      PairDst D;
+      D.s_dst = it.s_dst;
+      D.s_dst_m = it.s_dst_m;
+      D.bb_dst = it.bb_dst;
+      D.yr_dst = it.yr_dst;
+      D.yc_dst = it.yc_dst;
+      D.s_ld = it.s_ld;
+      D.s_ld_m = it.s_ld_m;
+      D.yr_ld = it.yr_ld;
+      D.yc_ld = it.yc_ld;
+      D.nt = it.nt;
+      D.ns = it.ns;
+      D.kt = it.kt;
+      D.ks = it.ks;
+      D.dsym = A.sym && it.s == it.t;
+#pragma unroll
+      for (int j = 0; j < TN; j++) scatter_pair2(A, D, m0, j * 8, m0 + r, j * 8 + 2 * q, H[j][0], H[j][1]);
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
 // Strips (Eq. u1v1): one CTA per column tile (TN columns) of one
 // rotating cluster's panel.  Z = [Y_c1; Y_c2] is gathered from the children's
 // panels (union of their frozen groups), W = Q_q^T Z on the DMMA pipe, then
@@ -1436,9 +1760,9 @@ __global__ void __launch_bounds__(256) csr_cols_kernel(const CsrBlockRow *__rest
 __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const double *__restrict__ q,
                                                        const double *__restrict__ b, int64_t ldb, double *__restrict__ y,
                                                        int64_t ldy, double *__restrict__ zb, int64_t zbl, int nrhs, int B,
-                                                       int *__restrict__ arrive, int64_t leaf0) {
-  __shared__ __align__(16) double sQ[64 * 65];
-  __shared__ double sx[64];
+                                                       int *__restrict__ arrive, int64_t leaf0, int ldq) {
+  extern __shared__ __align__(16) double sQ[];   // n x ldq (ldq = max n + 1 <= 129)
+  __shared__ double sx[128];
   __shared__ int s_go;
   int level = 0;
   int64_t idx = leaf0 + blockIdx.x;  // in-level index (global)
@@ -1447,7 +1771,7 @@ __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const dou
     const int n = sd.n[cl], k = sd.k[cl];
     if (n > 0) {
       const double *Q = q + sd.q_off[cl];
-      for (int e = threadIdx.x; e < n * n; e += blockDim.x) cp8(&sQ[(e / n) * 65 + e % n], Q + e, true);
+      for (int e = threadIdx.x; e < n * n; e += blockDim.x) cp8(&sQ[(e / n) * ldq + e % n], Q + e, true);
       cp_commit();
       int64_t c1 = 0;
       int k1 = 0;
@@ -1468,7 +1792,7 @@ __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const dou
         __syncthreads();
         for (int j = threadIdx.x; j < n; j += blockDim.x) {
           double acc = 0.0;
-          for (int i = 0; i < n; i++) acc = fma(sQ[i * 65 + j], sx[i], acc);
+          for (int i = 0; i < n; i++) acc = fma(sQ[i * ldq + j], sx[i], acc);
           if (j < k) zb[sd.zb_off[cl] + j + r * zbl] = acc;
           else y[sd.loc_off[cl] + (j - k) + r * ldy] = acc;
         }
@@ -1492,10 +1816,10 @@ __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const dou
 
 __global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, const double *__restrict__ q,
                                                       const double *__restrict__ y, int64_t ldy, double *__restrict__ x,
-                                                      int64_t ldx, int nrhs, int B, int64_t leaf0) {
-  __shared__ __align__(16) double sQ[64 * 65];
-  __shared__ double sv[64];
-  __shared__ double sw[64];
+                                                      int64_t ldx, int nrhs, int B, int64_t leaf0, int ldq) {
+  extern __shared__ __align__(16) double sQ[];   // n x ldq (ldq = max n + 1 <= 129)
+  __shared__ double sv[128];
+  __shared__ double sw[128];
   const int64_t leaf = leaf0 + blockIdx.x;
   for (int r = 0; r < nrhs; r++) {
     // walk the path root -> leaf; sv[0:k] holds the basis coefficients from the parent
@@ -1506,7 +1830,7 @@ __global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, const doub
       __syncthreads();
       if (n == 0) continue;
       const double *Q = q + sd.q_off[cl];
-      for (int e = threadIdx.x; e < n * n; e += blockDim.x) cp8(&sQ[(e / n) * 65 + e % n], Q + e, true);
+      for (int e = threadIdx.x; e < n * n; e += blockDim.x) cp8(&sQ[(e / n) * ldq + e % n], Q + e, true);
       cp_commit();
       for (int j = threadIdx.x; j < n; j += blockDim.x)
         if (j >= k) sv[j] = y[sd.loc_off[cl] + (j - k) + r * ldy];
@@ -1515,7 +1839,7 @@ __global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, const doub
       if (level == 0) {
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
           double acc = 0.0;
-          for (int j = 0; j < n; j++) acc = fma(sQ[i * 65 + j], sv[j], acc);
+          for (int j = 0; j < n; j++) acc = fma(sQ[i * ldq + j], sv[j], acc);
           x[((leaf - leaf0) * B + i) + r * ldx] = acc;
         }
       } else {
@@ -1526,7 +1850,7 @@ __global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, const doub
         const int rlo = second ? k1 : 0, rhi = second ? n : k1;
         for (int i = rlo + threadIdx.x; i < rhi; i += blockDim.x) {
           double acc = 0.0;
-          for (int j = 0; j < n; j++) acc = fma(sQ[i * 65 + j], sv[j], acc);
+          for (int j = 0; j < n; j++) acc = fma(sQ[i * ldq + j], sv[j], acc);
           sw[i - rlo] = acc;
         }
         __syncthreads();
@@ -1544,6 +1868,19 @@ __global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, const doub
     cudaError_t e_ = (x);                                                                                \
     if (e_ != cudaSuccess) return fail(H2SP_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
+template <int KP>
+static h2sp_status launch_pairs_wy128(const PairArgs &a, const double *wy_row, const double *wy_col, int64_t nchunks,
+                                      cudaStream_t st) {
+  using C = PairWy128Cfg<KP>;
+  static bool attr = false;
+  if (!attr) {
+    H2SP_CK(cudaFuncSetAttribute(pair_wy128_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
+    attr = true;
+  }
+  pair_wy128_kernel<KP><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a, wy_row, wy_col);
+  H2SP_CK(cudaGetLastError());
+  return H2SP_OK;
+}
 
 template <int NP>
 static h2sp_status launch_pairs(const PairArgs &a, int64_t nchunks, cudaStream_t st) {
@@ -1738,7 +2075,31 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
         nmax = std::max(nmax, int(nn[c]));
         kmax = std::max(kmax, int(kk[c]));
       }
-      if (kmax <= 32) {
+      if (k == 0 && nmax > 64 && wyo && kmax <= 32) {
+        // 128-point leaves: CTA per leaf, rows in registers (compact-WY output only)
+        const int kp = kmax <= 16 ? 16 : 32;
+        const size_t smem = size_t(128 * (kp + 4) + kp * (kp + 4) + kp * (128 + 4)) * sizeof(double);
+        if (kp == 16) {
+          static bool a16 = false;
+          if (!a16) {
+            H2SP_CK(cudaFuncSetAttribute(qr_cta_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            a16 = true;
+          }
+          qr_cta_kernel<16><<<unsigned(M), 128, smem, s>>>(sd, M, leaf, rh, wyo, P->wy_kp, P->wy_n, magic_ptr,
+                                                           P->magic);
+        } else {
+          static bool a32 = false;
+          if (!a32) {
+            H2SP_CK(cudaFuncSetAttribute(qr_cta_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            a32 = true;
+          }
+          qr_cta_kernel<32><<<unsigned(M), 128, smem, s>>>(sd, M, leaf, rh, wyo, P->wy_kp, P->wy_n, magic_ptr,
+                                                           P->magic);
+        }
+        H2SP_CK(cudaGetLastError());
+        return H2SP_OK;
+      }
+      if (kmax <= 32 && nmax <= 64) {
         // 4 independent warps (clusters) per CTA: same per-cluster latency, a quarter of
         // the SM slots taken from the concurrent congruence
         const int wpb = std::max(1, std::min(4, int((96 * 1024) / (size_t(per_warp_reg) * 8))));
@@ -1754,7 +2115,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       attr_ = true;                                                                                        \
     }                                                                                                      \
     qr_reg_kernel<NR_, KP_><<<grid, 32 * wpb, smem, s>>>(sd, L, k, M, per_warp_reg, leaf, tr, rh, qo,        \
-                                                        magic_ptr, P->magic, wyo, P->wy_kp);               \
+                                                        magic_ptr, P->magic, wyo, P->wy_kp, P->wy_n);      \
   } while (0)
         if (nmax <= 32) {
           switch (kp) {
@@ -1777,7 +2138,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       }
       const int wpb = std::max(1, std::min(4, int((96 * 1024) / (size_t(per_warp) * 8))));
       qr_kernel<<<unsigned((M + wpb - 1) / wpb), 32 * wpb, size_t(per_warp) * 8 * wpb, s>>>(
-          sd, L, k, M, per_warp, leaf, tr, rh, qo, magic_ptr, P->magic);
+          sd, L, k, M, per_warp, leaf, tr, rh, qo, magic_ptr, P->magic, wyo, P->wy_kp, P->wy_n);
       H2SP_CK(cudaGetLastError());
       return H2SP_OK;
     };
@@ -1874,10 +2235,16 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     if (h2sp_status e = pre(s1, qform_idx)) return e;
     const int64_t nleaf = int64_t(1) << L;
     const unsigned grid = unsigned(nleaf * (sym ? 1 : 2));
-    if (P->wy_kp == 16)
-      wy_form_q_kernel<16><<<grid, 128, 0, s1>>>(rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf);
-    else
-      wy_form_q_kernel<24><<<grid, 128, 0, s1>>>(rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf);
+    if (P->wy_n == 128) {
+      if (P->wy_kp == 16)
+        launch_wy_form_q<16, 128>(grid, s1, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf);
+      else
+        launch_wy_form_q<32, 128>(grid, s1, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf);
+    } else if (P->wy_kp == 16) {
+      launch_wy_form_q<16, 64>(grid, s1, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf);
+    } else {
+      launch_wy_form_q<24, 64>(grid, s1, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf);
+    }
     H2SP_CK(cudaGetLastError());
     if (h2sp_status e = post(s1, qform_idx)) return e;
   }
@@ -1926,7 +2293,10 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       a.debug = pair_debug;
       if (h2sp_status e = pre(st, li[k].pairs)) return e;
       h2sp_status s;
-      if (k == 0 && P->wy_kp) {
+      if (k == 0 && P->wy_kp && P->wy_n == 128) {
+        s = P->wy_kp == 16 ? launch_pairs_wy128<16>(a, wy_row, wy_col, lp.n_pair_chunks, st)
+                           : launch_pairs_wy128<32>(a, wy_row, wy_col, lp.n_pair_chunks, st);
+      } else if (k == 0 && P->wy_kp) {
         s = P->wy_kp == 16 ? launch_pairs_wy<16>(a, wy_row, wy_col, lp.n_pair_chunks, st)
                            : launch_pairs_wy<24>(a, wy_row, wy_col, lp.n_pair_chunks, st);
       } else switch (pad16(lp.np_pair)) {
@@ -2003,6 +2373,18 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   return H2SP_OK;
 }
 
+// Q tile of the apply kernels: (n_max) x (n_max + 1), n_max = 64 or 128
+static int apply_ldq(const h2sp_plan_s *P) {
+  const int n = P->nmax <= 64 ? 64 : 128;
+  static bool attr = false;
+  if (!attr) {  // both sizes fit the opt-in limit (129 x 128 doubles = 132 KB)
+    cudaFuncSetAttribute(apply_ut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 129 * 8);
+    cudaFuncSetAttribute(apply_v_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 129 * 8);
+    attr = true;
+  }
+  return n + 1;
+}
+
 h2sp_status launch_apply_Ut(const h2sp_plan_s *P, const double *q, const double *b, int64_t ldb, double *y,
                             int64_t ldy, int nrhs, unsigned char *ws, void *stream, bool col_side) {
   cudaStream_t st = (cudaStream_t)stream;
@@ -2012,8 +2394,9 @@ h2sp_status launch_apply_Ut(const h2sp_plan_s *P, const double *q, const double 
   const int64_t zbl = col_side ? P->zb_col_len : P->zb_row_len;
   int *arrive = (int *)(ws + P->meta_bytes + ((size_t(std::max(P->zb_row_len, P->zb_col_len)) * nrhs * 8 + 255) / 256) * 256);
   H2SP_CK(cudaMemsetAsync(arrive, 0, size_t(P->ncl) * sizeof(int), st));
-  apply_ut_kernel<<<unsigned(P->n_leaves_local), 128, 0, st>>>(sd, P->L, q, b, ldb, y, ldy, zb, zbl, nrhs, P->B,
-                                                                 arrive, P->first_leaf);
+  const int ldq = apply_ldq(P);
+  apply_ut_kernel<<<unsigned(P->n_leaves_local), 128, size_t(ldq - 1) * ldq * 8, st>>>(
+      sd, P->L, q, b, ldb, y, ldy, zb, zbl, nrhs, P->B, arrive, P->first_leaf, ldq);
   H2SP_CK(cudaGetLastError());
   return H2SP_OK;
 }
@@ -2023,8 +2406,9 @@ h2sp_status launch_apply_V(const h2sp_plan_s *P, const double *q, const double *
   cudaStream_t st = (cudaStream_t)stream;
   const Clusters cl = make_clusters(P, ws);
   const Side sd = side_of(cl, col_side);
-  apply_v_kernel<<<unsigned(P->n_leaves_local), 128, 0, st>>>(sd, P->L, q, y, ldy, x, ldx, nrhs, P->B,
-                                                               P->first_leaf);
+  const int ldq = apply_ldq(P);
+  apply_v_kernel<<<unsigned(P->n_leaves_local), 128, size_t(ldq - 1) * ldq * 8, st>>>(
+      sd, P->L, q, y, ldy, x, ldx, nrhs, P->B, P->first_leaf, ldq);
   H2SP_CK(cudaGetLastError());
   return H2SP_OK;
 }

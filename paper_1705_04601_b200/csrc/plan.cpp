@@ -162,9 +162,12 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
     };
     local(kr, nr, "row");
     local(kc, nc, "column");
-    for (int64_t c = 0; c < ncl; c++)
-      if (nr[c] > 64 || nc[c] > 64)
-        throw PlanError(H2SP_EUNSUPPORTED, "local size n_t > 64 (kernels are built for B, 2r <= 64)");
+    P->nmax = 0;
+    for (int64_t c = 0; c < ncl; c++) {
+      P->nmax = std::max(P->nmax, std::max(nr[c], nc[c]));
+      if (c < nleaf ? (nr[c] > 128 || nc[c] > 128) : (nr[c] > 64 || nc[c] > 64))
+        throw PlanError(H2SP_EUNSUPPORTED, "local size n_t > 128 at a leaf or > 64 above (kernels are built for B <= 128, 2r <= 64)");
+    }
     // ---- sharding by top-level subtrees: rank g owns cluster g of the
     //      partition level Pl = L - log2(world) and all of its descendants
     int lw = 0;
@@ -799,8 +802,16 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
         int kmx = 0;
         for (int64_t i = 0; i < M; i++) kmx = std::max(kmx, int(std::max(kr[base + i], kc[base + i])));
         P->wy_kp = 0;
-        if (!(flags & H2SP_PLAN_EXPLICIT_Q) && lp.np_pair > 48 && lp.np_pair <= 64 && kmx >= 1 && kmx <= 24)
+        P->wy_n = 64;
+        if (lp.np_pair > 64) {  // 128-point leaves: only the compact-WY kernel exists (k <= 32)
+          if ((flags & H2SP_PLAN_EXPLICIT_Q) || kmx > 32)
+            throw PlanError(H2SP_EUNSUPPORTED, "leaves with n_t > 64 need the compact-WY congruence (k_t <= 32, "
+                                               "no H2SP_PLAN_EXPLICIT_Q)");
+          P->wy_n = 128;
+          P->wy_kp = kmx <= 16 ? 16 : 32;
+        } else if (!(flags & H2SP_PLAN_EXPLICIT_Q) && lp.np_pair > 48 && kmx >= 1 && kmx <= 24) {
           P->wy_kp = kmx <= 16 ? 16 : 24;
+        }
       }
       lp.np_rstrip = round8(npr);
       lp.np_cstrip = round8(npc);
@@ -940,7 +951,7 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
           if (n[c] == 0 || !need[c]) continue;
           li.items++;
           li.flops += 2.0 * n[c] * n[c] * kk[c];
-          li.bytes += 8.0 * (n[c] * n[c] + 2.0 * 64 * P->wy_kp);
+          li.bytes += 8.0 * (n[c] * n[c] + 2.0 * P->wy_n * P->wy_kp);
         }
       }
       P->launch_info.push_back(li);
@@ -983,7 +994,7 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
     P->ws_yc = carve(yc_len);
     P->ws_wy_row = P->ws_wy_col = 0;
     if (P->wy_kp) {
-      const int64_t per = int64_t(2) * 64 * P->wy_kp;
+      const int64_t per = int64_t(2) * P->wy_n * P->wy_kp;
       P->ws_wy_row = carve(per * nleaf);
       P->ws_wy_col = sym ? P->ws_wy_row : carve(per * nleaf);
     }

@@ -70,6 +70,11 @@ CASES += [
     ("cfg2-16384", lambda: h2gen.make_config(2, N=16384)),
     ("cfg3-16384", lambda: h2gen.make_config(3, N=16384)),      # 3-D, r = 24: 48-wide internal tiles
     ("cfg4-16384", lambda: h2gen.make_config(4, N=16384)),      # sphere, general mode, r = 32
+    # 128-point leaves (pair_wy128_kernel, qr_kernel with V / M output, 128-wide apply tiles)
+    ("rand-B128-sym", lambda: h2gen.random_h2(5, 128, 6, True, eta=0.7, max_rank=32)),
+    ("rand-B128-gen", lambda: h2gen.random_h2(5, 128, 5, False, eta=0.7, max_rank=32)),
+    ("rand-B128-gen-k16", lambda: h2gen.random_h2(5, 128, 11, False, eta=0.7, max_rank=16)),
+    ("cfg5-16384", lambda: h2gen.make_config(5, N=16384)),      # config-5 recipe: 3-D, B = 128, r = 32
 ]
 
 
@@ -145,10 +150,10 @@ def test_dense_reconstruction_from_gpu_factors():
     assert np.linalg.norm(U @ S @ V.T - A) / np.linalg.norm(A) <= 1e-12
 
 
-@pytest.mark.parametrize("sym", [True, False])
-def test_apply_parity(sym):
+@pytest.mark.parametrize("sym,B", [(True, 16), (False, 16), (True, 128), (False, 128)])
+def test_apply_parity(sym, B):
     _need_gpu()
-    h = h2gen.random_h2(5, 16, 20 + sym, sym, eta=0.7)
+    h = h2gen.random_h2(5, B, 20 + sym, sym, eta=0.7, max_rank=32)
     plan, sp, out = _run(h)
     res = oracle.sparsify(h)
     rng = np.random.default_rng(3)

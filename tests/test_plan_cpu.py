@@ -30,6 +30,8 @@ def _cases():
     yield "eta0", lambda: h2gen.eta0_h2(3, 4, 0)
     yield "axis-gen", lambda: h2gen.axis_aligned_h2(4, 8, 2, False)
     yield "L0", lambda: h2gen.eta0_h2(0, 16, 0)
+    yield "rand-gen-B128", lambda: h2gen.random_h2(5, 128, 5, False, eta=0.7, max_rank=32)
+    yield "rand-sym-B128", lambda: h2gen.random_h2(5, 128, 6, True, eta=0.7, max_rank=32)
 
 
 CASES = list(_cases())
@@ -110,10 +112,16 @@ def test_plan_rejects_bad_structures():
 
 
 def test_plan_unsupported_leaf_size():
-    h = h2gen.eta0_h2(1, 128, 0)
-    with pytest.raises(h2sp.H2spError) as e:
-        h2sp.Plan(h2gen.pack(h))
-    assert e.value.status == 7
+    """Leaves up to 128 points are supported through the compact-WY level-0
+    congruence only (k <= 32); anything else is H2SP_EUNSUPPORTED (7)."""
+    h2sp.Plan(h2gen.pack(h2gen.eta0_h2(1, 128, 0)))          # B = 128, k = 0: fine
+    cases = [(h2gen.eta0_h2(1, 160, 0), {}),                   # n_t > 128
+             (h2gen.eta0_h2(1, 128, 0), {"explicit_q": True}),  # no explicit-Q kernel for n_t > 64
+             (h2gen.random_h2(5, 128, 1, True, eta=0.7, r=40, ragged=False), {})]  # k_t > 32 at B = 128
+    for h, kw in cases:
+        with pytest.raises(h2sp.H2spError) as e:
+            h2sp.Plan(h2gen.pack(h), **kw)
+        assert e.value.status == 7
 
 
 @pytest.mark.parametrize("name,make", [c for c in CASES if c[0] in ("cfg1", "rand-sym-1", "rand-gen-2", "fig3-half")],
