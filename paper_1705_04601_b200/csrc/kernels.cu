@@ -149,6 +149,23 @@ __device__ __forceinline__ void store2(double *d, double v0, double v1) {
     d[1] = v1;
   }
 }
+// Stores of final S values.  Compiling with -DH2SP_S_STREAM uses the
+// evict-first (streaming) policy for them (they are never re-read by the
+// build); measured 1 % slower on config 2, so plain stores are the default.
+#ifdef H2SP_S_STREAM
+__device__ __forceinline__ void st_s(double *d, double v) { __stcs(d, v); }
+__device__ __forceinline__ void store2_s(double *d, double v0, double v1) {
+  if ((reinterpret_cast<uintptr_t>(d) & 15) == 0) {
+    __stcs(reinterpret_cast<double2 *>(d), make_double2(v0, v1));
+  } else {
+    __stcs(d, v0);
+    __stcs(d + 1, v1);
+  }
+}
+#else
+__device__ __forceinline__ void st_s(double *d, double v) { *d = v; }
+__device__ __forceinline__ void store2_s(double *d, double v0, double v1) { store2(d, v0, v1); }
+#endif
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
@@ -1041,11 +1058,11 @@ __device__ __forceinline__ void scatter_pair2(const PairArgs &A, const PairDst &
   if (row0 + 8 <= D.nt && col0 + 8 <= D.ns && !D.dsym && (r_nn || r_bb) && (c_nn || c_bb)) {
     if (r_nn && c_nn) {
       const int a = row - D.kt, b = col - D.ks;
-      if (D.s_dst >= 0) store2(A.s_val + D.s_dst + int64_t(a) * D.s_ld + b, v0, v1);
+      if (D.s_dst >= 0) store2_s(A.s_val + D.s_dst + int64_t(a) * D.s_ld + b, v0, v1);
       if (D.s_dst_m >= 0 && !(A.debug & 4)) {
         double *d = A.s_val + D.s_dst_m + int64_t(b) * D.s_ld_m + a;
-        d[0] = v0;
-        d[D.s_ld_m] = v1;
+        st_s(d, v0);
+        st_s(d + D.s_ld_m, v1);
       }
     } else if (r_nn) {
       if (D.yc_dst >= 0) {
@@ -1072,12 +1089,12 @@ __device__ __forceinline__ void scatter_pair2(const PairArgs &A, const PairDst &
         const int b = c - D.ks;
         if (D.dsym) {
           if (a <= b) {
-            A.s_val[D.s_dst + int64_t(a) * D.s_ld + b] = v;
-            A.s_val[D.s_dst + int64_t(b) * D.s_ld + a] = v;
+            st_s(A.s_val + D.s_dst + int64_t(a) * D.s_ld + b, v);
+            st_s(A.s_val + D.s_dst + int64_t(b) * D.s_ld + a, v);
           }
         } else {
-          if (D.s_dst >= 0) A.s_val[D.s_dst + int64_t(a) * D.s_ld + b] = v;
-          if (D.s_dst_m >= 0) A.s_val[D.s_dst_m + int64_t(b) * D.s_ld_m + a] = v;
+          if (D.s_dst >= 0) st_s(A.s_val + D.s_dst + int64_t(a) * D.s_ld + b, v);
+          if (D.s_dst_m >= 0) st_s(A.s_val + D.s_dst_m + int64_t(b) * D.s_ld_m + a, v);
         }
       } else if (D.yc_dst >= 0) {
         A.yc[D.yc_dst + int64_t(c) * D.yc_ld + a] = v;
@@ -1694,12 +1711,18 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS) strip_kernel(StripA
         if (T.y_dst >= 0) d = A.y_out + T.y_dst + int64_t(row) * T.y_ld + T.c0 + col;
       } else {
         const int a = row - kq;
-        if (T.s_dst >= 0) d = A.s_val + T.s_dst + int64_t(a) * T.s_ld + T.c0 + col;
+        if (T.s_dst >= 0) {
+          double *ds = A.s_val + T.s_dst + int64_t(a) * T.s_ld + T.c0 + col;
+          if (two)
+            store2_s(ds, v0, v1);
+          else
+            st_s(ds, v0);
+        }
         const int64_t t0 = tdst[col];
-        if (t0 >= 0) A.s_val[t0 + a] = v0;
+        if (t0 >= 0) st_s(A.s_val + t0 + a, v0);
         if (two) {
           const int64_t t1 = tdst[col + 1];
-          if (t1 >= 0) A.s_val[t1 + a] = v1;
+          if (t1 >= 0) st_s(A.s_val + t1 + a, v1);
         }
       }
       if (d) {
