@@ -2231,6 +2231,10 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     const char *e = getenv("H2SP_CSR_AT");
     return e ? atoi(e) : 0;
   }();
+  static const int csr_level = [] {  // H2SP_CSR_AT=2: after the congruence of this level
+    const char *e = getenv("H2SP_CSR_LEVEL");
+    return e ? atoi(e) : 0;
+  }();
   if (csr_at == 0) {
     if (!serial) H2SP_CK(cudaStreamWaitEvent(s2, ev_begin, 0));
     if (h2sp_status e = csr()) return e;
@@ -2284,8 +2288,9 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
                                          s1, !sym))
         return e;
     }
-    H2SP_CK(cudaEventRecord(ev_apply, s1));
   }
+  // everything on s1 (QR chain, level-0 Q formation, applies) joins through ev_apply
+  H2SP_CK(cudaEventRecord(ev_apply, s1));
   for (int k = 0; k <= L; k++) {
     const LevelPlan &lp = P->levels[k];
     if (k > 0) H2SP_CK(cudaStreamWaitEvent(st, ev_ready(k), 0));
@@ -2336,8 +2341,8 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     //      with the whole upper-level congruence chain.  Set 1 (born at a level
     //      >= 1) on s4: it needs the level-(k-1) congruence (its new strips).
     H2SP_CK(cudaEventRecord(ev_pairs(k), st));
-    if (k == 0 && csr_at == 2) {
-      H2SP_CK(cudaStreamWaitEvent(s2, ev_pairs(0), 0));
+    if (k == std::min(csr_level, L) && csr_at == 2) {
+      H2SP_CK(cudaStreamWaitEvent(s2, ev_pairs(k), 0));
       if (h2sp_status e = csr()) return e;
     }
     for (int set = 0; set < 2; set++) {
@@ -2384,7 +2389,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   H2SP_CK(cudaEventRecord(ev_strips1_done, s4));
   // ---- join
   if (L > 0) H2SP_CK(cudaStreamWaitEvent(st, ev_ready(L), 0));
-  if (ap) H2SP_CK(cudaStreamWaitEvent(st, ev_apply, 0));
+  H2SP_CK(cudaStreamWaitEvent(st, ev_apply, 0));
   H2SP_CK(cudaStreamWaitEvent(st, ev_csr, 0));
   H2SP_CK(cudaStreamWaitEvent(st, ev_strips_done, 0));
   H2SP_CK(cudaStreamWaitEvent(st, ev_strips1_done, 0));

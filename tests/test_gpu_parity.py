@@ -281,12 +281,19 @@ def test_virtual_shards_bitwise(name, make, G):
     assert np.all(seen == 1)
 
 
-def test_graph_capture_replay_equals_direct():
+@pytest.mark.parametrize("name,make", [
+    ("rand-B16-sym", lambda: h2gen.random_h2(5, 16, 50, True, eta=0.7)),
+    ("rand-B64-gen-wy", lambda: h2gen.random_h2(4, 64, 51, False, eta=0.7, max_rank=16)),  # compact-WY path
+    ("rand-B128-sym", lambda: h2gen.random_h2(5, 128, 52, True, eta=0.7, max_rank=32)),
+])
+def test_graph_capture_replay_equals_direct(name, make):
     """The whole build (fork/join over the library's side streams) captured in a
-    CUDA graph and replayed gives the direct build's S and Q bitwise."""
+    CUDA graph and replayed gives the direct build's S and Q bitwise; capture
+    also proves every side-stream launch is joined back (an unjoined fork is a
+    capture error)."""
     _need_gpu()
     import paper_1705_04601_b200 as h2sp
-    h = h2gen.random_h2(5, 16, 50, True, eta=0.7)
+    h = make()
     packed = h2gen.pack(h)
     plan = h2sp.Plan(packed)
     sp = h2sp.Sparsifier(plan, packed)
