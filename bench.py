@@ -245,10 +245,19 @@ def main():
     import h2gen
     import paper_1705_04601_b200 as h2sp
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # H2SP_BENCH_SHARED_GPU=1 (plumbing test only): ranks share the visible GPUs
+    # round robin and reduce the timings over gloo (every rank still times its own
+    # independent build; no rank's kernels wait on another's)
+    shared = os.environ.get("H2SP_BENCH_SHARED_GPU") == "1"
+    dev_idx = local_rank % torch.cuda.device_count() if shared else local_rank
+    torch.cuda.set_device(dev_idx)
+    dev = torch.device("cuda", dev_idx)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    red_dev = torch.device("cpu") if shared else dev
 
     shard = args.shard and world > 1
     seed = args.config + (0 if shard else 1000 * rank)
@@ -299,7 +308,7 @@ def main():
     if world > 1:
         dist.barrier()
     ms = t_start.elapsed_time(t_end) / args.steps
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
@@ -346,7 +355,7 @@ def main():
                                 f"cuBLAS DGEMM measured {FP64_DGEMM_TFLOPS}",
                  "hbm_peak_gbs": peaks["hbm_gbs"]})
     # whole-job throughput: the work of every rank (shards: their own flops) / max time
-    fl_t = torch.tensor([step_flops], dtype=torch.float64, device=dev)
+    fl_t = torch.tensor([step_flops], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(fl_t)
     job_flops = float(fl_t.item())
@@ -381,7 +390,7 @@ def main():
             step_e2e()
         e1.record(stream)
         torch.cuda.synchronize()
-        ems = torch.tensor([e0.elapsed_time(e1) / k_e2e], dtype=torch.float64, device=dev)
+        ems = torch.tensor([e0.elapsed_time(e1) / k_e2e], dtype=torch.float64, device=red_dev)
         if world > 1:
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         h2d = sum(int(v.numel()) * v.element_size() for v in host_in.values()) + hb.numel() * 8

@@ -118,11 +118,13 @@ struct LevelPlan {
   int np_row, np_col;    // max n_t at this level (row / column side)
   int mp;                // max strip width at this level
   int64_t n_pairs, n_pair_chunks;
+  int64_t pair_split;    // level 0: chunks of the first half of the leaves (0 = no split)
   int64_t n_coup;
   size_t pairs_off, pair_chunks_off;          // byte offsets in meta
   size_t coup_off;
   struct StripSet {                           // strip panels of one set at this level (tiles = launch size)
     int64_t n_rtiles, n_ctiles;
+    int64_t n_rtiles_a;  // set 0: row tiles of the first half of the clusters (0 = no split)
     size_t rtiles_off, rpanels_off, rgroups_off;
     size_t ctiles_off, cpanels_off, cgroups_off;
   } sp[2];                                    // [0]: groups born at level 0, [1]: born at a level >= 1

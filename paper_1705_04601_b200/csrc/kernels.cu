@@ -1964,7 +1964,8 @@ static h2sp_status launch_strips(const StripArgs &a, int np, int64_t ntiles, cud
 // stream, so a build stays stream-ordered (and CUDA-graph capturable).
 struct DeviceAux {
   bool init = false;
-  cudaStream_t side[5];    // QR/coupling chain, CSR, strips (set 0), main chain, strips (set 1)
+  cudaStream_t side[6];    // QR/coupling chain, CSR, strips (set 0 / first half), main chain, strips (set 1),
+                           // strips (set 0, second half)
   std::vector<cudaEvent_t> ev;
 };
 static DeviceAux g_aux[64];
@@ -1981,14 +1982,19 @@ static h2sp_status get_aux(int L, DeviceAux **out) {
     H2SP_CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     H2SP_CK(cudaStreamCreateWithPriority(&a.side[0], cudaStreamNonBlocking, hi));
     H2SP_CK(cudaStreamCreateWithPriority(&a.side[1], cudaStreamNonBlocking, lo));
-    // priorities: QR/coupling chain (feeds every level) > main chain = strips > CSR
-    const int mid = hi < lo ? hi + 1 : hi;
-    H2SP_CK(cudaStreamCreateWithPriority(&a.side[2], cudaStreamNonBlocking, mid));  // strips
-    H2SP_CK(cudaStreamCreateWithPriority(&a.side[3], cudaStreamNonBlocking, mid));  // main chain
-    H2SP_CK(cudaStreamCreateWithPriority(&a.side[4], cudaStreamNonBlocking, mid));  // strips, set 1
+    // priorities: QR/coupling chain (feeds every level) > main chain = strips > CSR.
+    // H2SP_PRIO="a,b,c" (scheduling experiments): levels below the highest for
+    // strips set 0, main chain, strips set 1 (clamped to the device range)
+    int off[3] = {2, 1, 2};  // main chain above the strips (measured: 1.30 vs 1.31 ms)
+    if (const char *e = getenv("H2SP_PRIO")) sscanf(e, "%d,%d,%d", &off[0], &off[1], &off[2]);
+    auto pr = [&](int o) { return hi < lo ? std::min(lo, hi + o) : hi; };
+    H2SP_CK(cudaStreamCreateWithPriority(&a.side[2], cudaStreamNonBlocking, pr(off[0])));  // strips, set 0
+    H2SP_CK(cudaStreamCreateWithPriority(&a.side[3], cudaStreamNonBlocking, pr(off[1])));  // main chain
+    H2SP_CK(cudaStreamCreateWithPriority(&a.side[4], cudaStreamNonBlocking, pr(off[2])));  // strips, set 1
+    H2SP_CK(cudaStreamCreateWithPriority(&a.side[5], cudaStreamNonBlocking, pr(off[0])));  // strips, set 0 B
     a.init = true;
   }
-  while (int(a.ev.size()) < 3 * L + 12) {
+  while (int(a.ev.size()) < 3 * L + 16) {
     cudaEvent_t e;
     H2SP_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     a.ev.push_back(e);
@@ -2019,7 +2025,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   const int L = P->L;
   DeviceAux *aux = nullptr;
   if (h2sp_status e = get_aux(L, &aux)) return e;
-  cudaStream_t s1 = aux->side[0], s2 = aux->side[1], s3 = aux->side[2], s4 = aux->side[4];
+  cudaStream_t s1 = aux->side[0], s2 = aux->side[1], s3 = aux->side[2], s4 = aux->side[4], s5 = aux->side[5];
   const cudaStream_t user_st = st;
   cudaEvent_t ev_begin = aux->ev[6 + 2 * L], ev_end = aux->ev[7 + 2 * L];
   static const bool serial = [] {
@@ -2027,7 +2033,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     return e && e[0] == '1';
   }();
   if (serial) {
-    s1 = s2 = s3 = s4 = st;
+    s1 = s2 = s3 = s4 = s5 = st;
   } else {
     // the main chain runs on an internal high-priority stream forked from the
     // caller's stream (the CSR stream has the lowest priority and fills gaps)
@@ -2039,6 +2045,8 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   auto ev_ready = [&](int k) { return aux->ev[3 + k]; };   // QR_k and couplings_{k-1} done
   auto ev_pairs = [&](int k) { return aux->ev[4 + L + k]; };  // congruence of level k done (main stream)
   cudaEvent_t ev_strips_done = aux->ev[5 + 2 * L];
+  cudaEvent_t ev_pairs_a = aux->ev[10 + 3 * L], ev_a_last = aux->ev[11 + 3 * L], ev_s5_done = aux->ev[12 + 3 * L];
+  bool a_recorded = false;  // ev_a_last recorded in this build (never wait on a stale record: graph capture)
   // The launch order (and so the index of h2sp_plan_launches / profiling
   // events) is: per level QR row, QR col, couplings, pairs, row strips,
   // column strips; then the CSR expansion.  Events 2i / 2i+1 bracket launch i
@@ -2059,7 +2067,9 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     qr_attr = true;
   }
   // Launch indices are assigned in the plan's canonical order; precompute them.
-  struct LvlIdx { int64_t qr_row = -1, qr_col = -1, coup = -1, pairs = -1, rstr[2] = {-1, -1}, cstr[2] = {-1, -1}; };
+  struct LvlIdx {
+    int64_t qr_row = -1, qr_col = -1, coup = -1, pairs = -1, rstr[2] = {-1, -1}, cstr[2] = {-1, -1}, rstr_b = -1;
+  };
   std::vector<LvlIdx> li(L + 1);
   int64_t csr_idx = -1, qform_idx = -1;
   {
@@ -2072,6 +2082,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       if (lp.n_pairs) li[k].pairs = c++;
       for (int set = 0; set < 2; set++) {
         if (lp.sp[set].n_rtiles) li[k].rstr[set] = c++;
+        if (lp.sp[set].n_rtiles_a) li[k].rstr_b = c++;
         if (lp.sp[set].n_ctiles) li[k].cstr[set] = c++;
       }
     }
@@ -2320,20 +2331,32 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       }();
       a.debug = pair_debug;
       if (h2sp_status e = pre(st, li[k].pairs)) return e;
-      h2sp_status s;
-      if (k == 0 && P->wy_kp && P->wy_n == 128) {
-        s = P->wy_kp == 16 ? launch_pairs_wy128<16>(a, wy_row, wy_col, lp.n_pair_chunks, st)
-                           : launch_pairs_wy128<32>(a, wy_row, wy_col, lp.n_pair_chunks, st);
-      } else if (k == 0 && P->wy_kp) {
-        s = P->wy_kp == 16 ? launch_pairs_wy<16>(a, wy_row, wy_col, lp.n_pair_chunks, st)
-                           : launch_pairs_wy<24>(a, wy_row, wy_col, lp.n_pair_chunks, st);
-      } else switch (pad16(lp.np_pair)) {
-        case 16: s = launch_pairs<16>(a, lp.n_pair_chunks, st); break;
-        case 32: s = launch_pairs<32>(a, lp.n_pair_chunks, st); break;
-        case 48: s = launch_pairs<48>(a, lp.n_pair_chunks, st); break;
-        default: s = launch_pairs<64>(a, lp.n_pair_chunks, st); break;
+      // level 0 may run as two launches (first / second half of the leaves), with
+      // ev_pairs_a recorded in between for the first half's strips
+      const int64_t split = k == 0 ? lp.pair_split : 0;
+      for (int part = 0; part < (split ? 2 : 1); part++) {
+        PairArgs ap_ = a;
+        int64_t nch = lp.n_pair_chunks;
+        if (split) {
+          ap_.chunks = a.chunks + (part ? split : 0);
+          nch = part ? lp.n_pair_chunks - split : split;
+        }
+        h2sp_status s;
+        if (k == 0 && P->wy_kp && P->wy_n == 128) {
+          s = P->wy_kp == 16 ? launch_pairs_wy128<16>(ap_, wy_row, wy_col, nch, st)
+                             : launch_pairs_wy128<32>(ap_, wy_row, wy_col, nch, st);
+        } else if (k == 0 && P->wy_kp) {
+          s = P->wy_kp == 16 ? launch_pairs_wy<16>(ap_, wy_row, wy_col, nch, st)
+                             : launch_pairs_wy<24>(ap_, wy_row, wy_col, nch, st);
+        } else switch (pad16(lp.np_pair)) {
+          case 16: s = launch_pairs<16>(ap_, nch, st); break;
+          case 32: s = launch_pairs<32>(ap_, nch, st); break;
+          case 48: s = launch_pairs<48>(ap_, nch, st); break;
+          default: s = launch_pairs<64>(ap_, nch, st); break;
+        }
+        if (s != H2SP_OK) return s;
+        if (split && part == 0) H2SP_CK(cudaEventRecord(ev_pairs_a, st));
       }
-      if (s != H2SP_OK) return s;
       if (h2sp_status e = post(st, li[k].pairs)) return e;
     }
     // ---- strips arriving from level k-1.  Set 0 (groups born at level 0) on s3:
@@ -2347,10 +2370,15 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     }
     for (int set = 0; set < 2; set++) {
       const LevelPlan::StripSet &sp = lp.sp[set];
-      cudaStream_t ss = set == 0 ? s3 : s4;
+      // set 0 with a split: first half on s3 (needs only the first half of the
+      // level-0 pairs), second half + column strips on s5; unsplit set 0 on s5
+      // too when level 0 was split (its panels may mix both halves)
+      const bool split0 = set == 0 && P->levels[0].pair_split > 0;
+      cudaStream_t ss = set == 0 ? (split0 ? s5 : s3) : s4;
       if (sp.n_rtiles || sp.n_ctiles) {
         H2SP_CK(cudaStreamWaitEvent(ss, ev_pairs(set == 0 ? 0 : k - 1), 0));
         H2SP_CK(cudaStreamWaitEvent(ss, ev_ready(k), 0));
+        if (split0 && a_recorded) H2SP_CK(cudaStreamWaitEvent(ss, ev_a_last, 0));  // children in the first half
       }
       if (sp.n_rtiles) {
         StripArgs a;
@@ -2362,10 +2390,26 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
         a.y_in = yr;
         a.y_out = yr;
         a.s_val = out->s_val;
-        if (h2sp_status e = pre(ss, li[k].rstr[set])) return e;
-        h2sp_status s = launch_strips(a, lp.np_rstrip, sp.n_rtiles, ss);
-        if (s != H2SP_OK) return s;
-        if (h2sp_status e = post(ss, li[k].rstr[set])) return e;
+        const int64_t na = sp.n_rtiles_a;
+        if (na > 0) {
+          H2SP_CK(cudaStreamWaitEvent(s3, ev_pairs_a, 0));
+          H2SP_CK(cudaStreamWaitEvent(s3, ev_ready(k), 0));
+          if (h2sp_status e = pre(s3, li[k].rstr[set])) return e;
+          if (h2sp_status e = launch_strips(a, lp.np_rstrip, na, s3)) return e;
+          if (h2sp_status e = post(s3, li[k].rstr[set])) return e;
+          H2SP_CK(cudaEventRecord(ev_a_last, s3));
+          a_recorded = true;
+          StripArgs b = a;
+          b.tiles = a.tiles + na;
+          if (h2sp_status e = pre(ss, li[k].rstr_b)) return e;
+          if (h2sp_status e = launch_strips(b, lp.np_rstrip, sp.n_rtiles - na, ss)) return e;
+          if (h2sp_status e = post(ss, li[k].rstr_b)) return e;
+        } else {
+          if (h2sp_status e = pre(ss, li[k].rstr[set])) return e;
+          h2sp_status s = launch_strips(a, lp.np_rstrip, sp.n_rtiles, ss);
+          if (s != H2SP_OK) return s;
+          if (h2sp_status e = post(ss, li[k].rstr[set])) return e;
+        }
       }
       if (sp.n_ctiles) {
         StripArgs a;
@@ -2385,6 +2429,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     }
   }
   H2SP_CK(cudaEventRecord(ev_strips_done, s3));
+  H2SP_CK(cudaEventRecord(ev_s5_done, s5));
   cudaEvent_t ev_strips1_done = aux->ev[9 + 2 * L];
   H2SP_CK(cudaEventRecord(ev_strips1_done, s4));
   // ---- join
@@ -2392,6 +2437,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   H2SP_CK(cudaStreamWaitEvent(st, ev_apply, 0));
   H2SP_CK(cudaStreamWaitEvent(st, ev_csr, 0));
   H2SP_CK(cudaStreamWaitEvent(st, ev_strips_done, 0));
+  H2SP_CK(cudaStreamWaitEvent(st, ev_s5_done, 0));
   H2SP_CK(cudaStreamWaitEvent(st, ev_strips1_done, 0));
   if (st != user_st) {
     H2SP_CK(cudaEventRecord(ev_end, st));

@@ -819,10 +819,27 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
       lp.pairs_off = mb.put(pairs[k]);
       auto pc = chunk(pairs[k], [](const PairItem &x) { return x.t; });
       lp.n_pair_chunks = int64_t(pc.size());
+      // split the level-0 congruence and the level-0-born row strips at the middle
+      // of the tree: the strips of the first half only need the first half's pairs
+      // (canonical pairs have their row <= both clusters), so their level chain
+      // starts while the second half of the level-0 congruence still runs
+      static const bool split = !getenv("H2SP_SPLIT") || atoi(getenv("H2SP_SPLIT")) != 0;
+      const bool do_split = split && world == 1 && M >= 2;
+      lp.pair_split = 0;
+      if (k == 0 && do_split) {
+        while (lp.pair_split < int64_t(pc.size()) && pairs[0][pc[lp.pair_split].begin].t < M / 2) lp.pair_split++;
+        if (lp.pair_split == int64_t(pc.size())) lp.pair_split = 0;
+      }
       lp.pair_chunks_off = mb.put(pc);
       for (int set = 0; set < 2; set++) {
         const int sidx = set * (L + 1) + k;
         lp.sp[set].n_rtiles = int64_t(rtil[sidx].size());
+        lp.sp[set].n_rtiles_a = 0;
+        if (set == 0 && do_split && P->levels[0].pair_split > 0) {
+          auto &na = lp.sp[set].n_rtiles_a;
+          while (na < int64_t(rtil[sidx].size()) && rpan[sidx][rtil[sidx][na].panel].q - base < M / 2) na++;
+          if (na == int64_t(rtil[sidx].size())) na = 0;  // nothing left for the second half: no split
+        }
         lp.sp[set].rtiles_off = mb.put(flat_tiles(rtil[sidx], rpan[sidx], true));
         lp.sp[set].rpanels_off = mb.put(rpan[sidx]);
         lp.sp[set].rgroups_off = mb.put(rgrp[sidx]);
@@ -891,9 +908,10 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
       }
       auto strip_info = [&](const std::vector<StripPanel> &pans, const std::vector<StripGroup> &grps,
                             const std::vector<StripTile> &tils, const std::vector<int32_t> &n,
-                            const std::vector<int32_t> &kk, int kind, double qb) {
+                            const std::vector<int32_t> &kk, int kind, double qb, int half) {
         h2sp_launch_info li{kind, k, int64_t(tils.size()), 0.0, qb};
         for (const auto &pn : pans) {
+          if (half >= 0 && (pn.q - base < M / 2) != (half == 0)) continue;
           const int64_t c1 = lvl_off(L, k - 1) + 2 * (pn.q - base);
           const double nq = n[pn.q], kq = kk[pn.q];
           for (int32_t g = pn.gbeg; g < pn.gend; g++) {
@@ -910,13 +928,22 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
       };
       for (int set = 0; set < 2; set++) {
         const int sidx = set * (L + 1) + k;
-        if (lp.sp[set].n_rtiles) {
+        const int64_t na = lp.sp[set].n_rtiles_a;
+        if (na > 0) {  // two launches: first half (A), second half (B)
+          launches += 2;
+          h2sp_launch_info a = strip_info(rpan[sidx], rgrp[sidx], rtil[sidx], nr, kr, 4, qbytes_row / 2, 0);
+          h2sp_launch_info b = strip_info(rpan[sidx], rgrp[sidx], rtil[sidx], nr, kr, 4, qbytes_row / 2, 1);
+          a.items = na;
+          b.items = lp.sp[set].n_rtiles - na;
+          P->launch_info.push_back(a);
+          P->launch_info.push_back(b);
+        } else if (lp.sp[set].n_rtiles) {
           launches++;
-          P->launch_info.push_back(strip_info(rpan[sidx], rgrp[sidx], rtil[sidx], nr, kr, 4, qbytes_row));
+          P->launch_info.push_back(strip_info(rpan[sidx], rgrp[sidx], rtil[sidx], nr, kr, 4, qbytes_row, -1));
         }
         if (lp.sp[set].n_ctiles) {
           launches++;
-          P->launch_info.push_back(strip_info(cpan[sidx], cgrp[sidx], ctil[sidx], nc, kc, 5, qbytes_col));
+          P->launch_info.push_back(strip_info(cpan[sidx], cgrp[sidx], ctil[sidx], nc, kc, 5, qbytes_col, -1));
         }
       }
     }
