@@ -1355,8 +1355,11 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
         const double b = sG[(k0 + q) * LD + m0 + r];
 #pragma unroll
         for (int i = 0; i < KP / 8; i++) dmma(pacc[(k0 >> 2) & 1][i], sVt[(k0 + q) * LDV + i * 8 + r], b);
-        if (k0 / 4 < TN && scat) {
-          const int j = k0 / 4;
+        // one tile of the previous H every (64/4)/TN k-steps: the stores are spread
+        // over the whole product instead of bunched at its start
+        constexpr int EVERY = (64 / 4) / TN;
+        if ((k0 / 4) % EVERY == 0 && scat) {
+          const int j = (k0 / 4) / EVERY;
           scatter_pair2(A, prev, m0, j * 8, m0 + r, j * 8 + 2 * q, H[j][0], H[j][1]);
         }
       }
