@@ -1284,7 +1284,9 @@ struct PairWyCfg {
   static constexpr int WARPS = 8;
   static constexpr int THREADS = WARPS * 32;
   static constexpr int V_D = NP * LDV, M_D = KP * LD, G_D = NP * LD, P_D = KP * LD;
-  static constexpr size_t SMEM = size_t(2 * V_D + 2 * M_D + G_D + P_D) * sizeof(double);
+  // V_s / M_s double-buffered (loaded a whole pair ahead) when two CTAs still fit an SM
+  static constexpr bool DB = size_t(3 * V_D + 3 * M_D + G_D + P_D) * sizeof(double) + 2048 <= 113 * 1024;
+  static constexpr size_t SMEM = size_t((DB ? 3 : 2) * (V_D + M_D) + G_D + P_D) * sizeof(double);
 };
 
 template <int KP>
@@ -1301,9 +1303,9 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
   using C = PairWyCfg<KP>;
   constexpr int LD = C::LD, LDV = C::LDV, TN = 8;
   extern __shared__ __align__(16) double sm[];
-  double *sVt = sm, *sVs = sVt + C::V_D;
-  double *sMt = sVs + C::V_D, *sMs = sMt + C::M_D;
-  double *sG = sMs + C::M_D, *sP = sG + C::G_D;
+  double *sVt = sm, *sMt = sVt + C::V_D;
+  double *sG = sMt + C::M_D, *sP = sG + C::G_D;
+  double *sVM = sP + C::P_D;  // V_s / M_s stage(s), each V_D + M_D
   __shared__ __align__(16) PairItem s_it[PAIR_CHUNK_MAX];
   const Chunk ch = A.chunks[blockIdx.x];
   stage_items(A.items, ch, s_it);
@@ -1314,7 +1316,7 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
   const int m0 = warp * 8;
   wy_load<KP>(sVt, sMt, wy_row, t);
   async_tile<64, 64, LD>(sG, A.close + s_it[0].g_src[0], nt, s_it[0].ns, A.B, A.chunks);
-  wy_load<KP>(sVs, sMs, wy_col, s_it[0].s);
+  wy_load<KP>(sVM, sVM + C::V_D, wy_col, s_it[0].s);
   cp_commit();
   double H[TN][2];
   PairDst prev;
@@ -1330,6 +1332,8 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
     }
     const PairItem &it = s_it[p - ch.begin];
     const int s = it.s;
+    const int stg = C::DB ? ((p - ch.begin) & 1) : 0;
+    double *sVs = sVM + stg * (C::V_D + C::M_D), *sMs = sVs + C::V_D;
     cp_wait_all();
     __syncthreads();
     if (it.t != t) {
@@ -1340,6 +1344,12 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
       cp_commit();
       cp_wait_all();
       __syncthreads();
+    }
+    const bool more = p + 1 < ch.end && !(A.debug & 2);
+    if (C::DB && more) {  // V_s / M_s of pair p+1 into the other stage (free since the barrier above)
+      double *nV = sVM + (stg ^ 1) * (C::V_D + C::M_D);
+      wy_load<KP>(nV, nV + C::V_D, wy_col, s_it[p + 1 - ch.begin].s);
+      cp_commit();
     }
     const bool scat = have_prev && !(A.debug & 1);
     // ---- step 1: P = V_t^T G (KP x 64); warp w computes columns 8w..8w+7,
@@ -1383,7 +1393,6 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
       for (int j = 0; j < TN; j++) dmma(H[j], a, sP[(k0 + q) * LD + j * 8 + r]);
     }
     __syncthreads();  // every warp is done with G and P
-    const bool more = p + 1 < ch.end && !(A.debug & 2);
     if (more) {
       const PairItem &nx = s_it[p + 1 - ch.begin];
       async_tile<64, 64, LD>(sG, A.close + nx.g_src[0], nx.nt, nx.ns, A.B, A.chunks);
@@ -1419,10 +1428,12 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
 #pragma unroll
       for (int j = 0; j < TN; j++) dmma(H[j], a, sMs[(k0 + q) * LD + j * 8 + r]);
     }
-    __syncthreads();  // every warp is done with V_s / M_s
-    if (more) {
-      wy_load<KP>(sVs, sMs, wy_col, s_it[p + 1 - ch.begin].s);
-      cp_commit();
+    if (!C::DB) {
+      __syncthreads();  // every warp is done with V_s / M_s
+      if (more) {
+        wy_load<KP>(sVs, sMs, wy_col, s_it[p + 1 - ch.begin].s);
+        cp_commit();
+      }
     }
     prev.s_dst = it.s_dst;
     prev.s_dst_m = it.s_dst_m;
