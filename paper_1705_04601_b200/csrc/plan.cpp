@@ -835,7 +835,8 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
         const int sidx = set * (L + 1) + k;
         lp.sp[set].n_rtiles = int64_t(rtil[sidx].size());
         lp.sp[set].n_rtiles_a = 0;
-        if (set == 0 && do_split && P->levels[0].pair_split > 0) {
+        static const int split_max = getenv("H2SP_SPLIT_MAXLEVEL") ? atoi(getenv("H2SP_SPLIT_MAXLEVEL")) : 1 << 20;
+        if (set == 0 && do_split && P->levels[0].pair_split > 0 && k <= split_max) {
           auto &na = lp.sp[set].n_rtiles_a;
           while (na < int64_t(rtil[sidx].size()) && rpan[sidx][rtil[sidx][na].panel].q - base < M / 2) na++;
           if (na == int64_t(rtil[sidx].size())) na = 0;  // nothing left for the second half: no split
