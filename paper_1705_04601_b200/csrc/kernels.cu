@@ -1682,19 +1682,34 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS) strip_kernel(StripA
     tdst[cc] = td;
   }
   __syncthreads();
-  // gather Z: each thread keeps one column cc (blockDim.x is a multiple of TN)
-  // and walks its rows; rows of an absent child and rows [n, n4) are zero-filled
+  // gather Z: each thread keeps one column pair (cc, cc + 1) and walks its rows
+  // (blockDim.x is a multiple of TN / 2); a pair contiguous and 16-byte aligned
+  // in a child's panel (the common case: even group widths) is one 16-byte copy.
+  // Rows of an absent child and rows [n, n4) are zero-filled.
   const int n4 = rup(n, 4);
   {
-    const int cc = threadIdx.x % TN, R = blockDim.x / TN;
+    const int cc = 2 * (threadIdx.x % (TN / 2)), R = blockDim.x / (TN / 2);
     const double *b1 = src1[cc] >= 0 ? A.y_in + T.src_c1 + src1[cc] : nullptr;
     const double *b2 = src2[cc] >= 0 ? A.y_in + T.src_c2 + src2[cc] : nullptr;
-    for (int i = threadIdx.x / TN; i < n4; i += R) {
-      const bool first = i < k1;
-      const double *bp = first ? b1 : (i < k1 + k2 ? b2 : nullptr);
-      const double *src = bp ? bp + int64_t(first ? i : i - k1) * (first ? T.ld_c1 : T.ld_c2)
-                             : reinterpret_cast<const double *>(A.tiles);
-      cp8(&sZ[i * C::LDZ + cc], src, bp != nullptr);
+    const double *b1n = src1[cc + 1] >= 0 ? A.y_in + T.src_c1 + src1[cc + 1] : nullptr;
+    const double *b2n = src2[cc + 1] >= 0 ? A.y_in + T.src_c2 + src2[cc + 1] : nullptr;
+    // 16-byte copies need: second column right after the first in the same child
+    // panel, and every row start 16-byte aligned (even ld, even first offset)
+    const bool v1 = b1 && b1n == b1 + 1 && ((reinterpret_cast<uintptr_t>(b1) | (uintptr_t(T.ld_c1) * 8)) & 15) == 0;
+    const bool v2 = b2 && b2n == b2 + 1 && ((reinterpret_cast<uintptr_t>(b2) | (uintptr_t(T.ld_c2) * 8)) & 15) == 0;
+    const void *any = A.tiles;
+    for (int i = threadIdx.x / (TN / 2); i < n4; i += R) {
+      const bool first = i < k1, second = !first && i < k1 + k2;
+      const int64_t off = int64_t(first ? i : i - k1) * (first ? T.ld_c1 : T.ld_c2);
+      const double *p0 = first ? b1 : (second ? b2 : nullptr);
+      const double *p1 = first ? b1n : (second ? b2n : nullptr);
+      double *d = &sZ[i * C::LDZ + cc];
+      if ((first && v1) || (second && v2)) {
+        cp16(d, p0 + off);
+      } else {
+        cp8(d, p0 ? (const void *)(p0 + off) : any, p0 != nullptr);
+        cp8(d + 1, p1 ? (const void *)(p1 + off) : any, p1 != nullptr);
+      }
     }
   }
   cp_commit();
