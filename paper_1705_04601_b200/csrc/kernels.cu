@@ -173,6 +173,11 @@ __device__ __forceinline__ void cp16(void *sdst, const void *gsrc) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc) : "memory");
 }
+// 16 zero bytes into shared memory through the async-copy path (src-size 0)
+__device__ __forceinline__ void cp16_zero(void *sdst, const void *any) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, 0;\n" ::"r"(s), "l"(any) : "memory");
+}
 
 // Asynchronously load an n x m row-major global block (leading dim ldg) into a
 // padded NR x NC shared tile with leading dimension LD, zero fill.  Pairs of
@@ -189,6 +194,8 @@ __device__ __forceinline__ void async_tile(double *s, const double *__restrict__
     const double *src = g + int64_t(i) * ldg + j;
     if (al && v0 && v1) {
       cp16(&s[i * LD + j], src);
+    } else if (!v0 && ((LD & 1) == 0)) {  // both padding (v1 implies v0): one 16-byte zero fill
+      cp16_zero(&s[i * LD + j], any);
     } else {
       cp8(&s[i * LD + j], v0 ? (const void *)src : any, v0);
       cp8(&s[i * LD + j + 1], v1 ? (const void *)(src + 1) : any, v1);
@@ -1706,6 +1713,8 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS) strip_kernel(StripA
       double *d = &sZ[i * C::LDZ + cc];
       if ((first && v1) || (second && v2)) {
         cp16(d, p0 + off);
+      } else if (!p0 && !p1) {
+        cp16_zero(d, any);
       } else {
         cp8(d, p0 ? (const void *)(p0 + off) : any, p0 != nullptr);
         cp8(d + 1, p1 ? (const void *)(p1 + off) : any, p1 != nullptr);
