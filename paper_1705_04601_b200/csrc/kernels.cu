@@ -1781,9 +1781,13 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS) strip_kernel(StripA
 // --------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) csr_cols_kernel(const CsrBlockRow *__restrict__ rows,
                                                        const int32_t *__restrict__ pat, int32_t *__restrict__ col,
-                                                       int splits) {
-  const CsrBlockRow br = rows[blockIdx.x / splits];
-  const int part = blockIdx.x % splits;
+                                                       int splits, int64_t nwork) {
+  // grid-stride over the (block row, part) work items: a capped grid
+  // (H2SP_CSR_GRID) keeps this bandwidth filler from crowding the latency-bound
+  // kernels it overlaps
+  for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+  const CsrBlockRow br = rows[w / splits];
+  const int part = int(w % splits);
   const int rowlen = br.rowlen;
   // this CTA writes whole rows [a0, a1) of the panel: a broadcast copy of the
   // block row's precomputed column pattern
@@ -1806,6 +1810,7 @@ __global__ void __launch_bounds__(256) csr_cols_kernel(const CsrBlockRow *__rest
         if (c0 + p < rowlen) d[p] = v[i];
       }
     }
+  }
   }
 }
 
@@ -2260,9 +2265,12 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
                                 cudaMemcpyDeviceToDevice, s2));
       if (out->s_col) {
         const int splits = 4;
-        csr_cols_kernel<<<unsigned(P->n_csr_rows * splits), 256, 0, s2>>>(
-            (const CsrBlockRow *)(meta + P->csr_rows_off), (const int32_t *)(meta + P->csr_pat_off), out->s_col,
-            splits);
+        static const int64_t grid_cap = getenv("H2SP_CSR_GRID") ? atoll(getenv("H2SP_CSR_GRID")) : 0;
+        const int64_t nwork = P->n_csr_rows * splits;
+        const int64_t grid = grid_cap > 0 ? std::min(grid_cap, nwork) : nwork;
+        csr_cols_kernel<<<unsigned(grid), 256, 0, s2>>>((const CsrBlockRow *)(meta + P->csr_rows_off),
+                                                        (const int32_t *)(meta + P->csr_pat_off), out->s_col, splits,
+                                                        nwork);
         H2SP_CK(cudaGetLastError());
       }
       if (h2sp_status e = post(s2, csr_idx)) return e;
