@@ -1123,13 +1123,6 @@ __device__ __forceinline__ void scatter_pair2(const PairArgs &A, const PairDst &
   }
 }
 
-// Steps (iv)+(ii)+(iii) for one chunk of pairs (t, s_1..s_c) of block row t.
-// Shared memory: Q_t (resident), G, Q_s; G and Q_s of pair p+1 are fetched
-// (cp.async) while pair p computes.  Warp w computes rows [16w, 16w+16) of
-// T = Q_t^T G and keeps them in registers; H = T Q_s takes its A fragments
-// from T by quad shuffles.  The scatter of pair p's H is software-pipelined
-// into the T-GEMM of pair p+1 (one 8x8 tile per k-step), so the stores fill
-// issue slots between DMMAs instead of forming an idle phase.
 // Stage the chunk's work items (<= PAIR_CHUNK_MAX, 144 B each, everything a
 // pair needs precomputed by the plan) into shared memory with one batch of
 // 16-byte async copies: one global round trip per CTA instead of a chain of
@@ -1145,6 +1138,13 @@ __device__ __forceinline__ int stage_items(const PairItem *items, const Chunk &c
   return nit;
 }
 
+// Steps (iv)+(ii)+(iii) for one chunk of pairs (t, s_1..s_c) of block row t.
+// Shared memory: Q_t (resident), G, Q_s; G and Q_s of pair p+1 are fetched
+// (cp.async) while pair p computes.  Warp w computes rows [8w, 8w+8) of
+// T = Q_t^T G and keeps them in registers; H = T Q_s takes its A fragments
+// from T by quad shuffles.  The scatter of pair p's H is software-pipelined
+// into the T-GEMM of pair p+1 (8x8 tiles spread over the k-steps), so the
+// stores fill issue slots between DMMAs instead of forming an idle phase.
 template <int NP>
 __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS) pair_kernel(PairArgs A) {
   using C = PairCfg<NP>;

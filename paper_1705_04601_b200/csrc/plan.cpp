@@ -859,7 +859,7 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
         qbytes_col += 8.0 * nc[base + i] * nc[base + i];
       }
       auto qr_info = [&](const std::vector<int32_t> &n, const std::vector<int32_t> &kk, int kind) {
-        h2sp_launch_info li{kind, k, 0, 0.0, 0.0};
+        h2sp_launch_info li{kind, k, 0, 0.0, 0.0, 0.0};
         const auto &need = (kind == 0) ? need_r : need_c;
         for (int64_t i = 0; i < M; i++) {
           const int64_t c = base + i;
@@ -886,7 +886,7 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
       }
       if (lp.n_coup) {
         launches++;
-        h2sp_launch_info li{2, k, lp.n_coup, 0.0, 0.0};
+        h2sp_launch_info li{2, k, lp.n_coup, 0.0, 0.0, 0.0};
         for (const auto &c : coup[k]) {
           const double a = kr[c.t], b = kc[c.s];
           li.flops += 2 * a * b * (a + b);
@@ -896,7 +896,7 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
       }
       if (lp.n_pairs) {
         launches++;
-        h2sp_launch_info li{3, k, lp.n_pairs, 0.0, qbytes_row + (sym ? 0.0 : qbytes_col)};
+        h2sp_launch_info li{3, k, lp.n_pairs, 0.0, qbytes_row + (sym ? 0.0 : qbytes_col), 0.0};
         for (const auto &it : pairs[k]) {
           const double a = nr[it.t], b = nc[it.s];
           li.flops += 2 * a * b * (a + b);
@@ -910,7 +910,7 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
       auto strip_info = [&](const std::vector<StripPanel> &pans, const std::vector<StripGroup> &grps,
                             const std::vector<StripTile> &tils, const std::vector<int32_t> &n,
                             const std::vector<int32_t> &kk, int kind, double qb, int half) {
-        h2sp_launch_info li{kind, k, int64_t(tils.size()), 0.0, qb};
+        h2sp_launch_info li{kind, k, int64_t(tils.size()), 0.0, qb, 0.0};
         for (const auto &pn : pans) {
           if (half >= 0 && (pn.q - base < M / 2) != (half == 0)) continue;
           const int64_t c1 = lvl_off(L, k - 1) + 2 * (pn.q - base);
@@ -966,11 +966,11 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
     P->rowptr_off = mb.put(rowptr);
     if (P->n_csr_rows) {  // CSR column expansion (+ the rowptr D2D copy)
       launches++;
-      P->launch_info.push_back(h2sp_launch_info{6, L, P->n_csr_rows, 0.0, 4.0 * double(nnz) + 16.0 * double(NR_loc + 1)});
+      P->launch_info.push_back(h2sp_launch_info{6, L, P->n_csr_rows, 0.0, 4.0 * double(nnz) + 16.0 * double(NR_loc + 1), 0.0});
     }
     if (P->wy_kp) {  // level-0 Q formed from V / M (kernels.cu wy_form_q_kernel), after the CSR entry
       launches++;
-      h2sp_launch_info li{7, 0, 0, 0.0, 0.0};
+      h2sp_launch_info li{7, 0, 0, 0.0, 0.0, 0.0};
       for (int side = 0; side < (sym ? 1 : 2); side++) {
         const auto &n = side ? nc : nr;
         const auto &kk = side ? kc : kr;
