@@ -399,3 +399,28 @@ def test_config3_full_size_properties():
     sp.apply_V(z[None, :].contiguous(), w)
     ref = oracle.h2_matvec(h, x)
     assert np.linalg.norm(w.cpu().numpy()[0] - ref) / np.linalg.norm(ref) <= 1e-12
+
+
+def test_config4_general_mode_properties():
+    """BASELINE configs[3] recipe (sphere, general mode U != V, r = B/2) at
+    N = 65536, beyond the oracle's O1 pass: P5 ||S||_F^2 = ||A_H2||_F^2 and the
+    defining identity S y = U^T A_H2 V y (GPU apply_V, the oracle's H^2 matvec,
+    GPU apply_Ut) against a CSR SpMV of the GPU S."""
+    _need_gpu()
+    h = h2gen.make_config(4, N=65536)
+    assert not h.symmetric
+    plan, sp, out = _run(h)
+    nnz = plan.sizes["s_nnz"]
+    v = out["s_val"][:nnz]
+    f = oracle.frobenius_sq(h)
+    fs = sum(float(torch.dot(c, c)) for c in v.split(1 << 30))
+    assert abs(fs - f) / f <= 1e-12
+    y = np.random.default_rng(8).standard_normal(h.N)
+    yt = torch.from_numpy(y[None, :]).cuda()
+    vy = torch.empty_like(yt)
+    sp.apply_V(yt, vy)
+    avy = torch.from_numpy(oracle.h2_matvec(h, vy.cpu().numpy()[0])[None, :]).cuda()
+    lhs = torch.empty_like(yt)
+    sp.apply_Ut(avy, lhs)
+    sy = _csr_spmv(out, nnz, plan.s_rows, yt[0])
+    assert float(torch.linalg.norm(lhs[0] - sy) / torch.linalg.norm(sy)) <= 1e-12
