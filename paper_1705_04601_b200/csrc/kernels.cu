@@ -549,6 +549,8 @@ __global__ void __launch_bounds__(128) qr_reg_kernel(Side sd, int L, int level, 
   for (int idx = lane; idx < K8 * LDT; idx += 32) Tw[idx] = 0.0;
   __syncwarp();
   double *Rg = rh + sd.rh_off[cl];
+  for (int idx = lane; idx < k * k; idx += 32)  // strictly lower triangle of R^ (lane-parallel)
+    if (idx % k < idx / k) Rg[idx] = 0.0;
   // ---- Householder factorisation.  Runtime loop over j with a shifting register
   //      window: x[u][0] is always the current column j, x[u][c] column j + c.
   for (int j = 0; j < k; j++) {
@@ -603,7 +605,6 @@ __global__ void __launch_bounds__(128) qr_reg_kernel(Side sd, int L, int level, 
       const int i = lane + 32 * u;
       if (i >= j && i < n) Vs[i * LDV + j] = v[u];
       if (i == j) {
-        for (int c = 0; c < j; c++) Rg[j * k + c] = 0.0;
         Rg[j * k + j] = beta;
 #pragma unroll
         for (int c = 1; c < KP; c++)
@@ -658,13 +659,19 @@ __global__ void __launch_bounds__(128) qr_reg_kernel(Side sd, int L, int level, 
   if (Wg) {
     // V and M for the compact-WY congruence; Q itself is formed later off the
     // critical path (wy_form_q_kernel)
-    for (int idx = lane; idx < wy_n * wy_kp; idx += 32) {
-      const int i = idx / wy_kp, c = idx - i * wy_kp;
-      Wg[idx] = (i < n && c < k) ? Vs[i * LDV + c] : 0.0;
+    {  // V: row-major wy_n x wy_kp (row / column advanced incrementally, no division)
+      int i = lane / wy_kp, c = lane % wy_kp;
+      for (int idx = lane; idx < wy_n * wy_kp; idx += 32) {
+        Wg[idx] = (i < n && c < k) ? Vs[i * LDV + c] : 0.0;
+        for (c += 32; c >= wy_kp; c -= wy_kp) i++;
+      }
     }
-    for (int idx = lane; idx < wy_n * wy_kp; idx += 32) {
-      const int a = idx / wy_n, c = idx - a * wy_n;
-      Wg[wy_n * wy_kp + idx] = (a < k && c < n) ? Mm[a * LDM + c] : 0.0;
+    {  // M: row-major wy_kp x wy_n
+      int a = lane / wy_n, c = lane % wy_n;
+      for (int idx = lane; idx < wy_n * wy_kp; idx += 32) {
+        Wg[wy_n * wy_kp + idx] = (a < k && c < n) ? Mm[a * LDM + c] : 0.0;
+        for (c += 32; c >= wy_n; c -= wy_n) a++;
+      }
     }
     return;
   }
