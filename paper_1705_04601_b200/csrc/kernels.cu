@@ -1290,6 +1290,9 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS)
 // rows 8w..8w+7 of T1 and H (registers), V_t / M_t resident per block row,
 // G and V_s / M_s reloaded per pair, the previous H scattered during step 1.
 // --------------------------------------------------------------------------
+#ifndef WY_SPLIT
+#define WY_SPLIT 2  // partial sums per tile in the skinny products of pair_wy_kernel
+#endif
 template <int KP>
 struct PairWyCfg {
   static constexpr int NP = 64;
@@ -1371,14 +1374,17 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
     {
       // two partial sums per tile (even / odd k-steps): twice the independent
       // DMMA chains of this skinny product
-      double pacc[2][KP / 8][2];
+      constexpr int NS = WY_SPLIT;  // partial sums per tile (k-steps round robin): independent DMMA chains
+      double pacc[NS][KP / 8][2];
 #pragma unroll
-      for (int i = 0; i < KP / 8; i++) pacc[0][i][0] = pacc[0][i][1] = pacc[1][i][0] = pacc[1][i][1] = 0.0;
+      for (int u = 0; u < NS; u++)
+#pragma unroll
+        for (int i = 0; i < KP / 8; i++) pacc[u][i][0] = pacc[u][i][1] = 0.0;
 #pragma unroll
       for (int k0 = 0; k0 < 64; k0 += 4) {
         const double b = sG[(k0 + q) * LD + m0 + r];
 #pragma unroll
-        for (int i = 0; i < KP / 8; i++) dmma(pacc[(k0 >> 2) & 1][i], sVt[(k0 + q) * LDV + i * 8 + r], b);
+        for (int i = 0; i < KP / 8; i++) dmma(pacc[(k0 >> 2) % NS][i], sVt[(k0 + q) * LDV + i * 8 + r], b);
         // one tile of the previous H every (64/4)/TN k-steps: the stores are spread
         // over the whole product instead of bunched at its start
         constexpr int EVERY = (64 / 4) / TN;
@@ -1389,8 +1395,13 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
       }
 #pragma unroll
       for (int i = 0; i < KP / 8; i++) {
-        sP[(i * 8 + r) * LD + m0 + 2 * q] = pacc[0][i][0] + pacc[1][i][0];
-        sP[(i * 8 + r) * LD + m0 + 2 * q + 1] = pacc[0][i][1] + pacc[1][i][1];
+#pragma unroll
+        for (int u = 1; u < NS; u++) {
+          pacc[0][i][0] += pacc[u][i][0];
+          pacc[0][i][1] += pacc[u][i][1];
+        }
+        sP[(i * 8 + r) * LD + m0 + 2 * q] = pacc[0][i][0];
+        sP[(i * 8 + r) * LD + m0 + 2 * q + 1] = pacc[0][i][1];
       }
     }
     __syncthreads();
@@ -1413,9 +1424,12 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
       cp_commit();
     }
     // ---- step 3: R = T1 V_s (8 x KP per warp), A fragments from the T1 accumulators
-    double R[KP / 8][2], R2[KP / 8][2];
+    constexpr int NS3 = WY_SPLIT;
+    double Rp[NS3][KP / 8][2];
 #pragma unroll
-    for (int i = 0; i < KP / 8; i++) R[i][0] = R[i][1] = R2[i][0] = R2[i][1] = 0.0;
+    for (int u = 0; u < NS3; u++)
+#pragma unroll
+      for (int i = 0; i < KP / 8; i++) Rp[u][i][0] = Rp[u][i][1] = 0.0;
 #pragma unroll
     for (int k0 = 0; k0 < 64; k0 += 4) {
       const int jt = k0 >> 3;
@@ -1424,12 +1438,18 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
       const double e1 = __shfl_sync(0xffffffffu, H[jt][1], srcl);
       const double a = (q & 1) ? e1 : e0;
 #pragma unroll
-      for (int i = 0; i < KP / 8; i++) dmma((k0 & 4) ? R2[i] : R[i], a, sVs[(k0 + q) * LDV + i * 8 + r]);
+      for (int i = 0; i < KP / 8; i++) dmma(Rp[(k0 >> 2) % NS3][i], a, sVs[(k0 + q) * LDV + i * 8 + r]);
     }
+    double R[KP / 8][2];
 #pragma unroll
     for (int i = 0; i < KP / 8; i++) {
-      R[i][0] += R2[i][0];
-      R[i][1] += R2[i][1];
+      R[i][0] = Rp[0][i][0];
+      R[i][1] = Rp[0][i][1];
+#pragma unroll
+      for (int u = 1; u < NS3; u++) {
+        R[i][0] += Rp[u][i][0];
+        R[i][1] += Rp[u][i][1];
+      }
     }
     // ---- step 4: H = T1 - R M_s
 #pragma unroll
