@@ -427,6 +427,12 @@ def main():
                        "job_flops_per_step": job_flops,
                        "hbm_frac_whole_step": plan.sizes["bytes"] / (ms_max * 1e-3) / (peaks["hbm_gbs"] * 1e9),
                        "breakdown_ms": {k: round(v, 4) for k, v in kinds.items()},
+                       # every launch of the step, in-run (concurrent launches share the GPU):
+                       # duration, executed FP64 TFLOP/s and algorithmic GB/s
+                       "per_launch": [{"kind": li["kind"], "level": li["level"], "us": round(per[j] * 1e3, 1),
+                                       "tflops": round(li["flops_exec"] / max(per[j], 1e-9) * 1e-9, 2),
+                                       "gbs": round(li["bytes"] / max(per[j], 1e-9) * 1e-6, 0)}
+                                      for j, li in enumerate(launches)],
                        # the paper's sparsity figures (Fig. 1 nnz/row; §3 Proposition, reading 12:
                        # informational, the printed bound is garbled)
                        "sparsity": {"nnz_per_row": plan.sizes["s_nnz"] / plan.s_rows,
