@@ -2050,7 +2050,9 @@ static h2sp_status get_aux(int L, DeviceAux **out) {
     // up; s2 (CSR index expansion, bandwidth filler) the lowest.
     int lo = 0, hi = 0;
     H2SP_CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    H2SP_CK(cudaStreamCreateWithPriority(&a.side[0], cudaStreamNonBlocking, hi));
+    int qr_off = 0;  // H2SP_PRIO_QR: levels below the highest for the QR / coupling chain
+    if (const char *e = getenv("H2SP_PRIO_QR")) qr_off = atoi(e);
+    H2SP_CK(cudaStreamCreateWithPriority(&a.side[0], cudaStreamNonBlocking, hi < lo ? std::min(lo, hi + qr_off) : hi));
     H2SP_CK(cudaStreamCreateWithPriority(&a.side[1], cudaStreamNonBlocking, lo));
     // priorities: QR/coupling chain (feeds every level) > main chain = strips > CSR.
     // H2SP_PRIO="a,b,c" (scheduling experiments): levels below the highest for
