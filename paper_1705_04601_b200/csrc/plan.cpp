@@ -824,10 +824,15 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
       // (canonical pairs have their row <= both clusters), so their level chain
       // starts while the second half of the level-0 congruence still runs
       static const bool split = !getenv("H2SP_SPLIT") || atoi(getenv("H2SP_SPLIT")) != 0;
-      const bool do_split = split && world == 1 && M >= 2;
+      // first part = leaves [0, lsplit) (H2SP_SPLIT_FRAC of them, default 1/2); at level
+      // k the clusters entirely inside it are p < lsplit >> k
+      static const double frac = getenv("H2SP_SPLIT_FRAC") ? atof(getenv("H2SP_SPLIT_FRAC")) : 0.5;
+      const int64_t lsplit = int64_t(double(int64_t(1) << L) * frac);
+      const int64_t bound = lsplit >> k;
+      const bool do_split = split && world == 1 && M >= 2 && lsplit > 0 && lsplit < (int64_t(1) << L);
       lp.pair_split = 0;
       if (k == 0 && do_split) {
-        while (lp.pair_split < int64_t(pc.size()) && pairs[0][pc[lp.pair_split].begin].t < M / 2) lp.pair_split++;
+        while (lp.pair_split < int64_t(pc.size()) && pairs[0][pc[lp.pair_split].begin].t < bound) lp.pair_split++;
         if (lp.pair_split == int64_t(pc.size())) lp.pair_split = 0;
       }
       lp.pair_chunks_off = mb.put(pc);
@@ -838,7 +843,7 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
         static const int split_max = getenv("H2SP_SPLIT_MAXLEVEL") ? atoi(getenv("H2SP_SPLIT_MAXLEVEL")) : 1 << 20;
         if (set == 0 && do_split && P->levels[0].pair_split > 0 && k <= split_max) {
           auto &na = lp.sp[set].n_rtiles_a;
-          while (na < int64_t(rtil[sidx].size()) && rpan[sidx][rtil[sidx][na].panel].q - base < M / 2) na++;
+          while (na < int64_t(rtil[sidx].size()) && rpan[sidx][rtil[sidx][na].panel].q - base < bound) na++;
           if (na == int64_t(rtil[sidx].size())) na = 0;  // nothing left for the second half: no split
         }
         lp.sp[set].rtiles_off = mb.put(flat_tiles(rtil[sidx], rpan[sidx], true));
@@ -912,7 +917,7 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
                             const std::vector<int32_t> &kk, int kind, double qb, int half) {
         h2sp_launch_info li{kind, k, int64_t(tils.size()), 0.0, qb, 0.0};
         for (const auto &pn : pans) {
-          if (half >= 0 && (pn.q - base < M / 2) != (half == 0)) continue;
+          if (half >= 0 && (pn.q - base < bound) != (half == 0)) continue;
           const int64_t c1 = lvl_off(L, k - 1) + 2 * (pn.q - base);
           const double nq = n[pn.q], kq = kk[pn.q];
           for (int32_t g = pn.gbeg; g < pn.gend; g++) {
