@@ -1,0 +1,125 @@
+"""Direct solve through the factorisation, x = V S^-1 U^T b (Eq. sp0, P:45-49;
+SURVEY §8(f) next #1), on the device.
+
+S is symmetric positive definite when A_H2 is (Proposition) and its
+rows are in level-major frozen order: the leaves' frozen unknowns first, each
+level's after the levels below, so the upper levels play the separators of a
+nested dissection and S is factorised in its own order (no reordering).  The
+sparse Cholesky is cuSOLVER's device low-level API (symbolic analysis, numeric
+factorisation, triangular solves) -- a library call, like cuBLAS, outside the
+sparsification hot path; the applies U^T b and V y are this package's kernels.
+"""
+import ctypes
+import ctypes.util
+
+import torch
+
+from . import Sparsifier
+
+_solver = None
+_sparse = None
+
+
+def _libs():
+    global _solver, _sparse
+    if _solver is None:
+        for name in ("libcusolver.so.11", "libcusolver.so"):
+            try:
+                _solver = ctypes.CDLL(name)
+                break
+            except OSError:
+                continue
+        for name in ("libcusparse.so.12", "libcusparse.so"):
+            try:
+                _sparse = ctypes.CDLL(name)
+                break
+            except OSError:
+                continue
+        if _solver is None or _sparse is None:
+            raise RuntimeError("cuSOLVER / cuSPARSE shared libraries not found")
+    return _solver, _sparse
+
+
+def _ck(st, what):
+    if st != 0:
+        raise RuntimeError(f"{what} failed with status {st}")
+
+
+class SparseCholesky:
+    """S = L L^T of a CSR matrix on the device (int64 row pointers, int32
+    columns, float64 values, all CUDA tensors; full symmetric storage)."""
+
+    def __init__(self, rowptr, col, val, n, stream=None):
+        sv, sp = _libs()
+        vp = ctypes.c_void_p
+        self.n = int(n)
+        self.nnz = int(col.numel())
+        if self.nnz >= 2 ** 31:
+            raise ValueError("cuSOLVER sparse Cholesky takes int32 indices (nnz < 2^31)")
+        self.rp = rowptr.to(torch.int32).contiguous()
+        self.col = col.contiguous()
+        self.val = val.contiguous()
+        self.handle = vp()
+        _ck(sv.cusolverSpCreate(ctypes.byref(self.handle)), "cusolverSpCreate")
+        st = stream if stream is not None else torch.cuda.current_stream()
+        _ck(sv.cusolverSpSetStream(self.handle, vp(st.cuda_stream)), "cusolverSpSetStream")
+        self.descr = vp()
+        _ck(sp.cusparseCreateMatDescr(ctypes.byref(self.descr)), "cusparseCreateMatDescr")
+        self.info = vp()
+        _ck(sv.cusolverSpCreateCsrcholInfo(ctypes.byref(self.info)), "cusolverSpCreateCsrcholInfo")
+        n_, nnz_ = ctypes.c_int(self.n), ctypes.c_int(self.nnz)
+        _ck(sv.cusolverSpXcsrcholAnalysis(self.handle, n_, nnz_, self.descr, vp(self.rp.data_ptr()),
+                                          vp(self.col.data_ptr()), self.info), "cusolverSpXcsrcholAnalysis")
+        internal, work = ctypes.c_size_t(), ctypes.c_size_t()
+        _ck(sv.cusolverSpDcsrcholBufferInfo(self.handle, n_, nnz_, self.descr, vp(self.val.data_ptr()),
+                                            vp(self.rp.data_ptr()), vp(self.col.data_ptr()), self.info,
+                                            ctypes.byref(internal), ctypes.byref(work)),
+            "cusolverSpDcsrcholBufferInfo")
+        self.internal_bytes = int(internal.value)
+        self.buffer = torch.empty(max(1, int(work.value)), dtype=torch.uint8, device=val.device)
+        _ck(sv.cusolverSpDcsrcholFactor(self.handle, n_, nnz_, self.descr, vp(self.val.data_ptr()),
+                                        vp(self.rp.data_ptr()), vp(self.col.data_ptr()), self.info,
+                                        vp(self.buffer.data_ptr())), "cusolverSpDcsrcholFactor")
+        pos = ctypes.c_int(-1)
+        _ck(sv.cusolverSpDcsrcholZeroPivot(self.handle, self.info, ctypes.c_double(0.0), ctypes.byref(pos)),
+            "cusolverSpDcsrcholZeroPivot")
+        if pos.value >= 0:
+            raise RuntimeError(f"S is not positive definite (zero pivot at row {pos.value})")
+
+    def solve(self, b, x=None):
+        """x = S^-1 b for one right-hand side (CUDA float64 vectors of length n)."""
+        sv, _ = _libs()
+        b = b.contiguous()
+        x = torch.empty_like(b) if x is None else x
+        _ck(sv.cusolverSpDcsrcholSolve(self.handle, ctypes.c_int(self.n), ctypes.c_void_p(b.data_ptr()),
+                                       ctypes.c_void_p(x.data_ptr()), self.info, ctypes.c_void_p(self.buffer.data_ptr())),
+            "cusolverSpDcsrcholSolve")
+        return x
+
+    def __del__(self):
+        try:
+            sv, sp = _libs()
+            sv.cusolverSpDestroyCsrcholInfo(self.info)
+            sp.cusparseDestroyMatDescr(self.descr)
+            sv.cusolverSpDestroy(self.handle)
+        except Exception:
+            pass
+
+
+def factor(sp: Sparsifier, plan):
+    """Cholesky of the S the last build wrote into sp.outputs (symmetric plans)."""
+    if not plan.symmetric:
+        raise ValueError("the sparse Cholesky needs a symmetric (SPD) plan")
+    nnz = plan.sizes["s_nnz"]
+    return SparseCholesky(sp.outputs["s_rowptr"], sp.outputs["s_col"][:nnz], sp.outputs["s_val"][:nnz], plan.s_rows)
+
+
+def solve(sp: Sparsifier, chol: SparseCholesky, b):
+    """x = V S^-1 U^T b (Eq. sp0) for one right-hand side b (CUDA float64, length N)."""
+    bt = b.reshape(1, -1).contiguous()
+    y = torch.empty_like(bt)
+    sp.apply_Ut(bt, y)
+    z = chol.solve(y[0]).reshape(1, -1)
+    x = torch.empty_like(bt)
+    sp.apply_V(z, x)
+    return x[0]
