@@ -106,15 +106,64 @@ class SparseCholesky:
             pass
 
 
-def factor(sp: Sparsifier, plan):
-    """Cholesky of the S the last build wrote into sp.outputs (symmetric plans)."""
+def metis_order(rowptr, col, n):
+    """Fill-reducing symmetric order of the pattern (cuSOLVER's host METIS nested
+    dissection); returns the permutation p (new row i = old row p[i]) as int64."""
+    import numpy as np
+    sv, sp_ = _libs()
+    rp = np.ascontiguousarray(rowptr.cpu().numpy().astype(np.int32))
+    cl = np.ascontiguousarray(col.cpu().numpy().astype(np.int32))
+    perm = np.empty(n, dtype=np.int32)
+    h, d = ctypes.c_void_p(), ctypes.c_void_p()
+    _ck(sv.cusolverSpCreate(ctypes.byref(h)), "cusolverSpCreate")
+    _ck(sp_.cusparseCreateMatDescr(ctypes.byref(d)), "cusparseCreateMatDescr")
+    try:
+        _ck(sv.cusolverSpXcsrmetisndHost(h, ctypes.c_int(n), ctypes.c_int(cl.size), d,
+                                         rp.ctypes.data_as(ctypes.c_void_p), cl.ctypes.data_as(ctypes.c_void_p),
+                                         None, perm.ctypes.data_as(ctypes.c_void_p)), "cusolverSpXcsrmetisndHost")
+    finally:
+        sp_.cusparseDestroyMatDescr(d)
+        sv.cusolverSpDestroy(h)
+    return perm.astype(np.int64)
+
+
+class OrderedCholesky:
+    """P^T S P = L L^T with a fill-reducing permutation P (METIS); solve
+    permutes the right-hand side in and the solution back out on the device."""
+
+    def __init__(self, rowptr, col, val, n):
+        import numpy as np
+        import scipy.sparse as sps
+        self.n = int(n)
+        perm = metis_order(rowptr, col, self.n)
+        S = sps.csr_matrix((val.cpu().numpy(), col.cpu().numpy(), rowptr.cpu().numpy()), shape=(self.n, self.n))
+        Sp = S[perm][:, perm].tocsr()
+        Sp.sort_indices()
+        dev = val.device
+        self.p = torch.from_numpy(perm).to(dev)
+        self.chol = SparseCholesky(torch.from_numpy(Sp.indptr.astype(np.int64)).to(dev),
+                                   torch.from_numpy(Sp.indices.astype(np.int32)).to(dev),
+                                   torch.from_numpy(Sp.data).to(dev), self.n)
+        self.internal_bytes = self.chol.internal_bytes
+
+    def solve(self, b, x=None):
+        zp = self.chol.solve(b[self.p].contiguous())
+        x = torch.empty_like(b) if x is None else x
+        x[self.p] = zp
+        return x
+
+
+def factor(sp: Sparsifier, plan, order: str = "s"):
+    """Cholesky of the S the last build wrote into sp.outputs (symmetric plans).
+    order="s": S's own level-major order; "metis": fill-reducing (host METIS)."""
     if not plan.symmetric:
         raise ValueError("the sparse Cholesky needs a symmetric (SPD) plan")
     nnz = plan.sizes["s_nnz"]
-    return SparseCholesky(sp.outputs["s_rowptr"], sp.outputs["s_col"][:nnz], sp.outputs["s_val"][:nnz], plan.s_rows)
+    args = (sp.outputs["s_rowptr"], sp.outputs["s_col"][:nnz], sp.outputs["s_val"][:nnz], plan.s_rows)
+    return OrderedCholesky(*args) if order == "metis" else SparseCholesky(*args)
 
 
-def solve(sp: Sparsifier, chol: SparseCholesky, b):
+def solve(sp: Sparsifier, chol, b):
     """x = V S^-1 U^T b (Eq. sp0) for one right-hand side b (CUDA float64, length N)."""
     bt = b.reshape(1, -1).contiguous()
     y = torch.empty_like(bt)
