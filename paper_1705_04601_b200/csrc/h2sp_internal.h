@@ -16,6 +16,10 @@ namespace h2sp {
 // admissible -> its orthogonalised coupling D~.  "_T" = read the canonical
 // (t <= s) block transposed (symmetric mode).
 constexpr int STRIP_TN = 128;  // columns per strip tile (plan.cpp tiles, kernels.cu strip_kernel TN)
+constexpr int STRIP_TN_SMALL = 64;  // narrower tiles for the small upper-level launches (more CTAs)
+// tile width of the strip launches of level k (H2SP_STRIP_NARROW_FROM: first level
+// with narrow tiles; default: none, measured no gain at levels >= 2, 3 or 4)
+int strip_tn_of_level(int k);
 
 enum GKind : int32_t { G_EMPTY = 0, G_BB = 1, G_BB_T = 2, G_DT = 3, G_DT_T = 4 };
 

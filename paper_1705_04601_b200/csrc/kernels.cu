@@ -2004,28 +2004,35 @@ static h2sp_status launch_pairs_wy(const PairArgs &a, const double *wy_row, cons
 }
 
 
-template <int NP>
+template <int NP, int TN>
 static h2sp_status launch_strips1(const StripArgs &a, int64_t ntiles, cudaStream_t st) {
-  using C = StripCfg<NP, STRIP_TN>;
+  using C = StripCfg<NP, TN>;
   static bool attr = false;
   if (!attr) {
-    H2SP_CK(cudaFuncSetAttribute(strip_kernel<NP, STRIP_TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
+    H2SP_CK(cudaFuncSetAttribute(strip_kernel<NP, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
     attr = true;
   }
-  strip_kernel<NP, STRIP_TN><<<unsigned(ntiles), C::THREADS, C::SMEM, st>>>(a);
+  strip_kernel<NP, TN><<<unsigned(ntiles), C::THREADS, C::SMEM, st>>>(a);
   H2SP_CK(cudaGetLastError());
   return H2SP_OK;
 }
 
 static int pad16(int x) { return x <= 16 ? 16 : x <= 32 ? 32 : x <= 48 ? 48 : 64; }
 
-static h2sp_status launch_strips(const StripArgs &a, int np, int64_t ntiles, cudaStream_t st) {
+template <int TN>
+static h2sp_status launch_strips_tn(const StripArgs &a, int np, int64_t ntiles, cudaStream_t st) {
   switch (pad16(np)) {
-    case 16: return launch_strips1<16>(a, ntiles, st);
-    case 32: return launch_strips1<32>(a, ntiles, st);
-    case 48: return launch_strips1<48>(a, ntiles, st);
-    default: return launch_strips1<64>(a, ntiles, st);
+    case 16: return launch_strips1<16, TN>(a, ntiles, st);
+    case 32: return launch_strips1<32, TN>(a, ntiles, st);
+    case 48: return launch_strips1<48, TN>(a, ntiles, st);
+    default: return launch_strips1<64, TN>(a, ntiles, st);
   }
+}
+
+// tn: the tile width the plan cut this level's panels into (strip_tn_of_level)
+static h2sp_status launch_strips(const StripArgs &a, int np, int tn, int64_t ntiles, cudaStream_t st) {
+  return tn == STRIP_TN_SMALL ? launch_strips_tn<STRIP_TN_SMALL>(a, np, ntiles, st)
+                              : launch_strips_tn<STRIP_TN>(a, np, ntiles, st);
 }
 
 // Side streams and events used to overlap the independent chains of one build
@@ -2470,18 +2477,18 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
           H2SP_CK(cudaStreamWaitEvent(s3, ev_pairs_a, 0));
           H2SP_CK(cudaStreamWaitEvent(s3, ev_ready(k), 0));
           if (h2sp_status e = pre(s3, li[k].rstr[set])) return e;
-          if (h2sp_status e = launch_strips(a, lp.np_rstrip, na, s3)) return e;
+          if (h2sp_status e = launch_strips(a, lp.np_rstrip, lp.mp, na, s3)) return e;
           if (h2sp_status e = post(s3, li[k].rstr[set])) return e;
           H2SP_CK(cudaEventRecord(ev_a_last, s3));
           a_recorded = true;
           StripArgs b = a;
           b.tiles = a.tiles + na;
           if (h2sp_status e = pre(ss, li[k].rstr_b)) return e;
-          if (h2sp_status e = launch_strips(b, lp.np_rstrip, sp.n_rtiles - na, ss)) return e;
+          if (h2sp_status e = launch_strips(b, lp.np_rstrip, lp.mp, sp.n_rtiles - na, ss)) return e;
           if (h2sp_status e = post(ss, li[k].rstr_b)) return e;
         } else {
           if (h2sp_status e = pre(ss, li[k].rstr[set])) return e;
-          h2sp_status s = launch_strips(a, lp.np_rstrip, sp.n_rtiles, ss);
+          h2sp_status s = launch_strips(a, lp.np_rstrip, lp.mp, sp.n_rtiles, ss);
           if (s != H2SP_OK) return s;
           if (h2sp_status e = post(ss, li[k].rstr[set])) return e;
         }
@@ -2497,7 +2504,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
         a.y_out = yc;
         a.s_val = out->s_val;
         if (h2sp_status e = pre(ss, li[k].cstr[set])) return e;
-        h2sp_status s = launch_strips(a, lp.np_cstrip, sp.n_ctiles, ss);
+        h2sp_status s = launch_strips(a, lp.np_cstrip, lp.mp, sp.n_ctiles, ss);
         if (s != H2SP_OK) return s;
         if (h2sp_status e = post(ss, li[k].cstr[set])) return e;
       }

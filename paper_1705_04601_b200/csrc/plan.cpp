@@ -31,6 +31,14 @@ struct PlanError : std::runtime_error {
 };
 
 inline int64_t lvl_off(int L, int k) { return (int64_t(1) << (L + 1)) - (int64_t(1) << (L - k + 1)); }
+}  // namespace
+namespace h2sp {
+int strip_tn_of_level(int k) {
+  static const int from = getenv("H2SP_STRIP_NARROW_FROM") ? atoi(getenv("H2SP_STRIP_NARROW_FROM")) : 1 << 20;
+  return k >= from ? STRIP_TN_SMALL : STRIP_TN;
+}
+}  // namespace h2sp
+namespace {
 inline int level_of(int L, int64_t c) {  // level of level-major cluster id c
   int k = 0;
   while (k < L && c >= lvl_off(L, k + 1)) k++;
@@ -503,10 +511,11 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
           }
           pn.width = col;
           pn.gend = int32_t(grps.size());
-          for (int32_t c0 = 0; c0 < col; c0 += STRIP_TN) {
+          const int tn = strip_tn_of_level(k);
+          for (int32_t c0 = 0; c0 < col; c0 += tn) {
             int32_t g0 = pn.gbeg;
             while (g0 + 1 < pn.gend && grps[g0 + 1].col0 <= c0) g0++;
-            tils.push_back(StripTile{int32_t(pidx), c0, std::min(col, c0 + STRIP_TN), g0});
+            tils.push_back(StripTile{int32_t(pidx), c0, std::min(col, c0 + tn), g0});
           }
           pans.push_back(pn);
         }
@@ -794,7 +803,7 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
       lp.np_row = npr;
       lp.np_col = npc;
       if (npr > 0 || npc > 0) levels_active++;
-      lp.mp = STRIP_TN;
+      lp.mp = strip_tn_of_level(k);
       lp.np_pair = round8(std::max(npr, npc));
       if (k == 0) {
         // compact-WY congruence at level 0 (kernels.cu pair_wy_kernel): n <= 64
