@@ -96,6 +96,15 @@ h2sp_status h2sp_build_host(h2sp_plan P, const h2sp_inputs *hi, const h2sp_outpu
                             const h2sp_outputs *dout, void *ws, size_t ws_bytes, void *stream) {
   if (!P || !hi || !ho || !di || !dout) return fail(H2SP_EINVAL, "NULL argument");
   cudaStream_t st = (cudaStream_t)stream;
+  // value-independent CSR indices: expanded and read back on a side stream that
+  // overlaps the input copies and the build (joined before returning)
+  const bool early = dout->s_col && ho->s_col && dout->s_rowptr && ho->s_rowptr;
+  if (early) {
+    if (h2sp_status s = check_ws(P, ws, ws_bytes, P->ws_total)) return s;
+    if (h2sp_status s = launch_csr_early(P, static_cast<unsigned char *>(ws), dout->s_rowptr, dout->s_col,
+                                         ho->s_rowptr, ho->s_col, stream))
+      return s;
+  }
   auto h2d = [&](const double *d, const double *h, int64_t n) -> h2sp_status {
     if (n == 0) return H2SP_OK;
     if (!d || !h) return fail(H2SP_EINVAL, "NULL input buffer");
@@ -109,7 +118,9 @@ h2sp_status h2sp_build_host(h2sp_plan P, const h2sp_inputs *hi, const h2sp_outpu
   }
   if (h2sp_status s = h2d(di->close, hi->close, P->close_len)) return s;
   if (h2sp_status s = h2d(di->coupling, hi->coupling, P->coupling_len)) return s;
-  if (h2sp_status s = h2sp_build(P, di, dout, ws, ws_bytes, stream)) return s;
+  h2sp_outputs d2 = *dout;
+  if (early) d2.s_col = nullptr, d2.s_rowptr = nullptr;  // already being produced on the side stream
+  if (h2sp_status s = h2sp_build(P, di, &d2, ws, ws_bytes, stream)) return s;
   auto d2h = [&](void *h, const void *d, size_t bytes) -> h2sp_status {
     if (bytes == 0 || !h) return H2SP_OK;
     if (!d) return fail(H2SP_EINVAL, "NULL device output");
@@ -119,6 +130,7 @@ h2sp_status h2sp_build_host(h2sp_plan P, const h2sp_inputs *hi, const h2sp_outpu
   if (!P->sym)
     if (h2sp_status s = d2h(ho->q_col, dout->q_col, size_t(P->q_col_len) * 8)) return s;
   if (h2sp_status s = d2h(ho->s_val, dout->s_val, size_t(P->s_nnz) * 8)) return s;
+  if (early) return launch_csr_early_join(P, stream);
   if (dout->s_col)
     if (h2sp_status s = d2h(ho->s_col, dout->s_col, size_t(P->s_nnz) * 4)) return s;
   if (dout->s_rowptr)

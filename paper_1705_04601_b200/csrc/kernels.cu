@@ -2041,8 +2041,9 @@ static h2sp_status launch_strips(const StripArgs &a, int np, int tn, int64_t nti
 // stream, so a build stays stream-ordered (and CUDA-graph capturable).
 struct DeviceAux {
   bool init = false;
-  cudaStream_t side[6];    // QR/coupling chain, CSR, strips (set 0 / first half), main chain, strips (set 1),
-                           // strips (set 0, second half)
+  cudaStream_t side[7];    // QR/coupling chain, CSR, strips (set 0 / first half), main chain, strips (set 1),
+                           // strips (set 0, second half), h2sp_build_host's early CSR + D2H
+  cudaEvent_t host_fork = nullptr, host_join = nullptr;
   std::vector<cudaEvent_t> ev;
 };
 static DeviceAux g_aux[64];
@@ -2071,6 +2072,9 @@ static h2sp_status get_aux(int L, DeviceAux **out) {
     H2SP_CK(cudaStreamCreateWithPriority(&a.side[3], cudaStreamNonBlocking, pr(off[1])));  // main chain
     H2SP_CK(cudaStreamCreateWithPriority(&a.side[4], cudaStreamNonBlocking, pr(off[2])));  // strips, set 1
     H2SP_CK(cudaStreamCreateWithPriority(&a.side[5], cudaStreamNonBlocking, pr(off[0])));  // strips, set 0 B
+    H2SP_CK(cudaStreamCreateWithPriority(&a.side[6], cudaStreamNonBlocking, lo));  // build_host: early CSR + D2H
+    H2SP_CK(cudaEventCreateWithFlags(&a.host_fork, cudaEventDisableTiming));
+    H2SP_CK(cudaEventCreateWithFlags(&a.host_join, cudaEventDisableTiming));
     a.init = true;
   }
   while (int(a.ev.size()) < 3 * L + 16) {
@@ -2526,6 +2530,41 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     H2SP_CK(cudaStreamWaitEvent(user_st, ev_end, 0));
   }
   if (launches) *launches = nl;
+  return H2SP_OK;
+}
+
+// h2sp_build_host: the CSR index arrays depend on the plan only, so they are
+// expanded and read back to the host on a side stream that starts with the call,
+// overlapping the host-to-device copies of the inputs and the build; the caller
+// joins through launch_csr_early_join after its own work.
+h2sp_status launch_csr_early(const h2sp_plan_s *P, unsigned char *ws, int64_t *d_rowptr, int32_t *d_col,
+                             int64_t *h_rowptr, int32_t *h_col, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  DeviceAux *aux = nullptr;
+  if (h2sp_status e = get_aux(P->L, &aux)) return e;
+  cudaStream_t s = aux->side[6];
+  const unsigned char *meta = ws;
+  H2SP_CK(cudaEventRecord(aux->host_fork, st));
+  H2SP_CK(cudaStreamWaitEvent(s, aux->host_fork, 0));
+  const size_t rp_bytes = size_t(P->n_rows_local + 1) * sizeof(int64_t);
+  if (d_rowptr) H2SP_CK(cudaMemcpyAsync(d_rowptr, meta + P->rowptr_off, rp_bytes, cudaMemcpyDeviceToDevice, s));
+  if (d_col && P->n_csr_rows) {
+    const int splits = 4;
+    const int64_t nwork = P->n_csr_rows * splits;
+    csr_cols_kernel<<<unsigned(nwork), 256, 0, s>>>((const CsrBlockRow *)(meta + P->csr_rows_off),
+                                                    (const int32_t *)(meta + P->csr_pat_off), d_col, splits, nwork);
+    H2SP_CK(cudaGetLastError());
+  }
+  if (h_col && d_col) H2SP_CK(cudaMemcpyAsync(h_col, d_col, size_t(P->s_nnz) * 4, cudaMemcpyDeviceToHost, s));
+  if (h_rowptr && d_rowptr) H2SP_CK(cudaMemcpyAsync(h_rowptr, d_rowptr, rp_bytes, cudaMemcpyDeviceToHost, s));
+  H2SP_CK(cudaEventRecord(aux->host_join, s));
+  return H2SP_OK;
+}
+
+h2sp_status launch_csr_early_join(const h2sp_plan_s *P, void *stream) {
+  DeviceAux *aux = nullptr;
+  if (h2sp_status e = get_aux(P->L, &aux)) return e;
+  H2SP_CK(cudaStreamWaitEvent((cudaStream_t)stream, aux->host_join, 0));
   return H2SP_OK;
 }
 
