@@ -212,7 +212,12 @@ h2sp_status h2sp_plan_upload(h2sp_plan plan, void *ws, size_t ws_bytes, void *st
  * NULL = legacy default stream).  Asynchronous; errors of the launches are
  * returned, faults inside kernels surface at the next synchronising call.
  * ws: device workspace of at least sizes.workspace_bytes bytes, 256-byte
- * aligned, uploaded with h2sp_plan_upload. */
+ * aligned, uploaded with h2sp_plan_upload.
+ * Internally the build forks onto the library's side streams (one set per
+ * device, created on first use) and joins back into `stream` with events, so
+ * it is stream-ordered and CUDA-graph capturable.  Builds issued from several
+ * host threads onto the same device must be serialised by the caller (they
+ * share those side streams and events); different devices are independent. */
 h2sp_status h2sp_build(h2sp_plan plan, const h2sp_inputs *in, const h2sp_outputs *out, void *ws,
                        size_t ws_bytes, void *stream);
 
