@@ -698,17 +698,18 @@ __global__ void __launch_bounds__(128) qr_reg_kernel(Side sd, int L, int level, 
 // convention H; emits R^ and the compact-WY factors V, M = T V^T only (leaves
 // this large always take the compact-WY congruence; wy_form_q_kernel forms Q).
 // --------------------------------------------------------------------------
-template <int KP>
-__global__ void __launch_bounds__(128) qr_cta_kernel(Side sd, int nclust, const double *__restrict__ leaf,
+template <int KP, int NW>
+__global__ void __launch_bounds__(32 * NW) qr_cta_kernel(Side sd, int nclust, const double *__restrict__ leaf,
                                                      double *__restrict__ rh, double *__restrict__ wy, int wy_kp,
                                                      int wy_n, const uint64_t *meta_magic, uint64_t magic) {
   if (meta_magic && threadIdx.x == 0 && blockIdx.x == 0 && *meta_magic != magic) __trap();
-  constexpr int LDV = KP + 4, LDT = KP + 4, LDM = 128 + 4;
+  constexpr int NROW = 32 * NW;  // rows (one per thread)
+  constexpr int LDV = KP + 4, LDT = KP + 4, LDM = NROW + 4;
   extern __shared__ __align__(16) double smc[];
-  double *Vs = smc;              // 128 x LDV (unit lower trapezoidal, zero padded)
-  double *Tw = Vs + 128 * LDV;   // KP x LDT
+  double *Vs = smc;               // NROW x LDV (unit lower trapezoidal, zero padded)
+  double *Tw = Vs + NROW * LDV;   // KP x LDT
   double *Mm = Tw + KP * LDT;    // G = V^T V (KP x KP, ld LDT), then M = T V^T (KP x LDM)
-  __shared__ double red_ss[2][4], red_w[2][4][KP], wsum[KP];
+  __shared__ double red_ss[2][NW], red_w[2][NW][KP], wsum[KP];
   __shared__ double s_alpha[2];
   const int ci = blockIdx.x;
   if (ci >= nclust) return;
@@ -727,7 +728,7 @@ __global__ void __launch_bounds__(128) qr_cta_kernel(Side sd, int nclust, const 
 #pragma unroll
     for (int c = 0; c < KP; c++) x[c] = (tid < n && c < k) ? __ldg(R + int64_t(tid) * k + c) : 0.0;
   }
-  for (int idx = tid; idx < 128 * LDV; idx += blockDim.x) Vs[idx] = 0.0;
+  for (int idx = tid; idx < NROW * LDV; idx += blockDim.x) Vs[idx] = 0.0;
   for (int idx = tid; idx < KP * LDT; idx += blockDim.x) Tw[idx] = 0.0;
   double *Rg = rh + sd.rh_off[cl];
   for (int j = 0; j < k; j++) {
@@ -738,7 +739,9 @@ __global__ void __launch_bounds__(128) qr_cta_kernel(Side sd, int nclust, const 
     if (lane == 0) red_ss[b][warp] = ss;
     if (tid == j) s_alpha[b] = x[0];
     __syncthreads();
-    ss = (red_ss[b][0] + red_ss[b][1]) + (red_ss[b][2] + red_ss[b][3]);
+    ss = 0.0;
+#pragma unroll
+    for (int w_ = 0; w_ < NW; w_++) ss += red_ss[b][w_];
     const double alpha = s_alpha[b];
     const double sigma = sqrt(ss);
     double beta, t;
@@ -765,7 +768,12 @@ __global__ void __launch_bounds__(128) qr_cta_kernel(Side sd, int nclust, const 
         red_w[b][warp][lane] = mine;
       }
       __syncthreads();
-      if (tid < KP) wsum[tid] = (red_w[b][0][tid] + red_w[b][1][tid]) + (red_w[b][2][tid] + red_w[b][3][tid]);
+      if (tid < KP) {
+        double acc_ = 0.0;
+#pragma unroll
+        for (int w_ = 0; w_ < NW; w_++) acc_ += red_w[b][w_][tid];
+        wsum[tid] = acc_;
+      }
       __syncthreads();
 #pragma unroll
       for (int c = 1; c < KP; c++)
@@ -788,10 +796,10 @@ __global__ void __launch_bounds__(128) qr_cta_kernel(Side sd, int nclust, const 
   const int r = lane >> 2, q = lane & 3;
   constexpr int KT = KP / 8;
   // ---- G = V^T V (KP x KP, all tiles; warps take tiles round robin)
-  for (int tile = warp; tile < KT * KT; tile += 4) {
+  for (int tile = warp; tile < KT * KT; tile += NW) {
     const int ta = tile / KT, tb = tile % KT;
     double acc[2] = {0.0, 0.0};
-    for (int k0 = 0; k0 < 128; k0 += 4) dmma(acc, Vs[(k0 + q) * LDV + ta * 8 + r], Vs[(k0 + q) * LDV + tb * 8 + r]);
+    for (int k0 = 0; k0 < NROW; k0 += 4) dmma(acc, Vs[(k0 + q) * LDV + ta * 8 + r], Vs[(k0 + q) * LDV + tb * 8 + r]);
     Mm[(ta * 8 + r) * LDT + tb * 8 + 2 * q] = acc[0];
     Mm[(ta * 8 + r) * LDT + tb * 8 + 2 * q + 1] = acc[1];
   }
@@ -810,8 +818,8 @@ __global__ void __launch_bounds__(128) qr_cta_kernel(Side sd, int nclust, const 
   }
   __syncthreads();
   // ---- M = T V^T (KP x 128) -> Mm (ld LDM); G is dead
-  for (int tile = warp; tile < KT * 16; tile += 4) {
-    const int ta = tile / 16, tc = tile % 16;
+  for (int tile = warp; tile < KT * (NROW / 8); tile += NW) {
+    const int ta = tile / (NROW / 8), tc = tile % (NROW / 8);
     double acc[2] = {0.0, 0.0};
 #pragma unroll
     for (int k0 = 0; k0 < KP; k0 += 4) dmma(acc, Tw[(ta * 8 + r) * LDT + k0 + q], Vs[(tc * 8 + r) * LDV + k0 + q]);
@@ -2192,27 +2200,31 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
         nmax = std::max(nmax, int(nn[c]));
         kmax = std::max(kmax, int(kk[c]));
       }
-      if (k == 0 && nmax > 64 && wyo && kmax <= 32) {
-        // 128-point leaves: CTA per leaf, rows in registers (compact-WY output only)
+      // level 0 on the compact-WY path: one CTA per leaf, one row per thread --
+      // 128-point leaves always; <= 64-point leaves only with H2SP_QR_CTA=1 (measured
+      // slower there than the warp-per-leaf register kernel: 62 vs 52 us alone)
+      static const bool qr_cta64 = getenv("H2SP_QR_CTA") && atoi(getenv("H2SP_QR_CTA")) != 0;
+      if (k == 0 && wyo && kmax <= 32 && (nmax > 64 || qr_cta64)) {
         const int kp = kmax <= 16 ? 16 : 32;
-        const size_t smem = size_t(128 * (kp + 4) + kp * (kp + 4) + kp * (128 + 4)) * sizeof(double);
-        if (kp == 16) {
-          static bool a16 = false;
-          if (!a16) {
-            H2SP_CK(cudaFuncSetAttribute(qr_cta_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-            a16 = true;
-          }
-          qr_cta_kernel<16><<<unsigned(M), 128, smem, s>>>(sd, M, leaf, rh, wyo, P->wy_kp, P->wy_n, magic_ptr,
-                                                           P->magic);
+        const int nw = nmax > 64 ? 4 : 2;
+        const size_t smem = size_t(32 * nw * (kp + 4) + kp * (kp + 4) + kp * (32 * nw + 4)) * sizeof(double);
+#define H2SP_QR_CTA(KP_, NW_)                                                                              \
+  do {                                                                                                     \
+    static bool a_ = false;                                                                                \
+    if (!a_) {                                                                                             \
+      H2SP_CK(cudaFuncSetAttribute(qr_cta_kernel<KP_, NW_>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                   int(smem)));                                                            \
+      a_ = true;                                                                                           \
+    }                                                                                                      \
+    qr_cta_kernel<KP_, NW_><<<unsigned(M), 32 * NW_, smem, s>>>(sd, M, leaf, rh, wyo, P->wy_kp, P->wy_n,   \
+                                                               magic_ptr, P->magic);                      \
+  } while (0)
+        if (nw == 4) {
+          if (kp == 16) H2SP_QR_CTA(16, 4); else H2SP_QR_CTA(32, 4);
         } else {
-          static bool a32 = false;
-          if (!a32) {
-            H2SP_CK(cudaFuncSetAttribute(qr_cta_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-            a32 = true;
-          }
-          qr_cta_kernel<32><<<unsigned(M), 128, smem, s>>>(sd, M, leaf, rh, wyo, P->wy_kp, P->wy_n, magic_ptr,
-                                                           P->magic);
+          if (kp == 16) H2SP_QR_CTA(16, 2); else H2SP_QR_CTA(32, 2);
         }
+#undef H2SP_QR_CTA
         H2SP_CK(cudaGetLastError());
         return H2SP_OK;
       }
