@@ -1,8 +1,10 @@
 // PROTOTYPE (not compiled): warp-specialised level-0 congruence, extracted from
 // paper_1705_04601_b200/csrc/kernels.cu of round 1.  Parity-green with all GPU
-// tests (H2SP_WY_WS=1) but 775 us vs 448 us for pair_wy_kernel<16> alone -- see
-// DESIGN.md §6.  Needs: async_tile / wy_load with a (tid, nthr) thread subset,
-// and the dispatch in launch_build (k == 0 && wy_kp == 16).
+// tests (H2SP_WY_WS=1).  Alone on config 2: 563 us with the even-k fast store
+// pass and setmaxnreg 96/40 (775 us without the fast pass; 370 us with the
+// stores skipped) vs 448 us for pair_wy_kernel<16> -- the 4-warp store group is
+// the bottleneck.  Needs: async_tile / wy_load with a (tid, nthr)
+// thread subset, and the dispatch in launch_build (k == 0 && wy_kp == 16).
 // --------------------------------------------------------------------------
 // Warp-specialised level-0 compact-WY congruence (k <= 16; H2SP_WY_WS=1):
 // 8 DMMA warps compute the pairs of a chunk exactly as pair_wy_kernel, stage
@@ -41,6 +43,33 @@ __device__ __forceinline__ void ws_store_pair(const PairArgs &A, const PairItem 
     }
     return sH[r * LDH + c];
   };
+  if (!dsym && ((kt | ks) & 1) == 0) {
+    // fast pass 1: even k_t, k_s -> a column pair never straddles a region edge;
+    // the lane's column class is fixed, one 16-byte store per row
+    const int c0 = 2 * lane;
+    if (c0 < ns) {
+      const bool two = c0 + 1 < ns;
+      for (int row = sw; row < nt; row += 4) {
+        double *d = nullptr;
+        if (row < kt) {
+          if (c0 < ks) {
+            if (it.bb_dst >= 0) d = A.bb_out + it.bb_dst + row * ks + c0;
+          } else if (it.yr_dst >= 0) {
+            d = A.yr + it.yr_dst + int64_t(row) * it.yr_ld + (c0 - ks);
+          }
+        } else if (c0 >= ks && it.s_dst >= 0) {
+          d = A.s_val + it.s_dst + int64_t(row - kt) * it.s_ld + (c0 - ks);
+        }
+        if (d) {
+          const double v0 = sH[row * LDH + c0];
+          if (two)
+            store2(d, v0, sH[row * LDH + c0 + 1]);
+          else
+            *d = v0;
+        }
+      }
+    }
+  } else
   // pass 1, row-major: lane -> column pair (2 lane, 2 lane + 1)
   for (int row = sw; row < nt; row += 4) {
     const int c0 = 2 * lane;
@@ -99,7 +128,7 @@ __global__ void __launch_bounds__(PairWsCfg::THREADS, 2) pair_wy_ws_kernel(PairA
   if (warp >= 8) {  // ---- store warpgroup
     // the CTA holds 80 registers / thread (2 CTAs x 384 threads); the store group
     // gives 48 back so the DMMA warps can grow to 104: (104 - 80) * 256 == (80 - 32) * 128
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 32;\n");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n");
     const int tid = threadIdx.x - C::MMA_THREADS;
     named_arrive(3, C::THREADS);  // staging buffer starts empty
     for (int p = ch.begin; p < ch.end; p++) {
@@ -109,7 +138,7 @@ __global__ void __launch_bounds__(PairWsCfg::THREADS, 2) pair_wy_ws_kernel(PairA
     }
     return;
   }
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 104;\n");
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 96;\n");
   const int lane = threadIdx.x & 31;
   const int r = lane >> 2, q = lane & 3;
   const int m0 = warp * 8;
