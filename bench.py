@@ -226,6 +226,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-n", type=int, default=16384, help="--impl reference sample size")
     ap.add_argument("--timeline", action="store_true", help="print per-launch start/end of the last step (stderr)")
+    ap.add_argument("--close-gen", action="store_true",
+                    help="matrix-free close blocks (h2sp_close_gen): the level-0 congruence evaluates C_ts from "
+                         "the points instead of reading them (SURVEY 8(d) config-5 protocol step 1)")
     ap.add_argument("--shard", action="store_true",
                     help="N>1: split ONE matrix into N top-level subtree shards (strong scaling) "
                          "instead of N independent matrices (weak scaling, default)")
@@ -261,13 +264,21 @@ def main():
 
     shard = args.shard and world > 1
     seed = args.config + (0 if shard else 1000 * rank)
-    h = h2gen.make_config(args.config, seed=seed, N=args.n)
+    h = h2gen.make_config(args.config, seed=seed, N=args.n, with_close=not args.close_gen)
     packed = h2gen.pack(h)
     t0 = time.perf_counter()
     plan = h2sp.Plan(packed, rank, world) if shard else h2sp.Plan(packed)
     plan_ms = (time.perf_counter() - t0) * 1e3
-    sp = h2sp.Sparsifier(plan, packed, device=dev)
+    gen = {"points": h.points, "kernel": h.meta["kernel"]} if args.close_gen else None
+    sp = h2sp.Sparsifier(plan, packed, device=dev, close_gen=gen)
     launches = plan.launches()
+    close_bytes = 0.0
+    if args.close_gen:   # C_ts is evaluated, not read: drop its 8 B^2 per level-0 pair from the byte counts
+        for li0 in launches:
+            if li0["kind"] == "congruence" and li0["level"] == 0:
+                li0["bytes"] -= li0["items"] * 8.0 * plan.B * plan.B
+                close_bytes += li0["items"] * 8.0 * plan.B * plan.B
+    bytes_step = plan.sizes["bytes"] - close_bytes
     n_launch = len(launches)
     assert n_launch == plan.sizes["launches"]
     nrhs = args.nrhs
@@ -400,7 +411,7 @@ def main():
                "d2h_bytes_per_step": d2h}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_oracle:
+    if rank == 0 and world == 1 and not args.no_oracle and h.close is not None:
         cpu = oracle_baseline(h, plan.sizes["flops"],
                               f"one full oracle pass (sparsify + CSR assembly) of the same matrix "
                               f"(N={plan.N}); build flops only")
@@ -416,16 +427,20 @@ def main():
                        "parallelism": (f"subtree shards x{world} of one matrix (no data-path collective; "
                                        f"Q of halo clusters recomputed per shard)") if shard else
                                       f"replicas x{world} (independent matrices per rank, no collective)",
-                       "l2": "inputs (close blocks %.2f GB) and outputs (S %.2f GB) exceed the 126 MB L2; no flush"
-                             % (plan.sizes["close"] * 8e-9, plan.sizes["s_nnz"] * 12e-9),
+                       "l2": ("inputs (close blocks %.2f GB) and outputs (S %.2f GB) exceed the 126 MB L2; no flush"
+                              % (plan.sizes["close"] * 8e-9, plan.sizes["s_nnz"] * 12e-9)) if not args.close_gen else
+                             ("outputs (S %.2f GB) exceed the 126 MB L2; no flush" % (plan.sizes["s_nnz"] * 12e-9)),
+                       "close": ("matrix-free: C_ts evaluated in the level-0 congruence from the points "
+                                 "(h2sp_close_gen; %.1f GB of close blocks never stored)" % (plan.sizes["close"] * 8e-9))
+                                if args.close_gen else "stored (B x B per near pair, read by the level-0 congruence)",
                        "plan_ms": plan_ms, "s_nnz": plan.sizes["s_nnz"], "s_blocks": plan.sizes["s_blocks"],
-                       "flops_per_step": step_flops, "bytes_per_step": plan.sizes["bytes"],
+                       "flops_per_step": step_flops, "bytes_per_step": bytes_step,
                        "flops_convention": "algorithmic (SURVEY 8(d): explicit-Q congruence 2 n_t n_s (n_t + n_s)); "
                                            "executed_flops_per_step counts what the kernels issue",
                        "executed_flops_per_step": plan.sizes["flops_executed"] + apply_flops,
                        "fp64_frac_of_peak_whole_step": value / world / FP64_PEAK_TFLOPS,
                        "job_flops_per_step": job_flops,
-                       "hbm_frac_whole_step": plan.sizes["bytes"] / (ms_max * 1e-3) / (peaks["hbm_gbs"] * 1e9),
+                       "hbm_frac_whole_step": bytes_step / (ms_max * 1e-3) / (peaks["hbm_gbs"] * 1e9),
                        "breakdown_ms": {k: round(v, 4) for k, v in kinds.items()},
                        # every launch of the step, in-run (concurrent launches share the GPU):
                        # duration, executed FP64 TFLOP/s and algorithmic GB/s

@@ -111,20 +111,47 @@ typedef struct {
   double flops_executed;       /* FP64 flops actually issued (<= flops)        */
 } h2sp_sizes;
 
+/* Matrix-free close blocks ("close_gen" mode, SURVEY §8(d) config-5 protocol
+ * step 1): instead of reading C_ts from `close`, the level-0 congruence
+ * evaluates C_ts[i][j] = K(x_{tB+i}, x_{sB+j}) from the points while it stages
+ * G (P:238-250 with G = C_ts at level 0).  The paper materialises the close
+ * blocks; this mode exists because config 5's 980 GB of close
+ * blocks fit no GPU.  Kernels (r = Euclidean distance, "same" = the same
+ * point, i.e. t == s and i == j):
+ *   H2SP_KERNEL_EXP       exp(-r / p0) + p1 [same]        configs 1, 2, 5
+ *   H2SP_KERNEL_INVSHIFT  1 / (r + p0) + p1 [same]        config 3
+ *   H2SP_KERNEL_LAPLACE   1 / (4 pi r); p1 at [same]      config 4
+ * points: DEVICE, N x dim row-major doubles in tree order (leaf i owns rows
+ * [iB, (i+1)B)), N = B << L (a sharded plan reads its own and its neighbours'
+ * leaves, so pass all N points).  dim in 1..3.  The diagonal blocks are
+ * bitwise symmetric (|x-y| is evaluated from the squared differences). */
+#define H2SP_KERNEL_EXP 1
+#define H2SP_KERNEL_INVSHIFT 2
+#define H2SP_KERNEL_LAPLACE 3
+typedef struct {
+  const double *points;
+  int32_t dim;
+  int32_t kernel;
+  double p0;
+  double p1;
+} h2sp_close_gen;
+
 /* Numeric inputs (DEVICE pointers, read-only, row-major FP64):
  *   leaf_basis_row: R_t of every leaf, B x k_t each, concatenated by leaf.
  *   transfer_row:   T_p of every internal cluster, (k_c1 + k_c2) x k_p each
  *                   (child 1 rows first), concatenated by level-major id.
  *   *_col: the column side (ignored, may be NULL, if symmetric).
- *   close:    C_ts (B x B) per N_0 pair in near_ptr/near_col order.
+ *   close:    C_ts (B x B) per N_0 pair in near_ptr/near_col order (or
+ *             close_gen: the blocks are evaluated on the fly, see above).
  *   coupling: D_b (k_t x k_s) per A_k pair, level-major, CSR order. */
 typedef struct {
   const double *leaf_basis_row;
   const double *transfer_row;
   const double *leaf_basis_col;
   const double *transfer_col;
-  const double *close;
+  const double *close;         /* ignored (may be NULL) when close_gen != NULL  */
   const double *coupling;
+  const h2sp_close_gen *close_gen;  /* HOST pointer to the descriptor, or NULL */
 } h2sp_inputs;
 
 /* Outputs (DEVICE pointers, caller-allocated with the lengths of h2sp_sizes):
@@ -257,7 +284,9 @@ h2sp_status h2sp_build_apply(h2sp_plan plan, const h2sp_inputs *in, const h2sp_o
 /* End-to-end variant with HOST buffers: copies the host inputs into the given
  * device input buffers, builds, and copies every output back into the host
  * output buffers (host pointers should be pinned for overlap).  All copies
- * are cudaMemcpyAsync on `stream`; the call returns after enqueueing them. */
+ * are cudaMemcpyAsync on `stream`; the call returns after enqueueing them.
+ * close_gen mode: host_in->close_gen->points (host) is copied into
+ * dev_in->close_gen->points (device), N * dim doubles. */
 h2sp_status h2sp_build_host(h2sp_plan plan, const h2sp_inputs *host_in, const h2sp_outputs *host_out,
                             const h2sp_inputs *dev_in, const h2sp_outputs *dev_out, void *ws, size_t ws_bytes,
                             void *stream);

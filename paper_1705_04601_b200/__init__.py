@@ -17,7 +17,7 @@ from typing import Dict, Optional
 
 import numpy as np
 
-__all__ = ["LIB_PATH", "H2spError", "Plan", "Sparsifier", "lib", "declared_symbols"]
+__all__ = ["LIB_PATH", "H2spError", "Plan", "Sparsifier", "lib", "declared_symbols", "close_gen_params"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libh2sp.so")
@@ -60,7 +60,28 @@ class _ApplyArgs(ctypes.Structure):
 
 class _Inputs(ctypes.Structure):
     _fields_ = [(n, _vp) for n in ("leaf_basis_row", "transfer_row", "leaf_basis_col", "transfer_col", "close",
-                                   "coupling")]
+                                   "coupling", "close_gen")]
+
+
+class _CloseGen(ctypes.Structure):
+    _fields_ = [("points", _vp), ("dim", _i32), ("kernel", _i32), ("p0", _f64), ("p1", _f64)]
+
+
+KERNEL_IDS = {"exp": 1, "invh": 2, "laplace": 3}   # include/h2sp.h H2SP_KERNEL_*
+
+
+def close_gen_params(kspec: dict):
+    """(kernel id, p0, p1) of include/h2sp.h h2sp_close_gen for a generator
+    kernel spec (h2gen._kernel_spec): exp(-r/ell) + nugget [same];
+    1/(r+h) + diag_add [same]; 1/(4 pi r) with 1/(4 pi h) at the same point."""
+    kind = kspec["kind"]
+    if kind == "exp":
+        return KERNEL_IDS[kind], float(kspec["ell"]), float(kspec["nugget"])
+    if kind == "invh":
+        return KERNEL_IDS[kind], float(kspec["h"]), float(kspec["diag_add"])
+    if kind == "laplace":
+        return KERNEL_IDS[kind], 0.0, 1.0 / (4.0 * np.pi * float(kspec["h"]))
+    raise ValueError(f"no close_gen kernel for {kind!r}")
 
 
 class _Outputs(ctypes.Structure):
@@ -230,7 +251,11 @@ class Sparsifier:
     """Device buffers for one plan: inputs (copied once from a packed dict),
     outputs and the uploaded workspace; ``build()`` runs ``h2sp_build``."""
 
-    def __init__(self, plan: Plan, packed: Optional[dict] = None, device="cuda", alloc_inputs: bool = True):
+    def __init__(self, plan: Plan, packed: Optional[dict] = None, device="cuda", alloc_inputs: bool = True,
+                 close_gen: Optional[dict] = None):
+        """close_gen: {"points": (N, d) tree-ordered array, "kernel": generator
+        kernel spec} -> matrix-free close blocks (h2sp_close_gen); no close
+        buffer is allocated."""
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_1705_04601_b200 needs a CUDA device (no CPU fallback)")
@@ -239,9 +264,19 @@ class Sparsifier:
         sz = plan.sizes
         f64 = dict(dtype=torch.float64, device=self.device)
         self.inputs = {}
+        self._gen = None
+        if close_gen is not None:
+            pts = np.ascontiguousarray(close_gen["points"], dtype=np.float64)
+            if pts.ndim != 2 or pts.shape[0] != int(sz["n"]) or not 1 <= pts.shape[1] <= 3:
+                raise ValueError(f"close_gen points must be (N={int(sz['n'])}, d<=3), got {pts.shape}")
+            kid, p0, p1 = close_gen_params(close_gen["kernel"])
+            self.inputs["points"] = torch.from_numpy(pts).to(self.device)
+            self._gen = _CloseGen(points=self.inputs["points"].data_ptr(), dim=pts.shape[1], kernel=kid, p0=p0, p1=p1)
         if alloc_inputs:
             names = [("leaf_basis_row", "leaf_row", "leaf_row"), ("transfer_row", "transfer_row", "transfer_row"),
-                     ("close", "close", "close"), ("coupling", "coupling", "coupling")]
+                     ("coupling", "coupling", "coupling")]
+            if self._gen is None:
+                names.append(("close", "close", "close"))
             if not plan.symmetric:
                 names += [("leaf_basis_col", "leaf_col", "leaf_col"), ("transfer_col", "transfer_col", "transfer_col")]
             for abi, key, szk in names:
@@ -267,7 +302,10 @@ class Sparsifier:
 
     def _abi_inputs(self, inputs=None):
         src = inputs if inputs is not None else self.inputs
-        return _Inputs(**{k: _dptr(src.get(k)) for k, _ in _Inputs._fields_})
+        a = _Inputs(**{k: _dptr(src.get(k)) for k, _ in _Inputs._fields_ if k != "close_gen"})
+        if self._gen is not None:
+            a.close_gen = ctypes.addressof(self._gen)
+        return a
 
     def _abi_outputs(self, outputs=None):
         o = outputs if outputs is not None else self.outputs
@@ -338,8 +376,14 @@ class Sparsifier:
 
     def build_host(self, host_inputs: dict, host_outputs: dict, stream=None):
         """End-to-end: H2D of host (pinned) inputs, build, D2H of all outputs."""
-        hi = _Inputs(**{k: _dptr(host_inputs.get(k)) for k, _ in _Inputs._fields_})
+        hi = _Inputs(**{k: _dptr(host_inputs.get(k)) for k, _ in _Inputs._fields_ if k != "close_gen"})
         ho = _Outputs(**{k: _dptr(host_outputs.get(k)) for k, _ in _Outputs._fields_})
+        hgen = None
+        if self._gen is not None:   # host points (pinned tensor) -> the device points buffer
+            hp = host_inputs["points"]
+            hgen = _CloseGen(points=_dptr(hp), dim=self._gen.dim, kernel=self._gen.kernel, p0=self._gen.p0,
+                             p1=self._gen.p1)
+            hi.close_gen = ctypes.addressof(hgen)
         _check(lib.h2sp_build_host(self.plan.handle, ctypes.byref(hi), ctypes.byref(ho),
                                    ctypes.byref(self._abi_inputs()), ctypes.byref(self._abi_outputs()), self.ws_ptr,
                                    self.ws_bytes, _stream_handle(stream)), "h2sp_build_host")

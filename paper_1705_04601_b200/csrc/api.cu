@@ -32,6 +32,23 @@ h2sp_status check_device() {
   return H2SP_OK;
 }
 
+h2sp_status check_inputs(const h2sp_plan_s *P, const h2sp_inputs *in) {
+  const h2sp_close_gen *g = in->close_gen;
+  if (g) {
+    if (!g->points) return fail(H2SP_EINVAL, "close_gen: NULL points");
+    if (g->dim < 1 || g->dim > 3) return fail(H2SP_EINVAL, "close_gen: dim must be 1, 2 or 3");
+    if (g->kernel < H2SP_KERNEL_EXP || g->kernel > H2SP_KERNEL_LAPLACE)
+      return fail(H2SP_EINVAL, "close_gen: unknown kernel id " + std::to_string(g->kernel));
+    if (g->kernel == H2SP_KERNEL_EXP && !(g->p0 > 0.0)) return fail(H2SP_EINVAL, "close_gen: exp length p0 <= 0");
+  }
+  if (!in->leaf_basis_row || (P->tr_row_len && !in->transfer_row) || (P->close_len && !in->close && !g) ||
+      (P->coupling_len && !in->coupling))
+    return fail(H2SP_EINVAL, "NULL input array");
+  if (!P->sym && ((P->leaf_col_len && !in->leaf_basis_col) || (P->tr_col_len && !in->transfer_col)))
+    return fail(H2SP_EINVAL, "NULL column-side input array in general mode");
+  return H2SP_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -48,11 +65,7 @@ h2sp_status h2sp_build(h2sp_plan P, const h2sp_inputs *in, const h2sp_outputs *o
                        void *stream) {
   if (!P || !in || !out) return fail(H2SP_EINVAL, "NULL plan, inputs or outputs");
   if (h2sp_status s = check_ws(P, ws, ws_bytes, P->ws_total)) return s;
-  if (!in->leaf_basis_row || (P->tr_row_len && !in->transfer_row) || (P->close_len && !in->close) ||
-      (P->coupling_len && !in->coupling))
-    return fail(H2SP_EINVAL, "NULL input array");
-  if (!P->sym && ((P->leaf_col_len && !in->leaf_basis_col) || (P->tr_col_len && !in->transfer_col)))
-    return fail(H2SP_EINVAL, "NULL column-side input array in general mode");
+  if (h2sp_status s = check_inputs(P, in)) return s;
   if (!out->q_row || !out->s_val || (!P->sym && !out->q_col)) return fail(H2SP_EINVAL, "NULL output array");
   if (h2sp_status s = check_device()) return s;
   int64_t nl = 0;
@@ -64,6 +77,7 @@ h2sp_status h2sp_build_ex(h2sp_plan P, const h2sp_inputs *in, const h2sp_outputs
   if (!P || !in || !out) return fail(H2SP_EINVAL, "NULL plan, inputs or outputs");
   if (events && n_events < 2 * P->launches) return fail(H2SP_EINVAL, "need 2 * launches events");
   if (h2sp_status s = check_ws(P, ws, ws_bytes, P->ws_total)) return s;
+  if (h2sp_status s = check_inputs(P, in)) return s;
   if (!out->q_row || !out->s_val || (!P->sym && !out->q_col)) return fail(H2SP_EINVAL, "NULL output array");
   if (h2sp_status s = check_device()) return s;
   int64_t nl = 0;
@@ -78,6 +92,7 @@ h2sp_status h2sp_build_apply(h2sp_plan P, const h2sp_inputs *in, const h2sp_outp
   if (events && n_events < 2 * P->launches) return fail(H2SP_EINVAL, "need 2 * launches events");
   if (h2sp_status s = check_ws(P, ws, ws_bytes, P->ws_total)) return s;
   if (!out->q_row || !out->s_val || (!P->sym && !out->q_col)) return fail(H2SP_EINVAL, "NULL output array");
+  if (h2sp_status s = check_inputs(P, in)) return s;
   if (ap->ws == ws) return fail(H2SP_EINVAL, "the apply workspace must differ from the build workspace");
   if (ap->nrhs < 1) return fail(H2SP_EINVAL, "nrhs < 1");
   if (h2sp_status s = check_ws(P, ap->ws, ap->ws_bytes, size_t(h2sp_apply_ws_bytes(P, ap->nrhs)))) return s;
@@ -116,7 +131,15 @@ h2sp_status h2sp_build_host(h2sp_plan P, const h2sp_inputs *hi, const h2sp_outpu
     if (h2sp_status s = h2d(di->leaf_basis_col, hi->leaf_basis_col, P->leaf_col_len)) return s;
     if (h2sp_status s = h2d(di->transfer_col, hi->transfer_col, P->tr_col_len)) return s;
   }
-  if (h2sp_status s = h2d(di->close, hi->close, P->close_len)) return s;
+  if (hi->close_gen || di->close_gen) {
+    if (!hi->close_gen || !di->close_gen) return fail(H2SP_EINVAL, "close_gen set on one side only");
+    if (hi->close_gen->dim != di->close_gen->dim) return fail(H2SP_EINVAL, "close_gen: dim differs");
+    if (h2sp_status s = h2d(di->close_gen->points, hi->close_gen->points,
+                            (int64_t(P->B) << P->L) * int64_t(hi->close_gen->dim)))
+      return s;
+  } else if (h2sp_status s = h2d(di->close, hi->close, P->close_len)) {
+    return s;
+  }
   if (h2sp_status s = h2d(di->coupling, hi->coupling, P->coupling_len)) return s;
   h2sp_outputs d2 = *dout;
   if (early) d2.s_col = nullptr, d2.s_rowptr = nullptr;  // already being produced on the side stream

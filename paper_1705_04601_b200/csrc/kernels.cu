@@ -998,6 +998,14 @@ struct PairCfg {
   static constexpr int MIN_BLOCKS = (NP == 64) ? 2 : (NP == 48) ? 3 : 6;  // smem-bound anyway at 48, 64
 };
 
+// Matrix-free close blocks (h2sp_close_gen): pts == nullptr -> read `close`.
+struct CloseGen {
+  const double *pts;
+  int dim, kind;
+  double p0, p1;
+  double q0;  // exp: -1 / p0; Laplace: 1 / (4 pi)
+};
+
 struct PairArgs {
   const PairItem *items;
   const Chunk *chunks;
@@ -1005,11 +1013,79 @@ struct PairArgs {
   int L, level, B;
   int sym;
   const double *close;
+  CloseGen gen;
   const double *bb_in, *dt_in;        // level k-1 results
   const double *q_row, *q_col;
   double *s_val, *bb_out, *yr, *yc;   // yc: transposed column strips (general) / yr (symmetric)
   int debug;                          // H2SP_PAIR_DEBUG (timing attribution only): 1 = skip scatter, 2 = skip loads
 };
+
+// close_gen mode: C_ts[i][j] = K(x_{tB+i}, x_{sB+j}) (include/h2sp.h).  A thread
+// owns column j of the tile (point y_j of s, kept in registers) and evaluates
+// rows i on request.  r^2 is summed without FMA contraction in coordinate
+// order, so r(i, j) == r(j, i) bitwise and diagonal blocks come out symmetric.
+// rsqrt / multiplications by precomputed constants replace sqrt and the
+// divisions (a few ulp from the numpy generator; parity tolerance 1e-13).
+struct GenCol {
+  const double *xt;  // points of t
+  double y0, y1, y2;
+  int j, nt;
+  bool jok, tss;     // column inside the tile; t == s
+};
+
+__device__ __forceinline__ GenCol gen_col(const CloseGen &g, int t, int s, int nt, int ns, int B, int j) {
+  GenCol c;
+  c.j = j;
+  c.nt = nt;
+  c.jok = j < ns;
+  c.tss = t == s;
+  c.xt = g.pts + int64_t(t) * B * g.dim;
+  c.y0 = c.y1 = c.y2 = 0.0;
+  if (c.jok) {
+    const double *ys = g.pts + (int64_t(s) * B + j) * g.dim;
+    c.y0 = __ldg(ys);
+    if (g.dim > 1) c.y1 = __ldg(ys + 1);
+    if (g.dim > 2) c.y2 = __ldg(ys + 2);
+  }
+  return c;
+}
+
+__device__ __forceinline__ double gen_entry(const CloseGen &g, const GenCol &c, int i) {
+  if (!c.jok || i >= c.nt) return 0.0;
+  const double *x = c.xt + i * g.dim;
+  const double d0 = __dsub_rn(__ldg(x), c.y0);
+  double r2 = __dmul_rn(d0, d0);
+  if (g.dim > 1) {
+    const double d1 = __dsub_rn(__ldg(x + 1), c.y1);
+    r2 = __dadd_rn(r2, __dmul_rn(d1, d1));
+  }
+  if (g.dim > 2) {
+    const double d2 = __dsub_rn(__ldg(x + 2), c.y2);
+    r2 = __dadd_rn(r2, __dmul_rn(d2, d2));
+  }
+  const bool same = c.tss && i == c.j;
+  const double ir = rsqrt(r2);                 // +inf at r = 0
+  if (g.kind == H2SP_KERNEL_LAPLACE) return same ? g.p1 : g.q0 * ir;   // q0 = 1 / (4 pi)
+  const double r = r2 > 0.0 ? r2 * ir : 0.0;
+  double v = g.kind == H2SP_KERNEL_EXP ? exp(r * g.q0)                  // q0 = -1 / p0
+                                       : 1.0 / (r + g.p0);
+  return same ? v + g.p1 : v;
+}
+
+template <int NP, int LD>
+__device__ __forceinline__ void gen_close_tile(double *sG, const CloseGen &g, int t, int s, int nt, int ns, int B) {
+  const GenCol c = gen_col(g, t, s, nt, ns, B, threadIdx.x % NP);
+  for (int i = threadIdx.x / NP; i < NP; i += blockDim.x / NP) sG[i * LD + c.j] = gen_entry(g, c, i);
+}
+
+// Level-0 G = C_ts: cp.async copy of the stored block, or evaluated (close_gen).
+template <int NP, int LD>
+__device__ __forceinline__ void load_close(const PairArgs &A, const PairItem &it, double *sG) {
+  if (A.gen.pts)
+    gen_close_tile<NP, LD>(sG, A.gen, it.t, it.s, it.nt, it.ns, A.B);
+  else
+    async_tile<NP, NP, LD>(sG, A.close + it.g_src[0], it.nt, it.ns, A.B, A.chunks);
+}
 
 // Issue the cp.async copies of G_ts (level 0: C_ts; else the 2x2 arrangement of
 // the children's bb parts / D~) into sG.
@@ -1019,7 +1095,7 @@ __device__ __forceinline__ void pair_load_G(const PairArgs &A, const PairItem &i
   const int nt = it.nt, ns = it.ns;
   const void *any = A.chunks;
   if (A.level == 0) {
-    async_tile<NP, NP, LD>(sG, A.close + it.g_src[0], nt, ns, A.B, any);
+    load_close<NP, LD>(A, it, sG);
   } else {
     const int kr0 = it.kr0, kr1 = it.kr1;
     const int kc0 = it.kc0, kc1 = it.kc1;
@@ -1340,7 +1416,7 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
   const int r = lane >> 2, q = lane & 3;
   const int m0 = warp * 8;
   wy_load<KP>(sVt, sMt, wy_row, t);
-  async_tile<64, 64, LD>(sG, A.close + s_it[0].g_src[0], nt, s_it[0].ns, A.B, A.chunks);
+  load_close<64, LD>(A, s_it[0], sG);
   wy_load<KP>(sVM, sVM + C::V_D, wy_col, s_it[0].s);
   cp_commit();
   double H[TN][2];
@@ -1426,10 +1502,17 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
       for (int j = 0; j < TN; j++) dmma(H[j], a, sP[(k0 + q) * LD + j * 8 + r]);
     }
     __syncthreads();  // every warp is done with G and P
+    // close_gen: G of pair p+1 is evaluated during step 3 (one row per k-step)
+    const bool gnext = more && A.gen.pts != nullptr;
+    GenCol gc;
     if (more) {
       const PairItem &nx = s_it[p + 1 - ch.begin];
-      async_tile<64, 64, LD>(sG, A.close + nx.g_src[0], nx.nt, nx.ns, A.B, A.chunks);
-      cp_commit();
+      if (gnext) {
+        gc = gen_col(A.gen, nx.t, nx.s, nx.nt, nx.ns, A.B, threadIdx.x & 63);
+      } else {
+        async_tile<64, 64, LD>(sG, A.close + nx.g_src[0], nx.nt, nx.ns, A.B, A.chunks);
+        cp_commit();
+      }
     }
     // ---- step 3: R = T1 V_s (8 x KP per warp), A fragments from the T1 accumulators
     constexpr int NS3 = WY_SPLIT;
@@ -1447,6 +1530,10 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
       const double a = (q & 1) ? e1 : e0;
 #pragma unroll
       for (int i = 0; i < KP / 8; i++) dmma(Rp[(k0 >> 2) % NS3][i], a, sVs[(k0 + q) * LDV + i * 8 + r]);
+      if (gnext) {  // 256 threads x 16 k-steps = the 64 x 64 entries
+        const int gi = (threadIdx.x >> 6) + 4 * (k0 >> 2);
+        sG[gi * LD + gc.j] = gen_entry(A.gen, gc, gi);
+      }
     }
     double R[KP / 8][2];
 #pragma unroll
@@ -1538,7 +1625,7 @@ __global__ void __launch_bounds__(PairWy128Cfg<KP>::THREADS, 1) pair_wy128_kerne
   const int r = lane >> 2, q = lane & 3;
   const int m0 = warp * 8;
   const int src_lo = r * 4 + (q >> 1), src_hi = src_lo + 2;
-  async_tile<128, 128, LD>(sG, A.close + s_it[0].g_src[0], s_it[0].nt, s_it[0].ns, A.B, A.chunks);
+  load_close<128, LD>(A, s_it[0], sG);
   wy128_load<KP>(sV, sM, wy_row, s_it[0].t);
   cp_commit();
   for (int p = ch.begin; p < ch.end; p++) {
@@ -1579,9 +1666,11 @@ __global__ void __launch_bounds__(PairWy128Cfg<KP>::THREADS, 1) pair_wy128_kerne
     }
     __syncthreads();  // G, P, M_t are dead
     const bool more = p + 1 < ch.end && !(A.debug & 2);
+    // close_gen: G of pair p+1 is evaluated during step 3 (one row per k-step)
+    const bool gnext = more && A.gen.pts != nullptr;
     wy128_load<KP>(sV, sM, wy_col, it.s);
     cp_commit();
-    if (more) {  // G of pair p+1 streams in behind steps 3-4
+    if (more && !gnext) {  // G of pair p+1 streams in behind steps 3-4
       const PairItem &nx = s_it[p + 1 - ch.begin];
       async_tile<128, 128, LD>(sG, A.close + nx.g_src[0], nx.nt, nx.ns, A.B, A.chunks);
       cp_commit();
@@ -1590,6 +1679,11 @@ __global__ void __launch_bounds__(PairWy128Cfg<KP>::THREADS, 1) pair_wy128_kerne
       cp_wait_all();
     }
     __syncthreads();
+    GenCol gc;
+    if (gnext) {
+      const PairItem &nx = s_it[p + 1 - ch.begin];
+      gc = gen_col(A.gen, nx.t, nx.s, nx.nt, nx.ns, A.B, threadIdx.x & 127);
+    }
     // ---- step 3: R = T1 V_s (8 x KP per warp)
     double R[2][KP / 8][2];
 #pragma unroll
@@ -1603,6 +1697,10 @@ __global__ void __launch_bounds__(PairWy128Cfg<KP>::THREADS, 1) pair_wy128_kerne
       const double a = (q & 1) ? e1 : e0;
 #pragma unroll
       for (int i = 0; i < KP / 8; i++) dmma(R[(k0 >> 2) & 1][i], a, sV[(k0 + q) * LDV + i * 8 + r]);
+      if (gnext) {  // 512 threads x 32 k-steps = the 128 x 128 entries
+        const int gi = (threadIdx.x >> 7) + 4 * (k0 >> 2);
+        sG[gi * LD + gc.j] = gen_entry(A.gen, gc, gi);
+      }
     }
 #pragma unroll
     for (int i = 0; i < KP / 8; i++) {
@@ -2415,6 +2513,15 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       a.B = P->B;
       a.sym = P->sym;
       a.close = in->close;
+      a.gen.pts = nullptr;
+      if (in->close_gen) {
+        a.gen.pts = in->close_gen->points;
+        a.gen.dim = in->close_gen->dim;
+        a.gen.kind = in->close_gen->kernel;
+        a.gen.p0 = in->close_gen->p0;
+        a.gen.p1 = in->close_gen->p1;
+        a.gen.q0 = a.gen.kind == H2SP_KERNEL_EXP ? -1.0 / a.gen.p0 : 1.0 / (4.0 * 3.141592653589793);
+      }
       a.bb_in = bb;
       a.dt_in = dt;
       a.q_row = out->q_row;

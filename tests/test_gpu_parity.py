@@ -358,6 +358,59 @@ def test_explicit_q_and_wy_agree(name):
     assert np.linalg.norm(a - b) <= 1e-13 * np.linalg.norm(b)
 
 
+@pytest.mark.parametrize("cfg,N", [(1, None), (2, 16384), (3, 16384), (4, 16384), (5, 16384)],
+                         ids=["cfg1", "cfg2-16384", "cfg3-16384", "cfg4-16384", "cfg5-16384"])
+def test_close_gen_matches_stored_close(cfg, N):
+    """Matrix-free close blocks (h2sp_close_gen, SURVEY §8(d) config-5 protocol
+    step 1): the level-0 congruence evaluates C_ts from the tree-ordered points.
+    S matches the oracle (run on the generator's stored blocks) and the
+    stored-close GPU build to rounding (one-ulp differences of exp / sqrt /
+    division between numpy and the device); Q does not depend on C (bitwise)."""
+    _need_gpu()
+    import paper_1705_04601_b200 as h2sp
+    h = h2gen.make_config(cfg, N=N)
+    packed = h2gen.pack(h)
+    plan = h2sp.Plan(packed)
+    ref = {k: (v.clone() if v is not None else None) for k, v in h2sp.Sparsifier(plan, packed).build().items()}
+    sp = h2sp.Sparsifier(plan, packed, close_gen={"points": h.points, "kernel": h.meta["kernel"]})
+    assert "close" not in sp.inputs
+    out = sp.build()
+    torch.cuda.synchronize()
+    _compare(h, plan, out)
+    assert torch.equal(out["q_row"], ref["q_row"])
+    if not h.symmetric:
+        assert torch.equal(out["q_col"], ref["q_col"])
+    assert torch.equal(out["s_col"], ref["s_col"]) and torch.equal(out["s_rowptr"], ref["s_rowptr"])
+    a, b = out["s_val"], ref["s_val"]
+    assert float(torch.linalg.norm(a - b)) <= 1e-13 * float(torch.linalg.norm(b))
+    if h.symmetric:
+        import scipy.sparse as sps
+        nnz = plan.sizes["s_nnz"]
+        S = sps.csr_matrix((a[:nnz].cpu().numpy(), out["s_col"][:nnz].cpu().numpy(),
+                            out["s_rowptr"].cpu().numpy()), shape=(h.N, h.N))
+        assert (S != S.T).nnz == 0
+
+
+def test_close_gen_build_host_e2e():
+    """h2sp_build_host in close_gen mode: the host points are copied in and the
+    outputs equal the device-resident close_gen build bitwise."""
+    _need_gpu()
+    import paper_1705_04601_b200 as h2sp
+    h = h2gen.make_config(5, N=4096)
+    packed = h2gen.pack(h)
+    plan = h2sp.Plan(packed)
+    sp = h2sp.Sparsifier(plan, packed, close_gen={"points": h.points, "kernel": h.meta["kernel"]})
+    ref = {k: (v.clone() if v is not None else None) for k, v in sp.build().items()}
+    host_in = {k: v.cpu().pin_memory() for k, v in sp.inputs.items()}
+    sp.inputs["points"].zero_()
+    host_out = {k: (torch.empty_like(v, device="cpu").pin_memory() if v is not None else None)
+                for k, v in sp.outputs.items()}
+    sp.build_host(host_in, host_out)
+    torch.cuda.synchronize()
+    for k in ("s_val", "s_col", "s_rowptr", "q_row"):
+        assert torch.equal(host_out[k], ref[k].cpu()), k
+
+
 def _csr_spmv(out, nnz, n_rows, z, chunks=16):
     """S z with S the GPU CSR output (test infrastructure: torch sparse SpMV over
     row chunks, int32 column indices widened per chunk)."""

@@ -175,3 +175,30 @@ def test_wy_congruence_flops():
         assert li["flops_exec"] == want
         assert plan.sizes["flops_executed"] == pytest.approx(sum(l["flops_exec"] for l in plan.launches()))
         assert plan.sizes["flops"] == pytest.approx(sum(l["flops"] for l in plan.launches()))
+
+
+def test_close_gen_descriptor_validation():
+    """h2sp_close_gen (matrix-free close blocks) is validated before any device
+    work: bad dim / kernel id / NULL points are H2SP_EINVAL (1); the binding maps
+    the generator's kernel specs to the header's kernel ids."""
+    h = h2gen.random_h2(3, 8, 0, True)
+    plan = h2sp.Plan(h2gen.pack(h))
+    ws = ctypes.create_string_buffer(int(plan.sizes["workspace_bytes"]) + 512)
+    wsp = (ctypes.addressof(ws) + 255) // 256 * 256
+    dummy = ctypes.c_double(0.0)
+    dp = ctypes.addressof(dummy)
+    pts = (ctypes.c_double * (3 * h.N))()
+    for dim, kern, p, why in ((5, 1, ctypes.addressof(pts), b"dim"), (3, 9, ctypes.addressof(pts), b"kernel"),
+                              (3, 1, None, b"points")):
+        g = h2sp._CloseGen(points=p, dim=dim, kernel=kern, p0=0.1, p1=0.01)
+        inp = h2sp._Inputs(leaf_basis_row=dp, transfer_row=dp, close=None, coupling=dp,
+                           close_gen=ctypes.addressof(g))
+        out = h2sp._Outputs(q_row=dp, s_val=dp)
+        st = h2sp.lib.h2sp_build(plan.handle, ctypes.byref(inp), ctypes.byref(out), wsp,
+                                 int(plan.sizes["workspace_bytes"]), None)
+        assert st == 1, (dim, kern)
+        assert why in h2sp.lib.h2sp_last_error()
+    assert h2sp.close_gen_params({"kind": "exp", "ell": 0.05, "nugget": 1e-2}) == (1, 0.05, 1e-2)
+    assert h2sp.close_gen_params({"kind": "invh", "h": 0.5, "diag_add": 1.0}) == (2, 0.5, 1.0)
+    k, p0, p1 = h2sp.close_gen_params({"kind": "laplace", "h": 0.25})
+    assert k == 3 and p1 == pytest.approx(1.0 / np.pi)
