@@ -224,6 +224,8 @@ def main():
     ap.add_argument("--nrhs", type=int, default=1)
     ap.add_argument("--no-oracle", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-depth", type=int, default=2,
+                    help="e2e leg: jobs in flight (own stream + device buffers each); 1 = strictly one after another")
     ap.add_argument("--ref-n", type=int, default=16384, help="--impl reference sample size")
     ap.add_argument("--timeline", action="store_true", help="print per-launch start/end of the last step (stderr)")
     ap.add_argument("--close-gen", action="store_true",
@@ -375,21 +377,43 @@ def main():
     # ---- e2e through the public API with HOST buffers (pinned), copies inside the timed region
     e2e = None
     if not args.no_e2e:
+        # Jobs stream through the public host-buffer API (h2sp_build_host + the
+        # applies with host vectors), `depth` of them in flight on their own
+        # streams and device buffer sets: job i+1's H2D (inputs) runs while job
+        # i's D2H (S, Q, x) drains -- PCIe is full duplex.  Every job still copies
+        # all of its inputs in and all of its outputs out inside the timed region.
+        depth = max(1, args.e2e_depth)
         host_in = {k: v.cpu().pin_memory() for k, v in sp.inputs.items()}
-        host_out = {k: (torch.empty(v.shape, dtype=v.dtype).pin_memory() if v is not None else None)
-                    for k, v in sp.outputs.items()}
         hb = b.cpu().pin_memory()
-        hx = torch.empty(x.shape, dtype=x.dtype).pin_memory()
+        sets = []
+        for d in range(depth):
+            spd = sp if d == 0 else h2sp.Sparsifier(plan, packed, device=dev, close_gen=gen)
+            sets.append({
+                "sp": spd, "stream": torch.cuda.Stream(device=dev),
+                "out": {k: (torch.empty(v.shape, dtype=v.dtype).pin_memory() if v is not None else None)
+                        for k, v in spd.outputs.items()},
+                "b": torch.empty_like(b), "y": torch.empty_like(y), "x": torch.empty_like(x),
+                "hx": torch.empty(x.shape, dtype=x.dtype).pin_memory(),
+                "aws": aws if d == 0 else spd.apply_ws(nrhs)})
 
-        def step_e2e():
-            sp.build_host(host_in, host_out)
-            b.copy_(hb, non_blocking=True)
-            sp.apply_Ut(b, y, ws=aws)
-            sp.apply_V(y, x, ws=aws)
-            hx.copy_(x, non_blocking=True)
+        def step_e2e(i):
+            st_ = sets[i % depth]
+            with torch.cuda.stream(st_["stream"]):
+                st_["sp"].build_host(host_in, st_["out"], stream=st_["stream"])
+                st_["b"].copy_(hb, non_blocking=True)
+                st_["sp"].apply_Ut(st_["b"], st_["y"], ws=st_["aws"], stream=st_["stream"])
+                st_["sp"].apply_V(st_["y"], st_["x"], ws=st_["aws"], stream=st_["stream"])
+                st_["hx"].copy_(st_["x"], non_blocking=True)
 
-        for _ in range(2):
-            step_e2e()
+        def run_e2e(n):
+            for st_ in sets:
+                st_["stream"].wait_stream(stream)
+            for i in range(n):
+                step_e2e(i)
+            for st_ in sets:
+                stream.wait_stream(st_["stream"])
+
+        run_e2e(2 * depth)
         torch.cuda.synchronize()
         k_e2e = max(3, min(args.steps, 10))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -397,18 +421,20 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
         e0.record(stream)
-        for _ in range(k_e2e):
-            step_e2e()
+        run_e2e(k_e2e)
         e1.record(stream)
         torch.cuda.synchronize()
         ems = torch.tensor([e0.elapsed_time(e1) / k_e2e], dtype=torch.float64, device=red_dev)
         if world > 1:
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         h2d = sum(int(v.numel()) * v.element_size() for v in host_in.values()) + hb.numel() * 8
-        d2h = sum(int(v.numel()) * v.element_size() for v in host_out.values() if v is not None) + hx.numel() * 8
+        d2h = sum(int(v.numel()) * v.element_size() for v in sets[0]["out"].values() if v is not None) \
+            + sets[0]["hx"].numel() * 8
         e2e = {"value": job_flops / (float(ems.item()) * 1e-3) / 1e12, "unit": UNIT,
                "ms_per_step": float(ems.item()), "steps": k_e2e, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h}
+               "d2h_bytes_per_step": d2h, "jobs_in_flight": depth,
+               "api": "h2sp_build_host + h2sp_apply_Ut/V with pinned host buffers, one stream and device "
+                      "buffer set per job in flight"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_oracle and h.close is not None:

@@ -1079,9 +1079,9 @@ __device__ __forceinline__ void gen_close_tile(double *sG, const CloseGen &g, in
 }
 
 // Level-0 G = C_ts: cp.async copy of the stored block, or evaluated (close_gen).
-template <int NP, int LD>
+template <int NP, int LD, bool GEN>
 __device__ __forceinline__ void load_close(const PairArgs &A, const PairItem &it, double *sG) {
-  if (A.gen.pts)
+  if constexpr (GEN)
     gen_close_tile<NP, LD>(sG, A.gen, it.t, it.s, it.nt, it.ns, A.B);
   else
     async_tile<NP, NP, LD>(sG, A.close + it.g_src[0], it.nt, it.ns, A.B, A.chunks);
@@ -1089,13 +1089,13 @@ __device__ __forceinline__ void load_close(const PairArgs &A, const PairItem &it
 
 // Issue the cp.async copies of G_ts (level 0: C_ts; else the 2x2 arrangement of
 // the children's bb parts / D~) into sG.
-template <int NP>
+template <int NP, bool GEN>
 __device__ __forceinline__ void pair_load_G(const PairArgs &A, const PairItem &it, double *sG) {
   constexpr int LD = PairCfg<NP>::LD;
   const int nt = it.nt, ns = it.ns;
   const void *any = A.chunks;
   if (A.level == 0) {
-    load_close<NP, LD>(A, it, sG);
+    load_close<NP, LD, GEN>(A, it, sG);
   } else {
     const int kr0 = it.kr0, kr1 = it.kr1;
     const int kc0 = it.kc0, kc1 = it.kc1;
@@ -1236,7 +1236,7 @@ __device__ __forceinline__ int stage_items(const PairItem *items, const Chunk &c
 // from T by quad shuffles.  The scatter of pair p's H is software-pipelined
 // into the T-GEMM of pair p+1 (8x8 tiles spread over the k-steps), so the
 // stores fill issue slots between DMMAs instead of forming an idle phase.
-template <int NP>
+template <int NP, bool GEN>
 __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS) pair_kernel(PairArgs A) {
   using C = PairCfg<NP>;
   constexpr int LD = C::LD;
@@ -1256,7 +1256,7 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS)
   const int m0 = warp * 8 * TM;
   // prologue: Q_t, G_0, Q_s0
   async_tile<NP, NP, LD>(sQt, A.q_row + s_it[0].q_off_t, nt, nt, nt, A.chunks);
-  pair_load_G<NP>(A, s_it[0], sG);
+  pair_load_G<NP, GEN>(A, s_it[0], sG);
   async_tile<NP, NP, LD>(sQs, A.q_col + s_it[0].q_off_s, s_it[0].ns, s_it[0].ns, s_it[0].ns, A.chunks);
   cp_commit();
   double H[TM][TN][2];  // result of the previous pair, scattered during the next T-GEMM
@@ -1315,7 +1315,7 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS)
     __syncthreads();  // every warp is done with G
     const bool more = p + 1 < ch.end && !(A.debug & 2);
     if (more) {
-      pair_load_G<NP>(A, s_it[p + 1 - ch.begin], sG);
+      pair_load_G<NP, GEN>(A, s_it[p + 1 - ch.begin], sG);
       cp_commit();
     }
     // ---- H = T Q_s; A fragment (row m0+8i+r, col k0+q) lives in lane (r, (k0%8+q)/2), element q%2
@@ -1398,7 +1398,7 @@ __device__ __forceinline__ void wy_load(double *sV, double *sM, const double *wy
   async_tile<KP, 64, C::LD>(sM, g + 64 * KP, KP, 64, 64, g);
 }
 
-template <int KP>
+template <int KP, bool GEN>
 __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(PairArgs A, const double *wy_row,
                                                                               const double *wy_col) {
   using C = PairWyCfg<KP>;
@@ -1416,7 +1416,7 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
   const int r = lane >> 2, q = lane & 3;
   const int m0 = warp * 8;
   wy_load<KP>(sVt, sMt, wy_row, t);
-  load_close<64, LD>(A, s_it[0], sG);
+  load_close<64, LD, GEN>(A, s_it[0], sG);
   wy_load<KP>(sVM, sVM + C::V_D, wy_col, s_it[0].s);
   cp_commit();
   double H[TN][2];
@@ -1503,7 +1503,7 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
     }
     __syncthreads();  // every warp is done with G and P
     // close_gen: G of pair p+1 is evaluated during step 3 (one row per k-step)
-    const bool gnext = more && A.gen.pts != nullptr;
+    const bool gnext = GEN && more;
     GenCol gc;
     if (more) {
       const PairItem &nx = s_it[p + 1 - ch.begin];
@@ -1610,7 +1610,7 @@ __device__ __forceinline__ void wy128_load(double *sV, double *sM, const double 
   async_tile<KP, 128, C::LD>(sM, g + 128 * KP, KP, 128, 128, g);
 }
 
-template <int KP>
+template <int KP, bool GEN>
 __global__ void __launch_bounds__(PairWy128Cfg<KP>::THREADS, 1) pair_wy128_kernel(PairArgs A, const double *wy_row,
                                                                                    const double *wy_col) {
   using C = PairWy128Cfg<KP>;
@@ -1625,7 +1625,7 @@ __global__ void __launch_bounds__(PairWy128Cfg<KP>::THREADS, 1) pair_wy128_kerne
   const int r = lane >> 2, q = lane & 3;
   const int m0 = warp * 8;
   const int src_lo = r * 4 + (q >> 1), src_hi = src_lo + 2;
-  load_close<128, LD>(A, s_it[0], sG);
+  load_close<128, LD, GEN>(A, s_it[0], sG);
   wy128_load<KP>(sV, sM, wy_row, s_it[0].t);
   cp_commit();
   for (int p = ch.begin; p < ch.end; p++) {
@@ -1667,7 +1667,7 @@ __global__ void __launch_bounds__(PairWy128Cfg<KP>::THREADS, 1) pair_wy128_kerne
     __syncthreads();  // G, P, M_t are dead
     const bool more = p + 1 < ch.end && !(A.debug & 2);
     // close_gen: G of pair p+1 is evaluated during step 3 (one row per k-step)
-    const bool gnext = more && A.gen.pts != nullptr;
+    const bool gnext = GEN && more;
     wy128_load<KP>(sV, sM, wy_col, it.s);
     cp_commit();
     if (more && !gnext) {  // G of pair p+1 streams in behind steps 3-4
@@ -2073,10 +2073,16 @@ static h2sp_status launch_pairs_wy128(const PairArgs &a, const double *wy_row, c
   using C = PairWy128Cfg<KP>;
   static bool attr = false;
   if (!attr) {
-    H2SP_CK(cudaFuncSetAttribute(pair_wy128_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
+    H2SP_CK(cudaFuncSetAttribute(pair_wy128_kernel<KP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(C::SMEM)));
+    H2SP_CK(cudaFuncSetAttribute(pair_wy128_kernel<KP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(C::SMEM)));
     attr = true;
   }
-  pair_wy128_kernel<KP><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a, wy_row, wy_col);
+  if (a.gen.pts)
+    pair_wy128_kernel<KP, true><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a, wy_row, wy_col);
+  else
+    pair_wy128_kernel<KP, false><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a, wy_row, wy_col);
   H2SP_CK(cudaGetLastError());
   return H2SP_OK;
 }
@@ -2087,10 +2093,14 @@ static h2sp_status launch_pairs(const PairArgs &a, int64_t nchunks, cudaStream_t
   using C = PairCfg<NP>;
   static bool attr = false;
   if (!attr) {
-    H2SP_CK(cudaFuncSetAttribute(pair_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
+    H2SP_CK(cudaFuncSetAttribute(pair_kernel<NP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
+    H2SP_CK(cudaFuncSetAttribute(pair_kernel<NP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
     attr = true;
   }
-  pair_kernel<NP><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a);
+  if (a.level == 0 && a.gen.pts)
+    pair_kernel<NP, true><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a);
+  else
+    pair_kernel<NP, false><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a);
   H2SP_CK(cudaGetLastError());
   return H2SP_OK;
 }
@@ -2101,10 +2111,16 @@ static h2sp_status launch_pairs_wy(const PairArgs &a, const double *wy_row, cons
   using C = PairWyCfg<KP>;
   static bool attr = false;
   if (!attr) {
-    H2SP_CK(cudaFuncSetAttribute(pair_wy_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
+    H2SP_CK(cudaFuncSetAttribute(pair_wy_kernel<KP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(C::SMEM)));
+    H2SP_CK(cudaFuncSetAttribute(pair_wy_kernel<KP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(C::SMEM)));
     attr = true;
   }
-  pair_wy_kernel<KP><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a, wy_row, wy_col);
+  if (a.gen.pts)
+    pair_wy_kernel<KP, true><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a, wy_row, wy_col);
+  else
+    pair_wy_kernel<KP, false><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a, wy_row, wy_col);
   H2SP_CK(cudaGetLastError());
   return H2SP_OK;
 }
