@@ -391,6 +391,42 @@ def test_close_gen_matches_stored_close(cfg, N):
         assert (S != S.T).nnz == 0
 
 
+def test_close_gen_shards_and_graph_bitwise():
+    """close_gen composes with the subtree shards (each shard reads
+    its neighbours' points) and with graph capture: shard rows and the replayed
+    graph equal the unsharded close_gen build bitwise."""
+    _need_gpu()
+    import paper_1705_04601_b200 as h2sp
+    h = h2gen.make_config(5, N=16384, with_close=False)
+    packed = h2gen.pack(h)
+    gen = {"points": h.points, "kernel": h.meta["kernel"]}
+    plan = h2sp.Plan(packed)
+    sp = h2sp.Sparsifier(plan, packed, close_gen=gen)
+    ref = {k: v.clone() for k, v in sp.build().items() if v is not None}
+    torch.cuda.synchronize()
+    full_val = ref["s_val"].cpu().numpy()
+    frow = ref["s_rowptr"].cpu().numpy()
+    G = 4
+    seen = np.zeros(h.N, dtype=np.int64)
+    for g in range(G):
+        sh = h2sp.Plan(packed, g, G)
+        o = h2sp.Sparsifier(sh, packed, close_gen=gen).build()
+        torch.cuda.synchronize()
+        rp, val = o["s_rowptr"].cpu().numpy(), o["s_val"].cpu().numpy()
+        for lr, r in enumerate(sh.global_rows()):
+            seen[r] += 1
+            assert np.array_equal(val[rp[lr]:rp[lr + 1]], full_val[frow[r]:frow[r + 1]]), (g, r)
+    assert np.all(seen == 1)
+    for v in sp.outputs.values():
+        if v is not None:
+            v.zero_()
+    gr = sp.capture()
+    gr.replay()
+    torch.cuda.synchronize()
+    for k, v in ref.items():
+        assert torch.equal(v, sp.outputs[k]), k
+
+
 def test_close_gen_build_host_e2e():
     """h2sp_build_host in close_gen mode: the host points are copied in and the
     outputs equal the device-resident close_gen build bitwise."""
