@@ -224,6 +224,9 @@ def main():
     ap.add_argument("--nrhs", type=int, default=1)
     ap.add_argument("--no-oracle", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="time CUDA-graph replays of the captured step (launch-bound small configs); the default "
+                         "eager steps carry the per-launch events the roofline needs inside the timed region")
     ap.add_argument("--e2e-depth", type=int, default=2,
                     help="e2e leg: jobs in flight (own stream + device buffers each); 1 = strictly one after another")
     ap.add_argument("--ref-n", type=int, default=16384, help="--impl reference sample size")
@@ -309,18 +312,39 @@ def main():
         for e in row:
             e.record(stream)
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    graph = None
+    if args.graph:
+        # the whole step (build + applies, fork/join over the library's side
+        # streams) captured once into a CUDA graph and replayed; per-launch
+        # durations then come from an untimed eager pass below
+        graph = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream(device=dev)
+        cap.wait_stream(stream)
+        with torch.cuda.graph(graph, stream=cap):
+            step()
+        torch.cuda.synchronize()
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local_rank) as clk:
         t_start.record(stream)
         for i in range(args.steps):
-            step(evs[i])
+            if graph is not None:
+                graph.replay()
+            else:
+                step(evs[i])
         t_end.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ms = t_start.elapsed_time(t_end) / args.steps
+    if graph is not None:     # per-launch events: eager steps outside the timed region
+        for i in range(args.steps):
+            step(evs[i])
+        torch.cuda.synchronize()
     ms_t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -459,6 +483,9 @@ def main():
                        "close": ("matrix-free: C_ts evaluated in the level-0 congruence from the points "
                                  "(h2sp_close_gen; %.1f GB of close blocks never stored)" % (plan.sizes["close"] * 8e-9))
                                 if args.close_gen else "stored (B x B per near pair, read by the level-0 congruence)",
+                       "step_launch": ("CUDA graph replay of the captured step (per-launch durations from "
+                                       "eager steps run after the timed region)") if args.graph else
+                                      "eager (per-launch CUDA events recorded inside the timed steps)",
                        "plan_ms": plan_ms, "s_nnz": plan.sizes["s_nnz"], "s_blocks": plan.sizes["s_blocks"],
                        "flops_per_step": step_flops, "bytes_per_step": bytes_step,
                        "flops_convention": "algorithmic (SURVEY 8(d): explicit-Q congruence 2 n_t n_s (n_t + n_s)); "
