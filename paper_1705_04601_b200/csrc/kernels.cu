@@ -1760,7 +1760,14 @@ struct StripCfg {
   static constexpr int NWM = NP / 16, NWN = TN / WN;
   static constexpr int WARPS = NWM * NWN;
   static constexpr int THREADS = WARPS * 32;
-  static constexpr size_t SMEM = (size_t(NP) * LDQ + size_t(NP) * LDZ) * sizeof(double) + TN * 16 + 64;
+  // the tile's groups (staged before the gather) alias the Z buffer
+  static constexpr size_t SMEM = (size_t(NP) * LDQ + size_t(NP) * LDZ) * sizeof(double) + TN * 16;
+  static_assert(size_t(NP) * LDZ * sizeof(double) >= (TN + 1) * sizeof(StripGroup), "groups alias sZ");
+#ifndef STRIP_MINB
+#define STRIP_MINB 5
+#endif
+  // 5 CTAs per SM at NP <= 32 (46 KB of shared memory, <= 48 registers)
+  static constexpr int MIN_BLOCKS = (NP <= 32 && TN == 128) ? STRIP_MINB : 1;
 };
 
 struct StripArgs {
@@ -1774,7 +1781,7 @@ struct StripArgs {
 };
 
 template <int NP, int TN>
-__global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS) strip_kernel(StripArgs A) {
+__global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::MIN_BLOCKS) strip_kernel(StripArgs A) {
   using C = StripCfg<NP, TN>;
   extern __shared__ __align__(16) double sm[];
   double *sQ = sm;                           // NP x LDQ
@@ -1782,7 +1789,7 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS) strip_kernel(StripA
   int64_t *tdst = reinterpret_cast<int64_t *>(sZ + NP * C::LDZ);  // per column: transposed S dst (b*ld folded in)
   int32_t *src1 = reinterpret_cast<int32_t *>(tdst + TN);          // per column: column in child-1 panel or -1
   int32_t *src2 = src1 + TN;
-  __shared__ StripGroup sg[TN + 1];            // groups overlapping this tile (<= TN of them)
+  StripGroup *sg = reinterpret_cast<StripGroup *>(sZ);  // groups overlapping this tile (<= TN + 1), dead before the gather
   __shared__ __align__(16) StripTileX s_tile;
   // round trip 1: the self-contained tile descriptor
   if (threadIdx.x < sizeof(StripTileX) / 16)
