@@ -391,6 +391,32 @@ def main():
                  "peak_source": "FP64 DMMA microbenchmark on this pool's B200 (profiles/r01_fp64_peak.txt); "
                                 f"cuBLAS DGEMM measured {FP64_DGEMM_TFLOPS}",
                  "hbm_peak_gbs": peaks["hbm_gbs"]})
+    # SURVEY 8(a) a8 on its own: y = U^T b and x = V y timed alone (after the
+    # timed region), against the HBM roofline -- algorithmic bytes = every Q_t
+    # read once (8 n_t^2) + the vectors in and out (8 N nrhs each)
+    def _time_apply(fn, reps=10):
+        fn()
+        e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_a.record(stream)
+        for _ in range(reps):
+            fn()
+        e_b.record(stream)
+        torch.cuda.synchronize()
+        return e_a.elapsed_time(e_b) / reps
+    ut_ms = _time_apply(lambda: sp.apply_Ut(b, y, ws=aws))
+    v_ms = _time_apply(lambda: sp.apply_V(y, x, ws=aws))
+    loc_rr, loc_cc = plan.local_rows()
+    vec_b = 8.0 * nrhs * (plan.n_tree_local + plan.s_rows)
+    ut_bytes = 8.0 * float(np.sum(offs["n_row"][loc_rr >= 0].astype(float) ** 2)) + vec_b
+    v_bytes = 8.0 * float(np.sum(offs["n_col"][(loc_rr if plan.symmetric else loc_cc) >= 0].astype(float) ** 2)) \
+        + vec_b
+    apply_info = {"ut_us": ut_ms * 1e3, "v_us": v_ms * 1e3, "ut_bytes": ut_bytes, "v_bytes": v_bytes, "nrhs": nrhs,
+                  "ut_gbs": ut_bytes / (ut_ms * 1e-3) / 1e9, "v_gbs": v_bytes / (v_ms * 1e-3) / 1e9,
+                  "hbm_peak_gbs": peaks["hbm_gbs"],
+                  "note": "h2sp_apply_Ut / h2sp_apply_V timed alone after the timed region (10 reps each); "
+                          "algorithmic bytes: every Q_t once + vectors in and out"}
+    apply_info["ut_frac"] = apply_info["ut_gbs"] / peaks["hbm_gbs"]
+    apply_info["v_frac"] = apply_info["v_gbs"] / peaks["hbm_gbs"]
     # whole-job throughput: the work of every rank (shards: their own flops) / max time
     fl_t = torch.tensor([step_flops], dtype=torch.float64, device=red_dev)
     if world > 1:
@@ -509,6 +535,7 @@ def main():
                                     "bound_printed": 4 * plan.L + 6 * (2.0 ** -plan.L - 1),
                                     "bound_corrected": 4 * plan.L - 2 + 3 * 2.0 ** -plan.L}},
             "roofline": roof,
+            "apply_roofline": apply_info,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps * (n_launch + n_apply_launch),

@@ -1760,14 +1760,18 @@ struct StripCfg {
   static constexpr int NWM = NP / 16, NWN = TN / WN;
   static constexpr int WARPS = NWM * NWN;
   static constexpr int THREADS = WARPS * 32;
-  // the tile's groups (staged before the gather) alias the Z buffer
-  static constexpr size_t SMEM = (size_t(NP) * LDQ + size_t(NP) * LDZ) * sizeof(double) + TN * 16;
-  static_assert(size_t(NP) * LDZ * sizeof(double) >= (TN + 1) * sizeof(StripGroup), "groups alias sZ");
 #ifndef STRIP_MINB
 #define STRIP_MINB 5
 #endif
-  // 5 CTAs per SM at NP <= 32 (46 KB of shared memory, <= 48 registers)
-  static constexpr int MIN_BLOCKS = (NP <= 32 && TN == 128) ? STRIP_MINB : 1;
+  // NP == 32: 5 CTAs per SM (46 KB of shared memory -- the tile's groups,
+  // staged before the gather, alias the Z buffer -- and <= 48 registers).
+  // Other widths keep the separate group array and no minimum-blocks hint
+  // (__launch_bounds__(512, 1) let NP = 48 / 64 grow to 76 registers = one CTA
+  // per SM: 1.35x slower strips on the config-5 recipe).
+  static constexpr bool SMALL = NP == 32 && TN == 128;
+  static constexpr int MIN_BLOCKS = SMALL ? STRIP_MINB : 0;
+  static constexpr size_t SMEM = (size_t(NP) * LDQ + size_t(NP) * LDZ) * sizeof(double) + TN * 16 + (SMALL ? 0 : 64);
+  static_assert(size_t(NP) * LDZ * sizeof(double) >= (TN + 1) * sizeof(StripGroup), "groups alias sZ");
 };
 
 struct StripArgs {
@@ -1789,7 +1793,9 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
   int64_t *tdst = reinterpret_cast<int64_t *>(sZ + NP * C::LDZ);  // per column: transposed S dst (b*ld folded in)
   int32_t *src1 = reinterpret_cast<int32_t *>(tdst + TN);          // per column: column in child-1 panel or -1
   int32_t *src2 = src1 + TN;
-  StripGroup *sg = reinterpret_cast<StripGroup *>(sZ);  // groups overlapping this tile (<= TN + 1), dead before the gather
+  __shared__ StripGroup sg_own[C::SMALL ? 1 : TN + 1];
+  // groups overlapping this tile (<= TN + 1); when aliased, dead before the gather
+  StripGroup *sg = C::SMALL ? reinterpret_cast<StripGroup *>(sZ) : sg_own;
   __shared__ __align__(16) StripTileX s_tile;
   // round trip 1: the self-contained tile descriptor
   if (threadIdx.x < sizeof(StripTileX) / 16)
