@@ -915,6 +915,100 @@ __host__ __device__ inline int coup_warp_doubles(int kt, int ks) {
   return A8 * coup_ld(ks) * 2 + B8 * coup_ld(ks) + A8 * coup_ld(kt) + 2;
 }
 
+// Register variant for ranks <= KP <= 32 (every BASELINE config): one warp per
+// pair, no shared memory -- X = R^_t D with both operands' DMMA fragments read
+// straight from L1/L2 (R^ blocks are shared by many pairs), then
+// D~ = X R^_s^T with X's A fragments taken from the accumulators by quad
+// shuffles.  Zero-padded to KP; ragged ranks take the predicated loads.
+template <int KP>
+__global__ void __launch_bounds__(128, KP == 32 ? 3 : 4) coupling_reg_kernel(const CouplingItem *__restrict__ items, int64_t n_items,
+                                                           Side rs, Side cs, const double *__restrict__ rh_row,
+                                                           const double *__restrict__ rh_col,
+                                                           const double *__restrict__ D, double *__restrict__ dt) {
+  constexpr int T = KP / 8;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t item = int64_t(blockIdx.x) * (blockDim.x >> 5) + warp;
+  if (item >= n_items) return;
+  const CouplingItem it = items[item];
+  const int kt = rs.k[it.t], ks = cs.k[it.s];
+  const double *Rt = rh_row + rs.rh_off[it.t];   // kt x kt, row-major
+  const double *Rs = rh_col + cs.rh_off[it.s];   // ks x ks
+  const double *Dg = D + it.d_src;               // kt x ks
+  const int r = lane >> 2, q = lane & 3;
+  // ---- X = R^_t D: A(m, kk) = R^_t[m][kk], B(kk, n) = D[kk][n]
+  double X[T][T][2];
+#pragma unroll
+  for (int i = 0; i < T; i++)
+#pragma unroll
+    for (int j = 0; j < T; j++) X[i][j][0] = X[i][j][1] = 0.0;
+#pragma unroll 2
+  for (int k0 = 0; k0 < KP; k0 += 4) {
+    const int kk = k0 + q;
+    double a[T], b[T];
+#pragma unroll
+    for (int i = 0; i < T; i++) {
+      const int m = i * 8 + r;
+      a[i] = (m < kt && kk < kt) ? __ldg(Rt + m * kt + kk) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < T; j++) {
+      const int n = j * 8 + r;
+      b[j] = (kk < kt && n < ks) ? __ldg(Dg + kk * ks + n) : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < T; i++)
+#pragma unroll
+      for (int j = 0; j < T; j++) dmma(X[i][j], a[i], b[j]);
+  }
+  // ---- D~ = X R^_s^T: A(m, kk) = X[m][kk] (lane (r, (k0 % 8 + q) / 2), element q % 2),
+  //      B(kk, n) = R^_s[n][kk]
+  //      in passes of JH column tiles (KP = 32: two passes, to stay within 128 registers)
+  constexpr int JH = KP == 32 ? T / 2 : T;
+  const int src_lo = r * 4 + (q >> 1), src_hi = src_lo + 2;
+  double *out = dt + it.dt_dst;
+#pragma unroll
+  for (int j0 = 0; j0 < T; j0 += JH) {
+    double Y[T][JH][2];
+#pragma unroll
+    for (int i = 0; i < T; i++)
+#pragma unroll
+      for (int j = 0; j < JH; j++) Y[i][j][0] = Y[i][j][1] = 0.0;
+#pragma unroll
+    for (int k0 = 0; k0 < KP; k0 += 4) {
+      const int jt = k0 >> 3;
+      const int srcl = (k0 & 4) ? src_hi : src_lo;
+      const int kk = k0 + q;
+      double a[T], b[JH];
+#pragma unroll
+      for (int i = 0; i < T; i++) {
+        const double e0 = __shfl_sync(0xffffffffu, X[i][jt][0], srcl);
+        const double e1 = __shfl_sync(0xffffffffu, X[i][jt][1], srcl);
+        a[i] = (q & 1) ? e1 : e0;
+      }
+#pragma unroll
+      for (int j = 0; j < JH; j++) {
+        const int n = (j0 + j) * 8 + r;
+        b[j] = (n < ks && kk < ks) ? __ldg(Rs + n * ks + kk) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < T; i++)
+#pragma unroll
+        for (int j = 0; j < JH; j++) dmma(Y[i][j], a[i], b[j]);
+    }
+#pragma unroll
+    for (int i = 0; i < T; i++) {
+      const int m = i * 8 + r;
+      if (m >= kt) continue;
+#pragma unroll
+      for (int j = 0; j < JH; j++) {
+        const int n = (j0 + j) * 8 + 2 * q;
+        if (n < ks) out[m * ks + n] = Y[i][j][0];
+        if (n + 1 < ks) out[m * ks + n + 1] = Y[i][j][1];
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(128) coupling_kernel(const CouplingItem *__restrict__ items, int64_t n_items,
                                                        int per_warp, Side rs, Side cs,
                                                        const double *__restrict__ rh_row,
@@ -2421,17 +2515,33 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     for (int64_t i = 0; i < (int64_t(1) << (L - k)); i++)
       kmax = std::max(kmax, std::max(P->k_row[lvl_off_d(L, k) + i], P->k_col[lvl_off_d(L, k) + i]));
     if (h2sp_status e = pre(s, li[k].coup)) return e;
-    const int per_warp = coup_warp_doubles(kmax, kmax);
-    const int ipc = std::max(1, std::min(4, int((96 * 1024) / (size_t(per_warp) * 8))));
-    coupling_kernel<<<unsigned((lp.n_coup + ipc - 1) / ipc), 32 * ipc, size_t(per_warp) * 8 * ipc, s>>>(
-        (const CouplingItem *)(meta + lp.coup_off), lp.n_coup, per_warp, rs, cs, rh_row, rh_col, in->coupling, dt);
+    const CouplingItem *items = (const CouplingItem *)(meta + lp.coup_off);
+    static const bool coup_smem = [] {  // H2SP_COUPLING_SMEM=1: the shared-memory kernel at every rank
+      const char *e = getenv("H2SP_COUPLING_SMEM");
+      return e && e[0] == '1';
+    }();
+    if (kmax <= 32 && !coup_smem) {
+      const unsigned grid = unsigned((lp.n_coup + 3) / 4);
+      switch ((kmax + 7) / 8) {
+        case 0:
+        case 1: coupling_reg_kernel<8><<<grid, 128, 0, s>>>(items, lp.n_coup, rs, cs, rh_row, rh_col, in->coupling, dt); break;
+        case 2: coupling_reg_kernel<16><<<grid, 128, 0, s>>>(items, lp.n_coup, rs, cs, rh_row, rh_col, in->coupling, dt); break;
+        case 3: coupling_reg_kernel<24><<<grid, 128, 0, s>>>(items, lp.n_coup, rs, cs, rh_row, rh_col, in->coupling, dt); break;
+        default: coupling_reg_kernel<32><<<grid, 128, 0, s>>>(items, lp.n_coup, rs, cs, rh_row, rh_col, in->coupling, dt); break;
+      }
+    } else {
+      const int per_warp = coup_warp_doubles(kmax, kmax);
+      const int ipc = std::max(1, std::min(4, int((96 * 1024) / (size_t(per_warp) * 8))));
+      coupling_kernel<<<unsigned((lp.n_coup + ipc - 1) / ipc), 32 * ipc, size_t(per_warp) * 8 * ipc, s>>>(
+          items, lp.n_coup, per_warp, rs, cs, rh_row, rh_col, in->coupling, dt);
+    }
     H2SP_CK(cudaGetLastError());
     return post(s, li[k].coup);
   };
 
-  // ---- CSR index expansion on s2 (independent of all values).  It is a pure
-  //      HBM write stream, so it is started after the level-0 congruence (which
-  //      needs every SM slot) and overlaps the latency-bound upper levels.
+  // ---- CSR index expansion on s2 (independent of all values): a pure HBM write
+  //      stream at the lowest priority, started with the build by default
+  //      (H2SP_CSR_AT below).
   static const bool no_csr = [] {   // debugging / attribution only: skip the index expansion
     const char *e = getenv("H2SP_NO_CSR");
     return e && e[0] == '1';
