@@ -485,6 +485,31 @@ def main():
                "d2h_bytes_per_step": d2h, "jobs_in_flight": depth,
                "api": "h2sp_build_host + h2sp_apply_Ut/V with pinned host buffers, one stream and device "
                       "buffer set per job in flight"}
+        # the link's own ceiling, measured here: pinned 512 MiB copies each way
+        # (alone), so e2e can be read against max(H2D, D2H) at full duplex
+        try:
+            nb = 1 << 26
+            hbuf = torch.empty(nb, dtype=torch.float64).pin_memory()
+            dbuf = torch.empty(nb, dtype=torch.float64, device=dev)
+
+            def _copy_gbs(fn):
+                fn()
+                a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_.record(stream)
+                for _ in range(3):
+                    fn()
+                b_.record(stream)
+                torch.cuda.synchronize()
+                return 3 * nb * 8 / (a_.elapsed_time(b_) * 1e-3) / 1e9
+            h2d_gbs = _copy_gbs(lambda: dbuf.copy_(hbuf, non_blocking=True))
+            d2h_gbs = _copy_gbs(lambda: hbuf.copy_(dbuf, non_blocking=True))
+            bound_ms = max(h2d / (h2d_gbs * 1e9), d2h / (d2h_gbs * 1e9)) * 1e3
+            e2e["pcie"] = {"h2d_gbs": h2d_gbs, "d2h_gbs": d2h_gbs, "bound_ms": bound_ms,
+                           "frac": bound_ms / float(ems.item()),
+                           "note": "bound = max(H2D bytes / H2D GB/s, D2H bytes / D2H GB/s), full duplex"}
+            del hbuf, dbuf
+        except RuntimeError as exc:  # pinned allocation refused: report without the bound
+            e2e["pcie"] = {"error": str(exc)[:120]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_oracle and h.close is not None:
