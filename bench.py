@@ -126,8 +126,15 @@ def oracle_baseline(h, flops: float, sample: str):
         res = oracle.sparsify(h)
         oracle.s_csr(res)
         dt = time.perf_counter() - t0
-    return {"value": flops / dt / 1e12, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
-            "seconds": dt, "host_cpus": os.cpu_count()}
+    out = {"value": flops / dt / 1e12, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+           "seconds": dt, "host_cpus": os.cpu_count()}
+    # also on all host cores (numpy's BLAS threads unrestricted; the
+    # oracle's small per-block products gain little from them)
+    t0 = time.perf_counter()
+    oracle.s_csr(oracle.sparsify(h))
+    dt_all = time.perf_counter() - t0
+    out["all_cores"] = {"value": flops / dt_all / 1e12, "cores": os.cpu_count(), "seconds": dt_all}
+    return out
 
 
 def run_reference(args, rank, world):
