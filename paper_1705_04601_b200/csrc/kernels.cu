@@ -2067,40 +2067,64 @@ __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const dou
                                                        const double *__restrict__ b, int64_t ldb, double *__restrict__ y,
                                                        int64_t ldy, double *__restrict__ zb, int64_t zbl, int nrhs, int B,
                                                        int *__restrict__ arrive, int64_t leaf0, int ldq) {
-  extern __shared__ __align__(16) double sQ[];   // n x ldq (ldq = max n + 1 <= 129)
+  // z = Q_t^T x_t with Q read straight from global memory (rows are coalesced
+  // across the threads of one column block): no shared-memory staging, so every
+  // leaf's CTA is resident at once (16 per SM) and the climb starts in one wave.
+  // Thread t = h n + j sums rows i = h, h + H, ... of column j (H = blockDim / n
+  // interleaved partial sums, added in a fixed order).
   __shared__ double sx[128];
+  __shared__ double red[128];
   __shared__ int s_go;
+  // metadata of every cluster this CTA may climb through (the leaf's ancestors)
+  // and of their children, in one round trip (level l in slot l)
+  __shared__ int m_n[64], m_k[64], m_k1[64];
+  __shared__ int64_t m_q[64], m_zb[64], m_loc[64], m_zb1[64], m_zb2[64];
+  (void)ldq;
   int level = 0;
   int64_t idx = leaf0 + blockIdx.x;  // in-level index (global)
+  for (int lv = threadIdx.x; lv <= L; lv += blockDim.x) {
+    const int64_t a = idx >> lv, cl = lvl_off_d(L, lv) + a;
+    m_n[lv] = sd.n[cl];
+    m_k[lv] = sd.k[cl];
+    m_q[lv] = sd.q_off[cl];
+    m_zb[lv] = sd.zb_off[cl];
+    m_loc[lv] = sd.loc_off[cl];
+    if (lv > 0) {
+      const int64_t c1 = lvl_off_d(L, lv - 1) + 2 * a;
+      m_k1[lv] = sd.k[c1];
+      m_zb1[lv] = sd.zb_off[c1];
+      m_zb2[lv] = sd.zb_off[c1 + 1];
+    }
+  }
+  __syncthreads();
   while (true) {
-    const int64_t cl = lvl_off_d(L, level) + idx;
-    const int n = sd.n[cl], k = sd.k[cl];
+    const int n = m_n[level], k = m_k[level];
     if (n > 0) {
-      const double *Q = q + sd.q_off[cl];
-      for (int e = threadIdx.x; e < n * n; e += blockDim.x) cp8(&sQ[(e / n) * ldq + e % n], Q + e, true);
-      cp_commit();
-      int64_t c1 = 0;
-      int k1 = 0;
-      if (level > 0) {
-        c1 = lvl_off_d(L, level - 1) + 2 * idx;
-        k1 = sd.k[c1];
-      }
+      const double *Q = q + m_q[level];
+      const int k1 = level > 0 ? m_k1[level] : 0;
+      const int H = blockDim.x / n;
+      const int t = threadIdx.x, j = t % n, h = t / n;
       for (int r = 0; r < nrhs; r++) {
         __syncthreads();
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
           double v;
           if (level == 0) v = b[((idx - leaf0) * B + i) + r * ldb];
-          else if (i < k1) v = __ldcg(zb + sd.zb_off[c1] + i + r * zbl);
-          else v = __ldcg(zb + sd.zb_off[c1 + 1] + (i - k1) + r * zbl);
+          else if (i < k1) v = __ldcg(zb + m_zb1[level] + i + r * zbl);
+          else v = __ldcg(zb + m_zb2[level] + (i - k1) + r * zbl);
           sx[i] = v;
         }
-        cp_wait_all();
         __syncthreads();
-        for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        if (h < H) {
           double acc = 0.0;
-          for (int i = 0; i < n; i++) acc = fma(sQ[i * ldq + j], sx[i], acc);
-          if (j < k) zb[sd.zb_off[cl] + j + r * zbl] = acc;
-          else y[sd.loc_off[cl] + (j - k) + r * ldy] = acc;
+          for (int i = h; i < n; i += H) acc = fma(__ldg(Q + int64_t(i) * n + j), sx[i], acc);
+          red[h * n + j] = acc;
+        }
+        __syncthreads();
+        if (t < n) {
+          double acc = red[t];
+          for (int u = 1; u < H; u++) acc += red[u * n + t];
+          if (t < k) zb[m_zb[level] + t + r * zbl] = acc;
+          else y[m_loc[level] + (t - k) + r * ldy] = acc;
         }
       }
     }
@@ -2126,20 +2150,41 @@ __global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, const doub
   extern __shared__ __align__(16) double sQ[];   // n x ldq (ldq = max n + 1 <= 129)
   __shared__ double sv[128];
   __shared__ double sw[128];
+  // metadata of the whole root -> leaf path in one round trip (level l in slot l),
+  // and the ancestors' Q pulled into L2 while the root levels run
+  __shared__ int p_n[64], p_k[64], p_k1[64];
+  __shared__ int64_t p_q[64], p_loc[64];
   const int64_t leaf = leaf0 + blockIdx.x;
+  for (int lv = threadIdx.x; lv <= L; lv += blockDim.x) {
+    const int64_t cl = lvl_off_d(L, lv) + (leaf >> lv);
+    p_n[lv] = sd.n[cl];
+    p_k[lv] = sd.k[cl];
+    p_q[lv] = sd.q_off[cl];
+    p_loc[lv] = sd.loc_off[cl];
+    p_k1[lv] = lv > 0 ? sd.k[lvl_off_d(L, lv - 1) + 2 * (leaf >> lv)] : 0;
+  }
+  __syncthreads();
+  for (int lv = 1; lv <= L; lv++) {  // upper-level Q blocks (the leaf's comes with its cp.async)
+    const int n = p_n[lv];
+    const double *Q = q + p_q[lv];
+    for (int e = threadIdx.x * 16; e < n * n; e += blockDim.x * 16)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(Q + e));
+  }
   for (int r = 0; r < nrhs; r++) {
     // walk the path root -> leaf; sv[0:k] holds the basis coefficients from the parent
     for (int level = L; level >= 0; level--) {
-      const int64_t idx = leaf >> level;
-      const int64_t cl = lvl_off_d(L, level) + idx;
-      const int n = sd.n[cl], k = sd.k[cl];
+      const int n = p_n[level], k = p_k[level];
       __syncthreads();
       if (n == 0) continue;
-      const double *Q = q + sd.q_off[cl];
-      for (int e = threadIdx.x; e < n * n; e += blockDim.x) cp8(&sQ[(e / n) * ldq + e % n], Q + e, true);
+      const double *Q = q + p_q[level];
+      {  // Q rows: warp w copies rows w, w + 4, ... (no per-element index division)
+        const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+        for (int i = threadIdx.x >> 5; i < n; i += nw)
+          for (int c = lane; c < n; c += 32) cp8(&sQ[i * ldq + c], Q + int64_t(i) * n + c, true);
+      }
       cp_commit();
       for (int j = threadIdx.x; j < n; j += blockDim.x)
-        if (j >= k) sv[j] = y[sd.loc_off[cl] + (j - k) + r * ldy];
+        if (j >= k) sv[j] = y[p_loc[level] + (j - k) + r * ldy];
       cp_wait_all();
       __syncthreads();
       if (level == 0) {
@@ -2150,8 +2195,7 @@ __global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, const doub
         }
       } else {
         // only the rows of the child on the path are needed
-        const int64_t c1 = lvl_off_d(L, level - 1) + 2 * idx;
-        const int k1 = sd.k[c1];
+        const int k1 = p_k1[level];
         const bool second = (leaf >> (level - 1)) & 1;
         const int rlo = second ? k1 : 0, rhi = second ? n : k1;
         for (int i = rlo + threadIdx.x; i < rhi; i += blockDim.x) {
@@ -2848,7 +2892,7 @@ h2sp_status launch_apply_Ut(const h2sp_plan_s *P, const double *q, const double 
   int *arrive = (int *)(ws + P->meta_bytes + ((size_t(std::max(P->zb_row_len, P->zb_col_len)) * nrhs * 8 + 255) / 256) * 256);
   H2SP_CK(cudaMemsetAsync(arrive, 0, size_t(P->ncl) * sizeof(int), st));
   const int ldq = apply_ldq(P);
-  apply_ut_kernel<<<unsigned(P->n_leaves_local), 128, size_t(ldq - 1) * ldq * 8, st>>>(
+  apply_ut_kernel<<<unsigned(P->n_leaves_local), 128, 0, st>>>(
       sd, P->L, q, b, ldb, y, ldy, zb, zbl, nrhs, P->B, arrive, P->first_leaf, ldq);
   H2SP_CK(cudaGetLastError());
   return H2SP_OK;
