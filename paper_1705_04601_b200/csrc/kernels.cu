@@ -2147,9 +2147,9 @@ __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const dou
 __global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, const double *__restrict__ q,
                                                       const double *__restrict__ y, int64_t ldy, double *__restrict__ x,
                                                       int64_t ldx, int nrhs, int B, int64_t leaf0, int ldq) {
-  extern __shared__ __align__(16) double sQ[];   // n x ldq (ldq = max n + 1 <= 129)
   __shared__ double sv[128];
   __shared__ double sw[128];
+  (void)ldq;
   // metadata of the whole root -> leaf path in one round trip (level l in slot l),
   // and the ancestors' Q pulled into L2 while the root levels run
   __shared__ int p_n[64], p_k[64], p_k1[64];
@@ -2164,47 +2164,53 @@ __global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, const doub
     p_k1[lv] = lv > 0 ? sd.k[lvl_off_d(L, lv - 1) + 2 * (leaf >> lv)] : 0;
   }
   __syncthreads();
-  for (int lv = 1; lv <= L; lv++) {  // upper-level Q blocks (the leaf's comes with its cp.async)
+  for (int lv = 1; lv <= L; lv++) {  // upper-level Q blocks (shared by many leaves)
     const int n = p_n[lv];
     const double *Q = q + p_q[lv];
     for (int e = threadIdx.x * 16; e < n * n; e += blockDim.x * 16)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(Q + e));
   }
   for (int r = 0; r < nrhs; r++) {
-    // walk the path root -> leaf; sv[0:k] holds the basis coefficients from the parent
+    // walk the path root -> leaf; sv[0:k] holds the basis coefficients from the parent.
+    // Q rows are read straight from global memory: H consecutive threads share a
+    // row (coalesced segments), partial sums over j = h, h + H, ... are added by
+    // a butterfly over those H lanes.
     for (int level = L; level >= 0; level--) {
       const int n = p_n[level], k = p_k[level];
       __syncthreads();
       if (n == 0) continue;
       const double *Q = q + p_q[level];
-      {  // Q rows: warp w copies rows w, w + 4, ... (no per-element index division)
-        const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-        for (int i = threadIdx.x >> 5; i < n; i += nw)
-          for (int c = lane; c < n; c += 32) cp8(&sQ[i * ldq + c], Q + int64_t(i) * n + c, true);
-      }
-      cp_commit();
       for (int j = threadIdx.x; j < n; j += blockDim.x)
         if (j >= k) sv[j] = y[p_loc[level] + (j - k) + r * ldy];
-      cp_wait_all();
       __syncthreads();
-      if (level == 0) {
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-          double acc = 0.0;
-          for (int j = 0; j < n; j++) acc = fma(sQ[i * ldq + j], sv[j], acc);
-          x[((leaf - leaf0) * B + i) + r * ldx] = acc;
-        }
-      } else {
-        // only the rows of the child on the path are needed
+      int rlo = 0, rhi = n;
+      if (level > 0) {  // only the rows of the child on the path are needed
         const int k1 = p_k1[level];
         const bool second = (leaf >> (level - 1)) & 1;
-        const int rlo = second ? k1 : 0, rhi = second ? n : k1;
-        for (int i = rlo + threadIdx.x; i < rhi; i += blockDim.x) {
-          double acc = 0.0;
-          for (int j = 0; j < n; j++) acc = fma(sQ[i * ldq + j], sv[j], acc);
-          sw[i - rlo] = acc;
+        rlo = second ? k1 : 0;
+        rhi = second ? n : k1;
+      }
+      const int rows = rhi - rlo;
+      int H = 1;
+      while (H < 32 && 2 * H * rows <= int(blockDim.x)) H *= 2;
+      for (int i0 = 0; i0 < rows; i0 += int(blockDim.x) / H) {
+        const int il = i0 + int(threadIdx.x) / H, h = threadIdx.x % H;
+        double acc = 0.0;
+        if (il < rows) {
+          const double *Qi = Q + int64_t(rlo + il) * n;
+          for (int j = h; j < n; j += H) acc = fma(__ldg(Qi + j), sv[j], acc);
         }
+        for (int o = H >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (h == 0 && il < rows) {
+          if (level == 0)
+            x[((leaf - leaf0) * B + il) + r * ldx] = acc;
+          else
+            sw[il] = acc;
+        }
+      }
+      if (level > 0) {
         __syncthreads();
-        for (int i = threadIdx.x; i < rhi - rlo; i += blockDim.x) sv[i] = sw[i];
+        for (int i = threadIdx.x; i < rows; i += blockDim.x) sv[i] = sw[i];
       }
     }
   }
@@ -2904,7 +2910,7 @@ h2sp_status launch_apply_V(const h2sp_plan_s *P, const double *q, const double *
   const Clusters cl = make_clusters(P, ws);
   const Side sd = side_of(cl, col_side);
   const int ldq = apply_ldq(P);
-  apply_v_kernel<<<unsigned(P->n_leaves_local), 128, size_t(ldq - 1) * ldq * 8, st>>>(
+  apply_v_kernel<<<unsigned(P->n_leaves_local), 128, 0, st>>>(
       sd, P->L, q, y, ldy, x, ldx, nrhs, P->B, P->first_leaf, ldq);
   H2SP_CK(cudaGetLastError());
   return H2SP_OK;
