@@ -2320,8 +2320,8 @@ static h2sp_status launch_strips(const StripArgs &a, int np, int tn, int64_t nti
 // stream, so a build stays stream-ordered (and CUDA-graph capturable).
 struct DeviceAux {
   bool init = false;
-  cudaStream_t side[7];    // QR/coupling chain, CSR, strips (set 0 / first half), main chain, strips (set 1),
-                           // strips (set 0, second half), h2sp_build_host's early CSR + D2H
+  cudaStream_t side[8];    // QR/coupling chain, CSR, strips (set 0 / first half), main chain, strips (set 1),
+                           // strips (set 0, second half), h2sp_build_host's early CSR + D2H, level-0 Q from V / M
   cudaEvent_t host_fork = nullptr, host_join = nullptr;
   std::vector<cudaEvent_t> ev;
 };
@@ -2352,6 +2352,7 @@ static h2sp_status get_aux(int L, DeviceAux **out) {
     H2SP_CK(cudaStreamCreateWithPriority(&a.side[4], cudaStreamNonBlocking, pr(off[2])));  // strips, set 1
     H2SP_CK(cudaStreamCreateWithPriority(&a.side[5], cudaStreamNonBlocking, pr(off[0])));  // strips, set 0 B
     H2SP_CK(cudaStreamCreateWithPriority(&a.side[6], cudaStreamNonBlocking, lo));  // build_host: early CSR + D2H
+    H2SP_CK(cudaStreamCreateWithPriority(&a.side[7], cudaStreamNonBlocking, hi < lo ? std::min(lo, hi + qr_off) : hi));
     H2SP_CK(cudaEventCreateWithFlags(&a.host_fork, cudaEventDisableTiming));
     H2SP_CK(cudaEventCreateWithFlags(&a.host_join, cudaEventDisableTiming));
     a.init = true;
@@ -2388,6 +2389,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   DeviceAux *aux = nullptr;
   if (h2sp_status e = get_aux(L, &aux)) return e;
   cudaStream_t s1 = aux->side[0], s2 = aux->side[1], s3 = aux->side[2], s4 = aux->side[4], s5 = aux->side[5];
+  cudaStream_t s7 = aux->side[7];
   const cudaStream_t user_st = st;
   cudaEvent_t ev_begin = aux->ev[6 + 2 * L], ev_end = aux->ev[7 + 2 * L];
   static const bool serial = [] {
@@ -2395,7 +2397,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     return e && e[0] == '1';
   }();
   if (serial) {
-    s1 = s2 = s3 = s4 = s5 = st;
+    s1 = s2 = s3 = s4 = s5 = s7 = st;
   } else {
     // the main chain runs on an internal high-priority stream forked from the
     // caller's stream (the CSR stream has the lowest priority and fills gaps)
@@ -2653,23 +2655,30 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     }
   }
   // ---- level-0 Q from V / M (compact-WY path): only an output and an input of
-  //      the applies, so it trails the QR / coupling chain on s1
+  //      the applies.  It needs only QR0, so it runs on its own stream (s7, the
+  //      QR chain's priority) right after QR0; the applies on s1 wait for it.
+  //      (Trailing the chain on s1 it delayed the applies -- on the step's
+  //      critical path -- by its own duration; first on s1 it delayed the chain.)
   if (P->wy_kp) {
-    if (h2sp_status e = pre(s1, qform_idx)) return e;
+    cudaEvent_t ev_qform = aux->ev[13 + 3 * L];
+    H2SP_CK(cudaStreamWaitEvent(s7, ev_qr0, 0));
+    if (h2sp_status e = pre(s7, qform_idx)) return e;
     const int64_t nleaf = int64_t(1) << L;
     const unsigned grid = unsigned(nleaf * (sym ? 1 : 2));
     if (P->wy_n == 128) {
       if (P->wy_kp == 16)
-        launch_wy_form_q<16, 128>(grid, s1, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf);
+        launch_wy_form_q<16, 128>(grid, s7, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf);
       else
-        launch_wy_form_q<32, 128>(grid, s1, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf);
+        launch_wy_form_q<32, 128>(grid, s7, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf);
     } else if (P->wy_kp == 16) {
-      launch_wy_form_q<16, 64>(grid, s1, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf);
+      launch_wy_form_q<16, 64>(grid, s7, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf);
     } else {
-      launch_wy_form_q<24, 64>(grid, s1, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf);
+      launch_wy_form_q<24, 64>(grid, s7, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf);
     }
     H2SP_CK(cudaGetLastError());
-    if (h2sp_status e = post(s1, qform_idx)) return e;
+    if (h2sp_status e = post(s7, qform_idx)) return e;
+    H2SP_CK(cudaEventRecord(ev_qform, s7));
+    H2SP_CK(cudaStreamWaitEvent(s1, ev_qform, 0));
   }
   // ---- the applies of the same pass (need Q only): on s1 after the QR chain
   cudaEvent_t ev_apply = aux->ev[8 + 2 * L];
