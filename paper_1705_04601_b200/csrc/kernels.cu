@@ -2684,11 +2684,25 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   cudaEvent_t ev_apply = aux->ev[8 + 2 * L];
   if (ap) {
     unsigned char *aws = static_cast<unsigned char *>(ap->ws);
+    // V w with w independent of U^T b's output: on s7 beside U^T b (both need
+    // only Q; V w uses neither the coefficient buffer nor the arrival counters)
+    const bool v_beside = ap->w && ap->b && ap->w != ap->y && s7 != s1;
+    cudaEvent_t ev_chain = aux->ev[14 + 3 * L], ev_v = aux->ev[15 + 3 * L];
+    if (v_beside) {
+      H2SP_CK(cudaEventRecord(ev_chain, s1));
+      H2SP_CK(cudaStreamWaitEvent(s7, ev_chain, 0));
+      if (h2sp_status e = launch_apply_V(P, sym ? out->q_row : q_col, ap->w, ap->ldw, ap->x, ap->ldx, ap->nrhs, aws,
+                                         s7, !sym))
+        return e;
+      H2SP_CK(cudaEventRecord(ev_v, s7));
+    }
     if (ap->b) {
       if (h2sp_status e = launch_apply_Ut(P, out->q_row, ap->b, ap->ldb, ap->y, ap->ldy, ap->nrhs, aws, s1, false))
         return e;
     }
-    if (ap->w) {
+    if (v_beside) {
+      H2SP_CK(cudaStreamWaitEvent(s1, ev_v, 0));
+    } else if (ap->w) {
       if (h2sp_status e = launch_apply_V(P, sym ? out->q_row : q_col, ap->w, ap->ldw, ap->x, ap->ldx, ap->nrhs, aws,
                                          s1, !sym))
         return e;

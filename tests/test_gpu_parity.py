@@ -332,6 +332,14 @@ def test_build_apply_matches_separate_calls(sym):
     torch.cuda.synchronize()
     assert torch.equal(s1, sp.outputs["s_val"])
     assert torch.equal(y1, y2) and torch.equal(x1, x2)
+    # independent w: V w runs beside U^T b on its own stream
+    w = torch.from_numpy(np.random.default_rng(6).standard_normal((2, h.N))).cuda()
+    x3 = torch.empty_like(b)
+    sp.apply_V(w, x3)
+    y4, x4 = torch.zeros_like(b), torch.zeros_like(b)
+    sp.build_apply(b, y4, w, x4, aws)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y4) and torch.equal(x3, x4)
 
 
 @pytest.mark.parametrize("name", ["cfg2-16384", "cfg3-16384", "rand-gen-B64"])
