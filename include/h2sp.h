@@ -258,8 +258,9 @@ h2sp_status h2sp_build_ex(h2sp_plan plan, const h2sp_inputs *in, const h2sp_outp
 
 /* One pass of the whole hot path (BASELINE.json north_star: "the same pass also
  * applies U^T b and V y"): h2sp_build plus y = U^T b and x = V w.  The applies
- * depend only on Q, so they run on the build's QR side stream right after the
- * QR chain, overlapping the congruence and strips.  Either apply is skipped if
+ * depend only on Q, so they run on the build's side streams right after the
+ * QR chain, overlapping the congruence and strips (V w beside U^T b when w is
+ * not y; after it when w == y).  Either apply is skipped if
  * its input pointer is NULL; w may be y (then x = V U^T b).  `ws` of the apply
  * must be a DIFFERENT uploaded workspace (>= h2sp_apply_ws_bytes(nrhs)) than
  * the build's.  Layouts as in h2sp_apply_Ut / h2sp_apply_V.  `events` as in
