@@ -38,7 +38,7 @@ import numpy as np
 __all__ = [
     "H2Input", "CONFIGS", "lvl_off", "cid", "make_points", "kd_tree", "block_tree",
     "make_config", "random_h2", "axis_aligned_h2", "fig3_h2", "eta0_h2",
-    "kernel_matrix", "pack",
+    "kernel_matrix", "pack", "coupling_block_descs",
 ]
 
 
@@ -340,7 +340,7 @@ def _pairs_same(near0):
 
 
 def make_config(idx: int, seed: Optional[int] = None, N: Optional[int] = None, method: Optional[str] = None,
-                with_close: bool = True) -> H2Input:
+                with_close: bool = True, with_couplings: bool = True) -> H2Input:
     """BASELINE.json ``configs[idx-1]`` with ``seed = idx`` (reading 17).  ``N``
     may be overridden to make smaller instances of the same recipe."""
     cfg = CONFIGS[idx]
@@ -359,7 +359,7 @@ def make_config(idx: int, seed: Optional[int] = None, N: Optional[int] = None, m
     if meth == "svd":
         h2 = _svd_h2(x, L, B, r, near0, adm, kspec, sym)
     else:
-        h2 = _cheb_h2(x, L, B, r, near0, adm, kspec, lo, hi, sym, with_close)
+        h2 = _cheb_h2(x, L, B, r, near0, adm, kspec, lo, hi, sym, with_close, with_couplings)
         if cfg.get("orthonormalize"):
             orthonormalize_h2(h2)
     h2.meta.update(config=idx, seed=seed, N=N, eta=eta, method=meth, kernel=kspec)
@@ -403,7 +403,7 @@ def _mirror_close(near0, close):
     return close
 
 
-def _cheb_h2(x, L, B, r, near0, adm, kspec, lo, hi, sym, with_close=True) -> H2Input:
+def _cheb_h2(x, L, B, r, near0, adm, kspec, lo, hi, sym, with_close=True, with_couplings=True) -> H2Input:
     ncl = n_clusters(L)
     rank_row = far_ranks(L, near0, adm, r, r, 0)
     rank_col = far_ranks(L, near0, adm, r, r, 1)
@@ -443,8 +443,8 @@ def _cheb_h2(x, L, B, r, near0, adm, kspec, lo, hi, sym, with_close=True) -> H2I
         clc, leaf_col, tr_col = clr, leaf_row, tr_row
     else:
         clc, leaf_col, tr_col = side(rank_col, 2)
-    coupling = []
-    for k in range(L):
+    coupling = [] if with_couplings else None
+    for k in range(L if with_couplings else 0):
         lst = []
         base = lvl_off(L, k)
         for (t, s) in adm[k]:
@@ -460,9 +460,48 @@ def _cheb_h2(x, L, B, r, near0, adm, kspec, lo, hi, sym, with_close=True) -> H2I
     close = _close_blocks(x, B, near0, kspec) if with_close else None
     if sym and close is not None:
         close = _mirror_close(near0, close)
-    return H2Input(L=L, B=B, symmetric=sym, rank_row=rank_row, rank_col=rank_col, leaf_row=leaf_row,
-                   leaf_col=leaf_col, transfer_row=tr_row, transfer_col=tr_col, near=near0, close=close,
-                   adm=adm, coupling=coupling, points=x)
+    h2 = H2Input(L=L, B=B, symmetric=sym, rank_row=rank_row, rank_col=rank_col, leaf_row=leaf_row,
+                 leaf_col=leaf_col, transfer_row=tr_row, transfer_col=tr_col, near=near0, close=close,
+                 adm=adm, coupling=coupling, points=x)
+    # interpolation nodes of every cluster (None where rank 0): the couplings are
+    # D_b = K(nodes_t, nodes_s), so they can also be evaluated on the device
+    h2.meta["cheb_nodes_row"] = [c.nodes if c is not None else None for c in clr]
+    h2.meta["cheb_nodes_col"] = [c.nodes if c is not None else None for c in clc]
+    return h2
+
+
+def coupling_block_descs(h2: H2Input):
+    """Layout of the couplings as kernel blocks (pure data movement, no kernel
+    arithmetic): flat row / column node arrays, and per admissible pair in the
+    `coupling` input order (level-major, CSR by row cluster) the int64 record
+    (x_off, y_off, out_off, nx | ny << 32) of include/h2sp.h h2sp_block_desc.
+    Needs a Chebyshev-built H2Input (meta cheb_nodes_*)."""
+    L = h2.L
+
+    def flat(nodes):
+        offs = np.zeros(len(nodes), dtype=np.int64)
+        parts, o = [], 0
+        for c, nd in enumerate(nodes):
+            offs[c] = o
+            if nd is not None:
+                parts.append(nd)
+                o += len(nd)
+        d = parts[0].shape[1] if parts else 1
+        return (np.ascontiguousarray(np.concatenate(parts), dtype=np.float64) if parts else np.zeros((0, d))), offs
+
+    xr, offr = flat(h2.meta["cheb_nodes_row"])
+    xc, offc = flat(h2.meta["cheb_nodes_col"])
+    rec = []
+    out = 0
+    for k in range(L):
+        base = lvl_off(L, k)
+        for (t, s) in h2.adm[k]:
+            ct, cs = base + int(t), base + int(s)
+            nx, ny = int(h2.rank_row[ct]), int(h2.rank_col[cs])
+            rec.append((offr[ct], offc[cs], out, nx | (ny << 32)))
+            out += nx * ny
+    desc = np.array(rec, dtype=np.int64).reshape(-1, 4)
+    return xr, xc, desc, out
 
 
 def _svd_h2(x, L, B, r, near0, adm, kspec, sym) -> H2Input:
@@ -845,6 +884,6 @@ def pack(h2: H2Input) -> dict:
         leaf_row=cat(h2.leaf_row), transfer_row=cat([h2.transfer_row[c] for c in range(ncl)]),
         leaf_col=cat(h2.leaf_col), transfer_col=cat([h2.transfer_col[c] for c in range(ncl)]),
         close=np.ascontiguousarray(h2.close, dtype=np.float64).ravel() if h2.close is not None else None,
-        coupling=cat([m for lst in h2.coupling for m in lst]),
+        coupling=cat([m for lst in h2.coupling for m in lst]) if h2.coupling is not None else None,
     )
     return out

@@ -136,6 +136,21 @@ typedef struct {
   double p1;
 } h2sp_close_gen;
 
+/* Kernel blocks on the device (first piece of GPU H^2
+ * construction): out[b] (nx x ny, row-major at out_off) = K(x_i, y_j) with
+ * x_i = x_nodes row x_off + i, y_j = y_nodes row y_off + j (dim columns each),
+ * for the kernels of h2sp_close_gen, whose `points` is ignored here (the "same
+ * point" term never applies).  With the Chebyshev nodes of the cluster boxes this is the
+ * coupling D_b = K(nodes_t, nodes_s) of the interpolation H^2 construction
+ * (configs 2-5), evaluated where the build consumes it instead of on the host.
+ * All pointers DEVICE except `k` (host); asynchronous on `stream`. */
+typedef struct {
+  int64_t x_off, y_off, out_off;
+  int32_t nx, ny;
+} h2sp_block_desc;
+h2sp_status h2sp_eval_kernel_blocks(const h2sp_close_gen *k, const double *x_nodes, const double *y_nodes,
+                                    const h2sp_block_desc *blocks, int64_t n_blocks, double *out, void *stream);
+
 /* Numeric inputs (DEVICE pointers, read-only, row-major FP64):
  *   leaf_basis_row: R_t of every leaf, B x k_t each, concatenated by leaf.
  *   transfer_row:   T_p of every internal cluster, (k_c1 + k_c2) x k_p each

@@ -17,7 +17,8 @@ from typing import Dict, Optional
 
 import numpy as np
 
-__all__ = ["LIB_PATH", "H2spError", "Plan", "Sparsifier", "lib", "declared_symbols", "close_gen_params"]
+__all__ = ["LIB_PATH", "H2spError", "Plan", "Sparsifier", "lib", "declared_symbols", "close_gen_params",
+           "eval_kernel_blocks"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libh2sp.so")
@@ -110,6 +111,7 @@ lib.h2sp_build_apply.argtypes = [_vp, ctypes.POINTER(_Inputs), ctypes.POINTER(_O
                                  ctypes.POINTER(_ApplyArgs), _vp, ctypes.POINTER(_vp), _i64]
 lib.h2sp_build_host.argtypes = [_vp, ctypes.POINTER(_Inputs), ctypes.POINTER(_Outputs), ctypes.POINTER(_Inputs),
                                 ctypes.POINTER(_Outputs), _vp, ctypes.c_size_t, _vp]
+lib.h2sp_eval_kernel_blocks.argtypes = [ctypes.POINTER(_CloseGen), _vp, _vp, _vp, _i64, _vp, _vp]
 lib.h2sp_apply_ws_bytes.argtypes = [_vp, ctypes.c_int]
 lib.h2sp_apply_ws_bytes.restype = _i64
 lib.h2sp_apply_Ut.argtypes = [_vp, _vp, _vp, _i64, _vp, _i64, ctypes.c_int, _vp, ctypes.c_size_t, _vp]
@@ -237,6 +239,18 @@ class Plan:
         return rowptr, col
 
 
+def eval_kernel_blocks(kspec: dict, x_nodes, y_nodes, descs, out, stream=None):
+    """h2sp_eval_kernel_blocks: out[b] = K(x_nodes[x_off + i], y_nodes[y_off + j]) for
+    every block record of ``descs`` (int64 CUDA tensor, 4 words per block, see
+    h2gen.coupling_block_descs); x_nodes / y_nodes: (n, d) float64 CUDA tensors."""
+    kid, p0, p1 = close_gen_params(kspec)
+    g = _CloseGen(points=None, dim=int(x_nodes.shape[1]), kernel=kid, p0=p0, p1=p1)
+    _check(lib.h2sp_eval_kernel_blocks(ctypes.byref(g), _dptr(x_nodes), _dptr(y_nodes), _dptr(descs),
+                                       int(descs.shape[0]), _dptr(out), _stream_handle(stream)),
+           "h2sp_eval_kernel_blocks")
+    return out
+
+
 def _dptr(t) -> Optional[int]:
     return None if t is None else t.data_ptr()
 
@@ -282,7 +296,7 @@ class Sparsifier:
             for abi, key, szk in names:
                 n = int(sz[szk])
                 t = torch.empty(max(n, 1), **f64)
-                if packed is not None and n:
+                if packed is not None and n and packed.get(key) is not None:
                     src = np.ascontiguousarray(packed[key], dtype=np.float64).ravel()
                     if src.size != n:
                         raise ValueError(f"input {key}: {src.size} values, plan expects {n}")

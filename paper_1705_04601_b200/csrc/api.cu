@@ -161,6 +161,18 @@ h2sp_status h2sp_build_host(h2sp_plan P, const h2sp_inputs *hi, const h2sp_outpu
   return H2SP_OK;
 }
 
+h2sp_status h2sp_eval_kernel_blocks(const h2sp_close_gen *k, const double *x_nodes, const double *y_nodes,
+                                    const h2sp_block_desc *blocks, int64_t n_blocks, double *out, void *stream) {
+  if (!k || n_blocks < 0) return fail(H2SP_EINVAL, "NULL kernel descriptor or n_blocks < 0");
+  if (n_blocks > 0 && (!x_nodes || !y_nodes || !blocks || !out)) return fail(H2SP_EINVAL, "NULL device array");
+  if (k->dim < 1 || k->dim > 3) return fail(H2SP_EINVAL, "kernel blocks: dim must be 1, 2 or 3");
+  if (k->kernel < H2SP_KERNEL_EXP || k->kernel > H2SP_KERNEL_LAPLACE)
+    return fail(H2SP_EINVAL, "kernel blocks: unknown kernel id " + std::to_string(k->kernel));
+  if (k->kernel == H2SP_KERNEL_EXP && !(k->p0 > 0.0)) return fail(H2SP_EINVAL, "kernel blocks: exp length p0 <= 0");
+  if (h2sp_status s = check_device()) return s;
+  return launch_kernel_blocks(k, x_nodes, y_nodes, blocks, n_blocks, out, stream);
+}
+
 int64_t h2sp_apply_ws_bytes(h2sp_plan P, int nrhs) {
   if (!P || nrhs < 0) return -1;
   int64_t z = P->zb_row_len > P->zb_col_len ? P->zb_row_len : P->zb_col_len;

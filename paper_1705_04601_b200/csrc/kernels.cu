@@ -1172,6 +1172,58 @@ __device__ __forceinline__ void gen_close_tile(double *sG, const CloseGen &g, in
   for (int i = threadIdx.x / NP; i < NP; i += blockDim.x / NP) sG[i * LD + c.j] = gen_entry(g, c, i);
 }
 
+// h2sp_eval_kernel_blocks: one CTA per block, threads over its entries (same
+// distance arithmetic as gen_entry, so K(x, y) == K(y, x) bitwise).
+__global__ void __launch_bounds__(128) kernel_blocks_kernel(CloseGen g, const double *__restrict__ xn,
+                                                            const double *__restrict__ yn,
+                                                            const h2sp_block_desc *__restrict__ blocks,
+                                                            double *__restrict__ out) {
+  const h2sp_block_desc bd = blocks[blockIdx.x];
+  const int ne = bd.nx * bd.ny;
+  for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+    const int i = e / bd.ny, j = e - i * bd.ny;
+    const double *x = xn + (bd.x_off + i) * g.dim, *y = yn + (bd.y_off + j) * g.dim;
+    const double d0 = __dsub_rn(__ldg(x), __ldg(y));
+    double r2 = __dmul_rn(d0, d0);
+    if (g.dim > 1) {
+      const double d1 = __dsub_rn(__ldg(x + 1), __ldg(y + 1));
+      r2 = __dadd_rn(r2, __dmul_rn(d1, d1));
+    }
+    if (g.dim > 2) {
+      const double d2 = __dsub_rn(__ldg(x + 2), __ldg(y + 2));
+      r2 = __dadd_rn(r2, __dmul_rn(d2, d2));
+    }
+    const double ir = rsqrt(r2);
+    double v;
+    if (g.kind == H2SP_KERNEL_LAPLACE) {
+      v = g.q0 * ir;
+    } else {
+      const double r = r2 > 0.0 ? r2 * ir : 0.0;
+      v = g.kind == H2SP_KERNEL_EXP ? exp(r * g.q0) : 1.0 / (r + g.p0);
+    }
+    out[bd.out_off + e] = v;
+  }
+}
+
+h2sp_status launch_kernel_blocks(const h2sp_close_gen *k, const double *xn, const double *yn,
+                                 const h2sp_block_desc *blocks, int64_t n_blocks, double *out, void *stream) {
+  if (n_blocks == 0) return H2SP_OK;
+  CloseGen g;
+  g.pts = nullptr;
+  g.dim = k->dim;
+  g.kind = k->kernel;
+  g.p0 = k->p0;
+  g.p1 = k->p1;
+  g.q0 = g.kind == H2SP_KERNEL_EXP ? -1.0 / g.p0 : 1.0 / (4.0 * 3.141592653589793);
+  for (int64_t b0 = 0; b0 < n_blocks; b0 += (int64_t(1) << 30)) {
+    const int64_t nb = std::min<int64_t>(n_blocks - b0, int64_t(1) << 30);
+    kernel_blocks_kernel<<<unsigned(nb), 128, 0, (cudaStream_t)stream>>>(g, xn, yn, blocks + b0, out);
+    const cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return fail(H2SP_ECUDA, std::string("kernel blocks: ") + cudaGetErrorString(err));
+  }
+  return H2SP_OK;
+}
+
 // Level-0 G = C_ts: cp.async copy of the stored block, or evaluated (close_gen).
 template <int NP, int LD, bool GEN>
 __device__ __forceinline__ void load_close(const PairArgs &A, const PairItem &it, double *sG) {

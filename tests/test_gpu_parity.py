@@ -455,6 +455,48 @@ def test_close_gen_build_host_e2e():
         assert torch.equal(host_out[k], ref[k].cpu()), k
 
 
+@pytest.mark.parametrize("cfg,N", [(2, 16384), (3, 16384), (5, 16384)])
+def test_device_couplings_match_generator(cfg, N):
+    """SURVEY §8(f) #2, first piece of GPU H^2 construction: h2sp_eval_kernel_blocks
+    evaluates the interpolation couplings D_b = K(nodes_t, nodes_s) on the device.
+    They match the generator's numpy values to rounding, D_st = D_ts^T bitwise in
+    symmetric mode, and a build fed with them matches the oracle."""
+    _need_gpu()
+    import paper_1705_04601_b200 as h2sp
+    h = h2gen.make_config(cfg, N=N)
+    packed = h2gen.pack(h)
+    xr, xc, desc, n = h2gen.coupling_block_descs(h)
+    dev = torch.empty(n, dtype=torch.float64, device="cuda")
+    h2sp.eval_kernel_blocks(h.meta["kernel"], torch.from_numpy(xr).cuda(), torch.from_numpy(xc).cuda(),
+                            torch.from_numpy(desc).cuda(), dev)
+    torch.cuda.synchronize()
+    ref = torch.from_numpy(packed["coupling"]).cuda()
+    assert float(torch.linalg.norm(dev - ref)) <= 1e-14 * float(torch.linalg.norm(ref))
+    if h.symmetric:
+        from h2gen import lvl_off
+        d = desc
+        pos = {}
+        i = 0
+        for k in range(h.L):
+            for (t, s) in h.adm[k]:
+                pos[(k, int(t), int(s))] = i
+                i += 1
+        dv = dev.cpu().numpy()
+        for (k, t, s), b in list(pos.items())[:4000]:
+            if t < s:
+                b2 = pos[(k, s, t)]
+                nx, ny = int(d[b, 3] & 0xffffffff), int(d[b, 3] >> 32)
+                A = dv[d[b, 2]:d[b, 2] + nx * ny].reshape(nx, ny)
+                Bm = dv[d[b2, 2]:d[b2, 2] + nx * ny].reshape(ny, nx)
+                assert np.array_equal(A, Bm.T)
+    plan = h2sp.Plan(packed)
+    sp = h2sp.Sparsifier(plan, packed)
+    sp.inputs["coupling"][:n].copy_(dev)
+    out = sp.build()
+    torch.cuda.synchronize()
+    _compare(h, plan, out)
+
+
 def _csr_spmv(out, nnz, n_rows, z, chunks=16):
     """S z with S the GPU CSR output (test infrastructure: torch sparse SpMV over
     row chunks, int32 column indices widened per chunk)."""
