@@ -202,3 +202,18 @@ def test_close_gen_descriptor_validation():
     assert h2sp.close_gen_params({"kind": "invh", "h": 0.5, "diag_add": 1.0}) == (2, 0.5, 1.0)
     k, p0, p1 = h2sp.close_gen_params({"kind": "laplace", "h": 0.25})
     assert k == 3 and p1 == pytest.approx(1.0 / np.pi)
+
+
+def test_coupling_block_descs_layout():
+    """h2gen.coupling_block_descs (the input of h2sp_eval_kernel_blocks) describes
+    exactly the generator's coupling layout: evaluating the kernel on the
+    described node blocks on the host reproduces pack()'s `coupling` bitwise."""
+    h = h2gen.make_config(2, N=4096)
+    packed = h2gen.pack(h)
+    xr, xc, desc, n = h2gen.coupling_block_descs(h)
+    assert n == packed["coupling"].size
+    out = np.empty(n)
+    for x_off, y_off, o, nn in desc:
+        nx, ny = int(nn & 0xffffffff), int(nn >> 32)
+        out[o:o + nx * ny] = h2gen.kernel_matrix(h.meta["kernel"], xr[x_off:x_off + nx], xc[y_off:y_off + ny]).ravel()
+    assert np.array_equal(out, packed["coupling"])
