@@ -1915,8 +1915,11 @@ struct StripCfg {
   // (__launch_bounds__(512, 1) let NP = 48 / 64 grow to 76 registers = one CTA
   // per SM: 1.35x slower strips on the config-5 recipe).
   static constexpr bool SMALL = NP == 32 && TN == 128;
+  // NP == 48: aliasing the group array alone (no hint, 54 registers) fits 3 CTAs
+  // per SM instead of 2 (74 KB of shared memory each)
+  static constexpr bool ALIAS = SMALL || (NP == 48 && TN == 128);
   static constexpr int MIN_BLOCKS = SMALL ? STRIP_MINB : 0;
-  static constexpr size_t SMEM = (size_t(NP) * LDQ + size_t(NP) * LDZ) * sizeof(double) + TN * 16 + (SMALL ? 0 : 64);
+  static constexpr size_t SMEM = (size_t(NP) * LDQ + size_t(NP) * LDZ) * sizeof(double) + TN * 16 + (ALIAS ? 0 : 64);
   static_assert(size_t(NP) * LDZ * sizeof(double) >= (TN + 1) * sizeof(StripGroup), "groups alias sZ");
 };
 
@@ -1939,9 +1942,9 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
   int64_t *tdst = reinterpret_cast<int64_t *>(sZ + NP * C::LDZ);  // per column: transposed S dst (b*ld folded in)
   int32_t *src1 = reinterpret_cast<int32_t *>(tdst + TN);          // per column: column in child-1 panel or -1
   int32_t *src2 = src1 + TN;
-  __shared__ StripGroup sg_own[C::SMALL ? 1 : TN + 1];
+  __shared__ StripGroup sg_own[C::ALIAS ? 1 : TN + 1];
   // groups overlapping this tile (<= TN + 1); when aliased, dead before the gather
-  StripGroup *sg = C::SMALL ? reinterpret_cast<StripGroup *>(sZ) : sg_own;
+  StripGroup *sg = C::ALIAS ? reinterpret_cast<StripGroup *>(sZ) : sg_own;
   __shared__ __align__(16) StripTileX s_tile;
   // round trip 1: the self-contained tile descriptor
   if (threadIdx.x < sizeof(StripTileX) / 16)
