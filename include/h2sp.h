@@ -109,6 +109,13 @@ typedef struct {
   double flops_congruence;     /* of which: congruence H = Q^T G Q             */
   double flops_strips;         /* of which: strip rotations                    */
   double flops_executed;       /* FP64 flops actually issued (<= flops)        */
+  double flops_unique;         /* sharded plan: the part of `flops` whose row /
+                                  rotating cluster this shard owns (the shards'
+                                  flops_unique add up to the unsharded flops;
+                                  flops - flops_unique is halo / mirror work
+                                  done twice).  = flops when world = 1.        */
+  int64_t bench_parts;         /* H2SP_PLAN_BENCH: partial slots (16 B each) in
+                                  the workspace; 0 otherwise                   */
 } h2sp_sizes;
 
 /* Matrix-free close blocks ("close_gen" mode, SURVEY §8(d) config-5 protocol
@@ -134,6 +141,16 @@ typedef struct {
   int32_t kernel;
   double p0;
   double p1;
+  /* Matrix-free far couplings (optional, config-5 protocol): with
+   * h2sp_inputs.coupling == NULL, D_b = K(nodes_t, nodes_s) is evaluated inside
+   * the coupling step (D~ = R^_t D R^_s^T) -- the interpolation H^2
+   * construction's couplings (SURVEY §8(d) generator), never stored (config 5:
+   * 130 GB).  nodes_row: DEVICE, (sum_c k_row[c]) x dim doubles, the k_c nodes
+   * of every cluster in level-major cluster order (rank-0 clusters have none);
+   * nodes_col likewise for the column side (NULL if symmetric).  Same
+   * arithmetic as h2sp_eval_kernel_blocks.  Both NULL: couplings are read. */
+  const double *nodes_row;
+  const double *nodes_col;
 } h2sp_close_gen;
 
 /* Kernel blocks on the device (first piece of GPU H^2
@@ -165,7 +182,7 @@ typedef struct {
   const double *leaf_basis_col;
   const double *transfer_col;
   const double *close;         /* ignored (may be NULL) when close_gen != NULL  */
-  const double *coupling;
+  const double *coupling;      /* NULL: evaluated from close_gen->nodes_*       */
   const h2sp_close_gen *close_gen;  /* HOST pointer to the descriptor, or NULL */
 } h2sp_inputs;
 
@@ -183,11 +200,23 @@ typedef struct {
   int64_t *s_rowptr;
   int32_t *s_col;
   double *s_val;
+  /* Bench mode (plan flag H2SP_PLAN_BENCH, SURVEY §8(b)/(d) config-5 protocol
+   * step 3): S is not stored (s_val / s_col ignored, may be NULL).  Every S
+   * block is reduced, in the congruence and strip epilogues, to one partial
+   * {sum_j S[i][j] w[j], sum_j S[i][j]^2} per block row i; a final pass sums a
+   * row's partials in block order (no atomics: bitwise reproducible, and
+   * independent of the shard count).  All DEVICE, global S order, N entries:
+   *   bench_w  (in)  w, indexed by S column (column-side S order)
+   *   bench_y  (out) y = S w at this plan's S rows (other rows untouched)
+   *   bench_r2 (out) ||S[i, :]||_2^2 at this plan's S rows (may be NULL)     */
+  const double *bench_w;
+  double *bench_y;
+  double *bench_r2;
 } h2sp_outputs;
 
 /* Symbolic phase (host, O(#blocks)): validates the structure and derives all
  * sizes, S offsets, the S block pattern, CSR row pointers and the per-level
- * work lists.  flags: 0 or H2SP_PLAN_EXPLICIT_Q. */
+ * work lists.  flags: 0 or any of H2SP_PLAN_EXPLICIT_Q, H2SP_PLAN_BENCH. */
 h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out);
 
 /* Plan flags.  By default the level-0 congruence H = Q_t^T G Q_s (n_t = B <= 64,
@@ -197,6 +226,10 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
  * rounding (and exactly equal when every Q is a permutation).
  * H2SP_PLAN_EXPLICIT_Q forces the explicit-Q product at every level. */
 #define H2SP_PLAN_EXPLICIT_Q 1
+/* Bench mode: S is reduced to y = S w and the row norms ||S[i,:]||^2 (see
+ * h2sp_outputs) instead of being stored -- config 5's S is ~2 TB.  The plan
+ * builds no CSR column pattern; s_rowptr may still be written. */
+#define H2SP_PLAN_BENCH 2
 /* Sharded plan: rank `rank` of `world` (a power of two <= 2^L)
  * owns the top-level subtree of cluster `rank` at the partition level
  * Lp = L - log2(world): S rows of its clusters, the congruences whose row cluster
@@ -226,7 +259,7 @@ void h2sp_plan_destroy(h2sp_plan plan);
 /* Description of the kernel launches of one h2sp_build, in launch order
  * (kind: 0 QR row side, 1 QR column side, 2 couplings, 3 merge+congruence+
  * freeze, 4 row strips, 5 column strips, 6 CSR index expansion, 7 level-0 Q
- * formed from its compact-WY factors, both sides).  flops and
+ * formed from its compact-WY factors, both sides, 8 bench-mode row sums).  flops and
  * bytes are the algorithmic FP64 flops and HBM bytes of that launch
  * (SURVEY §8(d) per-unit figures x units in the launch); items = work units;
  * flops_exec = the FP64 flops the kernel actually issues (differs from flops
@@ -296,6 +329,18 @@ typedef struct {
 h2sp_status h2sp_build_apply(h2sp_plan plan, const h2sp_inputs *in, const h2sp_outputs *out, void *ws,
                              size_t ws_bytes, const h2sp_apply_args *ap, void *stream, void *const *events,
                              int64_t n_events);
+
+/* h2sp_build_apply with the plan's work lists and the rest of the workspace in
+ * separate device buffers: `meta` (sizes.meta_bytes, filled by h2sp_plan_upload)
+ * and `scratch` (>= sizes.workspace_bytes - sizes.meta_bytes bytes), both
+ * 256-byte aligned.  Several plans -- the virtual shards of one matrix
+ * (SURVEY §8(d) config-5 protocol step 2) -- can keep their work lists resident
+ * and take turns on one scratch buffer (builds ordered on one stream).  `ap`
+ * may be NULL (no applies); otherwise ap->ws is the applies' scratch only (no
+ * meta at its head), >= h2sp_apply_ws_bytes(nrhs) - sizes.meta_bytes bytes. */
+h2sp_status h2sp_build_meta(h2sp_plan plan, const h2sp_inputs *in, const h2sp_outputs *out, const void *meta,
+                            void *scratch, size_t scratch_bytes, const h2sp_apply_args *ap, void *stream,
+                            void *const *events, int64_t n_events);
 
 /* End-to-end variant with HOST buffers: copies the host inputs into the given
  * device input buffers, builds, and copies every output back into the host

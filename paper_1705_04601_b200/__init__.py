@@ -43,7 +43,8 @@ class _Sizes(ctypes.Structure):
                                     "coupling", "q_row", "q_col", "s_nnz", "s_rows", "rank", "world", "first_leaf",
                                     "n_leaves_local", "s_blocks", "workspace_bytes", "meta_bytes",
                                     "levels_active", "launches")] + \
-               [(n, _f64) for n in ("flops", "bytes", "flops_congruence", "flops_strips", "flops_executed")]
+               [(n, _f64) for n in ("flops", "bytes", "flops_congruence", "flops_strips", "flops_executed",
+                                    "flops_unique")] + [("bench_parts", _i64)]
 
 
 class _LaunchInfo(ctypes.Structure):
@@ -51,7 +52,9 @@ class _LaunchInfo(ctypes.Structure):
 
 
 PLAN_EXPLICIT_Q = 1   # include/h2sp.h H2SP_PLAN_EXPLICIT_Q
-LAUNCH_KINDS = ("qr_row", "qr_col", "coupling", "congruence", "strips_row", "strips_col", "csr", "q_form")
+PLAN_BENCH = 2        # include/h2sp.h H2SP_PLAN_BENCH
+LAUNCH_KINDS = ("qr_row", "qr_col", "coupling", "congruence", "strips_row", "strips_col", "csr", "q_form",
+                "bench_reduce")
 
 
 class _ApplyArgs(ctypes.Structure):
@@ -65,7 +68,8 @@ class _Inputs(ctypes.Structure):
 
 
 class _CloseGen(ctypes.Structure):
-    _fields_ = [("points", _vp), ("dim", _i32), ("kernel", _i32), ("p0", _f64), ("p1", _f64)]
+    _fields_ = [("points", _vp), ("dim", _i32), ("kernel", _i32), ("p0", _f64), ("p1", _f64), ("nodes_row", _vp),
+                ("nodes_col", _vp)]
 
 
 KERNEL_IDS = {"exp": 1, "invh": 2, "laplace": 3}   # include/h2sp.h H2SP_KERNEL_*
@@ -86,7 +90,7 @@ def close_gen_params(kspec: dict):
 
 
 class _Outputs(ctypes.Structure):
-    _fields_ = [(n, _vp) for n in ("q_row", "q_col", "s_rowptr", "s_col", "s_val")]
+    _fields_ = [(n, _vp) for n in ("q_row", "q_col", "s_rowptr", "s_col", "s_val", "bench_w", "bench_y", "bench_r2")]
 
 
 _st = ctypes.c_int
@@ -109,6 +113,8 @@ lib.h2sp_build_ex.argtypes = [_vp, ctypes.POINTER(_Inputs), ctypes.POINTER(_Outp
 lib.h2sp_plan_launches.argtypes = [_vp, ctypes.POINTER(_LaunchInfo), _i64, ctypes.POINTER(_i64)]
 lib.h2sp_build_apply.argtypes = [_vp, ctypes.POINTER(_Inputs), ctypes.POINTER(_Outputs), _vp, ctypes.c_size_t,
                                  ctypes.POINTER(_ApplyArgs), _vp, ctypes.POINTER(_vp), _i64]
+lib.h2sp_build_meta.argtypes = [_vp, ctypes.POINTER(_Inputs), ctypes.POINTER(_Outputs), _vp, _vp, ctypes.c_size_t,
+                                ctypes.POINTER(_ApplyArgs), _vp, ctypes.POINTER(_vp), _i64]
 lib.h2sp_build_host.argtypes = [_vp, ctypes.POINTER(_Inputs), ctypes.POINTER(_Outputs), ctypes.POINTER(_Inputs),
                                 ctypes.POINTER(_Outputs), _vp, ctypes.c_size_t, _vp]
 lib.h2sp_eval_kernel_blocks.argtypes = [ctypes.POINTER(_CloseGen), _vp, _vp, _vp, _i64, _vp, _vp]
@@ -148,7 +154,7 @@ class Plan:
     rank_col, near_ptr, near_col, adm_ptr[k], adm_col[k]).  ``explicit_q``
     sets H2SP_PLAN_EXPLICIT_Q (no compact-WY level-0 congruence)."""
 
-    def __init__(self, packed: dict, rank: int = 0, world: int = 1, explicit_q: bool = False):
+    def __init__(self, packed: dict, rank: int = 0, world: int = 1, explicit_q: bool = False, bench: bool = False):
         self._keep = []
         L = int(packed["L"])
         rr = np.ascontiguousarray(packed["rank_row"], dtype=np.int32)
@@ -165,9 +171,10 @@ class Plan:
                         rank_row=_ptr(rr, _i32), rank_col=_ptr(rc, _i32) if rc is not None else None,
                         near_ptr=_ptr(npt, _i64), near_col=_ptr(ncl, _i32), adm_ptr=ap_arr, adm_col=ac_arr)
         h = _vp()
-        _check(lib.h2sp_plan_create_shard(ctypes.byref(st), int(rank), int(world), PLAN_EXPLICIT_Q if explicit_q else 0,
-                                          ctypes.byref(h)),
+        flags = (PLAN_EXPLICIT_Q if explicit_q else 0) | (PLAN_BENCH if bench else 0)
+        _check(lib.h2sp_plan_create_shard(ctypes.byref(st), int(rank), int(world), flags, ctypes.byref(h)),
                "h2sp_plan_create_shard")
+        self.bench = bool(bench)
         self.handle = h
         self._keep = None
         sz = _Sizes()
@@ -266,10 +273,15 @@ class Sparsifier:
     outputs and the uploaded workspace; ``build()`` runs ``h2sp_build``."""
 
     def __init__(self, plan: Plan, packed: Optional[dict] = None, device="cuda", alloc_inputs: bool = True,
-                 close_gen: Optional[dict] = None):
+                 close_gen: Optional[dict] = None, inputs: Optional[dict] = None, outputs: Optional[dict] = None,
+                 workspace: bool = True):
         """close_gen: {"points": (N, d) tree-ordered array, "kernel": generator
-        kernel spec} -> matrix-free close blocks (h2sp_close_gen); no close
-        buffer is allocated."""
+        kernel spec [, "nodes_row": (sum k, d), "nodes_col": ...]} -> matrix-free
+        close blocks (h2sp_close_gen); with nodes also matrix-free couplings (no
+        coupling buffer).  inputs / outputs: ready device tensors to use instead
+        of allocating (e.g. bases built on the device by h2sp construction, or
+        the global outputs shared by the virtual shards of one matrix).
+        workspace=False: no build workspace (VirtualShards supplies meta + scratch)."""
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_1705_04601_b200 needs a CUDA device (no CPU fallback)")
@@ -277,23 +289,38 @@ class Sparsifier:
         self.device = torch.device(device)
         sz = plan.sizes
         f64 = dict(dtype=torch.float64, device=self.device)
-        self.inputs = {}
+        self.inputs = dict(inputs) if inputs else {}
         self._gen = None
+        coup_gen = False
         if close_gen is not None:
-            pts = np.ascontiguousarray(close_gen["points"], dtype=np.float64)
+            def dev(a):
+                if isinstance(a, torch.Tensor):
+                    return a.to(self.device, dtype=torch.float64).contiguous()
+                return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(self.device)
+            pts = close_gen["points"]
             if pts.ndim != 2 or pts.shape[0] != int(sz["n"]) or not 1 <= pts.shape[1] <= 3:
-                raise ValueError(f"close_gen points must be (N={int(sz['n'])}, d<=3), got {pts.shape}")
+                raise ValueError(f"close_gen points must be (N={int(sz['n'])}, d<=3), got {tuple(pts.shape)}")
             kid, p0, p1 = close_gen_params(close_gen["kernel"])
-            self.inputs["points"] = torch.from_numpy(pts).to(self.device)
+            self.inputs["points"] = dev(pts)
             self._gen = _CloseGen(points=self.inputs["points"].data_ptr(), dim=pts.shape[1], kernel=kid, p0=p0, p1=p1)
+            if close_gen.get("nodes_row") is not None:
+                self.inputs["nodes_row"] = dev(close_gen["nodes_row"])
+                self._gen.nodes_row = self.inputs["nodes_row"].data_ptr()
+                if not plan.symmetric:
+                    self.inputs["nodes_col"] = dev(close_gen["nodes_col"])
+                    self._gen.nodes_col = self.inputs["nodes_col"].data_ptr()
+                coup_gen = True
         if alloc_inputs:
-            names = [("leaf_basis_row", "leaf_row", "leaf_row"), ("transfer_row", "transfer_row", "transfer_row"),
-                     ("coupling", "coupling", "coupling")]
+            names = [("leaf_basis_row", "leaf_row", "leaf_row"), ("transfer_row", "transfer_row", "transfer_row")]
+            if not coup_gen:
+                names.append(("coupling", "coupling", "coupling"))
             if self._gen is None:
                 names.append(("close", "close", "close"))
             if not plan.symmetric:
                 names += [("leaf_basis_col", "leaf_col", "leaf_col"), ("transfer_col", "transfer_col", "transfer_col")]
             for abi, key, szk in names:
+                if abi in self.inputs:
+                    continue
                 n = int(sz[szk])
                 t = torch.empty(max(n, 1), **f64)
                 if packed is not None and n and packed.get(key) is not None:
@@ -302,21 +329,39 @@ class Sparsifier:
                         raise ValueError(f"input {key}: {src.size} values, plan expects {n}")
                     t[:n].copy_(torch.from_numpy(src))
                 self.inputs[abi] = t
-        self.outputs = {
-            "q_row": torch.empty(max(int(sz["q_row"]), 1), **f64),
-            "q_col": torch.empty(max(int(sz["q_col"]), 1), **f64) if not plan.symmetric else None,
-            "s_rowptr": torch.empty(plan.s_rows + 1, dtype=torch.int64, device=self.device),
-            "s_col": torch.empty(max(int(sz["s_nnz"]), 1), dtype=torch.int32, device=self.device),
-            "s_val": torch.empty(max(int(sz["s_nnz"]), 1), **f64),
-        }
-        self.ws = torch.empty(int(sz["workspace_bytes"]) + 256, dtype=torch.uint8, device=self.device)
-        self.ws_ptr = (self.ws.data_ptr() + 255) // 256 * 256
-        self.ws_bytes = int(sz["workspace_bytes"])
-        _check(lib.h2sp_plan_upload(plan.handle, self.ws_ptr, self.ws_bytes, _stream_handle(None)), "h2sp_plan_upload")
+        if outputs is not None:
+            self.outputs = outputs
+        elif plan.bench:
+            N = int(sz["n"])
+            self.outputs = {
+                "q_row": torch.empty(max(int(sz["q_row"]), 1), **f64),
+                "q_col": torch.empty(max(int(sz["q_col"]), 1), **f64) if not plan.symmetric else None,
+                "s_rowptr": None, "s_col": None, "s_val": None,
+                "bench_w": torch.zeros(N, **f64), "bench_y": torch.zeros(N, **f64),
+                "bench_r2": torch.zeros(N, **f64),
+            }
+        else:
+            self.outputs = {
+                "q_row": torch.empty(max(int(sz["q_row"]), 1), **f64),
+                "q_col": torch.empty(max(int(sz["q_col"]), 1), **f64) if not plan.symmetric else None,
+                "s_rowptr": torch.empty(plan.s_rows + 1, dtype=torch.int64, device=self.device),
+                "s_col": torch.empty(max(int(sz["s_nnz"]), 1), dtype=torch.int32, device=self.device),
+                "s_val": torch.empty(max(int(sz["s_nnz"]), 1), **f64),
+            }
+        self.ws = None
+        self.ws_ptr, self.ws_bytes = None, 0
+        if workspace:
+            self.ws = torch.empty(int(sz["workspace_bytes"]) + 256, dtype=torch.uint8, device=self.device)
+            self.ws_ptr = (self.ws.data_ptr() + 255) // 256 * 256
+            self.ws_bytes = int(sz["workspace_bytes"])
+            _check(lib.h2sp_plan_upload(plan.handle, self.ws_ptr, self.ws_bytes, _stream_handle(None)),
+                   "h2sp_plan_upload")
 
     def _abi_inputs(self, inputs=None):
         src = inputs if inputs is not None else self.inputs
         a = _Inputs(**{k: _dptr(src.get(k)) for k, _ in _Inputs._fields_ if k != "close_gen"})
+        if self._gen is not None and self._gen.nodes_row:
+            a.coupling = None
         if self._gen is not None:
             a.close_gen = ctypes.addressof(self._gen)
         return a
@@ -431,3 +476,62 @@ class Sparsifier:
         _check(lib.h2sp_apply_V(self.plan.handle, q.data_ptr(), y.data_ptr(), y.shape[-1], x.data_ptr(),
                                 x.shape[-1], nrhs, ptr, nb, _stream_handle(stream)), "h2sp_apply_V")
         return x
+
+
+class VirtualShards:
+    """The virtual shards of ONE matrix processed one after another on one
+    device (SURVEY §8(d) config-5 protocol step 2): G sharded plans (top-level
+    subtrees), each with its work lists resident in its own device buffer, all
+    taking turns on one shared scratch buffer (h2sp_build_meta), with shared
+    inputs and global outputs (Q, and in bench mode y = S w and the row norms).
+    ``plans``: Plan objects (same matrix, ranks 0..G-1 of world G)."""
+
+    def __init__(self, plans, packed: Optional[dict] = None, device="cuda", close_gen: Optional[dict] = None,
+                 inputs: Optional[dict] = None, nrhs: int = 1):
+        import torch
+        self.plans = list(plans)
+        self.device = torch.device(device)
+        first = Sparsifier(self.plans[0], packed, device=device, close_gen=close_gen, inputs=inputs, workspace=False)
+        self.shards = [first] + [Sparsifier(p, None, device=device, alloc_inputs=False, close_gen=None,
+                                            inputs=first.inputs, outputs=first.outputs, workspace=False)
+                                 for p in self.plans[1:]]
+        for sp in self.shards[1:]:
+            sp._gen = first._gen
+        self.inputs, self.outputs = first.inputs, first.outputs
+        self._meta = []
+        for p in self.plans:   # every shard's work lists stay resident
+            mb = int(p.sizes["meta_bytes"])
+            buf = torch.empty(mb + 256, dtype=torch.uint8, device=self.device)
+            ptr = (buf.data_ptr() + 255) // 256 * 256
+            _check(lib.h2sp_plan_upload(p.handle, ptr, mb, _stream_handle(None)), "h2sp_plan_upload")
+            self._meta.append((buf, ptr))
+        need = max(int(p.sizes["workspace_bytes"]) - int(p.sizes["meta_bytes"]) for p in self.plans)
+        self.scratch = torch.empty(need + 256, dtype=torch.uint8, device=self.device)
+        self.scratch_ptr = (self.scratch.data_ptr() + 255) // 256 * 256
+        self.scratch_bytes = need
+        self.nrhs = nrhs
+        aneed = max(int(lib.h2sp_apply_ws_bytes(p.handle, nrhs)) - int(p.sizes["meta_bytes"]) for p in self.plans)
+        self.apply_scratch = torch.empty(aneed + 256, dtype=torch.uint8, device=self.device)
+        self.apply_ptr = (self.apply_scratch.data_ptr() + 255) // 256 * 256
+        self.apply_bytes = aneed
+
+    def build(self, applies=None, events=None, stream=None):
+        """One pass over all shards.  applies: per shard (b, y, w, x) tensors or
+        None (b, x: (nrhs, n_tree_local); y, w: (nrhs, s_rows) of that shard);
+        events: per shard a list of 2 * launches torch.cuda.Event or None."""
+        for i, (sp, (_, mptr)) in enumerate(zip(self.shards, self._meta)):
+            ap = None
+            if applies is not None and applies[i] is not None:
+                b, y, w, x = applies[i]
+                ap = _ApplyArgs(b=_dptr(b), ldb=b.shape[-1] if b is not None else 0, y=_dptr(y),
+                                ldy=y.shape[-1] if y is not None else 0, w=_dptr(w),
+                                ldw=w.shape[-1] if w is not None else 0, x=_dptr(x),
+                                ldx=x.shape[-1] if x is not None else 0, nrhs=self.nrhs, ws=self.apply_ptr,
+                                ws_bytes=self.apply_bytes)
+            ev = events[i] if events is not None else None
+            arr = (_vp * len(ev))(*[e.cuda_event for e in ev]) if ev else None
+            _check(lib.h2sp_build_meta(sp.plan.handle, ctypes.byref(sp._abi_inputs()),
+                                       ctypes.byref(sp._abi_outputs()), mptr, self.scratch_ptr, self.scratch_bytes,
+                                       ctypes.byref(ap) if ap is not None else None, _stream_handle(stream), arr,
+                                       len(ev) if ev else 0), "h2sp_build_meta")
+        return self.outputs

@@ -70,7 +70,9 @@ struct StripGroup {      // one frozen group (l, s) of a panel
   int32_t col0, m;       // columns [col0, col0 + m) of the panel
   int32_t pos_c1, pos_c2;  // column of the group in the children's panels, -1 if absent
   int64_t s_dst_t;       // W[k_q + a][col0 + b] -> S[s_dst_t + b*s_ld_t + a] (transposed), -1 if none
-  int32_t s_ld_t, pad_;
+                         // (bench mode: partial slot s_dst_t + b*s_ld_t of S row b of the fixed cluster)
+  int32_t s_ld_t;
+  int32_t wc0;           // S column index (column side) of the group's first column (bench mode weights)
 };
 
 static_assert(sizeof(StripGroup) == 32, "staged as 4 x 8 bytes");
@@ -86,7 +88,7 @@ struct StripTileX {
   int32_t gend;                // end of the panel's groups
   int16_t n, kq, k1, k2;       // n_q, k_q, k_c1, k_c2
   int32_t ld_c1, ld_c2, y_ld, s_ld;
-  int32_t pad_;
+  int32_t wq0;                 // S column index (column side) of q's first frozen column (bench mode)
   int64_t q_off;               // Q_q in the side's Q array
   int64_t src_c1, src_c2, y_dst, s_dst;  // as StripPanel
   int64_t pad2_;
@@ -111,6 +113,8 @@ struct CsrBlockRow {     // rows [row0, row0 + m_r) of S, all with the same colu
   int32_t m_r;
   int32_t rowlen;
   int32_t blk_begin, nblk;
+  int64_t grow0;         // global S row index of row0 (row side S order)
+  int64_t part_base;     // bench mode: partial slot of (row0, block 0); row a, block j -> part_base + a*nblk + j
 };
 
 struct CsrBlock {        // columns [col0, col0 + m_c) at row positions [colpos, colpos + m_c)
@@ -179,6 +183,10 @@ struct h2sp_plan_s {
   int32_t wy_kp, wy_n;                      // wy_n: padded leaf size of V / M (64 or 128)
   size_t ws_wy_row, ws_wy_col;
   int32_t nmax;                             // largest local size n_t
+  int32_t bench;                            // H2SP_PLAN_BENCH: S reduced to S*w and row norms, never stored
+  int64_t n_part;                           // bench mode: partial slots (double2 {S*w, |S|^2} per block row x block)
+  size_t ws_part;                           // bench mode: partial buffer in the workspace
+  double flops_unique;                      // sharded: work attributed to this shard's own clusters only
   int64_t launches;
   std::vector<h2sp_launch_info> launch_info;
   uint64_t magic;                           // first 8 bytes of the meta image (checked on device)
@@ -189,16 +197,21 @@ void set_error(const std::string &msg);
 h2sp_status fail(h2sp_status s, const std::string &msg);
 
 // kernels.cu
-h2sp_status launch_build(const h2sp_plan_s *p, const h2sp_inputs *in, const h2sp_outputs *out, unsigned char *ws,
-                         void *stream, int64_t *launches, void *const *events, int64_t n_events,
-                         const h2sp_apply_args *ap = nullptr);
+// meta: the plan's work lists on the device; scratch: the rest of the workspace
+// (sizes.workspace_bytes - meta_bytes); ap_scratch: the applies' scratch (ap != NULL)
+h2sp_status launch_build(const h2sp_plan_s *p, const h2sp_inputs *in, const h2sp_outputs *out,
+                         const unsigned char *meta, unsigned char *scratch, void *stream, int64_t *launches,
+                         void *const *events, int64_t n_events, const h2sp_apply_args *ap = nullptr,
+                         unsigned char *ap_scratch = nullptr);
 h2sp_status launch_csr_early(const h2sp_plan_s *p, unsigned char *ws, int64_t *d_rowptr, int32_t *d_col,
                              int64_t *h_rowptr, int32_t *h_col, void *stream);
 h2sp_status launch_csr_early_join(const h2sp_plan_s *p, void *stream);
 h2sp_status launch_kernel_blocks(const h2sp_close_gen *k, const double *xn, const double *yn,
                                  const h2sp_block_desc *blocks, int64_t n_blocks, double *out, void *stream);
 h2sp_status launch_apply_Ut(const h2sp_plan_s *p, const double *q, const double *b, int64_t ldb, double *y,
-                            int64_t ldy, int nrhs, unsigned char *ws, void *stream, bool col_side);
+                            int64_t ldy, int nrhs, const unsigned char *meta, unsigned char *scratch, void *stream,
+                            bool col_side);
 h2sp_status launch_apply_V(const h2sp_plan_s *p, const double *q, const double *y, int64_t ldy, double *x,
-                           int64_t ldx, int nrhs, unsigned char *ws, void *stream, bool col_side);
+                           int64_t ldx, int nrhs, const unsigned char *meta, unsigned char *scratch, void *stream,
+                           bool col_side);
 }  // namespace h2sp

@@ -15,11 +15,36 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "h2sp_internal.h"
 
 namespace h2sp {
+
+#define H2SP_CK(x)                                                                                       \
+  do {                                                                                                   \
+    cudaError_t e_ = (x);                                                                                \
+    if (e_ != cudaSuccess) return fail(H2SP_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// Dynamic shared-memory opt-in, per device and kernel (cudaFuncSetAttribute is a
+// per-device setting): set on first use on each device, under a lock (builds on
+// different devices may run on different host threads).
+static h2sp_status ensure_smem(const void *fn, size_t bytes) {
+  int dev = 0;
+  H2SP_CK(cudaGetDevice(&dev));
+  static std::mutex mu;
+  static std::map<std::pair<int, const void *>, size_t> done;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_pair(dev, fn);
+  const auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return H2SP_OK;
+  H2SP_CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+  done[key] = bytes;
+  return H2SP_OK;
+}
 
 struct Clusters {  // device views of the per-cluster arrays in the meta region
   const int32_t *n_row, *k_row, *n_col, *k_col;
@@ -891,15 +916,13 @@ __global__ void __launch_bounds__(NW * 2) wy_form_q_kernel(Side sr, Side sc, con
 }
 
 template <int KP, int NW>
-static void launch_wy_form_q(unsigned grid, cudaStream_t st, const Side &rs, const Side &cs, const double *wr,
+static h2sp_status launch_wy_form_q(unsigned grid, cudaStream_t st, const Side &rs, const Side &cs, const double *wr,
                              const double *wc, double *qr, double *qc, int64_t nleaf) {
   constexpr size_t smem = size_t(NW * (KP + 4) + KP * (NW + 4)) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(wy_form_q_kernel<KP, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = true;
-  }
+  if (h2sp_status e = ensure_smem((const void *)wy_form_q_kernel<KP, NW>, smem)) return e;
   wy_form_q_kernel<KP, NW><<<grid, NW * 2, smem, st>>>(rs, cs, wr, wc, qr, qc, nleaf);
+  H2SP_CK(cudaGetLastError());
+  return H2SP_OK;
 }
 
 // --------------------------------------------------------------------------
@@ -909,6 +932,35 @@ static void launch_wy_form_q(unsigned grid, cudaStream_t st, const Side &rs, con
 // small products on the DMMA pipe: W = D R^_s^T, D~ = R^_t W.
 // Per-warp shared memory (doubles): D A8 x LDB | Rs B8 x LDB | Rt A8 x LDA | W A8 x LDB
 // --------------------------------------------------------------------------
+// Kernel function of h2sp_close_gen for two distinct points x, y (dim coordinates):
+// r^2 summed without FMA contraction in coordinate order (K(x, y) == K(y, x)
+// bitwise), rsqrt and multiplications by precomputed constants instead of sqrt
+// and divisions.  Shared by h2sp_eval_kernel_blocks and the matrix-free couplings.
+struct CloseGen {
+  const double *pts;
+  int dim, kind;
+  double p0, p1;
+  double q0;                         // exp: -1 / p0; Laplace: 1 / (4 pi)
+  const double *nodes_row, *nodes_col;  // matrix-free couplings (nullptr: read D)
+};
+
+__device__ __forceinline__ double kernel_eval(const CloseGen &g, const double *x, const double *y) {
+  const double d0 = __dsub_rn(__ldg(x), __ldg(y));
+  double r2 = __dmul_rn(d0, d0);
+  if (g.dim > 1) {
+    const double d1 = __dsub_rn(__ldg(x + 1), __ldg(y + 1));
+    r2 = __dadd_rn(r2, __dmul_rn(d1, d1));
+  }
+  if (g.dim > 2) {
+    const double d2 = __dsub_rn(__ldg(x + 2), __ldg(y + 2));
+    r2 = __dadd_rn(r2, __dmul_rn(d2, d2));
+  }
+  const double ir = rsqrt(r2);
+  if (g.kind == H2SP_KERNEL_LAPLACE) return g.q0 * ir;
+  const double r = r2 > 0.0 ? r2 * ir : 0.0;
+  return g.kind == H2SP_KERNEL_EXP ? exp(r * g.q0) : 1.0 / (r + g.p0);
+}
+
 __host__ __device__ inline int coup_ld(int k) { return rup(rup(k, 8), 16) + 4; }
 __host__ __device__ inline int coup_warp_doubles(int kt, int ks) {
   const int A8 = rup(kt, 8), B8 = rup(ks, 8);
@@ -920,11 +972,14 @@ __host__ __device__ inline int coup_warp_doubles(int kt, int ks) {
 // straight from L1/L2 (R^ blocks are shared by many pairs), then
 // D~ = X R^_s^T with X's A fragments taken from the accumulators by quad
 // shuffles.  Zero-padded to KP; ragged ranks take the predicated loads.
-template <int KP>
+// GEN: D evaluated from the cluster nodes (h2sp_close_gen.nodes_*): B fragment
+// (kk, n) = K(node kk of t, node n of s), each entry of D exactly once per warp.
+template <int KP, bool GEN>
 __global__ void __launch_bounds__(128, KP == 32 ? 3 : 4) coupling_reg_kernel(const CouplingItem *__restrict__ items, int64_t n_items,
                                                            Side rs, Side cs, const double *__restrict__ rh_row,
                                                            const double *__restrict__ rh_col,
-                                                           const double *__restrict__ D, double *__restrict__ dt) {
+                                                           const double *__restrict__ D, double *__restrict__ dt,
+                                                           CloseGen g) {
   constexpr int T = KP / 8;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t item = int64_t(blockIdx.x) * (blockDim.x >> 5) + warp;
@@ -933,7 +988,9 @@ __global__ void __launch_bounds__(128, KP == 32 ? 3 : 4) coupling_reg_kernel(con
   const int kt = rs.k[it.t], ks = cs.k[it.s];
   const double *Rt = rh_row + rs.rh_off[it.t];   // kt x kt, row-major
   const double *Rs = rh_col + cs.rh_off[it.s];   // ks x ks
-  const double *Dg = D + it.d_src;               // kt x ks
+  const double *Dg = GEN ? nullptr : D + it.d_src;  // kt x ks
+  const double *xt = GEN ? g.nodes_row + rs.zb_off[it.t] * g.dim : nullptr;  // nodes of t, s
+  const double *xs = GEN ? g.nodes_col + cs.zb_off[it.s] * g.dim : nullptr;
   const int r = lane >> 2, q = lane & 3;
   // ---- X = R^_t D: A(m, kk) = R^_t[m][kk], B(kk, n) = D[kk][n]
   double X[T][T][2];
@@ -953,7 +1010,10 @@ __global__ void __launch_bounds__(128, KP == 32 ? 3 : 4) coupling_reg_kernel(con
 #pragma unroll
     for (int j = 0; j < T; j++) {
       const int n = j * 8 + r;
-      b[j] = (kk < kt && n < ks) ? __ldg(Dg + kk * ks + n) : 0.0;
+      if constexpr (GEN)
+        b[j] = (kk < kt && n < ks) ? kernel_eval(g, xt + kk * g.dim, xs + n * g.dim) : 0.0;
+      else
+        b[j] = (kk < kt && n < ks) ? __ldg(Dg + kk * ks + n) : 0.0;
     }
 #pragma unroll
     for (int i = 0; i < T; i++)
@@ -1092,13 +1152,6 @@ struct PairCfg {
   static constexpr int MIN_BLOCKS = (NP == 64) ? 2 : (NP == 48) ? 3 : 6;  // smem-bound anyway at 48, 64
 };
 
-// Matrix-free close blocks (h2sp_close_gen): pts == nullptr -> read `close`.
-struct CloseGen {
-  const double *pts;
-  int dim, kind;
-  double p0, p1;
-  double q0;  // exp: -1 / p0; Laplace: 1 / (4 pi)
-};
 
 struct PairArgs {
   const PairItem *items;
@@ -1111,7 +1164,9 @@ struct PairArgs {
   const double *bb_in, *dt_in;        // level k-1 results
   const double *q_row, *q_col;
   double *s_val, *bb_out, *yr, *yc;   // yc: transposed column strips (general) / yr (symmetric)
-  int debug;                          // H2SP_PAIR_DEBUG (timing attribution only): 1 = skip scatter, 2 = skip loads
+  const double *bw;                   // bench mode: w (S column order)
+  double2 *part;                      // bench mode: partial slots {S w, |S|^2}
+  int debug;                          // -DH2SP_TIMING_KNOBS builds only (attribution): 1 = skip scatter, 2 = skip loads
 };
 
 // close_gen mode: C_ts[i][j] = K(x_{tB+i}, x_{sB+j}) (include/h2sp.h).  A thread
@@ -1183,32 +1238,14 @@ __global__ void __launch_bounds__(128) kernel_blocks_kernel(CloseGen g, const do
   for (int e = threadIdx.x; e < ne; e += blockDim.x) {
     const int i = e / bd.ny, j = e - i * bd.ny;
     const double *x = xn + (bd.x_off + i) * g.dim, *y = yn + (bd.y_off + j) * g.dim;
-    const double d0 = __dsub_rn(__ldg(x), __ldg(y));
-    double r2 = __dmul_rn(d0, d0);
-    if (g.dim > 1) {
-      const double d1 = __dsub_rn(__ldg(x + 1), __ldg(y + 1));
-      r2 = __dadd_rn(r2, __dmul_rn(d1, d1));
-    }
-    if (g.dim > 2) {
-      const double d2 = __dsub_rn(__ldg(x + 2), __ldg(y + 2));
-      r2 = __dadd_rn(r2, __dmul_rn(d2, d2));
-    }
-    const double ir = rsqrt(r2);
-    double v;
-    if (g.kind == H2SP_KERNEL_LAPLACE) {
-      v = g.q0 * ir;
-    } else {
-      const double r = r2 > 0.0 ? r2 * ir : 0.0;
-      v = g.kind == H2SP_KERNEL_EXP ? exp(r * g.q0) : 1.0 / (r + g.p0);
-    }
-    out[bd.out_off + e] = v;
+    out[bd.out_off + e] = kernel_eval(g, x, y);
   }
 }
 
 h2sp_status launch_kernel_blocks(const h2sp_close_gen *k, const double *xn, const double *yn,
                                  const h2sp_block_desc *blocks, int64_t n_blocks, double *out, void *stream) {
   if (n_blocks == 0) return H2SP_OK;
-  CloseGen g;
+  CloseGen g{};
   g.pts = nullptr;
   g.dim = k->dim;
   g.kind = k->kernel;
@@ -1295,12 +1332,15 @@ struct PairDst {          // the destinations of one pair, kept in registers
   bool dsym;
 };
 
+// BENCH (bench mode): the nn part is not stored here (bench_pair reduces it).
+template <bool BENCH = false>
 __device__ __forceinline__ void scatter_pair2(const PairArgs &A, const PairDst &D, int row0, int col0, int row,
                                               int col, double v0, double v1) {
   const bool r_nn = row0 >= D.kt, r_bb = row0 + 8 <= D.kt;
   const bool c_nn = col0 >= D.ks, c_bb = col0 + 8 <= D.ks;
   if (row0 + 8 <= D.nt && col0 + 8 <= D.ns && !D.dsym && (r_nn || r_bb) && (c_nn || c_bb)) {
     if (r_nn && c_nn) {
+      if (BENCH) return;
       const int a = row - D.kt, b = col - D.ks;
       if (D.s_dst >= 0) store2_s(A.s_val + D.s_dst + int64_t(a) * D.s_ld + b, v0, v1);
       if (D.s_dst_m >= 0 && !(A.debug & 4)) {
@@ -1330,6 +1370,7 @@ __device__ __forceinline__ void scatter_pair2(const PairArgs &A, const PairDst &
     if (row >= D.kt) {
       const int a = row - D.kt;
       if (c >= D.ks) {
+        if (BENCH) continue;
         const int b = c - D.ks;
         if (D.dsym) {
           if (a <= b) {
@@ -1360,6 +1401,87 @@ __device__ __forceinline__ void scatter_pair2(const PairArgs &A, const PairDst &
   }
 }
 
+// Bench mode (H2SP_PLAN_BENCH, include/h2sp.h h2sp_outputs): the nn part of H --
+// S block (t@k, s@k) and, symmetric, its mirror (s@k, t@k) = H_nn^T -- reduced
+// to per-row partials {sum_j S[i][j] w[j], sum_j S[i][j]^2} in a fixed order:
+// a row's entries are summed by its lane quad (shuffles), a mirror row's
+// (= H column's) by the 8 lanes of a tile column (shuffles) and then over the
+// warps in warp order through `scratch` (WARPS * NP + NP double2; all threads
+// of the CTA must call this).  Diagonal blocks of symmetric mode (H_sym[a][b] =
+// H[min(a,b)][max(a,b)]): entries with a <= b come from row a, a > b from
+// column a.  Lane (r, q) of warp w holds H[m0 + r][8j + 2q + e].
+template <int NP, int TN, int WARPS>
+__device__ __forceinline__ void bench_pair(const PairArgs &A, const PairDst &D, int t, int s, const double (&H)[TN][2],
+                                           int m0, double2 *scratch) {
+  static_assert(WARPS * 8 == NP && TN * 8 == NP, "warp w owns rows 8w..8w+7 of the NP x NP tile");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, r = lane >> 2, q = lane & 3;
+  double2 *colp = scratch, *rowp = scratch + WARPS * NP;
+  const int row = m0 + r, a = row - D.kt;
+  const bool vrow = row >= D.kt && row < D.nt;
+  const bool cols = D.dsym || D.s_dst_m >= 0;   // CTA-uniform
+  const double *w_s = A.bw + A.cs.s_off[s];      // weights of block (t, s)'s columns
+  const double wa = (vrow && cols) ? __ldg(A.bw + A.cs.s_off[t] + a) : 0.0;  // weight of mirror column a
+  double ry = 0.0, rr = 0.0;
+#pragma unroll
+  for (int j = 0; j < TN; j++) {
+    double cy[2], cr[2];
+#pragma unroll
+    for (int e = 0; e < 2; e++) {
+      const int col = j * 8 + 2 * q + e, b = col - D.ks;
+      const bool v = vrow && col >= D.ks && col < D.ns;
+      const double h = H[j][e];
+      if (v && D.s_dst >= 0 && (!D.dsym || a <= b)) {
+        ry = fma(h, __ldg(w_s + b), ry);
+        rr = fma(h, h, rr);
+      }
+      const bool cc = v && (D.dsym ? a < b : true);
+      cy[e] = cc ? h * wa : 0.0;
+      cr[e] = cc ? h * h : 0.0;
+    }
+    if (cols) {
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1)
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          cy[e] += __shfl_xor_sync(0xffffffffu, cy[e], o);
+          cr[e] += __shfl_xor_sync(0xffffffffu, cr[e], o);
+        }
+      if (r == 0) {
+        colp[warp * NP + j * 8 + 2 * q] = make_double2(cy[0], cr[0]);
+        colp[warp * NP + j * 8 + 2 * q + 1] = make_double2(cy[1], cr[1]);
+      }
+    }
+  }
+  ry += __shfl_xor_sync(0xffffffffu, ry, 1);
+  rr += __shfl_xor_sync(0xffffffffu, rr, 1);
+  ry += __shfl_xor_sync(0xffffffffu, ry, 2);
+  rr += __shfl_xor_sync(0xffffffffu, rr, 2);
+  if (q == 0) rowp[row] = make_double2(ry, rr);
+  __syncthreads();
+  for (int i = threadIdx.x; i < NP; i += blockDim.x) {
+    if (D.s_dst >= 0 && i >= D.kt && i < D.nt) {  // row i - kt of block (t, s)
+      double2 v = rowp[i];
+      if (D.dsym)
+#pragma unroll
+        for (int w_ = 0; w_ < WARPS; w_++) {
+          v.x += colp[w_ * NP + i].x;
+          v.y += colp[w_ * NP + i].y;
+        }
+      A.part[D.s_dst + int64_t(i - D.kt) * D.s_ld] = v;
+    }
+    if (!D.dsym && D.s_dst_m >= 0 && i >= D.ks && i < D.ns) {  // row i - ks of the mirror block (s, t)
+      double2 v = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int w_ = 0; w_ < WARPS; w_++) {
+        v.x += colp[w_ * NP + i].x;
+        v.y += colp[w_ * NP + i].y;
+      }
+      A.part[D.s_dst_m + int64_t(i - D.ks) * D.s_ld_m] = v;
+    }
+  }
+  __syncthreads();
+}
+
 // Stage the chunk's work items (<= PAIR_CHUNK_MAX, 144 B each, everything a
 // pair needs precomputed by the plan) into shared memory with one batch of
 // 16-byte async copies: one global round trip per CTA instead of a chain of
@@ -1382,7 +1504,7 @@ __device__ __forceinline__ int stage_items(const PairItem *items, const Chunk &c
 // from T by quad shuffles.  The scatter of pair p's H is software-pipelined
 // into the T-GEMM of pair p+1 (8x8 tiles spread over the k-steps), so the
 // stores fill issue slots between DMMAs instead of forming an idle phase.
-template <int NP, bool GEN>
+template <int NP, bool GEN, bool BENCH>
 __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS) pair_kernel(PairArgs A) {
   using C = PairCfg<NP>;
   constexpr int LD = C::LD;
@@ -1415,7 +1537,7 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS)
         for (int i = 0; i < TM; i++)
 #pragma unroll
           for (int j = 0; j < TN; j++)
-            scatter_pair2(A, prev, m0 + i * 8, j * 8, m0 + i * 8 + r, j * 8 + 2 * q, H[i][j][0], H[i][j][1]);
+            scatter_pair2<BENCH>(A, prev, m0 + i * 8, j * 8, m0 + i * 8 + r, j * 8 + 2 * q, H[i][j][0], H[i][j][1]);
       }
       break;
     }
@@ -1454,7 +1576,7 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS)
         const int tile = (k0 / 4) * TPK + u;
         if (tile < TM * TN && scat) {
           const int i = tile / TN, j = tile % TN;
-          scatter_pair2(A, prev, m0 + i * 8, j * 8, m0 + i * 8 + r, j * 8 + 2 * q, H[i][j][0], H[i][j][1]);
+          scatter_pair2<BENCH>(A, prev, m0 + i * 8, j * 8, m0 + i * 8 + r, j * 8 + 2 * q, H[i][j][0], H[i][j][1]);
         }
       }
     }
@@ -1486,11 +1608,6 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS)
         for (int j = 0; j < TN; j++) dmma(H[i][j], a[i], b[j]);
     }
     __syncthreads();  // every warp is done with Q_s
-    if (more) {
-      const PairItem &nx = s_it[p + 1 - ch.begin];
-      async_tile<NP, NP, LD>(sQs, A.q_col + nx.q_off_s, nx.ns, nx.ns, nx.ns, A.chunks);
-      cp_commit();
-    }
     prev.s_dst = it.s_dst;
     prev.s_dst_m = it.s_dst_m;
     prev.bb_dst = it.bb_dst;
@@ -1506,6 +1623,14 @@ __global__ void __launch_bounds__(PairCfg<NP>::THREADS, PairCfg<NP>::MIN_BLOCKS)
     prev.ks = it.ks;
     prev.dsym = A.sym && s == t;
     have_prev = true;
+    // bench mode: the S part reduced now (Q_s's buffer is the scratch), the
+    // other parts scattered during the next pair's T-GEMM as usual
+    if constexpr (BENCH) bench_pair<NP, TN, C::WARPS>(A, prev, t, s, H[0], m0, reinterpret_cast<double2 *>(sQs));
+    if (more) {
+      const PairItem &nx = s_it[p + 1 - ch.begin];
+      async_tile<NP, NP, LD>(sQs, A.q_col + nx.q_off_s, nx.ns, nx.ns, nx.ns, A.chunks);
+      cp_commit();
+    }
   }
 }
 
@@ -1544,7 +1669,7 @@ __device__ __forceinline__ void wy_load(double *sV, double *sM, const double *wy
   async_tile<KP, 64, C::LD>(sM, g + 64 * KP, KP, 64, 64, g);
 }
 
-template <int KP, bool GEN>
+template <int KP, bool GEN, bool BENCH>
 __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(PairArgs A, const double *wy_row,
                                                                               const double *wy_col) {
   using C = PairWyCfg<KP>;
@@ -1573,7 +1698,7 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
     if (p == ch.end) {
       if (have_prev && !(A.debug & 1)) {
 #pragma unroll
-        for (int j = 0; j < TN; j++) scatter_pair2(A, prev, m0, j * 8, m0 + r, j * 8 + 2 * q, H[j][0], H[j][1]);
+        for (int j = 0; j < TN; j++) scatter_pair2<BENCH>(A, prev, m0, j * 8, m0 + r, j * 8 + 2 * q, H[j][0], H[j][1]);
       }
       break;
     }
@@ -1620,7 +1745,7 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
         constexpr int EVERY = (64 / 4) / TN;
         if ((k0 / 4) % EVERY == 0 && scat) {
           const int j = (k0 / 4) / EVERY;
-          scatter_pair2(A, prev, m0, j * 8, m0 + r, j * 8 + 2 * q, H[j][0], H[j][1]);
+          scatter_pair2<BENCH>(A, prev, m0, j * 8, m0 + r, j * 8 + 2 * q, H[j][0], H[j][1]);
         }
       }
 #pragma unroll
@@ -1703,6 +1828,22 @@ __global__ void __launch_bounds__(PairWyCfg<KP>::THREADS, 2) pair_wy_kernel(Pair
 #pragma unroll
       for (int j = 0; j < TN; j++) dmma(H[j], a, sMs[(k0 + q) * LD + j * 8 + r]);
     }
+    if constexpr (BENCH) {
+      // the S part of H reduced now; this pair's V_s / M_s stage is the scratch
+      // (with DB it is next written at the top of pair p + 1, after a barrier)
+      PairDst cur;
+      cur.s_dst = it.s_dst;
+      cur.s_dst_m = it.s_dst_m;
+      cur.s_ld = it.s_ld;
+      cur.s_ld_m = it.s_ld_m;
+      cur.nt = nt;
+      cur.ns = it.ns;
+      cur.kt = ktt;
+      cur.ks = it.ks;
+      cur.dsym = A.sym && s == t;
+      __syncthreads();  // every warp is done with V_s / M_s
+      bench_pair<64, TN, C::WARPS>(A, cur, t, s, H, m0, reinterpret_cast<double2 *>(sVs));
+    }
     if (!C::DB) {
       __syncthreads();  // every warp is done with V_s / M_s
       if (more) {
@@ -1756,7 +1897,7 @@ __device__ __forceinline__ void wy128_load(double *sV, double *sM, const double 
   async_tile<KP, 128, C::LD>(sM, g + 128 * KP, KP, 128, 128, g);
 }
 
-template <int KP, bool GEN>
+template <int KP, bool GEN, bool BENCH>
 __global__ void __launch_bounds__(PairWy128Cfg<KP>::THREADS, 1) pair_wy128_kernel(PairArgs A, const double *wy_row,
                                                                                    const double *wy_col) {
   using C = PairWy128Cfg<KP>;
@@ -1865,28 +2006,30 @@ __global__ void __launch_bounds__(PairWy128Cfg<KP>::THREADS, 1) pair_wy128_kerne
       for (int j = 0; j < TN; j++) dmma(H[j], a, sM[(k0 + q) * LD + j * 8 + r]);
     }
     __syncthreads();  // every warp is done with V_s / M_s
+    PairDst D;
+    D.s_dst = it.s_dst;
+    D.s_dst_m = it.s_dst_m;
+    D.bb_dst = it.bb_dst;
+    D.yr_dst = it.yr_dst;
+    D.yc_dst = it.yc_dst;
+    D.s_ld = it.s_ld;
+    D.s_ld_m = it.s_ld_m;
+    D.yr_ld = it.yr_ld;
+    D.yc_ld = it.yc_ld;
+    D.nt = it.nt;
+    D.ns = it.ns;
+    D.kt = it.kt;
+    D.ks = it.ks;
+    D.dsym = A.sym && it.s == it.t;
+    // bench mode: the S part reduced with the (free) V / M buffer as scratch
+    if constexpr (BENCH) bench_pair<128, TN, C::WARPS>(A, D, it.t, it.s, H, m0, reinterpret_cast<double2 *>(sV));
     if (more) {  // V_t / M_t of the next pair, in flight during the scatter
       wy128_load<KP>(sV, sM, wy_row, s_it[p + 1 - ch.begin].t);
       cp_commit();
     }
     if (!(A.debug & 1)) {
-      PairDst D;
-      D.s_dst = it.s_dst;
-      D.s_dst_m = it.s_dst_m;
-      D.bb_dst = it.bb_dst;
-      D.yr_dst = it.yr_dst;
-      D.yc_dst = it.yc_dst;
-      D.s_ld = it.s_ld;
-      D.s_ld_m = it.s_ld_m;
-      D.yr_ld = it.yr_ld;
-      D.yc_ld = it.yc_ld;
-      D.nt = it.nt;
-      D.ns = it.ns;
-      D.kt = it.kt;
-      D.ks = it.ks;
-      D.dsym = A.sym && it.s == it.t;
 #pragma unroll
-      for (int j = 0; j < TN; j++) scatter_pair2(A, D, m0, j * 8, m0 + r, j * 8 + 2 * q, H[j][0], H[j][1]);
+      for (int j = 0; j < TN; j++) scatter_pair2<BENCH>(A, D, m0, j * 8, m0 + r, j * 8 + 2 * q, H[j][0], H[j][1]);
     }
   }
 }
@@ -1931,9 +2074,16 @@ struct StripArgs {
   const double *y_in;
   double *y_out;
   double *s_val;
+  const double *bw;   // bench mode: w (S column order)
+  double2 *part;      // bench mode: partial slots
 };
 
-template <int NP, int TN>
+// BENCH (bench mode, include/h2sp.h): rows [k_q, n_q) of W are reduced instead
+// of stored -- per (row, frozen group) of the direct block {sum W w, sum W^2}
+// (8 lanes per item, columns round robin, fixed shuffle tree) and per column of
+// the transposed blocks (TPC lanes per column, rows round robin); W is staged
+// in the Z buffer for it.  Tiles hold whole groups (plan.cpp).
+template <int NP, int TN, bool BENCH>
 __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::MIN_BLOCKS) strip_kernel(StripArgs A) {
   using C = StripCfg<NP, TN>;
   extern __shared__ __align__(16) double sm[];
@@ -1943,6 +2093,8 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
   int32_t *src1 = reinterpret_cast<int32_t *>(tdst + TN);          // per column: column in child-1 panel or -1
   int32_t *src2 = src1 + TN;
   __shared__ StripGroup sg_own[C::ALIAS ? 1 : TN + 1];
+  __shared__ int4 s_gtab[BENCH ? TN + 1 : 1];   // bench: the tile's groups {first column, width, w index}
+  __shared__ int s_ngt;
   // groups overlapping this tile (<= TN + 1); when aliased, dead before the gather
   StripGroup *sg = C::ALIAS ? reinterpret_cast<StripGroup *>(sZ) : sg_own;
   __shared__ __align__(16) StripTileX s_tile;
@@ -1983,6 +2135,15 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
     src2[cc] = a2;
     tdst[cc] = td;
   }
+  if constexpr (BENCH) {  // the tile's whole groups (tile starts at group g0's first column)
+    for (int g = threadIdx.x; g < ng; g += blockDim.x)
+      if (sg[g].col0 < T.c0 + ncol) s_gtab[g] = make_int4(sg[g].col0 - T.c0, sg[g].m, sg[g].wc0, 0);
+    if (threadIdx.x == 0) {
+      int c = 0;
+      while (c < ng && sg[c].col0 < T.c0 + ncol) c++;
+      s_ngt = c;
+    }
+  }
   __syncthreads();
   // gather Z: each thread keeps one column pair (cc, cc + 1) and walks its rows
   // (blockDim.x is a multiple of TN / 2); a pair contiguous and 16-byte aligned
@@ -2021,14 +2182,78 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
   __syncthreads();
   const int warp = threadIdx.x >> 5;
   const int m0 = (warp / C::NWN) * 16, n0 = (warp % C::NWN) * C::WN;
-  if (m0 >= n) return;  // no rows of W for this warp (nothing after this needs the CTA barrier)
+  if (!BENCH && m0 >= n) return;  // no rows of W for this warp (nothing after this needs the CTA barrier)
   double acc[2][C::WN / 8][2];
   zero_acc(acc);
-  warp_gemm<C::LDQ, C::LDZ, 2, C::WN / 8, true>(sQ, sZ, m0, n0, n4, acc);
+  if (m0 < n) warp_gemm<C::LDQ, C::LDZ, 2, C::WN / 8, true>(sQ, sZ, m0, n0, n4, acc);
   // epilogue straight from the accumulators: lane (r, q) holds W[row][col], W[row][col + 1]
   // rows [0, k_q) -> q's panel; rows [k_q, n_q) -> S row segment and the transposed block
   const int lane = threadIdx.x & 31;
   const int r = lane >> 2, q4 = lane & 3;
+  if constexpr (BENCH) {
+    __syncthreads();  // every warp is done reading Z: stage W there
+    if (m0 < n) {
+#pragma unroll
+      for (int i = 0; i < 2; i++)
+#pragma unroll
+        for (int j = 0; j < C::WN / 8; j++) {
+          const int row = m0 + i * 8 + r, col = n0 + j * 8 + 2 * q4;
+          sZ[row * C::LDZ + col] = acc[i][j][0];
+          sZ[row * C::LDZ + col + 1] = acc[i][j][1];
+        }
+    }
+    __syncthreads();
+    const int nfz = n - kq;  // frozen rows of W
+    if (T.s_dst >= 0) {      // direct block(s): item (row a, group g) on 8 lanes
+      const int ngt = s_ngt;
+      const int items = nfz * ngt;
+      const int sub = threadIdx.x & 7;
+      for (int it0 = threadIdx.x >> 3; it0 < rup(items, int(blockDim.x) >> 3); it0 += blockDim.x >> 3) {
+        double y = 0.0, r2 = 0.0;
+        int a = 0, g = 0;
+        if (it0 < items) {
+          a = it0 / ngt;
+          g = it0 - a * ngt;
+          const int4 gt = s_gtab[g];
+          const double *wr = sZ + (kq + a) * C::LDZ + gt.x;
+          const double *ww = A.bw + gt.z;
+          for (int c = sub; c < gt.y; c += 8) {
+            const double v = wr[c];
+            y = fma(v, __ldg(ww + c), y);
+            r2 = fma(v, v, r2);
+          }
+        }
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+          y += __shfl_xor_sync(0xffffffffu, y, o);
+          r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+        }
+        if (sub == 0 && it0 < items) A.part[T.s_dst + g + int64_t(a) * T.s_ld] = make_double2(y, r2);
+      }
+    }
+    {  // transposed blocks: column cc on TPC lanes
+      constexpr int TPC = C::THREADS / TN >= 4 ? 4 : C::THREADS / TN >= 2 ? 2 : 1;  // power of two
+      static_assert(C::THREADS >= TN, "one lane per column at least");
+      const int cc = threadIdx.x / TPC, sub = threadIdx.x % TPC;
+      const int64_t td = cc < ncol ? tdst[cc] : -1;
+      double y = 0.0, r2 = 0.0;
+      if (td >= 0) {
+        const double *ww = A.bw + T.wq0;
+        for (int a = sub; a < nfz; a += TPC) {
+          const double v = sZ[(kq + a) * C::LDZ + cc];
+          y = fma(v, __ldg(ww + a), y);
+          r2 = fma(v, v, r2);
+        }
+      }
+#pragma unroll
+      for (int o = 1; o < TPC; o <<= 1) {
+        y += __shfl_xor_sync(0xffffffffu, y, o);
+        r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+      }
+      if (sub == 0 && td >= 0) A.part[td] = make_double2(y, r2);
+    }
+    if (m0 >= n) return;
+  }
 #pragma unroll
   for (int i = 0; i < 2; i++) {
     const int row = m0 + i * 8 + r;
@@ -2042,7 +2267,7 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
       double *d = nullptr;
       if (row < kq) {
         if (T.y_dst >= 0) d = A.y_out + T.y_dst + int64_t(row) * T.y_ld + T.c0 + col;
-      } else {
+      } else if (!BENCH) {
         const int a = row - kq;
         if (T.s_dst >= 0) {
           double *ds = A.s_val + T.s_dst + int64_t(a) * T.s_ld + T.c0 + col;
@@ -2064,6 +2289,34 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
         else
           d[0] = v0;
       }
+    }
+  }
+}
+
+// Bench mode: y[i] = sum of row i's partial slots, in block order (one warp per
+// S row, lanes round robin over the blocks, fixed shuffle tree), and the row
+// norms likewise.  One CTA per S block row.
+__global__ void __launch_bounds__(256) bench_reduce_kernel(const CsrBlockRow *__restrict__ rows,
+                                                           const double2 *__restrict__ part, double *__restrict__ y,
+                                                           double *__restrict__ r2) {
+  const CsrBlockRow br = rows[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int a = warp; a < br.m_r; a += blockDim.x >> 5) {
+    const double2 *p = part + br.part_base + int64_t(a) * br.nblk;
+    double sy = 0.0, sr = 0.0;
+    for (int j = lane; j < br.nblk; j += 32) {
+      const double2 v = __ldcs(p + j);
+      sy += v.x;
+      sr += v.y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sy += __shfl_xor_sync(0xffffffffu, sy, o);
+      sr += __shfl_xor_sync(0xffffffffu, sr, o);
+    }
+    if (lane == 0) {
+      y[br.grow0 + a] = sy;
+      if (r2) r2[br.grow0 + a] = sr;
     }
   }
 }
@@ -2121,7 +2374,7 @@ __global__ void __launch_bounds__(256) csr_cols_kernel(const CsrBlockRow *__rest
 __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const double *__restrict__ q,
                                                        const double *__restrict__ b, int64_t ldb, double *__restrict__ y,
                                                        int64_t ldy, double *__restrict__ zb, int64_t zbl, int nrhs, int B,
-                                                       int *__restrict__ arrive, int64_t leaf0, int ldq) {
+                                                       int *__restrict__ arrive, int64_t leaf0) {
   // z = Q_t^T x_t with Q read straight from global memory (rows are coalesced
   // across the threads of one column block): no shared-memory staging, so every
   // leaf's CTA is resident at once (16 per SM) and the climb starts in one wave.
@@ -2134,7 +2387,6 @@ __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const dou
   // and of their children, in one round trip (level l in slot l)
   __shared__ int m_n[64], m_k[64], m_k1[64];
   __shared__ int64_t m_q[64], m_zb[64], m_loc[64], m_zb1[64], m_zb2[64];
-  (void)ldq;
   int level = 0;
   int64_t idx = leaf0 + blockIdx.x;  // in-level index (global)
   for (int lv = threadIdx.x; lv <= L; lv += blockDim.x) {
@@ -2201,10 +2453,9 @@ __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const dou
 
 __global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, const double *__restrict__ q,
                                                       const double *__restrict__ y, int64_t ldy, double *__restrict__ x,
-                                                      int64_t ldx, int nrhs, int B, int64_t leaf0, int ldq) {
+                                                      int64_t ldx, int nrhs, int B, int64_t leaf0) {
   __shared__ double sv[128];
   __shared__ double sw[128];
-  (void)ldq;
   // metadata of the whole root -> leaf path in one round trip (level l in slot l),
   // and the ancestors' Q pulled into L2 while the root levels run
   __shared__ int p_n[64], p_k[64], p_k1[64];
@@ -2274,99 +2525,91 @@ __global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, const doub
 // --------------------------------------------------------------------------
 // Host orchestration
 // --------------------------------------------------------------------------
-#define H2SP_CK(x)                                                                                       \
-  do {                                                                                                   \
-    cudaError_t e_ = (x);                                                                                \
-    if (e_ != cudaSuccess) return fail(H2SP_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
-  } while (0)
+template <int KP, bool GEN, bool BENCH>
+static h2sp_status launch_pairs_wy128_t(const PairArgs &a, const double *wy_row, const double *wy_col, int64_t nchunks,
+                                        cudaStream_t st) {
+  using C = PairWy128Cfg<KP>;
+  if (h2sp_status e = ensure_smem((const void *)pair_wy128_kernel<KP, GEN, BENCH>, C::SMEM)) return e;
+  pair_wy128_kernel<KP, GEN, BENCH><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a, wy_row, wy_col);
+  H2SP_CK(cudaGetLastError());
+  return H2SP_OK;
+}
 template <int KP>
 static h2sp_status launch_pairs_wy128(const PairArgs &a, const double *wy_row, const double *wy_col, int64_t nchunks,
-                                      cudaStream_t st) {
-  using C = PairWy128Cfg<KP>;
-  static bool attr = false;
-  if (!attr) {
-    H2SP_CK(cudaFuncSetAttribute(pair_wy128_kernel<KP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(C::SMEM)));
-    H2SP_CK(cudaFuncSetAttribute(pair_wy128_kernel<KP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(C::SMEM)));
-    attr = true;
-  }
-  if (a.gen.pts)
-    pair_wy128_kernel<KP, true><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a, wy_row, wy_col);
-  else
-    pair_wy128_kernel<KP, false><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a, wy_row, wy_col);
-  H2SP_CK(cudaGetLastError());
-  return H2SP_OK;
+                                      cudaStream_t st, bool bench) {
+  const bool gen = a.gen.pts != nullptr;
+  if (bench)
+    return gen ? launch_pairs_wy128_t<KP, true, true>(a, wy_row, wy_col, nchunks, st)
+               : launch_pairs_wy128_t<KP, false, true>(a, wy_row, wy_col, nchunks, st);
+  return gen ? launch_pairs_wy128_t<KP, true, false>(a, wy_row, wy_col, nchunks, st)
+             : launch_pairs_wy128_t<KP, false, false>(a, wy_row, wy_col, nchunks, st);
 }
 
-template <int NP>
-static h2sp_status launch_pairs(const PairArgs &a, int64_t nchunks, cudaStream_t st) {
-  static_assert(PairCfg<NP>::WARPS >= 1, "");
+template <int NP, bool GEN, bool BENCH>
+static h2sp_status launch_pairs_t(const PairArgs &a, int64_t nchunks, cudaStream_t st) {
   using C = PairCfg<NP>;
-  static bool attr = false;
-  if (!attr) {
-    H2SP_CK(cudaFuncSetAttribute(pair_kernel<NP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
-    H2SP_CK(cudaFuncSetAttribute(pair_kernel<NP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
-    attr = true;
-  }
-  if (a.level == 0 && a.gen.pts)
-    pair_kernel<NP, true><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a);
-  else
-    pair_kernel<NP, false><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a);
+  if (h2sp_status e = ensure_smem((const void *)pair_kernel<NP, GEN, BENCH>, C::SMEM)) return e;
+  pair_kernel<NP, GEN, BENCH><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a);
   H2SP_CK(cudaGetLastError());
   return H2SP_OK;
 }
+template <int NP>
+static h2sp_status launch_pairs(const PairArgs &a, int64_t nchunks, cudaStream_t st, bool bench) {
+  static_assert(PairCfg<NP>::WARPS >= 1, "");
+  const bool gen = a.level == 0 && a.gen.pts != nullptr;
+  if (bench)
+    return gen ? launch_pairs_t<NP, true, true>(a, nchunks, st) : launch_pairs_t<NP, false, true>(a, nchunks, st);
+  return gen ? launch_pairs_t<NP, true, false>(a, nchunks, st) : launch_pairs_t<NP, false, false>(a, nchunks, st);
+}
 
+template <int KP, bool GEN, bool BENCH>
+static h2sp_status launch_pairs_wy_t(const PairArgs &a, const double *wy_row, const double *wy_col, int64_t nchunks,
+                                     cudaStream_t st) {
+  using C = PairWyCfg<KP>;
+  if (h2sp_status e = ensure_smem((const void *)pair_wy_kernel<KP, GEN, BENCH>, C::SMEM)) return e;
+  pair_wy_kernel<KP, GEN, BENCH><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a, wy_row, wy_col);
+  H2SP_CK(cudaGetLastError());
+  return H2SP_OK;
+}
 template <int KP>
 static h2sp_status launch_pairs_wy(const PairArgs &a, const double *wy_row, const double *wy_col, int64_t nchunks,
-                                   cudaStream_t st) {
-  using C = PairWyCfg<KP>;
-  static bool attr = false;
-  if (!attr) {
-    H2SP_CK(cudaFuncSetAttribute(pair_wy_kernel<KP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(C::SMEM)));
-    H2SP_CK(cudaFuncSetAttribute(pair_wy_kernel<KP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(C::SMEM)));
-    attr = true;
-  }
-  if (a.gen.pts)
-    pair_wy_kernel<KP, true><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a, wy_row, wy_col);
-  else
-    pair_wy_kernel<KP, false><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a, wy_row, wy_col);
-  H2SP_CK(cudaGetLastError());
-  return H2SP_OK;
+                                   cudaStream_t st, bool bench) {
+  const bool gen = a.gen.pts != nullptr;
+  if (bench)
+    return gen ? launch_pairs_wy_t<KP, true, true>(a, wy_row, wy_col, nchunks, st)
+               : launch_pairs_wy_t<KP, false, true>(a, wy_row, wy_col, nchunks, st);
+  return gen ? launch_pairs_wy_t<KP, true, false>(a, wy_row, wy_col, nchunks, st)
+             : launch_pairs_wy_t<KP, false, false>(a, wy_row, wy_col, nchunks, st);
 }
 
-
-template <int NP, int TN>
+template <int NP, int TN, bool BENCH>
 static h2sp_status launch_strips1(const StripArgs &a, int64_t ntiles, cudaStream_t st) {
   using C = StripCfg<NP, TN>;
-  static bool attr = false;
-  if (!attr) {
-    H2SP_CK(cudaFuncSetAttribute(strip_kernel<NP, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
-    attr = true;
-  }
-  strip_kernel<NP, TN><<<unsigned(ntiles), C::THREADS, C::SMEM, st>>>(a);
+  if (h2sp_status e = ensure_smem((const void *)strip_kernel<NP, TN, BENCH>, C::SMEM)) return e;
+  strip_kernel<NP, TN, BENCH><<<unsigned(ntiles), C::THREADS, C::SMEM, st>>>(a);
   H2SP_CK(cudaGetLastError());
   return H2SP_OK;
 }
 
 static int pad16(int x) { return x <= 16 ? 16 : x <= 32 ? 32 : x <= 48 ? 48 : 64; }
 
-template <int TN>
+template <int TN, bool BENCH>
 static h2sp_status launch_strips_tn(const StripArgs &a, int np, int64_t ntiles, cudaStream_t st) {
   switch (pad16(np)) {
-    case 16: return launch_strips1<16, TN>(a, ntiles, st);
-    case 32: return launch_strips1<32, TN>(a, ntiles, st);
-    case 48: return launch_strips1<48, TN>(a, ntiles, st);
-    default: return launch_strips1<64, TN>(a, ntiles, st);
+    case 16: return launch_strips1<16, TN, BENCH>(a, ntiles, st);
+    case 32: return launch_strips1<32, TN, BENCH>(a, ntiles, st);
+    case 48: return launch_strips1<48, TN, BENCH>(a, ntiles, st);
+    default: return launch_strips1<64, TN, BENCH>(a, ntiles, st);
   }
 }
 
 // tn: the tile width the plan cut this level's panels into (strip_tn_of_level)
-static h2sp_status launch_strips(const StripArgs &a, int np, int tn, int64_t ntiles, cudaStream_t st) {
-  return tn == STRIP_TN_SMALL ? launch_strips_tn<STRIP_TN_SMALL>(a, np, ntiles, st)
-                              : launch_strips_tn<STRIP_TN>(a, np, ntiles, st);
+static h2sp_status launch_strips(const StripArgs &a, int np, int tn, int64_t ntiles, cudaStream_t st, bool bench) {
+  if (bench)
+    return tn == STRIP_TN_SMALL ? launch_strips_tn<STRIP_TN_SMALL, true>(a, np, ntiles, st)
+                                : launch_strips_tn<STRIP_TN, true>(a, np, ntiles, st);
+  return tn == STRIP_TN_SMALL ? launch_strips_tn<STRIP_TN_SMALL, false>(a, np, ntiles, st)
+                              : launch_strips_tn<STRIP_TN, false>(a, np, ntiles, st);
 }
 
 // Side streams and events used to overlap the independent chains of one build
@@ -2421,25 +2664,27 @@ static h2sp_status get_aux(int L, DeviceAux **out) {
   return H2SP_OK;
 }
 
-h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp_outputs *out, unsigned char *ws,
-                         void *stream, int64_t *launches, void *const *events, int64_t n_events,
-                         const h2sp_apply_args *ap) {
+h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp_outputs *out,
+                         const unsigned char *meta, unsigned char *scratch, void *stream, int64_t *launches,
+                         void *const *events, int64_t n_events, const h2sp_apply_args *ap, unsigned char *ap_scratch) {
   cudaStream_t st = (cudaStream_t)stream;
-  const unsigned char *meta = ws;
+  // workspace regions: plan offsets count from the start of a combined
+  // meta | scratch workspace; the two parts may live in separate buffers
+  auto reg = [&](size_t off) { return scratch + (off - P->meta_bytes); };
   const Clusters cl = make_clusters(P, meta);
   const Side rs = side_of(cl, false), cs = side_of(cl, true);
   const bool sym = P->sym != 0;
-  double *rh_row = (double *)(ws + P->ws_rh_row);
-  double *rh_col = sym ? rh_row : (double *)(ws + P->ws_rh_col);
-  double *dt = (double *)(ws + P->ws_dt);
-  double *bb = (double *)(ws + P->ws_bb);
-  double *yr = (double *)(ws + P->ws_yr);
-  double *yc = sym ? yr : (double *)(ws + P->ws_yc);
+  double *rh_row = (double *)reg(P->ws_rh_row);
+  double *rh_col = sym ? rh_row : (double *)reg(P->ws_rh_col);
+  double *dt = (double *)reg(P->ws_dt);
+  double *bb = (double *)reg(P->ws_bb);
+  double *yr = (double *)reg(P->ws_yr);
+  double *yc = sym ? yr : (double *)reg(P->ws_yc);
   const double *leaf_col = sym ? in->leaf_basis_row : in->leaf_basis_col;
   const double *tr_col = sym ? in->transfer_row : in->transfer_col;
   double *q_col = sym ? out->q_row : out->q_col;
-  double *wy_row = P->wy_kp ? (double *)(ws + P->ws_wy_row) : nullptr;
-  double *wy_col = P->wy_kp ? (double *)(ws + P->ws_wy_col) : nullptr;
+  double *wy_row = P->wy_kp ? (double *)reg(P->ws_wy_row) : nullptr;
+  double *wy_col = P->wy_kp ? (double *)reg(P->ws_wy_col) : nullptr;
   const int L = P->L;
   DeviceAux *aux = nullptr;
   if (h2sp_status e = get_aux(L, &aux)) return e;
@@ -2479,12 +2724,8 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     if (events && 2 * i + 1 < n_events) H2SP_CK(cudaEventRecord((cudaEvent_t)events[2 * i + 1], s));
     return H2SP_OK;
   };
-  static bool qr_attr = false;
-  if (!qr_attr) {
-    H2SP_CK(cudaFuncSetAttribute(qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    H2SP_CK(cudaFuncSetAttribute(coupling_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    qr_attr = true;
-  }
+  if (h2sp_status e = ensure_smem((const void *)qr_kernel, 200 * 1024)) return e;
+  if (h2sp_status e = ensure_smem((const void *)coupling_kernel, 200 * 1024)) return e;
   // Launch indices are assigned in the plan's canonical order; precompute them.
   struct LvlIdx {
     int64_t qr_row = -1, qr_col = -1, coup = -1, pairs = -1, rstr[2] = {-1, -1}, cstr[2] = {-1, -1}, rstr_b = -1;
@@ -2538,12 +2779,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
         const size_t smem = size_t(32 * nw * (kp + 4) + kp * (kp + 4) + kp * (32 * nw + 4)) * sizeof(double);
 #define H2SP_QR_CTA(KP_, NW_)                                                                              \
   do {                                                                                                     \
-    static bool a_ = false;                                                                                \
-    if (!a_) {                                                                                             \
-      H2SP_CK(cudaFuncSetAttribute(qr_cta_kernel<KP_, NW_>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
-                                   int(smem)));                                                            \
-      a_ = true;                                                                                           \
-    }                                                                                                      \
+    if (h2sp_status e_ = ensure_smem((const void *)qr_cta_kernel<KP_, NW_>, smem)) return e_;            \
     qr_cta_kernel<KP_, NW_><<<unsigned(M), 32 * NW_, smem, s>>>(sd, M, leaf, rh, wyo, P->wy_kp, P->wy_n,   \
                                                                magic_ptr, P->magic);                      \
   } while (0)
@@ -2565,12 +2801,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
         const int kp = kmax <= 8 ? 8 : kmax <= 16 ? 16 : kmax <= 24 ? 24 : 32;
 #define H2SP_QR_REG(NR_, KP_)                                                                              \
   do {                                                                                                     \
-    static bool attr_ = false;                                                                             \
-    if (!attr_) {                                                                                          \
-      H2SP_CK(cudaFuncSetAttribute(qr_reg_kernel<NR_, KP_>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                                   100 * 1024));                                                           \
-      attr_ = true;                                                                                        \
-    }                                                                                                      \
+    if (h2sp_status e_ = ensure_smem((const void *)qr_reg_kernel<NR_, KP_>, 100 * 1024)) return e_;      \
     qr_reg_kernel<NR_, KP_><<<grid, 32 * wpb, smem, s>>>(sd, L, k, M, per_warp_reg, leaf, tr, rh, qo,        \
                                                         magic_ptr, P->magic, wyo, P->wy_kp, P->wy_n);      \
   } while (0)
@@ -2615,6 +2846,21 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     }
     return H2SP_OK;
   };
+  // matrix-free close blocks / couplings (h2sp_close_gen)
+  CloseGen cgen{};
+  if (in->close_gen) {
+    cgen.pts = in->close_gen->points;
+    cgen.dim = in->close_gen->dim;
+    cgen.kind = in->close_gen->kernel;
+    cgen.p0 = in->close_gen->p0;
+    cgen.p1 = in->close_gen->p1;
+    cgen.q0 = cgen.kind == H2SP_KERNEL_EXP ? -1.0 / cgen.p0 : 1.0 / (4.0 * 3.141592653589793);
+    if (!in->coupling) {
+      cgen.nodes_row = in->close_gen->nodes_row;
+      cgen.nodes_col = sym ? in->close_gen->nodes_row : in->close_gen->nodes_col;
+    }
+  }
+  const bool coup_gen = cgen.nodes_row != nullptr;
   auto coupling = [&](int k, cudaStream_t s) -> h2sp_status {
     const LevelPlan &lp = P->levels[k];
     if (!lp.n_coup) return H2SP_OK;
@@ -2627,14 +2873,28 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       const char *e = getenv("H2SP_COUPLING_SMEM");
       return e && e[0] == '1';
     }();
+    if (coup_gen && !(kmax <= 32 && !coup_smem))
+      return fail(H2SP_EUNSUPPORTED, "matrix-free couplings need ranks <= 32");
     if (kmax <= 32 && !coup_smem) {
       const unsigned grid = unsigned((lp.n_coup + 3) / 4);
       switch ((kmax + 7) / 8) {
         case 0:
-        case 1: coupling_reg_kernel<8><<<grid, 128, 0, s>>>(items, lp.n_coup, rs, cs, rh_row, rh_col, in->coupling, dt); break;
-        case 2: coupling_reg_kernel<16><<<grid, 128, 0, s>>>(items, lp.n_coup, rs, cs, rh_row, rh_col, in->coupling, dt); break;
-        case 3: coupling_reg_kernel<24><<<grid, 128, 0, s>>>(items, lp.n_coup, rs, cs, rh_row, rh_col, in->coupling, dt); break;
-        default: coupling_reg_kernel<32><<<grid, 128, 0, s>>>(items, lp.n_coup, rs, cs, rh_row, rh_col, in->coupling, dt); break;
+        case 1:
+          if (coup_gen) coupling_reg_kernel<8, true><<<grid, 128, 0, s>>>(items, lp.n_coup, rs, cs, rh_row, rh_col, nullptr, dt, cgen);
+          else coupling_reg_kernel<8, false><<<grid, 128, 0, s>>>(items, lp.n_coup, rs, cs, rh_row, rh_col, in->coupling, dt, cgen);
+          break;
+        case 2:
+          if (coup_gen) coupling_reg_kernel<16, true><<<grid, 128, 0, s>>>(items, lp.n_coup, rs, cs, rh_row, rh_col, nullptr, dt, cgen);
+          else coupling_reg_kernel<16, false><<<grid, 128, 0, s>>>(items, lp.n_coup, rs, cs, rh_row, rh_col, in->coupling, dt, cgen);
+          break;
+        case 3:
+          if (coup_gen) coupling_reg_kernel<24, true><<<grid, 128, 0, s>>>(items, lp.n_coup, rs, cs, rh_row, rh_col, nullptr, dt, cgen);
+          else coupling_reg_kernel<24, false><<<grid, 128, 0, s>>>(items, lp.n_coup, rs, cs, rh_row, rh_col, in->coupling, dt, cgen);
+          break;
+        default:
+          if (coup_gen) coupling_reg_kernel<32, true><<<grid, 128, 0, s>>>(items, lp.n_coup, rs, cs, rh_row, rh_col, nullptr, dt, cgen);
+          else coupling_reg_kernel<32, false><<<grid, 128, 0, s>>>(items, lp.n_coup, rs, cs, rh_row, rh_col, in->coupling, dt, cgen);
+          break;
       }
     } else {
       const int per_warp = coup_warp_doubles(kmax, kmax);
@@ -2649,12 +2909,18 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   // ---- CSR index expansion on s2 (independent of all values): a pure HBM write
   //      stream at the lowest priority, started with the build by default
   //      (H2SP_CSR_AT below).
-  static const bool no_csr = [] {   // debugging / attribution only: skip the index expansion
+#ifdef H2SP_TIMING_KNOBS
+  // attribution builds only (-DH2SP_TIMING_KNOBS): skip the index expansion
+  static const bool no_csr = [] {
     const char *e = getenv("H2SP_NO_CSR");
     return e && e[0] == '1';
   }();
+#else
+  constexpr bool no_csr = false;
+#endif
+  const bool bench = P->bench != 0;
   auto csr = [&]() -> h2sp_status {
-    if (csr_idx >= 0 && !no_csr) {
+    if (csr_idx >= 0 && !no_csr && !bench) {
       if (h2sp_status e = pre(s2, csr_idx)) return e;
       if (out->s_rowptr)
         H2SP_CK(cudaMemcpyAsync(out->s_rowptr, meta + P->rowptr_off, size_t(P->n_rows_local + 1) * sizeof(int64_t),
@@ -2722,13 +2988,13 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     const unsigned grid = unsigned(nleaf * (sym ? 1 : 2));
     if (P->wy_n == 128) {
       if (P->wy_kp == 16)
-        launch_wy_form_q<16, 128>(grid, s7, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf);
+        { if (h2sp_status e = launch_wy_form_q<16, 128>(grid, s7, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf)) return e; }
       else
-        launch_wy_form_q<32, 128>(grid, s7, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf);
+        { if (h2sp_status e = launch_wy_form_q<32, 128>(grid, s7, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf)) return e; }
     } else if (P->wy_kp == 16) {
-      launch_wy_form_q<16, 64>(grid, s7, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf);
+      { if (h2sp_status e = launch_wy_form_q<16, 64>(grid, s7, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf)) return e; }
     } else {
-      launch_wy_form_q<24, 64>(grid, s7, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf);
+      { if (h2sp_status e = launch_wy_form_q<24, 64>(grid, s7, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf)) return e; }
     }
     H2SP_CK(cudaGetLastError());
     if (h2sp_status e = post(s7, qform_idx)) return e;
@@ -2738,7 +3004,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   // ---- the applies of the same pass (need Q only): on s1 after the QR chain
   cudaEvent_t ev_apply = aux->ev[8 + 2 * L];
   if (ap) {
-    unsigned char *aws = static_cast<unsigned char *>(ap->ws);
+    unsigned char *aws = ap_scratch;  // the applies' own scratch; the work lists are the build's
     // V w with w independent of U^T b's output: on s7 beside U^T b (both need
     // only Q; V w uses neither the coefficient buffer nor the arrival counters)
     const bool v_beside = ap->w && ap->b && ap->w != ap->y && s7 != s1;
@@ -2746,20 +3012,20 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     if (v_beside) {
       H2SP_CK(cudaEventRecord(ev_chain, s1));
       H2SP_CK(cudaStreamWaitEvent(s7, ev_chain, 0));
-      if (h2sp_status e = launch_apply_V(P, sym ? out->q_row : q_col, ap->w, ap->ldw, ap->x, ap->ldx, ap->nrhs, aws,
-                                         s7, !sym))
+      if (h2sp_status e = launch_apply_V(P, sym ? out->q_row : q_col, ap->w, ap->ldw, ap->x, ap->ldx, ap->nrhs, meta,
+                                         aws, s7, !sym))
         return e;
       H2SP_CK(cudaEventRecord(ev_v, s7));
     }
     if (ap->b) {
-      if (h2sp_status e = launch_apply_Ut(P, out->q_row, ap->b, ap->ldb, ap->y, ap->ldy, ap->nrhs, aws, s1, false))
+      if (h2sp_status e = launch_apply_Ut(P, out->q_row, ap->b, ap->ldb, ap->y, ap->ldy, ap->nrhs, meta, aws, s1, false))
         return e;
     }
     if (v_beside) {
       H2SP_CK(cudaStreamWaitEvent(s1, ev_v, 0));
     } else if (ap->w) {
-      if (h2sp_status e = launch_apply_V(P, sym ? out->q_row : q_col, ap->w, ap->ldw, ap->x, ap->ldx, ap->nrhs, aws,
-                                         s1, !sym))
+      if (h2sp_status e = launch_apply_V(P, sym ? out->q_row : q_col, ap->w, ap->ldw, ap->x, ap->ldx, ap->nrhs, meta,
+                                         aws, s1, !sym))
         return e;
     }
   }
@@ -2780,15 +3046,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       a.B = P->B;
       a.sym = P->sym;
       a.close = in->close;
-      a.gen.pts = nullptr;
-      if (in->close_gen) {
-        a.gen.pts = in->close_gen->points;
-        a.gen.dim = in->close_gen->dim;
-        a.gen.kind = in->close_gen->kernel;
-        a.gen.p0 = in->close_gen->p0;
-        a.gen.p1 = in->close_gen->p1;
-        a.gen.q0 = a.gen.kind == H2SP_KERNEL_EXP ? -1.0 / a.gen.p0 : 1.0 / (4.0 * 3.141592653589793);
-      }
+      a.gen = cgen;
       a.bb_in = bb;
       a.dt_in = dt;
       a.q_row = out->q_row;
@@ -2797,11 +3055,18 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       a.bb_out = bb;
       a.yr = yr;
       a.yc = yc;
+#ifdef H2SP_TIMING_KNOBS
+      // attribution builds only (-DH2SP_TIMING_KNOBS): 1 = skip the scatter, 2 = skip the loads
       static const int pair_debug = [] {
         const char *e = getenv("H2SP_PAIR_DEBUG");
         return e ? atoi(e) : 0;
       }();
       a.debug = pair_debug;
+#else
+      a.debug = 0;
+#endif
+      a.bw = out->bench_w;
+      a.part = bench ? (double2 *)reg(P->ws_part) : nullptr;
       if (h2sp_status e = pre(st, li[k].pairs)) return e;
       // level 0 may run as two launches (first / second half of the leaves), with
       // ev_pairs_a recorded in between for the first half's strips
@@ -2815,16 +3080,16 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
         }
         h2sp_status s;
         if (k == 0 && P->wy_kp && P->wy_n == 128) {
-          s = P->wy_kp == 16 ? launch_pairs_wy128<16>(ap_, wy_row, wy_col, nch, st)
-                             : launch_pairs_wy128<32>(ap_, wy_row, wy_col, nch, st);
+          s = P->wy_kp == 16 ? launch_pairs_wy128<16>(ap_, wy_row, wy_col, nch, st, bench)
+                             : launch_pairs_wy128<32>(ap_, wy_row, wy_col, nch, st, bench);
         } else if (k == 0 && P->wy_kp) {
-          s = P->wy_kp == 16 ? launch_pairs_wy<16>(ap_, wy_row, wy_col, nch, st)
-                             : launch_pairs_wy<24>(ap_, wy_row, wy_col, nch, st);
+          s = P->wy_kp == 16 ? launch_pairs_wy<16>(ap_, wy_row, wy_col, nch, st, bench)
+                             : launch_pairs_wy<24>(ap_, wy_row, wy_col, nch, st, bench);
         } else switch (pad16(lp.np_pair)) {
-          case 16: s = launch_pairs<16>(ap_, nch, st); break;
-          case 32: s = launch_pairs<32>(ap_, nch, st); break;
-          case 48: s = launch_pairs<48>(ap_, nch, st); break;
-          default: s = launch_pairs<64>(ap_, nch, st); break;
+          case 16: s = launch_pairs<16>(ap_, nch, st, bench); break;
+          case 32: s = launch_pairs<32>(ap_, nch, st, bench); break;
+          case 48: s = launch_pairs<48>(ap_, nch, st, bench); break;
+          default: s = launch_pairs<64>(ap_, nch, st, bench); break;
         }
         if (s != H2SP_OK) return s;
         if (split && part == 0) H2SP_CK(cudaEventRecord(ev_pairs_a, st));
@@ -2862,23 +3127,25 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
         a.y_in = yr;
         a.y_out = yr;
         a.s_val = out->s_val;
+        a.bw = out->bench_w;
+        a.part = bench ? (double2 *)reg(P->ws_part) : nullptr;
         const int64_t na = sp.n_rtiles_a;
         if (na > 0) {
           H2SP_CK(cudaStreamWaitEvent(s3, ev_pairs_a, 0));
           H2SP_CK(cudaStreamWaitEvent(s3, ev_ready(k), 0));
           if (h2sp_status e = pre(s3, li[k].rstr[set])) return e;
-          if (h2sp_status e = launch_strips(a, lp.np_rstrip, lp.mp, na, s3)) return e;
+          if (h2sp_status e = launch_strips(a, lp.np_rstrip, lp.mp, na, s3, bench)) return e;
           if (h2sp_status e = post(s3, li[k].rstr[set])) return e;
           H2SP_CK(cudaEventRecord(ev_a_last, s3));
           a_recorded = true;
           StripArgs b = a;
           b.tiles = a.tiles + na;
           if (h2sp_status e = pre(ss, li[k].rstr_b)) return e;
-          if (h2sp_status e = launch_strips(b, lp.np_rstrip, lp.mp, sp.n_rtiles - na, ss)) return e;
+          if (h2sp_status e = launch_strips(b, lp.np_rstrip, lp.mp, sp.n_rtiles - na, ss, bench)) return e;
           if (h2sp_status e = post(ss, li[k].rstr_b)) return e;
         } else {
           if (h2sp_status e = pre(ss, li[k].rstr[set])) return e;
-          h2sp_status s = launch_strips(a, lp.np_rstrip, lp.mp, sp.n_rtiles, ss);
+          h2sp_status s = launch_strips(a, lp.np_rstrip, lp.mp, sp.n_rtiles, ss, bench);
           if (s != H2SP_OK) return s;
           if (h2sp_status e = post(ss, li[k].rstr[set])) return e;
         }
@@ -2893,8 +3160,10 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
         a.y_in = yc;
         a.y_out = yc;
         a.s_val = out->s_val;
+        a.bw = out->bench_w;
+        a.part = bench ? (double2 *)reg(P->ws_part) : nullptr;
         if (h2sp_status e = pre(ss, li[k].cstr[set])) return e;
-        h2sp_status s = launch_strips(a, lp.np_cstrip, lp.mp, sp.n_ctiles, ss);
+        h2sp_status s = launch_strips(a, lp.np_cstrip, lp.mp, sp.n_ctiles, ss, bench);
         if (s != H2SP_OK) return s;
         if (h2sp_status e = post(ss, li[k].cstr[set])) return e;
       }
@@ -2911,6 +3180,15 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   H2SP_CK(cudaStreamWaitEvent(st, ev_strips_done, 0));
   H2SP_CK(cudaStreamWaitEvent(st, ev_s5_done, 0));
   H2SP_CK(cudaStreamWaitEvent(st, ev_strips1_done, 0));
+  // ---- bench mode: every S block has left its partials; sum them per row
+  if (bench && P->n_csr_rows) {
+    if (h2sp_status e = pre(st, csr_idx)) return e;
+    bench_reduce_kernel<<<unsigned(P->n_csr_rows), 256, 0, st>>>((const CsrBlockRow *)(meta + P->csr_rows_off),
+                                                                 (const double2 *)reg(P->ws_part), out->bench_y,
+                                                                 out->bench_r2);
+    H2SP_CK(cudaGetLastError());
+    if (h2sp_status e = post(st, csr_idx)) return e;
+  }
   if (st != user_st) {
     H2SP_CK(cudaEventRecord(ev_end, st));
     H2SP_CK(cudaStreamWaitEvent(user_st, ev_end, 0));
@@ -2954,42 +3232,31 @@ h2sp_status launch_csr_early_join(const h2sp_plan_s *P, void *stream) {
   return H2SP_OK;
 }
 
-// Q tile of the apply kernels: (n_max) x (n_max + 1), n_max = 64 or 128
-static int apply_ldq(const h2sp_plan_s *P) {
-  const int n = P->nmax <= 64 ? 64 : 128;
-  static bool attr = false;
-  if (!attr) {  // both sizes fit the opt-in limit (129 x 128 doubles = 132 KB)
-    cudaFuncSetAttribute(apply_ut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 129 * 8);
-    cudaFuncSetAttribute(apply_v_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 129 * 8);
-    attr = true;
-  }
-  return n + 1;
-}
-
 h2sp_status launch_apply_Ut(const h2sp_plan_s *P, const double *q, const double *b, int64_t ldb, double *y,
-                            int64_t ldy, int nrhs, unsigned char *ws, void *stream, bool col_side) {
+                            int64_t ldy, int nrhs, const unsigned char *meta, unsigned char *scratch, void *stream,
+                            bool col_side) {
   cudaStream_t st = (cudaStream_t)stream;
-  const Clusters cl = make_clusters(P, ws);
+  const Clusters cl = make_clusters(P, meta);
   const Side sd = side_of(cl, col_side);
-  double *zb = (double *)(ws + P->meta_bytes);
+  double *zb = (double *)scratch;
   const int64_t zbl = col_side ? P->zb_col_len : P->zb_row_len;
-  int *arrive = (int *)(ws + P->meta_bytes + ((size_t(std::max(P->zb_row_len, P->zb_col_len)) * nrhs * 8 + 255) / 256) * 256);
+  int *arrive = (int *)(scratch + ((size_t(std::max(P->zb_row_len, P->zb_col_len)) * nrhs * 8 + 255) / 256) * 256);
   H2SP_CK(cudaMemsetAsync(arrive, 0, size_t(P->ncl) * sizeof(int), st));
-  const int ldq = apply_ldq(P);
   apply_ut_kernel<<<unsigned(P->n_leaves_local), 128, 0, st>>>(
-      sd, P->L, q, b, ldb, y, ldy, zb, zbl, nrhs, P->B, arrive, P->first_leaf, ldq);
+      sd, P->L, q, b, ldb, y, ldy, zb, zbl, nrhs, P->B, arrive, P->first_leaf);
   H2SP_CK(cudaGetLastError());
   return H2SP_OK;
 }
 
 h2sp_status launch_apply_V(const h2sp_plan_s *P, const double *q, const double *y, int64_t ldy, double *x,
-                           int64_t ldx, int nrhs, unsigned char *ws, void *stream, bool col_side) {
+                           int64_t ldx, int nrhs, const unsigned char *meta, unsigned char *scratch, void *stream,
+                           bool col_side) {
   cudaStream_t st = (cudaStream_t)stream;
-  const Clusters cl = make_clusters(P, ws);
+  const Clusters cl = make_clusters(P, meta);
+  (void)scratch;
   const Side sd = side_of(cl, col_side);
-  const int ldq = apply_ldq(P);
   apply_v_kernel<<<unsigned(P->n_leaves_local), 128, 0, st>>>(
-      sd, P->L, q, y, ldy, x, ldx, nrhs, P->B, P->first_leaf, ldq);
+      sd, P->L, q, y, ldy, x, ldx, nrhs, P->B, P->first_leaf);
   H2SP_CK(cudaGetLastError());
   return H2SP_OK;
 }

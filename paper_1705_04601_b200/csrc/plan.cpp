@@ -78,6 +78,7 @@ struct Grp {  // a frozen column group (l, s) of a strip panel, at columns [col0
 
 struct BlockRec {
   int64_t roff, coff;
+  int64_t grow;  // global S row of roff (row side)
   int32_t mr, mc;
   int32_t kind;  // 0 pair direct, 1 pair mirror, 2 rstrip direct, 3 rstrip transposed, 4 cstrip transposed
   int32_t level;
@@ -126,7 +127,7 @@ h2sp_status h2sp_plan_create(const h2sp_structure *st, int flags, h2sp_plan *out
 }
 
 h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world, int flags, h2sp_plan *out) {
-  if (flags & ~H2SP_PLAN_EXPLICIT_Q) return fail(H2SP_EINVAL, "unknown plan flags");
+  if (flags & ~(H2SP_PLAN_EXPLICIT_Q | H2SP_PLAN_BENCH)) return fail(H2SP_EINVAL, "unknown plan flags");
   if (!st || !out) return fail(H2SP_EINVAL, "NULL structure or output pointer");
   *out = nullptr;
   h2sp_plan_s *P = nullptr;
@@ -143,6 +144,8 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
     P->L = L;
     P->B = B;
     P->sym = st->symmetric ? 1 : 0;
+    P->bench = (flags & H2SP_PLAN_BENCH) ? 1 : 0;
+    const bool bench = P->bench != 0;
     P->N = int64_t(B) << L;
     const int64_t ncl = (int64_t(1) << (L + 1)) - 1;
     const int64_t nleaf = int64_t(1) << L;
@@ -333,6 +336,7 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
     // ---------------------------------------------------------------- work lists
     const bool sym = P->sym;
     double flops_qr = 0, flops_coup = 0, flops_cong = 0, flops_strip = 0;
+    double uniq_qr = 0, uniq_coup = 0, uniq_cong = 0, uniq_strip = 0;  // owned work only (sharded plans)
     int64_t dt_len = 0, bb_len = 0, yr_len = 0, yc_len = 0;
     std::vector<std::vector<PairItem>> pairs(L + 1);
     // strip panels, index set * (L+1) + level (set 0: groups born at level 0, set 1: later)
@@ -352,12 +356,14 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
       // QR flops (approximate Householder count)
       for (int64_t i = 0; i < M; i++) {
         double n = nr[base + i], kk = kr[base + i];
-        flops_qr += 2 * n * kk * kk + 4 * n * n * kk;
+        double f = 2 * n * kk * kk + 4 * n * n * kk;
         if (!sym) {
           n = nc[base + i];
           kk = kc[base + i];
-          flops_qr += 2 * n * kk * kk + 4 * n * n * kk;
+          f += 2 * n * kk * kk + 4 * n * n * kk;
         }
+        flops_qr += f;
+        if (mine(k, i)) uniq_qr += f;
       }
       // couplings
       if (k < L) {
@@ -374,6 +380,7 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
           coup[k].push_back(CouplingItem{int32_t(ct), int32_t(cs), coup_in[k][j], dt_len});
           dt_len += sz;
           flops_coup += 2.0 * kr[ct] * kc[cs] * (kr[ct] + kc[cs]);
+          if (mine(k + 1, t / 2)) uniq_coup += 2.0 * kr[ct] * kc[cs] * (kr[ct] + kc[cs]);
         }
       }
       // near pairs: items for canonical pairs
@@ -443,6 +450,7 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
         pair_index[k][j] = int64_t(pairs[k].size());
         pairs[k].push_back(it);
         flops_cong += 2.0 * nr[ct] * nc[cs] * (nr[ct] + nc[cs]);
+        if (mine(k, t)) uniq_cong += 2.0 * nr[ct] * nc[cs] * (nr[ct] + nc[cs]);
       }
       // ---- strips arriving from level k-1 (Eq. u1v1): one panel per rotating cluster
       //      and per panel set: set 0 = groups born at level 0 (they depend on the
@@ -492,17 +500,23 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
             sg.s_dst_t = -1;
             const int64_t gi = int64_t(grps.size());
             const int64_t cf = lvl_off(L, g.l) + g.s;  // fixed cluster
+            sg.wc0 = row_side ? int32_t(P->s_off_col[cf]) : 0;
             if (mq > 0) {
               if (row_side) {
-                if (mine(k, p)) blocks.push_back(BlockRec{loc_off[cq], P->s_off_col[cf], mq, g.m, 2, sidx, gi});
+                if (mine(k, p))
+                  blocks.push_back(BlockRec{loc_off[cq], P->s_off_col[cf], P->s_off_row[cq], mq, g.m, 2, sidx, gi});
                 if (sym && mine(g.l, g.s))
-                  blocks.push_back(BlockRec{loc_off[cf], P->s_off_col[cq], g.m, mq, 3, sidx, gi});
+                  blocks.push_back(BlockRec{loc_off[cf], P->s_off_col[cq], P->s_off_row[cf], g.m, mq, 3, sidx, gi});
               } else if (mine(g.l, g.s)) {
-                blocks.push_back(BlockRec{loc_off[cf], P->s_off_col[cq], g.m, mq, 4, sidx, gi});
+                blocks.push_back(BlockRec{loc_off[cf], P->s_off_col[cq], P->s_off_row[cf], g.m, mq, 4, sidx, gi});
               }
             }
             const double rows = (takeA ? kq[c1] : 0) + (takeB ? kq[c1 + 1] : 0);
             flops_strip += 2.0 * nq[cq] * rows * g.m;
+            // a row panel's groups all sit with its rotating cluster's owner (the
+            // symmetric halo copies elsewhere are duplicates); a column-strip group
+            // exists only with its fixed row cluster's owner
+            if (!row_side || mine(k, p)) uniq_strip += 2.0 * nq[cq] * rows * g.m;
             grps.push_back(sg);
             if (kq[cq] > 0) cur[p].push_back(Grp{g.l, g.s, g.m, col});
             col += g.m;
@@ -512,10 +526,23 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
           pn.width = col;
           pn.gend = int32_t(grps.size());
           const int tn = strip_tn_of_level(k);
-          for (int32_t c0 = 0; c0 < col; c0 += tn) {
-            int32_t g0 = pn.gbeg;
-            while (g0 + 1 < pn.gend && grps[g0 + 1].col0 <= c0) g0++;
-            tils.push_back(StripTile{int32_t(pidx), c0, std::min(col, c0 + tn), g0});
+          if (bench) {
+            // bench mode: tiles hold whole groups (each group's partial sums come
+            // from one CTA, so no two CTAs add into one slot)
+            int32_t g = pn.gbeg;
+            while (g < pn.gend) {
+              int32_t e = g, w = 0;
+              while (e < pn.gend && w + grps[e].m <= tn) w += grps[e++].m;
+              if (e == g) throw PlanError(H2SP_EUNSUPPORTED, "bench mode: frozen group wider than a strip tile");
+              tils.push_back(StripTile{int32_t(pidx), grps[g].col0, grps[g].col0 + w, g});
+              g = e;
+            }
+          } else {
+            for (int32_t c0 = 0; c0 < col; c0 += tn) {
+              int32_t g0 = pn.gbeg;
+              while (g0 + 1 < pn.gend && grps[g0 + 1].col0 <= c0) g0++;
+              tils.push_back(StripTile{int32_t(pidx), c0, std::min(col, c0 + tn), g0});
+            }
           }
           pans.push_back(pn);
         }
@@ -550,9 +577,10 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
           newc.push_back(NewStrip{item, 1, s, col0});
         }
         if (canon && mr(ct) > 0 && mc(cs) > 0) {
-          if (mine(k, t)) blocks.push_back(BlockRec{loc_off[ct], P->s_off_col[cs], mr(ct), mc(cs), 0, k, item});
+          if (mine(k, t))
+            blocks.push_back(BlockRec{loc_off[ct], P->s_off_col[cs], P->s_off_row[ct], mr(ct), mc(cs), 0, k, item});
           if (sym && t != s && mine(k, s))
-            blocks.push_back(BlockRec{loc_off[cs], P->s_off_col[ct], mc(cs), mr(ct), 1, k, item});
+            blocks.push_back(BlockRec{loc_off[cs], P->s_off_col[ct], P->s_off_row[cs], mc(cs), mr(ct), 1, k, item});
         }
       }
       // ---- panel bases of level k, and the destinations that point into them
@@ -655,7 +683,8 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
     std::vector<CsrBlock> csr_blocks;
     const int64_t NR_loc = P->n_rows_local;
     std::vector<int64_t> rowptr(NR_loc + 1, 0);
-    int64_t nnz = 0;
+    std::vector<int32_t> row_nblk(bench ? NR_loc : 0, 0);  // bench: blocks per local row (partial slot stride)
+    int64_t nnz = 0, n_part = 0;
     {
       size_t j = 0;
       int64_t row = 0;  // next S row without a pointer
@@ -666,27 +695,36 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
         if (rowlen > INT32_MAX) throw PlanError(H2SP_EUNSUPPORTED, "S row longer than 2^31");
         const int64_t r0 = blocks[j].roff, m_r = blocks[j].mr;
         for (; row < r0; row++) rowptr[row] = nnz;  // empty rows
-        CsrBlockRow br{r0, nnz, 0, int32_t(m_r), int32_t(rowlen), int32_t(csr_blocks.size()), int32_t(e - j)};
+        const int32_t nblk = int32_t(e - j);
+        CsrBlockRow br{r0, nnz, 0, int32_t(m_r), int32_t(rowlen), int32_t(csr_blocks.size()), nblk,
+                       blocks[j].grow, n_part};
         csr_rows.push_back(br);
         int64_t colpos = 0;
+        // S block -> its destination: the S values (stored mode, row length ld) or
+        // the block's partial slot in every row (bench mode, stride nblk)
+        const int32_t ld = bench ? nblk : int32_t(rowlen);
         for (size_t x = j; x < e; x++) {
           const BlockRec &b = blocks[x];
           if (b.mr != m_r) throw PlanError(H2SP_ETREE, "internal: inconsistent block row height");
+          if (b.grow != blocks[j].grow) throw PlanError(H2SP_ETREE, "internal: inconsistent block row start");
           csr_blocks.push_back(CsrBlock{int32_t(b.coff), b.mc, int32_t(colpos), 0});
-          int64_t dst = nnz + colpos;
+          const int64_t dst = bench ? n_part + int64_t(x - j) : nnz + colpos;
           switch (b.kind) {
-            case 0: pairs[b.level][b.idx].s_dst = dst; pairs[b.level][b.idx].s_ld = int32_t(rowlen); break;
-            case 1: pairs[b.level][b.idx].s_dst_m = dst; pairs[b.level][b.idx].s_ld_m = int32_t(rowlen); break;
+            case 0: pairs[b.level][b.idx].s_dst = dst; pairs[b.level][b.idx].s_ld = ld; break;
+            case 1: pairs[b.level][b.idx].s_dst_m = dst; pairs[b.level][b.idx].s_ld_m = ld; break;
             case 2:
               if (rgrp_direct[b.level].empty()) rgrp_direct[b.level].assign(rgrp[b.level].size(), -1);
               rgrp_direct[b.level][b.idx] = dst;
               break;
-            case 3: rgrp[b.level][b.idx].s_dst_t = dst; rgrp[b.level][b.idx].s_ld_t = int32_t(rowlen); break;
-            case 4: cgrp[b.level][b.idx].s_dst_t = dst; cgrp[b.level][b.idx].s_ld_t = int32_t(rowlen); break;
+            case 3: rgrp[b.level][b.idx].s_dst_t = dst; rgrp[b.level][b.idx].s_ld_t = ld; break;
+            case 4: cgrp[b.level][b.idx].s_dst_t = dst; cgrp[b.level][b.idx].s_ld_t = ld; break;
           }
           colpos += b.mc;
         }
         for (int64_t a = 0; a < m_r; a++) rowptr[r0 + a] = nnz + a * rowlen;
+        if (bench)
+          for (int64_t a = 0; a < m_r; a++) row_nblk[r0 + a] = nblk;
+        n_part += m_r * nblk;
         row = r0 + m_r;
         nnz += m_r * rowlen;
         j = e;
@@ -694,6 +732,7 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
       for (; row <= NR_loc; row++) rowptr[row] = nnz;
     }
     P->s_nnz = nnz;
+    P->n_part = bench ? n_part : 0;
     P->s_blocks = int64_t(blocks.size());
     // direct strip output of a panel: its groups are consecutive blocks of S row
     // block (q@k) (set 0 at the row start, set 1 right after), so contiguous in S
@@ -703,19 +742,20 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
         if (mq == 0 || pn.gend == pn.gbeg || loc_off[pn.q] < 0) continue;
         const int64_t d0 = rgrp_direct[sidx][pn.gbeg];
         const int64_t r0 = loc_off[pn.q];
-        if (sidx <= L && d0 != rowptr[r0]) throw PlanError(H2SP_ETREE, "internal: strip panel not at the start of its S row");
+        if (!bench && sidx <= L && d0 != rowptr[r0])
+          throw PlanError(H2SP_ETREE, "internal: strip panel not at the start of its S row");
         for (int32_t g = pn.gbeg; g < pn.gend; g++)
-          if (rgrp_direct[sidx][g] != d0 + rgrp[sidx][g].col0)
+          if (rgrp_direct[sidx][g] != d0 + (bench ? int64_t(g - pn.gbeg) : int64_t(rgrp[sidx][g].col0)))
             throw PlanError(H2SP_ETREE, "internal: strip panel not contiguous in S");
         pn.s_dst = d0;
-        pn.s_ld = int32_t(rowptr[r0 + 1] - rowptr[r0]);
+        pn.s_ld = bench ? row_nblk[r0] : int32_t(rowptr[r0 + 1] - rowptr[r0]);
       }
 
     // ---------------------------------------------------------------- meta image
     MetaBuilder mb;
     mb.buf.resize(256, 0);
     P->magic = 0x4832535050000000ull ^ (uint64_t(P->N) << 8) ^ uint64_t(nnz & 0xffffff) ^ (uint64_t(blocks.size()) << 40) ^
-               (uint64_t(rank) << 32) ^ (uint64_t(world) << 36);
+               (uint64_t(rank) << 32) ^ (uint64_t(world) << 36) ^ (uint64_t(P->bench) << 60);
     std::memcpy(mb.buf.data(), &P->magic, 8);
     P->ca.n_row = mb.put(nr);
     P->ca.k_row = mb.put(kr);
@@ -787,6 +827,9 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
         x.src_c2 = pn.src_c2;
         x.y_dst = pn.y_dst;
         x.s_dst = pn.s_dst;
+        // bench mode: tiles start on a group boundary; slot of the tile's first group
+        if (bench && pn.s_dst >= 0) x.s_dst = pn.s_dst + (t.g0 - pn.gbeg);
+        x.wq0 = int32_t(P->s_off_col[q]);
       }
       return out;
     };
@@ -965,9 +1008,11 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
     P->n_csr_rows = int64_t(csr_rows.size());
     P->n_csr_blocks = int64_t(csr_blocks.size());
     // per block row column pattern (value-independent), 16-byte aligned rows
+    // (bench mode: no column indices, no pattern)
     std::vector<int32_t> csr_pat;
     for (auto &br : csr_rows) {
       br.pat_off = int64_t(csr_pat.size());
+      if (bench) continue;
       for (int32_t j = 0; j < br.nblk; j++) {
         const CsrBlock &b = csr_blocks[br.blk_begin + j];
         for (int32_t e = 0; e < b.m_c; e++) csr_pat.push_back(b.col0 + e);
@@ -978,9 +1023,14 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
     P->csr_rows_off = mb.put(csr_rows);
     P->csr_blocks_off = mb.put(csr_blocks);
     P->rowptr_off = mb.put(rowptr);
-    if (P->n_csr_rows) {  // CSR column expansion (+ the rowptr D2D copy)
+    if (P->n_csr_rows && !bench) {  // CSR column expansion (+ the rowptr D2D copy)
       launches++;
       P->launch_info.push_back(h2sp_launch_info{6, L, P->n_csr_rows, 0.0, 4.0 * double(nnz) + 16.0 * double(NR_loc + 1), 0.0});
+    }
+    if (P->n_csr_rows && bench) {  // bench mode: row sums of the partial slots -> S w, row norms
+      launches++;
+      P->launch_info.push_back(
+          h2sp_launch_info{8, L, P->n_csr_rows, 0.0, 16.0 * double(n_part) + 16.0 * double(NR_loc), 0.0});
     }
     if (P->wy_kp) {  // level-0 Q formed from V / M (kernels.cu wy_form_q_kernel), after the CSR entry
       launches++;
@@ -1034,6 +1084,7 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
     P->ws_bb = carve(bb_len);
     P->ws_yr = carve(yr_len);
     P->ws_yc = carve(yc_len);
+    P->ws_part = bench ? carve(2 * n_part) : 0;
     P->ws_wy_row = P->ws_wy_col = 0;
     if (P->wy_kp) {
       const int64_t per = int64_t(2) * P->wy_n * P->wy_kp;
@@ -1051,9 +1102,12 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
         if (!sym || kt(adm[k][j]) <= ks(adm[k][j]))
           coup_read += double(kr[lvl_off(L, k) + kt(adm[k][j])]) * kc[lvl_off(L, k) + ks(adm[k][j])];
     double in_bytes = 8.0 * (close_read + coup_read + P->leaf_row_len + P->leaf_col_len + P->tr_row_len + P->tr_col_len);
-    double out_bytes = 8.0 * (P->q_row_len + P->q_col_len) + 12.0 * double(nnz) + 8.0 * double(NR_loc + 1);
+    // stored mode: S as CSR; bench mode: S w and the row norms (16 B per row) plus the partials
+    double out_bytes = 8.0 * (P->q_row_len + P->q_col_len) +
+                       (bench ? 16.0 * double(NR_loc) + 32.0 * double(n_part) : 12.0 * double(nnz) + 8.0 * double(NR_loc + 1));
     double mid_bytes = 2.0 * 8.0 * double(P->rh_row_len + P->rh_col_len + dt_len + bb_len + yr_len + yc_len);
     P->flops = flops_qr + flops_coup + flops_cong + flops_strip;
+    P->flops_unique = world == 1 ? P->flops : uniq_qr + uniq_coup + uniq_cong + uniq_strip;
     P->flops_cong = flops_cong;
     P->flops_strip = flops_strip;
     P->bytes = in_bytes + out_bytes + mid_bytes;
@@ -1100,6 +1154,8 @@ h2sp_status h2sp_plan_sizes(h2sp_plan P, h2sp_sizes *o) {
   o->flops_congruence = P->flops_cong;
   o->flops_strips = P->flops_strip;
   o->flops_executed = P->flops_exec;
+  o->flops_unique = P->flops_unique;
+  o->bench_parts = P->n_part;
   return H2SP_OK;
 }
 
@@ -1137,6 +1193,7 @@ h2sp_status h2sp_plan_launches(h2sp_plan P, h2sp_launch_info *out, int64_t max, 
 h2sp_status h2sp_plan_pattern(h2sp_plan P, int64_t *rowptr, int32_t *col) {
   if (!P || !rowptr) return fail(H2SP_EINVAL, "NULL plan or rowptr");
   std::memcpy(rowptr, P->meta.data() + P->rowptr_off, size_t(P->n_rows_local + 1) * sizeof(int64_t));
+  if (col && P->bench) return fail(H2SP_EINVAL, "bench-mode plan: no column pattern");
   if (col) {
     const CsrBlockRow *rows = reinterpret_cast<const CsrBlockRow *>(P->meta.data() + P->csr_rows_off);
     const CsrBlock *blks = reinterpret_cast<const CsrBlock *>(P->meta.data() + P->csr_blocks_off);

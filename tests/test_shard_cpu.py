@@ -94,3 +94,48 @@ def test_gloo_world2_shards_cover_s():
     assert all(p.exitcode == 0 for p in ps)
     rows_ok, nnz_ok = q.get(timeout=5)
     assert rows_ok and nnz_ok
+
+
+@pytest.mark.parametrize("name,make", INPUTS, ids=[i[0] for i in INPUTS])
+@pytest.mark.parametrize("G", [2, 4])
+def test_shard_unique_flops_add_up_to_unsharded(name, make, G):
+    """flops_unique (work of the shard's own row / rotating clusters) adds up to
+    the unsharded plan's algorithmic flops exactly: the job's work for a
+    multi-GPU TFLOP/s, without the halo / mirror work done twice."""
+    p = h2gen.pack(make())
+    full = h2sp.Plan(p).sizes
+    assert full["flops_unique"] == full["flops"]
+    shards = [h2sp.Plan(p, g, G).sizes for g in range(G)]
+    tot = sum(s["flops_unique"] for s in shards)
+    assert abs(tot - full["flops"]) <= 1e-9 * full["flops"]
+    assert all(s["flops_unique"] <= s["flops"] * (1 + 1e-12) for s in shards)
+
+
+@pytest.mark.parametrize("name,make", INPUTS, ids=[i[0] for i in INPUTS])
+def test_bench_plan_matches_stored_plan(name, make):
+    """Bench mode (H2SP_PLAN_BENCH) changes where S goes, not the work: same
+    pattern size, blocks and flops; one partial slot per (S row, block); no
+    column pattern; the CSR expansion launch replaced by the row-sum launch."""
+    p = h2gen.pack(make())
+    a, b = h2sp.Plan(p), h2sp.Plan(p, bench=True)
+    for k in ("s_nnz", "s_blocks", "s_rows", "q_row", "q_col"):
+        assert a.sizes[k] == b.sizes[k], k
+    for k in ("flops", "flops_executed", "flops_congruence", "flops_strips"):
+        assert a.sizes[k] == b.sizes[k], k
+    assert a.sizes["bench_parts"] == 0
+    # slots: sum over block rows of (rows x blocks) -- every block row's blocks
+    # are the column runs of its pattern
+    rp, col = a.pattern()
+    runs = 0
+    for r in range(a.s_rows):
+        c = col[rp[r]:rp[r + 1]]
+        if len(c):
+            runs += 1 + int(np.count_nonzero(np.diff(c) != 1))
+    # one slot per (row, block); adjacent blocks of a row may form one column run
+    assert runs <= b.sizes["bench_parts"] <= a.sizes["s_nnz"]
+    assert b.sizes["bench_parts"] >= a.sizes["s_blocks"]
+    kinds_a = [l["kind"] for l in a.launches()]
+    kinds_b = [l["kind"] for l in b.launches()]
+    assert ("csr" in kinds_a) and ("csr" not in kinds_b) and ("bench_reduce" in kinds_b)
+    with pytest.raises(h2sp.H2spError):
+        b.pattern(with_cols=True)
