@@ -220,13 +220,283 @@ def _oracle_flops(res, h):
     return f
 
 
+def _env_knobs():
+    """Every H2SP_* environment variable in effect (scheduling experiments only;
+    the work-skipping switches exist only in -DH2SP_TIMING_KNOBS builds)."""
+    return {k: v for k, v in sorted(os.environ.items()) if k.startswith("H2SP_")}
+
+
+def _cpu_sample_baseline(cfg_idx: int, n_sample: int, full_flops: float):
+    """The oracle as it stands, 1 thread, on a bounded sample of the recipe;
+    its rate (algorithmic TFLOP/s) is the baseline, extrapolated to the full
+    workload by the flop count (labelled as such)."""
+    import h2gen
+    import oracle
+    h = h2gen.make_config(cfg_idx, N=n_sample)
+    res0 = oracle.sparsify(h)
+    flops = _oracle_flops(res0, h)
+    try:
+        from threadpoolctl import threadpool_limits
+        lim = threadpool_limits(1)
+    except Exception:  # noqa: BLE001
+        lim = None
+    t0 = time.perf_counter()
+    oracle.s_csr(oracle.sparsify(h))
+    dt = time.perf_counter() - t0
+    del lim
+    rate = flops / dt
+    return {"value": rate / 1e12, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": (f"configs[{cfg_idx - 1}] recipe at N={n_sample} (L={h.L}): one full oracle pass (sparsify + "
+                       f"CSR assembly), {flops:.3g} algorithmic flops in {dt:.1f} s on 1 host thread; the full "
+                       f"workload ({full_flops:.3g} flops) extrapolates to {full_flops / rate / 3600:.1f} h"),
+            "extrapolated": True, "seconds": dt, "sample_flops": flops, "host_cpus": os.cpu_count()}
+
+
+def run_protocol(args, rank, world, local_rank):
+    """BASELINE configs[4] at full size (N = 4,194,304) by the SURVEY §8(d)
+    config-5 protocol (paper_1705_04601_b200.protocol): inputs built on the
+    device (Chebyshev bases / transfers / nodes, h2sp_cheb_construct; close
+    blocks and couplings matrix-free), S in bench mode (S w and row norms
+    reduced in the epilogues), 8 virtual shards (top-level subtrees) one after
+    another on one scratch buffer (h2sp_build_meta).  With N GPUs rank g takes
+    shards [8g/N, 8(g+1)/N) of the SAME matrix (strong scaling, no data-path
+    collective: halo Q / R^ recomputed per shard; the checks go through an
+    NCCL all_reduce); time = max over ranks."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import h2gen
+    from paper_1705_04601_b200.protocol import ProtocolRun
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    V = args.virtual_shards
+    if V % world:
+        raise SystemExit(f"--virtual-shards {V} must be a multiple of the GPU count {world}")
+    mine = list(range(rank * V // world, (rank + 1) * V // world))
+    t0 = time.perf_counter()
+    h = h2gen.make_structure(args.config, N=args.n)
+    struct_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    run = ProtocolRun(h, V=V, shards=mine, device=dev, nrhs=args.nrhs, plan_threads=args.plan_threads)
+    setup_s = time.perf_counter() - t0
+    plans = run.plans
+    N, B, nrhs = run.N, run.B, args.nrhs
+    f64 = dict(dtype=torch.float64, device=dev)
+    gw = torch.Generator(device="cpu").manual_seed(args.config)
+    w_host = torch.randn(N, generator=gw, dtype=torch.float64)
+    b_host = torch.randn(nrhs, N, generator=gw, dtype=torch.float64)
+    run.outputs["bench_w"].copy_(w_host)
+    b_full = b_host.to(dev)
+    x_full = torch.empty(nrhs, N, **f64)
+    applies = []
+    for i, p in enumerate(plans):
+        a0, a1 = run.leaf_range(i)
+        applies.append((b_full[:, a0:a1].contiguous(), torch.empty(nrhs, p.s_rows, **f64),
+                        torch.randn(nrhs, p.s_rows, **f64), torch.empty(nrhs, a1 - a0, **f64)))
+    launches = [p.launches() for p in plans]
+    n_launch = [len(l) for l in launches]
+    stream = torch.cuda.current_stream()
+
+    def step(events=None):
+        run.build(applies, events=events)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2 * n)] for n in n_launch] for _ in range(args.steps)]
+    for st_ in evs:
+        for row in st_:
+            for e in row:
+                e.record(stream)
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        t_start.record(stream)
+        for i in range(args.steps):
+            step(evs[i])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t_start.elapsed_time(t_end) / args.steps
+    red = torch.tensor([ms], **f64)
+    if world > 1:
+        dist.all_reduce(red, op=dist.ReduceOp.MAX)
+    ms_max = float(red.item())
+    # per-launch durations (per shard, averaged over the timed steps)
+    per = [np.zeros(n) for n in n_launch]
+    for i in range(args.steps):
+        for s_, n in enumerate(n_launch):
+            for j in range(n):
+                per[s_][j] += evs[i][s_][2 * j].elapsed_time(evs[i][s_][2 * j + 1]) / args.steps
+    # the checks (||S||_F^2, ||S w||^2 of this rank's rows) through the collective
+    chk = torch.stack([run.outputs["bench_r2"].sum(), (run.outputs["bench_y"] ** 2).sum()])
+    if world > 1:
+        dist.all_reduce(chk)
+    offs = plans[0].offsets()
+    loc_any = np.zeros(int(plans[0].sizes["n_clusters"]), dtype=bool)
+    for p in plans:
+        loc_any |= p.local_rows()[0] >= 0
+    apply_flops = 2 * 2.0 * nrhs * float(np.sum(offs["n_row"][loc_any].astype(float) ** 2))
+    tot = torch.tensor([sum(p.sizes["flops_unique"] for p in plans) + apply_flops,
+                        sum(p.sizes["flops"] for p in plans) + apply_flops,
+                        sum(p.sizes["flops_executed"] for p in plans) + apply_flops,
+                        float(sum(p.sizes["s_nnz"] for p in plans))], **f64)
+    if world > 1:
+        dist.all_reduce(tot)
+    job_flops, job_done, job_exec, s_nnz = (float(v) for v in tot.cpu())
+    value = job_flops / (ms_max * 1e-3) / 1e12
+    # dominant kernel: the level-0 congruence (pair_wy128_kernel), over this rank's shards
+    top_fl = top_ex = top_ms = 0.0
+    kinds, per_level = {}, {}
+    for s_, lst in enumerate(launches):
+        for j, li in enumerate(lst):
+            kinds[li["kind"]] = kinds.get(li["kind"], 0.0) + per[s_][j]
+            key = f"{li['kind']}@{li['level']}"
+            d = per_level.setdefault(key, [0.0, 0.0])
+            d[0] += per[s_][j]
+            d[1] += li["flops_exec"]
+            if li["kind"] == "congruence" and li["level"] == 0:
+                top_fl += li["flops"]
+                top_ex += li["flops_exec"]
+                top_ms += per[s_][j]
+    roof = {"bound": "tensor", "achieved": top_fl / (top_ms * 1e-3) / 1e12, "peak": FP64_PEAK_TFLOPS,
+            "unit": "TFLOP/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = _ncu_traffic_protocol()
+    roof.update({"kernel": "congruence@level0 (pair_wy128_kernel<32>, compact-WY, close_gen, bench epilogue)",
+                 "launch_ms_summed_over_shards": top_ms, "share_of_step": top_ms / ms,
+                 "algorithmic_flops": top_fl, "executed_flops": top_ex,
+                 "executed_frac": top_ex / (top_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                 "peak_source": "FP64 DMMA microbenchmark on this pool's B200 (profiles/r01_fp64_peak.txt); "
+                                f"cuBLAS DGEMM measured {FP64_DGEMM_TFLOPS}"})
+    # ---- e2e: the public API with HOST buffers, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        h_pts = torch.from_numpy(np.ascontiguousarray(h.points)).pin_memory()
+        h_lo = torch.from_numpy(np.ascontiguousarray(h.meta["box_lo"])).pin_memory()
+        h_hi = torch.from_numpy(np.ascontiguousarray(h.meta["box_hi"])).pin_memory()
+        h_w = w_host.pin_memory()
+        h_b = b_host.pin_memory()
+        h_y = torch.empty(N, dtype=torch.float64).pin_memory()
+        h_r2 = torch.empty(N, dtype=torch.float64).pin_memory()
+        h_q = torch.empty(run.outputs["q_row"].numel(), dtype=torch.float64).pin_memory()
+        h_x = torch.empty(nrhs, N, dtype=torch.float64).pin_memory()
+
+        def step_e2e():
+            run.points.copy_(h_pts, non_blocking=True)
+            run.box_lo.copy_(h_lo, non_blocking=True)
+            run.box_hi.copy_(h_hi, non_blocking=True)
+            run.outputs["bench_w"].copy_(h_w, non_blocking=True)
+            b_full.copy_(h_b, non_blocking=True)
+            for i, ap_ in enumerate(applies):
+                a0, a1 = run.leaf_range(i)
+                ap_[0].copy_(b_full[:, a0:a1])
+            run.reconstruct()
+            step()
+            for i, ap_ in enumerate(applies):
+                a0, a1 = run.leaf_range(i)
+                x_full[:, a0:a1].copy_(ap_[3])
+            h_y.copy_(run.outputs["bench_y"], non_blocking=True)
+            h_r2.copy_(run.outputs["bench_r2"], non_blocking=True)
+            h_q.copy_(run.outputs["q_row"], non_blocking=True)
+            h_x.copy_(x_full, non_blocking=True)
+
+        step_e2e()
+        torch.cuda.synchronize()
+        k_e2e = max(2, min(args.steps, 3))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        e0.record(stream)
+        for _ in range(k_e2e):
+            step_e2e()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = torch.tensor([e0.elapsed_time(e1) / k_e2e], **f64)
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        h2d = sum(t.numel() * 8 for t in (h_pts, h_lo, h_hi, h_w, h_b))
+        d2h = sum(t.numel() * 8 for t in (h_y, h_r2, h_q, h_x))
+        e2e = {"value": job_flops / (float(ems.item()) * 1e-3) / 1e12, "unit": UNIT,
+               "ms_per_step": float(ems.item()), "steps": k_e2e, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h,
+               "api": "pinned host points / boxes / w / b in; h2sp_cheb_construct (bases, transfers, nodes on the "
+                      "device), h2sp_build_meta per virtual shard (+ U^T b, V w), y = S w, row norms, Q and x out"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_oracle:
+        cpu = _cpu_sample_baseline(args.config, args.ref_n, job_flops)
+    if rank == 0:
+        cfgd = h2gen.CONFIGS[args.config]
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_desc(args.config, N, h.meta.get("seed")), "N": N, "B": B, "L": h.L,
+                       "nrhs": nrhs, "mode": "symmetric" if cfgd["symmetric"] else "general",
+                       "protocol": (f"SURVEY 8(d) config-5 protocol: inputs built on the device "
+                                    f"(h2sp_cheb_construct; close blocks and couplings matrix-free), S in bench mode "
+                                    f"(y = S w and row norms reduced in the epilogues; {s_nnz:.3g} nonzeros = "
+                                    f"{s_nnz * 12e-12:.2f} TB of CSR never stored), {V} virtual shards one after "
+                                    f"another on one scratch buffer"),
+                       "parallelism": (f"{V} virtual subtree shards of one matrix over {world} GPU(s) "
+                                       f"({len(mine)} per GPU; no data-path collective: halo Q / R^ recomputed per "
+                                       f"shard; NCCL all_reduce of the checks)"),
+                       "l2": "inputs (bases 1 GB) and the per-shard intermediates (~100 GB) exceed the 126 MB L2; "
+                             "no flush",
+                       "structure_s": struct_s, "setup_s": setup_s, "s_nnz": s_nnz,
+                       "flops_per_step": job_flops, "flops_done_per_step": job_done,
+                       "flops_redundant_frac": job_done / job_flops - 1.0,
+                       "executed_flops_per_step": job_exec,
+                       "flops_convention": "algorithmic (SURVEY 8(d): explicit-Q congruence 2 n_t n_s (n_t + n_s)), "
+                                           "each pair / strip counted once (flops_unique of the shards)",
+                       "fp64_frac_of_peak_whole_step": value / world / FP64_PEAK_TFLOPS,
+                       "breakdown_ms_summed": {k: round(v, 3) for k, v in kinds.items()},
+                       "per_kind_level": {k: {"ms": round(v[0], 3), "tflops_exec": round(v[1] / max(v[0], 1e-9) * 1e-9, 2)}
+                                          for k, v in per_level.items()},
+                       "checks": {"S_frob2": float(chk[0]), "y_norm2": float(chk[1])},
+                       "env": _env_knobs()},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps * sum(n + 2 for n in n_launch),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _ncu_traffic_protocol():
+    """dram bytes of one level-0 congruence launch of the protocol run, from the
+    committed ncu summary (profiles/*_ncu_top_c5.json), per algorithmic flop
+    scaled to... (None when absent)."""
+    import glob
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_top_c5.json")), reverse=True):
+        try:
+            with open(p) as f:
+                return json.load(f).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            continue
+    return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=None, help="timed steps (default 5 for config 5, else 20)")
+    ap.add_argument("--warmup", type=int, default=None, help="untimed steps (default 3 for config 5, else 5)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5,
+                    help="BASELINE configs[config-1]; 5 (default, the metric's workload) runs the SURVEY 8(d) "
+                         "protocol at full size, 1-4 the stored-S path")
+    ap.add_argument("--virtual-shards", type=int, default=8, help="config 5: virtual subtree shards of the matrix")
+    ap.add_argument("--plan-threads", type=int, default=8, help="config 5: shard plans created in parallel")
     ap.add_argument("--n", type=int, default=None, help="override N (smaller instance of the recipe)")
     ap.add_argument("--nrhs", type=int, default=1)
     ap.add_argument("--no-oracle", action="store_true", help="skip the cpu_baseline leg")
@@ -241,10 +511,15 @@ def main():
     ap.add_argument("--close-gen", action="store_true",
                     help="matrix-free close blocks (h2sp_close_gen): the level-0 congruence evaluates C_ts from "
                          "the points instead of reading them (SURVEY 8(d) config-5 protocol step 1)")
+    ap.add_argument("--stored", action="store_true", help="config 5: the stored-S path (needs a small --n)")
     ap.add_argument("--shard", action="store_true",
                     help="N>1: split ONE matrix into N top-level subtree shards (strong scaling) "
                          "instead of N independent matrices (weak scaling, default)")
     args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 5 if args.config == 5 else 20
+    if args.warmup is None:
+        args.warmup = 3 if args.config == 5 else 5
     args.warmup = max(args.warmup, 3)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -252,6 +527,9 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.config == 5 and not args.stored:
+        run_protocol(args, rank, world, local_rank)
         return
 
     import numpy as np

@@ -38,7 +38,8 @@ import numpy as np
 __all__ = [
     "H2Input", "CONFIGS", "lvl_off", "cid", "make_points", "kd_tree", "block_tree",
     "make_config", "random_h2", "axis_aligned_h2", "fig3_h2", "eta0_h2",
-    "kernel_matrix", "pack", "coupling_block_descs",
+    "kernel_matrix", "pack", "coupling_block_descs", "make_structure", "fill_cheb_bases", "cheb_cos_table",
+    "cheb_base_orders",
 ]
 
 
@@ -142,6 +143,11 @@ def kd_tree(points: np.ndarray, L: int):
     ncl = n_clusters(L)
     lo = np.zeros((ncl, d))
     hi = np.zeros((ncl, d))
+    # rank of every point along each axis in the (coordinate, index) order: a
+    # segment sorted by (coordinate, index) is the segment sorted by this rank
+    rank = np.empty((d, N), dtype=np.int64)
+    for a in range(d):
+        rank[a, np.argsort(points[:, a], kind="stable")] = np.arange(N)
     # top-down: at level k the segments have size N >> (L - k)
     for k in range(L, -1, -1):
         M = 1 << (L - k)
@@ -155,11 +161,8 @@ def kd_tree(points: np.ndarray, L: int):
         if k == 0:
             break
         axis = np.argmax(bhi - blo, axis=1)                        # [M]
-        coord = seg[np.arange(M)[:, None], np.arange(size)[None, :], axis[:, None]]
-        idx = perm.reshape(M, size)
-        segid = np.repeat(np.arange(M), size)
-        order = np.lexsort((idx.ravel(), coord.ravel(), segid))   # stable on (coord, index)
-        perm = perm[order]
+        key = np.repeat(np.arange(M, dtype=np.int64) * N, size) + rank[np.repeat(axis, size), perm]
+        perm = perm[np.argsort(key)]                                # keys distinct: (segment, coord, index)
     return perm, lo, hi
 
 
@@ -311,6 +314,29 @@ def _lagrange(nodes: np.ndarray, x: np.ndarray) -> np.ndarray:
     return out
 
 
+def cheb_cos_table(kind: int) -> np.ndarray:
+    """[(p - 1) * 8 + j] = the Chebyshev cosine _cheb_nodes uses for order p
+    (1..8), node j -- the same numpy expression, so a device construction fed
+    with it reproduces the generator's nodes bit for bit (layout only)."""
+    out = np.zeros(64)
+    for p in range(1, 9):
+        j = np.arange(p)
+        if kind == 1:
+            c = np.cos((2 * j + 1) * math.pi / (2 * p))
+        else:
+            c = np.cos((2 * j + 1.5) * math.pi / (2 * p + 1))
+        out[(p - 1) * 8:(p - 1) * 8 + p] = c
+    return out
+
+
+def cheb_base_orders(d: int, r: int) -> Tuple[int, ...]:
+    """Tensor orders of a rank-r cluster, largest-extent axis first."""
+    base = _ORDERS.get((d, r))
+    if base is None:
+        raise ValueError(f"no tensor order table for d={d}, r={r}")
+    return tuple(base)
+
+
 class _ChebCluster:
     def __init__(self, lo, hi, r, kind):
         d = len(lo)
@@ -340,7 +366,7 @@ def _pairs_same(near0):
 
 
 def make_config(idx: int, seed: Optional[int] = None, N: Optional[int] = None, method: Optional[str] = None,
-                with_close: bool = True, with_couplings: bool = True) -> H2Input:
+                with_close: bool = True, with_couplings: bool = True, orthonormalize: Optional[bool] = None) -> H2Input:
     """BASELINE.json ``configs[idx-1]`` with ``seed = idx`` (reading 17).  ``N``
     may be overridden to make smaller instances of the same recipe."""
     cfg = CONFIGS[idx]
@@ -360,9 +386,39 @@ def make_config(idx: int, seed: Optional[int] = None, N: Optional[int] = None, m
         h2 = _svd_h2(x, L, B, r, near0, adm, kspec, sym)
     else:
         h2 = _cheb_h2(x, L, B, r, near0, adm, kspec, lo, hi, sym, with_close, with_couplings)
-        if cfg.get("orthonormalize"):
+        h2.meta.update(box_lo=lo, box_hi=hi, r=r, dim=x.shape[1])
+        if cfg.get("orthonormalize") if orthonormalize is None else orthonormalize:
             orthonormalize_h2(h2)
     h2.meta.update(config=idx, seed=seed, N=N, eta=eta, method=meth, kernel=kspec)
+    return h2
+
+
+def make_structure(idx: int, seed: Optional[int] = None, N: Optional[int] = None) -> H2Input:
+    """The STRUCTURE of BASELINE.json ``configs[idx-1]`` only -- tree-ordered
+    points, cluster boxes, block cluster tree and ranks, no numeric arrays --
+    for instances whose bases / couplings / close blocks are built on the device
+    (config 5 at full size: 130 GB of couplings and 980 GB of close blocks are
+    never materialised).  Same seed, tree and ranks as make_config."""
+    cfg = CONFIGS[idx]
+    N = N or cfg["N"]
+    seed = idx if seed is None else seed
+    rng = np.random.default_rng(seed)
+    B, r, eta, sym = cfg["B"], cfg["r"], cfg["eta"], cfg["symmetric"]
+    L = int(round(math.log2(N // B)))
+    assert B << L == N
+    pts = make_points(cfg["points"], N, rng)
+    perm, lo, hi = kd_tree(pts, L)
+    x = np.ascontiguousarray(pts[perm])
+    del pts
+    near0, adm = block_tree(lo, hi, L, eta)
+    rank_row = far_ranks(L, near0, adm, r, r, 0)
+    rank_col = far_ranks(L, near0, adm, r, r, 1)
+    if sym:
+        rank_row = rank_col = np.maximum(rank_row, rank_col)
+    h2 = H2Input(L=L, B=B, symmetric=sym, rank_row=rank_row, rank_col=rank_col, leaf_row=None, leaf_col=None,
+                 transfer_row=None, transfer_col=None, near=near0, close=None, adm=adm, coupling=None, points=x)
+    h2.meta.update(config=idx, seed=seed, N=N, eta=eta, method="cheb", kernel=_kernel_spec(cfg, N), box_lo=lo,
+                   box_hi=hi, r=r, dim=x.shape[1], structure_only=True)
     return h2
 
 
@@ -403,6 +459,54 @@ def _mirror_close(near0, close):
     return close
 
 
+def _cheb_side(x, L, B, rank, lo, hi, kind):
+    """Chebyshev clusters, leaf bases and transfers of one side."""
+    ncl = n_clusters(L)
+    cl = [None] * ncl
+    for c in range(ncl):
+        if rank[c] > 0:
+            cl[c] = _ChebCluster(lo[c], hi[c], int(rank[c]), kind)
+    leaf = []
+    for i in range(1 << L):
+        c = cid(L, 0, i)
+        if rank[c] > 0:
+            leaf.append(cl[c].basis(x[i * B:(i + 1) * B]))
+        else:
+            leaf.append(np.zeros((B, 0)))
+    transfer: List[Optional[np.ndarray]] = [None] * ncl
+    for k in range(1, L + 1):
+        for i in range(1 << (L - k)):
+            p = cid(L, k, i)
+            c1, c2 = cid(L, k - 1, 2 * i), cid(L, k - 1, 2 * i + 1)
+            rows = []
+            for c in (c1, c2):
+                kc = int(rank[c])
+                if rank[p] > 0 and kc > 0:
+                    rows.append(cl[p].basis(cl[c].nodes))
+                else:
+                    rows.append(np.zeros((kc, int(rank[p]))))
+            transfer[p] = np.vstack(rows)
+    return cl, leaf, transfer
+
+
+def fill_cheb_bases(h2: H2Input) -> H2Input:
+    """Numeric nested bases of a structure-only input (make_structure) with the
+    same Chebyshev recipe as make_config -- for the oracle's checks on instances
+    whose close blocks / couplings stay matrix-free (config 5 at full size).
+    Couplings and close blocks are not built (evaluate them from the points /
+    nodes, meta cheb_nodes_*)."""
+    x, L, B = h2.points, h2.L, h2.B
+    lo, hi = h2.meta["box_lo"], h2.meta["box_hi"]
+    clr, h2.leaf_row, h2.transfer_row = _cheb_side(x, L, B, h2.rank_row, lo, hi, 1)
+    if h2.symmetric:
+        clc, h2.leaf_col, h2.transfer_col = clr, h2.leaf_row, h2.transfer_row
+    else:
+        clc, h2.leaf_col, h2.transfer_col = _cheb_side(x, L, B, h2.rank_col, lo, hi, 2)
+    h2.meta["cheb_nodes_row"] = [c.nodes if c is not None else None for c in clr]
+    h2.meta["cheb_nodes_col"] = [c.nodes if c is not None else None for c in clc]
+    return h2
+
+
 def _cheb_h2(x, L, B, r, near0, adm, kspec, lo, hi, sym, with_close=True, with_couplings=True) -> H2Input:
     ncl = n_clusters(L)
     rank_row = far_ranks(L, near0, adm, r, r, 0)
@@ -411,38 +515,11 @@ def _cheb_h2(x, L, B, r, near0, adm, kspec, lo, hi, sym, with_close=True, with_c
         rank = np.maximum(rank_row, rank_col)
         rank_row = rank_col = rank
 
-    def side(rank, kind):
-        cl = [None] * ncl
-        for c in range(ncl):
-            if rank[c] > 0:
-                cl[c] = _ChebCluster(lo[c], hi[c], int(rank[c]), kind)
-        leaf = []
-        for i in range(1 << L):
-            c = cid(L, 0, i)
-            if rank[c] > 0:
-                leaf.append(cl[c].basis(x[i * B:(i + 1) * B]))
-            else:
-                leaf.append(np.zeros((B, 0)))
-        transfer: List[Optional[np.ndarray]] = [None] * ncl
-        for k in range(1, L + 1):
-            for i in range(1 << (L - k)):
-                p = cid(L, k, i)
-                c1, c2 = cid(L, k - 1, 2 * i), cid(L, k - 1, 2 * i + 1)
-                rows = []
-                for c in (c1, c2):
-                    kc = int(rank[c])
-                    if rank[p] > 0 and kc > 0:
-                        rows.append(cl[p].basis(cl[c].nodes))
-                    else:
-                        rows.append(np.zeros((kc, int(rank[p]))))
-                transfer[p] = np.vstack(rows)
-        return cl, leaf, transfer
-
-    clr, leaf_row, tr_row = side(rank_row, 1)
+    clr, leaf_row, tr_row = _cheb_side(x, L, B, rank_row, lo, hi, 1)
     if sym:
         clc, leaf_col, tr_col = clr, leaf_row, tr_row
     else:
-        clc, leaf_col, tr_col = side(rank_col, 2)
+        clc, leaf_col, tr_col = _cheb_side(x, L, B, rank_col, lo, hi, 2)
     coupling = [] if with_couplings else None
     for k in range(L if with_couplings else 0):
         lst = []
@@ -870,6 +947,8 @@ def pack(h2: H2Input) -> dict:
         adm_col.append(np.ascontiguousarray(a[:, 1] if len(a) else np.zeros(0), dtype=np.int32))
 
     def cat(mats):
+        if mats is None:
+            return None
         mats = [m for m in mats if m is not None]
         if not mats:
             return np.zeros(0)
@@ -881,8 +960,10 @@ def pack(h2: H2Input) -> dict:
         rank_row=np.ascontiguousarray(h2.rank_row, dtype=np.int32),
         rank_col=np.ascontiguousarray(h2.rank_col, dtype=np.int32),
         near_ptr=near_ptr, near_col=near_col, adm_ptr=adm_ptr, adm_col=adm_col,
-        leaf_row=cat(h2.leaf_row), transfer_row=cat([h2.transfer_row[c] for c in range(ncl)]),
-        leaf_col=cat(h2.leaf_col), transfer_col=cat([h2.transfer_col[c] for c in range(ncl)]),
+        leaf_row=cat(h2.leaf_row),
+        transfer_row=cat([h2.transfer_row[c] for c in range(ncl)]) if h2.transfer_row is not None else None,
+        leaf_col=cat(h2.leaf_col),
+        transfer_col=cat([h2.transfer_col[c] for c in range(ncl)]) if h2.transfer_col is not None else None,
         close=np.ascontiguousarray(h2.close, dtype=np.float64).ravel() if h2.close is not None else None,
         coupling=cat([m for lst in h2.coupling for m in lst]) if h2.coupling is not None else None,
     )

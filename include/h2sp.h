@@ -168,6 +168,36 @@ typedef struct {
 h2sp_status h2sp_eval_kernel_blocks(const h2sp_close_gen *k, const double *x_nodes, const double *y_nodes,
                                     const h2sp_block_desc *blocks, int64_t n_blocks, double *out, void *stream);
 
+/* GPU H^2 construction (the input side of the path,
+ * P:601-602): nested cluster bases by tensor Chebyshev interpolation on each
+ * cluster's box, the recipe of the synthetic inputs, so that no
+ * numeric input of config 5 is built on the host.  For `side` (0 row, 1
+ * column) of the plan and every cluster of rank k > 0 (k must equal
+ * prod(orders)):
+ *   box = [lo - pad, hi + pad], pad = max(1e-9 (hi - lo), 1e-12) per axis;
+ *   axis a gets order orders[i] where a is the i-th axis by decreasing
+ *   extent (stable); axis nodes mid + half * cheb_cos[(p-1)*8 + j] (p = 1: mid);
+ *   nodes: the tensor grid, axis 0 slowest -> nodes[(zb(c) + j) * dim ...]
+ *   (zb(c) = sum of the ranks of the clusters before c, level-major);
+ *   leaf_basis (as h2sp_inputs.leaf_basis_*): row i of R_t = the tensor
+ *     Lagrange basis of t at point i of t;
+ *   transfer (as h2sp_inputs.transfer_*): row i of T_p = p's basis at node
+ *     i of its children (child 1 first).
+ * Every step is an explicitly rounded IEEE operation, so with the cosine table
+ * of the numpy generator the arrays are bitwise equal to it.
+ * points: DEVICE N x dim (tree order); box_lo / box_hi: DEVICE n_clusters x dim
+ * tight boxes; `meta`: the plan's uploaded work lists (h2sp_plan_upload).
+ * Outputs DEVICE, lengths from h2sp_sizes (nodes: sum of ranks x dim).
+ * Asynchronous on `stream`.  H2SP_ERANK if a rank is neither 0 nor prod(orders). */
+typedef struct {
+  int32_t dim;            /* 1..3 */
+  int32_t orders[3];      /* base orders, largest-extent axis first; prod <= 64 */
+  double cheb_cos[64];    /* [(p - 1) * 8 + j]: Chebyshev cosines of order p = 1..8 */
+} h2sp_cheb_spec;
+h2sp_status h2sp_cheb_construct(h2sp_plan plan, const void *meta, int side, const h2sp_cheb_spec *spec,
+                                const double *points, const double *box_lo, const double *box_hi, double *leaf_basis,
+                                double *transfer, double *nodes, void *stream);
+
 /* Numeric inputs (DEVICE pointers, read-only, row-major FP64):
  *   leaf_basis_row: R_t of every leaf, B x k_t each, concatenated by leaf.
  *   transfer_row:   T_p of every internal cluster, (k_c1 + k_c2) x k_p each

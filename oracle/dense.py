@@ -194,3 +194,181 @@ def pattern_rule(h2: H2Input) -> Set[Tuple[int, int, int, int]]:
                 if mc[cid(L, lvl, s)] > 0:
                     out.add((j, t0, lvl, s))
     return out
+
+
+# ---------------------------------------------------------------------------
+# Checks at sizes where the close blocks / couplings are never stored (config 5
+# at full size): the same definitions, with C_ts and D_b evaluated from the
+# points / interpolation nodes (h2gen.kernel_matrix and the plain-C helper
+# close_norm.c) instead of read from arrays.
+# ---------------------------------------------------------------------------
+
+def _close_lib():
+    import ctypes
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libclosenorm.so")
+    lib = ctypes.CDLL(path)
+    P = ctypes.POINTER
+    lib.oracle_close_frob_sq.argtypes = [P(ctypes.c_double), ctypes.c_int, ctypes.c_int, P(ctypes.c_int32),
+                                        P(ctypes.c_int32), ctypes.c_int64, ctypes.c_int, ctypes.c_double,
+                                        ctypes.c_double, P(ctypes.c_double)]
+    lib.oracle_close_frob_sq.restype = None
+    return lib
+
+
+_KIND = {"exp": 1, "invh": 2, "laplace": 3}
+
+
+def close_frob_sq(h2: H2Input, pairs: np.ndarray) -> np.ndarray:
+    """||C_ts||_F^2 of each leaf pair (t, s) of ``pairs`` -- from h2.close when the
+    blocks are stored, else evaluated from the points (close_norm.c)."""
+    import ctypes
+    pairs = np.asarray(pairs, dtype=np.int32).reshape(-1, 2)
+    if h2.close is not None:
+        key = {(int(t), int(s)): i for i, (t, s) in enumerate(h2.near)}
+        return np.array([float(np.sum(h2.close[key[(int(t), int(s))]] ** 2)) for (t, s) in pairs])
+    ks = h2.meta["kernel"]
+    kind = _KIND[ks["kind"]]
+    p0, p1 = {"exp": (ks.get("ell"), ks.get("nugget")), "invh": (ks.get("h"), ks.get("diag_add")),
+              "laplace": (0.0, 1.0 / (4.0 * np.pi * ks.get("h", 1.0)))}[ks["kind"]]
+    x = np.ascontiguousarray(h2.points, dtype=np.float64)
+    pt = np.ascontiguousarray(pairs[:, 0])
+    ps = np.ascontiguousarray(pairs[:, 1])
+    out = np.zeros(len(pairs))
+    P = ctypes.POINTER
+    _close_lib().oracle_close_frob_sq(x.ctypes.data_as(P(ctypes.c_double)), x.shape[1], h2.B,
+                                      pt.ctypes.data_as(P(ctypes.c_int32)), ps.ctypes.data_as(P(ctypes.c_int32)),
+                                      len(pairs), kind, float(p0), float(p1), out.ctypes.data_as(P(ctypes.c_double)))
+    return out
+
+
+def _coupling(h2: H2Input, k: int, j: int, t: int, s: int) -> np.ndarray:
+    if h2.coupling is not None:
+        return h2.coupling[k][j]
+    from h2gen import kernel_matrix
+    base = lvl_off(h2.L, k)
+    return kernel_matrix(h2.meta["kernel"], h2.meta["cheb_nodes_row"][base + t], h2.meta["cheb_nodes_col"][base + s])
+
+
+def gram_matrices(h2: H2Input, side: str = "row") -> List[np.ndarray]:
+    """G_t = R_t^T R_t of every cluster by the nested recursion
+    G_p = sum_a T^(a)T G_ca T^(a) (R_p = diag(R_c1, R_c2) T_p)."""
+    L = h2.L
+    leaf = h2.leaf_row if side == "row" else h2.leaf_col
+    tr = h2.transfer_row if side == "row" else h2.transfer_col
+    rank = h2.rank_row if side == "row" else h2.rank_col
+    G = [None] * n_clusters(L)
+    for i in range(1 << L):
+        R = np.asarray(leaf[i])
+        G[cid(L, 0, i)] = R.T @ R
+    for k in range(1, L + 1):
+        for i in range(1 << (L - k)):
+            p = cid(L, k, i)
+            c1, c2 = cid(L, k - 1, 2 * i), cid(L, k - 1, 2 * i + 1)
+            k1 = int(rank[c1])
+            T = tr[p]
+            G[p] = T[:k1].T @ G[c1] @ T[:k1] + T[k1:].T @ G[c2] @ T[k1:]
+    return G
+
+
+def frobenius_sq_rows(h2: H2Input, level: int, index: int) -> float:
+    """||A_H2[I_c, :]||_F^2 for the rows I_c of cluster c = (level, index):
+    the close blocks with t among c's leaves, tr(D^T G^R_t D G^C_s) for the
+    admissible pairs with t inside c (levels <= level), and for the admissible
+    pairs of c's ancestors a the same with the Gram of a's basis restricted to
+    I_c: R_a[I_c] = R_c T_p1[c's rows] T_p2[p1's rows] ... (nested bases,
+    P:76-84), so G = M^T G_c M.  When k_c = 0 the S rows
+    of c's subtree, (k', t', a) with t' inside c, are U_c^T A V with U_c an
+    orthonormal basis of the coordinates I_c (their count is |I_c| because
+    sum m = |I_c| - k_c), so their ||.||_F^2 equals this (pin P5 per subtree,
+    P:472-484; QR-independent)."""
+    L = h2.L
+    lo_leaf, hi_leaf = index << level, (index + 1) << level
+    near = np.asarray(h2.near)
+    sel = near[(near[:, 0] >= lo_leaf) & (near[:, 0] < hi_leaf)]
+    tot = float(np.sum(close_frob_sq(h2, sel)))
+    Gr = gram_matrices(h2, "row")
+    Gc = Gr if h2.symmetric else gram_matrices(h2, "col")
+    for k in range(min(level + 1, L)):
+        base = lvl_off(L, k)
+        a = np.asarray(h2.adm[k])
+        if not len(a):
+            continue
+        lo_t, hi_t = index << (level - k), (index + 1) << (level - k)
+        for j in np.nonzero((a[:, 0] >= lo_t) & (a[:, 0] < hi_t))[0]:
+            t, s = int(a[j, 0]), int(a[j, 1])
+            D = _coupling(h2, k, int(j), t, s)
+            tot += float(np.trace(D.T @ Gr[base + t] @ D @ Gc[base + s]))
+    # ancestors of c: their bases restricted to the rows of c
+    c = cid(L, level, index)
+    M = np.eye(int(h2.rank_row[c]))
+    u, ui = c, index
+    for k in range(level + 1, L):
+        pi = ui >> 1
+        p = cid(L, k, pi)
+        k1 = int(h2.rank_row[cid(L, k - 1, 2 * pi)])
+        T = h2.transfer_row[p]
+        M = M @ (T[:k1] if (ui & 1) == 0 else T[k1:])
+        G = M.T @ Gr[c] @ M
+        a = np.asarray(h2.adm[k])
+        if len(a):
+            base = lvl_off(L, k)
+            for j in np.nonzero(a[:, 0] == pi)[0]:
+                s = int(a[j, 1])
+                D = _coupling(h2, k, int(j), pi, s)
+                tot += float(np.trace(D.T @ G @ D @ Gc[base + s]))
+        u, ui = p, pi
+    return tot
+
+
+def h2_matvec_rows(h2: H2Input, x: np.ndarray, leaves) -> Dict[int, np.ndarray]:
+    """(A_H2 x) on the rows of the given leaves (pin P13 on a sample at any N):
+    close part sum_s C_ts x_s, far part by the standard upward pass (all
+    clusters) and the coupling / downward passes along the leaves' root paths
+    only.  Close blocks / couplings evaluated when not stored."""
+    from h2gen import kernel_matrix
+    L, B = h2.L, h2.B
+    x = np.asarray(x, dtype=np.float64)
+    ncl = n_clusters(L)
+    xh: List[np.ndarray] = [None] * ncl
+    for i in range(1 << L):
+        xh[cid(L, 0, i)] = np.asarray(h2.leaf_col[i]).T @ x[i * B:(i + 1) * B]
+    for k in range(1, L + 1):
+        for i in range(1 << (L - k)):
+            p = cid(L, k, i)
+            xh[p] = h2.transfer_col[p].T @ np.concatenate([xh[cid(L, k - 1, 2 * i)], xh[cid(L, k - 1, 2 * i + 1)]])
+    near = np.asarray(h2.near)
+    adm_rows = []
+    for k in range(L):
+        a = np.asarray(h2.adm[k])
+        adm_rows.append(a)
+    out = {}
+    for leaf in leaves:
+        y = np.zeros(B)
+        for j in np.nonzero(near[:, 0] == leaf)[0]:
+            s = int(near[j, 1])
+            if h2.close is not None:
+                C = h2.close[j]
+            else:
+                same = np.eye(B, dtype=bool) if s == leaf else None
+                C = kernel_matrix(h2.meta["kernel"], h2.points[leaf * B:(leaf + 1) * B], h2.points[s * B:(s + 1) * B],
+                                  same)
+            y += C @ x[s * B:(s + 1) * B]
+        yh = np.zeros(0)                  # the root's coefficients (k_root = 0)
+        for k in range(L - 1, -1, -1):   # root path, top down
+            t = leaf >> k
+            p = cid(L, k, t)
+            acc = np.zeros(int(h2.rank_row[p]))
+            if yh.size:                   # parent's coefficients through its transfer
+                v = h2.transfer_row[cid(L, k + 1, t >> 1)] @ yh
+                k1 = int(h2.rank_row[cid(L, k, 2 * (t >> 1))])
+                acc = acc + (v[:k1] if (t & 1) == 0 else v[k1:])
+            a = adm_rows[k]
+            if len(a):
+                for j in np.nonzero(a[:, 0] == t)[0]:
+                    s = int(a[j, 1])
+                    acc = acc + _coupling(h2, k, int(j), t, s) @ xh[lvl_off(L, k) + s]
+            yh = acc
+        y += np.asarray(h2.leaf_row[leaf]) @ yh
+        out[int(leaf)] = y
+    return out

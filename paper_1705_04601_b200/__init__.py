@@ -228,6 +228,13 @@ class Plan:
         m = np.diff(np.append(s_off, self.N))
         return off["n_row"] - m
 
+    def ranks(self, side: int = 0) -> np.ndarray:
+        """Rank k_t of every cluster (level-major), row (0) or column (1) side."""
+        off = self.offsets()
+        key = "s_off_row" if side == 0 else "s_off_col"
+        m = np.diff(np.append(off[key], self.N))
+        return (off["n_row" if side == 0 else "n_col"] - m).astype(np.int64)
+
     def launches(self):
         """Per-launch descriptors of one build (kind, level, items, flops, bytes, flops_exec)."""
         n = _i64()
@@ -535,3 +542,38 @@ class VirtualShards:
                                        ctypes.byref(ap) if ap is not None else None, _stream_handle(stream), arr,
                                        len(ev) if ev else 0), "h2sp_build_meta")
         return self.outputs
+
+
+class _ChebSpec(ctypes.Structure):
+    _fields_ = [("dim", _i32), ("orders", _i32 * 3), ("cheb_cos", _f64 * 64)]
+
+
+lib.h2sp_cheb_construct.argtypes = [_vp, _vp, ctypes.c_int, ctypes.POINTER(_ChebSpec), _vp, _vp, _vp, _vp, _vp, _vp,
+                                    _vp]
+
+
+def cheb_construct(plan: Plan, meta_ptr: int, points, box_lo, box_hi, orders, cos_table, side: int = 0,
+                   stream=None) -> dict:
+    """h2sp_cheb_construct: the nested Chebyshev bases of one side on the device.
+    points (N, d), box_lo / box_hi (n_clusters, d): float64 CUDA tensors;
+    orders: base tensor orders (largest-extent axis first); cos_table: the 64
+    cosines (h2gen.cheb_cos_table).  Returns {"leaf", "transfer", "nodes"}."""
+    import torch
+    d = int(points.shape[1])
+    sz = plan.sizes
+    f64 = dict(dtype=torch.float64, device=points.device)
+    leaf = torch.zeros(max(int(sz["leaf_row" if side == 0 else "leaf_col"]), 1), **f64)
+    tr = torch.zeros(max(int(sz["transfer_row" if side == 0 else "transfer_col"]), 1), **f64)
+    off = plan.offsets()
+    n_nodes = int(sum(int(x) for x in (plan.ranks(side))))
+    nodes = torch.zeros(max(n_nodes, 1), d, **f64)
+    spec = _ChebSpec(dim=d)
+    for a in range(3):
+        spec.orders[a] = int(orders[a]) if a < d else 1
+    for i in range(64):
+        spec.cheb_cos[i] = float(cos_table[i])
+    _check(lib.h2sp_cheb_construct(plan.handle, meta_ptr, int(side), ctypes.byref(spec), _dptr(points), _dptr(box_lo),
+                                   _dptr(box_hi), _dptr(leaf), _dptr(tr), _dptr(nodes), _stream_handle(stream)),
+           "h2sp_cheb_construct")
+    del off
+    return {"leaf": leaf, "transfer": tr, "nodes": nodes}

@@ -10,6 +10,10 @@
 using namespace h2sp;
 
 namespace {
+constexpr int L_MAX_CHEB = 30;
+}
+
+namespace {
 
 h2sp_status check_ws(const h2sp_plan_s *P, const void *ws, size_t ws_bytes, size_t need) {
   if (!ws) return fail(H2SP_EINVAL, "workspace is NULL");
@@ -248,6 +252,32 @@ h2sp_status h2sp_eval_kernel_blocks(const h2sp_close_gen *k, const double *x_nod
   if (k->kernel == H2SP_KERNEL_EXP && !(k->p0 > 0.0)) return fail(H2SP_EINVAL, "kernel blocks: exp length p0 <= 0");
   if (h2sp_status s = check_device()) return s;
   return launch_kernel_blocks(k, x_nodes, y_nodes, blocks, n_blocks, out, stream);
+}
+
+h2sp_status h2sp_cheb_construct(h2sp_plan P, const void *meta, int side, const h2sp_cheb_spec *spec,
+                                const double *points, const double *box_lo, const double *box_hi, double *leaf_basis,
+                                double *transfer, double *nodes, void *stream) {
+  if (!P || !meta || !spec || !points || !box_lo || !box_hi || !leaf_basis || !nodes)
+    return fail(H2SP_EINVAL, "NULL argument");
+  if (side != 0 && side != 1) return fail(H2SP_EINVAL, "side must be 0 (row) or 1 (column)");
+  if (spec->dim < 1 || spec->dim > 3) return fail(H2SP_EINVAL, "dim must be 1, 2 or 3");
+  int r = 1;
+  for (int a = 0; a < spec->dim; a++) {
+    if (spec->orders[a] < 1 || spec->orders[a] > 8) return fail(H2SP_EINVAL, "orders must lie in [1, 8]");
+    r *= spec->orders[a];
+  }
+  if (r > 64) return fail(H2SP_EINVAL, "prod(orders) > 64");
+  const auto &k = (side && !P->sym) ? P->k_col : P->k_row;
+  for (int64_t c = 0; c < P->ncl; c++)
+    if (k[c] != 0 && k[c] != r)
+      return fail(H2SP_ERANK, "cluster " + std::to_string(c) + ": rank " + std::to_string(k[c]) +
+                                  " is neither 0 nor prod(orders) = " + std::to_string(r));
+  if (P->ncl > (int64_t(1) << L_MAX_CHEB)) return fail(H2SP_EUNSUPPORTED, "too many clusters");
+  if ((side ? P->tr_col_len : P->tr_row_len) > 0 && !transfer && !(side && P->sym))
+    return fail(H2SP_EINVAL, "NULL transfer");
+  if (h2sp_status s = check_device()) return s;
+  return launch_cheb_construct(P, static_cast<const unsigned char *>(meta), side, spec, points, box_lo, box_hi,
+                               leaf_basis, transfer, nodes, stream);
 }
 
 int64_t h2sp_apply_ws_bytes(h2sp_plan P, int nrhs) {

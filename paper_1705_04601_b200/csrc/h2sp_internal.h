@@ -206,6 +206,9 @@ h2sp_status launch_build(const h2sp_plan_s *p, const h2sp_inputs *in, const h2sp
 h2sp_status launch_csr_early(const h2sp_plan_s *p, unsigned char *ws, int64_t *d_rowptr, int32_t *d_col,
                              int64_t *h_rowptr, int32_t *h_col, void *stream);
 h2sp_status launch_csr_early_join(const h2sp_plan_s *p, void *stream);
+h2sp_status launch_cheb_construct(const h2sp_plan_s *P, const unsigned char *meta, int side, const h2sp_cheb_spec *s,
+                                  const double *points, const double *box_lo, const double *box_hi, double *leaf,
+                                  double *transfer, double *nodes, void *stream);
 h2sp_status launch_kernel_blocks(const h2sp_close_gen *k, const double *xn, const double *yn,
                                  const h2sp_block_desc *blocks, int64_t n_blocks, double *out, void *stream);
 h2sp_status launch_apply_Ut(const h2sp_plan_s *p, const double *q, const double *b, int64_t ldb, double *y,

@@ -3261,4 +3261,175 @@ h2sp_status launch_apply_V(const h2sp_plan_s *P, const double *q, const double *
   return H2SP_OK;
 }
 
+
+
+// --------------------------------------------------------------------------
+// GPU H^2 construction (the input side of the path):
+// nested bases by tensor Chebyshev interpolation on each cluster's box -- the
+// recipe of the synthetic inputs evaluated where the build
+// consumes it.  Per cluster of rank k = prod(p_a) > 0:
+//   box padded by max(1e-9 ext, 1e-12) per axis; orders p_a = the base orders
+//   assigned to the axes by decreasing extent (stable);
+//   axis nodes  mid + half * c_j (c_j = the host's cosine table; p = 1: mid);
+//   nodes       tensor grid, axis 0 slowest;
+//   basis(x)[j] = prod_a l_{j_a}(x_a), l_j(x) = prod_{m != j} (x - n_m) / (n_j - n_m)
+//               multiplied in the order m = 0.., axes 0..d-1;
+//   leaf R_t = basis_t(points of t), transfer rows of child c = basis_p(nodes_c).
+// Every operation is an explicitly rounded IEEE op (no contraction), so the
+// arrays equal the numpy generator's bit for bit.
+// --------------------------------------------------------------------------
+struct ChebArgs {
+  int dim, ords[3];
+  double cosv[9][8];            // cosv[p][j], p = 1..8
+  const double *lo, *hi;        // tight cluster boxes, n_clusters x dim
+};
+
+struct ChebBox {
+  int p[3];
+  double nodes[3][8];
+};
+
+__device__ __forceinline__ ChebBox cheb_box(const ChebArgs &A, int64_t c) {
+  ChebBox b;
+  double lo[3], hi[3], ext[3];
+  for (int a = 0; a < 3; a++) {
+    lo[a] = hi[a] = ext[a] = 0.0;
+    b.p[a] = 1;
+  }
+  for (int a = 0; a < A.dim; a++) {
+    const double l = A.lo[c * A.dim + a], h = A.hi[c * A.dim + a];
+    ext[a] = __dsub_rn(h, l);
+    const double pad = fmax(__dmul_rn(ext[a], 1e-9), 1e-12);
+    lo[a] = __dsub_rn(l, pad);
+    hi[a] = __dadd_rn(h, pad);
+  }
+  // axes by decreasing extent, stable (argsort of -ext)
+  int order[3] = {0, 1, 2};
+  for (int i = 1; i < A.dim; i++)
+    for (int j = i; j > 0 && ext[order[j]] > ext[order[j - 1]]; j--) {
+      const int t = order[j];
+      order[j] = order[j - 1];
+      order[j - 1] = t;
+    }
+  for (int i = 0; i < A.dim; i++) b.p[order[i]] = A.ords[i];
+  for (int a = 0; a < A.dim; a++) {
+    const int p = b.p[a];
+    const double mid = __ddiv_rn(__dadd_rn(lo[a], hi[a]), 2.0);
+    const double half = __ddiv_rn(__dsub_rn(hi[a], lo[a]), 2.0);
+    for (int j = 0; j < 8; j++) b.nodes[a][j] = (j < p) ? (p == 1 ? mid : __dadd_rn(mid, __dmul_rn(half, A.cosv[p][j]))) : 0.0;
+  }
+  return b;
+}
+
+// basis_b(x) -> out[0 .. prod p) (stride 1)
+__device__ __forceinline__ void cheb_basis(const ChebBox &b, int dim, const double *x, double *out) {
+  double l[3][8];
+  for (int a = 0; a < dim; a++) {
+    const int p = b.p[a];
+    for (int j = 0; j < p; j++) {
+      double v = 1.0;
+      for (int m = 0; m < p; m++)
+        if (m != j) v = __dmul_rn(v, __ddiv_rn(__dsub_rn(x[a], b.nodes[a][m]), __dsub_rn(b.nodes[a][j], b.nodes[a][m])));
+      l[a][j] = v;
+    }
+  }
+  const int p0 = b.p[0], p1 = dim > 1 ? b.p[1] : 1, p2 = dim > 2 ? b.p[2] : 1;
+  for (int j0 = 0; j0 < p0; j0++)
+    for (int j1 = 0; j1 < p1; j1++)
+      for (int j2 = 0; j2 < p2; j2++) {
+        double v = l[0][j0];
+        if (dim > 1) v = __dmul_rn(v, l[1][j1]);
+        if (dim > 2) v = __dmul_rn(v, l[2][j2]);
+        out[(j0 * p1 + j1) * p2 + j2] = v;
+      }
+}
+
+// one thread per (cluster, node): the node coordinates
+__global__ void __launch_bounds__(256) cheb_nodes_kernel(ChebArgs A, Side sd, int64_t ncl, int r, double *__restrict__ nodes) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= ncl * r) return;
+  const int64_t c = t / r;
+  const int j = int(t - c * r);
+  if (sd.k[c] == 0) return;
+  const ChebBox b = cheb_box(A, c);
+  const int p1 = A.dim > 1 ? b.p[1] : 1, p2 = A.dim > 2 ? b.p[2] : 1;
+  const int j0 = j / (p1 * p2), j1 = (j / p2) % p1, j2 = j % p2;
+  double *o = nodes + (sd.zb_off[c] + j) * A.dim;
+  o[0] = b.nodes[0][j0];
+  if (A.dim > 1) o[1] = b.nodes[1][j1];
+  if (A.dim > 2) o[2] = b.nodes[2][j2];
+}
+
+// one thread per (leaf, point): row i of R_t
+__global__ void __launch_bounds__(128) cheb_leaf_kernel(ChebArgs A, Side sd, int64_t nleaf, int B,
+                                                        const double *__restrict__ pts, double *__restrict__ leaf) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nleaf * B) return;
+  const int64_t c = t / B;
+  const int i = int(t - c * B);
+  const int k = sd.k[c];
+  if (k == 0) return;
+  const ChebBox b = cheb_box(A, c);
+  double x[3] = {0.0, 0.0, 0.0};
+  for (int a = 0; a < A.dim; a++) x[a] = pts[t * A.dim + a];
+  double row[64];
+  cheb_basis(b, A.dim, x, row);
+  double *o = leaf + sd.leaf_off[c] + int64_t(i) * k;
+  for (int j = 0; j < k; j++) o[j] = row[j];
+}
+
+// one thread per (internal cluster p, row of T_p): row i is child c's node
+// i (child 1 first) under p's basis; zero rows when p has rank 0 handled by
+// the k == 0 exit (T_p has no columns then)
+__global__ void __launch_bounds__(128) cheb_transfer_kernel(ChebArgs A, Side sd, int L, int64_t nint, int rmax,
+                                                            const double *__restrict__ nodes, double *__restrict__ tr) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nint * 2 * rmax) return;
+  const int64_t pi = t / (2 * rmax);           // internal cluster index (level-major, after the leaves)
+  const int i = int(t - pi * 2 * rmax);        // row of T_p (< k_c1 + k_c2)
+  const int64_t p = (int64_t(1) << L) + pi;
+  const int kp = sd.k[p], n = sd.n[p];
+  if (kp == 0 || i >= n) return;
+  int k_ = 0;  // level of p
+  while (p >= lvl_off_d(L, k_ + 1)) k_++;
+  const int64_t c1 = lvl_off_d(L, k_ - 1) + 2 * (p - lvl_off_d(L, k_));
+  const int k1 = sd.k[c1];
+  const int64_t c = i < k1 ? c1 : c1 + 1;
+  const int ii = i < k1 ? i : i - k1;
+  const ChebBox b = cheb_box(A, p);
+  double x[3] = {0.0, 0.0, 0.0};
+  for (int a = 0; a < A.dim; a++) x[a] = nodes[(sd.zb_off[c] + ii) * A.dim + a];
+  double row[64];
+  cheb_basis(b, A.dim, x, row);
+  double *o = tr + sd.tr_off[p] + int64_t(i) * kp;
+  for (int j = 0; j < kp; j++) o[j] = row[j];
+}
+
+h2sp_status launch_cheb_construct(const h2sp_plan_s *P, const unsigned char *meta, int side, const h2sp_cheb_spec *s,
+                                  const double *points, const double *box_lo, const double *box_hi, double *leaf,
+                                  double *transfer, double *nodes, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const Clusters cl = make_clusters(P, meta);
+  const Side sd = side_of(cl, side != 0);
+  ChebArgs A{};
+  A.dim = s->dim;
+  for (int a = 0; a < 3; a++) A.ords[a] = a < s->dim ? s->orders[a] : 1;
+  for (int p = 0; p <= 8; p++)
+    for (int j = 0; j < 8; j++) A.cosv[p][j] = (p >= 1 && j < p) ? s->cheb_cos[(p - 1) * 8 + j] : 0.0;
+  A.lo = box_lo;
+  A.hi = box_hi;
+  int r = 1;
+  for (int a = 0; a < s->dim; a++) r *= s->orders[a];
+  const int64_t ncl = P->ncl, nleaf = int64_t(1) << P->L;
+  cheb_nodes_kernel<<<unsigned((ncl * r + 255) / 256), 256, 0, st>>>(A, sd, ncl, r, nodes);
+  H2SP_CK(cudaGetLastError());
+  cheb_leaf_kernel<<<unsigned((nleaf * P->B + 127) / 128), 128, 0, st>>>(A, sd, nleaf, P->B, points, leaf);
+  H2SP_CK(cudaGetLastError());
+  const int64_t nint = ncl - nleaf;
+  if (nint > 0) {
+    cheb_transfer_kernel<<<unsigned((nint * 2 * r + 127) / 128), 128, 0, st>>>(A, sd, P->L, nint, r, nodes, transfer);
+    H2SP_CK(cudaGetLastError());
+  }
+  return H2SP_OK;
+}
 }  // namespace h2sp

@@ -319,3 +319,73 @@ def test_orthonormalize_preserves_matrix():
     for R in h1.leaf_row:
         if R.shape[1]:
             assert np.abs(R.T @ R - np.eye(R.shape[1])).max() <= 1e-13
+
+
+# ---- checks at sizes where C / D are never stored (config 5 at full size) ----
+
+def test_close_frob_sq_c_helper_matches_generator_blocks():
+    """The plain-C close-block norms (close_norm.c) equal the generator's stored
+    blocks for each config kernel (exp / 1/(r+h) / Laplace, incl. the diagonal
+    self-terms)."""
+    for cfg, N in ((2, 4096), (3, 4096), (4, 4096)):
+        h = h2gen.make_config(cfg, N=N)
+        ref = np.array([float(np.sum(C * C)) for C in h.close])
+        hs = h2gen.make_structure(cfg, N=N)
+        got = oracle.close_frob_sq(hs, hs.near)
+        assert np.allclose(got, ref, rtol=1e-13, atol=0), cfg
+
+
+@pytest.mark.parametrize("make", [lambda: h2gen.random_h2(4, 8, 3, True), lambda: h2gen.random_h2(4, 8, 4, False),
+                                  lambda: h2gen.make_config(2, N=2048)])
+def test_frobenius_sq_rows_is_the_dense_row_norm(make):
+    h = make()
+    A = oracle.dense_A(h)
+    L, B = h.L, h.B
+    for level in range(L + 1):
+        for index in (0, (1 << (L - level)) - 1):
+            rows = slice((index << level) * B, ((index + 1) << level) * B)
+            ref = float(np.sum(A[rows] ** 2))
+            assert abs(oracle.frobenius_sq_rows(h, level, index) - ref) <= 1e-12 * ref
+
+
+def test_subtree_frobenius_identity_on_oracle_S():
+    """The reading behind the per-subtree P5: for a rank-0 cluster c, the S rows
+    of c's subtree carry exactly ||A_H2[I_c, :]||_F^2."""
+    h = h2gen.make_config(5, N=16384)
+    res = oracle.sparsify(h)
+    S = oracle.s_dense(res)
+    L = h.L
+    kr = np.asarray(h.rank_row)
+    for level in range(1, L + 1):
+        M = 1 << (L - level)
+        cs = [h2gen.cid(L, level, i) for i in range(M)]
+        if any(kr[c] for c in cs):
+            continue
+        for index in range(min(M, 2)):
+            rows = []
+            for k in range(level + 1):
+                for t in range(index << (level - k), (index + 1) << (level - k)):
+                    c = h2gen.cid(L, k, t)
+                    rows += list(range(res.off_row[c], res.off_row[c] + int(res.m_row[c])))
+            got = float(np.sum(S[rows] ** 2))
+            ref = oracle.frobenius_sq_rows(h, level, index)
+            assert abs(got - ref) <= 1e-12 * ref
+        return
+    pytest.fail("no rank-0 level")
+
+
+def test_structure_only_inputs_reproduce_make_config():
+    """make_structure + fill_cheb_bases = make_config's tree, ranks and bases
+    bit for bit; the matvec on sampled rows with C / D evaluated on the fly
+    equals the full H^2 matvec."""
+    h = h2gen.make_config(5, N=8192)
+    hs = h2gen.fill_cheb_bases(h2gen.make_structure(5, N=8192))
+    assert np.array_equal(h.near, hs.near) and np.array_equal(h.rank_row, hs.rank_row)
+    for a, b in zip(h.leaf_row, hs.leaf_row):
+        assert np.array_equal(a, b)
+    x = np.random.default_rng(1).standard_normal(h.N)
+    full = oracle.h2_matvec(h, x)
+    rows = oracle.h2_matvec_rows(hs, x, [0, 17, (h.N // h.B) - 1])
+    for leaf, y in rows.items():
+        ref = full[leaf * h.B:(leaf + 1) * h.B]
+        assert np.linalg.norm(y - ref) <= 1e-13 * np.linalg.norm(full)
