@@ -187,7 +187,7 @@ h2sp_status h2sp_eval_kernel_blocks(const h2sp_close_gen *k, const double *x_nod
  * of the numpy generator the arrays are bitwise equal to it.
  * points: DEVICE N x dim (tree order); box_lo / box_hi: DEVICE n_clusters x dim
  * tight boxes; `meta`: the plan's uploaded work lists (h2sp_plan_upload).
- * Outputs DEVICE, lengths from h2sp_sizes (nodes: sum of ranks x dim).
+ * Outputs DEVICE, lengths as in the plan sizes; nodes: sum of ranks x dim.
  * Asynchronous on `stream`.  H2SP_ERANK if a rank is neither 0 nor prod(orders). */
 typedef struct {
   int32_t dim;            /* 1..3 */
