@@ -334,10 +334,21 @@ def run_protocol(args, rank, world, local_rank):
         for s_, n in enumerate(n_launch):
             for j in range(n):
                 per[s_][j] += evs[i][s_][2 * j].elapsed_time(evs[i][s_][2 * j + 1]) / args.steps
-    # the checks (||S||_F^2, ||S w||^2 of this rank's rows) through the collective
-    chk = torch.stack([run.outputs["bench_r2"].sum(), (run.outputs["bench_y"] ** 2).sum()])
-    if world > 1:
-        dist.all_reduce(chk)
+    # the checks (||S||_F^2, ||S w||^2 of this rank's rows) through libh2sp's NCCL
+    # communicator (bootstrapped from the torch process group; world 1 included,
+    # so the single-GPU run exercises the same path)
+    import paper_1705_04601_b200 as h2sp
+    nccl_info = None
+    chk = torch.stack([run.outputs["bench_r2"].sum(), (run.outputs["bench_y"] ** 2).sum()]).contiguous()
+    try:
+        comm = h2sp.torch_comm(rank, world)
+        comm.allreduce(chk)
+        torch.cuda.synchronize()
+        nccl_info = {"comm_nranks": world, "comm_ok": True}
+    except h2sp.H2spError as exc:
+        if world > 1:
+            raise
+        nccl_info = {"comm_ok": False, "error": str(exc)[:200]}
     offs = plans[0].offsets()
     loc_any = np.zeros(int(plans[0].sizes["n_clusters"]), dtype=bool)
     for p in plans:
@@ -459,7 +470,9 @@ def run_protocol(args, rank, world, local_rank):
                        "breakdown_ms_summed": {k: round(v, 3) for k, v in kinds.items()},
                        "per_kind_level": {k: {"ms": round(v[0], 3), "tflops_exec": round(v[1] / max(v[0], 1e-9) * 1e-9, 2)}
                                           for k, v in per_level.items()},
-                       "checks": {"S_frob2": float(chk[0]), "y_norm2": float(chk[1])},
+                       "checks": {"S_frob2": float(chk[0]), "y_norm2": float(chk[1]),
+                                  "collective": "h2sp_comm_allreduce (NCCL) over all ranks"},
+                       "nccl": nccl_info,
                        "env": _env_knobs()},
             "roofline": roof,
             "cpu_baseline": cpu,

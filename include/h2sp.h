@@ -402,6 +402,25 @@ h2sp_status h2sp_apply_Ut(h2sp_plan plan, const double *q_row, const double *b, 
 h2sp_status h2sp_apply_V(h2sp_plan plan, const double *q_col, const double *y, int64_t ldy, double *x,
                          int64_t ldx, int nrhs, void *ws, size_t ws_bytes, void *stream);
 
+/* Multi-GPU communicator: one process per GPU; NCCL over
+ * NVLink, loaded with dlopen on first use (H2SP_ENCCL if unavailable -- no
+ * fallback).  Bootstrap: rank 0 calls h2sp_comm_unique_id, the caller's
+ * process group (torch.distributed) broadcasts the 128 bytes, every rank calls
+ * h2sp_comm_init on its own device (the current CUDA device).  The sharded
+ * build has no data-path exchange (each shard recomputes its halo Q / R^,
+ * DESIGN.md §10); the collectives are the checks and the assembly of the
+ * distributed results: h2sp_comm_allreduce sums (H2SP_SUM) or maximises
+ * (H2SP_MAX) n doubles of a DEVICE buffer in place on `stream` -- e.g. the
+ * bench-mode y = S w of all ranks (their rows are disjoint). */
+typedef struct h2sp_comm_s *h2sp_comm;
+#define H2SP_SUM 0
+#define H2SP_MAX 1
+h2sp_status h2sp_comm_unique_id(void *id /* 128 bytes out */);
+h2sp_status h2sp_comm_init(const void *id, int rank, int world, h2sp_comm *out);
+h2sp_status h2sp_comm_allreduce(h2sp_comm comm, double *buf, int64_t n, int op, void *stream);
+h2sp_status h2sp_comm_info(h2sp_comm comm, int *rank, int *world);
+void h2sp_comm_destroy(h2sp_comm comm);
+
 #ifdef __cplusplus
 }
 #endif

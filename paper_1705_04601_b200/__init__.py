@@ -577,3 +577,54 @@ def cheb_construct(plan: Plan, meta_ptr: int, points, box_lo, box_hi, orders, co
            "h2sp_cheb_construct")
     del off
     return {"leaf": leaf, "transfer": tr, "nodes": nodes}
+
+
+lib.h2sp_comm_unique_id.argtypes = [_vp]
+lib.h2sp_comm_init.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)]
+lib.h2sp_comm_allreduce.argtypes = [_vp, _vp, _i64, ctypes.c_int, _vp]
+lib.h2sp_comm_info.argtypes = [_vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+lib.h2sp_comm_destroy.argtypes = [_vp]
+lib.h2sp_comm_destroy.restype = None
+SUM, MAX = 0, 1
+
+
+class Comm:
+    """NCCL communicator of libh2sp (h2sp_comm_*), bootstrapped through a torch
+    process group: rank 0 draws the unique id, the group broadcasts it."""
+
+    def __init__(self, rank: int, world: int, broadcast=None):
+        """broadcast(bytes) -> bytes: the caller's rank-0 broadcast (e.g. through
+        torch.distributed.broadcast_object_list); None for world == 1."""
+        buf = ctypes.create_string_buffer(128)
+        if rank == 0:
+            _check(lib.h2sp_comm_unique_id(buf), "h2sp_comm_unique_id")
+        uid = bytes(buf.raw)
+        if world > 1:
+            uid = broadcast(uid)
+        ctypes.memmove(buf, uid, 128)
+        h = _vp()
+        _check(lib.h2sp_comm_init(buf, int(rank), int(world), ctypes.byref(h)), "h2sp_comm_init")
+        self.handle = h
+        self.rank, self.world = rank, world
+
+    def allreduce(self, t, op: int = SUM, stream=None):
+        """In-place sum / max of a contiguous float64 CUDA tensor across ranks."""
+        _check(lib.h2sp_comm_allreduce(self.handle, t.data_ptr(), t.numel(), op, _stream_handle(stream)),
+               "h2sp_comm_allreduce")
+        return t
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h and lib is not None:
+            lib.h2sp_comm_destroy(h)
+            self.handle = None
+
+
+def torch_comm(rank: int, world: int) -> Comm:
+    """A Comm bootstrapped from the initialised torch.distributed default group."""
+    def bcast(uid: bytes) -> bytes:
+        import torch.distributed as dist
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        return obj[0]
+    return Comm(rank, world, bcast if world > 1 else None)

@@ -3321,27 +3321,25 @@ __device__ __forceinline__ ChebBox cheb_box(const ChebArgs &A, int64_t c) {
   return b;
 }
 
-// basis_b(x) -> out[0 .. prod p) (stride 1)
-__device__ __forceinline__ void cheb_basis(const ChebBox &b, int dim, const double *x, double *out) {
-  double l[3][8];
-  for (int a = 0; a < dim; a++) {
-    const int p = b.p[a];
-    for (int j = 0; j < p; j++) {
-      double v = 1.0;
-      for (int m = 0; m < p; m++)
-        if (m != j) v = __dmul_rn(v, __ddiv_rn(__dsub_rn(x[a], b.nodes[a][m]), __dsub_rn(b.nodes[a][j], b.nodes[a][m])));
-      l[a][j] = v;
-    }
-  }
-  const int p0 = b.p[0], p1 = dim > 1 ? b.p[1] : 1, p2 = dim > 2 ? b.p[2] : 1;
-  for (int j0 = 0; j0 < p0; j0++)
-    for (int j1 = 0; j1 < p1; j1++)
-      for (int j2 = 0; j2 < p2; j2++) {
-        double v = l[0][j0];
-        if (dim > 1) v = __dmul_rn(v, l[1][j1]);
-        if (dim > 2) v = __dmul_rn(v, l[2][j2]);
-        out[(j0 * p1 + j1) * p2 + j2] = v;
-      }
+// Lagrange polynomial j of the p nodes of axis a at x: prod_{m != j} (x - n_m) / (n_j - n_m),
+// multiplied in the order m = 0, 1, ... (the generator's order)
+__device__ __forceinline__ double cheb_lagrange(const ChebBox &b, int a, int j, double x) {
+  double v = 1.0;
+#pragma unroll
+  for (int m = 0; m < 8; m++)
+    if (m < b.p[a] && m != j) v = __dmul_rn(v, __ddiv_rn(__dsub_rn(x, b.nodes[a][m]), __dsub_rn(b.nodes[a][j], b.nodes[a][m])));
+  return v;
+}
+
+// basis function jj (axis-0-slowest multi-index) of box b at the point (x0, x1, x2):
+// ((l_0 * l_1) * l_2) as the generator's reshaped outer products
+__device__ __forceinline__ double cheb_basis_fn(const ChebBox &b, int dim, int jj, double x0, double x1, double x2) {
+  const int p1 = dim > 1 ? b.p[1] : 1, p2 = dim > 2 ? b.p[2] : 1;
+  const int j0 = jj / (p1 * p2), j1 = (jj / p2) % p1, j2 = jj % p2;
+  double v = cheb_lagrange(b, 0, j0, x0);
+  if (dim > 1) v = __dmul_rn(v, cheb_lagrange(b, 1, j1, x1));
+  if (dim > 2) v = __dmul_rn(v, cheb_lagrange(b, 2, j2, x2));
+  return v;
 }
 
 // one thread per (cluster, node): the node coordinates
@@ -3370,12 +3368,10 @@ __global__ void __launch_bounds__(128) cheb_leaf_kernel(ChebArgs A, Side sd, int
   const int k = sd.k[c];
   if (k == 0) return;
   const ChebBox b = cheb_box(A, c);
-  double x[3] = {0.0, 0.0, 0.0};
-  for (int a = 0; a < A.dim; a++) x[a] = pts[t * A.dim + a];
-  double row[64];
-  cheb_basis(b, A.dim, x, row);
+  const double *xp = pts + t * A.dim;
+  const double x0 = xp[0], x1 = A.dim > 1 ? xp[1] : 0.0, x2 = A.dim > 2 ? xp[2] : 0.0;
   double *o = leaf + sd.leaf_off[c] + int64_t(i) * k;
-  for (int j = 0; j < k; j++) o[j] = row[j];
+  for (int j = 0; j < k; j++) o[j] = cheb_basis_fn(b, A.dim, j, x0, x1, x2);
 }
 
 // one thread per (internal cluster p, row of T_p): row i is child c's node
@@ -3397,12 +3393,10 @@ __global__ void __launch_bounds__(128) cheb_transfer_kernel(ChebArgs A, Side sd,
   const int64_t c = i < k1 ? c1 : c1 + 1;
   const int ii = i < k1 ? i : i - k1;
   const ChebBox b = cheb_box(A, p);
-  double x[3] = {0.0, 0.0, 0.0};
-  for (int a = 0; a < A.dim; a++) x[a] = nodes[(sd.zb_off[c] + ii) * A.dim + a];
-  double row[64];
-  cheb_basis(b, A.dim, x, row);
+  const double *xp = nodes + (sd.zb_off[c] + ii) * A.dim;
+  const double x0 = xp[0], x1 = A.dim > 1 ? xp[1] : 0.0, x2 = A.dim > 2 ? xp[2] : 0.0;
   double *o = tr + sd.tr_off[p] + int64_t(i) * kp;
-  for (int j = 0; j < kp; j++) o[j] = row[j];
+  for (int j = 0; j < kp; j++) o[j] = cheb_basis_fn(b, A.dim, j, x0, x1, x2);
 }
 
 h2sp_status launch_cheb_construct(const h2sp_plan_s *P, const unsigned char *meta, int side, const h2sp_cheb_spec *s,
