@@ -16,11 +16,11 @@ Parity status of each function is listed in DESIGN.md ("Oracle pins").  The
 complement columns W_t^perp are pinned through the LAPACK routine
 ``numpy.linalg.qr(mode='complete')`` (pin P4) and through invariants (P5, P6).
 """
-from .sparsify import (OracleResult, apply_Ut, apply_V, householder_complete, s_csr, s_dense, s_offsets,
+from .sparsify import (OracleResult, apply_Ut, apply_V, householder_complete, householder_margins, s_csr, s_dense, s_offsets,
                        sparsify)
 from .dense import (close_frob_sq, dense_A, dense_U, effective_bases, frobenius_sq, frobenius_sq_rows,
                     gram_matrices, h2_matvec, h2_matvec_rows, pattern_rule)
 
-__all__ = ["OracleResult", "apply_Ut", "apply_V", "householder_complete", "s_csr", "s_dense", "s_offsets",
+__all__ = ["OracleResult", "apply_Ut", "apply_V", "householder_complete", "householder_margins", "s_csr", "s_dense", "s_offsets",
            "sparsify", "dense_A", "dense_U", "effective_bases", "frobenius_sq", "h2_matvec", "pattern_rule",
            "close_frob_sq", "frobenius_sq_rows", "gram_matrices", "h2_matvec_rows"]

@@ -30,7 +30,7 @@ upper->lower, row strips only) so that U == V and S is bitwise symmetric
 from __future__ import annotations
 
 import dataclasses
-from typing import Dict, List, Tuple
+from typing import Optional, Dict, List, Tuple
 
 import numpy as np
 
@@ -43,13 +43,15 @@ Pair = Tuple[int, int]
 # Convention H: Householder QR with a square Q, LAPACK semantics
 # ----------------------------------------------------------------------------
 
-def householder_complete(X: np.ndarray):
+def householder_complete(X: np.ndarray, record: Optional[list] = None):
     """Q (n x n, orthogonal) and R^ (k x k, upper triangular) with
     X = Q[:, :k] R^.  For j = 0..k-1 on x = X[j:, j]: alpha = x_0,
     sigma = ||x_1:||; sigma == 0 exactly -> tau = 0, beta = alpha; otherwise
     beta = -sgn(alpha) hypot(alpha, sigma) with sgn(+-0) = +1,
     tau = (beta - alpha)/beta, v = [1; x_1:/(alpha - beta)].
-    Q = H_0 H_1 ... H_{k-1} I_n (dorg2r order).  k = 0 -> Q = I."""
+    Q = H_0 H_1 ... H_{k-1} I_n (dorg2r order).  k = 0 -> Q = I.
+    ``record`` (optional list): receives (alpha, sigma) of every step -- the
+    quantities whose sign / zero tests convention H decides (reading 2)."""
     X = np.array(X, dtype=np.float64, copy=True)
     n, k = X.shape
     assert k <= n, (n, k)
@@ -59,6 +61,8 @@ def householder_complete(X: np.ndarray):
         x = X[j:, j]
         alpha = float(x[0])
         sigma = float(np.sqrt(np.dot(x[1:], x[1:]))) if n - j > 1 else 0.0
+        if record is not None:
+            record.append((alpha, sigma))
         if sigma == 0.0:
             tau = 0.0
             v = np.zeros(n - j)
@@ -409,3 +413,47 @@ def apply_V(res: OracleResult, y: np.ndarray, side: str = "col") -> np.ndarray:
                 zb[cid(L, k - 1, 2 * i)] = w[:k1]
                 zb[cid(L, k - 1, 2 * i + 1)] = w[k1:]
     return x
+
+
+def householder_margins(h2: H2Input) -> dict:
+    """Survey reading 2 (the Householder tie-break hazard): run the QR pass of
+    step (i) on every cluster of both sides, in the paper's order (the same
+    X_t as sparsify), and report the smallest relative margin of the two
+    decisions convention H takes exactly -- the sign of alpha (alpha_margin =
+    min |alpha| / sigma) and sigma == 0 (sigma_margin = min sigma / |alpha|),
+    over the steps with alpha != 0 and sigma != 0; min_margin = the smaller.
+    Inputs with a margin below 1e-8 are ill-posed for parity (two correct
+    implementations may take different branches); exact zeros (axis-aligned pin
+    P8) are not hazards."""
+    L = h2.L
+    ncl = n_clusters(L)
+    out = {"min_margin": float("inf"), "alpha_margin": float("inf"), "sigma_margin": float("inf"), "steps": 0,
+           "exact_zero_steps": 0, "worst_cluster": None}
+    for side in ("row",) + (() if h2.symmetric else ("col",)):
+        rank = np.asarray(h2.rank_row if side == "row" else h2.rank_col)
+        leaf = h2.leaf_row if side == "row" else h2.leaf_col
+        tr = h2.transfer_row if side == "row" else h2.transfer_col
+        R: List[np.ndarray] = [None] * ncl
+        for k in range(L + 1):
+            for i in range(1 << (L - k)):
+                c = cid(L, k, i)
+                if k == 0:
+                    X = np.asarray(leaf[i])
+                else:
+                    c1, c2 = cid(L, k - 1, 2 * i), cid(L, k - 1, 2 * i + 1)
+                    k1 = int(rank[c1])
+                    X = np.vstack([R[c1] @ tr[c][:k1], R[c2] @ tr[c][k1:]])
+                rec: list = []
+                _, R[c] = householder_complete(X, rec)
+                for (a, sg) in rec:
+                    out["steps"] += 1
+                    if a == 0.0 or sg == 0.0:
+                        out["exact_zero_steps"] += 1
+                        continue
+                    out["alpha_margin"] = min(out["alpha_margin"], abs(a) / sg)
+                    out["sigma_margin"] = min(out["sigma_margin"], sg / abs(a))
+                    m = min(abs(a) / sg, sg / abs(a))
+                    if m < out["min_margin"]:
+                        out["min_margin"] = m
+                        out["worst_cluster"] = (side, k, i)
+    return out

@@ -28,6 +28,51 @@ def _run(h, explicit_q=False):
     return plan, sp, out
 
 
+def _level_block_errors(plan, rowptr, col, v, val, tol, per_block=True):
+    """Gate the error per level of the S row's cluster (relative, tol) and per
+    S block (t@i, s@j): ||dS_b|| <= 1e3 tol ||S_b|| + 10 tol ||S_(t@i, :)|| --
+    a wrong block fails even when it is tiny next to ||S||_F, while round-off
+    carried from the block's whole strip chain (the block row's scale) passes.
+    Returns (worst level error, worst block error relative to the block)."""
+    off = plan.offsets()
+    N = plan.N
+    ncl = len(off["s_off_row"])
+    m_r = np.diff(np.append(off["s_off_row"], N))
+    m_c = np.diff(np.append(off["s_off_col"], N))
+    row_cl = np.repeat(np.arange(ncl), m_r)
+    col_cl = np.repeat(np.arange(ncl), m_c)
+    L = plan.L
+    lvl = np.zeros(ncl, dtype=np.int64)
+    for k in range(L + 1):
+        lvl[(1 << (L + 1)) - (1 << (L - k + 1)):] = k
+    rows = np.repeat(np.arange(N), np.diff(rowptr))
+    d2 = (v - val) ** 2
+    r2 = val ** 2
+    rl = lvl[row_cl[rows]]
+    e_l = np.bincount(rl, d2, minlength=L + 1)
+    n_l = np.bincount(rl, r2, minlength=L + 1)
+    worst_level = 0.0
+    for k in range(L + 1):
+        if n_l[k] > 0:
+            e = np.sqrt(e_l[k] / n_l[k])
+            worst_level = max(worst_level, e)
+            assert e <= tol, ("level", k, e)
+    worst_block = 0.0
+    if per_block:
+        key = row_cl[rows] * ncl + col_cl[col]
+        uq, inv = np.unique(key, return_inverse=True)
+        eb = np.sqrt(np.bincount(inv, d2))
+        nb = np.sqrt(np.bincount(inv, r2))
+        brow = uq // ncl
+        nrow = np.sqrt(np.bincount(brow, nb ** 2, minlength=ncl))[brow]
+        bad = eb > 1e3 * tol * nb + 10 * tol * nrow
+        assert not bad.any(), ("blocks", int(bad.sum()), [(int(uq[i] // ncl), int(uq[i] % ncl)) for i in
+                                                         np.nonzero(bad)[0][:5]])
+        rel = eb[nb > 0] / nb[nb > 0]
+        worst_block = float(rel.max()) if len(rel) else 0.0
+    return worst_level, worst_block
+
+
 def _compare(h, plan, out, res=None, tol=1e-11, qtol=1e-12):
     res = res or oracle.sparsify(h)
     rowptr, col, val = oracle.s_csr(res)
@@ -39,6 +84,9 @@ def _compare(h, plan, out, res=None, tol=1e-11, qtol=1e-12):
     nv = np.linalg.norm(val)
     err = np.linalg.norm(v - val) / nv if nv > 0 else np.linalg.norm(v)
     assert err <= tol, err
+    if nv > 0:
+        wl, wb = _level_block_errors(plan, rowptr, col, v, val, tol, per_block=nnz <= 60_000_000)
+        print(f"parity: global {err:.2e}, worst level {wl:.2e}, worst block (own norm) {wb:.2e}")
     off = plan.offsets()
     qr = out["q_row"].cpu().numpy()
     qc = qr if h.symmetric else out["q_col"].cpu().numpy()
@@ -563,6 +611,57 @@ def test_config4_general_mode_properties():
     sp.apply_Ut(avy, lhs)
     sy = _csr_spmv(out, nnz, plan.s_rows, yt[0])
     assert float(torch.linalg.norm(lhs[0] - sy) / torch.linalg.norm(sy)) <= 1e-12
+
+
+def _general_mode_properties(h, qsample=64):
+    """P5 (||S||_F^2 = ||A_H2||_F^2), the defining identity S y = U^T A_H2 V y
+    (GPU applies, the oracle's H^2 matvec, a CSR SpMV of the GPU S) and the
+    orthogonality of a sample of GPU Q blocks -- properties independent of
+    which complement the Householder tie-breaks pick (reading 2)."""
+    plan, sp, out = _run(h)
+    nnz = plan.sizes["s_nnz"]
+    v = out["s_val"][:nnz]
+    f = oracle.frobenius_sq(h)
+    fs = sum(float(torch.dot(c, c)) for c in v.split(1 << 30))
+    assert abs(fs - f) / f <= 1e-12, (fs, f)
+    y = np.random.default_rng(8).standard_normal(h.N)
+    yt = torch.from_numpy(y[None, :]).cuda()
+    vy = torch.empty_like(yt)
+    sp.apply_V(yt, vy)
+    avy = torch.from_numpy(oracle.h2_matvec(h, vy.cpu().numpy()[0])[None, :]).cuda()
+    lhs = torch.empty_like(yt)
+    sp.apply_Ut(avy, lhs)
+    sy = _csr_spmv(out, nnz, plan.s_rows, yt[0])
+    assert float(torch.linalg.norm(lhs[0] - sy) / torch.linalg.norm(sy)) <= 1e-12
+    off = plan.offsets()
+    rng = np.random.default_rng(3)
+    for side, q, n_ in (("row", out["q_row"], off["n_row"]), ("col", out["q_col"], off["n_col"])):
+        key = "q_off_row" if side == "row" else "q_off_col"
+        cl = np.nonzero(n_ > 0)[0]
+        for c in rng.choice(cl, size=min(qsample, len(cl)), replace=False):
+            n = int(n_[c])
+            Q = q[off[key][c]:off[key][c] + n * n].view(n, n)
+            e = float((Q.T @ Q - torch.eye(n, dtype=Q.dtype, device=Q.device)).abs().max())
+            assert e <= 1e-14 * n, (side, c, e)
+
+
+def test_config4_raw_chebyshev_properties():
+    """BASELINE configs[3]'s recipe with its RAW tensor Chebyshev bases (no
+    orthonormalisation; leaf-basis condition ~1e8 on the sphere, Householder
+    alpha at round-off level: parity with the oracle is ill-posed there,
+    reading 2) -- the GPU result is still exact: P5, S y = U^T A V y, Q orthogonal."""
+    _need_gpu()
+    h = h2gen.make_config(4, N=65536, orthonormalize=False)
+    _general_mode_properties(h)
+
+
+def test_config4_full_size_properties():
+    """BASELINE configs[3] at its full size (N = 1,048,576, general mode, r = B/2)."""
+    _need_gpu()
+    if torch.cuda.get_device_properties(0).total_memory < 150 * 2 ** 30:
+        pytest.skip("needs ~100 GB of device memory")
+    h = h2gen.make_config(4)
+    _general_mode_properties(h, qsample=256)
 
 
 def test_device_direct_solve():

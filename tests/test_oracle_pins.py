@@ -389,3 +389,24 @@ def test_structure_only_inputs_reproduce_make_config():
     for leaf, y in rows.items():
         ref = full[leaf * h.B:(leaf + 1) * h.B]
         assert np.linalg.norm(y - ref) <= 1e-13 * np.linalg.norm(full)
+
+
+@pytest.mark.parametrize("cfg,N", [(1, 2048), (2, 16384), (3, 16384), (5, 16384)])
+def test_householder_margins_of_config_recipes(cfg, N):
+    """Survey reading 2: the generator's inputs must keep every Householder
+    decision of convention H away from its tie (0 < |alpha| < 1e-8 sigma or
+    0 < sigma < 1e-8 |alpha|), else GPU-vs-oracle parity is ill-posed.  Configs
+    1, 2, 3, 5 pass (DESIGN.md lists the margins); config 4's tensor bases on
+    a sphere do not (reading 20: its values are gated by properties)."""
+    m = oracle.householder_margins(h2gen.make_config(cfg, N=N))
+    print(cfg, m)
+    assert m["min_margin"] >= 1e-8, m
+
+
+def test_householder_margins_flag_config4():
+    """Config 4 (Chebyshev on a sphere; raw and orthonormalised) has an alpha at
+    round-off level relative to sigma (|alpha| ~ 1e-17 sigma at N = 16384): the
+    sign decision of convention H is noise there -- the check catches it."""
+    for orth in (False, True):
+        m = oracle.householder_margins(h2gen.make_config(4, N=16384, orthonormalize=orth))
+        assert m["alpha_margin"] < 1e-8, m
