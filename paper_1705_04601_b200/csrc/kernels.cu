@@ -2061,7 +2061,9 @@ struct StripCfg {
   // NP == 48: aliasing the group array alone (no hint, 54 registers) fits 3 CTAs
   // per SM instead of 2 (74 KB of shared memory each)
   static constexpr bool ALIAS = SMALL || (NP == 48 && TN == 128);
-  static constexpr int MIN_BLOCKS = SMALL ? STRIP_MINB : 0;
+  // (NP == 48: the minimum-blocks hint 3 pins the register budget at <= 56 so the
+  // 3 CTAs per SM cannot silently drop to 2 after a code change)
+  static constexpr int MIN_BLOCKS = SMALL ? STRIP_MINB : (NP == 48 && TN == 128) ? 3 : 0;
   static constexpr size_t SMEM = (size_t(NP) * LDQ + size_t(NP) * LDZ) * sizeof(double) + TN * 16 + (ALIAS ? 0 : 64);
   static_assert(size_t(NP) * LDZ * sizeof(double) >= (TN + 1) * sizeof(StripGroup), "groups alias sZ");
 };
@@ -3007,7 +3009,22 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     unsigned char *aws = ap_scratch;  // the applies' own scratch; the work lists are the build's
     // V w with w independent of U^T b's output: on s7 beside U^T b (both need
     // only Q; V w uses neither the coefficient buffer nor the arrival counters)
-    const bool v_beside = ap->w && ap->b && ap->w != ap->y && s7 != s1;
+    // ... only when the four vectors' byte ranges are pairwise disjoint (x may
+    // alias b, w may be y: then V w runs after U^T b on s1, in order)
+    auto range = [&](const void *p, int64_t ld, int64_t rows) {
+      const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+      return std::make_pair(a, a + uintptr_t((ld * (ap->nrhs - 1) + rows) * 8));
+    };
+    const int64_t ntree = P->n_leaves_local * P->B;
+    bool disjoint = ap->w && ap->b && ap->x && ap->y;
+    if (disjoint) {
+      const std::pair<uintptr_t, uintptr_t> r[4] = {range(ap->b, ap->ldb, ntree), range(ap->y, ap->ldy, P->n_rows_local),
+                                                    range(ap->w, ap->ldw, P->n_cols_local), range(ap->x, ap->ldx, ntree)};
+      for (int i = 0; i < 4; i++)
+        for (int j = i + 1; j < 4; j++)
+          if (r[i].first < r[j].second && r[j].first < r[i].second) disjoint = false;
+    }
+    const bool v_beside = disjoint && s7 != s1;
     cudaEvent_t ev_chain = aux->ev[14 + 3 * L], ev_v = aux->ev[15 + 3 * L];
     if (v_beside) {
       H2SP_CK(cudaEventRecord(ev_chain, s1));
