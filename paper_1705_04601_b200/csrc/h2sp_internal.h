@@ -184,6 +184,7 @@ struct h2sp_plan_s {
   size_t ws_wy_row, ws_wy_col;
   int32_t nmax;                             // largest local size n_t
   int32_t bench;                            // H2SP_PLAN_BENCH: S reduced to S*w and row norms, never stored
+  int32_t strip_aligned;                    // every frozen size m_t is a multiple of 32 (matrix-wide)
   int64_t n_part;                           // bench mode: partial slots (double2 {S*w, |S|^2} per block row x block)
   size_t ws_part;                           // bench mode: partial buffer in the workspace
   double flops_unique;                      // sharded: work attributed to this shard's own clusters only

@@ -2078,13 +2078,19 @@ struct StripArgs {
   double *s_val;
   const double *bw;   // bench mode: w (S column order)
   double2 *part;      // bench mode: partial slots
+  int aligned;        // bench mode: every frozen group width is a multiple of 32 (plan-wide)
 };
 
 // BENCH (bench mode, include/h2sp.h): rows [k_q, n_q) of W are reduced instead
 // of stored -- per (row, frozen group) of the direct block {sum W w, sum W^2}
-// (8 lanes per item, columns round robin, fixed shuffle tree) and per column of
-// the transposed blocks (TPC lanes per column, rows round robin); W is staged
-// in the Z buffer for it.  Tiles hold whole groups (plan.cpp).
+// and per column of the transposed blocks, the weights w staged per tile.
+// Aligned plans (every group 32k wide, so each warp's 32 columns lie in one
+// group): straight from the accumulators -- a row's 8 values per lane, the
+// lane quad (shuffles), then the group's warp slabs in order; a column's rows
+// over the 8 lane rows (shuffles), then the row warps in order.  Otherwise W is
+// staged in the Z buffer: 8 lanes per (row, group), TPC lanes per column.
+// Fixed orders either way (the choice is plan-wide, so shards agree).  Tiles
+// hold whole groups (plan.cpp).
 template <int NP, int TN, bool BENCH>
 __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::MIN_BLOCKS) strip_kernel(StripArgs A) {
   using C = StripCfg<NP, TN>;
@@ -2094,6 +2100,8 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
   int64_t *tdst = reinterpret_cast<int64_t *>(sZ + NP * C::LDZ);  // per column: transposed S dst (b*ld folded in)
   int32_t *src1 = reinterpret_cast<int32_t *>(tdst + TN);          // per column: column in child-1 panel or -1
   int32_t *src2 = src1 + TN;
+  double *s_wc = reinterpret_cast<double *>(src2 + TN);   // bench: w of every tile column (TN)
+  double *s_wq = s_wc + TN;                               // bench: w of q's frozen rows (NP)
   __shared__ StripGroup sg_own[C::ALIAS ? 1 : TN + 1];
   __shared__ int4 s_gtab[BENCH ? TN + 1 : 1];   // bench: the tile's groups {first column, width, w index}
   __shared__ int s_ngt;
@@ -2132,12 +2140,16 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
       if (gr.pos_c1 >= 0) a1 = gr.pos_c1 + b;
       if (gr.pos_c2 >= 0) a2 = gr.pos_c2 + b;
       if (gr.s_dst_t >= 0) td = gr.s_dst_t + int64_t(b) * gr.s_ld_t;
+      if (BENCH) s_wc[cc] = T.s_dst >= 0 ? __ldg(A.bw + gr.wc0 + b) : 0.0;
+    } else if (BENCH) {
+      s_wc[cc] = 0.0;
     }
     src1[cc] = a1;
     src2[cc] = a2;
     tdst[cc] = td;
   }
   if constexpr (BENCH) {  // the tile's whole groups (tile starts at group g0's first column)
+    for (int a = threadIdx.x; a < NP; a += blockDim.x) s_wq[a] = a < n - kq ? __ldg(A.bw + T.wq0 + a) : 0.0;
     for (int g = threadIdx.x; g < ng; g += blockDim.x)
       if (sg[g].col0 < T.c0 + ncol) s_gtab[g] = make_int4(sg[g].col0 - T.c0, sg[g].m, sg[g].wc0, 0);
     if (threadIdx.x == 0) {
@@ -2192,7 +2204,78 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
   // rows [0, k_q) -> q's panel; rows [k_q, n_q) -> S row segment and the transposed block
   const int lane = threadIdx.x & 31;
   const int r = lane >> 2, q4 = lane & 3;
-  if constexpr (BENCH) {
+  if (BENCH && A.aligned) {
+    __syncthreads();  // every warp is done reading Z: its space holds the slab partials
+    double2 *dslab = reinterpret_cast<double2 *>(sZ);   // [NWN][NP]: (row, warp column slab)
+    double2 *tslab = dslab + C::NWN * NP;               // [NWM][TN]: (column, warp row slab)
+    const int wn = warp % C::NWN, wm = warp / C::NWN;
+    if (m0 < n) {
+#pragma unroll
+      for (int i = 0; i < 2; i++) {  // direct: a row's values of this warp's 32 columns
+        const int row = m0 + i * 8 + r;
+        double y = 0.0, y2 = 0.0;
+#pragma unroll
+        for (int j = 0; j < C::WN / 8; j++)
+#pragma unroll
+          for (int e = 0; e < 2; e++) {
+            const double v = acc[i][j][e];
+            y = fma(v, s_wc[n0 + j * 8 + 2 * q4 + e], y);
+            y2 = fma(v, v, y2);
+          }
+        y += __shfl_xor_sync(0xffffffffu, y, 1);
+        y2 += __shfl_xor_sync(0xffffffffu, y2, 1);
+        y += __shfl_xor_sync(0xffffffffu, y, 2);
+        y2 += __shfl_xor_sync(0xffffffffu, y2, 2);
+        if (q4 == 0) dslab[wn * NP + row] = make_double2(y, y2);
+      }
+#pragma unroll
+      for (int j = 0; j < C::WN / 8; j++)  // transposed: a column's values of this warp's 16 rows
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          double y = 0.0, y2 = 0.0;
+#pragma unroll
+          for (int i = 0; i < 2; i++) {
+            const int row = m0 + i * 8 + r;
+            const double v = row >= kq ? acc[i][j][e] : 0.0;
+            y = fma(v, s_wq[row >= kq ? row - kq : 0], y);
+            y2 = fma(v, v, y2);
+          }
+#pragma unroll
+          for (int o = 4; o < 32; o <<= 1) {
+            y += __shfl_xor_sync(0xffffffffu, y, o);
+            y2 += __shfl_xor_sync(0xffffffffu, y2, o);
+          }
+          if (r == 0) tslab[wm * TN + n0 + j * 8 + 2 * q4 + e] = make_double2(y, y2);
+        }
+    }
+    __syncthreads();
+    const int nfz = n - kq;
+    const int nwm = (n + 15) / 16;   // row warps that computed
+    if (T.s_dst >= 0) {              // (row a, group g): the group's column slabs in order
+      const int ngt = s_ngt;
+      for (int it = threadIdx.x; it < nfz * ngt; it += blockDim.x) {
+        const int a = it / ngt, g = it - a * ngt;
+        const int4 gt = s_gtab[g];
+        double2 v = make_double2(0.0, 0.0);
+        for (int sl = gt.x / C::WN; sl < (gt.x + gt.y) / C::WN; sl++) {
+          v.x += dslab[sl * NP + kq + a].x;
+          v.y += dslab[sl * NP + kq + a].y;
+        }
+        A.part[T.s_dst + g + int64_t(a) * T.s_ld] = v;
+      }
+    }
+    for (int cc = threadIdx.x; cc < ncol; cc += blockDim.x) {   // transposed: row slabs in order
+      const int64_t td = tdst[cc];
+      if (td < 0) continue;
+      double2 v = make_double2(0.0, 0.0);
+      for (int sl = kq / 16; sl < nwm; sl++) {
+        v.x += tslab[sl * TN + cc].x;
+        v.y += tslab[sl * TN + cc].y;
+      }
+      A.part[td] = v;
+    }
+    if (m0 >= n) return;
+  } else if constexpr (BENCH) {
     __syncthreads();  // every warp is done reading Z: stage W there
     if (m0 < n) {
 #pragma unroll
@@ -2218,10 +2301,10 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
           g = it0 - a * ngt;
           const int4 gt = s_gtab[g];
           const double *wr = sZ + (kq + a) * C::LDZ + gt.x;
-          const double *ww = A.bw + gt.z;
+          const double *ww = s_wc + gt.x;
           for (int c = sub; c < gt.y; c += 8) {
             const double v = wr[c];
-            y = fma(v, __ldg(ww + c), y);
+            y = fma(v, ww[c], y);
             r2 = fma(v, v, r2);
           }
         }
@@ -2240,10 +2323,9 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
       const int64_t td = cc < ncol ? tdst[cc] : -1;
       double y = 0.0, r2 = 0.0;
       if (td >= 0) {
-        const double *ww = A.bw + T.wq0;
         for (int a = sub; a < nfz; a += TPC) {
           const double v = sZ[(kq + a) * C::LDZ + cc];
-          y = fma(v, __ldg(ww + a), y);
+          y = fma(v, s_wq[a], y);
           r2 = fma(v, v, r2);
         }
       }
@@ -2587,8 +2669,11 @@ static h2sp_status launch_pairs_wy(const PairArgs &a, const double *wy_row, cons
 template <int NP, int TN, bool BENCH>
 static h2sp_status launch_strips1(const StripArgs &a, int64_t ntiles, cudaStream_t st) {
   using C = StripCfg<NP, TN>;
-  if (h2sp_status e = ensure_smem((const void *)strip_kernel<NP, TN, BENCH>, C::SMEM)) return e;
-  strip_kernel<NP, TN, BENCH><<<unsigned(ntiles), C::THREADS, C::SMEM, st>>>(a);
+  constexpr size_t smem = C::SMEM + (BENCH ? size_t(TN + NP) * sizeof(double) : 0);  // + staged weights
+  static_assert(!BENCH || size_t(NP) * C::LDZ * sizeof(double) >= (C::NWN * NP + (NP / 16) * TN) * 16,
+                "slab partials fit the Z buffer");
+  if (h2sp_status e = ensure_smem((const void *)strip_kernel<NP, TN, BENCH>, smem)) return e;
+  strip_kernel<NP, TN, BENCH><<<unsigned(ntiles), C::THREADS, smem, st>>>(a);
   H2SP_CK(cudaGetLastError());
   return H2SP_OK;
 }
@@ -3146,6 +3231,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
         a.s_val = out->s_val;
         a.bw = out->bench_w;
         a.part = bench ? (double2 *)reg(P->ws_part) : nullptr;
+        a.aligned = P->strip_aligned;
         const int64_t na = sp.n_rtiles_a;
         if (na > 0) {
           H2SP_CK(cudaStreamWaitEvent(s3, ev_pairs_a, 0));
@@ -3179,6 +3265,7 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
         a.s_val = out->s_val;
         a.bw = out->bench_w;
         a.part = bench ? (double2 *)reg(P->ws_part) : nullptr;
+        a.aligned = P->strip_aligned;
         if (h2sp_status e = pre(ss, li[k].cstr[set])) return e;
         h2sp_status s = launch_strips(a, lp.np_cstrip, lp.mp, sp.n_ctiles, ss, bench);
         if (s != H2SP_OK) return s;

@@ -258,6 +258,12 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
       }
       if (a != P->N || b != P->N) throw PlanError(H2SP_ERANK, "sum of frozen sizes != N");
     }
+    // frozen group widths are frozen sizes m: all multiples of 32 -> the strip
+    // kernels' bench epilogue can reduce straight from the accumulators (a
+    // property of the whole matrix, so every shard of it agrees)
+    P->strip_aligned = 1;
+    for (int64_t c = 0; c < ncl; c++)
+      if (mr(c) % 32 || mc(c) % 32) P->strip_aligned = 0;
     // local S rows of this shard: the owned clusters' rows, in S order (== s_off for one rank)
     std::vector<int64_t> loc_off(ncl, -1), loc_off_c(ncl, -1);
     {
