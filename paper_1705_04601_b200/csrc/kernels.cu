@@ -1221,6 +1221,50 @@ __device__ __forceinline__ double gen_entry(const CloseGen &g, const GenCol &c, 
   return same ? v + g.p1 : v;
 }
 
+// exp(x) for x <= 0 with a 64-entry table of 2^(j/64) (in shared memory): x =
+// (k/64) ln 2 + f, |f| <= ln2/128, exp(f) by its degree-6 Taylor polynomial
+// (truncation < 3e-20), result 2^(k>>6) * tab[k & 63] * exp(f): ~10 FP64
+// operations instead of the library exp's ~25, within a few ulp of it -- the
+// FP64 datapath is shared with the DMMA (DMMA = DFMA rate on sm_100a).
+__device__ const double g_exp2_64[64] = {1.0,1.0108892860517005,1.0218971486541166,1.0330248790212284,1.0442737824274138,1.0556451783605572,1.0671404006768237,1.0787607977571199,1.0905077326652577,1.102382583307841,1.1143867425958924,1.1265216186082418,1.1387886347566916,1.1511892299529827,1.1637248587775775,1.1763969916502812,1.189207115002721,1.202156731452703,1.215247359980469,1.22848053610687,1.241857812073484,1.255380757024691,1.2690509571917332,1.2828700160787783,1.2968395546510096,1.3109612115247644,1.3252366431597413,1.339667524053303,1.3542555469368927,1.3690024229745905,1.383909881963832,1.3989796725383112,1.4142135623730951,1.42961333839197,1.4451808069770467,1.460917794180647,1.4768261459394993,1.4929077282912648,1.5091644275934228,1.5255981507445384,1.5422108254079407,1.559004400237837,1.5759808451078865,1.593142151342267,1.6104903319492543,1.6280274218573478,1.645755478153965,1.6636765803267364,1.681792830507429,1.7001063537185235,1.718619298122478,1.7373338352737062,1.7562521603732995,1.7753764925265212,1.7947090750031072,1.8142521755003989,1.8340080864093424,1.8539791250833855,1.8741676341103,1.8945759815869656,1.9152065613971474,1.9360617934922943,1.9571441241754002,1.978456026387951};
+
+__device__ __forceinline__ double exp_neg_tab(double x, const double *tab) {
+  if (x < -700.0) return 0.0;
+  const double kd = rint(x * 92.33248261689366);                         // 64 / ln 2
+  const double f = fma(kd, -2.9815858269852933e-12, fma(kd, -0.01083042469326756, x));  // x - kd ln2/64
+  double pz = fma(f, 1.0 / 720.0, 1.0 / 120.0);
+  pz = fma(pz, f, 1.0 / 24.0);
+  pz = fma(pz, f, 1.0 / 6.0);
+  pz = fma(pz, f, 0.5);
+  pz = fma(pz, f, 1.0);
+  pz = fma(pz, f, 1.0);
+  const int k = int(kd);
+  return __hiloint2double((1023 + (k >> 6)) << 20, 0) * (tab[k & 63] * pz);
+}
+
+// gen_entry with t's points staged in shared memory (xs: nt x dim) and the exp table
+__device__ __forceinline__ double gen_entry_s(const CloseGen &g, const GenCol &c, int i, const double *xs,
+                                              const double *tab) {
+  if (!c.jok || i >= c.nt) return 0.0;
+  const double *x = xs + i * g.dim;
+  const double d0 = __dsub_rn(x[0], c.y0);
+  double r2 = __dmul_rn(d0, d0);
+  if (g.dim > 1) {
+    const double d1 = __dsub_rn(x[1], c.y1);
+    r2 = __dadd_rn(r2, __dmul_rn(d1, d1));
+  }
+  if (g.dim > 2) {
+    const double d2 = __dsub_rn(x[2], c.y2);
+    r2 = __dadd_rn(r2, __dmul_rn(d2, d2));
+  }
+  const bool same = c.tss && i == c.j;
+  const double ir = rsqrt(r2);
+  if (g.kind == H2SP_KERNEL_LAPLACE) return same ? g.p1 : g.q0 * ir;
+  const double r = r2 > 0.0 ? r2 * ir : 0.0;
+  const double v = g.kind == H2SP_KERNEL_EXP ? exp_neg_tab(r * g.q0, tab) : 1.0 / (r + g.p0);
+  return same ? v + g.p1 : v;
+}
+
 template <int NP, int LD>
 __device__ __forceinline__ void gen_close_tile(double *sG, const CloseGen &g, int t, int s, int nt, int ns, int B) {
   const GenCol c = gen_col(g, t, s, nt, ns, B, threadIdx.x % NP);
@@ -1906,12 +1950,17 @@ __global__ void __launch_bounds__(PairWy128Cfg<KP>::THREADS, 1) pair_wy128_kerne
   double *sG = sm, *sV = sG + C::G_D, *sM = sV + C::V_D;
   double *sP = sV;  // KP x LD, after step 1
   __shared__ __align__(16) PairItem s_it[PAIR_CHUNK_MAX];
+  // close_gen: points of the next pair's row cluster t (staged once per t) and the exp table
+  __shared__ __align__(16) double s_xt[GEN ? 128 * 3 : 2];
+  __shared__ double s_tab[GEN ? 64 : 1];
+  if (GEN && threadIdx.x < 64) s_tab[threadIdx.x] = g_exp2_64[threadIdx.x];
   const Chunk ch = A.chunks[blockIdx.x];
   stage_items(A.items, ch, s_it);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = lane >> 2, q = lane & 3;
   const int m0 = warp * 8;
   const int src_lo = r * 4 + (q >> 1), src_hi = src_lo + 2;
+  int xt_staged = -1;   // cluster whose points are in s_xt
   load_close<128, LD, GEN>(A, s_it[0], sG);
   wy128_load<KP>(sV, sM, wy_row, s_it[0].t);
   cp_commit();
@@ -1956,6 +2005,11 @@ __global__ void __launch_bounds__(PairWy128Cfg<KP>::THREADS, 1) pair_wy128_kerne
     // close_gen: G of pair p+1 is evaluated during step 3 (one row per k-step)
     const bool gnext = GEN && more;
     wy128_load<KP>(sV, sM, wy_col, it.s);
+    if (gnext && s_it[p + 1 - ch.begin].t != xt_staged) {  // points of the next row cluster
+      xt_staged = s_it[p + 1 - ch.begin].t;
+      const double *src = A.gen.pts + int64_t(xt_staged) * A.B * A.gen.dim;
+      for (int c = threadIdx.x; c < A.B * A.gen.dim; c += blockDim.x) cp8(s_xt + c, src + c, true);
+    }
     cp_commit();
     if (more && !gnext) {  // G of pair p+1 streams in behind steps 3-4
       const PairItem &nx = s_it[p + 1 - ch.begin];
@@ -1986,7 +2040,7 @@ __global__ void __launch_bounds__(PairWy128Cfg<KP>::THREADS, 1) pair_wy128_kerne
       for (int i = 0; i < KP / 8; i++) dmma(R[(k0 >> 2) & 1][i], a, sV[(k0 + q) * LDV + i * 8 + r]);
       if (gnext) {  // 512 threads x 32 k-steps = the 128 x 128 entries
         const int gi = (threadIdx.x >> 7) + 4 * (k0 >> 2);
-        sG[gi * LD + gc.j] = gen_entry(A.gen, gc, gi);
+        sG[gi * LD + gc.j] = gen_entry_s(A.gen, gc, gi, s_xt, s_tab);
       }
     }
 #pragma unroll
