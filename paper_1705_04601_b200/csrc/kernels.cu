@@ -1456,10 +1456,10 @@ __device__ __forceinline__ void scatter_pair2(const PairArgs &A, const PairDst &
 // column a.  Lane (r, q) of warp w holds H[m0 + r][8j + 2q + e].
 template <int NP, int TN, int WARPS>
 __device__ __forceinline__ void bench_pair(const PairArgs &A, const PairDst &D, int t, int s, const double (&H)[TN][2],
-                                           int m0, double2 *scratch) {
+                                           int m0, double2 *scratch, double2 *rowp_ = nullptr) {
   static_assert(WARPS * 8 == NP && TN * 8 == NP, "warp w owns rows 8w..8w+7 of the NP x NP tile");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, r = lane >> 2, q = lane & 3;
-  double2 *colp = scratch, *rowp = scratch + WARPS * NP;
+  double2 *colp = scratch, *rowp = rowp_ ? rowp_ : scratch + WARPS * NP;
   const int row = m0 + r, a = row - D.kt;
   const bool vrow = row >= D.kt && row < D.nt;
   const bool cols = D.dsym || D.s_dst_m >= 0;   // CTA-uniform
@@ -1961,7 +1961,18 @@ __global__ void __launch_bounds__(PairWy128Cfg<KP>::THREADS, 1) pair_wy128_kerne
   const int m0 = warp * 8;
   const int src_lo = r * 4 + (q >> 1), src_hi = src_lo + 2;
   int xt_staged = -1;   // cluster whose points are in s_xt
-  load_close<128, LD, GEN>(A, s_it[0], sG);
+  if constexpr (GEN) {  // the first G with the same evaluation as the rest (bitwise independent of chunking)
+    xt_staged = s_it[0].t;
+    const double *src = A.gen.pts + int64_t(xt_staged) * A.B * A.gen.dim;
+    for (int c = threadIdx.x; c < A.B * A.gen.dim; c += blockDim.x) cp8(s_xt + c, src + c, true);
+    cp_commit();
+    cp_wait_all();
+    __syncthreads();
+    const GenCol c0 = gen_col(A.gen, s_it[0].t, s_it[0].s, s_it[0].nt, s_it[0].ns, A.B, threadIdx.x & 127);
+    for (int i = threadIdx.x >> 7; i < 128; i += blockDim.x >> 7) sG[i * LD + c0.j] = gen_entry_s(A.gen, c0, i, s_xt, s_tab);
+  } else {
+    load_close<128, LD, GEN>(A, s_it[0], sG);
+  }
   wy128_load<KP>(sV, sM, wy_row, s_it[0].t);
   cp_commit();
   for (int p = ch.begin; p < ch.end; p++) {
@@ -2085,6 +2096,198 @@ __global__ void __launch_bounds__(PairWy128Cfg<KP>::THREADS, 1) pair_wy128_kerne
 #pragma unroll
       for (int j = 0; j < TN; j++) scatter_pair2<BENCH>(A, D, m0, j * 8, m0 + r, j * 8 + 2 * q, H[j][0], H[j][1]);
     }
+  }
+}
+
+
+// --------------------------------------------------------------------------
+// Level-0 compact-WY congruence for 128-point leaves with matrix-free close
+// blocks (close_gen; config 5).  G_ts = C_ts is never stored: its entries are
+// evaluated where the products consume them -- as the B operand of
+// P = V_t^T G (warp w: column 8w+r, rows k) and as the initial accumulator of
+// T1 = G - M_t^T P (warp w: rows 8w..8w+7) -- 64 evaluations per thread per
+// pair instead of 32, and no 135 KB G buffer.  That leaves room for V_t, M_t
+// resident over the chunk (one block row t) and for V_s, M_s of pair p+1
+// loading during the epilogue of pair p and steps 1-2 of pair p+1: no load is
+// exposed in the pair loop (the FP64 datapath -- DMMA and the kernel
+// evaluations -- is the bottleneck resource).
+// --------------------------------------------------------------------------
+template <int KP>
+struct PairWy128gCfg {
+  static constexpr int NP = 128;
+  static constexpr int LD = NP + 4;    // M, P rows
+  static constexpr int LDV = KP + 4;   // V rows
+  static constexpr int WARPS = 16;
+  static constexpr int THREADS = WARPS * 32;
+  static constexpr int V_D = NP * LDV, M_D = KP * LD, P_D = KP * LD, X_D = NP * 3;
+  static constexpr size_t SMEM = size_t(2 * V_D + 3 * M_D + 2 * X_D) * sizeof(double);
+  static_assert(P_D * 2 >= WARPS * NP * 2, "the bench column partials fit the P buffer");
+};
+
+// K(x, y) of h2sp_close_gen for row point x and column point y (the same
+// arithmetic as gen_entry_s); `same`: the same point (diagonal of t == s)
+__device__ __forceinline__ double gen_eval(const CloseGen &g, const double *x, const double *y, bool same,
+                                           const double *tab) {
+  const double d0 = __dsub_rn(x[0], y[0]);
+  double r2 = __dmul_rn(d0, d0);
+  if (g.dim > 1) {
+    const double d1 = __dsub_rn(x[1], y[1]);
+    r2 = __dadd_rn(r2, __dmul_rn(d1, d1));
+  }
+  if (g.dim > 2) {
+    const double d2 = __dsub_rn(x[2], y[2]);
+    r2 = __dadd_rn(r2, __dmul_rn(d2, d2));
+  }
+  const double ir = rsqrt(r2);
+  if (g.kind == H2SP_KERNEL_LAPLACE) return same ? g.p1 : g.q0 * ir;
+  const double r = r2 > 0.0 ? r2 * ir : 0.0;
+  const double v = g.kind == H2SP_KERNEL_EXP ? exp_neg_tab(r * g.q0, tab) : 1.0 / (r + g.p0);
+  return same ? v + g.p1 : v;
+}
+
+template <int KP, bool BENCH>
+__global__ void __launch_bounds__(PairWy128gCfg<KP>::THREADS, 1) pair_wy128g_kernel(PairArgs A, const double *wy_row,
+                                                                                     const double *wy_col) {
+  using C = PairWy128gCfg<KP>;
+  constexpr int LD = C::LD, LDV = C::LDV, TN = 16;
+  extern __shared__ __align__(16) double sm[];
+  double *sVt = sm, *sMt = sVt + C::V_D, *sP = sMt + C::M_D, *sVs = sP + C::P_D, *sMs = sVs + C::V_D;
+  double *sXt = sMs + C::M_D, *sYs = sXt + C::X_D;   // points of t (rows), of s (columns): 128 x dim
+  __shared__ __align__(16) PairItem s_it[PAIR_CHUNK_MAX];
+  __shared__ double s_tab[64];
+  __shared__ double2 s_rowp[BENCH ? 128 : 1];
+  if (threadIdx.x < 64) s_tab[threadIdx.x] = g_exp2_64[threadIdx.x];
+  const Chunk ch = A.chunks[blockIdx.x];
+  stage_items(A.items, ch, s_it);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = lane >> 2, q = lane & 3;
+  const int m0 = warp * 8;
+  const int src_lo = r * 4 + (q >> 1), src_hi = src_lo + 2;
+  const int dim = A.gen.dim;
+  auto load_pts = [&](double *dst, int c) {   // the B points of leaf c
+    const double *src = A.gen.pts + int64_t(c) * A.B * dim;
+    for (int e = threadIdx.x; e < A.B * dim; e += blockDim.x) cp8(dst + e, src + e, true);
+  };
+  int t = s_it[0].t;
+  wy128_load<KP>(sVt, sMt, wy_row, t);
+  load_pts(sXt, t);
+  wy128_load<KP>(sVs, sMs, wy_col, s_it[0].s);
+  load_pts(sYs, s_it[0].s);
+  cp_commit();
+  for (int p = ch.begin; p < ch.end; p++) {
+    const PairItem &it = s_it[p - ch.begin];
+    cp_wait_all();
+    __syncthreads();
+    if (it.t != t) {  // new block row (chunks are one row each; kept for generality)
+      t = it.t;
+      wy128_load<KP>(sVt, sMt, wy_row, t);
+      load_pts(sXt, t);
+      cp_commit();
+      cp_wait_all();
+      __syncthreads();
+    }
+    const int nt = it.nt, ns = it.ns;
+    const bool tss = it.t == it.s;
+    // ---- step 1: P = V_t^T G (KP x 128); warp w: columns 8w..8w+7, B operand
+    //      G[k0 + q][8w + r] evaluated in place
+    {
+      const int c1 = m0 + r;
+      double yc[3] = {0.0, 0.0, 0.0};
+      for (int a = 0; a < dim; a++) yc[a] = sYs[c1 * dim + a];
+      double pacc[2][KP / 8][2];
+#pragma unroll
+      for (int i = 0; i < KP / 8; i++) pacc[0][i][0] = pacc[0][i][1] = pacc[1][i][0] = pacc[1][i][1] = 0.0;
+#pragma unroll 4
+      for (int k0 = 0; k0 < 128; k0 += 4) {
+        const int i = k0 + q;
+        const double b = (i < nt && c1 < ns) ? gen_eval(A.gen, sXt + i * dim, yc, tss && i == c1, s_tab) : 0.0;
+#pragma unroll
+        for (int ii = 0; ii < KP / 8; ii++) dmma(pacc[(k0 >> 2) & 1][ii], sVt[(k0 + q) * LDV + ii * 8 + r], b);
+      }
+#pragma unroll
+      for (int ii = 0; ii < KP / 8; ii++) {
+        sP[(ii * 8 + r) * LD + m0 + 2 * q] = pacc[0][ii][0] + pacc[1][ii][0];
+        sP[(ii * 8 + r) * LD + m0 + 2 * q + 1] = pacc[0][ii][1] + pacc[1][ii][1];
+      }
+    }
+    __syncthreads();
+    // ---- step 2: T1 = G - M_t^T P (rows m0..m0+7 in registers), G evaluated as the accumulator
+    double H[TN][2];
+    {
+      const int row = m0 + r;
+      double xr[3] = {0.0, 0.0, 0.0};
+      for (int a = 0; a < dim; a++) xr[a] = sXt[row * dim + a];
+#pragma unroll
+      for (int j = 0; j < TN; j++)
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          const int c = j * 8 + 2 * q + e;
+          H[j][e] = (row < nt && c < ns) ? gen_eval(A.gen, xr, sYs + c * dim, tss && row == c, s_tab) : 0.0;
+        }
+    }
+#pragma unroll 2
+    for (int k0 = 0; k0 < KP; k0 += 4) {
+      const double a = -sMt[(k0 + q) * LD + m0 + r];
+#pragma unroll
+      for (int j = 0; j < TN; j++) dmma(H[j], a, sP[(k0 + q) * LD + j * 8 + r]);
+    }
+    // ---- step 3: R = T1 V_s (8 x KP per warp), A fragments from the T1 accumulators
+    double R[2][KP / 8][2];
+#pragma unroll
+    for (int i = 0; i < KP / 8; i++) R[0][i][0] = R[0][i][1] = R[1][i][0] = R[1][i][1] = 0.0;
+#pragma unroll
+    for (int k0 = 0; k0 < 128; k0 += 4) {
+      const int jt = k0 >> 3;
+      const int srcl = (k0 & 4) ? src_hi : src_lo;
+      const double e0 = __shfl_sync(0xffffffffu, H[jt][0], srcl);
+      const double e1 = __shfl_sync(0xffffffffu, H[jt][1], srcl);
+      const double a = (q & 1) ? e1 : e0;
+#pragma unroll
+      for (int i = 0; i < KP / 8; i++) dmma(R[(k0 >> 2) & 1][i], a, sVs[(k0 + q) * LDV + i * 8 + r]);
+    }
+#pragma unroll
+    for (int i = 0; i < KP / 8; i++) {
+      R[0][i][0] += R[1][i][0];
+      R[0][i][1] += R[1][i][1];
+    }
+    // ---- step 4: H = T1 - R M_s
+#pragma unroll
+    for (int k0 = 0; k0 < KP; k0 += 4) {
+      const int jt = k0 >> 3;
+      const int srcl = (k0 & 4) ? src_hi : src_lo;
+      const double e0 = __shfl_sync(0xffffffffu, R[0][jt][0], srcl);
+      const double e1 = __shfl_sync(0xffffffffu, R[0][jt][1], srcl);
+      const double a = -((q & 1) ? e1 : e0);
+#pragma unroll
+      for (int j = 0; j < TN; j++) dmma(H[j], a, sMs[(k0 + q) * LD + j * 8 + r]);
+    }
+    __syncthreads();  // every warp is done with V_s, M_s, the points of s and P
+    if (p + 1 < ch.end) {  // V_s, M_s, points of the next pair: in flight until its step 3
+      const PairItem &nx = s_it[p + 1 - ch.begin];
+      wy128_load<KP>(sVs, sMs, wy_col, nx.s);
+      load_pts(sYs, nx.s);
+      cp_commit();
+    }
+    PairDst D;
+    D.s_dst = it.s_dst;
+    D.s_dst_m = it.s_dst_m;
+    D.bb_dst = it.bb_dst;
+    D.yr_dst = it.yr_dst;
+    D.yc_dst = it.yc_dst;
+    D.s_ld = it.s_ld;
+    D.s_ld_m = it.s_ld_m;
+    D.yr_ld = it.yr_ld;
+    D.yc_ld = it.yc_ld;
+    D.nt = nt;
+    D.ns = ns;
+    D.kt = it.kt;
+    D.ks = it.ks;
+    D.dsym = A.sym && tss;
+    // bench mode: the S part reduced with the (free) P buffer as scratch
+    if constexpr (BENCH)
+      bench_pair<128, TN, C::WARPS>(A, D, it.t, it.s, H, m0, reinterpret_cast<double2 *>(sP), s_rowp);
+#pragma unroll
+    for (int j = 0; j < TN; j++) scatter_pair2<BENCH>(A, D, m0, j * 8, m0 + r, j * 8 + 2 * q, H[j][0], H[j][1]);
   }
 }
 
@@ -2672,10 +2875,24 @@ static h2sp_status launch_pairs_wy128_t(const PairArgs &a, const double *wy_row,
   H2SP_CK(cudaGetLastError());
   return H2SP_OK;
 }
+template <int KP, bool BENCH>
+static h2sp_status launch_pairs_wy128g_t(const PairArgs &a, const double *wy_row, const double *wy_col,
+                                         int64_t nchunks, cudaStream_t st) {
+  using C = PairWy128gCfg<KP>;
+  if (h2sp_status e = ensure_smem((const void *)pair_wy128g_kernel<KP, BENCH>, C::SMEM)) return e;
+  pair_wy128g_kernel<KP, BENCH><<<unsigned(nchunks), C::THREADS, C::SMEM, st>>>(a, wy_row, wy_col);
+  H2SP_CK(cudaGetLastError());
+  return H2SP_OK;
+}
 template <int KP>
 static h2sp_status launch_pairs_wy128(const PairArgs &a, const double *wy_row, const double *wy_col, int64_t nchunks,
                                       cudaStream_t st, bool bench) {
   const bool gen = a.gen.pts != nullptr;
+  // matrix-free close blocks: G evaluated inside the products (no G buffer)
+  static const bool old_gen = getenv("H2SP_WY128_GBUF") && atoi(getenv("H2SP_WY128_GBUF")) != 0;
+  if (gen && !old_gen)
+    return bench ? launch_pairs_wy128g_t<KP, true>(a, wy_row, wy_col, nchunks, st)
+                 : launch_pairs_wy128g_t<KP, false>(a, wy_row, wy_col, nchunks, st);
   if (bench)
     return gen ? launch_pairs_wy128_t<KP, true, true>(a, wy_row, wy_col, nchunks, st)
                : launch_pairs_wy128_t<KP, false, true>(a, wy_row, wy_col, nchunks, st);
