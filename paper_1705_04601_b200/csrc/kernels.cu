@@ -2888,9 +2888,13 @@ template <int KP>
 static h2sp_status launch_pairs_wy128(const PairArgs &a, const double *wy_row, const double *wy_col, int64_t nchunks,
                                       cudaStream_t st, bool bench) {
   const bool gen = a.gen.pts != nullptr;
-  // matrix-free close blocks: G evaluated inside the products (no G buffer)
-  static const bool old_gen = getenv("H2SP_WY128_GBUF") && atoi(getenv("H2SP_WY128_GBUF")) != 0;
-  if (gen && !old_gen)
+  // matrix-free close blocks, H2SP_WY128_GEVAL=1: G evaluated inside the products
+  // (pair_wy128g_kernel, no G buffer, no exposed load) -- measured 8 % slower
+  // than evaluating every entry once into the G buffer (config 5: 2996 vs
+  // 2795 ms per step; the FP64 datapath, shared by DMMA and the evaluations,
+  // is the bottleneck, so the second evaluation costs more than the loads it hides)
+  static const bool geval = getenv("H2SP_WY128_GEVAL") && atoi(getenv("H2SP_WY128_GEVAL")) != 0;
+  if (gen && geval)
     return bench ? launch_pairs_wy128g_t<KP, true>(a, wy_row, wy_col, nchunks, st)
                  : launch_pairs_wy128g_t<KP, false>(a, wy_row, wy_col, nchunks, st);
   if (bench)
