@@ -2634,6 +2634,269 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
   }
 }
 
+// --------------------------------------------------------------------------
+// Strips, bench mode on aligned plans (config 5): a persistent, software-
+// pipelined version of strip_kernel.  One CTA per SM walks a contiguous range
+// of tiles (consecutive tiles share a panel, so Q_q stays loaded); while the
+// DMMA of tile i runs, Z of tile i+1 is in flight (double-buffered), the groups
+// of tile i+2 and the descriptor of tile i+3 too (4 metadata stages).  Per
+// tile the same arithmetic as strip_kernel's aligned path (same GEMM order,
+// same slab reductions), so results are bitwise equal to it.  The one-tile-
+// per-CTA kernel spends most of its time in dependent round trips (descriptor
+// -> Q / groups -> Z) that only 2 co-resident CTAs can overlap.
+// --------------------------------------------------------------------------
+template <int NP, int TN>
+struct PipeMeta {
+  StripTileX tile;
+  StripGroup grp[TN + 1];
+};
+template <int NP, int TN>
+struct PipeMaps {
+  int64_t tdst[TN];
+  int32_t src1[TN], src2[TN];
+  double wc[TN];
+  double wq[NP];
+  int4 gtab[TN + 1];
+  int ngt, pad_[3];
+};
+template <int NP, int TN>
+struct StripPipeCfg {
+  using C = StripCfg<NP, TN>;
+  static constexpr size_t Q_B = size_t(NP) * C::LDQ * sizeof(double);
+  static constexpr size_t Z_B = size_t(NP) * C::LDZ * sizeof(double);
+  static constexpr size_t SMEM = Q_B + 2 * Z_B + 4 * sizeof(PipeMeta<NP, TN>) + 2 * sizeof(PipeMaps<NP, TN>);
+};
+
+template <int NP, int TN>
+__global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, 1) strip_pipe_kernel(StripArgs A, int64_t ntiles) {
+  using C = StripCfg<NP, TN>;
+  using PC = StripPipeCfg<NP, TN>;
+  extern __shared__ __align__(16) double sm[];
+  unsigned char *base = reinterpret_cast<unsigned char *>(sm);
+  double *sQ = sm;
+  double *sZ0 = reinterpret_cast<double *>(base + PC::Q_B);
+  PipeMeta<NP, TN> *meta = reinterpret_cast<PipeMeta<NP, TN> *>(base + PC::Q_B + 2 * PC::Z_B);
+  PipeMaps<NP, TN> *maps = reinterpret_cast<PipeMaps<NP, TN> *>(meta + 4);
+  const int64_t tb = ntiles * blockIdx.x / gridDim.x, te = ntiles * (blockIdx.x + 1) / gridDim.x;
+  if (tb >= te) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = lane >> 2, q4 = lane & 3;
+  const int m0 = (warp / C::NWN) * 16, n0 = (warp % C::NWN) * C::WN;
+  auto zbuf = [&](int64_t i) { return sZ0 + ((i - tb) & 1) * (size_t(NP) * C::LDZ); };
+  auto load_desc = [&](int64_t i) {
+    if (i < te && threadIdx.x < int(sizeof(StripTileX) / 16))
+      cp16(reinterpret_cast<char *>(&meta[(i - tb) & 3].tile) + 16 * threadIdx.x,
+           reinterpret_cast<const char *>(A.tiles + i) + 16 * threadIdx.x);
+  };
+  auto load_groups = [&](int64_t i) {   // needs the descriptor of tile i in shared memory
+    if (i >= te) return;
+    PipeMeta<NP, TN> &M = meta[(i - tb) & 3];
+    const int ng = min(M.tile.gend - M.tile.g0, TN + 1);
+    for (int g = threadIdx.x; g < ng * 2; g += blockDim.x)
+      cp16(reinterpret_cast<char *>(&M.grp[g >> 1]) + 16 * (g & 1),
+           reinterpret_cast<const char *>(&A.groups[M.tile.g0 + (g >> 1)]) + 16 * (g & 1));
+  };
+  // per-column maps, weights and the group table of tile i (its descriptor and groups landed)
+  auto make_maps = [&](int64_t i) {
+    const PipeMeta<NP, TN> &M = meta[(i - tb) & 3];
+    PipeMaps<NP, TN> &X = maps[(i - tb) & 1];
+    const StripTileX &T = M.tile;
+    const int ng = min(T.gend - T.g0, TN + 1);
+    for (int cc = threadIdx.x; cc < TN; cc += blockDim.x) {
+      int32_t a1 = -1, a2 = -1;
+      int64_t td = -1;
+      double wc = 0.0;
+      if (cc < T.ncol) {
+        const int c = T.c0 + cc;
+        int g = 0;
+        while (g + 1 < ng && M.grp[g + 1].col0 <= c) g++;
+        const StripGroup gr = M.grp[g];
+        const int b = c - gr.col0;
+        if (gr.pos_c1 >= 0) a1 = gr.pos_c1 + b;
+        if (gr.pos_c2 >= 0) a2 = gr.pos_c2 + b;
+        if (gr.s_dst_t >= 0) td = gr.s_dst_t + int64_t(b) * gr.s_ld_t;
+        if (T.s_dst >= 0) wc = __ldg(A.bw + gr.wc0 + b);
+      }
+      X.src1[cc] = a1;
+      X.src2[cc] = a2;
+      X.tdst[cc] = td;
+      X.wc[cc] = wc;
+    }
+    for (int a = threadIdx.x; a < NP; a += blockDim.x) X.wq[a] = a < T.n - T.kq ? __ldg(A.bw + T.wq0 + a) : 0.0;
+    for (int g = threadIdx.x; g < ng; g += blockDim.x)
+      if (M.grp[g].col0 < T.c0 + T.ncol) X.gtab[g] = make_int4(M.grp[g].col0 - T.c0, M.grp[g].m, M.grp[g].wc0, 0);
+    if (threadIdx.x == 0) {
+      int c = 0;
+      while (c < ng && M.grp[c].col0 < T.c0 + T.ncol) c++;
+      X.ngt = c;
+    }
+  };
+  // asynchronous gather of Z of tile i (maps of tile i complete, CTA barrier passed)
+  auto gather = [&](int64_t i) {
+    const StripTileX &T = meta[(i - tb) & 3].tile;
+    const PipeMaps<NP, TN> &X = maps[(i - tb) & 1];
+    double *sZ = zbuf(i);
+    const int n4 = rup(int(T.n), 4), k1 = T.k1, k2 = T.k2;
+    const int cc = 2 * (threadIdx.x % (TN / 2)), R = blockDim.x / (TN / 2);
+    const double *b1 = X.src1[cc] >= 0 ? A.y_in + T.src_c1 + X.src1[cc] : nullptr;
+    const double *b2 = X.src2[cc] >= 0 ? A.y_in + T.src_c2 + X.src2[cc] : nullptr;
+    const double *b1n = X.src1[cc + 1] >= 0 ? A.y_in + T.src_c1 + X.src1[cc + 1] : nullptr;
+    const double *b2n = X.src2[cc + 1] >= 0 ? A.y_in + T.src_c2 + X.src2[cc + 1] : nullptr;
+    const bool v1 = b1 && b1n == b1 + 1 && ((reinterpret_cast<uintptr_t>(b1) | (uintptr_t(T.ld_c1) * 8)) & 15) == 0;
+    const bool v2 = b2 && b2n == b2 + 1 && ((reinterpret_cast<uintptr_t>(b2) | (uintptr_t(T.ld_c2) * 8)) & 15) == 0;
+    const void *any = A.tiles;
+    for (int i_ = threadIdx.x / (TN / 2); i_ < n4; i_ += R) {
+      const bool first = i_ < k1, second = !first && i_ < k1 + k2;
+      const int64_t off = int64_t(first ? i_ : i_ - k1) * (first ? T.ld_c1 : T.ld_c2);
+      const double *p0 = first ? b1 : (second ? b2 : nullptr);
+      const double *p1 = first ? b1n : (second ? b2n : nullptr);
+      double *d = &sZ[i_ * C::LDZ + cc];
+      if ((first && v1) || (second && v2)) {
+        cp16(d, p0 + off);
+      } else if (!p0 && !p1) {
+        cp16_zero(d, any);
+      } else {
+        cp8(d, p0 ? (const void *)(p0 + off) : any, p0 != nullptr);
+        cp8(d + 1, p1 ? (const void *)(p1 + off) : any, p1 != nullptr);
+      }
+    }
+  };
+  // ---- prologue: tile tb ready to compute, tb+1 groups landed, tb+2 descriptor landed
+  load_desc(tb);
+  load_desc(tb + 1);
+  load_desc(tb + 2);
+  cp_commit();
+  cp_wait_all();
+  __syncthreads();
+  load_groups(tb);
+  load_groups(tb + 1);
+  async_tile<NP, NP, C::LDQ>(sQ, A.q + meta[0].tile.q_off, meta[0].tile.n, meta[0].tile.n, meta[0].tile.n, A.tiles);
+  int64_t q_loaded = meta[0].tile.q_off;
+  cp_commit();
+  cp_wait_all();
+  __syncthreads();
+  make_maps(tb);
+  __syncthreads();
+  gather(tb);
+  load_desc(tb + 3);
+  cp_commit();
+  for (int64_t i = tb; i < te; i++) {
+    cp_wait_all();
+    __syncthreads();  // Z_i, groups(i+1), descriptors(i+2, i+3) landed; tile i-1 fully done
+    const StripTileX &T = meta[(i - tb) & 3].tile;
+    const PipeMaps<NP, TN> &X = maps[(i - tb) & 1];
+    if (T.q_off != q_loaded) {  // panel change: Q_q (exposed, rare)
+      async_tile<NP, NP, C::LDQ>(sQ, A.q + T.q_off, T.n, T.n, T.n, A.tiles);
+      cp_commit();
+      cp_wait_all();
+      __syncthreads();
+      q_loaded = T.q_off;
+    }
+    // ---- prepare tile i+1 (maps, then Z in flight), groups of i+2
+    if (i + 1 < te) {
+      make_maps(i + 1);
+      __syncthreads();
+      gather(i + 1);
+    }
+    load_groups(i + 2);
+    cp_commit();
+    // ---- W = Q_q^T Z_i
+    const int n = T.n, kq = T.kq, ncol = T.ncol;
+    double *sZ = zbuf(i);
+    double acc[2][C::WN / 8][2];
+    zero_acc(acc);
+    if (m0 < n) warp_gemm<C::LDQ, C::LDZ, 2, C::WN / 8, true>(sQ, sZ, m0, n0, rup(n, 4), acc);
+    // ---- epilogue: carry rows [0, kq) -> q's panel; rows [kq, n) reduced (aligned slabs)
+#pragma unroll
+    for (int i2 = 0; i2 < 2; i2++) {
+      const int row = m0 + i2 * 8 + r;
+      if (row >= kq || row >= n || T.y_dst < 0) continue;
+#pragma unroll
+      for (int j = 0; j < C::WN / 8; j++) {
+        const int col = n0 + j * 8 + 2 * q4;
+        if (col >= ncol) continue;
+        double *d = A.y_out + T.y_dst + int64_t(row) * T.y_ld + T.c0 + col;
+        if (col + 1 < ncol)
+          store2(d, acc[i2][j][0], acc[i2][j][1]);
+        else
+          d[0] = acc[i2][j][0];
+      }
+    }
+    __syncthreads();  // every warp is done reading Z_i: its space holds the slab partials
+    double2 *dslab = reinterpret_cast<double2 *>(sZ);
+    double2 *tslab = dslab + C::NWN * NP;
+    const int wn = warp % C::NWN, wm = warp / C::NWN;
+    if (m0 < n) {
+#pragma unroll
+      for (int i2 = 0; i2 < 2; i2++) {
+        const int row = m0 + i2 * 8 + r;
+        double y = 0.0, y2 = 0.0;
+#pragma unroll
+        for (int j = 0; j < C::WN / 8; j++)
+#pragma unroll
+          for (int e = 0; e < 2; e++) {
+            const double v = acc[i2][j][e];
+            y = fma(v, X.wc[n0 + j * 8 + 2 * q4 + e], y);
+            y2 = fma(v, v, y2);
+          }
+        y += __shfl_xor_sync(0xffffffffu, y, 1);
+        y2 += __shfl_xor_sync(0xffffffffu, y2, 1);
+        y += __shfl_xor_sync(0xffffffffu, y, 2);
+        y2 += __shfl_xor_sync(0xffffffffu, y2, 2);
+        if (q4 == 0) dslab[wn * NP + row] = make_double2(y, y2);
+      }
+#pragma unroll
+      for (int j = 0; j < C::WN / 8; j++)
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          double y = 0.0, y2 = 0.0;
+#pragma unroll
+          for (int i2 = 0; i2 < 2; i2++) {
+            const int row = m0 + i2 * 8 + r;
+            const double v = row >= kq ? acc[i2][j][e] : 0.0;
+            y = fma(v, X.wq[row >= kq ? row - kq : 0], y);
+            y2 = fma(v, v, y2);
+          }
+#pragma unroll
+          for (int o = 4; o < 32; o <<= 1) {
+            y += __shfl_xor_sync(0xffffffffu, y, o);
+            y2 += __shfl_xor_sync(0xffffffffu, y2, o);
+          }
+          if (r == 0) tslab[wm * TN + n0 + j * 8 + 2 * q4 + e] = make_double2(y, y2);
+        }
+    }
+    __syncthreads();
+    const int nfz = n - kq;
+    const int nwm = (n + 15) / 16;
+    if (T.s_dst >= 0) {
+      const int ngt = X.ngt;
+      for (int it = threadIdx.x; it < nfz * ngt; it += blockDim.x) {
+        const int a = it / ngt, g = it - a * ngt;
+        const int4 gt = X.gtab[g];
+        double2 v = make_double2(0.0, 0.0);
+        for (int sl = gt.x / C::WN; sl < (gt.x + gt.y) / C::WN; sl++) {
+          v.x += dslab[sl * NP + kq + a].x;
+          v.y += dslab[sl * NP + kq + a].y;
+        }
+        A.part[T.s_dst + g + int64_t(a) * T.s_ld] = v;
+      }
+    }
+    for (int cc = threadIdx.x; cc < ncol; cc += blockDim.x) {
+      const int64_t td = X.tdst[cc];
+      if (td < 0) continue;
+      double2 v = make_double2(0.0, 0.0);
+      for (int sl = kq / 16; sl < nwm; sl++) {
+        v.x += tslab[sl * TN + cc].x;
+        v.y += tslab[sl * TN + cc].y;
+      }
+      A.part[td] = v;
+    }
+    __syncthreads();  // tile i's metadata stage is free again
+    load_desc(i + 4);
+    cp_commit();
+  }
+}
+
 // Bench mode: y[i] = sum of row i's partial slots, in block order (one warp per
 // S row, lanes round robin over the blocks, fixed shuffle tree), and the row
 // norms likewise.  One CTA per S block row.
@@ -2944,6 +3207,21 @@ static h2sp_status launch_pairs_wy(const PairArgs &a, const double *wy_row, cons
 template <int NP, int TN, bool BENCH>
 static h2sp_status launch_strips1(const StripArgs &a, int64_t ntiles, cudaStream_t st) {
   using C = StripCfg<NP, TN>;
+  // bench mode, aligned plans: the pipelined persistent kernel (H2SP_STRIP_PIPE=0: one tile per CTA)
+  static const bool pipe = !getenv("H2SP_STRIP_PIPE") || atoi(getenv("H2SP_STRIP_PIPE")) != 0;
+  if constexpr (BENCH && NP >= 32) {
+    if (pipe && a.aligned) {
+      using PC = StripPipeCfg<NP, TN>;
+      if (h2sp_status e = ensure_smem((const void *)strip_pipe_kernel<NP, TN>, PC::SMEM)) return e;
+      int dev = 0, nsm = 148;
+      H2SP_CK(cudaGetDevice(&dev));
+      H2SP_CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+      const int64_t grid = std::min<int64_t>(ntiles, nsm);
+      if (grid > 0) strip_pipe_kernel<NP, TN><<<unsigned(grid), C::THREADS, PC::SMEM, st>>>(a, ntiles);
+      H2SP_CK(cudaGetLastError());
+      return H2SP_OK;
+    }
+  }
   constexpr size_t smem = C::SMEM + (BENCH ? size_t(TN + NP) * sizeof(double) : 0);  // + staged weights
   static_assert(!BENCH || size_t(NP) * C::LDZ * sizeof(double) >= (C::NWN * NP + (NP / 16) * TN) * 16,
                 "slab partials fit the Z buffer");
