@@ -439,6 +439,49 @@ def run_protocol(args, rank, world, local_rank):
                "d2h_bytes_per_step": d2h,
                "api": "pinned host points / boxes / w / b in; h2sp_cheb_construct (bases, transfers, nodes on the "
                       "device), h2sp_build_meta per virtual shard (+ U^T b, V w), y = S w, row norms, Q and x out"}
+    # ---- SURVEY 8(a) a8 alone: y = U^T b and x = V y of one shard (its Q from the
+    #      last step), nrhs = 1, 8, 32, against the HBM roofline (every Q_t of the
+    #      shard's subtree read once + the vectors)
+    apply_info = None
+    if rank == 0 and not args.no_apply:
+        import paper_1705_04601_b200 as h2sp_
+        p0 = plans[0]
+        loc0, _ = p0.local_rows()
+        qbytes = 8.0 * float(np.sum(offs["n_row"][loc0 >= 0].astype(float) ** 2))
+        apply_info = {"shard": 0, "q_bytes": qbytes, "hbm_peak_gbs": _peaks()["hbm_gbs"], "by_nrhs": {}}
+        for nr in (1, 8, 32):
+            need = int(h2sp_.lib.h2sp_apply_ws_bytes(p0.handle, nr))
+            aws = torch.empty(need + 256, dtype=torch.uint8, device=dev)
+            aptr = (aws.data_ptr() + 255) // 256 * 256
+            h2sp_._check(h2sp_.lib.h2sp_plan_upload(p0.handle, aptr, need, h2sp_._stream_handle(None)), "upload")
+            a0, a1 = run.leaf_range(0)
+            bb = torch.randn(nr, a1 - a0, **f64)
+            yy = torch.empty(nr, p0.s_rows, **f64)
+            xx = torch.empty_like(bb)
+            q = run.outputs["q_row"]
+
+            def ut():
+                h2sp_._check(h2sp_.lib.h2sp_apply_Ut(p0.handle, q.data_ptr(), bb.data_ptr(), bb.shape[-1], yy.data_ptr(),
+                                                     yy.shape[-1], nr, aptr, need, h2sp_._stream_handle(None)), "Ut")
+
+            def vv():
+                h2sp_._check(h2sp_.lib.h2sp_apply_V(p0.handle, q.data_ptr(), yy.data_ptr(), yy.shape[-1], xx.data_ptr(),
+                                                    xx.shape[-1], nr, aptr, need, h2sp_._stream_handle(None)), "V")
+            res = {}
+            for name, fn in (("ut", ut), ("v", vv)):
+                fn()
+                e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e_a.record(stream)
+                for _ in range(5):
+                    fn()
+                e_b.record(stream)
+                torch.cuda.synchronize()
+                ms_ = e_a.elapsed_time(e_b) / 5
+                byt = qbytes + 8.0 * nr * ((a1 - a0) + p0.s_rows)
+                res[name] = {"us": ms_ * 1e3, "gbs": byt / (ms_ * 1e-3) / 1e9,
+                             "frac": byt / (ms_ * 1e-3) / 1e9 / apply_info["hbm_peak_gbs"]}
+            apply_info["by_nrhs"][nr] = res
+            del aws
     cpu = None
     if rank == 0 and world == 1 and not args.no_oracle:
         cpu = _cpu_sample_baseline(args.config, args.ref_n, job_flops)
@@ -475,6 +518,7 @@ def run_protocol(args, rank, world, local_rank):
                        "nccl": nccl_info,
                        "env": _env_knobs()},
             "roofline": roof,
+            "apply_roofline": apply_info,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps * sum(n + 2 for n in n_launch),
@@ -514,6 +558,7 @@ def main():
     ap.add_argument("--nrhs", type=int, default=1)
     ap.add_argument("--no-oracle", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-apply", action="store_true", help="skip the standalone apply timing (config 5)")
     ap.add_argument("--graph", action="store_true",
                     help="time CUDA-graph replays of the captured step (launch-bound small configs); the default "
                          "eager steps carry the per-launch events the roofline needs inside the timed region")

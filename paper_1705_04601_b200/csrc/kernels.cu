@@ -121,11 +121,11 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 //   A(m, kk) = AT ? sA[kk*LDA + m] : sA[m*LDA + kk];  B(kk, n) = sB[kk*LDB + n].
 template <int LDA, int LDB, int TM, int TN, bool AT>
 __device__ __forceinline__ void warp_gemm(const double *__restrict__ sA, const double *__restrict__ sB, int m0,
-                                          int n0, int kmax, double (&acc)[TM][TN][2]) {
+                                          int n0, int kmax, double (&acc)[TM][TN][2], int kmin = 0) {
   const int lane = threadIdx.x & 31;
   const int r = lane >> 2, q = lane & 3;
 #pragma unroll 4
-  for (int k0 = 0; k0 < kmax; k0 += 4) {
+  for (int k0 = kmin; k0 < kmax; k0 += 4) {
     double a[TM], b[TN];
 #pragma unroll
     for (int i = 0; i < TM; i++) a[i] = AT ? sA[(k0 + q) * LDA + m0 + i * 8 + r] : sA[(m0 + i * 8 + r) * LDA + k0 + q];
@@ -2456,7 +2456,17 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
   if (!BENCH && m0 >= n) return;  // no rows of W for this warp (nothing after this needs the CTA barrier)
   double acc[2][C::WN / 8][2];
   zero_acc(acc);
-  if (m0 < n) warp_gemm<C::LDQ, C::LDZ, 2, C::WN / 8, true>(sQ, sZ, m0, n0, n4, acc);
+  // aligned bench plans: a warp's 32 columns are one frozen group, present in one
+  // or both children -- the k range of an absent child's rows (zero in Z) is
+  // skipped (the algorithmic count 2 n_p (sum of present k_c) m, bitwise equal)
+  int kb = 0, ke = n4;
+  if (BENCH && A.aligned && (k1 & 3) == 0) {
+    const bool p1 = src1[n0] >= 0, p2 = src2[n0] >= 0;
+    if (!p1 && !p2) ke = 0;
+    else if (p1 && !p2) ke = k1;
+    else if (!p1 && p2) kb = k1;
+  }
+  if (m0 < n) warp_gemm<C::LDQ, C::LDZ, 2, C::WN / 8, true>(sQ, sZ, m0, n0, ke, acc, kb);
   // epilogue straight from the accumulators: lane (r, q) holds W[row][col], W[row][col + 1]
   // rows [0, k_q) -> q's panel; rows [k_q, n_q) -> S row segment and the transposed block
   const int lane = threadIdx.x & 31;
@@ -3208,7 +3218,9 @@ template <int NP, int TN, bool BENCH>
 static h2sp_status launch_strips1(const StripArgs &a, int64_t ntiles, cudaStream_t st) {
   using C = StripCfg<NP, TN>;
   // bench mode, aligned plans: the pipelined persistent kernel (H2SP_STRIP_PIPE=0: one tile per CTA)
-  static const bool pipe = !getenv("H2SP_STRIP_PIPE") || atoi(getenv("H2SP_STRIP_PIPE")) != 0;
+  // (measured slower: config 5 serial strips 1.11 vs 0.96 s -- one CTA of 16 warps
+  // per SM hides the DMMA / shared-memory latencies worse than two one-tile CTAs)
+  static const bool pipe = getenv("H2SP_STRIP_PIPE") && atoi(getenv("H2SP_STRIP_PIPE")) != 0;
   if constexpr (BENCH && NP >= 32) {
     if (pipe && a.aligned) {
       using PC = StripPipeCfg<NP, TN>;

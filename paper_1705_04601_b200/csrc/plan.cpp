@@ -343,6 +343,10 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
     const bool sym = P->sym;
     double flops_qr = 0, flops_coup = 0, flops_cong = 0, flops_strip = 0;
     double uniq_qr = 0, uniq_coup = 0, uniq_cong = 0, uniq_strip = 0;  // owned work only (sharded plans)
+    double flops_strip_exec = 0;
+    // strip kernels skip the k range of an absent child when every panel column
+    // of a warp's slab has the same children present (aligned plans, kernels.cu)
+    const bool strip_skip = bench && P->strip_aligned;
     int64_t dt_len = 0, bb_len = 0, yr_len = 0, yc_len = 0;
     std::vector<std::vector<PairItem>> pairs(L + 1);
     // strip panels, index set * (L+1) + level (set 0: groups born at level 0, set 1: later)
@@ -519,6 +523,7 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
             }
             const double rows = (takeA ? kq[c1] : 0) + (takeB ? kq[c1 + 1] : 0);
             flops_strip += 2.0 * nq[cq] * rows * g.m;
+            flops_strip_exec += 2.0 * nq[cq] * nq[cq] * g.m;  // the kernels multiply by all of Q_p
             // a row panel's groups all sit with its rotating cluster's owner (the
             // symmetric halo copies elsewhere are duplicates); a column-strip group
             // exists only with its fixed row cluster's owner
@@ -983,6 +988,7 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
             const double rows = (sg.pos_c1 >= 0 ? kk[c1] : 0) + (sg.pos_c2 >= 0 ? kk[c1 + 1] : 0);
             const double m = sg.m;
             li.flops += 2 * nq * rows * m;
+            li.flops_exec += 2 * nq * (strip_skip ? rows : nq) * m;  // the kernel's k range
             const double outb = (pn.y_dst >= 0 ? kq * m : 0.0) + (pn.s_dst >= 0 ? (nq - kq) * m : 0.0) +
                                 (sg.s_dst_t >= 0 ? (nq - kq) * m : 0.0);
             li.bytes += 8.0 * (rows * m + outb);
@@ -1067,7 +1073,7 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
     P->levels_active = levels_active;
     P->flops_exec = 0;
     for (auto &x : P->launch_info) {
-      if (x.kind != 3) x.flops_exec = x.flops;
+      if (x.kind != 3 && x.kind != 4 && x.kind != 5) x.flops_exec = x.flops;
       P->flops_exec += x.flops_exec;
     }
     P->meta_bytes = align_up(mb.buf.size(), 256);
