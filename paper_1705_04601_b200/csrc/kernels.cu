@@ -2049,10 +2049,13 @@ __global__ void __launch_bounds__(PairWy128Cfg<KP>::THREADS, 1) pair_wy128_kerne
       const double a = (q & 1) ? e1 : e0;
 #pragma unroll
       for (int i = 0; i < KP / 8; i++) dmma(R[(k0 >> 2) & 1][i], a, sV[(k0 + q) * LDV + i * 8 + r]);
-      if (gnext) {  // 512 threads x 32 k-steps = the 128 x 128 entries
-        const int gi = (threadIdx.x >> 7) + 4 * (k0 >> 2);
-        sG[gi * LD + gc.j] = gen_entry_s(A.gen, gc, gi, s_xt, s_tab);
-      }
+    }
+    // G of pair p+1 (512 threads x 32 rows = the 128 x 128 entries) in a rolled loop
+    // after the DMMAs: the evaluations share the FP64 datapath with them anyway, and
+    // inlining one per unrolled k-step made the kernel 188 KB of code (i-cache misses)
+    if (gnext) {
+#pragma unroll 2
+      for (int gi = threadIdx.x >> 7; gi < 128; gi += 4) sG[gi * LD + gc.j] = gen_entry_s(A.gen, gc, gi, s_xt, s_tab);
     }
 #pragma unroll
     for (int i = 0; i < KP / 8; i++) {
