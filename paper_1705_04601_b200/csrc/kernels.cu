@@ -2988,17 +2988,21 @@ __global__ void __launch_bounds__(256) csr_cols_kernel(const CsrBlockRow *__rest
 // recomputing the (few, small) ancestor products it needs.
 // Vectors column-major (ld) with nrhs columns; zb = basis coefficients.
 // --------------------------------------------------------------------------
+constexpr int APPLY_RC = 8;   // right-hand sides per pass over Q (each Q element read once per pass)
+
 __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const double *__restrict__ q,
                                                        const double *__restrict__ b, int64_t ldb, double *__restrict__ y,
                                                        int64_t ldy, double *__restrict__ zb, int64_t zbl, int nrhs, int B,
                                                        int *__restrict__ arrive, int64_t leaf0) {
   // z = Q_t^T x_t with Q read straight from global memory (rows are coalesced
   // across the threads of one column block): no shared-memory staging, so every
-  // leaf's CTA is resident at once (16 per SM) and the climb starts in one wave.
-  // Thread t = h n + j sums rows i = h, h + H, ... of column j (H = blockDim / n
-  // interleaved partial sums, added in a fixed order).
-  __shared__ double sx[128];
-  __shared__ double red[128];
+  // leaf's CTA is resident at once and the climb starts in one wave.  Thread
+  // t = h n + j sums rows i = h, h + H, ... of column j (H = blockDim / n
+  // interleaved partial sums, added in a fixed order) for APPLY_RC right-hand
+  // sides at once: every Q element is read once per APPLY_RC vectors; the row
+  // loop is unrolled for independent loads in flight.
+  __shared__ double sx[128 * APPLY_RC];
+  __shared__ double red[128 * APPLY_RC];
   __shared__ int s_go;
   // metadata of every cluster this CTA may climb through (the leaf's ancestors)
   // and of their children, in one round trip (level l in slot l)
@@ -3028,27 +3032,39 @@ __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const dou
       const int k1 = level > 0 ? m_k1[level] : 0;
       const int H = blockDim.x / n;
       const int t = threadIdx.x, j = t % n, h = t / n;
-      for (int r = 0; r < nrhs; r++) {
+      for (int r0 = 0; r0 < nrhs; r0 += APPLY_RC) {
+        const int rc = min(APPLY_RC, nrhs - r0);
         __syncthreads();
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        for (int e = threadIdx.x; e < n * rc; e += blockDim.x) {
+          const int i = e % n, rr = e / n, r = r0 + rr;
           double v;
           if (level == 0) v = b[((idx - leaf0) * B + i) + r * ldb];
           else if (i < k1) v = __ldcg(zb + m_zb1[level] + i + r * zbl);
           else v = __ldcg(zb + m_zb2[level] + (i - k1) + r * zbl);
-          sx[i] = v;
+          sx[i * APPLY_RC + rr] = v;
         }
         __syncthreads();
         if (h < H) {
-          double acc = 0.0;
-          for (int i = h; i < n; i += H) acc = fma(__ldg(Q + int64_t(i) * n + j), sx[i], acc);
-          red[h * n + j] = acc;
+          double acc[APPLY_RC];
+#pragma unroll
+          for (int rr = 0; rr < APPLY_RC; rr++) acc[rr] = 0.0;
+#pragma unroll 4
+          for (int i = h; i < n; i += H) {
+            const double qv = __ldg(Q + int64_t(i) * n + j);
+#pragma unroll
+            for (int rr = 0; rr < APPLY_RC; rr++)
+              if (rr < rc) acc[rr] = fma(qv, sx[i * APPLY_RC + rr], acc[rr]);
+          }
+#pragma unroll
+          for (int rr = 0; rr < APPLY_RC; rr++) red[(h * n + j) * APPLY_RC + rr] = acc[rr];
         }
         __syncthreads();
-        if (t < n) {
-          double acc = red[t];
-          for (int u = 1; u < H; u++) acc += red[u * n + t];
-          if (t < k) zb[m_zb[level] + t + r * zbl] = acc;
-          else y[m_loc[level] + (t - k) + r * ldy] = acc;
+        for (int e = threadIdx.x; e < n * rc; e += blockDim.x) {
+          const int tj = e % n, rr = e / n, r = r0 + rr;
+          double acc = red[tj * APPLY_RC + rr];
+          for (int u = 1; u < H; u++) acc += red[(u * n + tj) * APPLY_RC + rr];
+          if (tj < k) zb[m_zb[level] + tj + r * zbl] = acc;
+          else y[m_loc[level] + (tj - k) + r * ldy] = acc;
         }
       }
     }
@@ -3071,8 +3087,8 @@ __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const dou
 __global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, const double *__restrict__ q,
                                                       const double *__restrict__ y, int64_t ldy, double *__restrict__ x,
                                                       int64_t ldx, int nrhs, int B, int64_t leaf0) {
-  __shared__ double sv[128];
-  __shared__ double sw[128];
+  __shared__ double sv[128 * APPLY_RC];
+  __shared__ double sw[128 * APPLY_RC];
   // metadata of the whole root -> leaf path in one round trip (level l in slot l),
   // and the ancestors' Q pulled into L2 while the root levels run
   __shared__ int p_n[64], p_k[64], p_k1[64];
@@ -3093,18 +3109,21 @@ __global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, const doub
     for (int e = threadIdx.x * 16; e < n * n; e += blockDim.x * 16)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(Q + e));
   }
-  for (int r = 0; r < nrhs; r++) {
+  for (int r0 = 0; r0 < nrhs; r0 += APPLY_RC) {
+    const int rc = min(APPLY_RC, nrhs - r0);
     // walk the path root -> leaf; sv[0:k] holds the basis coefficients from the parent.
     // Q rows are read straight from global memory: H consecutive threads share a
     // row (coalesced segments), partial sums over j = h, h + H, ... are added by
-    // a butterfly over those H lanes.
+    // a butterfly over those H lanes; APPLY_RC right-hand sides per Q read.
     for (int level = L; level >= 0; level--) {
       const int n = p_n[level], k = p_k[level];
       __syncthreads();
       if (n == 0) continue;
       const double *Q = q + p_q[level];
-      for (int j = threadIdx.x; j < n; j += blockDim.x)
-        if (j >= k) sv[j] = y[p_loc[level] + (j - k) + r * ldy];
+      for (int e = threadIdx.x; e < n * rc; e += blockDim.x) {
+        const int jj = e % n, rr = e / n;
+        if (jj >= k) sv[jj * APPLY_RC + rr] = y[p_loc[level] + (jj - k) + (r0 + rr) * ldy];
+      }
       __syncthreads();
       int rlo = 0, rhi = n;
       if (level > 0) {  // only the rows of the child on the path are needed
@@ -3118,22 +3137,36 @@ __global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, const doub
       while (H < 32 && 2 * H * rows <= int(blockDim.x)) H *= 2;
       for (int i0 = 0; i0 < rows; i0 += int(blockDim.x) / H) {
         const int il = i0 + int(threadIdx.x) / H, h = threadIdx.x % H;
-        double acc = 0.0;
+        double acc[APPLY_RC];
+#pragma unroll
+        for (int rr = 0; rr < APPLY_RC; rr++) acc[rr] = 0.0;
         if (il < rows) {
           const double *Qi = Q + int64_t(rlo + il) * n;
-          for (int j = h; j < n; j += H) acc = fma(__ldg(Qi + j), sv[j], acc);
+#pragma unroll 4
+          for (int jj = h; jj < n; jj += H) {
+            const double qv = __ldg(Qi + jj);
+#pragma unroll
+            for (int rr = 0; rr < APPLY_RC; rr++)
+              if (rr < rc) acc[rr] = fma(qv, sv[jj * APPLY_RC + rr], acc[rr]);
+          }
         }
-        for (int o = H >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+#pragma unroll
+        for (int rr = 0; rr < APPLY_RC; rr++)
+          for (int o = H >> 1; o > 0; o >>= 1) acc[rr] += __shfl_xor_sync(0xffffffffu, acc[rr], o);
         if (h == 0 && il < rows) {
-          if (level == 0)
-            x[((leaf - leaf0) * B + il) + r * ldx] = acc;
-          else
-            sw[il] = acc;
+#pragma unroll
+          for (int rr = 0; rr < APPLY_RC; rr++) {
+            if (rr >= rc) continue;
+            if (level == 0)
+              x[((leaf - leaf0) * B + il) + (r0 + rr) * ldx] = acc[rr];
+            else
+              sw[il * APPLY_RC + rr] = acc[rr];
+          }
         }
       }
       if (level > 0) {
         __syncthreads();
-        for (int i = threadIdx.x; i < rows; i += blockDim.x) sv[i] = sw[i];
+        for (int e = threadIdx.x; e < rows * APPLY_RC; e += blockDim.x) sv[e] = sw[e];
       }
     }
   }

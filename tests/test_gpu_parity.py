@@ -218,6 +218,36 @@ def test_apply_parity(sym, B):
     assert np.abs(x.cpu().numpy() - xo).max() <= 1e-12 * np.abs(b).max()
 
 
+@pytest.mark.parametrize("nrhs", [1, 8, 11, 32])
+def test_apply_many_rhs_and_repeatable(nrhs):
+    """The applies read each Q once per 8 right-hand sides (apply kernels'
+    APPLY_RC): nrhs = 1, 8, 11 (a ragged chunk), 32 against the oracle, config-5
+    recipe leaves (B = 128); and bitwise repeatable over 10 runs (the upward pass
+    continues through atomic arrival counters -- a race would show here;
+    compute-sanitizer is closed on this pool)."""
+    _need_gpu()
+    h = h2gen.make_config(5, N=8192)
+    plan, sp, out = _run(h)
+    res = oracle.sparsify(h)
+    b = np.random.default_rng(nrhs).standard_normal((nrhs, h.N))
+    bt = torch.from_numpy(b).cuda()
+    y = torch.empty_like(bt)
+    x = torch.empty_like(bt)
+    sp.apply_Ut(bt, y)
+    sp.apply_V(y, x)
+    torch.cuda.synchronize()
+    yo = oracle.apply_Ut(res, b.T, "row").T
+    xo = oracle.apply_V(res, yo.T, "col").T
+    assert np.abs(y.cpu().numpy() - yo).max() <= 1e-12 * np.abs(b).max()
+    assert np.abs(x.cpu().numpy() - xo).max() <= 1e-12 * np.abs(b).max()
+    y0, x0 = y.clone(), x.clone()
+    for _ in range(10):
+        sp.apply_Ut(bt, y)
+        sp.apply_V(y, x)
+        torch.cuda.synchronize()
+        assert torch.equal(y, y0) and torch.equal(x, x0)
+
+
 def test_solve_through_gpu_factors():
     """x = V S^-1 U^T b equals A_H2^-1 b (Eq. sp0) using GPU apply and GPU S."""
     _need_gpu()
