@@ -2988,8 +2988,9 @@ __global__ void __launch_bounds__(256) csr_cols_kernel(const CsrBlockRow *__rest
 // recomputing the (few, small) ancestor products it needs.
 // Vectors column-major (ld) with nrhs columns; zb = basis coefficients.
 // --------------------------------------------------------------------------
-constexpr int APPLY_RC = 8;   // right-hand sides per pass over Q (each Q element read once per pass)
-
+// APPLY_RC: right-hand sides per pass over Q (each Q element read once per pass):
+// 1 for a single vector, 8 otherwise
+template <int APPLY_RC>
 __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const double *__restrict__ q,
                                                        const double *__restrict__ b, int64_t ldb, double *__restrict__ y,
                                                        int64_t ldy, double *__restrict__ zb, int64_t zbl, int nrhs, int B,
@@ -3084,6 +3085,7 @@ __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const dou
   }
 }
 
+template <int APPLY_RC>
 __global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, const double *__restrict__ q,
                                                       const double *__restrict__ y, int64_t ldy, double *__restrict__ x,
                                                       int64_t ldx, int nrhs, int B, int64_t leaf0) {
@@ -3947,8 +3949,12 @@ h2sp_status launch_apply_Ut(const h2sp_plan_s *P, const double *q, const double 
   const int64_t zbl = col_side ? P->zb_col_len : P->zb_row_len;
   int *arrive = (int *)(scratch + ((size_t(std::max(P->zb_row_len, P->zb_col_len)) * nrhs * 8 + 255) / 256) * 256);
   H2SP_CK(cudaMemsetAsync(arrive, 0, size_t(P->ncl) * sizeof(int), st));
-  apply_ut_kernel<<<unsigned(P->n_leaves_local), 128, 0, st>>>(
-      sd, P->L, q, b, ldb, y, ldy, zb, zbl, nrhs, P->B, arrive, P->first_leaf);
+  if (nrhs == 1)
+    apply_ut_kernel<1><<<unsigned(P->n_leaves_local), 128, 0, st>>>(sd, P->L, q, b, ldb, y, ldy, zb, zbl, nrhs, P->B,
+                                                                    arrive, P->first_leaf);
+  else
+    apply_ut_kernel<8><<<unsigned(P->n_leaves_local), 128, 0, st>>>(sd, P->L, q, b, ldb, y, ldy, zb, zbl, nrhs, P->B,
+                                                                    arrive, P->first_leaf);
   H2SP_CK(cudaGetLastError());
   return H2SP_OK;
 }
@@ -3960,8 +3966,12 @@ h2sp_status launch_apply_V(const h2sp_plan_s *P, const double *q, const double *
   const Clusters cl = make_clusters(P, meta);
   (void)scratch;
   const Side sd = side_of(cl, col_side);
-  apply_v_kernel<<<unsigned(P->n_leaves_local), 128, 0, st>>>(
-      sd, P->L, q, y, ldy, x, ldx, nrhs, P->B, P->first_leaf);
+  if (nrhs == 1)
+    apply_v_kernel<1><<<unsigned(P->n_leaves_local), 128, 0, st>>>(sd, P->L, q, y, ldy, x, ldx, nrhs, P->B,
+                                                                   P->first_leaf);
+  else
+    apply_v_kernel<8><<<unsigned(P->n_leaves_local), 128, 0, st>>>(sd, P->L, q, y, ldy, x, ldx, nrhs, P->B,
+                                                                   P->first_leaf);
   H2SP_CK(cudaGetLastError());
   return H2SP_OK;
 }
