@@ -723,10 +723,17 @@ __global__ void __launch_bounds__(128) qr_reg_kernel(Side sd, int L, int level, 
 // convention H; emits R^ and the compact-WY factors V, M = T V^T only (leaves
 // this large always take the compact-WY congruence; wy_form_q_kernel forms Q).
 // --------------------------------------------------------------------------
+// Also at levels >= 1 (X = [R^_c1 T[:k1]; R^_c2 T[k1:]], the children's R^ and
+// T staged in the V / T / M region first) and with the explicit Q = I - V M
+// written to `qout` when wy == nullptr: the k = n / 2 clusters of configs 4 and
+// 5 (n = 64, k = 32) run here at 5 CTAs (10 warps) per SM instead of the
+// warp-per-cluster kernel's 45 KB of shared memory per warp (4 warps per SM).
 template <int KP, int NW>
 __global__ void __launch_bounds__(32 * NW) qr_cta_kernel(Side sd, int nclust, const double *__restrict__ leaf,
                                                      double *__restrict__ rh, double *__restrict__ wy, int wy_kp,
-                                                     int wy_n, const uint64_t *meta_magic, uint64_t magic) {
+                                                     int wy_n, const uint64_t *meta_magic, uint64_t magic, int L = 0,
+                                                     int level = 0, const double *__restrict__ transfer = nullptr,
+                                                     double *__restrict__ qout = nullptr) {
   if (meta_magic && threadIdx.x == 0 && blockIdx.x == 0 && *meta_magic != magic) __trap();
   constexpr int NROW = 32 * NW;  // rows (one per thread)
   constexpr int LDV = KP + 4, LDT = KP + 4, LDM = NROW + 4;
@@ -738,20 +745,50 @@ __global__ void __launch_bounds__(32 * NW) qr_cta_kernel(Side sd, int nclust, co
   __shared__ double s_alpha[2];
   const int ci = blockIdx.x;
   if (ci >= nclust) return;
-  const int64_t cl = ci;  // level 0
+  const int64_t cl = lvl_off_d(L, level) + ci;
   const int n = sd.n[cl], k = sd.k[cl];
   if (n == 0 || !sd.need[cl]) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double *Wg = wy + int64_t(ci) * 2 * wy_n * wy_kp;
+  double *Wg = wy ? wy + int64_t(ci) * 2 * wy_n * wy_kp : nullptr;
+  double *Qg = wy ? nullptr : qout + sd.q_off[cl];
   if (k == 0) {
-    for (int idx = tid; idx < 2 * wy_n * wy_kp; idx += blockDim.x) Wg[idx] = 0.0;
+    if (Wg)
+      for (int idx = tid; idx < 2 * wy_n * wy_kp; idx += blockDim.x) Wg[idx] = 0.0;
+    else
+      for (int idx = tid; idx < n * n; idx += blockDim.x) Qg[idx] = (idx / n == idx % n) ? 1.0 : 0.0;
     return;
   }
   double x[KP];
-  {
+  if (level == 0) {
     const double *R = leaf + sd.leaf_off[cl];
 #pragma unroll
     for (int c = 0; c < KP; c++) x[c] = (tid < n && c < k) ? __ldg(R + int64_t(tid) * k + c) : 0.0;
+  } else {  // X = [R^_c1 T[:k1]; R^_c2 T[k1:]]
+    const int64_t c1 = lvl_off_d(L, level - 1) + 2 * int64_t(ci), c2 = c1 + 1;
+    const int k1 = sd.k[c1], k2 = sd.k[c2];
+    double *sT = smc, *sR1 = sT + n * k, *sR2 = sR1 + k1 * k1;
+    const double *T = transfer + sd.tr_off[cl];
+    for (int idx = tid; idx < n * k; idx += blockDim.x) cp8(&sT[idx], T + idx, true);
+    for (int idx = tid; idx < k1 * k1; idx += blockDim.x) cp8(&sR1[idx], rh + sd.rh_off[c1] + idx, true);
+    for (int idx = tid; idx < k2 * k2; idx += blockDim.x) cp8(&sR2[idx], rh + sd.rh_off[c2] + idx, true);
+    cp_commit();
+    cp_wait_all();
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < KP; c++) x[c] = 0.0;
+    if (tid < n) {
+      const bool first = tid < k1;
+      const int ii = first ? tid : tid - k1, kk = first ? k1 : k2, roff = first ? 0 : k1;
+      const double *Rr = first ? sR1 : sR2;
+      for (int l = ii; l < kk; l++) {
+        const double rv = Rr[ii * kk + l];
+        const double *Trow = sT + (roff + l) * k;
+#pragma unroll
+        for (int c = 0; c < KP; c++)
+          if (c < k) x[c] = fma(rv, Trow[c], x[c]);
+      }
+    }
+    __syncthreads();  // the staging region becomes V / T / M
   }
   for (int idx = tid; idx < NROW * LDV; idx += blockDim.x) Vs[idx] = 0.0;
   for (int idx = tid; idx < KP * LDT; idx += blockDim.x) Tw[idx] = 0.0;
@@ -853,6 +890,22 @@ __global__ void __launch_bounds__(32 * NW) qr_cta_kernel(Side sd, int nclust, co
     Mm[(ta * 8 + r) * LDM + tc * 8 + 2 * q + 1] = acc[1];
   }
   __syncthreads();
+  if (!Wg) {  // Q = I - V M (n x n) from 8 x 8 DMMA tiles, straight to global
+    const int N8 = (n + 7) / 8;
+    for (int tile = warp; tile < N8 * N8; tile += NW) {
+      const int ti = tile / N8, tc = tile % N8;
+      double acc[2] = {0.0, 0.0};
+#pragma unroll
+      for (int k0 = 0; k0 < KP; k0 += 4) dmma(acc, Vs[(ti * 8 + r) * LDV + k0 + q], Mm[(k0 + q) * LDM + tc * 8 + r]);
+      const int i = ti * 8 + r;
+#pragma unroll
+      for (int e = 0; e < 2; e++) {
+        const int c = tc * 8 + 2 * q + e;
+        if (i < n && c < n) Qg[i * n + c] = (i == c ? 1.0 : 0.0) - acc[e];
+      }
+    }
+    return;
+  }
   for (int idx = tid; idx < wy_n * wy_kp; idx += blockDim.x) {
     const int i = idx / wy_kp, c = idx - i * wy_kp;
     Wg[idx] = (i < n && c < k) ? Vs[i * LDV + c] : 0.0;
@@ -3479,6 +3532,17 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
           if (kp == 16) H2SP_QR_CTA(16, 2); else H2SP_QR_CTA(32, 2);
         }
 #undef H2SP_QR_CTA
+        H2SP_CK(cudaGetLastError());
+        return H2SP_OK;
+      }
+      // k = n / 2 = 32 (configs 4 and 5 above the leaves, config 4's leaves): one
+      // 64-thread CTA per cluster, explicit Q (H2SP_QR_WARP32=1: the warp kernel)
+      static const bool qr_warp32 = getenv("H2SP_QR_WARP32") && atoi(getenv("H2SP_QR_WARP32")) != 0;
+      if (!wyo && kmax > 24 && kmax <= 32 && nmax > 32 && nmax <= 64 && !qr_warp32) {
+        constexpr size_t smem = size_t(64 * (32 + 4) + 32 * (32 + 4) + 32 * (64 + 4)) * sizeof(double);
+        if (h2sp_status e_ = ensure_smem((const void *)qr_cta_kernel<32, 2>, smem)) return e_;
+        qr_cta_kernel<32, 2><<<unsigned(M), 64, smem, s>>>(sd, M, leaf, rh, nullptr, 0, 0, magic_ptr, P->magic, L, k,
+                                                            tr, qo);
         H2SP_CK(cudaGetLastError());
         return H2SP_OK;
       }
