@@ -139,3 +139,46 @@ def test_bench_plan_matches_stored_plan(name, make):
     assert ("csr" in kinds_a) and ("csr" not in kinds_b) and ("bench_reduce" in kinds_b)
     with pytest.raises(h2sp.H2spError):
         b.pattern(with_cols=True)
+
+
+def _gloo_protocol_worker(rank, world, port, q):
+    """The multi-GPU bench's host logic on gloo: rank g takes virtual shards
+    [V g / world, V (g+1) / world) of ONE matrix (bench mode, as bench.py's
+    run_protocol), and the job's work is the all-reduced sum of flops_unique."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+    V = 4
+    packed = h2gen.pack(h2gen.make_structure(5, N=16384))
+    mine = list(range(rank * V // world, (rank + 1) * V // world))
+    plans = [h2sp.Plan(packed, g, V, bench=True) for g in mine]
+    t = torch.tensor([sum(p.sizes["flops_unique"] for p in plans), float(sum(p.s_rows for p in plans))],
+                     dtype=torch.float64)
+    dist.all_reduce(t)
+    shards = torch.zeros(V, dtype=torch.int64)
+    for g in mine:
+        shards[g] += 1
+    dist.all_reduce(shards)
+    if rank == 0:
+        full = h2sp.Plan(packed, bench=True)
+        q.put((abs(float(t[0]) - full.sizes["flops"]) <= 1e-9 * full.sizes["flops"], int(t[1]) == full.N,
+               bool((shards == 1).all())))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_protocol_shard_split():
+    import multiprocessing as mp
+    import random
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 31000 + random.randint(0, 2000)
+    ps = [ctx.Process(target=_gloo_protocol_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(timeout=180)
+    assert all(p.exitcode == 0 for p in ps)
+    flops_ok, rows_ok, shards_ok = q.get(timeout=5)
+    assert flops_ok and rows_ok and shards_ok
