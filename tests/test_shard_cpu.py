@@ -120,8 +120,11 @@ def test_bench_plan_matches_stored_plan(name, make):
     a, b = h2sp.Plan(p), h2sp.Plan(p, bench=True)
     for k in ("s_nnz", "s_blocks", "s_rows", "q_row", "q_col"):
         assert a.sizes[k] == b.sizes[k], k
-    for k in ("flops", "flops_executed", "flops_congruence", "flops_strips"):
+    for k in ("flops", "flops_congruence", "flops_strips"):
         assert a.sizes[k] == b.sizes[k], k
+    # executed work: bench plans on aligned trees skip the k range of an absent
+    # child in the strips (the kernel's loop), so they execute no more
+    assert b.sizes["flops_executed"] <= a.sizes["flops_executed"]
     assert a.sizes["bench_parts"] == 0
     # slots: sum over block rows of (rows x blocks) -- every block row's blocks
     # are the column runs of its pattern
