@@ -38,7 +38,7 @@ import numpy as np
 __all__ = [
     "H2Input", "CONFIGS", "lvl_off", "cid", "make_points", "kd_tree", "block_tree",
     "make_config", "random_h2", "axis_aligned_h2", "fig3_h2", "eta0_h2",
-    "kernel_matrix", "pack", "coupling_block_descs", "make_structure", "fill_cheb_bases", "cheb_cos_table",
+    "kernel_matrix", "pack", "make_ifmm", "random_sparse", "coupling_block_descs", "make_structure", "fill_cheb_bases", "cheb_cos_table",
     "cheb_base_orders",
 ]
 
@@ -246,9 +246,21 @@ def kernel_matrix(spec: dict, x: np.ndarray, y: np.ndarray, same_index=None) -> 
             K = 1.0 / (4.0 * math.pi * r)
         if same_index is not None:
             K = np.where(same_index, 1.0 / (4.0 * math.pi * spec["h"]), K)
+    elif kind == "ifmm":
+        K = _ifmm(r, spec["d"])
+        if same_index is not None:
+            K = np.where(same_index, 1.0, K)
     else:
         raise ValueError(kind)
     return K
+
+
+def _ifmm(r: np.ndarray, d: float) -> np.ndarray:
+    """The interaction matrix of the paper's preconditioning example (Example
+    "mat1", P:882-892): A_ij = 1 if i == j, |r_i - r_j| / d if 0 < |r_i - r_j| < d,
+    d / |r_i - r_j| otherwise (the i == j case is applied by the caller, by index)."""
+    with np.errstate(divide="ignore"):
+        return np.where(r < d, r / d, d / np.maximum(r, 1e-300))
 
 
 def _kernel_spec(cfg: dict, N: int) -> dict:
@@ -393,6 +405,61 @@ def make_config(idx: int, seed: Optional[int] = None, N: Optional[int] = None, m
     return h2
 
 
+def make_ifmm(N: int, d: float, B: int, r: int, seed: int = 53, eta: float = 0.7) -> H2Input:
+    """H^2 input of the paper's preconditioning example (DESIGN.md
+    §9e): N uniform points in the unit cube (3-D, "randomly distributed 3D
+    data"), kernel of Example mat1 with parameter d, nested Chebyshev
+    bases of rank r (the tensor orders of _ORDERS[(3, r)]) and leaves of B
+    points, symmetric.  The operator of GMRES and the H^2 matrix behind the
+    preconditioner are two such inputs on the same points with different r (the
+    paper's eps = 1e-9 and 1e-3 approximations, reading 25)."""
+    rng = np.random.default_rng(seed)
+    L = int(round(math.log2(N // B)))
+    assert B << L == N
+    pts = make_points("cube", N, rng)
+    perm, lo, hi = kd_tree(pts, L)
+    x = pts[perm]
+    near0, adm = block_tree(lo, hi, L, eta)
+    kspec = dict(kind="ifmm", d=float(d))
+    h2 = _cheb_h2(x, L, B, r, near0, adm, kspec, lo, hi, True)
+    h2.meta.update(box_lo=lo, box_hi=hi, r=r, dim=3, config="ifmm", seed=seed, N=N, eta=eta, method="cheb",
+                   kernel=kspec)
+    return h2
+
+
+def random_sparse(nb: int, bs: int, seed: int, density: float = 0.2, decay: float = 2.0, shift: float = 1.0,
+                  symmetric_pattern: bool = True):
+    """Seeded block-sparse test matrix in CSR (rowptr int64, col int32 ascending,
+    val float64) for the ILUt parity tests: nb x nb blocks of bs x bs, block
+    (I, J) present with probability `density` (always for I == J; mirrored when
+    `symmetric_pattern`), entries N(0, 1) * exp(-|I - J| / decay), and the
+    diagonal raised by `shift` times the row's absolute sum (shift >= 1:
+    diagonally dominant, no zero pivot).  Shapes only -- no method arithmetic."""
+    rng = np.random.default_rng(seed)
+    P = rng.random((nb, nb)) < density
+    if symmetric_pattern:
+        P = P | P.T
+    np.fill_diagonal(P, True)
+    n = nb * bs
+    rows, cols, vals = [], [], []
+    for I in range(nb):
+        Js = np.nonzero(P[I])[0]
+        blk = rng.standard_normal((bs, len(Js) * bs)) * np.repeat(np.exp(-np.abs(Js - I) / decay), bs)[None, :]
+        c = (Js[:, None] * bs + np.arange(bs)[None, :]).ravel()
+        for a in range(bs):
+            i = I * bs + a
+            v = blk[a].copy()
+            dpos = np.nonzero(c == i)[0][0]
+            v[dpos] = 0.0
+            v[dpos] = shift * np.abs(v).sum() + 1.0
+            rows.append(np.full(len(c), i))
+            cols.append(c)
+            vals.append(v)
+    rowptr = np.zeros(n + 1, dtype=np.int64)
+    rowptr[1:] = np.cumsum([len(c) for c in cols])
+    return rowptr, np.concatenate(cols).astype(np.int32), np.concatenate(vals)
+
+
 def make_structure(idx: int, seed: Optional[int] = None, N: Optional[int] = None) -> H2Input:
     """The STRUCTURE of BASELINE.json ``configs[idx-1]`` only -- tree-ordered
     points, cluster boxes, block cluster tree and ranks, no numeric arrays --
@@ -443,6 +510,8 @@ def _close_blocks(x, B, near0, kspec):
             with np.errstate(divide="ignore"):
                 K = 1.0 / (4.0 * math.pi * rr)
             K = np.where(same, 1.0 / (4.0 * math.pi * kspec["h"]), K)
+        elif kind == "ifmm":
+            K = np.where(same, 1.0, _ifmm(rr, kspec["d"]))
         out[c0:c0 + chunk] = K
     return out
 
