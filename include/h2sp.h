@@ -421,6 +421,112 @@ h2sp_status h2sp_comm_allreduce(h2sp_comm comm, double *buf, int64_t n, int op, 
 h2sp_status h2sp_comm_info(h2sp_comm comm, int *rank, int *world);
 void h2sp_comm_destroy(h2sp_comm comm);
 
+/* ------------------------------------------------------------------------
+ * The preconditioning workload ("Sparsification method as a
+ * preconditioner") and the direct solve (§8(f) #1, x = V S^-1 U^T b,
+ * Eq. sp0).  The paper solves A x = b by GMRES "for the matrix
+ * approximated in H^2 format with accuracy 1e-9" and, "as a preconditioner,
+ * the H^2 approximation of A with accuracy 1e-3 sparsified and factorized with
+ * ILUt decomposition".  The operator's matvec here is
+ * the exact sparse factorisation of that H^2 matrix, A x = U S U^T x
+ * (symmetric plans, V = U); the preconditioner is
+ * M^-1 = U_M (L U)^-1 U_M^T with L U = ILUT(S_M).  Vectors are in tree order
+ * (h2sp_apply_Ut's b / h2sp_apply_V's x); S-order temporaries stay inside.
+ * ------------------------------------------------------------------------ */
+
+/* A square CSR matrix on the DEVICE: rowptr[n + 1] (int64), col (int32,
+ * ascending and unique within a row), val (FP64).  S as h2sp_build writes it
+ * (s_rowptr / s_col / s_val) is one. */
+typedef struct {
+  int64_t n;
+  const int64_t *rowptr;
+  const int32_t *col;
+  const double *val;
+} h2sp_csr;
+
+/* ILUT factors in row-pool form, DEVICE, caller-owned (allocated with n and
+ * pool_cap): row i of L (strict lower; unit diagonal implied) is
+ * pool_col/pool_val[l_start[i] .. + l_len[i]), row i of U (strict upper) is
+ * [u_start[i] .. + u_len[i]), both in ascending column order; diag[i] = u_ii.
+ * Rows are placed in the pool in completion order (the pool holds L and U). */
+typedef struct {
+  int64_t n;
+  int64_t *l_start, *u_start;
+  int32_t *l_len, *u_len;
+  double *diag;
+  int32_t *pool_col;
+  double *pool_val;
+  int64_t pool_cap;
+} h2sp_ilut_factors;
+
+/* Device workspace of h2sp_ilut for an n x n matrix (per-warp work rows and
+ * candidate lists, completion flags), or -1. */
+int64_t h2sp_ilut_ws_bytes(int64_t n);
+/* ILUT(tau, p) of A (reading 24: Saad's Algorithm 10.6, IKJ order,
+ * dual dropping -- w_k / u_kk dropped if |.| < tau ||a_i||_2 or == 0; after the
+ * row: entries below tau ||a_i||_2 dropped, then only the p largest of the L
+ * part and of the U part kept (ties: smaller column; p < 0 keeps all); the
+ * diagonal is always kept).  tau = 0, p < 0: the complete LU without pivoting
+ * (the direct solve of §8(f) #1; S is SPD in symmetric mode, Proposition
+ * P:504-509, so no pivot vanishes in exact arithmetic).  The factors are
+ * bitwise those of the algorithm run row by row in this arithmetic order.
+ * Synchronises the stream.  pool_used (HOST, may be NULL): entries written.
+ * Errors: H2SP_ENOMEM if pool_cap is too small (pool_used = entries requested
+ * so far -- a lower bound; retry with a larger pool), H2SP_EINVAL on a zero
+ * pivot (message names the first row) or bad arguments, H2SP_EUNSUPPORTED if
+ * n > ~1.6M (the per-warp presence bitmap lives in shared memory). */
+h2sp_status h2sp_ilut(const h2sp_csr *A, double tau, int p, h2sp_ilut_factors *F, void *ws, size_t ws_bytes,
+                      int64_t *pool_used, void *stream);
+/* x = (L U)^-1 b (forward substitution with the unit L, then backward with
+ * U), asynchronous on the stream; x may alias b. */
+int64_t h2sp_ilu_solve_ws_bytes(int64_t n);
+h2sp_status h2sp_ilu_solve(const h2sp_ilut_factors *F, const double *b, double *x, void *ws, size_t ws_bytes,
+                           void *stream);
+/* y = A x for a device CSR matrix (asynchronous). */
+h2sp_status h2sp_csr_spmv(const h2sp_csr *A, const double *x, double *y, void *stream);
+
+/* A sparsified symmetric H^2 matrix A = U S U^T: the plan, its Q batch (q_row
+ * of h2sp_build), its stored S and an apply workspace (h2sp_apply_ws_bytes(plan,
+ * 1), uploaded with h2sp_plan_upload).  All DEVICE pointers. */
+typedef struct {
+  h2sp_plan plan;
+  const double *q;
+  h2sp_csr S;
+  void *apply_ws;
+  size_t apply_ws_bytes;
+} h2sp_sparsified;
+
+typedef struct {
+  int restart;   /* m of GMRES(m)                                      */
+  int maxiter;   /* total Arnoldi steps                                */
+  double tol;    /* stop when the residual estimate <= tol * ||b||_2   */
+} h2sp_gmres_opts;
+
+typedef struct {
+  int iters;          /* Arnoldi steps taken                                       */
+  int restarts;       /* cycles completed                                          */
+  int converged;
+  int history_len;    /* entries of history produced (may exceed history_cap)      */
+  double *history;    /* HOST, caller-owned, history_cap doubles (may be NULL):
+                         ||r_j|| / ||b|| -- 1, then the estimate after each step    */
+  int history_cap;
+} h2sp_gmres_info;
+
+/* Device workspace of h2sp_gmres: the (restart + 1) Krylov vectors and
+ * temporaries. */
+int64_t h2sp_gmres_ws_bytes(int64_t n, int restart);
+/* Solve A x = b by restarted GMRES(m) with right preconditioning (Saad,
+ * Algorithm 9.5; x0 = 0), x = M^-1 u: A from `A`, M^-1 from `M` and `F` (the
+ * ILUT of M's S) -- both NULL for no preconditioner.  Arnoldi by classical
+ * Gram-Schmidt with one re-orthogonalisation; the Hessenberg least-squares
+ * problem is reduced by Givens rotations on the host (a handful of scalars per
+ * step; one device-to-host read of the step's dot products).  Synchronous.
+ * Errors: H2SP_EUNSUPPORTED for nonsymmetric or sharded plans, H2SP_EINVAL on
+ * size mismatches / bad options. */
+h2sp_status h2sp_gmres(const h2sp_sparsified *A, const h2sp_sparsified *M, const h2sp_ilut_factors *F,
+                       const double *b, double *x, const h2sp_gmres_opts *opt, h2sp_gmres_info *info, void *ws,
+                       size_t ws_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

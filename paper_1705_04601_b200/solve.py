@@ -172,3 +172,24 @@ def solve(sp: Sparsifier, chol, b):
     x = torch.empty_like(bt)
     sp.apply_V(z, x)
     return x[0]
+
+
+def factor_lu(sp: Sparsifier, stream=None):
+    """The complete LU of the S the last build wrote (h2sp_ilut at tau = 0,
+    p < 0: this package's sync-free row-by-row factorisation in S's own
+    level-major order, no library call).  Works for symmetric (SPD S,
+    Proposition) and general plans with nonzero pivots."""
+    from .krylov import CsrMatrix, IlutFactors
+    return IlutFactors(CsrMatrix.from_sparsifier(sp), 0.0, -1, stream=stream)
+
+
+def solve_lu(sp: Sparsifier, fac, b, stream=None):
+    """x = V (L U)^-1 U^T b (Eq. sp0, P:45-49) with the device LU of factor_lu;
+    b tree order (CUDA float64, length N)."""
+    bt = b.reshape(1, -1).contiguous()
+    y = torch.empty_like(bt)
+    sp.apply_Ut(bt, y, stream=stream)
+    fac.solve(y[0], y[0], stream=stream)
+    x = torch.empty_like(bt)
+    sp.apply_V(y, x, stream=stream)
+    return x[0]
