@@ -573,7 +573,17 @@ def main():
     ap.add_argument("--shard", action="store_true",
                     help="N>1: split ONE matrix into N top-level subtree shards (strong scaling) "
                          "instead of N independent matrices (weak scaling, default)")
+    ap.add_argument("--workload", choices=["h2sp", "precond"], default="h2sp",
+                    help="precond: the paper's GMRES + sparsified-H2 ILUt experiment (bench_precond.py, SURVEY 8(f) #3)")
+    ap.add_argument("--d", type=float, default=1e-3, help="precond: Example mat1 parameter d")
+    ap.add_argument("--tau", type=float, default=2e-2, help="precond: ILUt drop tolerance")
     args = ap.parse_args()
+    if args.workload == "precond":
+        import bench_precond
+        args.steps = args.steps or 3
+        args.warmup = max(args.warmup or 3, 3)
+        bench_precond.run(args, ClockSampler, _peaks())
+        return
     if args.steps is None:
         args.steps = 5 if args.config == 5 else 20
     if args.warmup is None:

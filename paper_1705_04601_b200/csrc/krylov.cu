@@ -92,79 +92,58 @@ struct IlutArgs {
   int64_t cap;
   unsigned long long *cursor;  // pool entries reserved so far
   unsigned long long *ticket;  // next row
-  int32_t *done;               // [n] 1 once U row i and u_ii are published
+  int32_t *done;               // [n] 1 once u_ii is published, 2 once U row i is
   int32_t *status;             // [0] bit 1 = pool overflow, bit 2 = zero pivot; [1] first zero-pivot row
   double *w;                   // [slots][n] work rows (zero between rows)
   int32_t *ccol;               // [slots][n] candidate columns
   double *cval;                // [slots][n] candidate values
 };
 
-// Next set bit in [from, lim) of the warp's bitmap, or lim.
-__device__ __forceinline__ int64_t next_bit(const uint32_t *bits, int64_t from, int64_t lim, int lane) {
-  if (from >= lim) return lim;
-  const int64_t w0 = from >> 5, wl = (lim + 31) >> 5;
-  for (int64_t base = w0; base < wl; base += 32) {
-    const int64_t wi = base + lane;
-    uint32_t v = 0;
-    if (wi < wl) {
-      v = bits[wi];
-      const int64_t lo = from - (wi << 5);
-      if (lo > 0) v &= ~0u << lo;
-      const int64_t hi = lim - (wi << 5);
-      if (hi < 32) v &= (1u << hi) - 1u;
-    }
-    const unsigned m = __ballot_sync(FULL, v != 0);
-    if (m) {
-      const int src = __ffs(m) - 1;
-      const uint32_t vv = __shfl_sync(FULL, v, src);
-      return ((base + src) << 5) + __ffs(vv) - 1;
-    }
-  }
-  return lim;
+// Bitmap word wi restricted to columns [lo, hi] (0 outside the word range).
+__device__ __forceinline__ uint32_t word_in(const uint32_t *bits, int64_t wi, int64_t lo, int64_t hi) {
+  const int64_t l = lo - (wi << 5), h = hi - (wi << 5);
+  if (l >= 32 || h < 0) return 0;
+  uint32_t v = bits[wi];
+  if (l > 0) v &= ~0u << l;
+  if (h < 31) v &= (2u << h) - 1u;
+  return v;
 }
 
-// Compact the present entries of w in [lo, hi] (bitmap order = ascending
-// column) into (ccol, cval); U part (upper = true): only entries surviving the
-// tau rule; L part: every present entry (rule 1 already dropped the rest).
+// Compact the present entries of w in [lo, hi] (ascending column) into (ccol,
+// cval); U part (upper = true): only entries surviving the tau rule; L part:
+// every present entry (rule 1 already dropped the rest).  Chunks of 1024
+// columns: lane l reads column base + 32 q + l for q < 32 (coalesced, up to
+// 32 loads in flight), empty chunks skipped on the bitmap.  This runs on the
+// critical path (the U part before the row is published).
 __device__ int64_t gather(const uint32_t *bits, const double *w, int64_t lo, int64_t hi, bool upper, double taui,
                           int32_t *ccol, double *cval, int lane) {
   int64_t cnt = 0;
   if (lo > hi) return 0;
-  const int64_t w0 = lo >> 5, w1 = hi >> 5;
-  for (int64_t base = w0; base <= w1; base += 32) {
-    const int64_t wi = base + lane;
-    uint32_t v = 0;
-    if (wi <= w1) {
-      v = bits[wi];
-      const int64_t l = lo - (wi << 5);
-      if (l > 0) v &= ~0u << l;
-      const int64_t h = hi - (wi << 5);
-      if (h < 31) v &= (2u << h) - 1u;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t base = lo & ~int64_t(1023); base <= hi; base += 1024) {
+    const uint32_t wd = word_in(bits, (base >> 5) + lane, lo, hi);
+    if (!__ballot_sync(FULL, wd != 0)) continue;
+    double v[32];
+    uint32_t pres = 0;
+#pragma unroll
+    for (int q = 0; q < 32; q++) {
+      const uint32_t wq = __shfl_sync(FULL, wd, q);
+      const bool pq = (wq >> lane) & 1u;
+      pres |= uint32_t(pq) << q;
+      v[q] = pq ? w[base + 32 * q + lane] : 0.0;
     }
-    uint32_t keep = v;
-    if (upper) {
-      keep = 0;
-      for (uint32_t t = v; t; t &= t - 1) {
-        const int b = __ffs(t) - 1;
-        const double x = w[(wi << 5) + b];
-        if (!(fabs(x) < taui || x == 0.0)) keep |= 1u << b;
+#pragma unroll
+    for (int q = 0; q < 32; q++) {
+      const bool pq = (pres >> q) & 1u;
+      const bool keep = pq && (!upper || !(fabs(v[q]) < taui || v[q] == 0.0));
+      const unsigned m = __ballot_sync(FULL, keep);
+      if (keep) {
+        const int64_t pos = cnt + __popc(m & lt);
+        ccol[pos] = int32_t(base + 32 * q + lane);
+        cval[pos] = v[q];
       }
+      cnt += __popc(m);
     }
-    const int c = __popc(keep);
-    int incl = c;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(FULL, incl, o);
-      if (lane >= o) incl += y;
-    }
-    int64_t pos = cnt + incl - c;
-    for (uint32_t t = keep; t; t &= t - 1) {
-      const int b = __ffs(t) - 1;
-      const int64_t j = (wi << 5) + b;
-      ccol[pos] = int32_t(j);
-      cval[pos] = w[j];
-      pos++;
-    }
-    cnt += __shfl_sync(FULL, incl, 31);
   }
   __syncwarp();
   return cnt;
@@ -260,7 +239,8 @@ __global__ void __launch_bounds__(256) ilut_kernel(IlutArgs A, int warps_per_cta
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (wid >= warps_per_cta) return;
   uint32_t *bits = smem + size_t(wid) * A.nwords;
-  int *hist = reinterpret_cast<int *>(smem + size_t(warps_per_cta) * A.nwords) + 256 * wid;
+  int *hist = reinterpret_cast<int *>(smem + size_t(warps_per_cta) * A.nwords) + 288 * wid;
+  int32_t *kbuf = hist + 256;  // the batch's columns
   const int64_t slot = int64_t(blockIdx.x) * warps_per_cta + wid;
   double *w = A.w + slot * A.n;
   int32_t *ccol = A.ccol + slot * A.n;
@@ -294,32 +274,90 @@ __global__ void __launch_bounds__(256) ilut_kernel(IlutArgs A, int warps_per_cta
       hi = max(hi, __shfl_xor_sync(FULL, hi, o));
     }
     __syncwarp();
-    // for k < i with w_k present, in increasing k
-    for (int64_t k = next_bit(bits, lo, i, lane); k < i; k = next_bit(bits, k + 1, i, lane)) {
-      if (lane == 0) wait_flag(A.done + k, 1);
+    // for k < i with w_k present, in increasing k -- 32 at a time: lane q takes
+    // the q-th next present k and evaluates rule 1 on it; every k before the
+    // first kept one is dropped at once (their values are final: no update
+    // lies between them), the first kept one is applied, and the batch restarts
+    // after it.  Rule 1 needs only u_kk (flag >= 1); the update needs U row k
+    // (flag >= 2) -- a dropped k never waits for k's U row.
+    for (int64_t cur = lo; cur < i;) {
+      const int64_t wi0 = cur >> 5, wi = wi0 + lane;
+      const int64_t wend = (i + 31) >> 5;
+      const uint32_t wd = wi < wend ? word_in(bits, wi, cur, i - 1) : 0u;
+      const int c = __popc(wd);
+      int excl = c;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, excl, o);
+        if (lane >= o) excl += y;
+      }
+      const int total = __shfl_sync(FULL, excl, 31);
+      excl -= c;
+      if (total == 0) {
+        cur = (wi0 + 32) << 5;
+        continue;
+      }
+      {  // scatter the first 32 present columns to kbuf in order
+        int r = excl;
+        for (uint32_t t = wd; t && r < 32; t &= t - 1, r++) kbuf[r] = int32_t((wi << 5) + __ffs(t) - 1);
+      }
       __syncwarp();
-      const double wk = __ddiv_rn(w[k], __ldcg(A.diag + k));
-      if (fabs(wk) < taui || wk == 0.0) {  // rule 1
-        __syncwarp();
-        if (lane == 0) {
-          w[k] = 0.0;
-          bits[k >> 5] &= ~(1u << (k & 31));
-        }
+      const int nk = min(total, 32);
+      const int64_t k = lane < nk ? int64_t(kbuf[lane]) : -1;
+      bool drop = true;
+      double wk = 0.0;
+      if (k >= 0) {
+        wait_flag(A.done + k, 1);
+        wk = __ddiv_rn(w[k], __ldcg(A.diag + k));
+        drop = fabs(wk) < taui || wk == 0.0;  // rule 1
+      }
+      const unsigned kept = __ballot_sync(FULL, !drop);
+      const int f = kept ? __ffs(kept) - 1 : nk;
+      __syncwarp();
+      if (lane < f && k >= 0) {
+        w[k] = 0.0;
+        atomicAnd(&bits[k >> 5], ~(1u << (k & 31)));
+      }
+      if (f == nk) {  // the whole batch dropped
+        cur = total > 32 ? int64_t(__shfl_sync(FULL, k, 31)) + 1 : int64_t((wi0 + 32) << 5);
         __syncwarp();
         continue;
       }
-      __syncwarp();
-      if (lane == 0) w[k] = wk;
-      const int64_t us = __ldcg(A.u_start + k);
-      const int32_t ul = __ldcg(A.u_len + k);
-      for (int32_t e = lane; e < ul; e += 32) {
-        const int32_t j = __ldcg(A.pool_col + us + e);
-        const double u = __ldcg(A.pool_val + us + e);
-        w[j] = __dsub_rn(w[j], __dmul_rn(wk, u));
-        atomicOr(&bits[j >> 5], 1u << (j & 31));
-        hi = max(hi, int64_t(j));
+      const int64_t kf = __shfl_sync(FULL, k, f);
+      const double wkf = __shfl_sync(FULL, wk, f);
+      if (lane == f) {
+        w[kf] = wkf;
+        wait_flag(A.done + kf, 2);
       }
       __syncwarp();
+      const int64_t us = __ldcg(A.u_start + kf);
+      const int32_t ul = __ldcg(A.u_len + kf);
+      for (int32_t e0 = 0; e0 < ul; e0 += 128) {  // four entries per lane in flight
+        int32_t j[4];
+        double u[4], x[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const int32_t e = e0 + 32 * q + lane;
+          j[q] = e < ul ? __ldcg(A.pool_col + us + e) : -1;
+          u[q] = e < ul ? __ldcg(A.pool_val + us + e) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) x[q] = j[q] >= 0 ? w[j[q]] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+          if (j[q] >= 0) {
+            w[j[q]] = __dsub_rn(x[q], __dmul_rn(wkf, u[q]));
+            atomicOr(&bits[j[q] >> 5], 1u << (j[q] & 31));
+            hi = max(hi, int64_t(j[q]));
+          }
+      }
+      cur = kf + 1;
+      __syncwarp();
+    }
+    // u_ii is final: publish it (flag 1) before the U row (flag 2)
+    if (lane == 0) {
+      A.diag[i] = w[i];
+      __threadfence();
+      st_release(A.done + i, 1);
     }
     for (int o = 16; o; o >>= 1) hi = max(hi, __shfl_xor_sync(FULL, hi, o));
     // rule 2, U part; publish U row i and u_ii first
@@ -337,13 +375,12 @@ __global__ void __launch_bounds__(256) ilut_kernel(IlutArgs A, int warps_per_cta
     if (lane == 0) {
       A.u_start[i] = st;
       A.u_len[i] = fits ? int32_t(cu) : 0;
-      A.diag[i] = uii;
       if (uii == 0.0) {
         atomicOr(&A.status[0], 2);
         atomicMin(&A.status[1], int32_t(i));
       }
       __threadfence();
-      st_release(A.done + i, 1);
+      st_release(A.done + i, 2);
     }
     // L part (kept entries of rule 1)
     int64_t cl = gather(bits, w, lo, i - 1, false, taui, ccol, cval, lane);
@@ -361,10 +398,16 @@ __global__ void __launch_bounds__(256) ilut_kernel(IlutArgs A, int warps_per_cta
     }
     // clear the touched range of w and the bitmap
     __syncwarp();
-    for (int64_t wi = (lo >> 5) + lane; wi <= (hi >> 5); wi += 32) {
-      for (uint32_t t = bits[wi]; t; t &= t - 1) w[(wi << 5) + __ffs(t) - 1] = 0.0;
-      bits[wi] = 0;
+    for (int64_t base = lo & ~int64_t(255); base <= hi; base += 256) {
+      const int64_t wi = (base >> 5) + (lane & 7);
+      const uint32_t wd = lane < 8 ? word_in(bits, wi, lo, hi) : 0u;
+      if (!__ballot_sync(FULL, wd != 0)) continue;
+#pragma unroll
+      for (int q = 0; q < 8; q++)
+        if ((__shfl_sync(FULL, wd, q) >> lane) & 1u) w[base + 32 * q + lane] = 0.0;
     }
+    __syncwarp();
+    for (int64_t wi = (lo >> 5) + lane; wi <= (hi >> 5); wi += 32) bits[wi] = 0;
     __syncwarp();
   }
 }
@@ -381,62 +424,123 @@ struct TrsvArgs {
   const int32_t *pool_col;
   const double *pool_val;
   const double *b;
-  double *x;
-  int32_t *flag;
+  double *y;                   // forward result (workspace), sentinel-initialised
+  double *x;                   // result, sentinel-initialised before the backward pass
   unsigned long long *ticket;  // [0] forward, [1] backward
 };
+
+// A solved value is its own completion flag: the vectors start filled with a
+// NaN payload no arithmetic produces, readers poll the value (relaxed, gpu
+// scope: one L2 round trip, no separate flag / fence).
+constexpr unsigned long long XSENT = 0x7ff4deadbeefcafeull;
+
+__device__ __forceinline__ unsigned long long ld_rlx(const double *p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ double poll(const double *p, unsigned long long v) {
+  while (v == XSENT) {
+    __nanosleep(16);
+    v = ld_rlx(p);
+  }
+  return __longlong_as_double(static_cast<long long>(v));
+}
+
+__device__ __forceinline__ void st_rlx(double *p, double v) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(v)) : "memory");
+}
+
+__global__ void fill_sentinel_kernel(double *v, int64_t n) {
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x)
+    v[e] = __longlong_as_double(static_cast<long long>(XSENT));
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
   return v;
 }
 
-__global__ void __launch_bounds__(256) trsv_lower_kernel(TrsvArgs A) {
-  const int lane = threadIdx.x & 31;
-  for (;;) {
-    unsigned long long t = 0;
-    if (lane == 0) t = atomicAdd(A.ticket, 1ull);
-    const int64_t i = int64_t(__shfl_sync(FULL, t, 0));
-    if (i >= A.n) return;
-    const int64_t s0 = A.l_start[i];
-    const int32_t len = A.l_len[i];
-    double acc = 0.0;
-    for (int32_t e = lane; e < len; e += 32) {
-      const int32_t j = A.pool_col[s0 + e];
-      wait_flag(A.flag + j, 1);
-      acc += A.pool_val[s0 + e] * __ldcg(A.x + j);
-    }
-    acc = warp_sum(acc);
-    if (lane == 0) {
-      A.x[i] = A.b[i] - acc;
-      __threadfence();
-      st_release(A.flag + i, 1);
-    }
-  }
-}
+// Rows are solved in blocks of TB = 32 consecutive rows (in solve order:
+// ascending for L, descending for U -- the U solve is the L solve of the
+// reversed index i' = n - 1 - i), one warp per block, blocks handed out in
+// solve order by a ticket.  Lane r owns row r of the block: it walks its
+// row's entries oldest first, summing those more than two blocks back (polling
+// each value -- the oldest are long done) and scattering the rest into three
+// dense 32 x 32 tiles in shared memory (two previous blocks, own block).  The
+// chain from block to block is then: poll the 32 values of a previous block,
+// 32 shuffle-FMAs per tile, the 32-step triangular solve of the own tile by
+// shuffles, 32 stores -- no per-row global round trip.
+constexpr int TB = 32;
 
-__global__ void __launch_bounds__(256) trsv_upper_kernel(TrsvArgs A) {
-  const int lane = threadIdx.x & 31;
+template <bool UPPER>
+__global__ void __launch_bounds__(32) trsv_block_kernel(TrsvArgs A) {
+  __shared__ double T[3 * TB][TB];  // [c][r]: column jp - (r0 - 2 TB) of row r
+  const int lane = threadIdx.x;
+  const int64_t n = A.n, nb = (n + TB - 1) / TB;
+  const double *src = UPPER ? A.y : A.b;
+  double *dst = UPPER ? A.x : A.y;
   for (;;) {
-    unsigned long long t = 0;
-    if (lane == 0) t = atomicAdd(A.ticket + 1, 1ull);
-    const int64_t tt = int64_t(__shfl_sync(FULL, t, 0));
-    if (tt >= A.n) return;
-    const int64_t i = A.n - 1 - tt;
-    const int64_t s0 = A.u_start[i];
-    const int32_t len = A.u_len[i];
+    unsigned long long tk = 0;
+    if (lane == 0) tk = atomicAdd(A.ticket + (UPPER ? 1 : 0), 1ull);
+    const int64_t t = int64_t(__shfl_sync(FULL, tk, 0));
+    if (t >= nb) return;
+    for (int c = 0; c < 3 * TB; c++) T[c][lane] = 0.0;
+    const int64_t r0 = t * TB, w0 = r0 - 2 * TB;
+    const int64_t ip = r0 + lane;
+    const bool live = ip < n;
+    const int64_t i = UPPER ? n - 1 - ip : ip;
     double acc = 0.0;
-    for (int32_t e = lane; e < len; e += 32) {
-      const int32_t j = A.pool_col[s0 + e];
-      wait_flag(A.flag + j, 2);
-      acc += A.pool_val[s0 + e] * __ldcg(A.x + j);
+    if (live) {
+      const int64_t s0 = UPPER ? A.u_start[i] : A.l_start[i];
+      const int32_t len = UPPER ? A.u_len[i] : A.l_len[i];
+      // oldest first: ascending column for L, descending for U
+      for (int32_t e0 = 0; e0 < len; e0 += 4) {
+        int64_t jp[4], j[4];
+        double v[4];
+        unsigned long long xv[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const int32_t e = e0 + q;
+          const int64_t idx = s0 + (UPPER ? len - 1 - e : e);
+          j[q] = e < len ? A.pool_col[idx] : 0;
+          v[q] = e < len ? A.pool_val[idx] : 0.0;
+          jp[q] = e < len ? (UPPER ? n - 1 - j[q] : j[q]) : INT64_MAX;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) xv[q] = jp[q] < w0 ? ld_rlx(dst + j[q]) : 0ull;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          if (jp[q] < w0)
+            acc += v[q] * poll(dst + j[q], xv[q]);
+          else if (jp[q] != INT64_MAX)
+            T[jp[q] - w0][lane] = v[q];
+        }
+      }
     }
-    acc = warp_sum(acc);
-    if (lane == 0) {
-      A.x[i] = (__ldcg(A.x + i) - acc) / A.diag[i];
-      __threadfence();
-      st_release(A.flag + i, 2);
+    __syncwarp();
+    double rhs = live ? src[i] - acc : 0.0;
+    const double dg = (UPPER && live) ? A.diag[i] : 1.0;
+    for (int pb = 0; pb < 2; pb++) {  // blocks t - 2, t - 1
+      const int64_t base = w0 + int64_t(pb) * TB;
+      if (base < 0) continue;
+      bool any = false;
+      for (int c = 0; c < TB; c++) any |= T[pb * TB + c][lane] != 0.0;
+      if (!__ballot_sync(FULL, any)) continue;
+      const int64_t jq = base + lane;
+      const double *px = dst + (UPPER ? n - 1 - jq : jq);
+      const double xp = poll(px, ld_rlx(px));
+      for (int c = 0; c < TB; c++) rhs -= T[pb * TB + c][lane] * __shfl_sync(FULL, xp, c);
     }
+    double xr = 0.0;
+    for (int c = 0; c < TB; c++) {
+      if (lane == c) xr = UPPER ? rhs / dg : rhs;
+      const double xc = __shfl_sync(FULL, xr, c);
+      if (lane > c) rhs -= T[2 * TB + c][lane] * xc;
+    }
+    if (live) st_rlx(dst + i, xr);
+    __syncwarp();
   }
 }
 
@@ -545,7 +649,7 @@ struct IlutCfg {
 IlutCfg ilut_cfg(int64_t n) {
   IlutCfg c{};
   c.nwords = int((n + 31) / 32);
-  const size_t per_warp = size_t(c.nwords) * 4 + 256 * 4;
+  const size_t per_warp = size_t(c.nwords) * 4 + 288 * 4;
   c.warps = int(std::max<size_t>(1, std::min<size_t>(8, (200u << 10) / per_warp)));
   c.smem = per_warp * c.warps;
   const int per_sm = std::max(1, 8 / c.warps);
@@ -583,16 +687,17 @@ IlutWs ilut_carve(unsigned char *base, int64_t n, int64_t slots) {
 }
 
 struct TrsvWs {
-  int32_t *flag;
+  double *y;
   unsigned long long *ticket;
   size_t bytes;
 };
 
 TrsvWs trsv_carve(unsigned char *base, int64_t n) {
   TrsvWs s{};
-  s.flag = reinterpret_cast<int32_t *>(base);
-  s.ticket = reinterpret_cast<unsigned long long *>(base ? base + align256(size_t(n) * 4) : nullptr);
-  s.bytes = align256(size_t(n) * 4) + 256;
+  const size_t yb = align256(size_t(n) * 8);
+  s.y = reinterpret_cast<double *>(base);
+  s.ticket = reinterpret_cast<unsigned long long *>(base ? base + yb : nullptr);
+  s.bytes = yb + 256;
   return s;
 }
 
@@ -613,13 +718,16 @@ h2sp_status launch_trsv(const h2sp_ilut_factors *F, const double *b, double *x, 
   const int64_t n = F->n;
   if (n == 0) return H2SP_OK;
   TrsvWs t = trsv_carve(ws, n);
-  KCK(cudaMemsetAsync(t.flag, 0, size_t(n) * 4, st));
+  const int64_t nb = (n + TB - 1) / TB;
+  const int fg = int(std::min<int64_t>(int64_t(num_sms()) * 4, (n + 255) / 256));
   KCK(cudaMemsetAsync(t.ticket, 0, 16, st));
-  TrsvArgs a{n, F->l_start, F->u_start, F->l_len, F->u_len, F->diag, F->pool_col, F->pool_val, b, x, t.flag, t.ticket};
-  const int grid = num_sms() * 8;
-  trsv_lower_kernel<<<grid, 256, 0, st>>>(a);
+  fill_sentinel_kernel<<<fg, 256, 0, st>>>(t.y, n);
+  TrsvArgs a{n, F->l_start, F->u_start, F->l_len, F->u_len, F->diag, F->pool_col, F->pool_val, b, t.y, x, t.ticket};
+  const int grid = int(std::min<int64_t>(int64_t(num_sms()) * 16, nb));
+  trsv_block_kernel<false><<<grid, 32, 0, st>>>(a);
   KCK(cudaGetLastError());
-  trsv_upper_kernel<<<grid, 256, 0, st>>>(a);
+  fill_sentinel_kernel<<<fg, 256, 0, st>>>(x, n);  // b (possibly aliased by x) is consumed
+  trsv_block_kernel<true><<<grid, 32, 0, st>>>(a);
   KCK(cudaGetLastError());
   return H2SP_OK;
 }

@@ -101,7 +101,14 @@ class IlutFactors:
         self.u_len = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
         self.diag = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
         nnz = int(A.col.numel())
-        cap = int(pool_cap) if pool_cap else max(1024, nnz + (2 * p * n if p >= 0 else nnz))
+        if pool_cap:
+            cap = int(pool_cap)
+        elif p >= 0:
+            cap = max(1024, 2 * p * n + n)
+        elif tau > 0:   # dropping: start at an eighth of S (grown on H2SP_ENOMEM)
+            cap = max(1024, 16 * n, nnz // 8)
+        else:           # complete LU: fill
+            cap = max(1024, 3 * nnz)
         ws_b = int(lib.h2sp_ilut_ws_bytes(n))
         ws = torch.empty(ws_b + 256, dtype=torch.uint8, device=dev)
         wsp = (ws.data_ptr() + 255) // 256 * 256
