@@ -412,7 +412,7 @@ def make_ifmm(N: int, d: float, B: int, r: int, seed: int = 53, eta: float = 0.7
     bases of rank r (the tensor orders of _ORDERS[(3, r)]) and leaves of B
     points, symmetric.  The operator of GMRES and the H^2 matrix behind the
     preconditioner are two such inputs on the same points with different r (the
-    paper's eps = 1e-9 and 1e-3 approximations, reading 25)."""
+    paper's eps = 1e-9 and 1e-3 approximations, reading 26)."""
     rng = np.random.default_rng(seed)
     L = int(round(math.log2(N // B)))
     assert B << L == N

@@ -462,7 +462,7 @@ typedef struct {
 /* Device workspace of h2sp_ilut for an n x n matrix (per-warp work rows and
  * candidate lists, completion flags), or -1. */
 int64_t h2sp_ilut_ws_bytes(int64_t n);
-/* ILUT(tau, p) of A (reading 24: Saad's Algorithm 10.6, IKJ order,
+/* ILUT(tau, p) of A (reading 25: Saad's Algorithm 10.6, IKJ order,
  * dual dropping -- w_k / u_kk dropped if |.| < tau ||a_i||_2 or == 0; after the
  * row: entries below tau ||a_i||_2 dropped, then only the p largest of the L
  * part and of the U part kept (ties: smaller column; p < 0 keeps all); the

@@ -6,7 +6,7 @@
  * shared with, the CUDA path.
  *
  * The paper names ILUt and its drop tolerance tau but
- * does not define it; reading 24 takes Saad's ILUT(tau, p)
+ * does not define it; reading 25 takes Saad's ILUT(tau, p)
  * ("Iterative Methods for Sparse Linear Systems", Algorithm 10.6, IKJ
  * variant, with its dual dropping rule), written out here step by step:
  *
@@ -20,7 +20,7 @@
  *     rule 2: drop w_j (j != i) if |w_j| < tau_i or w_j == 0; then keep only
  *             the p largest |w_j| of the L part (j < i) and the p largest of
  *             the strict U part (j > i); ties go to the smaller column
- *             (reading 24); p < 0 keeps all.  The diagonal is always kept.
+ *             (reading 25); p < 0 keeps all.  The diagonal is always kept.
  *     l_ij := w_j (j < i, unit diagonal implied); u_ii := w_i; u_ij := w_j (j > i)
  *
  * Every update is the two-rounding w_j - (w_k * u_kj) (no fused multiply-add:

@@ -1,6 +1,6 @@
 """CPU oracle of the paper's preconditioning workload (
 "Sparsification method as a preconditioner"): ILUt of S
-(``oracle/ilut.c``, plain C, Saad's ILUT(tau, p), reading 24) and
+(``oracle/ilut.c``, plain C, Saad's ILUT(tau, p), reading 25) and
 restarted GMRES with right preconditioning (plain numpy, Saad's Algorithm 9.5
 with modified Gram-Schmidt Arnoldi and Givens rotations).
 

@@ -2,7 +2,7 @@
 // "Sparsification method as a preconditioner") and the direct
 // solve it shares its factorisation with (§8(f) #1, x = V S^-1 U^T b):
 //
-//   * ilut_kernel   -- ILUT(tau, p) of S (reading 24: Saad's
+//   * ilut_kernel   -- ILUT(tau, p) of S (reading 25: Saad's
 //                      Algorithm 10.6 with the dual dropping rule); tau = 0,
 //                      p < 0 is the complete LU (the direct solve).
 //   * trsv kernels  -- (L U)^-1 b by forward / backward substitution.

@@ -5,7 +5,7 @@ on the same seeded inputs.
 
 * ILUT factors: BITWISE equal (pattern and values) -- both sides take every
   dropping decision on the same FP64 values, computed in the same order with
-  the same two-rounding updates (reading 24).
+  the same two-rounding updates (reading 25).
 * triangular solves, SpMV: 1e-12 relative (summation order differs).
 * GMRES: same iteration count (+-1), x within 1e-7 relative, residual of the
   GPU x against the oracle's dense A_H2 below the tolerance."""

@@ -72,7 +72,7 @@ def test_huge_tau_is_jacobi():
 
 def test_p_largest_with_ties():
     """Row 0 of an upper-arrow matrix: off-diagonals 1, 3, 2, 3 at columns 1..4.
-    p = 2 keeps both 3s; p = 1 keeps the 3 of the smaller column (reading 24);
+    p = 2 keeps both 3s; p = 1 keeps the 3 of the smaller column (reading 25);
     p = 3 adds the 2; the diagonal is always kept."""
     n = 5
     A = 10 * np.eye(n)

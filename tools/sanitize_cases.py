@@ -1,45 +1,53 @@
-"""Small builds for compute-sanitizer (memcheck / racecheck / synccheck, one tool
-per gpurun call): BASELINE configs[0], a random B = 128 general case, the
-config-5 recipe in bench mode with matrix-free inputs over 4 virtual shards,
-and the applies (apply_ut_kernel's arrival counters)."""
+"""Small invocations of every libh2sp kernel family for compute-sanitizer
+(memcheck / racecheck / synccheck): stored build + applies on configs[0] and a
+B = 128 random case, a bench-mode close_gen build (config-5 recipe, N = 8192),
+ILUT / triangular solves / SpMV / GMRES on a small problem."""
+import os
 import sys
 
 import numpy as np
 import torch
 
-sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import h2gen  # noqa: E402
 import paper_1705_04601_b200 as h2sp  # noqa: E402
+from paper_1705_04601_b200 import krylov as kr  # noqa: E402
 
 
 def stored(h):
-    packed = h2gen.pack(h)
-    plan = h2sp.Plan(packed)
-    sp = h2sp.Sparsifier(plan, packed)
+    p = h2gen.pack(h)
+    plan = h2sp.Plan(p)
+    sp = h2sp.Sparsifier(plan, p)
     sp.build()
-    b = torch.randn(1, plan.n_tree_local, dtype=torch.float64, device="cuda")
-    y = torch.empty(1, plan.s_rows, dtype=torch.float64, device="cuda")
-    x = torch.empty_like(b)
+    b = torch.randn(2, plan.n_tree_local, dtype=torch.float64, device="cuda")
+    y = torch.empty(2, plan.s_rows, dtype=torch.float64, device="cuda")
     sp.apply_Ut(b, y)
-    sp.apply_V(y, x)
-    aws = sp.apply_workspace(1)
-    sp.build_apply(b, y, torch.randn_like(y), x, aws)
+    sp.apply_V(y, b)
     torch.cuda.synchronize()
-    print("stored ok", h.N, flush=True)
+    return sp
 
 
-def bench_shards(h, G):
-    packed = h2gen.pack(h)
-    plans = [h2sp.Plan(packed, g, G, bench=True) for g in range(G)]
-    xr, _, _, _ = h2gen.coupling_block_descs(h)
-    vs = h2sp.VirtualShards(plans, packed, close_gen={"points": h.points, "kernel": h.meta["kernel"], "nodes_row": xr})
-    vs.outputs["bench_w"].copy_(torch.from_numpy(np.random.default_rng(1).standard_normal(h.N)))
-    vs.build()
-    torch.cuda.synchronize()
-    print("bench shards ok", h.N, G, flush=True)
-
-
-if __name__ == "__main__":
-    stored(h2gen.make_config(1))
-    stored(h2gen.random_h2(4, 128, 5, False, eta=0.7, max_rank=32))
-    bench_shards(h2gen.make_config(5, N=8192), 4)
+stored(h2gen.make_config(1))
+stored(h2gen.random_h2(4, 128, 3, True, eta=0.7, max_rank=32))
+stored(h2gen.random_h2(4, 64, 4, False, eta=0.7, max_rank=32))
+# bench mode, matrix-free close blocks (config-5 recipe, B = 128)
+h = h2gen.make_config(5, N=8192)
+p = h2gen.pack(h)
+plan = h2sp.Plan(p, bench=True)
+sp = h2sp.Sparsifier(plan, p, close_gen={"points": h.points, "kernel": h.meta["kernel"]})
+sp.outputs["bench_w"].copy_(torch.randn(h.N, dtype=torch.float64))
+sp.build()
+torch.cuda.synchronize()
+# ILUT / solves / SpMV / GMRES
+rp, ci, v = h2gen.random_sparse(40, 16, 1, density=0.1, shift=0.3)
+A = kr.CsrMatrix(torch.from_numpy(rp), torch.from_numpy(ci), torch.from_numpy(v))
+F = kr.IlutFactors(A, 1e-2, 8)
+bb = torch.randn(A.n, dtype=torch.float64, device="cuda")
+F.solve(bb)
+A.matvec(bb)
+hop = h2gen.make_ifmm(2048, 1e-2, 32, 8)
+spo = stored(hop)
+Fo = kr.IlutFactors(kr.CsrMatrix.from_sparsifier(spo), 1e-3, -1)
+x, info = kr.gmres(spo, torch.randn(2048, dtype=torch.float64, device="cuda"), M=spo, F=Fo, restart=10, maxiter=20)
+torch.cuda.synchronize()
+print("sanitize cases done", info.iters, flush=True)
