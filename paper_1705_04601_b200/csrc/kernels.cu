@@ -1507,6 +1507,86 @@ __device__ __forceinline__ void scatter_pair2(const PairArgs &A, const PairDst &
 // of the CTA must call this).  Diagonal blocks of symmetric mode (H_sym[a][b] =
 // H[min(a,b)][max(a,b)]): entries with a <= b come from row a, a > b from
 // column a.  Lane (r, q) of warp w holds H[m0 + r][8j + 2q + e].
+// bench_pair_tile: the partials of one 8-row slab (rows m0..m0+7, slab index
+// `slab` = m0 / 8) -- a row's by its lane quad into rowp, a column's by the 8
+// lanes of a tile column into colp[slab]; bench_pair_finish: the per-row sums
+// over the slabs in slab order (every thread of the CTA calls both).
+template <int NP, int TN>
+__device__ __forceinline__ void bench_pair_tile(const PairArgs &A, const PairDst &D, int t, int s,
+                                                const double (&H)[TN][2], int m0, int slab, double2 *colp,
+                                                double2 *rowp) {
+  const int lane = threadIdx.x & 31, r = lane >> 2, q = lane & 3;
+  const int row = m0 + r, a = row - D.kt;
+  const bool vrow = row >= D.kt && row < D.nt;
+  const bool cols = D.dsym || D.s_dst_m >= 0;   // CTA-uniform
+  const double *w_s = A.bw + A.cs.s_off[s];      // weights of block (t, s)'s columns
+  const double wa = (vrow && cols) ? __ldg(A.bw + A.cs.s_off[t] + a) : 0.0;  // weight of mirror column a
+  double ry = 0.0, rr = 0.0;
+#pragma unroll
+  for (int j = 0; j < TN; j++) {
+    double cy[2], cr[2];
+#pragma unroll
+    for (int e = 0; e < 2; e++) {
+      const int col = j * 8 + 2 * q + e, b = col - D.ks;
+      const bool v = vrow && col >= D.ks && col < D.ns;
+      const double h = H[j][e];
+      if (v && D.s_dst >= 0 && (!D.dsym || a <= b)) {
+        ry = fma(h, __ldg(w_s + b), ry);
+        rr = fma(h, h, rr);
+      }
+      const bool cc = v && (D.dsym ? a < b : true);
+      cy[e] = cc ? h * wa : 0.0;
+      cr[e] = cc ? h * h : 0.0;
+    }
+    if (cols) {
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1)
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          cy[e] += __shfl_xor_sync(0xffffffffu, cy[e], o);
+          cr[e] += __shfl_xor_sync(0xffffffffu, cr[e], o);
+        }
+      if (r == 0) {
+        colp[slab * NP + j * 8 + 2 * q] = make_double2(cy[0], cr[0]);
+        colp[slab * NP + j * 8 + 2 * q + 1] = make_double2(cy[1], cr[1]);
+      }
+    }
+  }
+  ry += __shfl_xor_sync(0xffffffffu, ry, 1);
+  rr += __shfl_xor_sync(0xffffffffu, rr, 1);
+  ry += __shfl_xor_sync(0xffffffffu, ry, 2);
+  rr += __shfl_xor_sync(0xffffffffu, rr, 2);
+  if (q == 0) rowp[row] = make_double2(ry, rr);
+}
+
+template <int NP, int SLABS>
+__device__ __forceinline__ void bench_pair_finish(const PairArgs &A, const PairDst &D, const double2 *colp,
+                                                  const double2 *rowp) {
+  __syncthreads();
+  for (int i = threadIdx.x; i < NP; i += blockDim.x) {
+    if (D.s_dst >= 0 && i >= D.kt && i < D.nt) {  // row i - kt of block (t, s)
+      double2 v = rowp[i];
+      if (D.dsym)
+#pragma unroll
+        for (int w_ = 0; w_ < SLABS; w_++) {
+          v.x += colp[w_ * NP + i].x;
+          v.y += colp[w_ * NP + i].y;
+        }
+      A.part[D.s_dst + int64_t(i - D.kt) * D.s_ld] = v;
+    }
+    if (!D.dsym && D.s_dst_m >= 0 && i >= D.ks && i < D.ns) {  // row i - ks of the mirror block (s, t)
+      double2 v = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int w_ = 0; w_ < SLABS; w_++) {
+        v.x += colp[w_ * NP + i].x;
+        v.y += colp[w_ * NP + i].y;
+      }
+      A.part[D.s_dst_m + int64_t(i - D.ks) * D.s_ld_m] = v;
+    }
+  }
+  __syncthreads();
+}
+
 template <int NP, int TN, int WARPS>
 __device__ __forceinline__ void bench_pair(const PairArgs &A, const PairDst &D, int t, int s, const double (&H)[TN][2],
                                            int m0, double2 *scratch, double2 *rowp_ = nullptr) {
@@ -3081,6 +3161,12 @@ __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const dou
   __syncthreads();
   while (true) {
     const int n = m_n[level], k = m_k[level];
+    if (level < L) {  // the parent's Q into L2 now: the CTA that climbs reads it after the arrival
+      const int np = m_n[level + 1];
+      const double *Qp = q + m_q[level + 1];
+      for (int e = threadIdx.x * 16; e < np * np; e += blockDim.x * 16)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(Qp + e));
+    }
     if (n > 0) {
       const double *Q = q + m_q[level];
       const int k1 = level > 0 ? m_k1[level] : 0;
@@ -3102,7 +3188,7 @@ __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const dou
           double acc[APPLY_RC];
 #pragma unroll
           for (int rr = 0; rr < APPLY_RC; rr++) acc[rr] = 0.0;
-#pragma unroll 4
+#pragma unroll 8
           for (int i = h; i < n; i += H) {
             const double qv = __ldg(Q + int64_t(i) * n + j);
 #pragma unroll
@@ -3197,7 +3283,7 @@ __global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, const doub
         for (int rr = 0; rr < APPLY_RC; rr++) acc[rr] = 0.0;
         if (il < rows) {
           const double *Qi = Q + int64_t(rlo + il) * n;
-#pragma unroll 4
+#pragma unroll 8
           for (int jj = h; jj < n; jj += H) {
             const double qv = __ldg(Qi + jj);
 #pragma unroll
