@@ -527,6 +527,41 @@ h2sp_status h2sp_gmres(const h2sp_sparsified *A, const h2sp_sparsified *M, const
                        const double *b, double *x, const h2sp_gmres_opts *opt, h2sp_gmres_info *info, void *ws,
                        size_t ws_bytes, void *stream);
 
+/* ------------------------------------------------------------------------
+ * Supernodal Cholesky of S on the device (the direct solve
+ * x = V S^-1 U^T b, Eq. sp0; the paper factorises S with CHOLMOD,
+ * P:804).  Symmetric (SPD, Proposition), unsharded,
+ * stored-S plans.  Supernodes = the row groups of S (the frozen rows of one
+ * cluster, in S's own level-major order -- no reordering); S = L L^T with L in
+ * dense row-major panels, one per supernode J: the blocks I of struct(J)
+ * (ascending, J first) stacked, (sum m_I) x m_J doubles.
+ * ------------------------------------------------------------------------ */
+typedef struct h2sp_chol_s *h2sp_chol;
+/* Host analysis from the plan's block pattern: block elimination tree,
+ * struct(J) by the supernodal symbolic factorisation, panel layout.  Outputs
+ * (HOST, may be NULL): the panel length in doubles and the device meta bytes.
+ * Errors: H2SP_EUNSUPPORTED for nonsymmetric / sharded / bench plans or a
+ * group wider than 128 rows. */
+h2sp_status h2sp_chol_analyse(h2sp_plan plan, h2sp_chol *out, int64_t *panel_doubles, int64_t *meta_bytes);
+/* Number of supernodes, elimination-tree parents [ns] (-1 = root), panel rows
+ * [ns] and the factorisation's flops (any output may be NULL). */
+h2sp_status h2sp_chol_info(h2sp_chol c, int32_t *ns, int32_t *parent, int64_t *panel_rows, double *flops);
+/* struct(J) (ascending block ids, J first): *count entries, at most cap written. */
+h2sp_status h2sp_chol_struct(h2sp_chol c, int32_t J, int32_t *blocks, int32_t cap, int32_t *count);
+/* Copy the analysis tables to a DEVICE buffer of meta_bytes (asynchronous). */
+h2sp_status h2sp_chol_upload(h2sp_chol c, void *meta, size_t meta_bytes, void *stream);
+/* Numeric factorisation of S (the stored output of h2sp_build, h2sp_csr) into
+ * `panel` (DEVICE, panel_doubles): scatter of S's lower triangle, then per
+ * supernode in order the dense Cholesky of the diagonal block, the triangular
+ * solve of the rows below and the Schur update of the later panels (64 x 64
+ * FP64 tensor-core tiles).  Synchronises the stream.  H2SP_EINVAL if a pivot
+ * is not positive (message names the supernode). */
+h2sp_status h2sp_chol_factor(h2sp_chol c, const h2sp_csr *S, const void *meta, double *panel, void *stream);
+/* x = S^-1 b = L^-T L^-1 b (S order, DEVICE; x may alias b), asynchronous. */
+h2sp_status h2sp_chol_solve(h2sp_chol c, const void *meta, const double *panel, const double *b, double *x,
+                            void *stream);
+void h2sp_chol_destroy(h2sp_chol c);
+
 #ifdef __cplusplus
 }
 #endif

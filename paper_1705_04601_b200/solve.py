@@ -193,3 +193,127 @@ def solve_lu(sp: Sparsifier, fac, b, stream=None):
     x = torch.empty_like(bt)
     sp.apply_V(y, x, stream=stream)
     return x[0]
+
+
+# ---------------------------------------------------------------------------
+# Supernodal Cholesky (libh2sp, csrc/chol.cu; include/h2sp.h h2sp_chol_*)
+# ---------------------------------------------------------------------------
+from . import _check, _stream_handle, lib  # noqa: E402
+
+_vp, _i32, _i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+lib.h2sp_chol_analyse.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_i64), ctypes.POINTER(_i64)]
+lib.h2sp_chol_info.argtypes = [_vp, ctypes.POINTER(_i32), _vp, _vp, ctypes.POINTER(ctypes.c_double)]
+lib.h2sp_chol_struct.argtypes = [_vp, _i32, _vp, _i32, ctypes.POINTER(_i32)]
+lib.h2sp_chol_upload.argtypes = [_vp, _vp, ctypes.c_size_t, _vp]
+lib.h2sp_chol_factor.argtypes = [_vp, _vp, _vp, _vp, _vp]
+lib.h2sp_chol_solve.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
+lib.h2sp_chol_destroy.argtypes = [_vp]
+lib.h2sp_chol_destroy.restype = None
+
+
+class CholAnalysis:
+    """Host analysis of S's supernodal Cholesky (h2sp_chol_analyse): the block
+    elimination tree and struct(J) of every supernode (= row group of S)."""
+
+    def __init__(self, plan):
+        import numpy as np
+        self.handle = _vp()
+        pd, mb = _i64(), _i64()
+        _check(lib.h2sp_chol_analyse(plan.handle, ctypes.byref(self.handle), ctypes.byref(pd), ctypes.byref(mb)),
+               "h2sp_chol_analyse")
+        self.panel_doubles, self.meta_bytes = int(pd.value), int(mb.value)
+        ns = _i32()
+        fl = ctypes.c_double()
+        _check(lib.h2sp_chol_info(self.handle, ctypes.byref(ns), None, None, ctypes.byref(fl)), "h2sp_chol_info")
+        self.ns, self.flops = int(ns.value), float(fl.value)
+        self.parent = np.zeros(self.ns, np.int32)
+        self.panel_rows = np.zeros(self.ns, np.int64)
+        _check(lib.h2sp_chol_info(self.handle, None, self.parent.ctypes.data, self.panel_rows.ctypes.data, None),
+               "h2sp_chol_info")
+
+    def struct(self, J: int):
+        import numpy as np
+        cnt = _i32()
+        _check(lib.h2sp_chol_struct(self.handle, J, None, 0, ctypes.byref(cnt)), "h2sp_chol_struct")
+        out = np.zeros(cnt.value, np.int32)
+        _check(lib.h2sp_chol_struct(self.handle, J, out.ctypes.data, cnt.value, ctypes.byref(cnt)), "h2sp_chol_struct")
+        return out
+
+    def __del__(self):
+        try:
+            lib.h2sp_chol_destroy(self.handle)
+        except Exception:  # noqa: BLE001
+            pass
+
+
+class CholFactor:
+    """S = L L^T on the device (h2sp_chol_factor) for the S of the last stored
+    build of a symmetric Sparsifier; solve(b) = S^-1 b in S order."""
+
+    def __init__(self, sp: Sparsifier, stream=None):
+        from .krylov import CsrMatrix
+        self.an = CholAnalysis(sp.plan)
+        dev = sp.outputs["s_val"].device
+        self.meta = torch.empty(self.an.meta_bytes + 256, dtype=torch.uint8, device=dev)
+        self.meta_ptr = (self.meta.data_ptr() + 255) // 256 * 256
+        self.panel = torch.empty(max(self.an.panel_doubles, 1), dtype=torch.float64, device=dev)
+        st = _stream_handle(stream)
+        _check(lib.h2sp_chol_upload(self.an.handle, self.meta_ptr, self.an.meta_bytes, st), "h2sp_chol_upload")
+        self.S = CsrMatrix.from_sparsifier(sp)
+        _check(lib.h2sp_chol_factor(self.an.handle, ctypes.byref(self.S.abi), self.meta_ptr, self.panel.data_ptr(), st),
+               "h2sp_chol_factor")
+
+    def solve(self, b, x=None, stream=None):
+        x = torch.empty_like(b) if x is None else x
+        _check(lib.h2sp_chol_solve(self.an.handle, self.meta_ptr, self.panel.data_ptr(), b.data_ptr(), x.data_ptr(),
+                                   _stream_handle(stream)), "h2sp_chol_solve")
+        return x
+
+    def dense_L(self, plan):
+        """Host dense L assembled from the panels (small N only; data movement)."""
+        import numpy as np
+        N = plan.N
+        off = plan.offsets()["s_off_row"]
+        an = self.an
+        P = self.panel.cpu().numpy()
+        L = np.zeros((N, N))
+        # supernode starts / sizes: the row groups, ascending
+        starts, ms = _groups(plan)
+        po = 0
+        for J in range(an.ns):
+            mJ = ms[J]
+            rows = []
+            for I in an.struct(J):
+                rows.extend(range(starts[I], starts[I] + ms[I]))
+            blk = P[po:po + len(rows) * mJ].reshape(len(rows), mJ)
+            L[np.array(rows)[:, None], np.arange(starts[J], starts[J] + mJ)[None, :]] = blk
+            po += len(rows) * mJ
+        return L
+
+
+def _groups(plan):
+    """(starts, sizes) of S's row groups (clusters with frozen rows), in S order."""
+    import numpy as np
+    off = plan.offsets()["s_off_row"]
+    N = plan.N
+    o = np.sort(np.unique(np.append(off, N)))
+    starts = o[:-1]
+    sizes = np.diff(o)
+    keep = sizes > 0
+    return starts[keep], sizes[keep]
+
+
+def factor_chol(sp: Sparsifier, stream=None) -> CholFactor:
+    """Supernodal Cholesky of the S the last build wrote (symmetric plans)."""
+    return CholFactor(sp, stream=stream)
+
+
+def solve_chol(sp: Sparsifier, fac: CholFactor, b, stream=None):
+    """x = V S^-1 U^T b (Eq. sp0) with the device supernodal Cholesky."""
+    bt = b.reshape(1, -1).contiguous()
+    y = torch.empty_like(bt)
+    sp.apply_Ut(bt, y, stream=stream)
+    fac.solve(y[0], y[0], stream=stream)
+    x = torch.empty_like(bt)
+    sp.apply_V(y, x, stream=stream)
+    return x[0]
