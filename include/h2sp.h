@@ -538,14 +538,20 @@ h2sp_status h2sp_gmres(const h2sp_sparsified *A, const h2sp_sparsified *M, const
  * ------------------------------------------------------------------------ */
 typedef struct h2sp_chol_s *h2sp_chol;
 /* Host analysis from the plan's block pattern: block elimination tree,
- * struct(J) by the supernodal symbolic factorisation, panel layout.  Outputs
- * (HOST, may be NULL): the panel length in doubles and the device meta bytes.
- * Errors: H2SP_EUNSUPPORTED for nonsymmetric / sharded / bench plans or a
- * group wider than 128 rows. */
-h2sp_status h2sp_chol_analyse(h2sp_plan plan, h2sp_chol *out, int64_t *panel_doubles, int64_t *meta_bytes);
+ * struct(J) by the supernodal symbolic factorisation, panel layout.
+ * amalgamate > 0: consecutive supernodes J, J + 1 with parent(J) = J + 1 are
+ * merged while the merged width stays <= amalgamate (<= 128) and the explicit
+ * zeros added to J's columns stay under a quarter of its rows; 0: the row
+ * groups themselves.  Outputs (HOST, may be NULL): the panel length in doubles
+ * and the device meta bytes.  Errors: H2SP_EUNSUPPORTED for nonsymmetric /
+ * sharded / bench plans or a group wider than 128 rows. */
+h2sp_status h2sp_chol_analyse(h2sp_plan plan, int amalgamate, h2sp_chol *out, int64_t *panel_doubles,
+                              int64_t *meta_bytes);
 /* Number of supernodes, elimination-tree parents [ns] (-1 = root), panel rows
  * [ns] and the factorisation's flops (any output may be NULL). */
 h2sp_status h2sp_chol_info(h2sp_chol c, int32_t *ns, int32_t *parent, int64_t *panel_rows, double *flops);
+/* First S row of every supernode and n: start[ns + 1] (HOST). */
+h2sp_status h2sp_chol_supernodes(h2sp_chol c, int64_t *start);
 /* struct(J) (ascending block ids, J first): *count entries, at most cap written. */
 h2sp_status h2sp_chol_struct(h2sp_chol c, int32_t J, int32_t *blocks, int32_t cap, int32_t *count);
 /* Copy the analysis tables to a DEVICE buffer of meta_bytes (asynchronous). */

@@ -204,12 +204,27 @@ __global__ void __launch_bounds__(256) chol_schur_kernel(CholMeta M, double *pan
   const bool diag = ti == tk;
   const double *P = panel + M.poff[J] + int64_t(m) * m;  // below rows
   const int32_t *blk = M.blk + M.roff[J] + m, *grow = M.grow + M.roff[J] + m;
+  // stage the two row blocks with 8-byte async copies (one round trip)
   for (int e = threadIdx.x; e < ST * m4; e += blockDim.x) {
     const int r = e / m4, k = e % m4;
     const int ra = ti * ST + r, rb = tk * ST + r;
-    sA[r * ldk + k] = (ra < R && k < m) ? P[int64_t(ra) * m + k] : 0.0;
-    if (!diag) sB[r * ldk + k] = (rb < R && k < m) ? P[int64_t(rb) * m + k] : 0.0;
+    double *da = &sA[r * ldk + k];
+    if (ra < R && k < m) {
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(unsigned(__cvta_generic_to_shared(da))),
+                   "l"(P + int64_t(ra) * m + k));
+    } else {
+      *da = 0.0;
+    }
+    if (!diag) {
+      double *db = &sB[r * ldk + k];
+      if (rb < R && k < m)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(unsigned(__cvta_generic_to_shared(db))),
+                     "l"(P + int64_t(rb) * m + k));
+      else
+        *db = 0.0;
+    }
   }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
   for (int r = threadIdx.x; r < ST; r += blockDim.x) {
     const int ra = ti * ST + r, rb = tk * ST + r;
     if (ra < R) {
@@ -221,6 +236,7 @@ __global__ void __launch_bounds__(256) chol_schur_kernel(CholMeta M, double *pan
       ck[r] = grow[rb] - int32_t(M.start[cK[r]]);
     }
   }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   const double *B = diag ? sA : sB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, r = lane >> 2, q = lane & 3;
@@ -242,22 +258,38 @@ __global__ void __launch_bounds__(256) chol_schur_kernel(CholMeta M, double *pan
 #pragma unroll
       for (int j = 0; j < 4; j++) dmma(acc[i][j], a[i], b[j]);
   }
+  // epilogue in three batches of independent loads: block offsets, targets, stores
+  int32_t pv[2][4][2];
 #pragma unroll
-  for (int i = 0; i < 2; i++) {
-    const int lr = m0 + 8 * i + r, ra = ti * ST + lr;
-    if (ra >= R) continue;
-    const int32_t I = rI[lr], il = ri[lr];
+  for (int i = 0; i < 2; i++)
 #pragma unroll
     for (int j = 0; j < 4; j++)
 #pragma unroll
       for (int e = 0; e < 2; e++) {
-        const int lc = n0 + 8 * j + 2 * q + e, rb = tk * ST + lc;
-        if (rb >= R || rb > ra) continue;
-        const int32_t K = cK[lc];
-        const int64_t dst = M.poff[K] + int64_t(__ldg(M.pos + int64_t(K) * M.ns + I) + il) * M.m[K] + ck[lc];
-        panel[dst] -= acc[i][j][e];
+        const int lr = m0 + 8 * i + r, lc = n0 + 8 * j + 2 * q + e;
+        const int ra = ti * ST + lr, rb = tk * ST + lc;
+        pv[i][j][e] = (ra < R && rb <= ra) ? __ldg(M.pos + int64_t(cK[lc]) * M.ns + rI[lr]) : -1;
       }
-  }
+  int64_t dst[2][4][2];
+  double old[2][4][2];
+#pragma unroll
+  for (int i = 0; i < 2; i++)
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+#pragma unroll
+      for (int e = 0; e < 2; e++) {
+        const int lr = m0 + 8 * i + r, lc = n0 + 8 * j + 2 * q + e;
+        const int32_t K = cK[lc];
+        dst[i][j][e] = pv[i][j][e] >= 0 ? M.poff[K] + int64_t(pv[i][j][e] + ri[lr]) * M.m[K] + ck[lc] : -1;
+        old[i][j][e] = dst[i][j][e] >= 0 ? panel[dst[i][j][e]] : 0.0;
+      }
+#pragma unroll
+  for (int i = 0; i < 2; i++)
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+#pragma unroll
+      for (int e = 0; e < 2; e++)
+        if (dst[i][j][e] >= 0) panel[dst[i][j][e]] = old[i][j][e] - acc[i][j][e];
 }
 
 // Solve, per supernode J.  Forward: (1) chol_diag_kernel<false>: x_J =
@@ -376,6 +408,28 @@ size_t schur_smem(int m) {
   return size_t(2) * ST * ldk * sizeof(double);
 }
 
+// supernodal symbolic factorisation: struct(J) = A's column J (lower) U {J}
+// U the structures of J's children minus themselves; parent(J) = the
+// smallest block of struct(J) below J
+void symbolic(int32_t ns, const std::vector<std::vector<int32_t>> &acol, std::vector<int32_t> &parent,
+              std::vector<std::vector<int32_t>> &st) {
+  parent.assign(ns, -1);
+  st.assign(ns, {});
+  std::vector<std::vector<int32_t>> children(ns);
+  for (int32_t J = 0; J < ns; J++) {
+    std::vector<int32_t> s = acol[J];
+    s.push_back(J);
+    for (int32_t ch : children[J]) s.insert(s.end(), st[ch].begin() + 1, st[ch].end());
+    std::sort(s.begin(), s.end());
+    s.erase(std::unique(s.begin(), s.end()), s.end());
+    st[J] = std::move(s);
+    if (st[J].size() > 1) {
+      parent[J] = st[J][1];
+      children[parent[J]].push_back(J);
+    }
+  }
+}
+
 template <typename T>
 size_t put(std::vector<unsigned char> &img, const std::vector<T> &v) {
   const size_t off = (img.size() + 255) & ~size_t(255);
@@ -388,7 +442,9 @@ size_t put(std::vector<unsigned char> &img, const std::vector<T> &v) {
 
 extern "C" {
 
-h2sp_status h2sp_chol_analyse(h2sp_plan P, h2sp_chol *out, int64_t *panel_doubles, int64_t *meta_bytes) {
+h2sp_status h2sp_chol_analyse(h2sp_plan P, int amalgamate, h2sp_chol *out, int64_t *panel_doubles,
+                              int64_t *meta_bytes) {
+  if (amalgamate > 128) return fail(H2SP_EINVAL, "chol: amalgamated supernodes are at most 128 wide");
   if (!P || !out) return fail(H2SP_EINVAL, "chol: NULL argument");
   *out = nullptr;
   if (!P->sym) return fail(H2SP_EUNSUPPORTED, "chol: symmetric plans only (S SPD, Proposition P:504-509)");
@@ -418,10 +474,9 @@ h2sp_status h2sp_chol_analyse(h2sp_plan P, h2sp_chol *out, int64_t *panel_double
         delete c;
         return fail(H2SP_EUNSUPPORTED, "chol: S row outside every group");
       }
-    const int32_t ns = c->ns;
-    c->mmax = ns ? *std::max_element(c->m.begin(), c->m.end()) : 0;
+    const int32_t ns0 = c->ns;
     // A's lower block pattern by column
-    std::vector<std::vector<int32_t>> acol(ns);
+    std::vector<std::vector<int32_t>> acol(ns0);
     for (int64_t r = 0; r < nr; r++)
       for (int32_t j = 0; j < rows[r].nblk; j++) {
         const CsrBlock &b = blocks[rows[r].blk_begin + j];
@@ -432,24 +487,53 @@ h2sp_status h2sp_chol_analyse(h2sp_plan P, h2sp_chol *out, int64_t *panel_double
         }
         if (J <= r) acol[J].push_back(int32_t(r));
       }
-    // supernodal symbolic factorisation: struct(J) = A's column J (lower) U {J}
-    // U the structures of J's children minus themselves; parent(J) = the
-    // smallest block of struct(J) below J
-    c->parent.assign(ns, -1);
-    c->st.assign(ns, {});
-    std::vector<std::vector<int32_t>> children(ns);
-    for (int32_t J = 0; J < ns; J++) {
-      std::vector<int32_t> s = acol[J];
-      s.push_back(J);
-      for (int32_t ch : children[J]) s.insert(s.end(), c->st[ch].begin() + 1, c->st[ch].end());
-      std::sort(s.begin(), s.end());
-      s.erase(std::unique(s.begin(), s.end()), s.end());
-      c->st[J] = std::move(s);
-      if (c->st[J].size() > 1) {
-        c->parent[J] = c->st[J][1];
-        children[c->parent[J]].push_back(J);
+    symbolic(ns0, acol, c->parent, c->st);
+    // relaxed amalgamation: a supernode J whose parent is J + 1 joins it (one
+    // wider panel: one potrf / trsm / Schur pass instead of two, K = the summed
+    // width) while the merged width stays <= amalgamate and the explicit zeros
+    // it adds to J's columns (rows of struct(J + 1) not in struct(J)) stay
+    // under a quarter of J's rows; then the same symbolic factorisation on the
+    // coarser partition (its structures contain the zeros)
+    if (amalgamate > 0) {
+      auto rows_of = [&](int32_t J) {
+        int64_t r = 0;
+        for (int32_t I : c->st[J]) r += c->m[I];
+        return r;
+      };
+      std::vector<int32_t> cgrp(ns0);
+      std::vector<int64_t> cstart;
+      std::vector<int32_t> cm;
+      for (int32_t J = 0; J < ns0; J++) {
+        bool join = false;
+        if (J > 0 && c->parent[J - 1] == J && cm.back() + c->m[J] <= amalgamate) {
+          const int64_t rj = rows_of(J - 1), rp = rows_of(J);
+          join = rp + c->m[J - 1] - rj <= rj / 4;
+        }
+        if (join) {
+          cm.back() += c->m[J];
+        } else {
+          cstart.push_back(c->start[J]);
+          cm.push_back(c->m[J]);
+        }
+        cgrp[J] = int32_t(cm.size()) - 1;
       }
+      const int32_t nc = int32_t(cm.size());
+      std::vector<std::vector<int32_t>> ccol(nc);
+      for (int32_t J = 0; J < ns0; J++)
+        for (int32_t I : acol[J]) ccol[cgrp[J]].push_back(cgrp[I]);
+      for (auto &v : ccol) {
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+      }
+      for (int64_t i = 0; i < c->n; i++) sgrp[size_t(i)] = cgrp[sgrp[size_t(i)]];
+      cstart.push_back(c->n);
+      c->start = std::move(cstart);
+      c->m = std::move(cm);
+      c->ns = nc;
+      symbolic(nc, ccol, c->parent, c->st);
     }
+    const int32_t ns = c->ns;
+    c->mmax = ns ? *std::max_element(c->m.begin(), c->m.end()) : 0;
     // layout
     c->poff.assign(size_t(ns) + 1, 0);
     c->prows.assign(ns, 0);
@@ -500,6 +584,12 @@ h2sp_status h2sp_chol_info(h2sp_chol c, int32_t *ns, int32_t *parent, int64_t *p
   if (panel_rows)
     for (int32_t J = 0; J < c->ns; J++) panel_rows[J] = c->prows[J];
   if (flops) *flops = c->flops;
+  return H2SP_OK;
+}
+
+h2sp_status h2sp_chol_supernodes(h2sp_chol c, int64_t *start) {
+  if (!c || !start) return fail(H2SP_EINVAL, "chol: NULL argument");
+  std::memcpy(start, c->start.data(), c->start.size() * sizeof(int64_t));
   return H2SP_OK;
 }
 

@@ -201,9 +201,10 @@ def solve_lu(sp: Sparsifier, fac, b, stream=None):
 from . import _check, _stream_handle, lib  # noqa: E402
 
 _vp, _i32, _i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
-lib.h2sp_chol_analyse.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_i64), ctypes.POINTER(_i64)]
+lib.h2sp_chol_analyse.argtypes = [_vp, ctypes.c_int, ctypes.POINTER(_vp), ctypes.POINTER(_i64), ctypes.POINTER(_i64)]
 lib.h2sp_chol_info.argtypes = [_vp, ctypes.POINTER(_i32), _vp, _vp, ctypes.POINTER(ctypes.c_double)]
 lib.h2sp_chol_struct.argtypes = [_vp, _i32, _vp, _i32, ctypes.POINTER(_i32)]
+lib.h2sp_chol_supernodes.argtypes = [_vp, _vp]
 lib.h2sp_chol_upload.argtypes = [_vp, _vp, ctypes.c_size_t, _vp]
 lib.h2sp_chol_factor.argtypes = [_vp, _vp, _vp, _vp, _vp]
 lib.h2sp_chol_solve.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
@@ -215,12 +216,12 @@ class CholAnalysis:
     """Host analysis of S's supernodal Cholesky (h2sp_chol_analyse): the block
     elimination tree and struct(J) of every supernode (= row group of S)."""
 
-    def __init__(self, plan):
+    def __init__(self, plan, amalgamate: int = 0):
         import numpy as np
         self.handle = _vp()
         pd, mb = _i64(), _i64()
-        _check(lib.h2sp_chol_analyse(plan.handle, ctypes.byref(self.handle), ctypes.byref(pd), ctypes.byref(mb)),
-               "h2sp_chol_analyse")
+        _check(lib.h2sp_chol_analyse(plan.handle, amalgamate, ctypes.byref(self.handle), ctypes.byref(pd),
+                                     ctypes.byref(mb)), "h2sp_chol_analyse")
         self.panel_doubles, self.meta_bytes = int(pd.value), int(mb.value)
         ns = _i32()
         fl = ctypes.c_double()
@@ -230,6 +231,9 @@ class CholAnalysis:
         self.panel_rows = np.zeros(self.ns, np.int64)
         _check(lib.h2sp_chol_info(self.handle, None, self.parent.ctypes.data, self.panel_rows.ctypes.data, None),
                "h2sp_chol_info")
+        st = np.zeros(self.ns + 1, np.int64)
+        _check(lib.h2sp_chol_supernodes(self.handle, st.ctypes.data), "h2sp_chol_supernodes")
+        self.starts, self.sizes = st[:-1], np.diff(st)
 
     def struct(self, J: int):
         import numpy as np
@@ -250,9 +254,9 @@ class CholFactor:
     """S = L L^T on the device (h2sp_chol_factor) for the S of the last stored
     build of a symmetric Sparsifier; solve(b) = S^-1 b in S order."""
 
-    def __init__(self, sp: Sparsifier, stream=None):
+    def __init__(self, sp: Sparsifier, stream=None, amalgamate: int = 0):
         from .krylov import CsrMatrix
-        self.an = CholAnalysis(sp.plan)
+        self.an = CholAnalysis(sp.plan, amalgamate)
         dev = sp.outputs["s_val"].device
         self.meta = torch.empty(self.an.meta_bytes + 256, dtype=torch.uint8, device=dev)
         self.meta_ptr = (self.meta.data_ptr() + 255) // 256 * 256
@@ -277,8 +281,7 @@ class CholFactor:
         an = self.an
         P = self.panel.cpu().numpy()
         L = np.zeros((N, N))
-        # supernode starts / sizes: the row groups, ascending
-        starts, ms = _groups(plan)
+        starts, ms = an.starts, an.sizes
         po = 0
         for J in range(an.ns):
             mJ = ms[J]
@@ -303,9 +306,10 @@ def _groups(plan):
     return starts[keep], sizes[keep]
 
 
-def factor_chol(sp: Sparsifier, stream=None) -> CholFactor:
-    """Supernodal Cholesky of the S the last build wrote (symmetric plans)."""
-    return CholFactor(sp, stream=stream)
+def factor_chol(sp: Sparsifier, stream=None, amalgamate: int = 0) -> CholFactor:
+    """Supernodal Cholesky of the S the last build wrote (symmetric plans);
+    amalgamate: merged supernode width bound (0 = the row groups)."""
+    return CholFactor(sp, stream=stream, amalgamate=amalgamate)
 
 
 def solve_chol(sp: Sparsifier, fac: CholFactor, b, stream=None):

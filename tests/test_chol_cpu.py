@@ -10,8 +10,9 @@ import paper_1705_04601_b200 as h2sp
 from paper_1705_04601_b200 import solve as sv
 
 
-def _brute(plan):
-    starts, ms = sv._groups(plan)
+def _brute(plan, starts=None):
+    if starts is None:
+        starts, _ = sv._groups(plan)
     ns = len(starts)
     rp, col = plan.pattern()
     N = plan.N
@@ -38,14 +39,23 @@ CASES = [("cfg1", lambda: h2gen.make_config(1)),
          ("eta0", lambda: h2gen.eta0_h2(3, 16, 5, symmetric=True))]
 
 
+@pytest.mark.parametrize("amalg", [0, 128])
 @pytest.mark.parametrize("name,make", CASES, ids=[c[0] for c in CASES])
-def test_symbolic_matches_graph_elimination(name, make):
+def test_symbolic_matches_graph_elimination(name, make, amalg):
+    """amalg = 0: supernodes = S's row groups; 128: relaxed amalgamation -- a
+    coarser contiguous partition (merged widths <= 128, each a union of row
+    groups) whose structures are again exactly the graph elimination's."""
     plan = h2sp.Plan(h2gen.pack(make()))
-    an = sv.CholAnalysis(plan)
-    structs, parent = _brute(plan)
+    an = sv.CholAnalysis(plan, amalg)
+    g0, m0 = sv._groups(plan)
+    if amalg == 0:
+        assert np.array_equal(an.starts, g0)
+    else:
+        assert np.all(np.isin(an.starts, g0)) and an.sizes.max() <= max(128, m0.max())
+    structs, parent = _brute(plan, an.starts)
     assert an.ns == len(structs)
     assert np.array_equal(an.parent, parent)
-    starts, ms = sv._groups(plan)
+    starts, ms = an.starts, an.sizes
     for J in range(an.ns):
         s = an.struct(J)
         assert np.array_equal(s, structs[J]), J

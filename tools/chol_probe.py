@@ -23,12 +23,13 @@ sp = h2sp.Sparsifier(plan, p)
 sp.build()
 torch.cuda.synchronize()
 t = time.time()
-an = sv.CholAnalysis(plan)
+AM = int(os.environ.get("CHOL_AMALG", "0"))
+an = sv.CholAnalysis(plan, AM)
 ta = time.time() - t
-fac = sv.factor_chol(sp)
+fac = sv.factor_chol(sp, amalgamate=AM)
 torch.cuda.synchronize()
 t = time.time()
-fac = sv.factor_chol(sp)
+fac = sv.factor_chol(sp, amalgamate=AM)
 torch.cuda.synchronize()
 tf = time.time() - t
 b = torch.from_numpy(np.random.default_rng(1).standard_normal(N)).cuda()
@@ -40,7 +41,7 @@ for _ in range(3):
 torch.cuda.synchronize()
 ts = (time.time() - t) / 3
 r = oracle.h2_matvec(h, x.cpu().numpy()) - b.cpu().numpy()
-print(f"config {cfg} N={N}: S nnz {plan.sizes['s_nnz']:.3e}, supernodes {an.ns}, L panel entries "
+print(f"config {cfg} N={N} amalgamate={AM}: S nnz {plan.sizes['s_nnz']:.3e}, supernodes {an.ns}, L panel entries "
       f"{an.panel_doubles:.3e}, flops {an.flops:.3e}; analysis {ta:.2f} s, factor {tf:.3f} s "
       f"({an.flops / tf / 1e12:.2f} TFLOP/s), solve {1e3 * ts:.1f} ms, residual "
       f"{np.linalg.norm(r) / np.linalg.norm(b.cpu().numpy()):.2e}", flush=True)
