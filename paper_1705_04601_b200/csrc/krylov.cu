@@ -2,7 +2,7 @@
 // "Sparsification method as a preconditioner") and the direct
 // solve it shares its factorisation with (§8(f) #1, x = V S^-1 U^T b):
 //
-//   * ilut_kernel   -- ILUT(tau, p) of S (reading 25: Saad's
+//   * ilut_cta_kernel -- ILUT(tau, p) of S (reading 25: Saad's
 //                      Algorithm 10.6 with the dual dropping rule); tau = 0,
 //                      p < 0 is the complete LU (the direct solve).
 //   * trsv kernels  -- (L U)^-1 b by forward / backward substitution.
@@ -14,13 +14,13 @@
 //
 // ILUT on a GPU.  Row i of the factor needs the U rows of every k < i its work
 // row touches, so rows form a dependency DAG that follows the (evolving) fill.
-// One warp factorises one row at a time; rows are handed out in increasing
+// One CTA (4 warps) factorises one row at a time; rows are handed out in increasing
 // order by an atomic ticket, a row waits (acquire) on the completion flag of
 // each U row it uses and publishes its own U row (release) BEFORE it selects
 // and writes its L part -- the L part is off every other row's critical path.
 // Tickets are taken only by running warps and a row waits only on smaller
 // rows, so there is no deadlock whatever the grid size.  The work row w is a
-// dense per-warp vector in HBM (touched entries only: O(row) per row) with a
+// dense per-CTA vector in HBM (touched entries only: O(row) per row) with a
 // presence bitmap in shared memory, scanned with warp ballots for "the next
 // k with w_k present" (new fill from U row k lands right of k, so one forward
 // cursor visits every k in increasing order, as the algorithm does).
@@ -109,46 +109,6 @@ __device__ __forceinline__ uint32_t word_in(const uint32_t *bits, int64_t wi, in
   return v;
 }
 
-// Compact the present entries of w in [lo, hi] (ascending column) into (ccol,
-// cval); U part (upper = true): only entries surviving the tau rule; L part:
-// every present entry (rule 1 already dropped the rest).  Chunks of 1024
-// columns: lane l reads column base + 32 q + l for q < 32 (coalesced, up to
-// 32 loads in flight), empty chunks skipped on the bitmap.  This runs on the
-// critical path (the U part before the row is published).
-__device__ int64_t gather(const uint32_t *bits, const double *w, int64_t lo, int64_t hi, bool upper, double taui,
-                          int32_t *ccol, double *cval, int lane) {
-  int64_t cnt = 0;
-  if (lo > hi) return 0;
-  const unsigned lt = (1u << lane) - 1u;
-  for (int64_t base = lo & ~int64_t(1023); base <= hi; base += 1024) {
-    const uint32_t wd = word_in(bits, (base >> 5) + lane, lo, hi);
-    if (!__ballot_sync(FULL, wd != 0)) continue;
-    double v[32];
-    uint32_t pres = 0;
-#pragma unroll
-    for (int q = 0; q < 32; q++) {
-      const uint32_t wq = __shfl_sync(FULL, wd, q);
-      const bool pq = (wq >> lane) & 1u;
-      pres |= uint32_t(pq) << q;
-      v[q] = pq ? w[base + 32 * q + lane] : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < 32; q++) {
-      const bool pq = (pres >> q) & 1u;
-      const bool keep = pq && (!upper || !(fabs(v[q]) < taui || v[q] == 0.0));
-      const unsigned m = __ballot_sync(FULL, keep);
-      if (keep) {
-        const int64_t pos = cnt + __popc(m & lt);
-        ccol[pos] = int32_t(base + 32 * q + lane);
-        cval[pos] = v[q];
-      }
-      cnt += __popc(m);
-    }
-  }
-  __syncwarp();
-  return cnt;
-}
-
 // Keep the p largest |cval| of c candidates (ties: smaller column, i.e.
 // earlier position), in place, column order preserved.  Returns the count.
 __device__ int64_t keep_largest(int32_t *ccol, double *cval, int64_t c, int p, int *hist, int lane) {
@@ -224,119 +184,194 @@ __device__ int64_t keep_largest(int32_t *ccol, double *cval, int64_t c, int p, i
   return out;
 }
 
-__device__ int64_t reserve(const IlutArgs &A, int64_t cnt, int lane) {
-  unsigned long long st = 0;
-  if (lane == 0 && cnt > 0) {
-    st = atomicAdd(A.cursor, static_cast<unsigned long long>(cnt));
-    if (int64_t(st) + cnt > A.cap) atomicOr(&A.status[0], 1);
+// ---------------------------------------------------------------------------
+// ilut_cta_kernel: one CTA of IW warps per row.  Warp 0 runs the rule-1
+// batches (lane q takes the q-th next present k and evaluates rule 1 on it;
+// every k before the first kept one is dropped at once -- their values are
+// final, no update lies between them --, the first kept one is applied and the
+// batch restarts after it; rule 1 needs only u_kk (flag >= 1), the update U row
+// k (flag >= 2), so a dropped k never waits for k's U row); a kept k's update
+// with U row k, the gathers of the U and L parts (1024-column chunks, chunk c
+// on warp c % IW, kept entries placed in chunk order through a shared-memory
+// scan) and the clean-up use all IW warps -- the U gather is on the row-to-row
+// chain whenever the next row keeps its l entry, so a row's publication comes
+// IW times sooner (one warp per row: 2.37 -> 1.30 s at N = 131,072, DESIGN 9e).
+// ---------------------------------------------------------------------------
+constexpr int IW = 4;
+
+__device__ int64_t gather_cta(const uint32_t *bits, const double *w, int64_t lo, int64_t hi, bool upper,
+                              double taui, int32_t *ccol, double *cval, int lane, int warp, int *s_cnt) {
+  int64_t cnt = 0;
+  if (lo > hi) return 0;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t g = lo & ~int64_t(1023); g <= hi; g += 1024 * IW) {
+    const int64_t base = g + 1024 * warp;
+    double v[32];
+    uint32_t keepm = 0;
+    if (base <= hi) {
+      const uint32_t wd = word_in(bits, (base >> 5) + lane, lo, hi);
+      if (__ballot_sync(FULL, wd != 0)) {
+#pragma unroll
+        for (int q = 0; q < 32; q++) {
+          const uint32_t wq = __shfl_sync(FULL, wd, q);
+          const bool pq = (wq >> lane) & 1u;
+          v[q] = pq ? w[base + 32 * q + lane] : 0.0;
+          if (pq && (!upper || !(fabs(v[q]) < taui || v[q] == 0.0))) keepm |= 1u << q;
+        }
+      }
+    }
+    int mine = 0;
+#pragma unroll
+    for (int q = 0; q < 32; q++) mine += __popc(__ballot_sync(FULL, (keepm >> q) & 1u));
+    if (lane == 0) s_cnt[warp] = mine;
+    __syncthreads();
+    int64_t off = cnt, tot = 0;
+    for (int u = 0; u < IW; u++) {
+      if (u < warp) off += s_cnt[u];
+      tot += s_cnt[u];
+    }
+    if (keepm | __ballot_sync(FULL, keepm != 0)) {
+#pragma unroll
+      for (int q = 0; q < 32; q++) {
+        const bool kq = (keepm >> q) & 1u;
+        const unsigned m = __ballot_sync(FULL, kq);
+        if (kq) {
+          const int64_t pos = off + __popc(m & lt);
+          ccol[pos] = int32_t(base + 32 * q + lane);
+          cval[pos] = v[q];
+        }
+        off += __popc(m);
+      }
+    }
+    cnt += tot;
+    __syncthreads();
   }
-  st = __shfl_sync(FULL, st, 0);
-  return int64_t(st);
+  return cnt;
 }
 
-__global__ void __launch_bounds__(256) ilut_kernel(IlutArgs A, int warps_per_cta) {
+__global__ void __launch_bounds__(32 * IW) ilut_cta_kernel(IlutArgs A) {
   extern __shared__ uint32_t smem[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (wid >= warps_per_cta) return;
-  uint32_t *bits = smem + size_t(wid) * A.nwords;
-  int *hist = reinterpret_cast<int *>(smem + size_t(warps_per_cta) * A.nwords) + 288 * wid;
-  int32_t *kbuf = hist + 256;  // the batch's columns
-  const int64_t slot = int64_t(blockIdx.x) * warps_per_cta + wid;
+  uint32_t *bits = smem;
+  int *hist = reinterpret_cast<int *>(smem + A.nwords);
+  int32_t *kbuf = hist + 256;
+  __shared__ int s_cnt[IW];
+  __shared__ long long s_row, s_kf, s_st;
+  __shared__ double s_wkf, s_taui;
+  __shared__ int s_lo, s_hi;
+  __shared__ long long s_c;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t slot = blockIdx.x;
   double *w = A.w + slot * A.n;
   int32_t *ccol = A.ccol + slot * A.n;
   double *cval = A.cval + slot * A.n;
-  for (int i = lane; i < A.nwords; i += 32) bits[i] = 0;
-  __syncwarp();
+  for (int i = tid; i < A.nwords; i += blockDim.x) bits[i] = 0;
+  __syncthreads();
   for (;;) {
-    unsigned long long row = 0;
-    if (lane == 0) row = atomicAdd(A.ticket, 1ull);
-    const int64_t i = int64_t(__shfl_sync(FULL, row, 0));
+    if (tid == 0) s_row = static_cast<long long>(atomicAdd(A.ticket, 1ull));
+    __syncthreads();
+    const int64_t i = s_row;
     if (i >= A.n) break;
     const int64_t e0 = A.rp[i], e1 = A.rp[i + 1];
-    // tau_i = tau * ||a_i||_2, the sum of squares in column order
-    double taui = 0.0;
-    if (lane == 0) {
-      double s = 0.0;
-      for (int64_t e = e0; e < e1; e++) s = __dadd_rn(s, __dmul_rn(A.av[e], A.av[e]));
-      taui = __dmul_rn(A.tau, sqrt(s));
+    if (tid == 0) {  // tau_i = tau * ||a_i||_2, the sum of squares in column order
+      double sq = 0.0;
+      for (int64_t e = e0; e < e1; e++) sq = __dadd_rn(sq, __dmul_rn(A.av[e], A.av[e]));
+      s_taui = __dmul_rn(A.tau, sqrt(sq));
+      s_lo = int(i);
+      s_hi = int(i);
     }
-    taui = __shfl_sync(FULL, taui, 0);
-    int64_t lo = i, hi = i;
-    for (int64_t e = e0 + lane; e < e1; e += 32) {
-      const int32_t j = A.ci[e];
-      w[j] = A.av[e];
-      atomicOr(&bits[j >> 5], 1u << (j & 31));
-      lo = min(lo, int64_t(j));
-      hi = max(hi, int64_t(j));
+    __syncthreads();
+    {
+      int lo = int(i), hi = int(i);
+      for (int64_t e = e0 + tid; e < e1; e += blockDim.x) {
+        const int32_t j = A.ci[e];
+        w[j] = A.av[e];
+        atomicOr(&bits[j >> 5], 1u << (j & 31));
+        lo = min(lo, j);
+        hi = max(hi, j);
+      }
+      atomicMin(&s_lo, lo);
+      atomicMax(&s_hi, hi);
     }
-    for (int o = 16; o; o >>= 1) {
-      lo = min(lo, __shfl_xor_sync(FULL, lo, o));
-      hi = max(hi, __shfl_xor_sync(FULL, hi, o));
-    }
-    __syncwarp();
-    // for k < i with w_k present, in increasing k -- 32 at a time: lane q takes
-    // the q-th next present k and evaluates rule 1 on it; every k before the
-    // first kept one is dropped at once (their values are final: no update
-    // lies between them), the first kept one is applied, and the batch restarts
-    // after it.  Rule 1 needs only u_kk (flag >= 1); the update needs U row k
-    // (flag >= 2) -- a dropped k never waits for k's U row.
-    for (int64_t cur = lo; cur < i;) {
-      const int64_t wi0 = cur >> 5, wi = wi0 + lane;
-      const int64_t wend = (i + 31) >> 5;
-      const uint32_t wd = wi < wend ? word_in(bits, wi, cur, i - 1) : 0u;
-      const int c = __popc(wd);
-      int excl = c;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(FULL, excl, o);
-        if (lane >= o) excl += y;
+    __syncthreads();
+    const int64_t lo = s_lo;
+    const double taui = s_taui;
+    int64_t cur = lo;  // warp 0's cursor
+    for (;;) {
+      if (warp == 0) {  // rule-1 batches until a kept k (or the end)
+        long long kf_out = -1;
+        double wkf_out = 0.0;
+        while (cur < i) {
+          const int64_t wi0 = cur >> 5, wi = wi0 + lane;
+          const int64_t wend = (i + 31) >> 5;
+          const uint32_t wd = wi < wend ? word_in(bits, wi, cur, i - 1) : 0u;
+          const int c = __popc(wd);
+          int excl = c;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, excl, o);
+            if (lane >= o) excl += y;
+          }
+          const int total = __shfl_sync(FULL, excl, 31);
+          excl -= c;
+          if (total == 0) {
+            cur = (wi0 + 32) << 5;
+            continue;
+          }
+          {
+            int r = excl;
+            for (uint32_t t = wd; t && r < 32; t &= t - 1, r++) kbuf[r] = int32_t((wi << 5) + __ffs(t) - 1);
+          }
+          __syncwarp();
+          const int nk = min(total, 32);
+          const int64_t k = lane < nk ? int64_t(kbuf[lane]) : -1;
+          bool drop = true;
+          double wk = 0.0;
+          if (k >= 0) {
+            wait_flag(A.done + k, 1);
+            wk = __ddiv_rn(w[k], __ldcg(A.diag + k));
+            drop = fabs(wk) < taui || wk == 0.0;  // rule 1
+          }
+          const unsigned kept = __ballot_sync(FULL, !drop);
+          const int f = kept ? __ffs(kept) - 1 : nk;
+          __syncwarp();
+          if (lane < f && k >= 0) {
+            w[k] = 0.0;
+            atomicAnd(&bits[k >> 5], ~(1u << (k & 31)));
+          }
+          if (f == nk) {
+            cur = total > 32 ? int64_t(__shfl_sync(FULL, k, 31)) + 1 : int64_t((wi0 + 32) << 5);
+            __syncwarp();
+            continue;
+          }
+          const int64_t kf = __shfl_sync(FULL, k, f);
+          const double wkf = __shfl_sync(FULL, wk, f);
+          if (lane == f) {
+            w[kf] = wkf;
+            wait_flag(A.done + kf, 2);
+          }
+          __syncwarp();
+          kf_out = kf;
+          wkf_out = wkf;
+          cur = kf + 1;
+          break;
+        }
+        if (lane == 0) {
+          s_kf = kf_out;
+          s_wkf = wkf_out;
+        }
       }
-      const int total = __shfl_sync(FULL, excl, 31);
-      excl -= c;
-      if (total == 0) {
-        cur = (wi0 + 32) << 5;
-        continue;
-      }
-      {  // scatter the first 32 present columns to kbuf in order
-        int r = excl;
-        for (uint32_t t = wd; t && r < 32; t &= t - 1, r++) kbuf[r] = int32_t((wi << 5) + __ffs(t) - 1);
-      }
-      __syncwarp();
-      const int nk = min(total, 32);
-      const int64_t k = lane < nk ? int64_t(kbuf[lane]) : -1;
-      bool drop = true;
-      double wk = 0.0;
-      if (k >= 0) {
-        wait_flag(A.done + k, 1);
-        wk = __ddiv_rn(w[k], __ldcg(A.diag + k));
-        drop = fabs(wk) < taui || wk == 0.0;  // rule 1
-      }
-      const unsigned kept = __ballot_sync(FULL, !drop);
-      const int f = kept ? __ffs(kept) - 1 : nk;
-      __syncwarp();
-      if (lane < f && k >= 0) {
-        w[k] = 0.0;
-        atomicAnd(&bits[k >> 5], ~(1u << (k & 31)));
-      }
-      if (f == nk) {  // the whole batch dropped
-        cur = total > 32 ? int64_t(__shfl_sync(FULL, k, 31)) + 1 : int64_t((wi0 + 32) << 5);
-        __syncwarp();
-        continue;
-      }
-      const int64_t kf = __shfl_sync(FULL, k, f);
-      const double wkf = __shfl_sync(FULL, wk, f);
-      if (lane == f) {
-        w[kf] = wkf;
-        wait_flag(A.done + kf, 2);
-      }
-      __syncwarp();
+      __syncthreads();
+      const int64_t kf = s_kf;
+      if (kf < 0) break;
+      const double wkf = s_wkf;
       const int64_t us = __ldcg(A.u_start + kf);
       const int32_t ul = __ldcg(A.u_len + kf);
-      for (int32_t e0 = 0; e0 < ul; e0 += 128) {  // four entries per lane in flight
+      int hi = 0;
+      for (int32_t e0u = 0; e0u < ul; e0u += 4 * 32 * IW) {
         int32_t j[4];
         double u[4], x[4];
 #pragma unroll
         for (int q = 0; q < 4; q++) {
-          const int32_t e = e0 + 32 * q + lane;
+          const int32_t e = e0u + 32 * IW * q + tid;
           j[q] = e < ul ? __ldcg(A.pool_col + us + e) : -1;
           u[q] = e < ul ? __ldcg(A.pool_val + us + e) : 0.0;
         }
@@ -347,32 +382,47 @@ __global__ void __launch_bounds__(256) ilut_kernel(IlutArgs A, int warps_per_cta
           if (j[q] >= 0) {
             w[j[q]] = __dsub_rn(x[q], __dmul_rn(wkf, u[q]));
             atomicOr(&bits[j[q] >> 5], 1u << (j[q] & 31));
-            hi = max(hi, int64_t(j[q]));
+            hi = max(hi, j[q]);
           }
       }
-      cur = kf + 1;
-      __syncwarp();
+      atomicMax(&s_hi, hi);
+      __syncthreads();
     }
-    // u_ii is final: publish it (flag 1) before the U row (flag 2)
-    if (lane == 0) {
+    const int64_t hi = s_hi;
+    if (tid == 0) {  // u_ii is final: publish it (flag 1)
       A.diag[i] = w[i];
       __threadfence();
       st_release(A.done + i, 1);
     }
-    for (int o = 16; o; o >>= 1) hi = max(hi, __shfl_xor_sync(FULL, hi, o));
-    // rule 2, U part; publish U row i and u_ii first
-    int64_t cu = gather(bits, w, i + 1, hi, true, taui, ccol, cval, lane);
-    cu = keep_largest(ccol, cval, cu, A.p, hist, lane);
-    int64_t st = reserve(A, cu, lane);
-    const bool fits = st + cu <= A.cap;
+    // rule 2, U part
+    int64_t cu = gather_cta(bits, w, i + 1, hi, true, taui, ccol, cval, lane, warp, s_cnt);
+    if (A.p >= 0 && cu > A.p) {
+      if (warp == 0) {
+        const int64_t kept = keep_largest(ccol, cval, cu, A.p, hist, lane);
+        if (lane == 0) s_c = kept;
+      }
+      __syncthreads();
+      cu = s_c;
+    }
+    if (tid == 0) {
+      unsigned long long st = 0;
+      if (cu > 0) {
+        st = atomicAdd(A.cursor, static_cast<unsigned long long>(cu));
+        if (int64_t(st) + cu > A.cap) atomicOr(&A.status[0], 1);
+      }
+      s_st = static_cast<long long>(st);
+    }
+    __syncthreads();
+    int64_t st = s_st;
+    bool fits = st + cu <= A.cap;
     if (fits)
-      for (int64_t a = lane; a < cu; a += 32) {
+      for (int64_t a = tid; a < cu; a += blockDim.x) {
         A.pool_col[st + a] = ccol[a];
         A.pool_val[st + a] = cval[a];
       }
-    const double uii = w[i];
-    __syncwarp();
-    if (lane == 0) {
+    __syncthreads();
+    if (tid == 0) {
+      const double uii = w[i];
       A.u_start[i] = st;
       A.u_len[i] = fits ? int32_t(cu) : 0;
       if (uii == 0.0) {
@@ -383,22 +433,37 @@ __global__ void __launch_bounds__(256) ilut_kernel(IlutArgs A, int warps_per_cta
       st_release(A.done + i, 2);
     }
     // L part (kept entries of rule 1)
-    int64_t cl = gather(bits, w, lo, i - 1, false, taui, ccol, cval, lane);
-    cl = keep_largest(ccol, cval, cl, A.p, hist, lane);
-    st = reserve(A, cl, lane);
-    const bool lfits = st + cl <= A.cap;
-    if (lfits)
-      for (int64_t a = lane; a < cl; a += 32) {
+    int64_t cl = gather_cta(bits, w, lo, i - 1, false, taui, ccol, cval, lane, warp, s_cnt);
+    if (A.p >= 0 && cl > A.p) {
+      if (warp == 0) {
+        const int64_t kept = keep_largest(ccol, cval, cl, A.p, hist, lane);
+        if (lane == 0) s_c = kept;
+      }
+      __syncthreads();
+      cl = s_c;
+    }
+    if (tid == 0) {
+      unsigned long long st2 = 0;
+      if (cl > 0) {
+        st2 = atomicAdd(A.cursor, static_cast<unsigned long long>(cl));
+        if (int64_t(st2) + cl > A.cap) atomicOr(&A.status[0], 1);
+      }
+      s_st = static_cast<long long>(st2);
+    }
+    __syncthreads();
+    st = s_st;
+    fits = st + cl <= A.cap;
+    if (fits)
+      for (int64_t a = tid; a < cl; a += blockDim.x) {
         A.pool_col[st + a] = ccol[a];
         A.pool_val[st + a] = cval[a];
       }
-    if (lane == 0) {
+    if (tid == 0) {
       A.l_start[i] = st;
-      A.l_len[i] = lfits ? int32_t(cl) : 0;
+      A.l_len[i] = fits ? int32_t(cl) : 0;
     }
-    // clear the touched range of w and the bitmap
-    __syncwarp();
-    for (int64_t base = lo & ~int64_t(255); base <= hi; base += 256) {
+    // clear the touched range of w, then the bitmap
+    for (int64_t base = (lo & ~int64_t(255)) + 256 * warp; base <= hi; base += 256 * IW) {
       const int64_t wi = (base >> 5) + (lane & 7);
       const uint32_t wd = lane < 8 ? word_in(bits, wi, lo, hi) : 0u;
       if (!__ballot_sync(FULL, wd != 0)) continue;
@@ -406,9 +471,9 @@ __global__ void __launch_bounds__(256) ilut_kernel(IlutArgs A, int warps_per_cta
       for (int q = 0; q < 8; q++)
         if ((__shfl_sync(FULL, wd, q) >> lane) & 1u) w[base + 32 * q + lane] = 0.0;
     }
-    __syncwarp();
-    for (int64_t wi = (lo >> 5) + lane; wi <= (hi >> 5); wi += 32) bits[wi] = 0;
-    __syncwarp();
+    __syncthreads();
+    for (int64_t wi = (lo >> 5) + tid; wi <= (hi >> 5); wi += blockDim.x) bits[wi] = 0;
+    __syncthreads();
   }
 }
 
@@ -646,15 +711,13 @@ struct IlutCfg {
   int64_t slots;
 };
 
-IlutCfg ilut_cfg(int64_t n) {
+IlutCfg ilut_cfg(int64_t n) {  // ilut_cta_kernel: one row per CTA of IW warps, 2 CTAs per SM
   IlutCfg c{};
   c.nwords = int((n + 31) / 32);
-  const size_t per_warp = size_t(c.nwords) * 4 + 288 * 4;
-  c.warps = int(std::max<size_t>(1, std::min<size_t>(8, (200u << 10) / per_warp)));
-  c.smem = per_warp * c.warps;
-  const int per_sm = std::max(1, 8 / c.warps);
-  c.ctas = num_sms() * per_sm;
-  c.slots = int64_t(c.ctas) * c.warps;
+  c.warps = IW;
+  c.smem = size_t(c.nwords) * 4 + 288 * 4;
+  c.ctas = num_sms() * 2;
+  c.slots = c.ctas;
   return c;
 }
 
@@ -796,8 +859,8 @@ h2sp_status h2sp_ilut(const h2sp_csr *A, double tau, int p, h2sp_ilut_factors *F
   a.w = s.w;
   a.ccol = s.ccol;
   a.cval = s.cval;
-  KCK(cudaFuncSetAttribute(ilut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(c.smem)));
-  ilut_kernel<<<c.ctas, 32 * c.warps, c.smem, st>>>(a, c.warps);
+  KCK(cudaFuncSetAttribute(ilut_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(c.smem)));
+  ilut_cta_kernel<<<c.ctas, 32 * IW, c.smem, st>>>(a);
   KCK(cudaGetLastError());
   unsigned long long used = 0;
   int32_t status[2];

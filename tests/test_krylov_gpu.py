@@ -52,6 +52,8 @@ CASES = [
     (64, 33, 6, 0.08, 4.0, 0.2, 2e-2, 12),  # rows span several bitmap words, ragged
     (150, 24, 7, 0.05, 6.0, 0.2, 1e-2, 40),  # n = 3600: more rows than warps
     (150, 24, 8, 0.05, 6.0, 0.2, 0.0, -1),   # complete LU with fill
+    (160, 64, 11, 0.25, 8.0, 0.2, 1e-2, -1),  # n = 10240, rows spanning several 4096-column gather groups
+    (160, 64, 12, 0.25, 8.0, 0.2, 1e-3, 30),
 ]
 
 
@@ -97,6 +99,25 @@ def test_ilut_pool_retry_and_zero_pivot():
     S = sps.csr_matrix(A)
     with pytest.raises(H2spError, match="zero pivot at row 0"):
         _gpu_ilut(S.indptr.astype(np.int64), S.indices.astype(np.int32), S.data, 0.0, -1)
+
+
+def test_ilut_on_S_repeatable():
+    """ILUT of a real S (Example mat1, N = 8192, the GPU's S): bitwise the same
+    factors on two runs, and bitwise those of the oracle's ILUT of the same
+    (host-copied) S -- the oracle here is fed the CUDA path's S only to check
+    the factorisation step in isolation."""
+    _need_gpu()
+    from paper_1705_04601_b200 import krylov as kr
+    sp = _sparsify_gpu(h2gen.make_ifmm(8192, 1e-2, 64, 8))
+    S = kr.CsrMatrix.from_sparsifier(sp)
+    F1 = kr.IlutFactors(S, 1e-3, -1)
+    F2 = kr.IlutFactors(S, 1e-3, -1)
+    a, b = F1.to_csr(), F2.to_csr()
+    for u, v in zip(a, b):
+        assert np.array_equal(np.asarray(u).view(np.uint8), np.asarray(v).view(np.uint8))
+    nnz = int(S.col.numel())
+    ref = okr.ilut(S.rowptr.cpu().numpy(), S.col.cpu().numpy(), S.val[:nnz].cpu().numpy(), 1e-3, -1)
+    _assert_bitwise(F1, ref)
 
 
 def test_ilu_solve_and_spmv():
