@@ -2164,11 +2164,6 @@ __global__ void __launch_bounds__(PairWy128Cfg<KP>::THREADS, 1) pair_wy128_kerne
       cp_wait_all();
     }
     __syncthreads();
-    GenCol gc;
-    if (gnext) {
-      const PairItem &nx = s_it[p + 1 - ch.begin];
-      gc = gen_col(A.gen, nx.t, nx.s, nx.nt, nx.ns, A.B, threadIdx.x & 127);
-    }
     // ---- step 3: R = T1 V_s (8 x KP per warp)
     double R[2][KP / 8][2];
 #pragma unroll
@@ -2182,13 +2177,6 @@ __global__ void __launch_bounds__(PairWy128Cfg<KP>::THREADS, 1) pair_wy128_kerne
       const double a = (q & 1) ? e1 : e0;
 #pragma unroll
       for (int i = 0; i < KP / 8; i++) dmma(R[(k0 >> 2) & 1][i], a, sV[(k0 + q) * LDV + i * 8 + r]);
-    }
-    // G of pair p+1 (512 threads x 32 rows = the 128 x 128 entries) in a rolled loop
-    // after the DMMAs: the evaluations share the FP64 datapath with them anyway, and
-    // inlining one per unrolled k-step made the kernel 188 KB of code (i-cache misses)
-    if (gnext) {
-#pragma unroll 2
-      for (int gi = threadIdx.x >> 7; gi < 128; gi += 4) sG[gi * LD + gc.j] = gen_entry_s(A.gen, gc, gi, s_xt, s_tab);
     }
 #pragma unroll
     for (int i = 0; i < KP / 8; i++) {
@@ -2205,6 +2193,17 @@ __global__ void __launch_bounds__(PairWy128Cfg<KP>::THREADS, 1) pair_wy128_kerne
       const double a = -((q & 1) ? e1 : e0);
 #pragma unroll
       for (int j = 0; j < TN; j++) dmma(H[j], a, sM[(k0 + q) * LD + j * 8 + r]);
+    }
+    // G of pair p+1 (512 threads x 32 rows = the 128 x 128 entries) in a rolled loop
+    // after step 4, where R is dead (after step 3, with R and H live, the kernel
+    // spilled at 128 registers); the evaluations share the FP64 datapath with the
+    // DMMA anyway, and inlining one per unrolled k-step made the kernel 188 KB of
+    // code (i-cache misses)
+    if (gnext) {
+      const PairItem &nx = s_it[p + 1 - ch.begin];
+      const GenCol gc = gen_col(A.gen, nx.t, nx.s, nx.nt, nx.ns, A.B, threadIdx.x & 127);
+#pragma unroll 2
+      for (int gi = threadIdx.x >> 7; gi < 128; gi += 4) sG[gi * LD + gc.j] = gen_entry_s(A.gen, gc, gi, s_xt, s_tab);
     }
     __syncthreads();  // every warp is done with V_s / M_s
     PairDst D;
