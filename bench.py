@@ -268,10 +268,31 @@ def run_protocol(args, rank, world, local_rank):
     import h2gen
     from paper_1705_04601_b200.protocol import ProtocolRun
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # H2SP_BENCH_SHARED_GPU=1 (plumbing test only): ranks share the visible GPUs
+    # round robin, reduce over gloo, and skip libh2sp's NCCL communicator (NCCL
+    # refuses two ranks on one device); every rank still times its own shards
+    shared = os.environ.get("H2SP_BENCH_SHARED_GPU") == "1"
+    dev_idx = local_rank % torch.cuda.device_count() if shared else local_rank
+    torch.cuda.set_device(dev_idx)
+    dev = torch.device("cuda", dev_idx)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    red_dev = torch.device("cpu") if shared else dev
+
+    def allreduce(t, op=None):
+        if world == 1:
+            return t
+        x = t.to(red_dev)
+        if op is None:
+            dist.all_reduce(x)
+        else:
+            dist.all_reduce(x, op=op)
+        t.copy_(x.to(t.device))
+        return t
+
     V = args.virtual_shards
     if V % world:
         raise SystemExit(f"--virtual-shards {V} must be a multiple of the GPU count {world}")
@@ -315,7 +336,7 @@ def run_protocol(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(dev_idx) as clk:
         t_start.record(stream)
         for i in range(args.steps):
             step(evs[i])
@@ -325,8 +346,7 @@ def run_protocol(args, rank, world, local_rank):
         dist.barrier()
     ms = t_start.elapsed_time(t_end) / args.steps
     red = torch.tensor([ms], **f64)
-    if world > 1:
-        dist.all_reduce(red, op=dist.ReduceOp.MAX)
+    allreduce(red, dist.ReduceOp.MAX)
     ms_max = float(red.item())
     # per-launch durations (per shard, averaged over the timed steps)
     per = [np.zeros(n) for n in n_launch]
@@ -340,15 +360,19 @@ def run_protocol(args, rank, world, local_rank):
     import paper_1705_04601_b200 as h2sp
     nccl_info = None
     chk = torch.stack([run.outputs["bench_r2"].sum(), (run.outputs["bench_y"] ** 2).sum()]).contiguous()
-    try:
-        comm = h2sp.torch_comm(rank, world)
-        comm.allreduce(chk)
-        torch.cuda.synchronize()
-        nccl_info = {"comm_nranks": world, "comm_ok": True}
-    except h2sp.H2spError as exc:
-        if world > 1:
-            raise
-        nccl_info = {"comm_ok": False, "error": str(exc)[:200]}
+    if shared and world > 1:
+        allreduce(chk)
+        nccl_info = {"comm_ok": False, "note": "H2SP_BENCH_SHARED_GPU plumbing run: checks over gloo"}
+    else:
+        try:
+            comm = h2sp.torch_comm(rank, world)
+            comm.allreduce(chk)
+            torch.cuda.synchronize()
+            nccl_info = {"comm_nranks": world, "comm_ok": True}
+        except h2sp.H2spError as exc:
+            if world > 1:
+                raise
+            nccl_info = {"comm_ok": False, "error": str(exc)[:200]}
     offs = plans[0].offsets()
     loc_any = np.zeros(int(plans[0].sizes["n_clusters"]), dtype=bool)
     for p in plans:
@@ -358,8 +382,7 @@ def run_protocol(args, rank, world, local_rank):
                         sum(p.sizes["flops"] for p in plans) + apply_flops,
                         sum(p.sizes["flops_executed"] for p in plans) + apply_flops,
                         float(sum(p.sizes["s_nnz"] for p in plans))], **f64)
-    if world > 1:
-        dist.all_reduce(tot)
+    allreduce(tot)
     job_flops, job_done, job_exec, s_nnz = (float(v) for v in tot.cpu())
     value = job_flops / (ms_max * 1e-3) / 1e12
     # dominant kernel: the level-0 congruence (pair_wy128_kernel), over this rank's shards
@@ -430,8 +453,7 @@ def run_protocol(args, rank, world, local_rank):
         e1.record(stream)
         torch.cuda.synchronize()
         ems = torch.tensor([e0.elapsed_time(e1) / k_e2e], **f64)
-        if world > 1:
-            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        allreduce(ems, dist.ReduceOp.MAX)
         h2d = sum(t.numel() * 8 for t in (h_pts, h_lo, h_hi, h_w, h_b))
         d2h = sum(t.numel() * 8 for t in (h_y, h_r2, h_q, h_x))
         e2e = {"value": job_flops / (float(ems.item()) * 1e-3) / 1e12, "unit": UNIT,
@@ -514,7 +536,7 @@ def run_protocol(args, rank, world, local_rank):
                        "per_kind_level": {k: {"ms": round(v[0], 3), "tflops_exec": round(v[1] / max(v[0], 1e-9) * 1e-9, 2)}
                                           for k, v in per_level.items()},
                        "checks": {"S_frob2": float(chk[0]), "y_norm2": float(chk[1]),
-                                  "collective": "h2sp_comm_allreduce (NCCL) over all ranks"},
+                                  "collective": ("torch gloo all_reduce (shared-GPU plumbing run)" if shared and world > 1 else "h2sp_comm_allreduce (NCCL) over all ranks")},
                        "nccl": nccl_info,
                        "env": _env_knobs()},
             "roofline": roof,
@@ -554,7 +576,7 @@ def main():
                          "protocol at full size, 1-4 the stored-S path")
     ap.add_argument("--virtual-shards", type=int, default=8, help="config 5: virtual subtree shards of the matrix")
     ap.add_argument("--plan-threads", type=int, default=8, help="config 5: shard plans created in parallel")
-    ap.add_argument("--n", type=int, default=None, help="override N (smaller instance of the recipe)")
+    ap.add_argument("--n", "--points", dest="n", type=int, default=None, help="override N (smaller instance of the recipe; --points under torchrun, which claims --n)")
     ap.add_argument("--nrhs", type=int, default=1)
     ap.add_argument("--no-oracle", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
