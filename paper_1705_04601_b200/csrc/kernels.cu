@@ -879,15 +879,26 @@ __global__ void __launch_bounds__(32 * NW) qr_cta_kernel(Side sd, int nclust, co
     }
   }
   __syncthreads();
-  // ---- M = T V^T (KP x 128) -> Mm (ld LDM); G is dead
+  // ---- M = T V^T (KP x 128); G is dead.  Compact-WY output with the leaf's
+  // padded layout (wy_kp == KP, wy_n == NROW): straight from the accumulators to
+  // global (rows a >= k and columns c >= n come out zero: T and V are zero
+  // there), so the launch needs no M staging (4 instead of 2 CTAs per SM);
+  // otherwise -> Mm (ld LDM) for the explicit Q below / the padded copy.
+  const bool m_direct = Wg && wy_kp == KP && wy_n == NROW;
   for (int tile = warp; tile < KT * (NROW / 8); tile += NW) {
     const int ta = tile / (NROW / 8), tc = tile % (NROW / 8);
     double acc[2] = {0.0, 0.0};
 #pragma unroll
     for (int k0 = 0; k0 < KP; k0 += 4) dmma(acc, Tw[(ta * 8 + r) * LDT + k0 + q], Vs[(tc * 8 + r) * LDV + k0 + q]);
     __syncwarp();
-    Mm[(ta * 8 + r) * LDM + tc * 8 + 2 * q] = acc[0];
-    Mm[(ta * 8 + r) * LDM + tc * 8 + 2 * q + 1] = acc[1];
+    if (m_direct) {
+      double *Mg = Wg + wy_n * wy_kp + (ta * 8 + r) * wy_n + tc * 8 + 2 * q;
+      Mg[0] = acc[0];
+      Mg[1] = acc[1];
+    } else {
+      Mm[(ta * 8 + r) * LDM + tc * 8 + 2 * q] = acc[0];
+      Mm[(ta * 8 + r) * LDM + tc * 8 + 2 * q + 1] = acc[1];
+    }
   }
   __syncthreads();
   if (!Wg) {  // Q = I - V M (n x n) from 8 x 8 DMMA tiles, straight to global
@@ -910,10 +921,11 @@ __global__ void __launch_bounds__(32 * NW) qr_cta_kernel(Side sd, int nclust, co
     const int i = idx / wy_kp, c = idx - i * wy_kp;
     Wg[idx] = (i < n && c < k) ? Vs[i * LDV + c] : 0.0;
   }
-  for (int idx = tid; idx < wy_n * wy_kp; idx += blockDim.x) {
-    const int a = idx / wy_n, c = idx - a * wy_n;
-    Wg[wy_n * wy_kp + idx] = (a < k && c < n) ? Mm[a * LDM + c] : 0.0;
-  }
+  if (!m_direct)
+    for (int idx = tid; idx < wy_n * wy_kp; idx += blockDim.x) {
+      const int a = idx / wy_n, c = idx - a * wy_n;
+      Wg[wy_n * wy_kp + idx] = (a < k && c < n) ? Mm[a * LDM + c] : 0.0;
+    }
 }
 
 // --------------------------------------------------------------------------
@@ -3604,7 +3616,11 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
       if (k == 0 && wyo && kmax <= 32 && (nmax > 64 || qr_cta64)) {
         const int kp = kmax <= 16 ? 16 : 32;
         const int nw = nmax > 64 ? 4 : 2;
-        const size_t smem = size_t(32 * nw * (kp + 4) + kp * (kp + 4) + kp * (32 * nw + 4)) * sizeof(double);
+        // M goes straight to global when the compact-WY layout is unpadded
+        // (wy_kp == kp, wy_n == 32 nw): the M staging shrinks to the K x K Gram
+        const bool m_direct = P->wy_kp == kp && P->wy_n == 32 * nw;
+        const size_t smem = size_t(32 * nw * (kp + 4) + kp * (kp + 4) +
+                                   (m_direct ? kp * (kp + 4) : kp * (32 * nw + 4))) * sizeof(double);
 #define H2SP_QR_CTA(KP_, NW_)                                                                              \
   do {                                                                                                     \
     if (h2sp_status e_ = ensure_smem((const void *)qr_cta_kernel<KP_, NW_>, smem)) return e_;            \
