@@ -383,7 +383,9 @@ h2sp_status h2sp_build_host(h2sp_plan plan, const h2sp_inputs *host_in, const h2
                             void *stream);
 
 /* Workspace bytes for h2sp_apply_Ut / h2sp_apply_V with nrhs right-hand sides
- * (meta region + basis-coefficient buffer).  The build workspace may be reused
+ * (meta region, then one half per direction -- basis coefficients and the
+ * arrival counters of U^T b; basis coefficients, cluster flags and the ticket of
+ * V y -- so the two applies may run side by side).  The build workspace may be reused
  * when it is at least this large (after the build has completed on the
  * stream); it must have been uploaded with h2sp_plan_upload. */
 int64_t h2sp_apply_ws_bytes(h2sp_plan plan, int nrhs);
@@ -397,8 +399,9 @@ int64_t h2sp_apply_ws_bytes(h2sp_plan plan, int nrhs);
 h2sp_status h2sp_apply_Ut(h2sp_plan plan, const double *q_row, const double *b, int64_t ldb, double *y,
                           int64_t ldy, int nrhs, void *ws, size_t ws_bytes, void *stream);
 /* x = V y: y in S order (column side), x in tree order.  Root to leaves:
- * x_t = Q_t [z_basis; y_t].  q_col as produced by h2sp_build (q_row if
- * symmetric). */
+ * x_t = Q_t [z_basis; y_t], each cluster's product computed once (by the CTA of
+ * its leftmost leaf) and handed down through the workspace.  q_col as produced
+ * by h2sp_build (q_row if symmetric). */
 h2sp_status h2sp_apply_V(h2sp_plan plan, const double *q_col, const double *y, int64_t ldy, double *x,
                          int64_t ldx, int nrhs, void *ws, size_t ws_bytes, void *stream);
 

@@ -283,8 +283,10 @@ h2sp_status h2sp_cheb_construct(h2sp_plan P, const void *meta, int side, const h
 int64_t h2sp_apply_ws_bytes(h2sp_plan P, int nrhs) {
   if (!P || nrhs < 0) return -1;
   int64_t z = P->zb_row_len > P->zb_col_len ? P->zb_row_len : P->zb_col_len;
-  // meta | basis coefficients (256-aligned) | arrival counters of the upward pass
-  return int64_t(P->meta_bytes) + (z * int64_t(nrhs) * 8 + 255) / 256 * 256 + P->ncl * 4;
+  // meta | upward pass: basis coefficients (256-aligned), arrival counters (256-aligned)
+  //      | downward pass: basis coefficients (256-aligned), cluster flags + ticket
+  const int64_t zb = (z * int64_t(nrhs) * 8 + 255) / 256 * 256, ab = (P->ncl * 4 + 255) / 256 * 256;
+  return int64_t(P->meta_bytes) + 2 * zb + ab + (P->ncl + 1) * 4;
 }
 
 static h2sp_status apply_common(h2sp_plan P, const double *q, const void *a, int64_t lda, void *b, int64_t ldb,

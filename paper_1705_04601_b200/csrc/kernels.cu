@@ -1510,6 +1510,33 @@ __device__ __forceinline__ void scatter_pair2(const PairArgs &A, const PairDst &
   }
 }
 
+// Sums over the 8 lane rows r = lane >> 2 of a DMMA accumulator layout (lane
+// bits 4, 3, 2) of NV (8 or 4) per-lane values by recursive halving: lanes 16,
+// 8, 4 apart exchange the half they do not keep (7 shuffles for 8 values instead
+// of 24; 4 values: two halvings and one butterfly step).  Afterwards v[0] of lane
+// (r, q) is the total of value index r (NV = 8) or r >> 1 (NV = 4, both lanes of
+// a pair) over the 8 lanes with the same q.  Fixed order.
+template <int NV>
+__device__ __forceinline__ void lane_rows_reduce(double (&v)[NV], int lane) {
+  static_assert(NV == 8 || NV == 4, "8 or 4 values per lane");
+  int cnt = NV;
+#pragma unroll
+  for (int o = 16; o >= 4; o >>= 1) {
+    if (cnt > 1) {
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int i = 0; i < cnt / 2; i++) {
+        const double send = up ? v[i] : v[i + cnt / 2];
+        const double keep = up ? v[i + cnt / 2] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+      cnt >>= 1;
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+    }
+  }
+}
+
 // Bench mode (H2SP_PLAN_BENCH, include/h2sp.h h2sp_outputs): the nn part of H --
 // S block (t@k, s@k) and, symmetric, its mirror (s@k, t@k) = H_nn^T -- reduced
 // to per-row partials {sum_j S[i][j] w[j], sum_j S[i][j]^2} in a fixed order:
@@ -1519,86 +1546,6 @@ __device__ __forceinline__ void scatter_pair2(const PairArgs &A, const PairDst &
 // of the CTA must call this).  Diagonal blocks of symmetric mode (H_sym[a][b] =
 // H[min(a,b)][max(a,b)]): entries with a <= b come from row a, a > b from
 // column a.  Lane (r, q) of warp w holds H[m0 + r][8j + 2q + e].
-// bench_pair_tile: the partials of one 8-row slab (rows m0..m0+7, slab index
-// `slab` = m0 / 8) -- a row's by its lane quad into rowp, a column's by the 8
-// lanes of a tile column into colp[slab]; bench_pair_finish: the per-row sums
-// over the slabs in slab order (every thread of the CTA calls both).
-template <int NP, int TN>
-__device__ __forceinline__ void bench_pair_tile(const PairArgs &A, const PairDst &D, int t, int s,
-                                                const double (&H)[TN][2], int m0, int slab, double2 *colp,
-                                                double2 *rowp) {
-  const int lane = threadIdx.x & 31, r = lane >> 2, q = lane & 3;
-  const int row = m0 + r, a = row - D.kt;
-  const bool vrow = row >= D.kt && row < D.nt;
-  const bool cols = D.dsym || D.s_dst_m >= 0;   // CTA-uniform
-  const double *w_s = A.bw + A.cs.s_off[s];      // weights of block (t, s)'s columns
-  const double wa = (vrow && cols) ? __ldg(A.bw + A.cs.s_off[t] + a) : 0.0;  // weight of mirror column a
-  double ry = 0.0, rr = 0.0;
-#pragma unroll
-  for (int j = 0; j < TN; j++) {
-    double cy[2], cr[2];
-#pragma unroll
-    for (int e = 0; e < 2; e++) {
-      const int col = j * 8 + 2 * q + e, b = col - D.ks;
-      const bool v = vrow && col >= D.ks && col < D.ns;
-      const double h = H[j][e];
-      if (v && D.s_dst >= 0 && (!D.dsym || a <= b)) {
-        ry = fma(h, __ldg(w_s + b), ry);
-        rr = fma(h, h, rr);
-      }
-      const bool cc = v && (D.dsym ? a < b : true);
-      cy[e] = cc ? h * wa : 0.0;
-      cr[e] = cc ? h * h : 0.0;
-    }
-    if (cols) {
-#pragma unroll
-      for (int o = 4; o < 32; o <<= 1)
-#pragma unroll
-        for (int e = 0; e < 2; e++) {
-          cy[e] += __shfl_xor_sync(0xffffffffu, cy[e], o);
-          cr[e] += __shfl_xor_sync(0xffffffffu, cr[e], o);
-        }
-      if (r == 0) {
-        colp[slab * NP + j * 8 + 2 * q] = make_double2(cy[0], cr[0]);
-        colp[slab * NP + j * 8 + 2 * q + 1] = make_double2(cy[1], cr[1]);
-      }
-    }
-  }
-  ry += __shfl_xor_sync(0xffffffffu, ry, 1);
-  rr += __shfl_xor_sync(0xffffffffu, rr, 1);
-  ry += __shfl_xor_sync(0xffffffffu, ry, 2);
-  rr += __shfl_xor_sync(0xffffffffu, rr, 2);
-  if (q == 0) rowp[row] = make_double2(ry, rr);
-}
-
-template <int NP, int SLABS>
-__device__ __forceinline__ void bench_pair_finish(const PairArgs &A, const PairDst &D, const double2 *colp,
-                                                  const double2 *rowp) {
-  __syncthreads();
-  for (int i = threadIdx.x; i < NP; i += blockDim.x) {
-    if (D.s_dst >= 0 && i >= D.kt && i < D.nt) {  // row i - kt of block (t, s)
-      double2 v = rowp[i];
-      if (D.dsym)
-#pragma unroll
-        for (int w_ = 0; w_ < SLABS; w_++) {
-          v.x += colp[w_ * NP + i].x;
-          v.y += colp[w_ * NP + i].y;
-        }
-      A.part[D.s_dst + int64_t(i - D.kt) * D.s_ld] = v;
-    }
-    if (!D.dsym && D.s_dst_m >= 0 && i >= D.ks && i < D.ns) {  // row i - ks of the mirror block (s, t)
-      double2 v = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int w_ = 0; w_ < SLABS; w_++) {
-        v.x += colp[w_ * NP + i].x;
-        v.y += colp[w_ * NP + i].y;
-      }
-      A.part[D.s_dst_m + int64_t(i - D.ks) * D.s_ld_m] = v;
-    }
-  }
-  __syncthreads();
-}
-
 template <int NP, int TN, int WARPS>
 __device__ __forceinline__ void bench_pair(const PairArgs &A, const PairDst &D, int t, int s, const double (&H)[TN][2],
                                            int m0, double2 *scratch, double2 *rowp_ = nullptr) {
@@ -1611,34 +1558,51 @@ __device__ __forceinline__ void bench_pair(const PairArgs &A, const PairDst &D, 
   const double *w_s = A.bw + A.cs.s_off[s];      // weights of block (t, s)'s columns
   const double wa = (vrow && cols) ? __ldg(A.bw + A.cs.s_off[t] + a) : 0.0;  // weight of mirror column a
   double ry = 0.0, rr = 0.0;
+  constexpr int GS = 2;   // accumulator tiles per group of column sums (4 values per lane: 8 shuffles per group
+                          // and quantity pair instead of 24; groups of 4 tiles save one more but cost 8 registers)
+  static_assert(TN % GS == 0, "whole groups");
 #pragma unroll
-  for (int j = 0; j < TN; j++) {
-    double cy[2], cr[2];
+  for (int j0 = 0; j0 < TN; j0 += GS) {
+    // this warp's 8 rows summed per column, one quantity at a time (registers): lane (r, q) ends
+    // with value ix of its 2 GS
+    const int ix = GS == 4 ? r : r >> 1;
+    double2 cres = make_double2(0.0, 0.0);
+    {
+      double cy[2 * GS];
 #pragma unroll
-    for (int e = 0; e < 2; e++) {
-      const int col = j * 8 + 2 * q + e, b = col - D.ks;
-      const bool v = vrow && col >= D.ks && col < D.ns;
-      const double h = H[j][e];
-      if (v && D.s_dst >= 0 && (!D.dsym || a <= b)) {
-        ry = fma(h, __ldg(w_s + b), ry);
-        rr = fma(h, h, rr);
-      }
-      const bool cc = v && (D.dsym ? a < b : true);
-      cy[e] = cc ? h * wa : 0.0;
-      cr[e] = cc ? h * h : 0.0;
-    }
-    if (cols) {
-#pragma unroll
-      for (int o = 4; o < 32; o <<= 1)
+      for (int jj = 0; jj < GS; jj++)
 #pragma unroll
         for (int e = 0; e < 2; e++) {
-          cy[e] += __shfl_xor_sync(0xffffffffu, cy[e], o);
-          cr[e] += __shfl_xor_sync(0xffffffffu, cr[e], o);
+          const int j = j0 + jj;
+          const int col = j * 8 + 2 * q + e, b = col - D.ks;
+          const bool v = vrow && col >= D.ks && col < D.ns;
+          const double h = H[j][e];
+          if (v && D.s_dst >= 0 && (!D.dsym || a <= b)) {
+            ry = fma(h, __ldg(w_s + b), ry);
+            rr = fma(h, h, rr);
+          }
+          cy[jj * 2 + e] = (v && (D.dsym ? a < b : true)) ? h * wa : 0.0;
         }
-      if (r == 0) {
-        colp[warp * NP + j * 8 + 2 * q] = make_double2(cy[0], cr[0]);
-        colp[warp * NP + j * 8 + 2 * q + 1] = make_double2(cy[1], cr[1]);
+      if (cols) {
+        lane_rows_reduce(cy, lane);
+        cres.x = cy[0];
       }
+    }
+    if (cols) {
+      double cr[2 * GS];
+#pragma unroll
+      for (int jj = 0; jj < GS; jj++)
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          const int j = j0 + jj;
+          const int col = j * 8 + 2 * q + e, b = col - D.ks;
+          const bool v = vrow && col >= D.ks && col < D.ns;
+          const double h = H[j][e];
+          cr[jj * 2 + e] = (v && (D.dsym ? a < b : true)) ? h * h : 0.0;
+        }
+      lane_rows_reduce(cr, lane);
+      cres.y = cr[0];
+      if (GS == 4 || (r & 1) == 0) colp[warp * NP + (j0 + (ix >> 1)) * 8 + 2 * q + (ix & 1)] = cres;
     }
   }
   ry += __shfl_xor_sync(0xffffffffu, ry, 1);
@@ -2642,25 +2606,45 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
         y2 += __shfl_xor_sync(0xffffffffu, y2, 2);
         if (q4 == 0) dslab[wn * NP + row] = make_double2(y, y2);
       }
+      {  // transposed: a column's values of this warp's 16 rows; lane (r, q4) ends with column r of its 8
+        static_assert(C::WN == 32, "8 columns per lane");
+        double2 cres;
+        {
+          double cy[8];
 #pragma unroll
-      for (int j = 0; j < C::WN / 8; j++)  // transposed: a column's values of this warp's 16 rows
+          for (int j = 0; j < C::WN / 8; j++)
 #pragma unroll
-        for (int e = 0; e < 2; e++) {
-          double y = 0.0, y2 = 0.0;
+            for (int e = 0; e < 2; e++) {
+              double y = 0.0;
 #pragma unroll
-          for (int i = 0; i < 2; i++) {
-            const int row = m0 + i * 8 + r;
-            const double v = row >= kq ? acc[i][j][e] : 0.0;
-            y = fma(v, s_wq[row >= kq ? row - kq : 0], y);
-            y2 = fma(v, v, y2);
-          }
-#pragma unroll
-          for (int o = 4; o < 32; o <<= 1) {
-            y += __shfl_xor_sync(0xffffffffu, y, o);
-            y2 += __shfl_xor_sync(0xffffffffu, y2, o);
-          }
-          if (r == 0) tslab[wm * TN + n0 + j * 8 + 2 * q4 + e] = make_double2(y, y2);
+              for (int i = 0; i < 2; i++) {
+                const int row = m0 + i * 8 + r;
+                y = fma(row >= kq ? acc[i][j][e] : 0.0, s_wq[row >= kq ? row - kq : 0], y);
+              }
+              cy[j * 2 + e] = y;
+            }
+          lane_rows_reduce(cy, lane);
+          cres.x = cy[0];
         }
+        {
+          double cr[8];
+#pragma unroll
+          for (int j = 0; j < C::WN / 8; j++)
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+              double y2 = 0.0;
+#pragma unroll
+              for (int i = 0; i < 2; i++) {
+                const double v = m0 + i * 8 + r >= kq ? acc[i][j][e] : 0.0;
+                y2 = fma(v, v, y2);
+              }
+              cr[j * 2 + e] = y2;
+            }
+          lane_rows_reduce(cr, lane);
+          cres.y = cr[0];
+        }
+        tslab[wm * TN + n0 + (r >> 1) * 8 + 2 * q4 + (r & 1)] = cres;
+      }
     }
     __syncthreads();
     const int nfz = n - kq;
@@ -3134,20 +3118,139 @@ __global__ void __launch_bounds__(256) csr_cols_kernel(const CsrBlockRow *__rest
 // --------------------------------------------------------------------------
 // APPLY_RC: right-hand sides per pass over Q (each Q element read once per pass):
 // 1 for a single vector, 8 otherwise
+__device__ __forceinline__ int ld_acquire_gpu(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int *p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Sum NV per-lane values over the 32 lanes of a warp: recursive halving (lanes
+// o apart exchange the half they do not keep: NV - 1 shuffles instead of
+// 5 NV), then a butterfly over the remaining lane bits.  Afterwards v[0] is the
+// warp total of value `slot` (returned); the 32 / NV lanes sharing a slot hold
+// the same total.  Fixed order.
+template <int NV>
+__device__ __forceinline__ int warp_reduce_many(double (&v)[NV], int lane) {
+  static_assert(NV >= 1 && NV <= 32 && (NV & (NV - 1)) == 0, "power of two");
+  int slot = 0, o = 16;
+#pragma unroll
+  for (int cnt = NV; cnt > 1; cnt >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < cnt / 2; i++) {
+      const double send = up ? v[i] : v[i + cnt / 2];
+      const double keep = up ? v[i + cnt / 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+    slot = 2 * slot + (up ? 1 : 0);
+    o >>= 1;
+  }
+#pragma unroll
+  for (int o2 = 16 / NV; o2 > 0; o2 >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o2);
+  return slot;
+}
+
+// predicated 16-byte read-only load (zeros when !ok); one LDG.128 whatever the predicate's shape
+__device__ __forceinline__ double2 ldg2(const double *p, bool ok) {
+  double2 v = make_double2(0.0, 0.0);
+  asm volatile("{ .reg .pred pp; setp.ne.b32 pp, %3, 0; @pp ld.global.nc.v2.f64 {%0, %1}, [%2]; }"
+               : "+d"(v.x), "+d"(v.y)
+               : "l"(p), "r"(int(ok)));
+  return v;
+}
+
+// z[j] = sum_i Q[i n + j] x[i] (j in [0, n), n <= 128; x = sx[i * APPLY_RC + rr]),
+// per-warp partial sums into red[(warp n + j) * APPLY_RC + rr].  The warps split
+// the rows (UR consecutive rows each per round), the lanes the columns in
+// 16-byte pairs (2 lane, 2 lane + 1 and + 64): every load of a round is issued
+// before the first FMA, so a lane keeps 2 UR 16-byte loads in flight.
+template <int APPLY_RC>
+__device__ __forceinline__ void apply_cols(const double *__restrict__ Q, int n, const double *sx, int rc, double *red) {
+  constexpr int UR = APPLY_RC == 1 ? 8 : 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const bool vec = (n & 1) == 0 && (reinterpret_cast<uintptr_t>(Q) & 15) == 0;
+  double acc[4][APPLY_RC];
+#pragma unroll
+  for (int c = 0; c < 4; c++)
+#pragma unroll
+    for (int rr = 0; rr < APPLY_RC; rr++) acc[c][rr] = 0.0;
+  if (vec) {
+    const int ja = 2 * lane, jb = 2 * lane + 64;
+    for (int base = 0; base < n; base += nw * UR) {
+      double2 qa[UR], qb[UR];
+#pragma unroll
+      for (int u = 0; u < UR; u++) {
+        const int i = base + warp * UR + u;
+        const double *row = Q + int64_t(i) * n;
+        qa[u] = ldg2(row + ja, i < n && ja < n);
+        qb[u] = ldg2(row + jb, i < n && jb < n);
+      }
+#pragma unroll
+      for (int u = 0; u < UR; u++) {
+        const int i = min(base + warp * UR + u, n - 1);   // rows past n carry zeros in qa / qb
+#pragma unroll
+        for (int rr = 0; rr < APPLY_RC; rr++) {
+          if (rr >= rc) continue;
+          const double xv = sx[i * APPLY_RC + rr];
+          acc[0][rr] = fma(qa[u].x, xv, acc[0][rr]);
+          acc[1][rr] = fma(qa[u].y, xv, acc[1][rr]);
+          acc[2][rr] = fma(qb[u].x, xv, acc[2][rr]);
+          acc[3][rr] = fma(qb[u].y, xv, acc[3][rr]);
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+      const int j = (c < 2 ? ja : jb) + (c & 1);
+      if (j < n)
+#pragma unroll
+        for (int rr = 0; rr < APPLY_RC; rr++) red[(warp * n + j) * APPLY_RC + rr] = acc[c][rr];
+    }
+  } else {
+    for (int base = 0; base < n; base += nw * UR) {
+      double qv[UR][4];
+#pragma unroll
+      for (int u = 0; u < UR; u++) {
+        const int i = base + warp * UR + u;
+#pragma unroll
+        for (int c = 0; c < 4; c++) qv[u][c] = (i < n && lane + 32 * c < n) ? __ldg(Q + int64_t(i) * n + lane + 32 * c) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < UR; u++) {
+        const int i = min(base + warp * UR + u, n - 1);
+#pragma unroll
+        for (int rr = 0; rr < APPLY_RC; rr++) {
+          if (rr >= rc) continue;
+          const double xv = sx[i * APPLY_RC + rr];
+#pragma unroll
+          for (int c = 0; c < 4; c++) acc[c][rr] = fma(qv[u][c], xv, acc[c][rr]);
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; c++)
+      if (lane + 32 * c < n)
+#pragma unroll
+        for (int rr = 0; rr < APPLY_RC; rr++) red[(warp * n + lane + 32 * c) * APPLY_RC + rr] = acc[c][rr];
+  }
+}
+
+// --------------------------------------------------------------------------
+// y = U^T b, leaves -> root, one launch: one CTA (4 warps) per leaf computes
+// z = Q_t^T x_t with Q read straight from global memory (apply_cols); the CTA
+// that completes the second child of a parent (atomic arrival counter)
+// continues with the parent, so the whole upward pass is one kernel.
+// --------------------------------------------------------------------------
 template <int APPLY_RC>
 __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const double *__restrict__ q,
                                                        const double *__restrict__ b, int64_t ldb, double *__restrict__ y,
                                                        int64_t ldy, double *__restrict__ zb, int64_t zbl, int nrhs, int B,
                                                        int *__restrict__ arrive, int64_t leaf0) {
-  // z = Q_t^T x_t with Q read straight from global memory (rows are coalesced
-  // across the threads of one column block): no shared-memory staging, so every
-  // leaf's CTA is resident at once and the climb starts in one wave.  Thread
-  // t = h n + j sums rows i = h, h + H, ... of column j (H = blockDim / n
-  // interleaved partial sums, added in a fixed order) for APPLY_RC right-hand
-  // sides at once: every Q element is read once per APPLY_RC vectors; the row
-  // loop is unrolled for independent loads in flight.
   __shared__ double sx[128 * APPLY_RC];
-  __shared__ double red[128 * APPLY_RC];
+  __shared__ double red[4 * 128 * APPLY_RC];
   __shared__ int s_go;
   // metadata of every cluster this CTA may climb through (the leaf's ancestors)
   // and of their children, in one round trip (level l in slot l)
@@ -3170,6 +3273,7 @@ __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const dou
     }
   }
   __syncthreads();
+  const int nw = blockDim.x >> 5;
   while (true) {
     const int n = m_n[level], k = m_k[level];
     if (level < L) {  // the parent's Q into L2 now: the CTA that climbs reads it after the arrival
@@ -3181,8 +3285,6 @@ __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const dou
     if (n > 0) {
       const double *Q = q + m_q[level];
       const int k1 = level > 0 ? m_k1[level] : 0;
-      const int H = blockDim.x / n;
-      const int t = threadIdx.x, j = t % n, h = t / n;
       for (int r0 = 0; r0 < nrhs; r0 += APPLY_RC) {
         const int rc = min(APPLY_RC, nrhs - r0);
         __syncthreads();
@@ -3195,25 +3297,12 @@ __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const dou
           sx[i * APPLY_RC + rr] = v;
         }
         __syncthreads();
-        if (h < H) {
-          double acc[APPLY_RC];
-#pragma unroll
-          for (int rr = 0; rr < APPLY_RC; rr++) acc[rr] = 0.0;
-#pragma unroll 8
-          for (int i = h; i < n; i += H) {
-            const double qv = __ldg(Q + int64_t(i) * n + j);
-#pragma unroll
-            for (int rr = 0; rr < APPLY_RC; rr++)
-              if (rr < rc) acc[rr] = fma(qv, sx[i * APPLY_RC + rr], acc[rr]);
-          }
-#pragma unroll
-          for (int rr = 0; rr < APPLY_RC; rr++) red[(h * n + j) * APPLY_RC + rr] = acc[rr];
-        }
+        apply_cols<APPLY_RC>(Q, n, sx, rc, red);
         __syncthreads();
         for (int e = threadIdx.x; e < n * rc; e += blockDim.x) {
           const int tj = e % n, rr = e / n, r = r0 + rr;
           double acc = red[tj * APPLY_RC + rr];
-          for (int u = 1; u < H; u++) acc += red[(u * n + tj) * APPLY_RC + rr];
+          for (int u = 1; u < nw; u++) acc += red[(u * n + tj) * APPLY_RC + rr];
           if (tj < k) zb[m_zb[level] + tj + r * zbl] = acc;
           else y[m_loc[level] + (tj - k) + r * ldy] = acc;
         }
@@ -3235,93 +3324,145 @@ __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const dou
   }
 }
 
-template <int APPLY_RC>
-__global__ void __launch_bounds__(128) apply_v_kernel(Side sd, int L, const double *__restrict__ q,
-                                                      const double *__restrict__ y, int64_t ldy, double *__restrict__ x,
-                                                      int64_t ldx, int nrhs, int B, int64_t leaf0) {
-  __shared__ double sv[128 * APPLY_RC];
-  __shared__ double sw[128 * APPLY_RC];
-  // metadata of the whole root -> leaf path in one round trip (level l in slot l),
-  // and the ancestors' Q pulled into L2 while the root levels run
-  __shared__ int p_n[64], p_k[64], p_k1[64];
-  __shared__ int64_t p_q[64], p_loc[64];
-  const int64_t leaf = leaf0 + blockIdx.x;
-  for (int lv = threadIdx.x; lv <= L; lv += blockDim.x) {
-    const int64_t cl = lvl_off_d(L, lv) + (leaf >> lv);
-    p_n[lv] = sd.n[cl];
-    p_k[lv] = sd.k[cl];
-    p_q[lv] = sd.q_off[cl];
-    p_loc[lv] = sd.loc_off[cl];
-    p_k1[lv] = lv > 0 ? sd.k[lvl_off_d(L, lv - 1) + 2 * (leaf >> lv)] : 0;
-  }
-  __syncthreads();
-  for (int lv = 1; lv <= L; lv++) {  // upper-level Q blocks (shared by many leaves)
-    const int n = p_n[lv];
-    const double *Q = q + p_q[lv];
-    for (int e = threadIdx.x * 16; e < n * n; e += blockDim.x * 16)
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(Q + e));
-  }
-  for (int r0 = 0; r0 < nrhs; r0 += APPLY_RC) {
-    const int rc = min(APPLY_RC, nrhs - r0);
-    // walk the path root -> leaf; sv[0:k] holds the basis coefficients from the parent.
-    // Q rows are read straight from global memory: H consecutive threads share a
-    // row (coalesced segments), partial sums over j = h, h + H, ... are added by
-    // a butterfly over those H lanes; APPLY_RC right-hand sides per Q read.
-    for (int level = L; level >= 0; level--) {
-      const int n = p_n[level], k = p_k[level];
-      __syncthreads();
-      if (n == 0) continue;
-      const double *Q = q + p_q[level];
-      for (int e = threadIdx.x; e < n * rc; e += blockDim.x) {
-        const int jj = e % n, rr = e / n;
-        if (jj >= k) sv[jj * APPLY_RC + rr] = y[p_loc[level] + (jj - k) + (r0 + rr) * ldy];
-      }
-      __syncthreads();
-      int rlo = 0, rhi = n;
-      if (level > 0) {  // only the rows of the child on the path are needed
-        const int k1 = p_k1[level];
-        const bool second = (leaf >> (level - 1)) & 1;
-        rlo = second ? k1 : 0;
-        rhi = second ? n : k1;
-      }
-      const int rows = rhi - rlo;
-      int H = 1;
-      while (H < 32 && 2 * H * rows <= int(blockDim.x)) H *= 2;
-      for (int i0 = 0; i0 < rows; i0 += int(blockDim.x) / H) {
-        const int il = i0 + int(threadIdx.x) / H, h = threadIdx.x % H;
-        double acc[APPLY_RC];
+// out[i] = sum_j Q[i n + j] v[j] for i in [0, n), n <= 128, APPLY_RC right-hand
+// sides at once (sv[rr * 128 + j]: conflict-free 16-byte reads).  Per round warp w takes rows
+// base + UR w .. + UR - 1; the lanes stride one row's columns in 16-byte pairs
+// (2 lane and 2 lane + 64), every load of a round issued before the first FMA;
+// the UR x APPLY_RC partial sums of a lane meet by recursive halving
+// (warp_reduce_many).  ready() is called by every thread once, after the first
+// round's loads are issued and before sv is read: it completes sv and ends with
+// a CTA barrier (the loads stay in flight across it).  emit(i, rr, value): one
+// lane per result.
+template <int APPLY_RC, class R, class F>
+__device__ __forceinline__ void apply_rows(const double *__restrict__ Q, int n, const double *sv, int rc, R &&ready,
+                                           F &&emit) {
+  constexpr int UR = APPLY_RC == 1 ? 8 : 2, NV = UR * APPLY_RC;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const bool vec = (n & 1) == 0 && (reinterpret_cast<uintptr_t>(Q) & 15) == 0;
+  const int ja = 2 * lane, jb = 2 * lane + 64;
+  for (int base = 0; base < n; base += nw * UR) {
+    const int i0 = base + warp * UR;
+    double acc[NV];
 #pragma unroll
-        for (int rr = 0; rr < APPLY_RC; rr++) acc[rr] = 0.0;
-        if (il < rows) {
-          const double *Qi = Q + int64_t(rlo + il) * n;
-#pragma unroll 8
-          for (int jj = h; jj < n; jj += H) {
-            const double qv = __ldg(Qi + jj);
+    for (int e = 0; e < NV; e++) acc[e] = 0.0;
+    if (vec) {
+      double2 qa[UR], qb[UR];
 #pragma unroll
-            for (int rr = 0; rr < APPLY_RC; rr++)
-              if (rr < rc) acc[rr] = fma(qv, sv[jj * APPLY_RC + rr], acc[rr]);
-          }
+      for (int u = 0; u < UR; u++) {
+        const double *row = Q + int64_t(i0 + u) * n;
+        qa[u] = ldg2(row + ja, i0 + u < n && ja < n);
+        qb[u] = ldg2(row + jb, i0 + u < n && jb < n);
+      }
+      if (base == 0) ready();
+      const int jas = min(ja, n - 2), jbs = min(jb, n - 2);   // lanes past n carry zeros in qa / qb
+#pragma unroll
+      for (int rr = 0; rr < APPLY_RC; rr++) {
+        if (rr >= rc) continue;
+        const double2 va = *reinterpret_cast<const double2 *>(sv + rr * 128 + jas);
+        const double2 vb = *reinterpret_cast<const double2 *>(sv + rr * 128 + jbs);
+#pragma unroll
+        for (int u = 0; u < UR; u++)
+          acc[u * APPLY_RC + rr] = fma(qb[u].y, vb.y, fma(qb[u].x, vb.x, fma(qa[u].y, va.y, fma(qa[u].x, va.x, 0.0))));
+      }
+    } else {
+      if (base == 0) ready();
+      for (int j = lane; j < n; j += 32) {
+        double qv[UR];
+#pragma unroll
+        for (int u = 0; u < UR; u++) qv[u] = i0 + u < n ? __ldg(Q + int64_t(i0 + u) * n + j) : 0.0;
+#pragma unroll
+        for (int rr = 0; rr < APPLY_RC; rr++) {
+          if (rr >= rc) continue;
+          const double v0 = sv[rr * 128 + j];
+#pragma unroll
+          for (int u = 0; u < UR; u++) acc[u * APPLY_RC + rr] = fma(qv[u], v0, acc[u * APPLY_RC + rr]);
         }
-#pragma unroll
-        for (int rr = 0; rr < APPLY_RC; rr++)
-          for (int o = H >> 1; o > 0; o >>= 1) acc[rr] += __shfl_xor_sync(0xffffffffu, acc[rr], o);
-        if (h == 0 && il < rows) {
-#pragma unroll
-          for (int rr = 0; rr < APPLY_RC; rr++) {
-            if (rr >= rc) continue;
-            if (level == 0)
-              x[((leaf - leaf0) * B + il) + (r0 + rr) * ldx] = acc[rr];
-            else
-              sw[il * APPLY_RC + rr] = acc[rr];
-          }
-        }
-      }
-      if (level > 0) {
-        __syncthreads();
-        for (int e = threadIdx.x; e < rows * APPLY_RC; e += blockDim.x) sv[e] = sw[e];
       }
     }
+    const int slot = warp_reduce_many<NV>(acc, lane);
+    const int u = slot / APPLY_RC, rr = slot % APPLY_RC;
+    if ((lane & (32 / NV - 1)) == 0 && i0 + u < n && rr < rc) emit(i0 + u, rr, acc[0]);
   }
+}
+
+// --------------------------------------------------------------------------
+// x = V y, root -> leaves, one launch: one CTA (8 warps) per cluster of the
+// shard's tree (its subtree and the path above it).  CTAs take their cluster
+// from a ticket counter in start order, the tickets numbering the clusters
+// level by level from the root down (the leaves last): cluster t's product
+// [c_1; c_2] = Q_t [c_t; y_t] is computed once -- its Q rows and y_t are
+// requested first, then the CTA waits for the parent's flag (acquire), reads
+// c_t from zb, multiplies, writes the children's coefficients to zb and
+// publishes its own flag (release).  A cluster's parent has a smaller ticket,
+// i.e. belongs to a CTA that is already running, so the waits cannot deadlock
+// whatever the hardware's block scheduling order; the upper levels are done
+// while the first wide levels stream, and the leaves (most of the bytes) find
+// their parents finished.  flags: [ncl] cluster flags + the ticket, zeroed
+// before the launch.
+// --------------------------------------------------------------------------
+template <int APPLY_RC>
+__global__ void __launch_bounds__(256) apply_v_kernel(Side sd, int L, const double *__restrict__ q,
+                                                      const double *__restrict__ y, int64_t ldy, double *__restrict__ x,
+                                                      int64_t ldx, double *zb, int64_t zbl, int nrhs, int B, int *flags,
+                                                      int64_t ncl, int64_t leaf0, int64_t nleaves) {
+  __shared__ __align__(16) double sv[128 * APPLY_RC];   // [rhs][column]
+  __shared__ int s_ticket;
+  if (threadIdx.x == 0) s_ticket = atomicAdd(flags + ncl, 1);
+  __syncthreads();
+  // ticket -> (level, in-level index): levels L .. 0, max(1, nleaves >> level) clusters each
+  int64_t t = s_ticket;
+  int lv = L;
+  for (; lv > 0; lv--) {
+    const int64_t cnt = max(int64_t(1), nleaves >> lv);
+    if (t < cnt) break;
+    t -= cnt;
+  }
+  const int64_t a = (leaf0 >> lv) + t, cl = lvl_off_d(L, lv) + a;
+  const int n = sd.n[cl], k = sd.k[cl];
+  int *flag = flags + cl;
+  if (n == 0) {  // nothing to multiply (levels without admissible blocks): the children carry no coefficients
+    if (lv > 0 && threadIdx.x == 0) st_release_gpu(flag, 1);
+    return;
+  }
+  const double *Q = q + sd.q_off[cl];
+  const int64_t loc = sd.loc_off[cl], zin = sd.zb_off[cl];
+  int k1 = 0;
+  int64_t zo1 = 0, zo2 = 0;
+  if (lv > 0) {
+    const int64_t c1 = lvl_off_d(L, lv - 1) + 2 * a;
+    k1 = sd.k[c1];
+    zo1 = sd.zb_off[c1];
+    zo2 = sd.zb_off[c1 + 1];
+  }
+  const int *pflag = (lv < L && k > 0) ? flags + lvl_off_d(L, lv + 1) + (a >> 1) : nullptr;
+  for (int r0 = 0; r0 < nrhs; r0 += APPLY_RC) {
+    const int rc = min(APPLY_RC, nrhs - r0);
+    auto ready = [&]() {  // (called with the Q loads in flight)
+      for (int e = threadIdx.x; e < (n - k) * rc; e += blockDim.x) {  // the cluster's own part of the vector
+        const int jj = e % (n - k), rr = e / (n - k);
+        sv[rr * 128 + k + jj] = y[loc + jj + (r0 + rr) * ldy];
+      }
+      if (r0 == 0 && pflag) {  // the parent's part, once its product is published
+        if (threadIdx.x == 0)
+          while (ld_acquire_gpu(pflag) == 0) __nanosleep(20);
+        __syncthreads();
+      }
+      for (int e = threadIdx.x; e < k * rc; e += blockDim.x) {
+        const int jj = e % k, rr = e / k;
+        sv[rr * 128 + jj] = __ldcg(zb + zin + jj + (r0 + rr) * zbl);
+      }
+      __syncthreads();
+    };
+    if (lv == 0) {
+      double *xo = x + (a - leaf0) * B + r0 * ldx;
+      apply_rows<APPLY_RC>(Q, n, sv, rc, ready, [&](int i, int rr, double v) { xo[i + rr * ldx] = v; });
+    } else {
+      double *z1 = zb + zo1 + r0 * zbl, *z2 = zb + zo2 + r0 * zbl - k1;
+      apply_rows<APPLY_RC>(Q, n, sv, rc, ready, [&](int i, int rr, double v) { (i < k1 ? z1 : z2)[i + rr * zbl] = v; });
+    }
+    __syncthreads();   // sv free for the next pass; every thread's zb stores ordered before the release
+  }
+  if (lv > 0 && threadIdx.x == 0) st_release_gpu(flag, 1);
 }
 
 // --------------------------------------------------------------------------
@@ -4129,14 +4270,24 @@ h2sp_status launch_apply_V(const h2sp_plan_s *P, const double *q, const double *
                            bool col_side) {
   cudaStream_t st = (cudaStream_t)stream;
   const Clusters cl = make_clusters(P, meta);
-  (void)scratch;
   const Side sd = side_of(cl, col_side);
+  // the downward pass's own half of the apply scratch (U^T b may run beside it):
+  // basis coefficients | cluster flags + ticket
+  const size_t zbytes = (size_t(std::max(P->zb_row_len, P->zb_col_len)) * nrhs * 8 + 255) / 256 * 256;
+  const size_t abytes = (size_t(P->ncl) * 4 + 255) / 256 * 256;
+  double *zb = (double *)(scratch + zbytes + abytes);
+  const int64_t zbl = col_side ? P->zb_col_len : P->zb_row_len;
+  int *flags = (int *)(scratch + zbytes + abytes + zbytes);
+  H2SP_CK(cudaMemsetAsync(flags, 0, (size_t(P->ncl) + 1) * sizeof(int), st));
+  // one CTA per cluster of the shard's tree: levels L .. 0, max(1, n_leaves_local >> level) each
+  int64_t nunits = 0;
+  for (int lv = 0; lv <= P->L; lv++) nunits += std::max<int64_t>(1, P->n_leaves_local >> lv);
   if (nrhs == 1)
-    apply_v_kernel<1><<<unsigned(P->n_leaves_local), 128, 0, st>>>(sd, P->L, q, y, ldy, x, ldx, nrhs, P->B,
-                                                                   P->first_leaf);
+    apply_v_kernel<1><<<unsigned(nunits), 256, 0, st>>>(sd, P->L, q, y, ldy, x, ldx, zb, zbl, nrhs, P->B, flags, P->ncl,
+                                                        P->first_leaf, P->n_leaves_local);
   else
-    apply_v_kernel<8><<<unsigned(P->n_leaves_local), 128, 0, st>>>(sd, P->L, q, y, ldy, x, ldx, nrhs, P->B,
-                                                                   P->first_leaf);
+    apply_v_kernel<8><<<unsigned(nunits), 256, 0, st>>>(sd, P->L, q, y, ldy, x, ldx, zb, zbl, nrhs, P->B, flags, P->ncl,
+                                                        P->first_leaf, P->n_leaves_local);
   H2SP_CK(cudaGetLastError());
   return H2SP_OK;
 }
