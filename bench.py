@@ -2,19 +2,22 @@
 """Benchmark of the B200-native H^2 sparsification hot path (arXiv 1705.04601).
 
 One *step* = one pass of the whole hot path of SURVEY.md §8(a) over one
-synthetic H^2 matrix already resident in HBM: h2sp_build (QR completion,
-couplings, merge + congruence + freeze, strips, CSR) followed by
-y = U^T b and x = V y (h2sp_apply_Ut / h2sp_apply_V).  The symbolic plan
-(row a1, host, structure only) is created once per matrix and reported as
-``config.plan_ms``.
+synthetic H^2 matrix: h2sp_build (QR completion, couplings, merge + congruence +
+freeze, strips, CSR or the bench-mode S reduction) and the applies y = U^T b,
+x = V w (h2sp_apply_Ut / h2sp_apply_V) of the same pass.  The symbolic plan
+(row a1, host, structure only) is created once per matrix and reported apart.
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config 1..5]
 
-Default workload: BASELINE.json configs[1] (N = 65,536 points in the unit
-square, exp(-|x-y|/0.1) + 1e-2 I, B = 64, r = 16, eta = 0.7, SPD -> symmetric
-mode).  With N > 1 GPUs (torchrun, one rank per GPU) every rank sparsifies its
-own independent matrix of the same recipe (weak scaling, no data-path
-collective); time = max over ranks.
+Default workload: BASELINE.json configs[4] at its full size (N = 4,194,304 points
+in the unit cube, exp(-|x-y|/0.05) + 1e-2 I, B = 128, r = 32, eta = 0.7, SPD ->
+symmetric mode), the configuration the metric is quoted on, by the SURVEY §8(d)
+config-5 protocol (inputs built on the device, 8 virtual subtree shards on one
+scratch buffer, bench-mode S; run_protocol below).  With N > 1 GPUs (torchrun,
+one rank per GPU) the 8 shards of the SAME matrix are split over the ranks
+(strong scaling, no data-path collective; the checks go through an NCCL
+all_reduce); time = max over ranks.  ``--config 1..4`` run the stored-S path on
+one matrix per rank (or ``--shard``: one matrix split in N subtree shards).
 
 ``--impl reference`` times the CPU oracle (oracle/, numpy, 1 thread) on a
 bounded sample of the workload; only rank 0 works.
@@ -810,6 +813,17 @@ def main():
         # i's D2H (S, Q, x) drains -- PCIe is full duplex.  Every job still copies
         # all of its inputs in and all of its outputs out inside the timed region.
         depth = max(1, args.e2e_depth)
+        # every job in flight needs its own device buffer set and pinned host outputs: full-size
+        # configs[2] / configs[3] (58 / 66 GB of S) fit only one of them
+        def _nbytes(dct):
+            return sum(v.numel() * v.element_size() for v in dct.values() if v is not None)
+        set_bytes = _nbytes(sp.inputs) + _nbytes(sp.outputs) + int(plan.sizes["workspace_bytes"])
+        free_dev = torch.cuda.mem_get_info(dev)[0]
+        import psutil
+        free_host = psutil.virtual_memory().available
+        while depth > 1 and ((depth - 1) * set_bytes > free_dev - (4 << 30)
+                             or _nbytes(sp.inputs) + depth * _nbytes(sp.outputs) > 0.7 * free_host):
+            depth -= 1
         host_in = {k: v.cpu().pin_memory() for k, v in sp.inputs.items()}
         hb = b.cpu().pin_memory()
         sets = []

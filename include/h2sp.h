@@ -372,6 +372,29 @@ h2sp_status h2sp_build_meta(h2sp_plan plan, const h2sp_inputs *in, const h2sp_ou
                             void *scratch, size_t scratch_bytes, const h2sp_apply_args *ap, void *stream,
                             void *const *events, int64_t n_events);
 
+/* QR sharing between the shard plans of ONE matrix that are built one after
+ * another on one scratch buffer with one set of Q outputs (h2sp_build_meta; SURVEY
+ * §8(d) config-5 protocol step 2: "QR/R^ for every cluster depends only on the
+ * bases, so it runs first for all clusters").  The mode is host-side state of
+ * the plan, read by the next h2sp_build* call:
+ *   H2SP_QR_NEED  (default) QR completion of the clusters this plan
+ *                 needs: its own subtree plus the halo closure over descendants
+ *                 -- at the upper levels of a 3-D tree that closure is nearly
+ *                 the whole tree, so every shard repeats almost the full chain;
+ *   H2SP_QR_ALL   QR completion of EVERY cluster of the tree (what an unsharded
+ *                 plan computes);
+ *   H2SP_QR_REUSE no QR launch at all: the caller guarantees that the head of
+ *                 `scratch` (R^ and the level-0 compact-WY factors; the same
+ *                 offsets and sizes in every shard plan of one matrix, of the
+ *                 same flags) and out->q_row / q_col still hold the results of
+ *                 an H2SP_QR_ALL build of the same inputs.
+ * Results are bitwise the same in every mode (each cluster's Q_t, R^_t depend on
+ * its subtree's bases only).  H2SP_EINVAL: unknown mode. */
+#define H2SP_QR_NEED 0
+#define H2SP_QR_ALL 1
+#define H2SP_QR_REUSE 2
+h2sp_status h2sp_plan_set_qr_mode(h2sp_plan plan, int mode);
+
 /* End-to-end variant with HOST buffers: copies the host inputs into the given
  * device input buffers, builds, and copies every output back into the host
  * output buffers (host pointers should be pinned for overlap).  All copies

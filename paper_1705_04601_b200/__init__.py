@@ -118,6 +118,9 @@ lib.h2sp_build_meta.argtypes = [_vp, ctypes.POINTER(_Inputs), ctypes.POINTER(_Ou
 lib.h2sp_build_host.argtypes = [_vp, ctypes.POINTER(_Inputs), ctypes.POINTER(_Outputs), ctypes.POINTER(_Inputs),
                                 ctypes.POINTER(_Outputs), _vp, ctypes.c_size_t, _vp]
 lib.h2sp_eval_kernel_blocks.argtypes = [ctypes.POINTER(_CloseGen), _vp, _vp, _vp, _i64, _vp, _vp]
+lib.h2sp_plan_set_qr_mode.argtypes = [_vp, ctypes.c_int]
+lib.h2sp_plan_set_qr_mode.restype = ctypes.c_int
+QR_NEED, QR_ALL, QR_REUSE = 0, 1, 2
 lib.h2sp_apply_ws_bytes.argtypes = [_vp, ctypes.c_int]
 lib.h2sp_apply_ws_bytes.restype = _i64
 lib.h2sp_apply_Ut.argtypes = [_vp, _vp, _vp, _i64, _vp, _i64, ctypes.c_int, _vp, ctypes.c_size_t, _vp]
@@ -491,12 +494,18 @@ class VirtualShards:
     subtrees), each with its work lists resident in its own device buffer, all
     taking turns on one shared scratch buffer (h2sp_build_meta), with shared
     inputs and global outputs (Q, and in bench mode y = S w and the row norms).
-    ``plans``: Plan objects (same matrix, ranks 0..G-1 of world G)."""
+    ``plans``: Plan objects (same matrix, ranks 0..G-1 of world G).
+    ``share_qr`` (protocol step 2: "QR/R^ for every cluster depends only on the
+    bases, so it runs first for all clusters"): the first shard's build runs the
+    QR completion of every cluster (H2SP_QR_ALL), the others reuse its R^ / V, M
+    (head of the shared scratch) and Q (H2SP_QR_REUSE) instead of repeating the
+    QR of their need sets; results are bitwise the same."""
 
     def __init__(self, plans, packed: Optional[dict] = None, device="cuda", close_gen: Optional[dict] = None,
-                 inputs: Optional[dict] = None, nrhs: int = 1):
+                 inputs: Optional[dict] = None, nrhs: int = 1, share_qr: bool = True):
         import torch
         self.plans = list(plans)
+        self.share_qr = bool(share_qr) and len(self.plans) > 1
         self.device = torch.device(device)
         first = Sparsifier(self.plans[0], packed, device=device, close_gen=close_gen, inputs=inputs, workspace=False)
         self.shards = [first] + [Sparsifier(p, None, device=device, alloc_inputs=False, close_gen=None,
@@ -537,6 +546,8 @@ class VirtualShards:
                                 ws_bytes=self.apply_bytes)
             ev = events[i] if events is not None else None
             arr = (_vp * len(ev))(*[e.cuda_event for e in ev]) if ev else None
+            mode = (QR_ALL if i == 0 else QR_REUSE) if self.share_qr else QR_NEED
+            _check(lib.h2sp_plan_set_qr_mode(sp.plan.handle, mode), "h2sp_plan_set_qr_mode")
             _check(lib.h2sp_build_meta(sp.plan.handle, ctypes.byref(sp._abi_inputs()),
                                        ctypes.byref(sp._abi_outputs()), mptr, self.scratch_ptr, self.scratch_bytes,
                                        ctypes.byref(ap) if ap is not None else None, _stream_handle(stream), arr,

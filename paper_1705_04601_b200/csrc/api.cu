@@ -280,6 +280,13 @@ h2sp_status h2sp_cheb_construct(h2sp_plan P, const void *meta, int side, const h
                                leaf_basis, transfer, nodes, stream);
 }
 
+h2sp_status h2sp_plan_set_qr_mode(h2sp_plan P, int mode) {
+  if (!P) return fail(H2SP_EINVAL, "NULL plan");
+  if (mode != H2SP_QR_NEED && mode != H2SP_QR_ALL && mode != H2SP_QR_REUSE) return fail(H2SP_EINVAL, "unknown QR mode");
+  P->qr_mode = mode;
+  return H2SP_OK;
+}
+
 int64_t h2sp_apply_ws_bytes(h2sp_plan P, int nrhs) {
   if (!P || nrhs < 0) return -1;
   int64_t z = P->zb_row_len > P->zb_col_len ? P->zb_row_len : P->zb_col_len;

@@ -150,11 +150,13 @@ struct ClusterArrays {   // byte offsets in meta of per-cluster arrays
   size_t zb_off_row, zb_off_col;           // int64 [ncl]: apply basis-coefficient slots (per rhs)
   size_t loc_off_row, loc_off_col;         // int64 [ncl]: local S row offset of owned clusters, -1 otherwise
   size_t need_row, need_col;               // int8 [ncl]: Q needed by this shard
+  size_t need_all;                         // int8 [ncl]: all ones (H2SP_QR_ALL builds)
 };
 
 }  // namespace h2sp
 
 struct h2sp_plan_s {
+  int32_t qr_mode = 0;                     // H2SP_QR_NEED / _ALL / _REUSE (h2sp_plan_set_qr_mode)
   int32_t L, B, sym;
   int32_t rank, world, part_level;         // sharding by top-level subtrees (world == 1: everything)
   int64_t first_leaf, n_leaves_local, n_rows_local, n_cols_local;
@@ -181,7 +183,7 @@ struct h2sp_plan_s {
   // compact-WY form of the level-0 Q (0 = explicit Q everywhere): per leaf,
   // V (wy_n x wy_kp, row-major) then M = T V^T (wy_kp x wy_n), zero padded
   int32_t wy_kp, wy_n;                      // wy_n: padded leaf size of V / M (64 or 128)
-  size_t ws_wy_row, ws_wy_col;
+  size_t ws_wy_row, ws_wy_col, ws_qr_end;
   int32_t nmax;                             // largest local size n_t
   int32_t bench;                            // H2SP_PLAN_BENCH: S reduced to S*w and row norms, never stored
   int32_t strip_aligned;                    // every frozen size m_t is a multiple of 32 (matrix-wide)

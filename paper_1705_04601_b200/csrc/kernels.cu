@@ -3163,7 +3163,7 @@ __device__ __forceinline__ double2 ldg2(const double *p, bool ok) {
 }
 
 // z[j] = sum_i Q[i n + j] x[i] (j in [0, n), n <= 128; x = sx[i * APPLY_RC + rr]),
-// per-warp partial sums into red[(warp n + j) * APPLY_RC + rr].  The warps split
+// per-warp partial sums into red[(rr * 4 + warp) * 128 + j] (4 warps).  The warps split
 // the rows (UR consecutive rows each per round), the lanes the columns in
 // 16-byte pairs (2 lane, 2 lane + 1 and + 64): every load of a round is issued
 // before the first FMA, so a lane keeps 2 UR 16-byte loads in flight.
@@ -3203,11 +3203,10 @@ __device__ __forceinline__ void apply_cols(const double *__restrict__ Q, int n, 
       }
     }
 #pragma unroll
-    for (int c = 0; c < 4; c++) {
-      const int j = (c < 2 ? ja : jb) + (c & 1);
-      if (j < n)
-#pragma unroll
-        for (int rr = 0; rr < APPLY_RC; rr++) red[(warp * n + j) * APPLY_RC + rr] = acc[c][rr];
+    for (int rr = 0; rr < APPLY_RC; rr++) {   // [rhs][warp][column]: conflict-free 16-byte stores
+      double *rw = red + (rr * 4 + warp) * 128;
+      if (ja < n) *reinterpret_cast<double2 *>(rw + ja) = make_double2(acc[0][rr], acc[1][rr]);
+      if (jb < n) *reinterpret_cast<double2 *>(rw + jb) = make_double2(acc[2][rr], acc[3][rr]);
     }
   } else {
     for (int base = 0; base < n; base += nw * UR) {
@@ -3234,7 +3233,7 @@ __device__ __forceinline__ void apply_cols(const double *__restrict__ Q, int n, 
     for (int c = 0; c < 4; c++)
       if (lane + 32 * c < n)
 #pragma unroll
-        for (int rr = 0; rr < APPLY_RC; rr++) red[(warp * n + lane + 32 * c) * APPLY_RC + rr] = acc[c][rr];
+        for (int rr = 0; rr < APPLY_RC; rr++) red[(rr * 4 + warp) * 128 + lane + 32 * c] = acc[c][rr];
   }
 }
 
@@ -3250,7 +3249,7 @@ __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const dou
                                                        int64_t ldy, double *__restrict__ zb, int64_t zbl, int nrhs, int B,
                                                        int *__restrict__ arrive, int64_t leaf0) {
   __shared__ double sx[128 * APPLY_RC];
-  __shared__ double red[4 * 128 * APPLY_RC];
+  __shared__ __align__(16) double red[4 * 128 * APPLY_RC];   // [rhs][warp][column]
   __shared__ int s_go;
   // metadata of every cluster this CTA may climb through (the leaf's ancestors)
   // and of their children, in one round trip (level l in slot l)
@@ -3301,8 +3300,8 @@ __global__ void __launch_bounds__(128) apply_ut_kernel(Side sd, int L, const dou
         __syncthreads();
         for (int e = threadIdx.x; e < n * rc; e += blockDim.x) {
           const int tj = e % n, rr = e / n, r = r0 + rr;
-          double acc = red[tj * APPLY_RC + rr];
-          for (int u = 1; u < nw; u++) acc += red[(u * n + tj) * APPLY_RC + rr];
+          double acc = red[rr * 4 * 128 + tj];
+          for (int u = 1; u < nw; u++) acc += red[(rr * 4 + u) * 128 + tj];
           if (tj < k) zb[m_zb[level] + tj + r * zbl] = acc;
           else y[m_loc[level] + (tj - k) + r * ldy] = acc;
         }
@@ -3654,6 +3653,13 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
   auto reg = [&](size_t off) { return scratch + (off - P->meta_bytes); };
   const Clusters cl = make_clusters(P, meta);
   const Side rs = side_of(cl, false), cs = side_of(cl, true);
+  // h2sp_plan_set_qr_mode: H2SP_QR_ALL -- the QR kernels (and the level-0 Q
+  // formation) take every cluster of the tree, not just this shard's need set;
+  // H2SP_QR_REUSE -- they are not launched: R^ / V, M (the head of scratch, at
+  // plan-independent offsets) and Q still hold an H2SP_QR_ALL build's results
+  Side rs_qr = rs, cs_qr = cs;
+  if (P->qr_mode == H2SP_QR_ALL) rs_qr.need = cs_qr.need = (const int8_t *)(meta + P->ca.need_all);
+  const bool qr_reuse = P->qr_mode == H2SP_QR_REUSE;
   const bool sym = P->sym != 0;
   double *rh_row = (double *)reg(P->ws_rh_row);
   double *rh_col = sym ? rh_row : (double *)reg(P->ws_rh_col);
@@ -3828,16 +3834,18 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     };
     if (lp.np_row > 0) {
       if (h2sp_status e = pre(s, li[k].qr_row)) return e;
-      if (h2sp_status e = launch(rs, P->n_row, P->k_row, in->leaf_basis_row, in->transfer_row, rh_row, out->q_row,
-                                 k == 0 ? (const uint64_t *)meta : nullptr, k == 0 ? wy_row : nullptr))
-        return e;
+      if (!qr_reuse)
+        if (h2sp_status e = launch(rs_qr, P->n_row, P->k_row, in->leaf_basis_row, in->transfer_row, rh_row, out->q_row,
+                                   k == 0 ? (const uint64_t *)meta : nullptr, k == 0 ? wy_row : nullptr))
+          return e;
       if (h2sp_status e = post(s, li[k].qr_row)) return e;
     }
     if (!sym && lp.np_col > 0) {
       if (h2sp_status e = pre(s, li[k].qr_col)) return e;
-      if (h2sp_status e = launch(cs, P->n_col, P->k_col, leaf_col, tr_col, rh_col, q_col, nullptr,
-                                 k == 0 ? wy_col : nullptr))
-        return e;
+      if (!qr_reuse)
+        if (h2sp_status e = launch(cs_qr, P->n_col, P->k_col, leaf_col, tr_col, rh_col, q_col, nullptr,
+                                   k == 0 ? wy_col : nullptr))
+          return e;
       if (h2sp_status e = post(s, li[k].qr_col)) return e;
     }
     return H2SP_OK;
@@ -3982,15 +3990,17 @@ h2sp_status launch_build(const h2sp_plan_s *P, const h2sp_inputs *in, const h2sp
     if (h2sp_status e = pre(s7, qform_idx)) return e;
     const int64_t nleaf = int64_t(1) << L;
     const unsigned grid = unsigned(nleaf * (sym ? 1 : 2));
-    if (P->wy_n == 128) {
+    if (qr_reuse) {
+      // Q is already there
+    } else if (P->wy_n == 128) {
       if (P->wy_kp == 16)
-        { if (h2sp_status e = launch_wy_form_q<16, 128>(grid, s7, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf)) return e; }
+        { if (h2sp_status e = launch_wy_form_q<16, 128>(grid, s7, rs_qr, cs_qr, wy_row, wy_col, out->q_row, q_col, nleaf)) return e; }
       else
-        { if (h2sp_status e = launch_wy_form_q<32, 128>(grid, s7, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf)) return e; }
+        { if (h2sp_status e = launch_wy_form_q<32, 128>(grid, s7, rs_qr, cs_qr, wy_row, wy_col, out->q_row, q_col, nleaf)) return e; }
     } else if (P->wy_kp == 16) {
-      { if (h2sp_status e = launch_wy_form_q<16, 64>(grid, s7, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf)) return e; }
+      { if (h2sp_status e = launch_wy_form_q<16, 64>(grid, s7, rs_qr, cs_qr, wy_row, wy_col, out->q_row, q_col, nleaf)) return e; }
     } else {
-      { if (h2sp_status e = launch_wy_form_q<24, 64>(grid, s7, rs, cs, wy_row, wy_col, out->q_row, q_col, nleaf)) return e; }
+      { if (h2sp_status e = launch_wy_form_q<24, 64>(grid, s7, rs_qr, cs_qr, wy_row, wy_col, out->q_row, q_col, nleaf)) return e; }
     }
     H2SP_CK(cudaGetLastError());
     if (h2sp_status e = post(s7, qform_idx)) return e;

@@ -788,6 +788,7 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
     P->ca.loc_off_col = mb.put(sym ? loc_off : loc_off_c);
     P->ca.need_row = mb.put(need_r);
     P->ca.need_col = mb.put(sym ? need_r : need_c);
+    P->ca.need_all = mb.put(std::vector<int8_t>(size_t(ncl), int8_t(1)));
     P->levels.resize(L + 1);
     int levels_active = 0;
     int64_t launches = 0;
@@ -1090,19 +1091,23 @@ h2sp_status h2sp_plan_create_shard(const h2sp_structure *st, int rank, int world
     P->bb_len = bb_len;
     P->yr_len = yr_len;
     P->yc_len = yc_len;
+    // the QR results (R^ chain, level-0 compact-WY factors) first: their sizes
+    // depend on the tree and ranks only, so they sit at the same scratch offsets
+    // in every shard plan of one matrix (h2sp_plan_set_qr_mode: H2SP_QR_REUSE)
     P->ws_rh_row = carve(P->rh_row_len);
     P->ws_rh_col = carve(P->rh_col_len);
-    P->ws_dt = carve(dt_len);
-    P->ws_bb = carve(bb_len);
-    P->ws_yr = carve(yr_len);
-    P->ws_yc = carve(yc_len);
-    P->ws_part = bench ? carve(2 * n_part) : 0;
     P->ws_wy_row = P->ws_wy_col = 0;
     if (P->wy_kp) {
       const int64_t per = int64_t(2) * P->wy_n * P->wy_kp;
       P->ws_wy_row = carve(per * nleaf);
       P->ws_wy_col = sym ? P->ws_wy_row : carve(per * nleaf);
     }
+    P->ws_qr_end = o;
+    P->ws_dt = carve(dt_len);
+    P->ws_bb = carve(bb_len);
+    P->ws_yr = carve(yr_len);
+    P->ws_yc = carve(yc_len);
+    P->ws_part = bench ? carve(2 * n_part) : 0;
     P->ws_total = o;
     // algorithmic work
     double close_read = 0;

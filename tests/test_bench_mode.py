@@ -45,7 +45,7 @@ def _oracle_S(h):
     return sps.csr_matrix((val, col, rowptr), shape=(h.N, h.N))
 
 
-def _bench(h, w, close_gen=None, shards=1):
+def _bench(h, w, close_gen=None, shards=1, share_qr=True, want_q=False):
     import paper_1705_04601_b200 as h2sp
     packed = h2gen.pack(h)
     if shards == 1:
@@ -58,12 +58,15 @@ def _bench(h, w, close_gen=None, shards=1):
         torch.cuda.synchronize()
         return sp.outputs["bench_y"].cpu().numpy(), sp.outputs["bench_r2"].cpu().numpy(), plan
     plans = [h2sp.Plan(packed, g, shards, bench=True) for g in range(shards)]
-    vs = h2sp.VirtualShards(plans, packed, close_gen=close_gen)
+    vs = h2sp.VirtualShards(plans, packed, close_gen=close_gen, share_qr=share_qr)
     vs.outputs["bench_w"].copy_(torch.from_numpy(w))
     vs.outputs["bench_y"].fill_(np.nan)
     vs.outputs["bench_r2"].fill_(np.nan)
     vs.build()
     torch.cuda.synchronize()
+    if want_q:
+        return (vs.outputs["bench_y"].cpu().numpy(), vs.outputs["bench_r2"].cpu().numpy(),
+                vs.outputs["q_row"].cpu().numpy())
     return vs.outputs["bench_y"].cpu().numpy(), vs.outputs["bench_r2"].cpu().numpy(), plans[0]
 
 
@@ -127,6 +130,23 @@ def test_virtual_shards_bitwise(name, make, G):
     yg, rg, _ = _bench(h, w, shards=G)
     assert np.array_equal(y1, yg)
     assert np.array_equal(r1, rg)
+
+
+@pytest.mark.parametrize("name,make,G", [
+    ("cfg5-16384", lambda: h2gen.make_config(5, N=16384), 8),
+    ("cfg4-8192", lambda: h2gen.make_config(4, N=8192), 4),
+])
+def test_shared_qr_pass_is_bitwise_the_per_shard_qr(name, make, G):
+    """Protocol step 2 (the QR pass runs once for all clusters): the
+    first shard's build with H2SP_QR_ALL and the others with H2SP_QR_REUSE give
+    the y, row norms and Q of builds that each repeat the QR of their need set."""
+    _need_gpu()
+    h = make()
+    w = np.random.default_rng(13).standard_normal(h.N)
+    ya, ra, qa = _bench(h, w, shards=G, share_qr=True, want_q=True)
+    yb, rb, qb = _bench(h, w, shards=G, share_qr=False, want_q=True)
+    assert np.array_equal(ya, yb) and np.array_equal(ra, rb)
+    assert np.array_equal(qa, qb)   # every shard's need sets together cover the Q the applies read
 
 
 def test_bench_close_gen_matrix_free_couplings():

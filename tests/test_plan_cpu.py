@@ -217,3 +217,14 @@ def test_coupling_block_descs_layout():
         nx, ny = int(nn & 0xffffffff), int(nn >> 32)
         out[o:o + nx * ny] = h2gen.kernel_matrix(h.meta["kernel"], xr[x_off:x_off + nx], xc[y_off:y_off + ny]).ravel()
     assert np.array_equal(out, packed["coupling"])
+
+
+def test_qr_mode_validation():
+    """h2sp_plan_set_qr_mode (include/h2sp.h): NEED / ALL / REUSE accepted, anything else H2SP_EINVAL."""
+    import paper_1705_04601_b200 as h2sp
+    h = h2gen.random_h2(3, 8, 0, True, eta=0.7)
+    plan = h2sp.Plan(h2gen.pack(h))
+    for mode in (h2sp.QR_NEED, h2sp.QR_ALL, h2sp.QR_REUSE, h2sp.QR_NEED):
+        assert h2sp.lib.h2sp_plan_set_qr_mode(plan.handle, mode) == 0
+    assert h2sp.lib.h2sp_plan_set_qr_mode(plan.handle, 7) != 0
+    assert h2sp.lib.h2sp_plan_set_qr_mode(None, 0) != 0

@@ -21,6 +21,8 @@ for w in $what; do
       -o gpurun_out/${tag}_wy128 -f python bench.py $args > gpurun_out/${tag}_ncu_wy128.log 2>&1; echo wy128 rc=$?; summ ${tag}_wy128;;
     apply) ncu --set full --import-source on --clock-control none -k regex:'apply_(ut|v)_kernel' -c 2 \
       -o gpurun_out/${tag}_apply -f python bench.py --steps 1 --warmup 1 --no-oracle --no-e2e > gpurun_out/${tag}_ncu_apply.log 2>&1; echo apply rc=$?; summ ${tag}_apply;;
+    qr) ncu --set full --import-source on --clock-control none -k regex:qr_cta_kernel -c 2 \
+      -o gpurun_out/${tag}_qr -f python bench.py $args > gpurun_out/${tag}_ncu_qr.log 2>&1; echo qr rc=$?; summ ${tag}_qr;;
   esac
 done
 du -sh gpurun_out
