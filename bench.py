@@ -675,7 +675,9 @@ def main():
     n_apply_launch = 2   # one fused kernel per direction (apply_ut_kernel, apply_v_kernel)
     loc_r, _ = plan.local_rows()
     apply_flops = 2 * 2.0 * nrhs * float(np.sum(offs["n_row"][loc_r >= 0].astype(float) ** 2))
-    step_flops = plan.sizes["flops"] + apply_flops
+    # a shard's share of the job's work: each pair / strip / QR once over the shards (flops_unique;
+    # plan.sizes["flops"] also counts the Q / R^ and cross pairs a shard recomputes)
+    step_flops = float(plan.sizes.get("flops_unique", plan.sizes["flops"])) + apply_flops
     stream = torch.cuda.current_stream()
 
     def step(events=None):
