@@ -2409,9 +2409,6 @@ __global__ void __launch_bounds__(PairWy128gCfg<KP>::THREADS, 1) pair_wy128g_ker
 // rows [k_q, n_q) -> S (contiguous row segments, and/or the transposed blocks),
 // rows [0, k_q) -> q's panel for the next level.
 // --------------------------------------------------------------------------
-#ifndef STRIP_TPC
-#define STRIP_TPC 2
-#endif
 template <int NP, int TN>
 struct StripCfg {
   static constexpr int LDQ = NP + 4;
@@ -2450,7 +2447,6 @@ struct StripArgs {
   const double *bw;   // bench mode: w (S column order)
   double2 *part;      // bench mode: partial slots
   int aligned;        // bench mode: every frozen group width is a multiple of 32 (plan-wide)
-  int64_t ntiles;     // tiles of this launch (bench mode: a CTA takes STRIP_TPC consecutive ones)
 };
 
 // BENCH (bench mode, include/h2sp.h): rows [k_q, n_q) of W are reduced instead
@@ -2464,8 +2460,7 @@ struct StripArgs {
 // Fixed orders either way (the choice is plan-wide, so shards agree).  Tiles
 // hold whole groups (plan.cpp).
 template <int NP, int TN, bool BENCH>
-__global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, (BENCH && NP == 64 && TN == 128) ? 2 : StripCfg<NP, TN>::MIN_BLOCKS)
-    strip_kernel(StripArgs A) {
+__global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::MIN_BLOCKS) strip_kernel(StripArgs A) {
   using C = StripCfg<NP, TN>;
   extern __shared__ __align__(16) double sm[];
   double *sQ = sm;                           // NP x LDQ
@@ -2480,34 +2475,23 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, (BENCH && NP == 64 
   __shared__ int s_ngt;
   // groups overlapping this tile (<= TN + 1); when aliased, dead before the gather
   StripGroup *sg = C::ALIAS ? reinterpret_cast<StripGroup *>(sZ) : sg_own;
-  // bench mode: a CTA takes STRIP_TPC consecutive tiles (they mostly share the panel, so Q_q stays
-  // loaded) -- their descriptors arrive in one round trip, and tile i + 1's groups are requested as
-  // soon as tile i's maps are built, so only the first tile pays the descriptor -> Q / groups chain
-  constexpr int TPC = (BENCH && NP == 64) ? STRIP_TPC : 1;   // (config 5: n = 2 r = 64 above the leaves)
-  __shared__ __align__(16) StripTileX s_tiles[TPC];
-  const int64_t t_first = int64_t(blockIdx.x) * TPC;
-  const int nt = TPC > 1 ? int(min(int64_t(TPC), A.ntiles - t_first)) : 1;
-  // round trip 1: the self-contained tile descriptors
-  for (int c = threadIdx.x; c < nt * int(sizeof(StripTileX) / 16); c += blockDim.x)
-    cp16(reinterpret_cast<char *>(s_tiles) + 16 * c, reinterpret_cast<const char *>(A.tiles + t_first) + 16 * c);
+  __shared__ __align__(16) StripTileX s_tile;
+  // round trip 1: the self-contained tile descriptor
+  if (threadIdx.x < sizeof(StripTileX) / 16)
+    cp16(reinterpret_cast<char *>(&s_tile) + 16 * threadIdx.x,
+         reinterpret_cast<const char *>(A.tiles + blockIdx.x) + 16 * threadIdx.x);
   cp_commit();
   cp_wait_all();
   __syncthreads();
-  int64_t q_loaded = -1;
-  bool groups_ready = false;   // this tile's groups were requested during the previous tile
-#pragma unroll 1
-  for (int tt = 0; tt < nt; tt++) {
-  const StripTileX &T = s_tiles[tt];
+  const StripTileX &T = s_tile;
   const int n = T.n, kq = T.kq, k1 = T.k1, k2 = T.k2;
   const int ncol = T.ncol;
-  // round trip 2: Q_q (unless the previous tile left it) and the (at most TN + 1) groups overlapping the tile
-  if (T.q_off != q_loaded) async_tile<NP, NP, C::LDQ>(sQ, A.q + T.q_off, n, n, n, A.tiles);
-  q_loaded = T.q_off;
+  // round trip 2: Q_q and the (at most TN + 1) groups overlapping the tile
+  async_tile<NP, NP, C::LDQ>(sQ, A.q + T.q_off, n, n, n, A.tiles);
   const int ng = min(T.gend - T.g0, TN + 1);
-  if (!groups_ready)
-    for (int g = threadIdx.x; g < ng * 2; g += blockDim.x)
-      cp16(reinterpret_cast<char *>(&sg[g >> 1]) + 16 * (g & 1),
-           reinterpret_cast<const char *>(&A.groups[T.g0 + (g >> 1)]) + 16 * (g & 1));
+  for (int g = threadIdx.x; g < ng * 2; g += blockDim.x)
+    cp16(reinterpret_cast<char *>(&sg[g >> 1]) + 16 * (g & 1),
+         reinterpret_cast<const char *>(&A.groups[T.g0 + (g >> 1)]) + 16 * (g & 1));
   cp_commit();
   cp_wait_all();
   __syncthreads();
@@ -2543,17 +2527,6 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, (BENCH && NP == 64 
     }
   }
   __syncthreads();
-  groups_ready = false;
-  if constexpr (BENCH && !C::ALIAS) {  // the next tile's groups (sg is dead: maps and group table built)
-    if (tt + 1 < nt) {
-      const StripTileX &Tn = s_tiles[tt + 1];
-      const int ngn = min(Tn.gend - Tn.g0, TN + 1);
-      for (int g = threadIdx.x; g < ngn * 2; g += blockDim.x)
-        cp16(reinterpret_cast<char *>(&sg[g >> 1]) + 16 * (g & 1),
-             reinterpret_cast<const char *>(&A.groups[Tn.g0 + (g >> 1)]) + 16 * (g & 1));
-      groups_ready = true;   // lands with the Z gather's copies below
-    }
-  }
   // gather Z: each thread keeps one column pair (cc, cc + 1) and walks its rows
   // (blockDim.x is a multiple of TN / 2); a pair contiguous and 16-byte aligned
   // in a child's panel (the common case: even group widths) is one 16-byte copy.
@@ -2591,7 +2564,7 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, (BENCH && NP == 64 
   __syncthreads();
   const int warp = threadIdx.x >> 5;
   const int m0 = (warp / C::NWN) * 16, n0 = (warp % C::NWN) * C::WN;
-  if (!BENCH && m0 >= n) return;  // no rows of W for this warp (nothing after this needs the CTA barrier; one tile)
+  if (!BENCH && m0 >= n) return;  // no rows of W for this warp (nothing after this needs the CTA barrier)
   double acc[2][C::WN / 8][2];
   zero_acc(acc);
   // aligned bench plans: a warp's 32 columns are one frozen group, present in one
@@ -2699,6 +2672,7 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, (BENCH && NP == 64 
       }
       A.part[td] = v;
     }
+    if (m0 >= n) return;
   } else if constexpr (BENCH) {
     __syncthreads();  // every warp is done reading Z: stage W there
     if (m0 < n) {
@@ -2760,8 +2734,8 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, (BENCH && NP == 64 
       }
       if (sub == 0 && td >= 0) A.part[td] = make_double2(y, r2);
     }
+    if (m0 >= n) return;
   }
-  if (!BENCH || m0 < n)
 #pragma unroll
   for (int i = 0; i < 2; i++) {
     const int row = m0 + i * 8 + r;
@@ -2798,8 +2772,6 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, (BENCH && NP == 64 
           d[0] = v0;
       }
     }
-  }
-  if (TPC > 1 && tt + 1 < nt) __syncthreads();   // Z / slab space, maps and weights are reused by the next tile
   }
 }
 
@@ -3594,10 +3566,7 @@ static h2sp_status launch_strips1(const StripArgs &a, int64_t ntiles, cudaStream
   static_assert(!BENCH || size_t(NP) * C::LDZ * sizeof(double) >= (C::NWN * NP + (NP / 16) * TN) * 16,
                 "slab partials fit the Z buffer");
   if (h2sp_status e = ensure_smem((const void *)strip_kernel<NP, TN, BENCH>, smem)) return e;
-  StripArgs b = a;
-  b.ntiles = ntiles;
-  constexpr int tpc = (BENCH && NP == 64) ? STRIP_TPC : 1;
-  strip_kernel<NP, TN, BENCH><<<unsigned((ntiles + tpc - 1) / tpc), C::THREADS, smem, st>>>(b);
+  strip_kernel<NP, TN, BENCH><<<unsigned(ntiles), C::THREADS, smem, st>>>(a);
   H2SP_CK(cudaGetLastError());
   return H2SP_OK;
 }
