@@ -1548,7 +1548,8 @@ __device__ __forceinline__ void lane_rows_reduce(double (&v)[NV], int lane) {
 // column a.  Lane (r, q) of warp w holds H[m0 + r][8j + 2q + e].
 template <int NP, int TN, int WARPS>
 __device__ __forceinline__ void bench_pair(const PairArgs &A, const PairDst &D, int t, int s, const double (&H)[TN][2],
-                                           int m0, double2 *scratch, double2 *rowp_ = nullptr) {
+                                           int m0, double2 *scratch, double2 *rowp_ = nullptr,
+                                           const double *ws_sm = nullptr, const double *wt_sm = nullptr) {
   static_assert(WARPS * 8 == NP && TN * 8 == NP, "warp w owns rows 8w..8w+7 of the NP x NP tile");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, r = lane >> 2, q = lane & 3;
   double2 *colp = scratch, *rowp = rowp_ ? rowp_ : scratch + WARPS * NP;
@@ -1556,7 +1557,9 @@ __device__ __forceinline__ void bench_pair(const PairArgs &A, const PairDst &D, 
   const bool vrow = row >= D.kt && row < D.nt;
   const bool cols = D.dsym || D.s_dst_m >= 0;   // CTA-uniform
   const double *w_s = A.bw + A.cs.s_off[s];      // weights of block (t, s)'s columns
-  const double wa = (vrow && cols) ? __ldg(A.bw + A.cs.s_off[t] + a) : 0.0;  // weight of mirror column a
+  // ws_sm / wt_sm: the weights staged in shared memory by the caller, indexed by tile column / row
+  // (zero outside the frozen range) instead of read through L1 per element
+  const double wa = (vrow && cols) ? (wt_sm ? wt_sm[row] : __ldg(A.bw + A.cs.s_off[t] + a)) : 0.0;  // weight of mirror column a
   double ry = 0.0, rr = 0.0;
   constexpr int GS = 2;   // accumulator tiles per group of column sums (4 values per lane: 8 shuffles per group
                           // and quantity pair instead of 24; groups of 4 tiles save one more but cost 8 registers)
@@ -1578,7 +1581,7 @@ __device__ __forceinline__ void bench_pair(const PairArgs &A, const PairDst &D, 
           const bool v = vrow && col >= D.ks && col < D.ns;
           const double h = H[j][e];
           if (v && D.s_dst >= 0 && (!D.dsym || a <= b)) {
-            ry = fma(h, __ldg(w_s + b), ry);
+            ry = fma(h, ws_sm ? ws_sm[col] : __ldg(w_s + b), ry);
             rr = fma(h, h, rr);
           }
           cy[jj * 2 + e] = (v && (D.dsym ? a < b : true)) ? h * wa : 0.0;
@@ -2062,6 +2065,7 @@ __global__ void __launch_bounds__(PairWy128Cfg<KP>::THREADS, 1) pair_wy128_kerne
   // close_gen: points of the next pair's row cluster t (staged once per t) and the exp table
   __shared__ __align__(16) double s_xt[GEN ? 128 * 3 : 2];
   __shared__ double s_tab[GEN ? 64 : 1];
+  __shared__ double s_wst[BENCH ? 256 : 1];   // bench mode: w of the pair's S columns (by tile column) | S rows' mirror (by tile row)
   if (GEN && threadIdx.x < 64) s_tab[threadIdx.x] = g_exp2_64[threadIdx.x];
   const Chunk ch = A.chunks[blockIdx.x];
   stage_items(A.items, ch, s_it);
@@ -2125,6 +2129,16 @@ __global__ void __launch_bounds__(PairWy128Cfg<KP>::THREADS, 1) pair_wy128_kerne
     // close_gen: G of pair p+1 is evaluated during step 3 (one row per k-step)
     const bool gnext = GEN && more;
     wy128_load<KP>(sV, sM, wy_col, it.s);
+    if constexpr (BENCH) {  // this pair's weights for the epilogue (land with V_s / M_s)
+      if (threadIdx.x < 256) {
+        const bool colside = threadIdx.x < 128;
+        const int i = threadIdx.x & 127;
+        const int lo = colside ? it.ks : it.kt, hi = colside ? it.ns : it.nt;
+        const bool ok = i >= lo && i < hi;
+        const double *src = A.bw + A.cs.s_off[colside ? it.s : it.t] + (i - lo);
+        cp8(s_wst + threadIdx.x, ok ? (const void *)src : (const void *)A.chunks, ok);
+      }
+    }
     if (gnext && s_it[p + 1 - ch.begin].t != xt_staged) {  // points of the next row cluster
       xt_staged = s_it[p + 1 - ch.begin].t;
       const double *src = A.gen.pts + int64_t(xt_staged) * A.B * A.gen.dim;
@@ -2198,7 +2212,8 @@ __global__ void __launch_bounds__(PairWy128Cfg<KP>::THREADS, 1) pair_wy128_kerne
     D.ks = it.ks;
     D.dsym = A.sym && it.s == it.t;
     // bench mode: the S part reduced with the (free) V / M buffer as scratch
-    if constexpr (BENCH) bench_pair<128, TN, C::WARPS>(A, D, it.t, it.s, H, m0, reinterpret_cast<double2 *>(sV));
+    if constexpr (BENCH)
+      bench_pair<128, TN, C::WARPS>(A, D, it.t, it.s, H, m0, reinterpret_cast<double2 *>(sV), nullptr, s_wst, s_wst + 128);
     if (more) {  // V_t / M_t of the next pair, in flight during the scatter
       wy128_load<KP>(sV, sM, wy_row, s_it[p + 1 - ch.begin].t);
       cp_commit();
