@@ -2598,6 +2598,24 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
   const int lane = threadIdx.x & 31;
   const int r = lane >> 2, q4 = lane & 3;
   if (BENCH && A.aligned) {
+    // rows [0, k_q) -> q's panel first: the stores leave while the slower warps finish their product
+    if (m0 < kq && T.y_dst >= 0) {
+#pragma unroll
+      for (int i = 0; i < 2; i++) {
+        const int row = m0 + i * 8 + r;
+        if (row >= kq) continue;
+#pragma unroll
+        for (int j = 0; j < C::WN / 8; j++) {
+          const int col = n0 + j * 8 + 2 * q4;
+          if (col >= ncol) continue;
+          double *d = A.y_out + T.y_dst + int64_t(row) * T.y_ld + T.c0 + col;
+          if (col + 1 < ncol)
+            store2(d, acc[i][j][0], acc[i][j][1]);
+          else
+            d[0] = acc[i][j][0];
+        }
+      }
+    }
     __syncthreads();  // every warp is done reading Z: its space holds the slab partials
     double2 *dslab = reinterpret_cast<double2 *>(sZ);   // [NWN][NP]: (row, warp column slab)
     double2 *tslab = dslab + C::NWN * NP;               // [NWM][TN]: (column, warp row slab)
@@ -2687,7 +2705,7 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
       }
       A.part[td] = v;
     }
-    if (m0 >= n) return;
+    return;   // (the panel rows were stored before the slab reduction)
   } else if constexpr (BENCH) {
     __syncthreads();  // every warp is done reading Z: stage W there
     if (m0 < n) {
