@@ -428,6 +428,19 @@ def run_protocol(args, rank, world, local_rank):
         h_q = torch.empty(run.outputs["q_row"].numel(), dtype=torch.float64).pin_memory()
         h_x = torch.empty(nrhs, N, dtype=torch.float64).pin_memory()
 
+        # Q (5.4 GB, the largest result) is final once the first shard's build -- the shared QR pass --
+        # is done (the later shards only read it): its D2H runs on a side stream beside them
+        q_stream = torch.cuda.Stream(device=dev)
+        q_ready, q_done = torch.cuda.Event(), torch.cuda.Event()
+        share_qr = run.vs.share_qr or len(plans) == 1
+
+        def q_readback():
+            q_ready.record(stream)
+            q_stream.wait_event(q_ready)
+            with torch.cuda.stream(q_stream):
+                h_q.copy_(run.outputs["q_row"], non_blocking=True)
+                q_done.record(q_stream)
+
         def step_e2e():
             run.points.copy_(h_pts, non_blocking=True)
             run.box_lo.copy_(h_lo, non_blocking=True)
@@ -438,13 +451,16 @@ def run_protocol(args, rank, world, local_rank):
                 a0, a1 = run.leaf_range(i)
                 ap_[0].copy_(b_full[:, a0:a1])
             run.reconstruct()
-            step()
+            run.build(applies, after_first=q_readback if share_qr else None)
             for i, ap_ in enumerate(applies):
                 a0, a1 = run.leaf_range(i)
                 x_full[:, a0:a1].copy_(ap_[3])
             h_y.copy_(run.outputs["bench_y"], non_blocking=True)
             h_r2.copy_(run.outputs["bench_r2"], non_blocking=True)
-            h_q.copy_(run.outputs["q_row"], non_blocking=True)
+            if share_qr:
+                stream.wait_event(q_done)   # the step ends when Q has arrived too
+            else:
+                h_q.copy_(run.outputs["q_row"], non_blocking=True)
             h_x.copy_(x_full, non_blocking=True)
 
         step_e2e()
@@ -466,7 +482,8 @@ def run_protocol(args, rank, world, local_rank):
                "ms_per_step": float(ems.item()), "steps": k_e2e, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h,
                "api": "pinned host points / boxes / w / b in; h2sp_cheb_construct (bases, transfers, nodes on the "
-                      "device), h2sp_build_meta per virtual shard (+ U^T b, V w), y = S w, row norms, Q and x out"}
+                      "device), h2sp_build_meta per virtual shard (+ U^T b, V w), y = S w, row norms, Q and x out "
+                      "(Q read back on a side stream from the end of the shared QR pass on)"}
     # ---- SURVEY 8(a) a8 alone: y = U^T b and x = V y of one shard (its Q from the
     #      last step), nrhs = 1, 8, 32, against the HBM roofline (every Q_t of the
     #      shard's subtree read once + the vectors)

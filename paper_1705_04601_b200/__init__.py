@@ -531,10 +531,13 @@ class VirtualShards:
         self.apply_ptr = (self.apply_scratch.data_ptr() + 255) // 256 * 256
         self.apply_bytes = aneed
 
-    def build(self, applies=None, events=None, stream=None):
+    def build(self, applies=None, events=None, stream=None, after_first=None):
         """One pass over all shards.  applies: per shard (b, y, w, x) tensors or
         None (b, x: (nrhs, n_tree_local); y, w: (nrhs, s_rows) of that shard);
-        events: per shard a list of 2 * launches torch.cuda.Event or None."""
+        events: per shard a list of 2 * launches torch.cuda.Event or None;
+        after_first: called once the first shard's build is enqueued -- with
+        share_qr the Q of every cluster is final from there on (the later shards
+        do not write it), so a caller may start reading it back beside them."""
         for i, (sp, (_, mptr)) in enumerate(zip(self.shards, self._meta)):
             ap = None
             if applies is not None and applies[i] is not None:
@@ -552,6 +555,8 @@ class VirtualShards:
                                        ctypes.byref(sp._abi_outputs()), mptr, self.scratch_ptr, self.scratch_bytes,
                                        ctypes.byref(ap) if ap is not None else None, _stream_handle(stream), arr,
                                        len(ev) if ev else 0), "h2sp_build_meta")
+            if i == 0 and after_first is not None:
+                after_first()
         return self.outputs
 
 

@@ -84,8 +84,8 @@ class ProtocolRun:
         fl, nl = int(p.sizes["first_leaf"]), int(p.sizes["n_leaves_local"])
         return fl * self.B, (fl + nl) * self.B
 
-    def build(self, applies=None, events=None, stream=None):
-        return self.vs.build(applies, events=events, stream=stream)
+    def build(self, applies=None, events=None, stream=None, after_first=None):
+        return self.vs.build(applies, events=events, stream=stream, after_first=after_first)
 
     def global_rows(self, i: int) -> np.ndarray:
         if not hasattr(self, "_grows"):
