@@ -2558,8 +2558,12 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
     const bool v1 = b1 && b1n == b1 + 1 && ((reinterpret_cast<uintptr_t>(b1) | (uintptr_t(T.ld_c1) * 8)) & 15) == 0;
     const bool v2 = b2 && b2n == b2 + 1 && ((reinterpret_cast<uintptr_t>(b2) | (uintptr_t(T.ld_c2) * 8)) & 15) == 0;
     const void *any = A.tiles;
+    // aligned bench plans: the product skips the k range of an absent child for this column's
+    // 32-wide slab (below), so those rows of Z need not even be zero-filled
+    const bool skip = BENCH && A.aligned && (k1 & 3) == 0;
     for (int i = threadIdx.x / (TN / 2); i < n4; i += R) {
       const bool first = i < k1, second = !first && i < k1 + k2;
+      if (skip && ((first && !b1) || (second && !b2))) continue;
       const int64_t off = int64_t(first ? i : i - k1) * (first ? T.ld_c1 : T.ld_c2);
       const double *p0 = first ? b1 : (second ? b2 : nullptr);
       const double *p1 = first ? b1n : (second ? b2n : nullptr);
