@@ -2474,6 +2474,23 @@ struct StripArgs {
 // staged in the Z buffer: 8 lanes per (row, group), TPC lanes per column.
 // Fixed orders either way (the choice is plan-wide, so shards agree).  Tiles
 // hold whole groups (plan.cpp).
+#ifdef H2SP_STRIP_CLOCKS
+// Attribution build only (tools/strip_clocks.py): thread 0 of a sample of CTAs stamps clock64() at the
+// phase boundaries of strip_kernel into a global table read back by h2sp_debug_strip_clocks.
+struct StripClk {
+  unsigned grid, smid;
+  unsigned long long gt0;
+  long long c[10];
+};
+__device__ StripClk g_strip_clk[16384];
+__device__ unsigned g_strip_clk_n;
+#define STRIP_CLK(i)                                        \
+  do {                                                      \
+    if (clk_slot >= 0 && threadIdx.x == 0) g_strip_clk[clk_slot].c[i] = clock64(); \
+  } while (0)
+#else
+#define STRIP_CLK(i) do { } while (0)
+#endif
 template <int NP, int TN, bool BENCH>
 __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::MIN_BLOCKS) strip_kernel(StripArgs A) {
   using C = StripCfg<NP, TN>;
@@ -2491,6 +2508,23 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
   // groups overlapping this tile (<= TN + 1); when aliased, dead before the gather
   StripGroup *sg = C::ALIAS ? reinterpret_cast<StripGroup *>(sZ) : sg_own;
   __shared__ __align__(16) StripTileX s_tile;
+#ifdef H2SP_STRIP_CLOCKS
+  int clk_slot = -1;
+  if (threadIdx.x == 0 && (blockIdx.x & 63) == 0) {
+    const unsigned sl = atomicAdd(&g_strip_clk_n, 1u);
+    if (sl < 16384u) {
+      clk_slot = int(sl);
+      unsigned smid;
+      unsigned long long gt;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+      g_strip_clk[sl].grid = gridDim.x;
+      g_strip_clk[sl].smid = smid;
+      g_strip_clk[sl].gt0 = gt;
+    }
+  }
+#endif
+  STRIP_CLK(0);
   // round trip 1: the self-contained tile descriptor
   if (threadIdx.x < sizeof(StripTileX) / 16)
     cp16(reinterpret_cast<char *>(&s_tile) + 16 * threadIdx.x,
@@ -2498,6 +2532,7 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
   cp_commit();
   cp_wait_all();
   __syncthreads();
+  STRIP_CLK(1);
   const StripTileX &T = s_tile;
   const int n = T.n, kq = T.kq, k1 = T.k1, k2 = T.k2;
   const int ncol = T.ncol;
@@ -2510,6 +2545,7 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
   cp_commit();
   cp_wait_all();
   __syncthreads();
+  STRIP_CLK(2);
   // per-column source / destination maps
   for (int cc = threadIdx.x; cc < TN; cc += blockDim.x) {
     int32_t a1 = -1, a2 = -1;
@@ -2542,6 +2578,7 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
     }
   }
   __syncthreads();
+  STRIP_CLK(3);
   // gather Z: each thread keeps one column pair (cc, cc + 1) and walks its rows
   // (blockDim.x is a multiple of TN / 2); a pair contiguous and 16-byte aligned
   // in a child's panel (the common case: even group widths) is one 16-byte copy.
@@ -2581,6 +2618,7 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
   cp_commit();
   cp_wait_all();
   __syncthreads();
+  STRIP_CLK(4);
   const int warp = threadIdx.x >> 5;
   const int m0 = (warp / C::NWN) * 16, n0 = (warp % C::NWN) * C::WN;
   if (!BENCH && m0 >= n) return;  // no rows of W for this warp (nothing after this needs the CTA barrier)
@@ -2597,6 +2635,7 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
     else if (!p1 && p2) kb = k1;
   }
   if (m0 < n) warp_gemm<C::LDQ, C::LDZ, 2, C::WN / 8, true>(sQ, sZ, m0, n0, ke, acc, kb);
+  STRIP_CLK(5);
   // epilogue straight from the accumulators: lane (r, q) holds W[row][col], W[row][col + 1]
   // rows [0, k_q) -> q's panel; rows [k_q, n_q) -> S row segment and the transposed block
   const int lane = threadIdx.x & 31;
@@ -2620,7 +2659,9 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
         }
       }
     }
+    STRIP_CLK(6);
     __syncthreads();  // every warp is done reading Z: its space holds the slab partials
+    STRIP_CLK(7);
     double2 *dslab = reinterpret_cast<double2 *>(sZ);   // [NWN][NP]: (row, warp column slab)
     double2 *tslab = dslab + C::NWN * NP;               // [NWM][TN]: (column, warp row slab)
     const int wn = warp % C::NWN, wm = warp / C::NWN;
@@ -2684,6 +2725,7 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
       }
     }
     __syncthreads();
+    STRIP_CLK(8);
     const int nfz = n - kq;
     const int nwm = (n + 15) / 16;   // row warps that computed
     if (T.s_dst >= 0) {              // (row a, group g): the group's column slabs in order
@@ -2709,6 +2751,7 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
       }
       A.part[td] = v;
     }
+    STRIP_CLK(9);
     return;   // (the panel rows were stored before the slab reduction)
   } else if constexpr (BENCH) {
     __syncthreads();  // every warp is done reading Z: stage W there
@@ -4505,3 +4548,18 @@ h2sp_status launch_cheb_construct(const h2sp_plan_s *P, const unsigned char *met
   return H2SP_OK;
 }
 }  // namespace h2sp
+
+#ifdef H2SP_STRIP_CLOCKS
+// attribution build: copy the strip phase stamps out (count returned; table reset)
+extern "C" int64_t h2sp_debug_strip_clocks(void *out, int64_t max_entries) {
+  unsigned n = 0;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&n, h2sp::g_strip_clk_n, sizeof(n));
+  int64_t m = n < 16384u ? n : 16384;
+  if (m > max_entries) m = max_entries;
+  cudaMemcpyFromSymbol(out, h2sp::g_strip_clk, size_t(m) * sizeof(h2sp::StripClk));
+  unsigned z = 0;
+  cudaMemcpyToSymbol(h2sp::g_strip_clk_n, &z, sizeof(z));
+  return m;
+}
+#endif
