@@ -2559,7 +2559,9 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
       if (gr.pos_c1 >= 0) a1 = gr.pos_c1 + b;
       if (gr.pos_c2 >= 0) a2 = gr.pos_c2 + b;
       if (gr.s_dst_t >= 0) td = gr.s_dst_t + int64_t(b) * gr.s_ld_t;
-      if (BENCH) s_wc[cc] = T.s_dst >= 0 ? __ldg(A.bw + gr.wc0 + b) : 0.0;
+      // (bench weights: asynchronous copies that land with the gather -- a plain load here put a
+      // global round trip into this phase: 2.3 of the tile's 20.9 kcycles, tools/strip_clocks.py)
+      if (BENCH) cp8(&s_wc[cc], T.s_dst >= 0 ? (const void *)(A.bw + gr.wc0 + b) : (const void *)A.tiles, T.s_dst >= 0);
     } else if (BENCH) {
       s_wc[cc] = 0.0;
     }
@@ -2568,7 +2570,8 @@ __global__ void __launch_bounds__(StripCfg<NP, TN>::THREADS, StripCfg<NP, TN>::M
     tdst[cc] = td;
   }
   if constexpr (BENCH) {  // the tile's whole groups (tile starts at group g0's first column)
-    for (int a = threadIdx.x; a < NP; a += blockDim.x) s_wq[a] = a < n - kq ? __ldg(A.bw + T.wq0 + a) : 0.0;
+    for (int a = threadIdx.x; a < NP; a += blockDim.x)
+      cp8(&s_wq[a], a < n - kq ? (const void *)(A.bw + T.wq0 + a) : (const void *)A.tiles, a < n - kq);
     for (int g = threadIdx.x; g < ng; g += blockDim.x)
       if (sg[g].col0 < T.c0 + ncol) s_gtab[g] = make_int4(sg[g].col0 - T.c0, sg[g].m, sg[g].wc0, 0);
     if (threadIdx.x == 0) {

@@ -33,7 +33,7 @@ r = buf[:n]
 g = r["grid"].max()
 r = r[r["grid"] == g]
 names = ["descriptor round trip + barrier", "Q / groups round trip + barrier", "column maps + barrier",
-         "gather issue", "gather wait + barrier", "product (warp 0)", "panel-row stores (warp 0)",
+         "gather of Z (issue, wait, barrier)", "product (warp 0)", "panel-row stores (warp 0)",
          "barrier after the product", "slab partials + barrier", "final sums + part stores"]
 d = np.diff(r["c"], axis=1).astype(float)
 tot = (r["c"][:, 9] - r["c"][:, 0]).astype(float)
