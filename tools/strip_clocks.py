@@ -1,7 +1,16 @@
 """Phase attribution of strip_kernel at the bench's full size (attribution build only:
 alt/libh2sp_clk.so, kernels.cu compiled with -DH2SP_STRIP_CLOCKS): thread 0 of every 64th
 CTA stamps clock64() at the phase boundaries; this prints the mean / median cycles per phase
-of the largest launch (level 1 of virtual shard 0).  Run under gpurun from the repo root."""
+of the largest launch (level 1 of virtual shard 0).  Run under gpurun from the repo root.
+
+Build the attribution library first (after __graft_entry__.build(), which leaves the other
+objects in build/):
+    nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
+         -DH2SP_STRIP_CLOCKS -c paper_1705_04601_b200/csrc/kernels.cu -o build/kernels_clk.o
+    nvcc -gencode arch=compute_100a,code=sm_100a -shared -o alt/libh2sp_clk.so build/plan.cpp.o \
+         build/kernels_clk.o build/api.cu.o build/comm.cpp.o build/krylov.cu.o build/chol.cu.o -lcudart -ldl
+The script swaps it in for paper_1705_04601_b200/libh2sp.so: rebuild (or restore) the product
+library afterwards."""
 import ctypes
 import shutil
 import sys
